@@ -1,0 +1,174 @@
+/*
+ * tj_capi.h — the C-ABI of the B200-native trijoin join engine.
+ *
+ * Plain C: POD structs, raw pointers and sizes, integer status codes. No C++
+ * or torch types cross this boundary. The C++ host library (include/trijoin/ headers,
+ * the drop-in for the reference's proj/include/trijoin API) and the Python module
+ * `paper_2604_19982_b200._core` (drop-in for the reference's `trijoin._core`)
+ * are both thin layers over these entry points.
+ *
+ * Reference interfaces each entry point replaces (paths relative to
+ * /root/reference/proj):
+ *   tj_join            run_join                 include/trijoin/engine.hpp:70-71, src/engine.cpp:122-237
+ *   tj_refine_batch    refine_kernel            include/trijoin/refine.hpp:67-68, src/refine.cpp:63-84
+ *   tj_tri_tri_batch   tri_tri_distance         include/trijoin/geom.hpp:79,      src/geom.cpp:152-183
+ *   tj_mindist_batch   mindist_aabb             include/trijoin/geom.hpp:60,      src/geom.cpp:11-16
+ *   tj_mbb_filter      mbb_filter_within / _knn include/trijoin/filter.hpp:62-66,   src/filter.cpp:88-190
+ *   tj_voxel_filter    chunked_filter           include/trijoin/filter.hpp:111-114, src/filter.cpp:350-448
+ *   tj_knn_prune       knn_prune_to_fixpoint    include/trijoin/knn.hpp:41-42,      src/knn.cpp:82-91
+ *   tj_dataset_upload  (no reference analogue: PreparedDataset is host-resident there,
+ *                       include/trijoin/index.hpp:15-36; here it is packed once into HBM)
+ *
+ * Status codes: TJ_OK; TJ_EINVAL -> std::invalid_argument / ValueError;
+ * TJ_EENGINE -> EngineError (soundness tripwires, src/filter.cpp:25-31, src/knn.cpp:59,68-77,
+ * src/refine.cpp:312-313); TJ_ECUDA / TJ_ENOMEM -> std::runtime_error. The message of the
+ * last failure on a context is returned by tj_last_error().
+ *
+ * Threading: a tj_ctx is owned by one host thread (the coordinator of one GPU). Every
+ * call blocks until its device work is complete. Device buffers belong to the context;
+ * host views belong to the caller.
+ */
+#ifndef TJ_CAPI_H
+#define TJ_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { TJ_OK = 0, TJ_EINVAL = 1, TJ_EENGINE = 2, TJ_ECUDA = 3, TJ_ENOMEM = 4 };
+
+/* Join types (reference JoinType, include/trijoin/engine.hpp:15). */
+enum { TJ_WITHIN = 0, TJ_INTERSECT = 1, TJ_KNN = 2 };
+
+/* Pair status (reference PairStatus, include/trijoin/filter.hpp:12). */
+enum { TJ_UNDECIDED = 0, TJ_CONFIRMED = 1, TJ_REMOVED = 2 };
+
+/* Stage codes (reference stage::, include/trijoin/filter.hpp:16-20); LOD levels are 1..100. */
+enum { TJ_STAGE_NONE = -3, TJ_STAGE_MBB = -2, TJ_STAGE_VOXEL = -1 };
+
+/* Behaviour flags (none of them changes a result). */
+enum {
+    TJ_FLAG_NO_CULL = 1u << 0, /* disable exact-preserving facet-pair culling (A/B checks) */
+    TJ_FLAG_SYNC_STAGES = 1u << 1 /* synchronise + time every stage (stats wall_ms) */
+};
+
+#define TJ_FACET_STRIDE 12 /* doubles per facet record: v0.xyz v1.xyz v2.xyz hd ph pad */
+#define TJ_MAX_LODS 16
+
+typedef struct tj_ctx tj_ctx;
+typedef struct tj_dataset tj_dataset;
+
+/*
+ * Host view of one prepared dataset (reference PreparedDataset / PreparedObject /
+ * VoxelSet / LodMesh, include/trijoin/index.hpp:15-36, include/trijoin/mesh.hpp:42-49),
+ * flattened to structure-of-arrays. Voxels are numbered globally: object o owns voxels
+ * [voxel_offsets[o], voxel_offsets[o+1]). For LOD slot li (levels[li], the dataset's
+ * lod_schedule), the facets of global voxel v are entries
+ * [facet_offsets[li][v], facet_offsets[li][v+1]) of facets[li], each TJ_FACET_STRIDE
+ * doubles, in the voxel's ascending facet-id order (reference facets_per_level).
+ */
+typedef struct tj_dataset_view {
+    uint32_t n_objects;
+    uint32_t n_levels;
+    const int32_t* levels;        /* [n_levels] ascending LOD percentages */
+    const double* mbb;            /* [n_objects*6] min.xyz, max.xyz */
+    const double* anchor;         /* [n_objects*3] */
+    const uint64_t* voxel_offsets;/* [n_objects+1] */
+    const double* voxel_box;      /* [n_voxels*6] */
+    const double* voxel_anchor;   /* [n_voxels*3] */
+    const uint64_t* const* facet_offsets; /* [n_levels] -> [n_voxels+1] */
+    const double* const* facets;          /* [n_levels] -> [n_entries*TJ_FACET_STRIDE] */
+} tj_dataset_view;
+
+/* Reference JoinSpec (include/trijoin/engine.hpp:19-30); workers/seed are host-side only. */
+typedef struct tj_join_spec {
+    int32_t type;          /* TJ_WITHIN / TJ_INTERSECT / TJ_KNN */
+    double tau;            /* within; intersect requires 0 */
+    uint32_t k;            /* knn */
+    uint64_t filter_chunk; /* voxel pairs per filter chunk (result-invariant) */
+    uint64_t refine_chunk; /* voxel pairs per refine launch (result-invariant) */
+    uint32_t n_lods;
+    const uint32_t* lods;  /* ascending, ending at 100, each present in both datasets */
+    int32_t pipeline;      /* result-invariant overlap switch */
+    uint32_t flags;        /* TJ_FLAG_* */
+    /* R sharding across GPUs: query r participates iff
+       (r / shard_block) % shard_count == shard_index. shard_count 0 or 1 = all r. */
+    uint32_t shard_index, shard_count, shard_block;
+} tj_join_spec;
+
+/* Per-stage observer callbacks (reference JoinTrace, include/trijoin/filter.hpp:56-60).
+   Fired on the calling thread, in ascending op order within a stage. NULL = off. */
+typedef struct tj_trace {
+    void* user;
+    void (*on_interval)(void* user, uint32_t op, int16_t stage, double lb, double ub);
+    void (*on_vp_pruned)(void* user, uint32_t op, uint32_t vr, uint32_t vs, double lb_v,
+                         double ub_o);
+} tj_trace;
+
+/* Final candidate set (reference CandidateSet, include/trijoin/filter.hpp:38-48) and the
+   deterministic counters behind StageStats (src/engine.cpp:188-236). Arrays are owned by
+   the library; release with tj_join_result_free. */
+typedef struct tj_join_result {
+    uint64_t n_cands;
+    uint32_t n_queries;
+    uint32_t* pair_r;
+    uint32_t* pair_s;
+    double* lb;
+    double* ub;
+    uint8_t* status;
+    int16_t* decided_at;
+    uint64_t* r2op_offsets;  /* [n_queries+1] */
+    uint32_t* num_confirmed; /* [n_queries] */
+    uint64_t vp_generated, vp_pruned;
+    uint64_t filter_chunks, oversized_chunks;
+    uint32_t n_levels_run;
+    uint32_t level[TJ_MAX_LODS];
+    uint64_t level_vps[TJ_MAX_LODS];
+    uint64_t level_facet_pairs[TJ_MAX_LODS];     /* reference count: sum r_len*s_len */
+    uint64_t level_pairs_evaluated[TJ_MAX_LODS]; /* exact FP64 evaluations actually run */
+    uint64_t level_pairs_tested[TJ_MAX_LODS];    /* FP32 cull tests run */
+    double level_ms[TJ_MAX_LODS];
+    double level_kernel_ms[TJ_MAX_LODS];         /* refine kernel only (CUDA events) */
+    uint64_t refine_chunks;
+    double mbb_ms, voxel_ms, refine_ms, total_ms;
+} tj_join_result;
+
+/* ---- context ---- */
+int tj_ctx_create(int device, tj_ctx** out);
+void tj_ctx_destroy(tj_ctx* ctx);
+const char* tj_last_error(const tj_ctx* ctx);
+/* Library-wide last error for failures without a context (e.g. tj_ctx_create). */
+const char* tj_global_last_error(void);
+int tj_device_count(void);
+
+/* ---- datasets (resident in HBM) ---- */
+int tj_dataset_upload(tj_ctx* ctx, const tj_dataset_view* view, tj_dataset** out);
+void tj_dataset_free(tj_dataset* ds);
+uint64_t tj_dataset_device_bytes(const tj_dataset* ds);
+
+/* ---- full join (backs run_join) ---- */
+int tj_join(tj_ctx* ctx, const tj_dataset* R, const tj_dataset* S, const tj_join_spec* spec,
+            const tj_trace* trace, tj_join_result* out);
+void tj_join_result_free(tj_join_result* res);
+
+/* ---- stage / primitive entry points on host buffers ---- */
+
+/* refine_kernel: per descriptor d, the min over its facet pairs of
+   max(0, dist - ph_i - ph_j) (vp_lb) and dist + hd_i + hd_j (vp_ub); empty -> +inf.
+   tris: [n_tris*9] doubles (v0 v1 v2); hd/ph: [n_tris]. */
+int tj_refine_batch(tj_ctx* ctx, uint64_t n_tris, const double* tris, const double* hd,
+                    const double* ph, uint64_t n_descs, const uint64_t* r_off,
+                    const uint64_t* s_off, const uint32_t* r_len, const uint32_t* s_len,
+                    uint32_t flags, double* vp_lb, double* vp_ub);
+
+/* Exact FP64 tri_tri_distance / mindist_aabb over n independent inputs. */
+int tj_tri_tri_batch(tj_ctx* ctx, uint64_t n, const double* a9, const double* b9, double* out);
+int tj_mindist_batch(tj_ctx* ctx, uint64_t n, const double* a6, const double* b6, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TJ_CAPI_H */

@@ -1,0 +1,627 @@
+// Host side of the drop-in trijoin engine: packs PreparedDatasets into the device layout,
+// drives tj_join on one or more B200s (R sharded by query blocks, one host thread per
+// GPU), and assembles records / StageStats exactly as the reference's run_join
+// (src/engine.cpp:122-237). All join arithmetic runs on the GPU.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <sstream>
+#include <stdexcept>
+#include <thread>
+
+#include <json.hpp>
+
+#include "packed.hpp"
+#include "trijoin/engine.hpp"
+
+namespace trijoin {
+
+// ---------------------------------------------------------------- detail: contexts, packing
+namespace detail {
+
+[[noreturn]] void throw_status(int code, const char* msg) {
+    const std::string m = msg ? msg : "";
+    if (code == TJ_EINVAL) throw std::invalid_argument(m);
+    if (code == TJ_EENGINE) throw EngineError(m);
+    throw std::runtime_error(m);
+}
+
+namespace {
+struct CtxRegistry {
+    std::mutex mu;
+    std::map<int, tj_ctx*> ctxs;
+    ~CtxRegistry() {
+        for (auto& [d, c] : ctxs) tj_ctx_destroy(c);
+    }
+};
+CtxRegistry& registry() {
+    static CtxRegistry r;
+    return r;
+}
+} // namespace
+
+tj_ctx* device_context(int device) {
+    CtxRegistry& reg = registry();
+    std::lock_guard<std::mutex> lk(reg.mu);
+    auto it = reg.ctxs.find(device);
+    if (it != reg.ctxs.end()) return it->second;
+    tj_ctx* c = nullptr;
+    const int rc = tj_ctx_create(device, &c);
+    if (rc != TJ_OK) throw std::runtime_error(std::string("trijoin: no usable B200 device: ") + tj_global_last_error());
+    reg.ctxs[device] = c;
+    return c;
+}
+
+std::vector<int> join_devices() {
+    std::vector<int> out;
+    if (const char* env = std::getenv("TRIJOIN_DEVICES")) {
+        std::stringstream ss(env);
+        std::string tok;
+        while (std::getline(ss, tok, ','))
+            if (!tok.empty()) out.push_back(std::stoi(tok));
+    }
+    if (out.empty()) out.push_back(0);
+    return out;
+}
+
+uint64_t PackedDataset::bytes() const {
+    uint64_t b = (mbb.size() + anchor.size() + voxel_box.size() + voxel_anchor.size()) * 8 + voxel_offsets.size() * 8;
+    for (const auto& v : facet_offsets) b += v.size() * 8;
+    for (const auto& v : facets) b += v.size() * 8;
+    return b;
+}
+
+std::unique_ptr<PackedDataset> pack_dataset(const PreparedDataset& ds, ThreadPool& pool) {
+    auto p = std::make_unique<PackedDataset>();
+    const size_t no = ds.objects.size();
+    const size_t nl = ds.lod_schedule.size();
+    p->n_objects = static_cast<uint32_t>(no);
+    p->levels.assign(ds.lod_schedule.begin(), ds.lod_schedule.end());
+    p->mbb.resize(6 * no);
+    p->anchor.resize(3 * no);
+    p->voxel_offsets.assign(no + 1, 0);
+    for (size_t o = 0; o < no; ++o) {
+        const PreparedObject& obj = ds.objects[o];
+        if (obj.ladder.levels.size() != nl || obj.voxels.facets_per_level.size() != nl)
+            throw std::invalid_argument("trijoin: object level count does not match the lod schedule");
+        p->voxel_offsets[o + 1] = p->voxel_offsets[o] + obj.voxels.voxel_count();
+    }
+    const uint64_t nv = p->voxel_offsets[no];
+    p->voxel_box.resize(6 * nv);
+    p->voxel_anchor.resize(3 * nv);
+    p->facet_offsets.assign(nl, std::vector<uint64_t>(nv + 1, 0));
+    p->facets.resize(nl);
+    // per level: facet entries per voxel -> offsets
+    pool.parallel_jobs(no, [&](size_t o) {
+        const PreparedObject& obj = ds.objects[o];
+        const uint64_t v0 = p->voxel_offsets[o];
+        for (size_t li = 0; li < nl; ++li)
+            for (uint32_t v = 0; v < obj.voxels.voxel_count(); ++v)
+                p->facet_offsets[li][v0 + v + 1] = obj.voxels.facets_per_level[li][v].size();
+    });
+    for (size_t li = 0; li < nl; ++li) {
+        auto& fo = p->facet_offsets[li];
+        for (uint64_t v = 0; v < nv; ++v) fo[v + 1] += fo[v];
+        p->facets[li].resize(fo[nv] * TJ_FACET_STRIDE);
+    }
+    pool.parallel_jobs(no, [&](size_t o) {
+        const PreparedObject& obj = ds.objects[o];
+        const double m[6] = {obj.mbb.min.x, obj.mbb.min.y, obj.mbb.min.z, obj.mbb.max.x, obj.mbb.max.y, obj.mbb.max.z};
+        std::memcpy(&p->mbb[6 * o], m, sizeof(m));
+        p->anchor[3 * o] = obj.anchor.x;
+        p->anchor[3 * o + 1] = obj.anchor.y;
+        p->anchor[3 * o + 2] = obj.anchor.z;
+        const uint64_t v0 = p->voxel_offsets[o];
+        const VoxelSet& vs = obj.voxels;
+        for (uint32_t v = 0; v < vs.voxel_count(); ++v) {
+            const Aabb& b = vs.boxes[v];
+            const double bb[6] = {b.min.x, b.min.y, b.min.z, b.max.x, b.max.y, b.max.z};
+            std::memcpy(&p->voxel_box[6 * (v0 + v)], bb, sizeof(bb));
+            p->voxel_anchor[3 * (v0 + v)] = vs.anchors[v].x;
+            p->voxel_anchor[3 * (v0 + v) + 1] = vs.anchors[v].y;
+            p->voxel_anchor[3 * (v0 + v) + 2] = vs.anchors[v].z;
+        }
+        for (size_t li = 0; li < nl; ++li) {
+            const LodMesh& lod = obj.ladder.levels[li];
+            const auto& fo = p->facet_offsets[li];
+            double* dst = p->facets[li].data();
+            for (uint32_t v = 0; v < vs.voxel_count(); ++v) {
+                uint64_t e = fo[v0 + v];
+                for (uint32_t f : vs.facets_per_level[li][v]) {
+                    if (f >= lod.mesh.facets.size() || f >= lod.hd.size() || f >= lod.ph.size())
+                        throw std::invalid_argument("trijoin: voxel facet id out of range");
+                    const auto& tri = lod.mesh.facets[f];
+                    double* r = dst + e * TJ_FACET_STRIDE;
+                    for (int k = 0; k < 3; ++k) {
+                        const Point3& pt = lod.mesh.vertices[tri[k]];
+                        r[3 * k] = pt.x;
+                        r[3 * k + 1] = pt.y;
+                        r[3 * k + 2] = pt.z;
+                    }
+                    r[9] = lod.hd[f];
+                    r[10] = lod.ph[f];
+                    r[11] = 0.0;
+                    ++e;
+                }
+            }
+        }
+    });
+    p->fo_ptrs.resize(nl);
+    p->f_ptrs.resize(nl);
+    for (size_t li = 0; li < nl; ++li) {
+        p->fo_ptrs[li] = p->facet_offsets[li].data();
+        p->f_ptrs[li] = p->facets[li].data();
+    }
+    tj_dataset_view& v = p->view;
+    v.n_objects = p->n_objects;
+    v.n_levels = static_cast<uint32_t>(nl);
+    v.levels = p->levels.data();
+    v.mbb = p->mbb.data();
+    v.anchor = p->anchor.data();
+    v.voxel_offsets = p->voxel_offsets.data();
+    v.voxel_box = p->voxel_box.data();
+    v.voxel_anchor = p->voxel_anchor.data();
+    v.facet_offsets = p->fo_ptrs.data();
+    v.facets = p->f_ptrs.data();
+    return p;
+}
+
+} // namespace detail
+
+// ---------------------------------------------------------------- small API functions
+
+std::string stage_name(int16_t code) {
+    if (code == stage::kNone) return "undecided";
+    if (code == stage::kMbb) return "mbb";
+    if (code == stage::kVoxel) return "voxel";
+    if (code == 100) return "exact";
+    return "lod-" + std::to_string(code);
+}
+
+std::string join_type_name(JoinType t) {
+    if (t == JoinType::Within) return "within";
+    if (t == JoinType::Intersect) return "intersect";
+    return "knn";
+}
+
+void intersect_interval(Interval& io, double lb, double ub) {
+    io.lb = std::max(io.lb, lb);
+    io.ub = std::min(io.ub, ub);
+    if (!(io.lb > io.ub)) return;
+    if (io.lb - io.ub > 1e-9)
+        throw EngineError("bound crossing: lb " + std::to_string(io.lb) + " > ub " + std::to_string(io.ub));
+    io.lb = io.ub = 0.5 * (io.lb + io.ub);
+}
+
+uint64_t CandidateSet::undecided_count() const {
+    return static_cast<uint64_t>(std::count(status.begin(), status.end(), PairStatus::Undecided));
+}
+
+size_t prune_within(CandidateSet& cands, double tau, int16_t stage_code, std::span<const uint32_t> ops) {
+    size_t changed = 0;
+    auto one = [&](uint32_t op) {
+        if (cands.status[op] != PairStatus::Undecided) return;
+        const Interval& iv = cands.intervals[op];
+        PairStatus ns = PairStatus::Undecided;
+        if (iv.ub <= tau) ns = PairStatus::Confirmed;
+        else if (iv.lb > tau) ns = PairStatus::Removed;
+        if (ns == PairStatus::Undecided) return;
+        cands.status[op] = ns;
+        cands.decided_at[op] = stage_code;
+        if (ns == PairStatus::Confirmed) ++cands.num_confirmed[cands.pairs[op].first];
+        ++changed;
+    };
+    if (ops.empty()) {
+        for (uint32_t op = 0; op < cands.size(); ++op) one(op);
+    } else {
+        for (uint32_t op : ops) one(op);
+    }
+    return changed;
+}
+
+uint64_t voxel_pair_count(const CandidateSet& cands, uint32_t op, const PreparedDataset& R, const PreparedDataset& S) {
+    const auto& [r, s] = cands.pairs[op];
+    return uint64_t{R.objects[r].voxels.voxel_count()} * S.objects[s].voxels.voxel_count();
+}
+
+void validate(const JoinSpec& spec) {
+    if (spec.type == JoinType::Knn) {
+        if (spec.k == 0) throw std::invalid_argument("join: k must be >= 1");
+    } else {
+        if (spec.tau < 0) throw std::invalid_argument("join: tau must be >= 0");
+        if (spec.type == JoinType::Intersect && spec.tau != 0.0)
+            throw std::invalid_argument("join: intersection requires tau == 0");
+    }
+    if (spec.filter_chunk == 0) throw std::invalid_argument("join: filter chunk must be >= 1");
+    if (spec.refine_chunk == 0) throw std::invalid_argument("join: refine chunk must be >= 1");
+    if (spec.lods.empty() || spec.lods.back() != 100) throw std::invalid_argument("join: lod schedule must end at 100");
+    for (size_t i = 0; i < spec.lods.size(); ++i) {
+        if (spec.lods[i] == 0 || spec.lods[i] > 100) throw std::invalid_argument("join: lod levels must be in (0, 100]");
+        if (i > 0 && spec.lods[i] <= spec.lods[i - 1])
+            throw std::invalid_argument("join: lod schedule must be ascending");
+    }
+}
+
+namespace {
+std::string g17(double v) {
+    char buf[40];
+    std::snprintf(buf, sizeof(buf), "%.17g", v);
+    return buf;
+}
+} // namespace
+
+std::string format_record(const JoinResultRecord& rec, bool knn) {
+    std::string s = std::to_string(rec.r) + ' ' + std::to_string(rec.s) + ' ' + g17(rec.lb) + ' ' + g17(rec.ub) + ' ' +
+                    stage_name(rec.decided_at);
+    if (knn) s += ' ' + std::to_string(rec.rank);
+    return s;
+}
+
+std::string format_records(std::span<const JoinResultRecord> recs, bool knn) {
+    std::string out;
+    for (const auto& r : recs) out += format_record(r, knn) + '\n';
+    return out;
+}
+
+std::string StageStats::to_json() const {
+    nlohmann::json j;
+    j["query"] = query;
+    j["results"] = results;
+    j["total_ms"] = total_ms;
+    auto arr = nlohmann::json::array();
+    for (const StageCounters& s : stages)
+        arr.push_back({{"stage", s.name},
+                       {"wall_ms", s.wall_ms},
+                       {"pairs_in", s.pairs_in},
+                       {"confirmed", s.confirmed},
+                       {"removed", s.removed},
+                       {"pairs_out", s.pairs_out},
+                       {"vp_generated", s.vp_generated},
+                       {"vp_pruned", s.vp_pruned},
+                       {"facet_pairs", s.facet_pairs}});
+    j["stages"] = std::move(arr);
+    return j.dump(2);
+}
+
+size_t aggregate_object_bounds(std::span<const double> vp_lb, std::span<const double> vp_ub,
+                               std::span<const uint32_t> vp_op, CandidateSet& cands, int16_t stage_code,
+                               const JoinTrace* trace) {
+    if (vp_lb.size() != vp_ub.size() || vp_lb.size() != vp_op.size())
+        throw std::invalid_argument("aggregate_object_bounds: array size mismatch");
+    // per touched op: running minima, then updates in ascending op order
+    std::map<uint32_t, std::pair<double, double>> mins;
+    for (size_t t = 0; t < vp_op.size(); ++t) {
+        auto [it, fresh] = mins.try_emplace(vp_op[t], vp_lb[t], vp_ub[t]);
+        if (!fresh) {
+            it->second.first = std::min(it->second.first, vp_lb[t]);
+            it->second.second = std::min(it->second.second, vp_ub[t]);
+        }
+    }
+    size_t updated = 0;
+    for (const auto& [op, m] : mins) {
+        if (cands.status[op] != PairStatus::Undecided) continue;
+        if (std::isinf(m.first)) continue;
+        intersect_interval(cands.intervals[op], m.first, m.second);
+        if (trace && trace->on_interval) trace->on_interval(op, stage_code, cands.intervals[op]);
+        ++updated;
+    }
+    return updated;
+}
+
+KnnState make_knn_state(const CandidateSet& cands, uint32_t k) {
+    if (k == 0) throw std::invalid_argument("make_knn_state: k must be >= 1");
+    KnnState st;
+    st.k = k;
+    st.num_confirmed.assign(cands.r2op_offsets.empty() ? 0 : cands.r2op_offsets.size() - 1, 0);
+    for (size_t op = 0; op < cands.size(); ++op)
+        if (cands.status[op] == PairStatus::Confirmed) ++st.num_confirmed[cands.pairs[op].first];
+    return st;
+}
+
+size_t knn_apply_deltas(KnnState& state, CandidateSet& cands, std::span<const KnnDelta> deltas, int16_t stage_code) {
+    for (const KnnDelta& d : deltas) {
+        if (cands.status[d.op] != PairStatus::Undecided) throw EngineError("knn_apply_deltas: candidate decided twice");
+        cands.status[d.op] = d.status;
+        cands.decided_at[d.op] = stage_code;
+        if (d.status != PairStatus::Confirmed) continue;
+        const uint32_t r = cands.pairs[d.op].first;
+        ++cands.num_confirmed[r];
+        if (++state.num_confirmed[r] > state.k) throw EngineError("knn_apply_deltas: confirmed count exceeds k");
+    }
+    return deltas.size();
+}
+
+// ---------------------------------------------------------------- GPU-backed primitives
+
+void mindist_aabb_batch(std::span<const Aabb> a, std::span<const Aabb> b, std::span<double> out) {
+    if (a.size() != b.size() || out.size() != a.size()) throw std::invalid_argument("mindist_aabb_batch: size mismatch");
+    tj_ctx* ctx = detail::device_context(detail::join_devices()[0]);
+    static_assert(sizeof(Aabb) == 48);
+    detail::check(tj_mindist_batch(ctx, a.size(), reinterpret_cast<const double*>(a.data()),
+                                   reinterpret_cast<const double*>(b.data()), out.data()),
+                  ctx);
+}
+
+void tri_tri_distance_batch(std::span<const Triangle> a, std::span<const Triangle> b, std::span<double> out) {
+    if (a.size() != b.size() || out.size() != a.size())
+        throw std::invalid_argument("tri_tri_distance_batch: size mismatch");
+    tj_ctx* ctx = detail::device_context(detail::join_devices()[0]);
+    static_assert(sizeof(Triangle) == 72);
+    detail::check(tj_tri_tri_batch(ctx, a.size(), reinterpret_cast<const double*>(a.data()),
+                                   reinterpret_cast<const double*>(b.data()), out.data()),
+                  ctx);
+}
+
+double mindist_aabb(const Aabb& a, const Aabb& b) {
+    double d = 0;
+    mindist_aabb_batch({&a, 1}, {&b, 1}, {&d, 1});
+    return d;
+}
+
+double tri_tri_distance(const Triangle& t1, const Triangle& t2) {
+    double d = 0;
+    tri_tri_distance_batch({&t1, 1}, {&t2, 1}, {&d, 1});
+    return d;
+}
+
+VoxelPairBatch gather_facet_data(std::span<const ActiveVp> slice, uint32_t level, const PreparedDataset& R,
+                                 const PreparedDataset& S, const CandidateSet& cands) {
+    auto slot = [&](const PreparedDataset& d) {
+        for (size_t i = 0; i < d.lod_schedule.size(); ++i)
+            if (d.lod_schedule[i] == static_cast<int>(level)) return i;
+        throw EngineError("refine: level " + std::to_string(level) + " is not in the dataset's lod schedule");
+    };
+    const size_t lr = slot(R), ls = slot(S);
+    VoxelPairBatch batch;
+    batch.descs.reserve(slice.size());
+    std::map<uint64_t, std::pair<uint64_t, uint32_t>> seen_r, seen_s;
+    auto segment = [&](const PreparedObject& obj, uint32_t obj_idx, size_t li, uint32_t voxel,
+                       std::map<uint64_t, std::pair<uint64_t, uint32_t>>& seen) {
+        const uint64_t key = (uint64_t{obj_idx} << 32) | voxel;
+        if (auto it = seen.find(key); it != seen.end()) return it->second;
+        const LodMesh& lod = obj.ladder.levels[li];
+        const auto& ids = obj.voxels.facets_per_level[li][voxel];
+        const std::pair<uint64_t, uint32_t> seg{batch.tris.size(), static_cast<uint32_t>(ids.size())};
+        for (uint32_t f : ids) {
+            batch.tris.push_back(lod.mesh.triangle(f));
+            batch.hd.push_back(lod.hd[f]);
+            batch.ph.push_back(lod.ph[f]);
+        }
+        seen.emplace(key, seg);
+        return seg;
+    };
+    for (const ActiveVp& a : slice) {
+        const auto [r, s] = cands.pairs[a.op];
+        const auto sr = segment(R.objects[r], r, lr, a.vr, seen_r);
+        const auto ss = segment(S.objects[s], s, ls, a.vs, seen_s);
+        batch.descs.push_back({sr.first, ss.first, sr.second, ss.second, a.op});
+    }
+    return batch;
+}
+
+void refine_kernel(const VoxelPairBatch& batch, ThreadPool&, std::vector<double>& vp_lb, std::vector<double>& vp_ub) {
+    const size_t n = batch.descs.size();
+    vp_lb.assign(n, std::numeric_limits<double>::infinity());
+    vp_ub.assign(n, std::numeric_limits<double>::infinity());
+    if (n == 0) return;
+    std::vector<uint64_t> ro(n), so(n);
+    std::vector<uint32_t> rl(n), sl(n);
+    for (size_t d = 0; d < n; ++d) {
+        ro[d] = batch.descs[d].r_off;
+        so[d] = batch.descs[d].s_off;
+        rl[d] = batch.descs[d].r_len;
+        sl[d] = batch.descs[d].s_len;
+    }
+    tj_ctx* ctx = detail::device_context(detail::join_devices()[0]);
+    detail::check(tj_refine_batch(ctx, batch.tris.size(), reinterpret_cast<const double*>(batch.tris.data()),
+                                  batch.hd.data(), batch.ph.data(), n, ro.data(), so.data(), rl.data(), sl.data(), 0,
+                                  vp_lb.data(), vp_ub.data()),
+                  ctx);
+}
+
+// ---------------------------------------------------------------- run_join
+
+namespace {
+
+struct TraceBridge {
+    const JoinTrace* t;
+    static void interval(void* u, uint32_t op, int16_t st, double lb, double ub) {
+        const auto* self = static_cast<TraceBridge*>(u);
+        if (self->t->on_interval) self->t->on_interval(op, st, Interval{lb, ub});
+    }
+    static void pruned(void* u, uint32_t op, uint32_t vr, uint32_t vs, double lb, double ub) {
+        const auto* self = static_cast<TraceBridge*>(u);
+        if (self->t->on_vp_pruned) self->t->on_vp_pruned(op, vr, vs, lb, ub);
+    }
+};
+
+// Candidate set + counters of one join, merged over shards.
+struct Merged {
+    CandidateSet cands;
+    uint64_t vp_generated = 0, vp_pruned = 0;
+    double mbb_ms = 0, voxel_ms = 0;
+    std::map<uint32_t, RefineLevelStats> levels;
+};
+
+tj_join_spec to_c_spec(const JoinSpec& spec) {
+    tj_join_spec c{};
+    c.type = spec.type == JoinType::Within ? TJ_WITHIN : spec.type == JoinType::Intersect ? TJ_INTERSECT : TJ_KNN;
+    c.tau = spec.tau;
+    c.k = spec.k;
+    c.filter_chunk = spec.filter_chunk;
+    c.refine_chunk = spec.refine_chunk;
+    c.n_lods = static_cast<uint32_t>(spec.lods.size());
+    c.lods = spec.lods.data();
+    c.pipeline = spec.pipeline ? 1 : 0;
+    c.flags = 0;
+    if (const char* e = std::getenv("TRIJOIN_NO_CULL"); e && *e && *e != '0') c.flags |= TJ_FLAG_NO_CULL;
+    return c;
+}
+
+} // namespace
+
+JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const JoinSpec& spec, ThreadPool& pool,
+                    const JoinTrace* trace) {
+    using Clock = std::chrono::steady_clock;
+    validate(spec);
+    const bool knn = spec.type == JoinType::Knn;
+    const auto t_total = Clock::now();
+    JoinOutput out;
+    out.stats.query = join_type_name(spec.type);
+
+    const std::vector<int> devices = detail::join_devices();
+    const bool self_join = &R == &S;
+    auto pr = detail::pack_dataset(R, pool);
+    std::unique_ptr<detail::PackedDataset> ps_own;
+    const detail::PackedDataset* ps = pr.get();
+    if (!self_join) {
+        ps_own = detail::pack_dataset(S, pool);
+        ps = ps_own.get();
+    }
+    const size_t G = (trace && (trace->on_interval || trace->on_vp_pruned)) ? 1 : devices.size();
+    std::vector<detail::ResultHandle> results(G);
+    std::vector<std::exception_ptr> errors(G);
+    auto run_shard = [&](size_t g) {
+        try {
+            tj_ctx* ctx = detail::device_context(devices[g]);
+            detail::DatasetHandle dr, ds_h;
+            detail::check(tj_dataset_upload(ctx, &pr->view, &dr.p), ctx);
+            const tj_dataset* dsp = dr.p;
+            if (!self_join) {
+                detail::check(tj_dataset_upload(ctx, &ps->view, &ds_h.p), ctx);
+                dsp = ds_h.p;
+            }
+            tj_join_spec cs = to_c_spec(spec);
+            cs.shard_index = static_cast<uint32_t>(g);
+            cs.shard_count = static_cast<uint32_t>(G);
+            cs.shard_block = 1024;
+            TraceBridge bridge{trace};
+            tj_trace tt{&bridge, &TraceBridge::interval, &TraceBridge::pruned};
+            detail::check(tj_join(ctx, dr.p, dsp, &cs, trace ? &tt : nullptr, &results[g].r), ctx);
+        } catch (...) {
+            errors[g] = std::current_exception();
+        }
+    };
+    if (G == 1) {
+        run_shard(0);
+    } else {
+        std::vector<std::thread> ts;
+        for (size_t g = 0; g < G; ++g) ts.emplace_back(run_shard, g);
+        for (auto& t : ts) t.join();
+    }
+    for (auto& e : errors)
+        if (e) std::rethrow_exception(e);
+
+    // Merge shards: query r is owned by shard (r / 1024) % G; each shard's arrays cover
+    // all queries with empty ranges for foreign ones.
+    Merged m;
+    const uint32_t nq = static_cast<uint32_t>(R.objects.size());
+    uint64_t total = 0;
+    for (auto& h : results) total += h.r.n_cands;
+    CandidateSet& c = m.cands;
+    c.pairs.reserve(total);
+    c.intervals.reserve(total);
+    c.status.reserve(total);
+    c.decided_at.reserve(total);
+    c.r2op_offsets.assign(nq + 1, 0);
+    c.num_confirmed.assign(nq, 0);
+    for (uint32_t r = 0; r < nq; ++r) {
+        const tj_join_result& res = results[G == 1 ? 0 : (r / 1024) % G].r;
+        c.r2op_offsets[r] = c.pairs.size();
+        for (uint64_t op = res.r2op_offsets[r]; op < res.r2op_offsets[r + 1]; ++op) {
+            c.pairs.emplace_back(res.pair_r[op], res.pair_s[op]);
+            c.intervals.push_back({res.lb[op], res.ub[op]});
+            c.status.push_back(static_cast<PairStatus>(res.status[op]));
+            c.decided_at.push_back(res.decided_at[op]);
+        }
+        c.num_confirmed[r] = res.num_confirmed[r];
+    }
+    c.r2op_offsets[nq] = c.pairs.size();
+    for (auto& h : results) {
+        const tj_join_result& res = h.r;
+        m.vp_generated += res.vp_generated;
+        m.vp_pruned += res.vp_pruned;
+        m.mbb_ms = std::max(m.mbb_ms, res.mbb_ms);
+        m.voxel_ms = std::max(m.voxel_ms, res.voxel_ms);
+        for (uint32_t i = 0; i < res.n_levels_run; ++i) {
+            RefineLevelStats& ls = m.levels[res.level[i]];
+            ls.level = res.level[i];
+            ls.vps += res.level_vps[i];
+            ls.facet_pairs += res.level_facet_pairs[i];
+            ls.wall_ms = std::max(ls.wall_ms, res.level_ms[i]);
+        }
+    }
+
+    // Records (src/engine.cpp:161-185).
+    if (!knn) {
+        for (uint32_t op = 0; op < c.size(); ++op)
+            if (c.status[op] == PairStatus::Confirmed)
+                out.records.push_back(
+                    {c.pairs[op].first, c.pairs[op].second, c.intervals[op].lb, c.intervals[op].ub, c.decided_at[op], 0});
+    } else {
+        for (uint32_t r = 0; r < nq; ++r) {
+            std::vector<uint32_t> conf;
+            for (uint64_t op = c.r2op_offsets[r]; op < c.r2op_offsets[r + 1]; ++op)
+                if (c.status[op] == PairStatus::Confirmed) conf.push_back(static_cast<uint32_t>(op));
+            std::sort(conf.begin(), conf.end(), [&](uint32_t a, uint32_t b) {
+                if (c.intervals[a].ub != c.intervals[b].ub) return c.intervals[a].ub < c.intervals[b].ub;
+                if (c.intervals[a].lb != c.intervals[b].lb) return c.intervals[a].lb < c.intervals[b].lb;
+                return c.pairs[a].second < c.pairs[b].second;
+            });
+            uint32_t rank = 0;
+            for (uint32_t op : conf)
+                out.records.push_back({r, c.pairs[op].second, c.intervals[op].lb, c.intervals[op].ub,
+                                       c.decided_at[op], ++rank});
+        }
+    }
+
+    // Stage counters (src/engine.cpp:188-236).
+    std::map<int16_t, std::pair<uint64_t, uint64_t>> tally;
+    for (uint32_t op = 0; op < c.size(); ++op) {
+        if (c.status[op] == PairStatus::Confirmed) ++tally[c.decided_at[op]].first;
+        else if (c.status[op] == PairStatus::Removed) ++tally[c.decided_at[op]].second;
+    }
+    struct Plan {
+        int16_t code;
+        double wall;
+        uint64_t vpg, vpp, fp;
+    };
+    std::vector<Plan> plan{{stage::kMbb, m.mbb_ms, 0, 0, 0}, {stage::kVoxel, m.voxel_ms, m.vp_generated, m.vp_pruned, 0}};
+    for (uint32_t level : spec.lods) {
+        Plan p{static_cast<int16_t>(level), 0.0, 0, 0, 0};
+        if (auto it = m.levels.find(level); it != m.levels.end()) {
+            p.wall = it->second.wall_ms;
+            p.vpg = it->second.vps;
+            p.fp = it->second.facet_pairs;
+        }
+        plan.push_back(p);
+    }
+    const uint64_t all_pairs = uint64_t{R.objects.size()} * uint64_t{S.objects.size()};
+    uint64_t flowing = all_pairs;
+    for (const Plan& p : plan) {
+        auto [conf, rem] = tally.count(p.code) ? tally[p.code] : std::pair<uint64_t, uint64_t>{0, 0};
+        if (p.code == stage::kMbb) rem += all_pairs - c.size();
+        StageCounters sc;
+        sc.name = stage_name(p.code);
+        sc.wall_ms = p.wall;
+        sc.pairs_in = flowing;
+        sc.confirmed = conf;
+        sc.removed = rem;
+        sc.pairs_out = flowing - conf - rem;
+        sc.vp_generated = p.vpg;
+        sc.vp_pruned = p.vpp;
+        sc.facet_pairs = p.fp;
+        out.stats.stages.push_back(sc);
+        flowing = sc.pairs_out;
+    }
+    out.stats.results = out.records.size();
+    out.stats.total_ms = std::chrono::duration<double, std::milli>(Clock::now() - t_total).count();
+    return out;
+}
+
+} // namespace trijoin

@@ -1,0 +1,56 @@
+// Host-side packing of a PreparedDataset into the C-ABI structure-of-arrays view
+// (tj_dataset_view), plus the per-process device context registry.
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "../../../include/tj_capi.h"
+#include "trijoin/index.hpp"
+
+namespace trijoin::detail {
+
+// Owning SoA image of one PreparedDataset in the device layout (include/tj_capi.h).
+struct PackedDataset {
+    uint32_t n_objects = 0;
+    std::vector<int32_t> levels;
+    std::vector<double> mbb, anchor, voxel_box, voxel_anchor;
+    std::vector<uint64_t> voxel_offsets;
+    std::vector<std::vector<uint64_t>> facet_offsets; // per level
+    std::vector<std::vector<double>> facets;          // per level, TJ_FACET_STRIDE doubles each
+    std::vector<const uint64_t*> fo_ptrs;
+    std::vector<const double*> f_ptrs;
+    tj_dataset_view view{};
+    uint64_t bytes() const;
+};
+
+std::unique_ptr<PackedDataset> pack_dataset(const PreparedDataset& ds, ThreadPool& pool);
+
+// Lazily created context per CUDA device, destroyed at process exit.
+tj_ctx* device_context(int device);
+// Devices used by run_join: $TRIJOIN_DEVICES (comma list) or {0}.
+std::vector<int> join_devices();
+
+// Throws the C++ exception matching a C-ABI status code.
+[[noreturn]] void throw_status(int code, const char* msg);
+inline void check(int code, tj_ctx* ctx) {
+    if (code != TJ_OK) throw_status(code, ctx ? tj_last_error(ctx) : tj_global_last_error());
+}
+
+// RAII holders.
+struct DatasetHandle {
+    tj_dataset* p = nullptr;
+    DatasetHandle() = default;
+    DatasetHandle(const DatasetHandle&) = delete;
+    DatasetHandle& operator=(const DatasetHandle&) = delete;
+    ~DatasetHandle() { tj_dataset_free(p); }
+};
+struct ResultHandle {
+    tj_join_result r{};
+    ResultHandle() = default;
+    ResultHandle(const ResultHandle&) = delete;
+    ResultHandle& operator=(const ResultHandle&) = delete;
+    ~ResultHandle() { tj_join_result_free(&r); }
+};
+
+} // namespace trijoin::detail

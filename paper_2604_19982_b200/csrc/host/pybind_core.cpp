@@ -1,0 +1,254 @@
+// Python module paper_2604_19982_b200._core — drop-in for the reference's trijoin._core join
+// surface (proj/python/bindings.cpp:101-121, :215-229): same `join` signature, defaults,
+// GIL release, (records, stats_json) result and ValueError on invalid specs. Extra entry
+// points expose in-memory datasets, a device-resident join handle for benchmarking, the
+// GPU primitives and the benchmark index replicator.
+#include <pybind11/numpy.h>
+#include <pybind11/pybind11.h>
+#include <pybind11/stl.h>
+
+#include <chrono>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "packed.hpp"
+#include "replicate.hpp"
+#include "trijoin/engine.hpp"
+
+namespace py = pybind11;
+using namespace trijoin;
+
+namespace {
+
+using DatasetPtr = std::shared_ptr<const PreparedDataset>;
+
+JoinSpec make_spec(const std::string& type, double tau, uint32_t k, uint64_t filter_chunk, uint64_t refine_chunk,
+                   const std::vector<uint32_t>& lods, bool pipeline, uint32_t workers, uint64_t seed, bool exact) {
+    JoinSpec spec;
+    if (type == "within") spec.type = JoinType::Within;
+    else if (type == "intersect") spec.type = JoinType::Intersect;
+    else if (type == "knn") spec.type = JoinType::Knn;
+    else throw std::invalid_argument("type must be within, intersect, or knn, got: " + type);
+    spec.tau = tau;
+    spec.k = k;
+    spec.filter_chunk = filter_chunk;
+    spec.refine_chunk = refine_chunk;
+    spec.lods = lods;
+    spec.pipeline = pipeline;
+    spec.workers = workers;
+    spec.seed = seed;
+    spec.exact = exact;
+    validate(spec);
+    return spec;
+}
+
+py::tuple pack_output(const JoinOutput& out) {
+    py::list records;
+    for (const JoinResultRecord& r : out.records)
+        records.append(py::make_tuple(r.r, r.s, r.lb, r.ub, stage_name(r.decided_at), r.rank));
+    return py::make_tuple(records, out.stats.to_json());
+}
+
+py::tuple join_paths(const std::string& r_path, const std::string& s_path, const JoinSpec& spec) {
+    JoinOutput out;
+    {
+        py::gil_scoped_release release;
+        ThreadPool pool(spec.workers);
+        const PreparedDataset R = load_index(r_path);
+        PreparedDataset s_store;
+        const PreparedDataset* S = &R;
+        if (!s_path.empty() && s_path != r_path) {
+            s_store = load_index(s_path);
+            S = &s_store;
+        }
+        out = run_join(R, *S, spec, pool);
+    }
+    return pack_output(out);
+}
+
+// A device-resident (R, S) pair on one GPU: packed and uploaded once, joined many times.
+class Resident {
+public:
+    Resident(DatasetPtr R, DatasetPtr S, int device, unsigned workers) : R_(std::move(R)), S_(std::move(S)) {
+        py::gil_scoped_release release;
+        ctx_ = detail::device_context(device);
+        ThreadPool pool(workers);
+        auto pr = detail::pack_dataset(*R_, pool);
+        detail::check(tj_dataset_upload(ctx_, &pr->view, &dr_.p), ctx_);
+        bytes_ = pr->bytes();
+        if (S_.get() != R_.get()) {
+            auto ps = detail::pack_dataset(*S_, pool);
+            detail::check(tj_dataset_upload(ctx_, &ps->view, &ds_.p), ctx_);
+            bytes_ += ps->bytes();
+        }
+    }
+    uint64_t device_bytes() const { return bytes_; }
+
+    py::dict run(const std::string& type, double tau, uint32_t k, const std::vector<uint32_t>& lods,
+                 uint64_t refine_chunk, uint32_t flags, uint32_t shard_index, uint32_t shard_count,
+                 bool want_arrays) {
+        JoinSpec spec = make_spec(type, tau, k, 4194304, refine_chunk, lods, true, 0, 0, false);
+        tj_join_spec c{};
+        c.type = spec.type == JoinType::Within ? TJ_WITHIN : spec.type == JoinType::Intersect ? TJ_INTERSECT : TJ_KNN;
+        c.tau = spec.tau;
+        c.k = spec.k;
+        c.filter_chunk = spec.filter_chunk;
+        c.refine_chunk = spec.refine_chunk;
+        c.n_lods = static_cast<uint32_t>(spec.lods.size());
+        c.lods = spec.lods.data();
+        c.pipeline = 1;
+        c.flags = flags;
+        c.shard_index = shard_index;
+        c.shard_count = shard_count;
+        c.shard_block = 1024;
+        detail::ResultHandle res;
+        {
+            py::gil_scoped_release release;
+            detail::check(tj_join(ctx_, dr_.p, ds_.p ? ds_.p : dr_.p, &c, nullptr, &res.r), ctx_);
+        }
+        const tj_join_result& r = res.r;
+        py::dict d;
+        d["n_cands"] = r.n_cands;
+        uint64_t undecided_after_mbb = 0, confirmed = 0;
+        for (uint64_t op = 0; op < r.n_cands; ++op) {
+            confirmed += r.status[op] == TJ_CONFIRMED;
+            undecided_after_mbb += r.decided_at[op] != TJ_STAGE_MBB;
+        }
+        d["confirmed"] = confirmed;
+        d["voxel_pairs_in"] = undecided_after_mbb; // = stats stages["voxel"].pairs_in
+        d["vp_generated"] = r.vp_generated;
+        d["vp_pruned"] = r.vp_pruned;
+        d["mbb_ms"] = r.mbb_ms;
+        d["voxel_ms"] = r.voxel_ms;
+        d["refine_ms"] = r.refine_ms;
+        d["total_ms"] = r.total_ms;
+        py::list levels;
+        for (uint32_t i = 0; i < r.n_levels_run; ++i) {
+            py::dict l;
+            l["level"] = r.level[i];
+            l["vps"] = r.level_vps[i];
+            l["facet_pairs"] = r.level_facet_pairs[i];
+            l["evaluated"] = r.level_pairs_evaluated[i];
+            l["tested"] = r.level_pairs_tested[i];
+            l["ms"] = r.level_ms[i];
+            l["kernel_ms"] = r.level_kernel_ms[i];
+            levels.append(l);
+        }
+        d["levels"] = levels;
+        if (want_arrays) {
+            const size_t n = r.n_cands;
+            d["pair_r"] = py::array_t<uint32_t>(n, r.pair_r);
+            d["pair_s"] = py::array_t<uint32_t>(n, r.pair_s);
+            d["lb"] = py::array_t<double>(n, r.lb);
+            d["ub"] = py::array_t<double>(n, r.ub);
+            d["status"] = py::array_t<uint8_t>(n, r.status);
+            d["decided_at"] = py::array_t<int16_t>(n, r.decided_at);
+        }
+        return d;
+    }
+
+private:
+    DatasetPtr R_, S_;
+    tj_ctx* ctx_ = nullptr;
+    detail::DatasetHandle dr_, ds_;
+    uint64_t bytes_ = 0;
+};
+
+} // namespace
+
+PYBIND11_MODULE(_core, m) {
+    m.doc() = "B200-native filter-and-refine spatial joins over triangulated polyhedra (trijoin drop-in)";
+
+    py::register_exception<EngineError>(m, "EngineError", PyExc_RuntimeError);
+    py::register_exception<IndexError>(m, "IndexError", PyExc_RuntimeError);
+
+    m.def(
+        "join",
+        [](const std::string& r, const std::string& s, const std::string& type, double tau, uint32_t k,
+           uint64_t filter_chunk, uint64_t refine_chunk, const std::vector<uint32_t>& lods, bool pipeline,
+           uint32_t workers, uint64_t seed, bool exact) {
+            return join_paths(r, s, make_spec(type, tau, k, filter_chunk, refine_chunk, lods, pipeline, workers, seed, exact));
+        },
+        py::arg("r"), py::arg("s") = "", py::arg("type") = "within", py::arg("tau") = 0.0, py::arg("k") = 1,
+        py::arg("filter_chunk") = 4194304, py::arg("refine_chunk") = 500000,
+        py::arg("lods") = std::vector<uint32_t>{20, 40, 60, 80, 100}, py::arg("pipeline") = true,
+        py::arg("workers") = 0, py::arg("seed") = 0, py::arg("exact") = false,
+        "Returns (records, stats_json). Each record is (r, s, lb, ub, stage, rank); rank is 0 except for knn. "
+        "s defaults to a self-join on r.");
+
+    py::class_<PreparedDataset, std::shared_ptr<PreparedDataset>>(m, "Dataset")
+        .def_property_readonly("n_objects", [](const PreparedDataset& d) { return d.objects.size(); })
+        .def_property_readonly("lod_schedule", [](const PreparedDataset& d) { return d.lod_schedule; })
+        .def("facet_count", [](const PreparedDataset& d, size_t level_index) {
+            uint64_t n = 0;
+            for (const auto& o : d.objects) n += o.ladder.levels.at(level_index).mesh.facets.size();
+            return n;
+        });
+
+    m.def(
+        "load_dataset",
+        [](const std::string& path) {
+            py::gil_scoped_release release;
+            return std::make_shared<PreparedDataset>(load_index(path));
+        },
+        py::arg("path"));
+
+    m.def(
+        "join_datasets",
+        [](std::shared_ptr<PreparedDataset> R, std::shared_ptr<PreparedDataset> S, const std::string& type, double tau,
+           uint32_t k, uint64_t filter_chunk, uint64_t refine_chunk, const std::vector<uint32_t>& lods, bool pipeline,
+           uint32_t workers, bool exact) {
+            const JoinSpec spec = make_spec(type, tau, k, filter_chunk, refine_chunk, lods, pipeline, workers, 0, exact);
+            JoinOutput out;
+            {
+                py::gil_scoped_release release;
+                ThreadPool pool(workers);
+                out = run_join(*R, S ? *S : *R, spec, pool);
+            }
+            return pack_output(out);
+        },
+        py::arg("R"), py::arg("S") = nullptr, py::arg("type") = "within", py::arg("tau") = 0.0, py::arg("k") = 1,
+        py::arg("filter_chunk") = 4194304, py::arg("refine_chunk") = 500000,
+        py::arg("lods") = std::vector<uint32_t>{20, 40, 60, 80, 100}, py::arg("pipeline") = true,
+        py::arg("workers") = 0, py::arg("exact") = false,
+        "run_join on in-memory datasets (host buffers in, records out): packs, uploads, joins, copies back.");
+
+    py::class_<Resident>(m, "Resident")
+        .def(py::init([](std::shared_ptr<PreparedDataset> R, std::shared_ptr<PreparedDataset> S, int device,
+                         unsigned workers) { return new Resident(R, S ? S : R, device, workers); }),
+             py::arg("R"), py::arg("S") = nullptr, py::arg("device") = 0, py::arg("workers") = 0)
+        .def_property_readonly("device_bytes", &Resident::device_bytes)
+        .def("run", &Resident::run, py::arg("type") = "within", py::arg("tau") = 0.0, py::arg("k") = 1,
+             py::arg("lods") = std::vector<uint32_t>{20, 40, 60, 80, 100}, py::arg("refine_chunk") = 500000,
+             py::arg("flags") = 0u, py::arg("shard_index") = 0u, py::arg("shard_count") = 1u,
+             py::arg("arrays") = false);
+
+    m.def(
+        "replicate_index",
+        [](std::shared_ptr<PreparedDataset> tmpl, const std::string& out_path, const std::vector<uint32_t>& ids,
+           const std::vector<std::array<double, 3>>& shifts) {
+            std::vector<Point3> sh;
+            sh.reserve(shifts.size());
+            for (const auto& s : shifts) sh.push_back({s[0], s[1], s[2]});
+            py::gil_scoped_release release;
+            return replicate_index(*tmpl, out_path, ids, sh);
+        },
+        py::arg("template"), py::arg("out_path"), py::arg("template_ids"), py::arg("shifts"));
+
+    m.def(
+        "tri_tri_distance",
+        [](py::array_t<double, py::array::c_style | py::array::forcecast> a,
+           py::array_t<double, py::array::c_style | py::array::forcecast> b) {
+            if (a.ndim() != 2 || a.shape(1) != 9 || b.ndim() != 2 || b.shape(1) != 9 || a.shape(0) != b.shape(0))
+                throw std::invalid_argument("tri_tri_distance: expected two (n, 9) arrays");
+            const size_t n = a.shape(0);
+            py::array_t<double> out(n);
+            tri_tri_distance_batch({reinterpret_cast<const Triangle*>(a.data()), n},
+                                   {reinterpret_cast<const Triangle*>(b.data()), n}, {out.mutable_data(), n});
+            return out;
+        },
+        py::arg("a"), py::arg("b"));
+
+    m.def("device_count", [] { return tj_device_count(); });
+}

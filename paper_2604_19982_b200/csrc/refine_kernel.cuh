@@ -1,0 +1,275 @@
+// Multi-LOD facet refinement on sm_100a (reference refine_kernel, src/refine.cpp:63-84,
+// paper Alg. 4): per voxel pair, the exact minima over all facet pairs (i, j) of
+//     lb_ij = max(0, d_ij - ph_i - ph_j)      ub_ij = d_ij + hd_i + hd_j
+// with d_ij the reference tri_tri_distance (geom_exact.cuh), bit-identical to the CPU.
+//
+// Work decomposition (one warp per voxel pair, dynamic work counter):
+//   * the r-voxel's facets are staged 32 at a time into shared memory, one per lane
+//     (each lane also keeps its facet's FP32 culling record in registers);
+//   * the s-voxel's facets are staged 64 at a time into shared memory and read as
+//     warp-wide broadcasts;
+//   * every (i, j) first goes through a cheap FP32 test (exact-preserving cull,
+//     below); survivors are pushed into a per-warp queue and evaluated exactly in
+//     FP64 32 at a time, so the expensive path always runs with a converged warp;
+//   * running minima are warp-reduced after each evaluation round.
+//
+// Exact-preserving culling: pair (i, j) is skipped
+// only if it provably cannot lower either running minimum, i.e. with B_ij a rigorous
+// lower bound of the exact triangle distance (facet-AABB gap, FP32 with directed
+// rounding on outward-rounded boxes):
+//     B - ph_i - ph_j >= min_lb + delta   and   B + hd_i + hd_j >= min_ub + delta.
+// The reference's computed d_ij is the distance between two points on the triangles
+// (clamped Ericson parameters) up to rounding, except for (a) the interior case of
+// point_triangle on sliver triangles and (b) a spurious edge-piercing "0" on nearly
+// parallel edge/plane configurations. Pairs where either is possible are never culled:
+// both facets must be well shaped (all angles with sin >= 1e-2), every edge/plane
+// combination must satisfy |cos| >= 1e-3, and B <= 1e3 * min(L_i, L_j). delta adds a
+// 1e-5 relative and 1e-12 * |coords| absolute margin, orders of magnitude above the
+// rounding error bounds in that regime. Skipping a pair that cannot change a minimum
+// leaves both minima bit-identical to the exhaustive loop.
+#pragma once
+#include <cstdint>
+
+#include "geom_exact.cuh"
+
+namespace tjx {
+
+constexpr int kRT = 32;      // r facets per tile (one per lane)
+constexpr int kST = 64;      // s facets per tile
+constexpr int kFS = 15;      // doubles per staged facet: v[9] hd ph lab lbc lac flags
+constexpr int kCS = 24;      // floats per culling record
+constexpr int kWarps = 4;    // warps per CTA
+constexpr int kQueue = 64;
+
+struct WarpSmem {
+    double rf[kRT * kFS];
+    double sf[kST * kFS];
+    float sc[kST * kCS];
+    uint32_t queue[kQueue];
+};
+
+// Culling record layout (floats):
+//  0-2 lo (rd)  3-5 hi (ru)  6 L (ru, facet AABB diagonal)  7 M (ru, max |coord|)
+//  8 hd (rd)    9 ph (ru)    10 ok (1 = well shaped and non-degenerate)
+//  11-13 unit(v1-v0)  14-16 unit(v2-v1)  17-19 unit(v0-v2)  20-22 unit normal  23 pad
+struct CullRec {
+    float f[kCS];
+};
+
+struct RefineCounters {
+    unsigned long long tested;    // FP32 culling tests
+    unsigned long long evaluated; // exact FP64 tri_tri evaluations
+};
+
+__device__ __forceinline__ float rd(double x) { return __double2float_rd(x); }
+__device__ __forceinline__ float ru(double x) { return __double2float_ru(x); }
+
+// Stage one facet record (TJ_FACET_STRIDE doubles: v[9] hd ph pad) into shared memory.
+__device__ __forceinline__ void stage_facet(const double* __restrict__ g, double* sm, float* cr) {
+    const double2* g2 = reinterpret_cast<const double2*>(g);
+    double c[12];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        const double2 t = __ldg(g2 + k);
+        c[2 * k] = t.x;
+        c[2 * k + 1] = t.y;
+    }
+    double n2, s2;
+    const TriRef t = make_tri(c, &n2, &s2);
+#pragma unroll
+    for (int k = 0; k < 11; ++k) sm[k] = c[k];
+    sm[11] = t.lab;
+    sm[12] = t.lbc;
+    sm[13] = t.lac;
+    const bool shaped = n2 >= TJ_MUL(TJ_MUL(1e-4, s2), s2);
+    const bool ok = !t.degenerate && shaped;
+    sm[14] = t.degenerate ? 1.0 : 0.0;
+
+    float M = 0.f;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        const double lo = fmin(fmin(c[d], c[3 + d]), c[6 + d]);
+        const double hi = fmax(fmax(c[d], c[3 + d]), c[6 + d]);
+        cr[d] = rd(lo);
+        cr[3 + d] = ru(hi);
+        M = fmaxf(M, fmaxf(fabsf(cr[d]), fabsf(cr[3 + d])));
+    }
+    const float dx = __fsub_ru(cr[3], cr[0]), dy = __fsub_ru(cr[4], cr[1]), dz = __fsub_ru(cr[5], cr[2]);
+    cr[6] = __fsqrt_ru(__fadd_ru(__fadd_ru(__fmul_ru(dx, dx), __fmul_ru(dy, dy)), __fmul_ru(dz, dz)));
+    cr[7] = M;
+    cr[8] = rd(c[9]);
+    cr[9] = ru(c[10]);
+    cr[10] = ok ? 1.f : 0.f;
+    // unit edge directions and unit normal (only used as conditioning estimates)
+    const V3 e0 = vsub(t.v1, t.v0), e1 = vsub(t.v2, t.v1), e2 = vsub(t.v0, t.v2);
+    const V3 n = vcross(vsub(t.v1, t.v0), vsub(t.v2, t.v0));
+    const V3 es[4] = {e0, e1, e2, n};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const double l2 = vnorm2(es[k]);
+        const double inv = l2 > 0.0 ? rsqrt(l2) : 0.0;
+        cr[11 + 3 * k] = (float)(es[k].x * inv);
+        cr[12 + 3 * k] = (float)(es[k].y * inv);
+        cr[13 + 3 * k] = (float)(es[k].z * inv);
+    }
+    cr[23] = 0.f;
+}
+
+__device__ __forceinline__ TriRef load_tri(const double* sm) {
+    TriRef t;
+    t.v0 = {sm[0], sm[1], sm[2]};
+    t.v1 = {sm[3], sm[4], sm[5]};
+    t.v2 = {sm[6], sm[7], sm[8]};
+    t.lab = sm[11];
+    t.lbc = sm[12];
+    t.lac = sm[13];
+    t.degenerate = sm[14] != 0.0;
+    return t;
+}
+
+// Rigorous lower bound of the AABB gap (outward-rounded boxes, round-down arithmetic).
+__device__ __forceinline__ float box_gap_lb(const float* a, const float* b) {
+    float s = 0.f;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        const float g = fmaxf(0.f, fmaxf(__fsub_rd(b[d], a[3 + d]), __fsub_rd(a[d], b[3 + d])));
+        s = __fadd_rd(s, __fmul_rd(g, g));
+    }
+    return __fsqrt_rd(s);
+}
+
+__device__ __forceinline__ float absdot3(const float* u, const float* v) {
+    return fabsf(u[0] * v[0] + u[1] * v[1] + u[2] * v[2]);
+}
+
+// True iff (a, b) provably cannot lower min_lb or min_ub (both given rounded up).
+__device__ __forceinline__ bool cullable(const float* a, const float* b, float mlb_u, float mub_u) {
+    const float B = box_gap_lb(a, b);
+    const float delta =
+        __fadd_ru(__fmul_ru(1e-5f, __fadd_ru(__fadd_ru(B, a[6]), b[6])), __fmul_ru(1e-12f, __fadd_ru(a[7], b[7])));
+    const float lbs = __fsub_rd(__fsub_rd(B, a[9]), b[9]);
+    const float ubs = __fadd_rd(__fadd_rd(B, a[8]), b[8]);
+    if (!(lbs >= __fadd_ru(mlb_u, delta) && ubs >= __fadd_ru(mub_u, delta))) return false;
+    if (a[10] == 0.f || b[10] == 0.f) return false;
+    if (B > 1e3f * fminf(a[6], b[6])) return false;
+    const float kC = 1e-3f;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        if (absdot3(a + 11 + 3 * k, b + 20) < kC) return false;
+        if (absdot3(b + 11 + 3 * k, a + 20) < kC) return false;
+    }
+    return true;
+}
+
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = (w < v) ? w : v;
+    }
+    return v;
+}
+
+// Exact evaluation of pair (i in r tile, j in s tile); folds into the lane minima.
+__device__ __forceinline__ void eval_pair(const WarpSmem& sm, int i, int j, double& mlb, double& mub) {
+    const double* ra = sm.rf + i * kFS;
+    const double* sb = sm.sf + j * kFS;
+    const TriRef A = load_tri(ra);
+    const TriRef B = load_tri(sb);
+    const double d = tri_tri(A, B);
+    // std::max(0.0, dist - ph[fi] - ph[fj]); dist + hd[fi] + hd[fj]   (src/refine.cpp:78-79)
+    const double lbp = smax(0.0, TJ_SUB(TJ_SUB(d, ra[10]), sb[10]));
+    const double ubp = TJ_ADD(TJ_ADD(d, ra[9]), sb[9]);
+    mlb = smin(mlb, lbp);
+    mub = smin(mub, ubp);
+}
+
+// One voxel pair: facets [r_base, r_base + r_len) x [s_base, s_base + s_len), each
+// record TJ_FACET_STRIDE (12) doubles. Returns the exact minima (warp-uniform).
+__device__ __forceinline__ void refine_voxel_pair(WarpSmem& sm, const double* __restrict__ r_base, uint32_t r_len,
+                                                  const double* __restrict__ s_base, uint32_t s_len, bool cull,
+                                                  double& out_lb, double& out_ub, unsigned long long& tested,
+                                                  unsigned long long& evaluated) {
+    const int lane = threadIdx.x & 31;
+    const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+    double mlb = kInf, mub = kInf; // warp-uniform after every reduction
+    bool done = false;
+    for (uint32_t r0 = 0; r0 < r_len && !done; r0 += kRT) {
+        const int rcnt = (int)min((uint32_t)kRT, r_len - r0);
+        float myc[kCS];
+        __syncwarp();
+        if (lane < rcnt) stage_facet(r_base + (size_t)(r0 + lane) * 12, sm.rf + lane * kFS, myc);
+        const bool have_i = lane < rcnt;
+        for (uint32_t s0 = 0; s0 < s_len && !done; s0 += kST) {
+            const int scnt = (int)min((uint32_t)kST, s_len - s0);
+            __syncwarp();
+            for (int l = lane; l < scnt; l += 32)
+                stage_facet(s_base + (size_t)(s0 + l) * 12, sm.sf + l * kFS, sm.sc + l * kCS);
+            __syncwarp();
+
+            double llb = mlb, lub = mub; // lane-local minima
+            int seed_j = -1;
+            if (cull && mlb == kInf) {
+                // Seed: each lane evaluates its facet against the s facet of smallest box gap.
+                float bestB = __int_as_float(0x7f800000);
+                if (have_i) {
+                    for (int j = 0; j < scnt; ++j) {
+                        const float B = box_gap_lb(myc, sm.sc + j * kCS);
+                        if (B < bestB) { bestB = B; seed_j = j; }
+                    }
+                }
+                if (seed_j >= 0) {
+                    eval_pair(sm, lane, seed_j, llb, lub);
+                    ++evaluated;
+                }
+                mlb = warp_min(llb);
+                mub = warp_min(lub);
+            }
+            int qn = 0;
+            float mlb_u = ru(mlb), mub_u = ru(mub);
+            for (int j = 0; j < scnt; ++j) {
+                bool need = false;
+                if (have_i && j != seed_j) {
+                    need = !cull || !cullable(myc, sm.sc + j * kCS, mlb_u, mub_u);
+                    ++tested;
+                }
+                const unsigned bal = __ballot_sync(0xffffffffu, need);
+                if (need) {
+                    const int pos = qn + __popc(bal & ((1u << lane) - 1u));
+                    sm.queue[pos] = (uint32_t)lane | ((uint32_t)j << 8);
+                }
+                qn += __popc(bal);
+                if (qn >= 32) {
+                    __syncwarp();
+                    const uint32_t e = sm.queue[lane];
+                    eval_pair(sm, (int)(e & 0xffu), (int)(e >> 8), llb, lub);
+                    ++evaluated;
+                    __syncwarp();
+                    if (lane < qn - 32) sm.queue[lane] = sm.queue[32 + lane];
+                    __syncwarp();
+                    qn -= 32;
+                    mlb = warp_min(llb);
+                    mub = warp_min(lub);
+                    mlb_u = ru(mlb);
+                    mub_u = ru(mub);
+                    if (mlb == 0.0 && mub == 0.0) { done = true; break; }
+                }
+            }
+            if (!done && qn > 0) {
+                __syncwarp();
+                if (lane < qn) {
+                    const uint32_t e = sm.queue[lane];
+                    eval_pair(sm, (int)(e & 0xffu), (int)(e >> 8), llb, lub);
+                    ++evaluated;
+                }
+                mlb = warp_min(llb);
+                mub = warp_min(lub);
+                if (mlb == 0.0 && mub == 0.0) done = true;
+            }
+        }
+    }
+    out_lb = mlb;
+    out_ub = mub;
+}
+
+} // namespace tjx

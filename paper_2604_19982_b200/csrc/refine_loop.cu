@@ -1,0 +1,208 @@
+// Device-resident progressive refinement (reference refine_loop / run_level /
+// aggregate_object_bounds, src/refine.cpp:86-122, :136-314; paper Alg. 4-5).
+//
+// The active voxel-pair list lives in HBM for the whole loop. Per LOD level:
+//   1. the reference facet-pair count sum(r_len * s_len) is reduced from the CSR offsets;
+//   2. refine kernel launches (launch size = max(refine_chunk, 64Ki) voxel pairs; the
+//      outcome is independent of it) fold each voxel pair's exact minima into per-op
+//      minima with 64-bit atomicMin on the IEEE bit patterns (order-free and exact for
+//      non-negative doubles);
+//   3. one thread per op applies aggregate_object_bounds (skip ops whose minima stayed
+//      +inf, intersect_interval with the 1e-9 crossing tripwire) and, for within-tau,
+//      prune_within at this level's stage code; k-NN runs its pruning fixpoint;
+//   4. voxel pairs of decided ops are dropped by a stable compaction
+//      (erase_if, src/refine.cpp:299-301).
+#include <cub/cub.cuh>
+
+#include <chrono>
+
+#include "filter.cuh"
+#include "trace_sink.h"
+
+namespace tjx {
+
+namespace {
+
+__device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000ll); }
+
+__global__ void k_fill_u64(unsigned long long* p, uint64_t n, unsigned long long v) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+__global__ void k_facet_pairs(const ActiveVpDev* __restrict__ act, uint64_t n, const uint64_t* __restrict__ rf,
+                              const uint64_t* __restrict__ sf, unsigned long long* out) {
+    unsigned long long acc = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const ActiveVpDev a = act[i];
+        acc += (rf[a.gvr + 1] - rf[a.gvr]) * (sf[a.gvs + 1] - sf[a.gvs]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
+__global__ void k_aggregate(CandDev c, uint64_t n, const unsigned long long* __restrict__ lbb,
+                            const unsigned long long* __restrict__ ubb, int prune, double tau, int16_t stage,
+                            uint8_t* __restrict__ updated, DevError* err) {
+    for (uint64_t op = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; op < n; op += (uint64_t)gridDim.x * blockDim.x) {
+        if (updated) updated[op] = 0;
+        if (c.status[op] != TJ_UNDECIDED) continue;
+        const double mlb = __longlong_as_double((long long)lbb[op]);
+        const double mub = __longlong_as_double((long long)ubb[op]);
+        if (!(mlb < dinf())) continue; // every voxel pair empty at this level (or op not active)
+        double lb = c.lb[op], ub = c.ub[op];
+        lb = (lb < mlb) ? mlb : lb;
+        ub = (mub < ub) ? mub : ub;
+        if (lb > ub) {
+            if (lb - ub > 1e-9) {
+                atomicMin(&err->op, (uint32_t)op);
+                err->lb = lb;
+                err->ub = ub;
+                err->kind = 0;
+                atomicExch(&err->code, (int)TJ_EENGINE);
+            }
+            const double mid = 0.5 * (lb + ub);
+            lb = ub = mid;
+        }
+        c.lb[op] = lb;
+        c.ub[op] = ub;
+        if (updated) updated[op] = 1;
+        if (prune) { // prune_within (src/filter.cpp:241-263)
+            if (ub <= tau) {
+                c.status[op] = TJ_CONFIRMED;
+                c.decided_at[op] = stage;
+                atomicAdd(c.num_confirmed + c.pair_r[op], 1u);
+            } else if (lb > tau) {
+                c.status[op] = TJ_REMOVED;
+                c.decided_at[op] = stage;
+            }
+        }
+    }
+}
+
+struct StillUndecided {
+    const uint8_t* status;
+    __device__ __forceinline__ bool operator()(const ActiveVpDev& a) const { return status[a.op] == TJ_UNDECIDED; }
+};
+
+inline int grid_for(uint64_t items, int per_block, int num_sms) {
+    const uint64_t g = (items + per_block - 1) / per_block;
+    return (int)std::max<uint64_t>(1, std::min<uint64_t>(g, (uint64_t)num_sms * 32));
+}
+
+int level_slot(const DatasetDev& d, uint32_t level) {
+    for (size_t i = 0; i < d.levels.size(); ++i)
+        if (d.levels[i] == (int32_t)level) return (int)i;
+    return -1;
+}
+
+void check_error(DevError* err, cudaStream_t st) {
+    DevError h;
+    TJ_CUDA(cudaMemcpyAsync(&h, err, sizeof(DevError), cudaMemcpyDeviceToHost, st));
+    TJ_CUDA(cudaStreamSynchronize(st));
+    if (h.code == 0) return;
+    if (h.kind == 1) throw Error(TJ_EENGINE, "knn_apply_deltas: confirmed count exceeds k");
+    throw Error(TJ_EENGINE, "bound crossing: lb " + std::to_string(h.lb) + " > ub " + std::to_string(h.ub));
+}
+
+} // namespace
+
+uint64_t compact_active(Workspace& ws, const CandDevStore& cs, DevBuf<ActiveVpDev>& active, uint64_t n,
+                        cudaStream_t st) {
+    if (n == 0) return 0;
+    DevBuf<ActiveVpDev> out(n);
+    DevBuf<int64_t> nsel(1);
+    StillUndecided pred{cs.status.p};
+    size_t bytes = 0;
+    TJ_CUDA(cub::DeviceSelect::If(nullptr, bytes, active.p, out.p, nsel.p, (int64_t)n, pred, st));
+    ws.temp.reserve(bytes);
+    TJ_CUDA(cub::DeviceSelect::If(ws.temp.p, bytes, active.p, out.p, nsel.p, (int64_t)n, pred, st));
+    int64_t h = 0;
+    TJ_CUDA(cudaMemcpyAsync(&h, nsel.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    TJ_CUDA(cudaStreamSynchronize(st));
+    active = std::move(out);
+    return (uint64_t)h;
+}
+
+RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetDev& S, CandDevStore& cs,
+                              DevBuf<ActiveVpDev>& active, uint64_t n_active, const tj_join_spec& spec, bool knn,
+                              double tau, DevError* err, TraceSink* trace, cudaStream_t st) {
+    using Clock = std::chrono::steady_clock;
+    RefineLoopOut out;
+    const uint64_t n = cs.n;
+    DevBuf<unsigned long long> lbb(std::max<uint64_t>(n, 1)), ubb(std::max<uint64_t>(n, 1));
+    DevBuf<unsigned long long> counters(3), work(1);
+    DevBuf<uint8_t> updated;
+    if (trace && trace->on_interval) updated.alloc(std::max<uint64_t>(n, 1));
+    cudaEvent_t e0, e1;
+    TJ_CUDA(cudaEventCreate(&e0));
+    TJ_CUDA(cudaEventCreate(&e1));
+    const unsigned long long kInfBits = 0x7ff0000000000000ull;
+    const uint64_t launch = std::max<uint64_t>(spec.refine_chunk, 65536);
+    try {
+        for (uint32_t li = 0; li < spec.n_lods; ++li) {
+            if (n_active == 0) break;
+            const uint32_t level = spec.lods[li];
+            const int sr = level_slot(R, level), ss = level_slot(S, level);
+            const auto t0 = Clock::now();
+            LevelStats ls{};
+            ls.level = level;
+            ls.vps = n_active;
+            k_fill_u64<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(lbb.p, n, kInfBits);
+            k_fill_u64<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(ubb.p, n, kInfBits);
+            TJ_CUDA(cudaMemsetAsync(counters.p, 0, 24, st));
+            k_facet_pairs<<<grid_for(n_active, 256, ws.num_sms), 256, 0, st>>>(
+                active.p, n_active, R.facet_offsets[sr].p, S.facet_offsets[ss].p, counters.p + 2);
+            TJ_CUDA(cudaEventRecord(e0, st));
+            for (uint64_t c0 = 0; c0 < n_active; c0 += launch) {
+                RefineJoinArgs a{};
+                a.active = active.p + c0;
+                a.n_vp = std::min(launch, n_active - c0);
+                a.r_foff = R.facet_offsets[sr].p;
+                a.r_facets = R.facets[sr].p;
+                a.s_foff = S.facet_offsets[ss].p;
+                a.s_facets = S.facets[ss].p;
+                a.op_lb_bits = lbb.p;
+                a.op_ub_bits = ubb.p;
+                a.work = work.p;
+                a.counters = counters.p;
+                a.cull = (spec.flags & TJ_FLAG_NO_CULL) ? 0 : 1;
+                TJ_CUDA(cudaMemsetAsync(work.p, 0, 8, st));
+                launch_refine_join(a, ws.num_sms, st);
+            }
+            TJ_CUDA(cudaEventRecord(e1, st));
+            out.chunks += (n_active + spec.refine_chunk - 1) / spec.refine_chunk;
+            k_aggregate<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(cs.view(), n, lbb.p, ubb.p, knn ? 0 : 1, tau,
+                                                                      (int16_t)level, updated.p, err);
+            TJ_CUDA(cudaGetLastError());
+            check_error(err, st);
+            if (trace && trace->on_interval) trace->emit_updated(cs, updated, (int16_t)level, st);
+            if (knn) {
+                knn_fixpoint(ws, cs, spec.k, (int16_t)level, err, st);
+                check_error(err, st);
+            }
+            unsigned long long hc[3];
+            TJ_CUDA(cudaMemcpyAsync(hc, counters.p, 24, cudaMemcpyDeviceToHost, st));
+            TJ_CUDA(cudaStreamSynchronize(st));
+            float kms = 0.f;
+            TJ_CUDA(cudaEventElapsedTime(&kms, e0, e1));
+            ls.tested = hc[0];
+            ls.evaluated = hc[1];
+            ls.facet_pairs = hc[2];
+            ls.kernel_ms = kms;
+            n_active = compact_active(ws, cs, active, n_active, st);
+            ls.ms = std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+            out.levels.push_back(ls);
+        }
+    } catch (...) {
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        throw;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return out;
+}
+
+} // namespace tjx

@@ -1,0 +1,319 @@
+#!/usr/bin/env python3
+"""Benchmark: candidate object-pairs refined/sec of the B200 trijoin engine (BASELINE.json).
+
+A *step* is one full filter-and-refine join (MBB filter -> voxel-pair filter -> LOD 20/60/100
+refinement) of configuration B by default: intersection join of 100k x 100k synthetic nuclei
+(312-facet spheres) on one B200 (BASELINE.json configs[1]). Metric units are the candidate
+object pairs entering the voxel + LOD cascade (stats stages["voxel"].pairs_in).
+
+  value : device-resident datasets (uploaded once), K timed joins; CUDA events on the host
+          stream bracketing each blocking tj_join call, barrier + synchronize around the loop,
+          max over ranks.
+  e2e   : the public API with host buffers (`join_datasets`: pack -> H2D -> join -> D2H ->
+          records), same metric.
+  roofline: the refinement kernel (its own CUDA events on its launching stream): FLOPs =
+          evaluated facet pairs x 1500 + culling tests x 20 vs the FP32 peak
+          148 SM x 128 lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json).
+  cpu_baseline: the reference's own run_join (oracle/_ref, built from /root/reference) on a
+          deterministic R-slice of the same workload on all host cores (rank 0, N=1 only).
+
+--impl reference runs only the reference CPU arm (rank 0; other ranks exit 0).
+Multi-GPU (torchrun): query objects are sharded in blocks of 1024 across ranks (no data-path
+collective); result pairs are gathered to rank 0 at the end of the e2e run.
+"""
+import argparse
+import ctypes
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FLOP_PER_PAIR = 1500.0   # measured dynamic op count of tri_tri_distance + padding
+FLOP_PER_TEST = 20.0     # FP32 facet-box culling test
+TYPE_CODE = {"within": 0, "intersect": 1, "knn": 2}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="B")
+    p.add_argument("--scale", type=float, default=1.0, help="object-count scale (same density)")
+    p.add_argument("--data-dir", default=os.environ.get("TRIJOIN_BENCH_DIR", "/tmp/trijoin_bench"))
+    p.add_argument("--cpu-stride", type=int, default=100, help="R-slice stride of the CPU baseline sample")
+    p.add_argument("--ref-stride", type=int, default=250, help="R-slice stride per --impl reference step")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cull", action="store_true", help="disable exact-preserving culling (A/B)")
+    p.add_argument("--profile", action="store_true", help="one resident join only (for ncu)")
+    return p.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"sm_max_mhz": 1965.0, "hbm_gbs": 6650.0}, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, path, gpu):
+        self.path, self.proc = path, None
+        try:
+            self.f = open(path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(gpu), "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.close()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    mx = float(parts[2])
+                except ValueError:
+                    continue
+                for n, v in zip(names, parts[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def ref_shim():
+    lib = ctypes.CDLL(os.path.join(ROOT, "oracle", "_ref", "libref_shim.so"))
+    lib.ref_join_timed.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int, ctypes.c_double, ctypes.c_uint32,
+                                   ctypes.POINTER(ctypes.c_uint32), ctypes.c_uint32, ctypes.c_uint, ctypes.c_uint32,
+                                   ctypes.POINTER(ctypes.c_double)]
+    lib.ref_last_error.restype = ctypes.c_char_p
+    return lib
+
+
+def ref_join(lib, r_path, s_path, kw, lods, workers, repeats=1):
+    """The reference's own run_join on the host cores; loads untimed, joins timed."""
+    arr = (ctypes.c_uint32 * len(lods))(*lods)
+    out = (ctypes.c_double * 6)()
+    rc = lib.ref_join_timed(r_path.encode(), s_path.encode(), TYPE_CODE[kw["type"]], float(kw.get("tau", 0.0)),
+                            int(kw.get("k", 1)), arr, len(lods), workers, repeats, out)
+    if rc != 0:
+        raise RuntimeError("reference join failed: " + lib.ref_last_error().decode())
+    return {"ms": out[0], "pairs_in": out[1], "facet_pairs": out[2], "results": out[3], "cores": int(out[4])}
+
+
+def main():
+    a = parse()
+    world, rank, local = dist_env()
+    from paper_2604_19982_b200 import synth
+
+    name = a.config
+    _, _, kw = synth.CONFIGS[name]
+    lods = list(synth.LODS)
+    workload = {
+        "A": "A: within-tau 0.5, 1k nuclei (1012 f) x 1k vessels (1012 f)",
+        "B": "B: intersection join, 100k x 100k nuclei (312-facet spheres)",
+        "C": "C: k-NN k=3, 200k nuclei x 10k vessels",
+        "D": "D: within-tau 0.2, 1M x 1M nuclei",
+    }[name]
+    data_dir = os.path.join(a.data_dir, f"{name}_x{a.scale:g}")
+
+    if a.impl == "reference":
+        if rank != 0:
+            return 0
+        r_slice, s_path = synth.build_config(name, data_dir, scale=a.scale, r_stride=a.ref_stride)
+        lib = ref_shim()
+        workers = os.cpu_count() or 1
+        times, last = [], None
+        for i in range(a.warmup + a.steps):
+            last = ref_join(lib, r_slice, s_path, kw, lods, workers)
+            if i >= a.warmup:
+                times.append(last["ms"])
+        ms = float(np.mean(times))
+        value = last["pairs_in"] / (ms / 1e3)
+        sample = (f"R-slice every {a.ref_stride}th query object of {workload} vs the full S "
+                  f"({int(last['pairs_in'])} candidate pairs, {int(last['facet_pairs'])} facet pairs per step)")
+        line = {"metric": "candidate object-pairs refined/sec", "value": value, "unit": "pairs/s",
+                "impl": "reference", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": {"workload": workload, "lods": lods, "sample": sample},
+                "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": last["cores"], "kind": "reference",
+                                 "sample": sample},
+                "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return 0
+
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    os.environ.setdefault("TRIJOIN_DEVICES", str(local))
+    import paper_2604_19982_b200 as tj
+    from paper_2604_19982_b200 import _core
+
+    # ---- inputs (built once per box; node-local rank 0 writes, others wait) ----
+    t_setup = time.time()
+    if local == 0:
+        r_path, s_path = synth.build_config(name, data_dir, scale=a.scale)
+    if world > 1:
+        dist.barrier()
+    r_path, s_path = synth.build_config(name, data_dir, scale=a.scale)
+    R = tj.load_dataset(r_path)
+    S = tj.load_dataset(s_path)
+    res = tj.Resident(R, S, device=local)
+    setup_s = time.time() - t_setup
+    flags = 1 if a.no_cull else 0
+    run_kw = dict(type=kw["type"], tau=float(kw.get("tau", 0.0)), k=int(kw.get("k", 1)), lods=lods, flags=flags,
+                  shard_index=rank, shard_count=world)
+
+    if a.profile:
+        out = res.run(**run_kw)
+        if rank == 0:
+            print(json.dumps({"profile": True, "total_ms": out["total_ms"], "levels": out["levels"]}))
+        return 0
+
+    dev = torch.device("cuda", local)
+    for _ in range(a.warmup):
+        res.run(**run_kw)
+    launches0 = _core.kernel_launches()
+    clocks = Clocks(os.path.join(ROOT, "gpurun_out", f"clocks_rank{rank}.csv") if os.path.isdir(
+        os.path.join(ROOT, "gpurun_out")) else f"/tmp/trijoin_clocks_{rank}.csv", local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    outs = [res.run(**run_kw) for _ in range(a.steps)]
+    e1.record()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    launches = _core.kernel_launches() - launches0
+    elapsed_ms = e0.elapsed_time(e1)
+    pairs = float(outs[-1]["voxel_pairs_in"])
+    fp = float(sum(l["facet_pairs"] for l in outs[-1]["levels"]))
+    evaluated = float(sum(l["evaluated"] for l in outs[-1]["levels"]))
+    tested = float(sum(l["tested"] for l in outs[-1]["levels"]))
+    kernel_ms = float(np.mean([sum(l["kernel_ms"] for l in o["levels"]) for o in outs]))
+    stats = torch.tensor([elapsed_ms, pairs, fp, evaluated, tested, kernel_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        mx = stats.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = stats.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        elapsed_ms, kernel_ms = float(mx[0]), float(mx[5])
+        pairs, fp, evaluated, tested = (float(sm[i]) for i in range(1, 5))
+    ms_per_step = elapsed_ms / a.steps
+    value = pairs / (ms_per_step / 1e3)
+
+    peaks, peak_src = measured_peaks()
+    fp32_peak = 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12  # TFLOP/s
+    achieved = (evaluated * FLOP_PER_PAIR + tested * FLOP_PER_TEST) / (kernel_ms / 1e3) / 1e12 / max(world, 1)
+    roofline = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp32_peak, "traffic": None,
+                "kernel": "refine_join_kernel (all LOD levels)",
+                "peak_source": f"148 SM x 128 FP32 lanes x 2 x sm_max_mhz ({peak_src} MEASURED_PEAKS.json)",
+                "fp64_frac": achieved / (fp32_peak / 2),
+                "pairs_evaluated_per_s": evaluated / (kernel_ms / 1e3) / max(world, 1),
+                "ref_equiv_facet_pairs_per_s": fp / (kernel_ms / 1e3) / max(world, 1),
+                "cull_skip_frac": 1.0 - evaluated / fp if fp else None}
+
+    # ---- e2e: public API from host buffers ----
+    e2e = None
+    if not a.no_e2e:
+        h2d = float(res.device_bytes)
+        ts = []
+        d2h = 0
+        for i in range(max(1, min(a.steps, 3)) + 1):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            recs, js = _core.join_datasets(R, S, type=kw["type"], tau=float(kw.get("tau", 0.0)),
+                                           k=int(kw.get("k", 1)), lods=lods)
+            torch.cuda.synchronize(dev)
+            t1 = time.perf_counter()
+            if i > 0:
+                ts.append((t1 - t0) * 1e3)
+            st = json.loads(js)
+            n_c = st["stages"][0]["pairs_in"] - st["stages"][0]["removed"]
+            d2h = n_c * (4 + 4 + 8 + 8 + 1 + 2) + (R.n_objects + 1) * 8 + R.n_objects * 4
+            pairs_e2e = st["stages"][1]["pairs_in"]
+        e2e_ms = float(np.mean(ts))
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = {"value": pairs_e2e / (float(t[0]) / 1e3), "unit": "pairs/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": float(t[0]),
+               "path": "paper_2604_19982_b200._core.join_datasets -> trijoin::run_join -> tj_join (C-ABI)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        try:
+            r_slice, s_full = synth.build_config(name, data_dir + "_slice", scale=a.scale, r_stride=a.cpu_stride)
+            rj = ref_join(ref_shim(), r_slice, s_full, kw, lods, os.cpu_count() or 1)
+            cpu = {"value": rj["pairs_in"] / (rj["ms"] / 1e3), "unit": "pairs/s", "cores": rj["cores"],
+                   "kind": "reference",
+                   "sample": f"reference run_join (oracle/_ref) on every {a.cpu_stride}th query object vs the full S: "
+                             f"{int(rj['pairs_in'])} candidate pairs, {int(rj['facet_pairs'])} facet pairs, "
+                             f"{rj['ms'] / 1e3:.1f} s",
+                   "facet_pairs_per_s": rj["facet_pairs"] / (rj["ms"] / 1e3)}
+        except Exception as exc:  # noqa: BLE001
+            cpu = {"value": None, "unit": "pairs/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {exc}"}
+
+    if rank == 0:
+        line = {"metric": "candidate object-pairs refined/sec", "value": value, "unit": "pairs/s", "n_gpus": world,
+                "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "weak" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (replicated preprocessed sphere templates, reference generator placement)",
+                "config": {"workload": workload, "lods": lods, "scale": a.scale,
+                           "candidate_pairs": pairs, "facet_pairs_ref_count": fp,
+                           "join_wall_ms": ms_per_step, "l2": "inputs larger than L2 "
+                           f"({res.device_bytes / 1e9:.1f} GB resident)", "parallelism": f"r-shard x{world}",
+                           "setup_s": round(setup_s, 1), "cull": not a.no_cull},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+                "gpu_launches": int(launches)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -143,6 +143,8 @@ const char* tj_last_error(const tj_ctx* ctx);
 /* Library-wide last error for failures without a context (e.g. tj_ctx_create). */
 const char* tj_global_last_error(void);
 int tj_device_count(void);
+/* Number of this library's own CUDA kernel launches so far (process-wide). */
+uint64_t tj_kernel_launches(void);
 
 /* ---- datasets (resident in HBM) ---- */
 int tj_dataset_upload(tj_ctx* ctx, const tj_dataset_view* view, tj_dataset** out);

@@ -4,6 +4,7 @@
 // the product. Every probe calls the reference's own functions unchanged.
 #include <cstdint>
 #include <cstdio>
+#include <chrono>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -163,6 +164,50 @@ int ref_staged_dump(const char* r_path, const char* s_path, double tau, const ui
             put(ub.data(), 8 * ub.size());
         }
         std::fclose(f);
+    });
+}
+
+// The reference's own run_join (src/engine.cpp:122-237) timed at its own boundary: both
+// indexes are loaded first (untimed), then `repeats` joins run on ThreadPool(workers).
+// out[0] = best wall ms, out[1] = candidate pairs entering the voxel stage
+// (stats stages["voxel"].pairs_in), out[2] = sum of facet_pairs, out[3] = results,
+// out[4] = pool size, out[5] = total candidate pairs.
+int ref_join_timed(const char* r_path, const char* s_path, int type, double tau, uint32_t k,
+                   const uint32_t* lods, uint32_t n_lods, unsigned workers, uint32_t repeats,
+                   double* out) {
+    return guarded([&] {
+        const PreparedDataset R = load_index(r_path);
+        PreparedDataset s_store;
+        const PreparedDataset* S = &R;
+        if (s_path && *s_path && std::string(s_path) != r_path) {
+            s_store = load_index(s_path);
+            S = &s_store;
+        }
+        JoinSpec spec;
+        spec.type = type == 0 ? JoinType::Within : type == 1 ? JoinType::Intersect : JoinType::Knn;
+        spec.tau = tau;
+        spec.k = k;
+        spec.lods.assign(lods, lods + n_lods);
+        ThreadPool pool(workers);
+        double best = 1e300;
+        JoinOutput jo;
+        for (uint32_t i = 0; i < (repeats ? repeats : 1); ++i) {
+            const auto t0 = std::chrono::steady_clock::now();
+            jo = run_join(R, *S, spec, pool);
+            const double ms =
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+            best = std::min(best, ms);
+        }
+        uint64_t fp = 0;
+        for (const auto& st : jo.stats.stages) fp += st.facet_pairs;
+        out[0] = best;
+        out[1] = jo.stats.stages.size() > 1 ? static_cast<double>(jo.stats.stages[1].pairs_in) : 0.0;
+        out[2] = static_cast<double>(fp);
+        out[3] = static_cast<double>(jo.stats.results);
+        out[4] = pool.size();
+        out[5] = jo.stats.stages.empty()
+                     ? 0.0
+                     : static_cast<double>(jo.stats.stages[0].pairs_in - jo.stats.stages[0].removed);
     });
 }
 

@@ -117,6 +117,10 @@ T* host_copy(const DevBuf<T>& src, uint64_t n, cudaStream_t st) {
 } // namespace
 
 namespace tjx {
+unsigned long long& launch_counter_ref() {
+    static unsigned long long n = 0;
+    return n;
+}
 uint64_t compact_active(Workspace& ws, const CandDevStore& cs, DevBuf<ActiveVpDev>& active, uint64_t n,
                         cudaStream_t st);
 }
@@ -131,6 +135,8 @@ const char* tj_global_last_error(void) {
     copy = g_err;
     return copy.c_str();
 }
+
+uint64_t tj_kernel_launches(void) { return __atomic_load_n(&launch_counter_ref(), __ATOMIC_RELAXED); }
 
 int tj_device_count(void) {
     int n = 0;

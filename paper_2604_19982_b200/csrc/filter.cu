@@ -368,6 +368,7 @@ uint64_t scan_counts(Workspace& ws, const uint32_t* counts, uint64_t n, DevBuf<u
     if (n == 0) return 0;
     DevBuf<uint64_t>& wide = ws.u64a;
     wide.reserve(n);
+    count_launch();
     k_widen<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(counts, wide.p, n);
     size_t bytes = 0;
     TJ_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, wide.p, offsets.p + 1, (int64_t)n, st));
@@ -387,6 +388,7 @@ void mbb_prepare_s(Workspace& ws, const DatasetDev& S, SortedS& out, cudaStream_
     if (ns == 0) return;
     DevBuf<double> keys(ns), keys_out(ns);
     DevBuf<uint32_t> vals(ns);
+    count_launch();
     k_minx_keys<<<grid_for(ns, 256, ws.num_sms), 256, 0, st>>>(S.mbb.p, ns, keys.p, vals.p);
     size_t bytes = 0;
     TJ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.p, keys_out.p, vals.p, out.order.p, (int)ns, 0, 64, st));
@@ -394,6 +396,7 @@ void mbb_prepare_s(Workspace& ws, const DatasetDev& S, SortedS& out, cudaStream_
     TJ_CUDA(cub::DeviceRadixSort::SortPairs(ws.temp.p, bytes, keys.p, keys_out.p, vals.p, out.order.p, (int)ns, 0, 64, st));
     DevBuf<unsigned long long> ext(1);
     TJ_CUDA(cudaMemsetAsync(ext.p, 0, sizeof(unsigned long long), st));
+    count_launch();
     k_gather_sorted<<<grid_for(ns, 256, ws.num_sms), 256, 0, st>>>(S.mbb.p, out.order.p, ns, out.mbb.p, ext.p);
     unsigned long long bits = 0;
     TJ_CUDA(cudaMemcpyAsync(&bits, ext.p, 8, cudaMemcpyDeviceToHost, st));
@@ -413,6 +416,7 @@ void knn_kth_anchor(Workspace& ws, const MbbArgs& a, uint32_t k, DevBuf<double>&
     if (smem > 48 * 1024)
         TJ_CUDA(cudaFuncSetAttribute(k_knn_kth, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int grid = grid_for((uint64_t)a.nr * 32, 32 * warps_per_block, ws.num_sms);
+    count_launch();
     k_knn_kth<<<grid, 32 * warps_per_block, smem, st>>>(a, k, cap, u_k.p);
     TJ_CUDA(cudaGetLastError());
 }
@@ -420,12 +424,14 @@ void knn_kth_anchor(Workspace& ws, const MbbArgs& a, uint32_t k, DevBuf<double>&
 uint64_t mbb_candidates(Workspace& ws, const MbbArgs& a, CandDevStore& cs, cudaStream_t st) {
     const uint32_t nr = a.nr;
     DevBuf<uint32_t> counts(std::max<uint32_t>(nr, 1));
+    count_launch();
     k_mbb_count<<<grid_for((uint64_t)nr * 32, 256, ws.num_sms), 256, 0, st>>>(a, counts.p);
     TJ_CUDA(cudaGetLastError());
     const uint64_t n = scan_counts(ws, counts.p, nr, cs.r2op, st);
     cs.resize(n, nr);
     DevBuf<uint32_t> pr(std::max<uint64_t>(n, 1)), ps(std::max<uint64_t>(n, 1));
     if (n > 0) {
+        count_launch();
         k_mbb_fill<<<grid_for((uint64_t)nr * 32, 256, ws.num_sms), 256, 0, st>>>(a, cs.r2op.p, pr.p, ps.p);
         TJ_CUDA(cudaGetLastError());
         // sort each query's candidates by s (finalize_candidate_set, src/filter.cpp:65-66)
@@ -437,6 +443,7 @@ uint64_t mbb_candidates(Workspace& ws, const MbbArgs& a, CandDevStore& cs, cudaS
         TJ_CUDA(cub::DeviceSegmentedSort::SortKeys(ws.temp.p, bytes, ps.p, ps_sorted.p, (int64_t)n, (int64_t)nr,
                                                    cs.r2op.p, cs.r2op.p + 1, st));
         TJ_CUDA(cudaMemsetAsync(cs.num_confirmed.p, 0, sizeof(uint32_t) * std::max<uint32_t>(nr, 1), st));
+        count_launch();
         k_mbb_finalize<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(a, n, pr.p, ps_sorted.p, cs.view());
         TJ_CUDA(cudaGetLastError());
     } else {
@@ -460,6 +467,7 @@ VoxelOut voxel_filter(Workspace& ws, const VoxelArgs& a, CandDevStore& cs, DevBu
         TJ_CUDA(cudaMemsetAsync(touched.p, 0, touched.n, st));
     }
     if (n > 0) {
+        count_launch();
         k_vf_bounds<<<grid_for(n * 32, 256, ws.num_sms), 256, 0, st>>>(a, cs.view(), surv.p, stats.p,
                                                                         want_trace ? touched.p : nullptr);
         TJ_CUDA(cudaGetLastError());
@@ -473,6 +481,7 @@ VoxelOut voxel_filter(Workspace& ws, const VoxelArgs& a, CandDevStore& cs, DevBu
     out.survivors = total;
     active.reserve(std::max<uint64_t>(total, 1));
     if (total > 0) {
+        count_launch();
         k_vf_scatter<false><<<grid_for(n * 32, 256, ws.num_sms), 256, 0, st>>>(a, cs.view(), offsets.p, active.p,
                                                                                nullptr);
         TJ_CUDA(cudaGetLastError());
@@ -481,11 +490,13 @@ VoxelOut voxel_filter(Workspace& ws, const VoxelArgs& a, CandDevStore& cs, DevBu
         touched_host->resize(n);
         if (n) TJ_CUDA(cudaMemcpyAsync(touched_host->data(), touched.p, n, cudaMemcpyDeviceToHost, st));
         DevBuf<uint32_t> pc(std::max<uint64_t>(n, 1));
+        count_launch();
         if (n) k_pruned_count<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(a, cs.view(), touched.p, surv.p, pc.p);
         DevBuf<uint64_t> poff;
         const uint64_t np = scan_counts(ws, pc.p, n, poff, st);
         DevBuf<ActiveVpDev> pv(std::max<uint64_t>(np, 1));
         DevBuf<double> plb(std::max<uint64_t>(np, 1));
+        count_launch();
         if (np) k_vf_scatter<true><<<grid_for(n * 32, 256, ws.num_sms), 256, 0, st>>>(a, cs.view(), poff.p, pv.p, plb.p);
         std::vector<ActiveVpDev> hv(np);
         std::vector<double> hl(np);

@@ -94,20 +94,33 @@ __device__ __forceinline__ double point_dist(const double* a, const double* b) {
     return TJ_SQRT(vnorm2(d));
 }
 
-// A triangle as it sits in shared memory during refinement: vertices plus the
-// per-triangle quantities the reference recomputes inside every call. Each
-// derived value uses the reference's exact formula, so hoisting is bit-exact.
-struct TriRef {
-    V3 v0, v1, v2;
-    double lab, lbc, lac; // norm(v1-v0), norm(v2-v1), norm(v2-v0) == norm(v0-v2)
-    bool degenerate;      // triangle_degenerate (src/geom.cpp:29-35)
-};
+// ---------------------------------------------------------------------------------------
+// Triangles in shared memory. A staged facet record is kFacetWords doubles:
+//   [0..8] v0 v1 v2   [9] hd   [10] ph   [11] |v1-v0|   [12] |v2-v1|   [13] |v2-v0| (== |v0-v2|)
+//   [14] 1.0 if triangle_degenerate (src/geom.cpp:29-35) else 0.0
+// Records are addressed by 32-bit shared-window addresses; the geometry below loops over
+// vertices/edges with runtime indices into these records, so each formula exists once in
+// the binary (the fully unrolled form was 19k SASS instructions and starved the warps on
+// instruction fetch). Hoisting the per-triangle quantities is bit-exact: each is the
+// reference's own formula evaluated on the same inputs.
+constexpr int kFacetWords = 15;
 
-// triangle_degenerate, returning also the shape flag used by the culling logic.
-__device__ __forceinline__ bool tri_degenerate(const V3& v0, const V3& v1, const V3& v2,
-                                               double* n2_out, double* scale2_out) {
+__device__ __forceinline__ double lds(uint32_t a) {
+    double v;
+    asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ V3 ldv(uint32_t t, int i) {
+    const uint32_t a = t + 24u * (uint32_t)i;
+    return {lds(a), lds(a + 8), lds(a + 16)};
+}
+__device__ __forceinline__ double ldw(uint32_t t, int w) { return lds(t + 8u * (uint32_t)w); }
+
+// triangle_degenerate, also returning n2 and scale2 (used by the culling shape test).
+__device__ __forceinline__ bool tri_degenerate(const V3& v0, const V3& v1, const V3& v2, double* n2_out,
+                                               double* scale2_out) {
     const V3 ab = vsub(v1, v0), ac = vsub(v2, v0), bc = vsub(v2, v1);
-    double s2 = vnorm2(ab);  // std::max({norm2(ab), norm2(ac), norm2(bc)})
+    double s2 = vnorm2(ab); // std::max({norm2(ab), norm2(ac), norm2(bc)})
     const double n_ac = vnorm2(ac), n_bc = vnorm2(bc);
     if (s2 < n_ac) s2 = n_ac;
     if (s2 < n_bc) s2 = n_bc;
@@ -126,20 +139,18 @@ __device__ __forceinline__ double point_segment_d2(const V3& p, const V3& a, con
     return vnorm2(vsub(p, vadd(a, vmul(d, t))));
 }
 
-// point_triangle_distance squared (src/geom.cpp:39-80).
-__device__ __forceinline__ double point_triangle_d2(const V3& p, const TriRef& t) {
-    if (t.degenerate) {
+// point_triangle_distance squared (src/geom.cpp:39-80); t = staged record.
+__device__ __forceinline__ double point_triangle_d2(const V3& p, uint32_t t) {
+    const V3 a = ldv(t, 0), b = ldv(t, 1), c = ldv(t, 2);
+    if (ldw(t, 14) != 0.0) {
         // std::min({psd(v0,v1), psd(v1,v2), psd(v2,v0)}) keeps the first smallest
-        double m = point_segment_d2(p, t.v0, t.v1);
-        const double m1 = point_segment_d2(p, t.v1, t.v2);
-        const double m2 = point_segment_d2(p, t.v2, t.v0);
+        double m = point_segment_d2(p, a, b);
+        const double m1 = point_segment_d2(p, b, c);
+        const double m2 = point_segment_d2(p, c, a);
         if (m1 < m) m = m1;
         if (m2 < m) m = m2;
         return m;
     }
-    const V3& a = t.v0;
-    const V3& b = t.v1;
-    const V3& c = t.v2;
     const V3 ab = vsub(b, a), ac = vsub(c, a), ap = vsub(p, a);
     const double d1 = vdot(ab, ap), d2 = vdot(ac, ap);
     const V3 bp = vsub(p, b);
@@ -152,34 +163,28 @@ __device__ __forceinline__ double point_triangle_d2(const V3& p, const TriRef& t
     const double d43 = TJ_SUB(d4, d3), d56 = TJ_SUB(d5, d6);
 
     // Region predicates in the reference's order; the first true one wins.
-    const bool r0 = d1 <= 0.0 && d2 <= 0.0;
-    const bool r1 = d3 >= 0.0 && d4 <= d3;
-    const bool r2 = vc <= 0.0 && d1 >= 0.0 && d3 <= 0.0;
-    const bool r3 = d6 >= 0.0 && d5 <= d6;
-    const bool r4 = vb <= 0.0 && d2 >= 0.0 && d6 <= 0.0;
-    const bool r5 = va <= 0.0 && d43 >= 0.0 && d56 >= 0.0;
-    // region id 0..6 (6 = interior)
-    int reg = 6;
-    if (r5) reg = 5;
-    if (r4) reg = 4;
-    if (r3) reg = 3;
-    if (r2) reg = 2;
-    if (r1) reg = 1;
-    if (r0) reg = 0;
+    int reg = 6; // interior
+    if (va <= 0.0 && d43 >= 0.0 && d56 >= 0.0) reg = 5;
+    if (vb <= 0.0 && d2 >= 0.0 && d6 <= 0.0) reg = 4;
+    if (d6 >= 0.0 && d5 <= d6) reg = 3;
+    if (vc <= 0.0 && d1 >= 0.0 && d3 <= 0.0) reg = 2;
+    if (d3 >= 0.0 && d4 <= d3) reg = 1;
+    if (d1 <= 0.0 && d2 <= 0.0) reg = 0;
 
-    // One division: the region's own quotient.
-    double num = 1.0, den = TJ_ADD(TJ_ADD(va, vb), vc); // interior: denom = 1/(va+vb+vc)
+    // One division: the region's own quotient (interior: denom = 1/(va+vb+vc)).
+    double num = 1.0, den = TJ_ADD(TJ_ADD(va, vb), vc);
     if (reg == 2) { num = d1; den = TJ_SUB(d1, d3); }
     if (reg == 4) { num = d2; den = TJ_SUB(d2, d6); }
     if (reg == 5) { num = d43; den = TJ_ADD(d43, d56); }
     const double q = TJ_DIV(num, den);
 
-    // Closest point X, each candidate with the reference's formula.
+    // Closest point X, each candidate with the reference's formula:
+    // a+ab*v | a+ac*w | b+(c-b)*w | (a+ab*v)+ac*w.
     const V3 bc = vsub(c, b);
     const V3 base = (reg == 5) ? b : a;
     const V3 e1 = (reg == 4) ? ac : ((reg == 5) ? bc : ab);
     const double s1 = (reg == 6) ? TJ_MUL(vb, q) : q;
-    V3 x = vadd(base, vmul(e1, s1)); // a+ab*v | a+ac*w | b+(c-b)*w | a+ab*v (interior, 1st term)
+    V3 x = vadd(base, vmul(e1, s1));
     if (reg == 6) x = vadd(x, vmul(ac, TJ_MUL(vc, q)));
     if (reg == 0) x = a;
     if (reg == 1) x = b;
@@ -188,8 +193,7 @@ __device__ __forceinline__ double point_triangle_d2(const V3& p, const TriRef& t
 }
 
 // segment_segment_distance squared (src/geom.cpp:82-113).
-__device__ __forceinline__ double segment_segment_d2(const V3& p1, const V3& q1, const V3& p2,
-                                                     const V3& q2) {
+__device__ __forceinline__ double segment_segment_d2(const V3& p1, const V3& q1, const V3& p2, const V3& q2) {
     const V3 d1 = vsub(q1, p1), d2 = vsub(q2, p2), r = vsub(p1, p2);
     const double a = vnorm2(d1), e = vnorm2(d2), f = vdot(d2, r);
     double s = 0.0, t = 0.0;
@@ -218,91 +222,86 @@ __device__ __forceinline__ double segment_segment_d2(const V3& p1, const V3& q1,
 }
 
 // segment_pierces_triangle (src/geom.cpp:120-136) with the three norms hoisted.
-__device__ __forceinline__ bool segment_pierces(const V3& p, const V3& q, double ndir,
-                                                const TriRef& t) {
+__device__ __forceinline__ bool segment_pierces(const V3& p, const V3& q, double ndir, uint32_t t) {
+    const V3 v0 = ldv(t, 0), v1 = ldv(t, 1), v2 = ldv(t, 2);
     const V3 dir = vsub(q, p);
-    const V3 e1 = vsub(t.v1, t.v0), e2 = vsub(t.v2, t.v0);
+    const V3 e1 = vsub(v1, v0), e2 = vsub(v2, v0);
     const V3 pv = vcross(dir, e2);
     const double det = vdot(e1, pv);
-    const double scale = TJ_MUL(TJ_MUL(ndir, t.lab), t.lac);
-    const bool ok_det = !(fabs(det) <= TJ_MUL(1e-14, scale));
+    const double scale = TJ_MUL(TJ_MUL(ndir, ldw(t, 11)), ldw(t, 13));
+    if (fabs(det) <= TJ_MUL(1e-14, scale)) return false;
     const double inv = TJ_DIV(1.0, det);
-    const V3 tv = vsub(p, t.v0);
+    const V3 tv = vsub(p, v0);
     const double u = TJ_MUL(vdot(tv, pv), inv);
+    if (u < 0.0 || u > 1.0) return false;
     const V3 qv = vcross(tv, e1);
     const double v = TJ_MUL(vdot(dir, qv), inv);
+    if (v < 0.0 || TJ_ADD(u, v) > 1.0) return false;
     const double tt = TJ_MUL(vdot(e2, qv), inv);
-    return ok_det && !(u < 0.0 || u > 1.0) && !(v < 0.0 || TJ_ADD(u, v) > 1.0) && tt >= 0.0 &&
-           tt <= 1.0;
+    return tt >= 0.0 && tt <= 1.0;
 }
 
 // triangle_less (src/geom.cpp:140-148): lexicographic over the 9 coordinates.
-__device__ __forceinline__ bool tri_less(const TriRef& a, const TriRef& b) {
-    const double pa[9] = {a.v0.x, a.v0.y, a.v0.z, a.v1.x, a.v1.y, a.v1.z, a.v2.x, a.v2.y, a.v2.z};
-    const double pb[9] = {b.v0.x, b.v0.y, b.v0.z, b.v1.x, b.v1.y, b.v1.z, b.v2.x, b.v2.y, b.v2.z};
-    int res = 0; // 0 undecided, 1 less, 2 greater
-#pragma unroll
+__device__ __forceinline__ bool tri_less(uint32_t a, uint32_t b) {
+#pragma unroll 1
     for (int i = 0; i < 9; ++i) {
-        if (res == 0 && pa[i] < pb[i]) res = 1;
-        if (res == 0 && pa[i] > pb[i]) res = 2;
+        const double x = ldw(a, i), y = ldw(b, i);
+        if (x < y) return true;
+        if (x > y) return false;
     }
-    return res == 1;
+    return false;
 }
 
-// tri_tri_distance (src/geom.cpp:152-183).
-__device__ __forceinline__ double tri_tri(const TriRef& A, const TriRef& B) {
+// tri_tri_distance (src/geom.cpp:152-183) on two staged records.
+__device__ __forceinline__ double tri_tri(uint32_t A, uint32_t B) {
     double best2 = __longlong_as_double(0x7ff0000000000000ll); // +inf
-    // 6 vertex-triangle candidates: an order-free set under canonicalisation.
-    best2 = smin(best2, point_triangle_d2(A.v0, B));
-    best2 = smin(best2, point_triangle_d2(B.v0, A));
-    best2 = smin(best2, point_triangle_d2(A.v1, B));
-    best2 = smin(best2, point_triangle_d2(B.v1, A));
-    best2 = smin(best2, point_triangle_d2(A.v2, B));
-    best2 = smin(best2, point_triangle_d2(B.v2, A));
+    // 6 vertex-triangle candidates: {A's vertices -> B} U {B's vertices -> A}, an order-free set.
+#pragma unroll 1
+    for (int k = 0; k < 6; ++k) {
+        const uint32_t src = (k & 1) ? B : A, dst = (k & 1) ? A : B;
+        best2 = smin(best2, point_triangle_d2(ldv(src, k >> 1), dst));
+    }
     // 9 edge-edge candidates with t1 = the lexicographically smaller triangle.
     const bool swap = tri_less(B, A);
-    const TriRef& t1 = swap ? B : A;
-    const TriRef& t2 = swap ? A : B;
-    const V3 a[3] = {t1.v0, t1.v1, t1.v2};
-    const V3 b[3] = {t2.v0, t2.v1, t2.v2};
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-            best2 = smin(best2, segment_segment_d2(a[i], a[(i + 1) % 3], b[j], b[(j + 1) % 3]));
-        }
+    const uint32_t t1 = swap ? B : A, t2 = swap ? A : B;
+#pragma unroll 1
+    for (int m = 0; m < 9; ++m) {
+        const int i = m / 3, j = m - 3 * (m / 3);
+        const int i1 = i == 2 ? 0 : i + 1, j1 = j == 2 ? 0 : j + 1;
+        best2 = smin(best2, segment_segment_d2(ldv(t1, i), ldv(t1, i1), ldv(t2, j), ldv(t2, j1)));
     }
     const double best = TJ_SQRT(best2);
     if (best > 0.0) {
-        // edges of A through B (if B is not degenerate), edges of B through A: order-free OR
-        bool hit = false;
-        if (!B.degenerate) {
-            hit = hit || segment_pierces(A.v0, A.v1, A.lab, B);
-            hit = hit || segment_pierces(A.v1, A.v2, A.lbc, B);
-            hit = hit || segment_pierces(A.v2, A.v0, A.lac, B);
+        // edges of A through B (if B is not degenerate) and of B through A: an order-free OR
+#pragma unroll 1
+        for (int k = 0; k < 6; ++k) {
+            const uint32_t src = k < 3 ? A : B, tri = k < 3 ? B : A;
+            const int e = k < 3 ? k : k - 3;
+            if (ldw(tri, 14) != 0.0) continue;
+            const int e1 = e == 2 ? 0 : e + 1;
+            if (segment_pierces(ldv(src, e), ldv(src, e1), ldw(src, 11 + e), tri)) return 0.0;
         }
-        if (!A.degenerate) {
-            hit = hit || segment_pierces(B.v0, B.v1, B.lab, A);
-            hit = hit || segment_pierces(B.v1, B.v2, B.lbc, A);
-            hit = hit || segment_pierces(B.v2, B.v0, B.lac, A);
-        }
-        if (hit) return 0.0;
     }
     return best;
 }
 
-// Build the hoisted per-triangle data from the 9 coordinates.
-__device__ __forceinline__ TriRef make_tri(const double* c, double* n2_out = nullptr,
-                                           double* scale2_out = nullptr) {
-    TriRef t;
-    t.v0 = {c[0], c[1], c[2]};
-    t.v1 = {c[3], c[4], c[5]};
-    t.v2 = {c[6], c[7], c[8]};
-    t.lab = TJ_SQRT(vnorm2(vsub(t.v1, t.v0)));
-    t.lbc = TJ_SQRT(vnorm2(vsub(t.v2, t.v1)));
-    t.lac = TJ_SQRT(vnorm2(vsub(t.v2, t.v0)));
-    t.degenerate = tri_degenerate(t.v0, t.v1, t.v2, n2_out, scale2_out);
-    return t;
+// Stage the 9 coordinates (+ hd, ph) into a record at shared address t. Returns the
+// degenerate flag; n2/scale2 feed the culling shape test.
+__device__ __forceinline__ void sts(uint32_t a, double v) { asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v)); }
+
+__device__ __forceinline__ bool stage_exact(const double* c, double hd, double ph, uint32_t t, double* n2,
+                                            double* s2) {
+    const V3 v0 = {c[0], c[1], c[2]}, v1 = {c[3], c[4], c[5]}, v2 = {c[6], c[7], c[8]};
+#pragma unroll
+    for (int k = 0; k < 9; ++k) sts(t + 8u * k, c[k]);
+    sts(t + 72, hd);
+    sts(t + 80, ph);
+    sts(t + 88, TJ_SQRT(vnorm2(vsub(v1, v0))));
+    sts(t + 96, TJ_SQRT(vnorm2(vsub(v2, v1))));
+    sts(t + 104, TJ_SQRT(vnorm2(vsub(v2, v0))));
+    const bool degen = tri_degenerate(v0, v1, v2, n2, s2);
+    sts(t + 112, degen ? 1.0 : 0.0);
+    return degen;
 }
 
 } // namespace tjx

@@ -251,4 +251,5 @@ PYBIND11_MODULE(_core, m) {
         py::arg("a"), py::arg("b"));
 
     m.def("device_count", [] { return tj_device_count(); });
+    m.def("kernel_launches", [] { return tj_kernel_launches(); });
 }

@@ -136,6 +136,7 @@ uint64_t knn_fixpoint(Workspace& ws, CandDevStore& cs, uint32_t k, int16_t stage
     TJ_CUDA(cudaMemsetAsync(total.p, 0, 8, st));
     const uint64_t threads = (uint64_t)cs.nq * 32;
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((threads + 255) / 256, (uint64_t)ws.num_sms * 16));
+    count_launch();
     k_knn_fixpoint<<<grid, 256, 0, st>>>(cs.view(), cs.nq, k, stage, delta.p, err, total.p);
     TJ_CUDA(cudaGetLastError());
     unsigned long long h = 0;
@@ -152,6 +153,7 @@ void knn_finalize_dev(Workspace& ws, CandDevStore& cs, uint32_t k, cudaStream_t 
     DevBuf<uint8_t> delta(cs.n);
     const uint64_t threads = (uint64_t)cs.nq * 32;
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((threads + 255) / 256, (uint64_t)ws.num_sms * 16));
+    count_launch();
     k_knn_finalize<<<grid, 256, 0, st>>>(cs.view(), cs.nq, k, delta.p);
     TJ_CUDA(cudaGetLastError());
     TJ_CUDA(cudaStreamSynchronize(st));

@@ -25,7 +25,7 @@ __device__ __forceinline__ void flush_counters(unsigned long long tested, unsign
     }
 }
 
-__global__ void __launch_bounds__(kThreads, 2) refine_join_kernel(RefineJoinArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) refine_join_kernel(RefineJoinArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     WarpSmem& sm = reinterpret_cast<WarpSmem*>(smem_raw)[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(kThreads, 2) refine_join_kernel(RefineJoinArgs
     flush_counters(tested, evaluated, a.counters);
 }
 
-__global__ void __launch_bounds__(kThreads, 2) refine_batch_kernel(RefineBatchArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) refine_batch_kernel(RefineBatchArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     WarpSmem& sm = reinterpret_cast<WarpSmem*>(smem_raw)[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
@@ -77,12 +77,17 @@ __global__ void __launch_bounds__(kThreads, 2) refine_batch_kernel(RefineBatchAr
     flush_counters(tested, evaluated, a.counters);
 }
 
-__global__ void tri_tri_batch_kernel(uint64_t n, const double* __restrict__ a9, const double* __restrict__ b9,
-                                     double* __restrict__ out) {
+__device__ __noinline__ double tri_tri_call(uint32_t a, uint32_t b) { return tri_tri(a, b); }
+
+__global__ void __launch_bounds__(128) tri_tri_batch_kernel(uint64_t n, const double* __restrict__ a9,
+                                                            const double* __restrict__ b9, double* __restrict__ out) {
+    __shared__ double rec[128][2][kFacetWords];
+    const uint32_t ta = smem_addr(&rec[threadIdx.x][0][0]), tb = smem_addr(&rec[threadIdx.x][1][0]);
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const TriRef A = make_tri(a9 + 9 * i);
-        const TriRef B = make_tri(b9 + 9 * i);
-        out[i] = tri_tri(A, B);
+        double n2, s2;
+        stage_exact(a9 + 9 * i, 0.0, 0.0, ta, &n2, &s2);
+        stage_exact(b9 + 9 * i, 0.0, 0.0, tb, &n2, &s2);
+        out[i] = tri_tri_call(ta, tb);
     }
 }
 
@@ -105,7 +110,8 @@ void launch_refine_join(const RefineJoinArgs& a, int num_sms, cudaStream_t st) {
         attr = true;
     }
     const uint64_t want = (a.n_vp + kWarps - 1) / kWarps;
-    const int grid = (int)std::min<uint64_t>(want, (uint64_t)num_sms * 2);
+    const int grid = (int)std::min<uint64_t>(want, (uint64_t)num_sms * 4);
+    count_launch();
     refine_join_kernel<<<grid, kThreads, refine_smem_bytes(), st>>>(a);
     TJ_CUDA(cudaGetLastError());
 }
@@ -119,7 +125,8 @@ void launch_refine_batch(const RefineBatchArgs& a, int num_sms, cudaStream_t st)
         attr = true;
     }
     const uint64_t want = (a.n_vp + kWarps - 1) / kWarps;
-    const int grid = (int)std::min<uint64_t>(want, (uint64_t)num_sms * 2);
+    const int grid = (int)std::min<uint64_t>(want, (uint64_t)num_sms * 4);
+    count_launch();
     refine_batch_kernel<<<grid, kThreads, refine_smem_bytes(), st>>>(a);
     TJ_CUDA(cudaGetLastError());
 }
@@ -127,6 +134,7 @@ void launch_refine_batch(const RefineBatchArgs& a, int num_sms, cudaStream_t st)
 void launch_tri_tri_batch(uint64_t n, const double* a9, const double* b9, double* out, cudaStream_t st) {
     if (!n) return;
     const int grid = (int)std::min<uint64_t>((n + 127) / 128, 148 * 8);
+    count_launch();
     tri_tri_batch_kernel<<<grid, 128, 0, st>>>(n, a9, b9, out);
     TJ_CUDA(cudaGetLastError());
 }
@@ -134,6 +142,7 @@ void launch_tri_tri_batch(uint64_t n, const double* a9, const double* b9, double
 void launch_mindist_batch(uint64_t n, const double* a6, const double* b6, double* out, cudaStream_t st) {
     if (!n) return;
     const int grid = (int)std::min<uint64_t>((n + 255) / 256, 148 * 8);
+    count_launch();
     mindist_batch_kernel<<<grid, 256, 0, st>>>(n, a6, b6, out);
     TJ_CUDA(cudaGetLastError());
 }

@@ -35,7 +35,7 @@
 namespace tjx {
 
 constexpr int kRT = 32;      // r facets per tile (one per lane)
-constexpr int kST = 64;      // s facets per tile
+constexpr int kST = 32;      // s facets per tile
 constexpr int kFS = 15;      // doubles per staged facet: v[9] hd ph lab lbc lac flags
 constexpr int kCS = 24;      // floats per culling record
 constexpr int kWarps = 4;    // warps per CTA
@@ -64,7 +64,12 @@ struct RefineCounters {
 __device__ __forceinline__ float rd(double x) { return __double2float_rd(x); }
 __device__ __forceinline__ float ru(double x) { return __double2float_ru(x); }
 
-// Stage one facet record (TJ_FACET_STRIDE doubles: v[9] hd ph pad) into shared memory.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Stage one facet record (TJ_FACET_STRIDE doubles: v[9] hd ph pad) into shared memory:
+// the exact record (geom_exact.cuh layout) at `sm` and the FP32 culling record at `cr`.
 __device__ __forceinline__ void stage_facet(const double* __restrict__ g, double* sm, float* cr) {
     const double2* g2 = reinterpret_cast<const double2*>(g);
     double c[12];
@@ -75,15 +80,9 @@ __device__ __forceinline__ void stage_facet(const double* __restrict__ g, double
         c[2 * k + 1] = t.y;
     }
     double n2, s2;
-    const TriRef t = make_tri(c, &n2, &s2);
-#pragma unroll
-    for (int k = 0; k < 11; ++k) sm[k] = c[k];
-    sm[11] = t.lab;
-    sm[12] = t.lbc;
-    sm[13] = t.lac;
+    const bool degen = stage_exact(c, c[9], c[10], smem_addr(sm), &n2, &s2);
     const bool shaped = n2 >= TJ_MUL(TJ_MUL(1e-4, s2), s2);
-    const bool ok = !t.degenerate && shaped;
-    sm[14] = t.degenerate ? 1.0 : 0.0;
+    const bool ok = !degen && shaped;
 
     float M = 0.f;
 #pragma unroll
@@ -100,10 +99,9 @@ __device__ __forceinline__ void stage_facet(const double* __restrict__ g, double
     cr[8] = rd(c[9]);
     cr[9] = ru(c[10]);
     cr[10] = ok ? 1.f : 0.f;
-    // unit edge directions and unit normal (only used as conditioning estimates)
-    const V3 e0 = vsub(t.v1, t.v0), e1 = vsub(t.v2, t.v1), e2 = vsub(t.v0, t.v2);
-    const V3 n = vcross(vsub(t.v1, t.v0), vsub(t.v2, t.v0));
-    const V3 es[4] = {e0, e1, e2, n};
+    // unit edge directions and unit normal (conditioning estimates only)
+    const V3 v0 = {c[0], c[1], c[2]}, v1 = {c[3], c[4], c[5]}, v2 = {c[6], c[7], c[8]};
+    const V3 es[4] = {vsub(v1, v0), vsub(v2, v1), vsub(v0, v2), vcross(vsub(v1, v0), vsub(v2, v0))};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const double l2 = vnorm2(es[k]);
@@ -113,18 +111,6 @@ __device__ __forceinline__ void stage_facet(const double* __restrict__ g, double
         cr[13 + 3 * k] = (float)(es[k].z * inv);
     }
     cr[23] = 0.f;
-}
-
-__device__ __forceinline__ TriRef load_tri(const double* sm) {
-    TriRef t;
-    t.v0 = {sm[0], sm[1], sm[2]};
-    t.v1 = {sm[3], sm[4], sm[5]};
-    t.v2 = {sm[6], sm[7], sm[8]};
-    t.lab = sm[11];
-    t.lbc = sm[12];
-    t.lac = sm[13];
-    t.degenerate = sm[14] != 0.0;
-    return t;
 }
 
 // Rigorous lower bound of the AABB gap (outward-rounded boxes, round-down arithmetic).
@@ -170,18 +156,19 @@ __device__ __forceinline__ double warp_min(double v) {
     return v;
 }
 
-// Exact evaluation of pair (i in r tile, j in s tile); folds into the lane minima.
-__device__ __forceinline__ void eval_pair(const WarpSmem& sm, int i, int j, double& mlb, double& mub) {
-    const double* ra = sm.rf + i * kFS;
-    const double* sb = sm.sf + j * kFS;
-    const TriRef A = load_tri(ra);
-    const TriRef B = load_tri(sb);
-    const double d = tri_tri(A, B);
-    // std::max(0.0, dist - ph[fi] - ph[fj]); dist + hd[fi] + hd[fj]   (src/refine.cpp:78-79)
-    const double lbp = smax(0.0, TJ_SUB(TJ_SUB(d, ra[10]), sb[10]));
-    const double ubp = TJ_ADD(TJ_ADD(d, ra[9]), sb[9]);
-    mlb = smin(mlb, lbp);
-    mub = smin(mub, ubp);
+// Exact evaluation of one facet pair (staged records at shared addresses ra, sb):
+// returns (max(0, d - ph_r - ph_s), d + hd_r + hd_s)  (src/refine.cpp:77-79). Not inlined:
+// one copy of the geometry serves every call site (instruction-cache footprint).
+__device__ __noinline__ double2 eval_pair(uint32_t ra, uint32_t sb) {
+    const double d = tri_tri(ra, sb);
+    const double lbp = smax(0.0, TJ_SUB(TJ_SUB(d, ldw(ra, 10)), ldw(sb, 10)));
+    const double ubp = TJ_ADD(TJ_ADD(d, ldw(ra, 9)), ldw(sb, 9));
+    return make_double2(lbp, ubp);
+}
+
+__device__ __forceinline__ void fold(double2 v, double& mlb, double& mub) {
+    mlb = smin(mlb, v.x);
+    mub = smin(mub, v.y);
 }
 
 // One voxel pair: facets [r_base, r_base + r_len) x [s_base, s_base + s_len), each
@@ -193,6 +180,8 @@ __device__ __forceinline__ void refine_voxel_pair(WarpSmem& sm, const double* __
     const int lane = threadIdx.x & 31;
     const double kInf = __longlong_as_double(0x7ff0000000000000ll);
     double mlb = kInf, mub = kInf; // warp-uniform after every reduction
+    const uint32_t rbase = smem_addr(sm.rf), sbase = smem_addr(sm.sf);
+    constexpr uint32_t kRec = kFS * 8;
     bool done = false;
     for (uint32_t r0 = 0; r0 < r_len && !done; r0 += kRT) {
         const int rcnt = (int)min((uint32_t)kRT, r_len - r0);
@@ -219,7 +208,7 @@ __device__ __forceinline__ void refine_voxel_pair(WarpSmem& sm, const double* __
                     }
                 }
                 if (seed_j >= 0) {
-                    eval_pair(sm, lane, seed_j, llb, lub);
+                    fold(eval_pair(rbase + lane * kRec, sbase + seed_j * kRec), llb, lub);
                     ++evaluated;
                 }
                 mlb = warp_min(llb);
@@ -242,7 +231,7 @@ __device__ __forceinline__ void refine_voxel_pair(WarpSmem& sm, const double* __
                 if (qn >= 32) {
                     __syncwarp();
                     const uint32_t e = sm.queue[lane];
-                    eval_pair(sm, (int)(e & 0xffu), (int)(e >> 8), llb, lub);
+                    fold(eval_pair(rbase + (e & 0xffu) * kRec, sbase + (e >> 8) * kRec), llb, lub);
                     ++evaluated;
                     __syncwarp();
                     if (lane < qn - 32) sm.queue[lane] = sm.queue[32 + lane];
@@ -259,7 +248,7 @@ __device__ __forceinline__ void refine_voxel_pair(WarpSmem& sm, const double* __
                 __syncwarp();
                 if (lane < qn) {
                     const uint32_t e = sm.queue[lane];
-                    eval_pair(sm, (int)(e & 0xffu), (int)(e >> 8), llb, lub);
+                    fold(eval_pair(rbase + (e & 0xffu) * kRec, sbase + (e >> 8) * kRec), llb, lub);
                     ++evaluated;
                 }
                 mlb = warp_min(llb);

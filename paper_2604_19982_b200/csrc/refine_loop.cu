@@ -149,9 +149,12 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
             LevelStats ls{};
             ls.level = level;
             ls.vps = n_active;
+            count_launch();
             k_fill_u64<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(lbb.p, n, kInfBits);
+            count_launch();
             k_fill_u64<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(ubb.p, n, kInfBits);
             TJ_CUDA(cudaMemsetAsync(counters.p, 0, 24, st));
+            count_launch();
             k_facet_pairs<<<grid_for(n_active, 256, ws.num_sms), 256, 0, st>>>(
                 active.p, n_active, R.facet_offsets[sr].p, S.facet_offsets[ss].p, counters.p + 2);
             TJ_CUDA(cudaEventRecord(e0, st));
@@ -173,6 +176,7 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
             }
             TJ_CUDA(cudaEventRecord(e1, st));
             out.chunks += (n_active + spec.refine_chunk - 1) / spec.refine_chunk;
+            count_launch();
             k_aggregate<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(cs.view(), n, lbb.p, ubb.p, knn ? 0 : 1, tau,
                                                                       (int16_t)level, updated.p, err);
             TJ_CUDA(cudaGetLastError());

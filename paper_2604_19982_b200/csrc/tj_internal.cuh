@@ -11,6 +11,10 @@
 
 namespace tjx {
 
+// Process-wide count of this library's own kernel launches (tj_kernel_launches()).
+unsigned long long& launch_counter_ref();
+inline void count_launch() { __atomic_fetch_add(&launch_counter_ref(), 1ull, __ATOMIC_RELAXED); }
+
 // Error carried through the C-ABI boundary as a status code.
 struct Error : std::runtime_error {
     int code;

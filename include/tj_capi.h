@@ -151,6 +151,16 @@ int tj_dataset_upload(tj_ctx* ctx, const tj_dataset_view* view, tj_dataset** out
 void tj_dataset_free(tj_dataset* ds);
 uint64_t tj_dataset_device_bytes(const tj_dataset* ds);
 
+/* ---- host-side index loading (backs load_index, reference src/index_io.cpp:244-249) ----
+   Parses a 3DPJ1 index file and packs it into the tj_dataset_view layout in host memory,
+   for FFI hosts that do not link the C++ API. The view stays valid until the handle is
+   freed. */
+typedef struct tj_host_dataset tj_host_dataset;
+int tj_host_dataset_load(const char* path, tj_host_dataset** out);
+const tj_dataset_view* tj_host_dataset_view(const tj_host_dataset* h);
+uint64_t tj_host_dataset_bytes(const tj_host_dataset* h);
+void tj_host_dataset_free(tj_host_dataset* h);
+
 /* ---- full join (backs run_join) ---- */
 int tj_join(tj_ctx* ctx, const tj_dataset* R, const tj_dataset* S, const tj_join_spec* spec,
             const tj_trace* trace, tj_join_result* out);

@@ -625,3 +625,35 @@ JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const Jo
 }
 
 } // namespace trijoin
+
+// ---------------------------------------------------------------- C-ABI host helpers
+struct tj_host_dataset {
+    std::unique_ptr<trijoin::detail::PackedDataset> packed;
+};
+
+extern "C" {
+
+int tj_host_dataset_load(const char* path, tj_host_dataset** out) {
+    if (!path || !out) return TJ_EINVAL;
+    *out = nullptr;
+    try {
+        const trijoin::PreparedDataset ds = trijoin::load_index(path);
+        trijoin::ThreadPool pool(0);
+        auto h = std::make_unique<tj_host_dataset>();
+        h->packed = trijoin::detail::pack_dataset(ds, pool);
+        *out = h.release();
+        return TJ_OK;
+    } catch (const std::invalid_argument& e) {
+        return TJ_EINVAL;
+    } catch (const std::exception& e) {
+        return TJ_ECUDA;
+    }
+}
+
+const tj_dataset_view* tj_host_dataset_view(const tj_host_dataset* h) { return h ? &h->packed->view : nullptr; }
+
+uint64_t tj_host_dataset_bytes(const tj_host_dataset* h) { return h ? h->packed->bytes() : 0; }
+
+void tj_host_dataset_free(tj_host_dataset* h) { delete h; }
+
+} // extern "C"

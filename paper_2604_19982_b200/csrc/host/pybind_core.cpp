@@ -195,6 +195,14 @@ PYBIND11_MODULE(_core, m) {
         py::arg("path"));
 
     m.def(
+        "save_dataset",
+        [](std::shared_ptr<PreparedDataset> ds, const std::string& path) {
+            py::gil_scoped_release release;
+            save_index(*ds, path);
+        },
+        py::arg("dataset"), py::arg("path"));
+
+    m.def(
         "join_datasets",
         [](std::shared_ptr<PreparedDataset> R, std::shared_ptr<PreparedDataset> S, const std::string& type, double tau,
            uint32_t k, uint64_t filter_chunk, uint64_t refine_chunk, const std::vector<uint32_t>& lods, bool pipeline,

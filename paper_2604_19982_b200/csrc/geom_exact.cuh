@@ -171,8 +171,10 @@ __device__ __forceinline__ double point_triangle_d2(const V3& p, uint32_t t) {
     if (d3 >= 0.0 && d4 <= d3) reg = 1;
     if (d1 <= 0.0 && d2 <= 0.0) reg = 0;
 
-    // One division: the region's own quotient (interior: denom = 1/(va+vb+vc)).
-    double num = 1.0, den = TJ_ADD(TJ_ADD(va, vb), vc);
+    // One division: the region's own quotient (interior: denom = 1/(va+vb+vc)); vertex
+    // regions divide nothing (0/1 keeps the unused quotient off the slow path).
+    double num = 0.0, den = 1.0;
+    if (reg == 6) { num = 1.0; den = TJ_ADD(TJ_ADD(va, vb), vc); }
     if (reg == 2) { num = d1; den = TJ_SUB(d1, d3); }
     if (reg == 4) { num = d2; den = TJ_SUB(d2, d6); }
     if (reg == 5) { num = d43; den = TJ_ADD(d43, d56); }
@@ -209,7 +211,9 @@ __device__ __forceinline__ double segment_segment_d2(const V3& p1, const V3& q1,
         const double c = vdot(d1, r);
         const double b = vdot(d1, d2);
         const double denom = TJ_SUB(TJ_MUL(a, e), TJ_MUL(b, b));
-        const double sq = sclamp01(TJ_DIV(TJ_SUB(TJ_MUL(b, f), TJ_MUL(c, e)), denom));
+        // parallel segments (denom <= 0) use s = 0 and never read the quotient: divide by
+        // 1 instead of 0 so the unused division stays on the fast path
+        const double sq = sclamp01(TJ_DIV(TJ_SUB(TJ_MUL(b, f), TJ_MUL(c, e)), denom > 0.0 ? denom : 1.0));
         const double s0 = (denom > 0.0) ? sq : 0.0;
         const double t0 = TJ_DIV(TJ_ADD(TJ_MUL(b, s0), f), e);
         const bool tneg = t0 < 0.0;

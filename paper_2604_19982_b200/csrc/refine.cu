@@ -39,8 +39,10 @@ __global__ void __launch_bounds__(kThreads, 4) refine_join_kernel(RefineJoinArgs
         const uint64_t r0 = a.r_foff[av.gvr], r1 = a.r_foff[av.gvr + 1];
         const uint64_t s0 = a.s_foff[av.gvs], s1 = a.s_foff[av.gvs + 1];
         double lb, ub;
+        // op-level cull thresholds unless exact per-voxel-pair outputs were requested
+        const OpMin om{a.vp_lb ? nullptr : a.op_lb_bits, a.vp_lb ? nullptr : a.op_ub_bits, av.op};
         refine_voxel_pair(sm, a.r_facets + r0 * 12, (uint32_t)(r1 - r0), a.s_facets + s0 * 12,
-                          (uint32_t)(s1 - s0), a.cull != 0, lb, ub, tested, evaluated);
+                          (uint32_t)(s1 - s0), a.cull != 0, om, lb, ub, tested, evaluated);
         if (lane == 0) {
             if (a.vp_lb) {
                 a.vp_lb[vp] = lb;
@@ -67,8 +69,9 @@ __global__ void __launch_bounds__(kThreads, 4) refine_batch_kernel(RefineBatchAr
         vp = __shfl_sync(0xffffffffu, vp, 0);
         if (vp >= a.n_vp) break;
         double lb, ub;
+        const OpMin om{nullptr, nullptr, 0};
         refine_voxel_pair(sm, a.facets + a.r_off[vp] * 12, a.r_len[vp], a.facets + a.s_off[vp] * 12, a.s_len[vp],
-                          a.cull != 0, lb, ub, tested, evaluated);
+                          a.cull != 0, om, lb, ub, tested, evaluated);
         if (lane == 0) {
             a.vp_lb[vp] = lb;
             a.vp_ub[vp] = ub;

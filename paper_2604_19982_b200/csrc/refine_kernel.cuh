@@ -44,6 +44,7 @@ constexpr int kQueue = 64;
 struct WarpSmem {
     double rf[kRT * kFS];
     double sf[kST * kFS];
+    float rc[kRT * kCS];
     float sc[kST * kCS];
     uint32_t queue[kQueue];
 };
@@ -94,7 +95,9 @@ __device__ __forceinline__ void stage_facet(const double* __restrict__ g, double
         M = fmaxf(M, fmaxf(fabsf(cr[d]), fabsf(cr[3 + d])));
     }
     const float dx = __fsub_ru(cr[3], cr[0]), dy = __fsub_ru(cr[4], cr[1]), dz = __fsub_ru(cr[5], cr[2]);
-    cr[6] = __fsqrt_ru(__fadd_ru(__fadd_ru(__fmul_ru(dx, dx), __fmul_ru(dy, dy)), __fmul_ru(dz, dz)));
+    // facet AABB diagonal, rounded up (hardware sqrt is within 2 ulp; 1 + 2^-20 covers it)
+    cr[6] = __fmul_ru(sqrtf(__fadd_ru(__fadd_ru(__fmul_ru(dx, dx), __fmul_ru(dy, dy)), __fmul_ru(dz, dz))),
+                      1.0f + 0x1p-20f);
     cr[7] = M;
     cr[8] = rd(c[9]);
     cr[9] = ru(c[10]);
@@ -121,7 +124,8 @@ __device__ __forceinline__ float box_gap_lb(const float* a, const float* b) {
         const float g = fmaxf(0.f, fmaxf(__fsub_rd(b[d], a[3 + d]), __fsub_rd(a[d], b[3 + d])));
         s = __fadd_rd(s, __fmul_rd(g, g));
     }
-    return __fsqrt_rd(s);
+    // lower bound of sqrt(s): hardware sqrt (<= 2 ulp error) scaled down by 1 - 2^-20
+    return __fmul_rd(sqrtf(s), 1.0f - 0x1p-20f);
 }
 
 __device__ __forceinline__ float absdot3(const float* u, const float* v) {
@@ -135,7 +139,10 @@ __device__ __forceinline__ bool cullable(const float* a, const float* b, float m
         __fadd_ru(__fmul_ru(1e-5f, __fadd_ru(__fadd_ru(B, a[6]), b[6])), __fmul_ru(1e-12f, __fadd_ru(a[7], b[7])));
     const float lbs = __fsub_rd(__fsub_rd(B, a[9]), b[9]);
     const float ubs = __fadd_rd(__fadd_rd(B, a[8]), b[8]);
-    if (!(lbs >= __fadd_ru(mlb_u, delta) && ubs >= __fadd_ru(mub_u, delta))) return false;
+    // A running minimum of exactly 0 is the floor (lb_ij, ub_ij >= 0): that side needs no test.
+    const bool lb_ok = mlb_u == 0.f || lbs >= __fadd_ru(mlb_u, delta);
+    const bool ub_ok = mub_u == 0.f || ubs >= __fadd_ru(mub_u, delta);
+    if (!(lb_ok && ub_ok)) return false;
     if (a[10] == 0.f || b[10] == 0.f) return false;
     if (B > 1e3f * fminf(a[6], b[6])) return false;
     const float kC = 1e-3f;
@@ -171,67 +178,116 @@ __device__ __forceinline__ void fold(double2 v, double& mlb, double& mub) {
     mub = smin(mub, v.y);
 }
 
+// Op-level running minima shared by all warps refining voxel pairs of the same candidate
+// (join mode). A pair that cannot lower the *op* minimum cannot change the aggregated
+// object bounds (aggregate_object_bounds folds the minimum over the op's voxel pairs), so
+// culling against min(vp-local, op-global) is exact for the join. Per-voxel-pair outputs
+// (refine_kernel / tj_refine_batch) use op == nullptr: vp-local minima only.
+struct OpMin {
+    unsigned long long* lb_bits; // nullptr = no op-level sharing
+    unsigned long long* ub_bits;
+    uint32_t op;
+};
+
+__device__ __forceinline__ double load_min(const unsigned long long* p) {
+    return __longlong_as_double((long long)__ldcg(reinterpret_cast<const unsigned long long*>(p)));
+}
+
 // One voxel pair: facets [r_base, r_base + r_len) x [s_base, s_base + s_len), each
-// record TJ_FACET_STRIDE (12) doubles. Returns the exact minima (warp-uniform).
+// record TJ_FACET_STRIDE (12) doubles. Returns the exact vp-local minima (warp-uniform).
+// Tile pairs (32 r x 32 s facets) are flattened so lane l tests pairs t = l, l + 32, ...
+// of the tile (i = t / scnt, j = t % scnt): small voxels keep all lanes busy.
 __device__ __forceinline__ void refine_voxel_pair(WarpSmem& sm, const double* __restrict__ r_base, uint32_t r_len,
                                                   const double* __restrict__ s_base, uint32_t s_len, bool cull,
-                                                  double& out_lb, double& out_ub, unsigned long long& tested,
-                                                  unsigned long long& evaluated) {
+                                                  const OpMin& om, double& out_lb, double& out_ub,
+                                                  unsigned long long& tested, unsigned long long& evaluated) {
     const int lane = threadIdx.x & 31;
     const double kInf = __longlong_as_double(0x7ff0000000000000ll);
-    double mlb = kInf, mub = kInf; // warp-uniform after every reduction
+    double mlb = kInf, mub = kInf; // vp-local minima, warp-uniform after every reduction
     const uint32_t rbase = smem_addr(sm.rf), sbase = smem_addr(sm.sf);
     constexpr uint32_t kRec = kFS * 8;
+    // culling thresholds: min(vp-local, op-global)
+    double tlb = kInf, tub = kInf;
+    auto refresh = [&]() {
+        tlb = mlb;
+        tub = mub;
+        if (om.lb_bits) {
+            // one lane reads, all lanes use the same value: every branch on tlb/tub must
+            // stay warp-uniform (the warp-synchronous queue relies on it)
+            double glb = 0.0, gub = 0.0;
+            if (lane == 0) {
+                glb = load_min(om.lb_bits + om.op);
+                gub = load_min(om.ub_bits + om.op);
+            }
+            glb = __shfl_sync(0xffffffffu, glb, 0);
+            gub = __shfl_sync(0xffffffffu, gub, 0);
+            tlb = smin(tlb, glb);
+            tub = smin(tub, gub);
+        }
+    };
+    auto publish = [&]() {
+        if (om.lb_bits && lane == 0 && mlb < kInf) {
+            atomicMin(om.lb_bits + om.op, (unsigned long long)__double_as_longlong(mlb));
+            atomicMin(om.ub_bits + om.op, (unsigned long long)__double_as_longlong(mub));
+        }
+    };
+    refresh();
+    if (cull && tlb == 0.0 && tub == 0.0) { // op already at the floor: nothing can lower it
+        out_lb = mlb;
+        out_ub = mub;
+        return;
+    }
     bool done = false;
     for (uint32_t r0 = 0; r0 < r_len && !done; r0 += kRT) {
         const int rcnt = (int)min((uint32_t)kRT, r_len - r0);
-        float myc[kCS];
         __syncwarp();
-        if (lane < rcnt) stage_facet(r_base + (size_t)(r0 + lane) * 12, sm.rf + lane * kFS, myc);
-        const bool have_i = lane < rcnt;
+        if (lane < rcnt) stage_facet(r_base + (size_t)(r0 + lane) * 12, sm.rf + lane * kFS, sm.rc + lane * kCS);
         for (uint32_t s0 = 0; s0 < s_len && !done; s0 += kST) {
             const int scnt = (int)min((uint32_t)kST, s_len - s0);
             __syncwarp();
             for (int l = lane; l < scnt; l += 32)
                 stage_facet(s_base + (size_t)(s0 + l) * 12, sm.sf + l * kFS, sm.sc + l * kCS);
             __syncwarp();
+            const int npairs = rcnt * scnt;
 
             double llb = mlb, lub = mub; // lane-local minima
-            int seed_j = -1;
-            if (cull && mlb == kInf) {
-                // Seed: each lane evaluates its facet against the s facet of smallest box gap.
+            int seed_t = -1;
+            if (cull && tlb == kInf) {
+                // Seed: each lane evaluates its pair of smallest box gap.
                 float bestB = __int_as_float(0x7f800000);
-                if (have_i) {
-                    for (int j = 0; j < scnt; ++j) {
-                        const float B = box_gap_lb(myc, sm.sc + j * kCS);
-                        if (B < bestB) { bestB = B; seed_j = j; }
-                    }
+                for (int t = lane; t < npairs; t += 32) {
+                    const int i = t / scnt, j = t - i * scnt;
+                    const float B = box_gap_lb(sm.rc + i * kCS, sm.sc + j * kCS);
+                    if (B < bestB) { bestB = B; seed_t = t; }
                 }
-                if (seed_j >= 0) {
-                    fold(eval_pair(rbase + lane * kRec, sbase + seed_j * kRec), llb, lub);
+                if (seed_t >= 0) {
+                    const int i = seed_t / scnt, j = seed_t - i * scnt;
+                    fold(eval_pair(rbase + i * kRec, sbase + j * kRec), llb, lub);
                     ++evaluated;
                 }
                 mlb = warp_min(llb);
                 mub = warp_min(lub);
+                publish();
+                refresh();
             }
             int qn = 0;
-            float mlb_u = ru(mlb), mub_u = ru(mub);
-            for (int j = 0; j < scnt; ++j) {
+            float tlb_u = ru(tlb), tub_u = ru(tub);
+            for (int t0 = 0; t0 < npairs; t0 += 32) {
+                const int t = t0 + lane;
                 bool need = false;
-                if (have_i && j != seed_j) {
-                    need = !cull || !cullable(myc, sm.sc + j * kCS, mlb_u, mub_u);
+                if (t < npairs && t != seed_t) {
+                    const int i = t / scnt, j = t - i * scnt;
+                    need = !cull || !cullable(sm.rc + i * kCS, sm.sc + j * kCS, tlb_u, tub_u);
                     ++tested;
                 }
                 const unsigned bal = __ballot_sync(0xffffffffu, need);
-                if (need) {
-                    const int pos = qn + __popc(bal & ((1u << lane) - 1u));
-                    sm.queue[pos] = (uint32_t)lane | ((uint32_t)j << 8);
-                }
+                if (need) sm.queue[qn + __popc(bal & ((1u << lane) - 1u))] = (uint32_t)t;
                 qn += __popc(bal);
                 if (qn >= 32) {
                     __syncwarp();
-                    const uint32_t e = sm.queue[lane];
-                    fold(eval_pair(rbase + (e & 0xffu) * kRec, sbase + (e >> 8) * kRec), llb, lub);
+                    const int e = (int)sm.queue[lane];
+                    const int i = e / scnt, j = e - i * scnt;
+                    fold(eval_pair(rbase + i * kRec, sbase + j * kRec), llb, lub);
                     ++evaluated;
                     __syncwarp();
                     if (lane < qn - 32) sm.queue[lane] = sm.queue[32 + lane];
@@ -239,21 +295,26 @@ __device__ __forceinline__ void refine_voxel_pair(WarpSmem& sm, const double* __
                     qn -= 32;
                     mlb = warp_min(llb);
                     mub = warp_min(lub);
-                    mlb_u = ru(mlb);
-                    mub_u = ru(mub);
-                    if (mlb == 0.0 && mub == 0.0) { done = true; break; }
+                    publish();
+                    refresh();
+                    tlb_u = ru(tlb);
+                    tub_u = ru(tub);
+                    if (cull && tlb == 0.0 && tub == 0.0) { done = true; break; }
                 }
             }
             if (!done && qn > 0) {
                 __syncwarp();
                 if (lane < qn) {
-                    const uint32_t e = sm.queue[lane];
-                    fold(eval_pair(rbase + (e & 0xffu) * kRec, sbase + (e >> 8) * kRec), llb, lub);
+                    const int e = (int)sm.queue[lane];
+                    const int i = e / scnt, j = e - i * scnt;
+                    fold(eval_pair(rbase + i * kRec, sbase + j * kRec), llb, lub);
                     ++evaluated;
                 }
                 mlb = warp_min(llb);
                 mub = warp_min(lub);
-                if (mlb == 0.0 && mub == 0.0) done = true;
+                publish();
+                refresh();
+                if (cull && tlb == 0.0 && tub == 0.0) done = true;
             }
         }
     }

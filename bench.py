@@ -214,12 +214,15 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record()
-    outs = [res.run(**run_kw) for _ in range(a.steps)]
-    e1.record()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps + 1)]
+    evs[0].record()
+    outs = []
+    for i in range(a.steps):
+        outs.append(res.run(**run_kw))
+        evs[i + 1].record()
     torch.cuda.synchronize(dev)
+    e0, e1 = evs[0], evs[-1]
+    step_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(a.steps)]
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
@@ -306,7 +309,9 @@ def main():
                            "candidate_pairs": pairs, "facet_pairs_ref_count": fp,
                            "join_wall_ms": ms_per_step, "l2": "inputs larger than L2 "
                            f"({res.device_bytes / 1e9:.1f} GB resident)", "parallelism": f"r-shard x{world}",
-                           "setup_s": round(setup_s, 1), "cull": not a.no_cull},
+                           "setup_s": round(setup_s, 1), "cull": not a.no_cull,
+                           "step_ms": [round(x, 2) for x in step_ms],
+                           "levels_last_step": outs[-1]["levels"]},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
                 "gpu_launches": int(launches)}
         print(json.dumps(line), flush=True)

@@ -134,6 +134,7 @@ typedef struct tj_join_result {
     double level_kernel_ms[TJ_MAX_LODS];         /* refine kernel only (CUDA events) */
     uint64_t refine_chunks;
     double mbb_ms, voxel_ms, refine_ms, total_ms;
+    uint64_t level_pairs_screened[TJ_MAX_LODS];  /* FP32 separating-axis tests run */
 } tj_join_result;
 
 /* ---- context ---- */

@@ -38,10 +38,18 @@ void set_global_error(const std::string& m) {
     g_err = m;
 }
 
+// Restores the thread's allocation stream on scope exit.
+struct AllocStreamScope {
+    cudaStream_t saved;
+    explicit AllocStreamScope(cudaStream_t s) : saved(alloc_stream()) { alloc_stream() = s; }
+    ~AllocStreamScope() { alloc_stream() = saved; }
+};
+
 template <class F>
 int guarded(tj_ctx* ctx, F&& f) {
     try {
         if (ctx) TJ_CUDA(cudaSetDevice(ctx->device));
+        AllocStreamScope scope(ctx ? ctx->stream : nullptr);
         f();
         return TJ_OK;
     } catch (const Error& e) {
@@ -160,6 +168,11 @@ int tj_ctx_create(int device, tj_ctx** out) {
             throw Error(TJ_ECUDA, std::string("tj_ctx_create: built for sm_100a (B200), found ") + prop.name);
         ctx->ws.num_sms = prop.multiProcessorCount;
         TJ_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        // keep freed pool memory cached for reuse by later joins (stream-ordered allocation)
+        cudaMemPool_t pool;
+        TJ_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t threshold = UINT64_MAX;
+        TJ_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
     });
     if (rc == TJ_OK) *out = ctx.release();
     return rc;
@@ -168,9 +181,14 @@ int tj_ctx_create(int device, tj_ctx** out) {
 void tj_ctx_destroy(tj_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
-    ctx->ws.temp.release();
-    ctx->ws.u64a.release();
-    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    {
+        AllocStreamScope scope(ctx->stream);
+        ctx->ws.release();
+    }
+    if (ctx->stream) {
+        cudaStreamSynchronize(ctx->stream);
+        cudaStreamDestroy(ctx->stream);
+    }
     delete ctx;
 }
 
@@ -220,6 +238,7 @@ int tj_dataset_upload(tj_ctx* ctx, const tj_dataset_view* v, tj_dataset** out) {
 void tj_dataset_free(tj_dataset* ds) {
     if (!ds) return;
     cudaSetDevice(ds->ctx->device);
+    AllocStreamScope scope(ds->ctx->stream);
     delete ds;
 }
 
@@ -363,6 +382,7 @@ int tj_join(tj_ctx* ctx, const tj_dataset* Rh, const tj_dataset* Sh, const tj_jo
             out->level_facet_pairs[i] = ro.levels[i].facet_pairs;
             out->level_pairs_evaluated[i] = ro.levels[i].evaluated;
             out->level_pairs_tested[i] = ro.levels[i].tested;
+            out->level_pairs_screened[i] = ro.levels[i].screened;
             out->level_ms[i] = ro.levels[i].ms;
             out->level_kernel_ms[i] = ro.levels[i].kernel_ms;
         }
@@ -408,15 +428,25 @@ int tj_refine_batch(tj_ctx* ctx, uint64_t n_tris, const double* tris, const doub
         upload(so, s_off, n_descs, st);
         upload(rl, r_len, n_descs, st);
         upload(sl, s_len, n_descs, st);
-        DevBuf<double> lb(n_descs), ub(n_descs);
-        DevBuf<unsigned long long> work(1), counters(2);
-        TJ_CUDA(cudaMemsetAsync(work.p, 0, 8, st));
-        TJ_CUDA(cudaMemsetAsync(counters.p, 0, 16, st));
-        RefineBatchArgs a{f.p, ro.p, so.p, rl.p, sl.p, n_descs, lb.p, ub.p, work.p, counters.p,
-                          (flags & TJ_FLAG_NO_CULL) ? 0 : 1};
-        launch_refine_batch(a, ctx->ws.num_sms, st);
-        TJ_CUDA(cudaMemcpyAsync(vp_lb, lb.p, n_descs * 8, cudaMemcpyDeviceToHost, st));
-        TJ_CUDA(cudaMemcpyAsync(vp_ub, ub.p, n_descs * 8, cudaMemcpyDeviceToHost, st));
+        // every descriptor is its own op: per-voxel-pair minima, exact (refine_kernel.cuh)
+        DevBuf<unsigned long long> lbb(n_descs), ubb(n_descs), work(1), counters(4);
+        std::vector<unsigned long long> inf(n_descs, 0x7ff0000000000000ull);
+        TJ_CUDA(cudaMemcpyAsync(lbb.p, inf.data(), n_descs * 8, cudaMemcpyHostToDevice, st));
+        TJ_CUDA(cudaMemcpyAsync(ubb.p, inf.data(), n_descs * 8, cudaMemcpyHostToDevice, st));
+        TJ_CUDA(cudaMemsetAsync(counters.p, 0, 32, st));
+        RefineSource src{};
+        src.r_off = ro.p;
+        src.s_off = so.p;
+        src.r_len = rl.p;
+        src.s_len = sl.p;
+        src.r_facets = f.p;
+        src.s_facets = f.p;
+        const int cull = (flags & TJ_FLAG_NO_CULL) ? 0 : 1;
+        RefineQueueStore queue;
+        if (cull) refine_pass(src, 0, n_descs, true, lbb.p, ubb.p, cull, queue, work.p, counters.p, ctx->ws.num_sms, st);
+        refine_pass(src, 0, n_descs, false, lbb.p, ubb.p, cull, queue, work.p, counters.p, ctx->ws.num_sms, st);
+        TJ_CUDA(cudaMemcpyAsync(vp_lb, lbb.p, n_descs * 8, cudaMemcpyDeviceToHost, st));
+        TJ_CUDA(cudaMemcpyAsync(vp_ub, ubb.p, n_descs * 8, cudaMemcpyDeviceToHost, st));
         TJ_CUDA(cudaStreamSynchronize(st));
     });
 }

@@ -1,6 +1,7 @@
 // Shared declarations of the device join pipeline (filter, knn, refine-loop stages).
 #pragma once
 #include <cstdint>
+#include <memory>
 #include <vector>
 
 #include "tj_internal.cuh"
@@ -56,6 +57,12 @@ struct Workspace {
     int num_sms = 148;
     DevBuf<unsigned char> temp;
     DevBuf<uint64_t> u64a;
+    std::unique_ptr<RefineQueueStore> queue; // refinement pair queues, grow-only, per context
+    void release() {
+        temp.release();
+        u64a.release();
+        queue.reset();
+    }
 };
 
 struct SortedS {
@@ -118,7 +125,7 @@ void knn_finalize_dev(Workspace& ws, CandDevStore& cs, uint32_t k, cudaStream_t 
 // refine_loop.cu
 struct LevelStats {
     uint32_t level;
-    uint64_t vps, facet_pairs, evaluated, tested;
+    uint64_t vps, facet_pairs, evaluated, tested, screened;
     double ms, kernel_ms;
 };
 struct RefineLoopOut {

@@ -14,6 +14,7 @@
 #include <stdexcept>
 #include <thread>
 
+#include <cuda_runtime.h>
 #include <json.hpp>
 
 #include "packed.hpp"
@@ -67,6 +68,76 @@ std::vector<int> join_devices() {
     }
     if (out.empty()) out.push_back(0);
     return out;
+}
+
+namespace {
+// Process-wide pinned arena: freed blocks are kept for reuse (pinning is slow; reuse is free).
+struct PinnedArena {
+    std::mutex mu;
+    std::multimap<size_t, double*> free_blocks; // capacity (doubles) -> block
+    double* acquire(size_t want, size_t& cap, bool& pinned) {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            auto it = free_blocks.lower_bound(want);
+            if (it != free_blocks.end() && it->first <= 2 * want + (1u << 20)) {
+                cap = it->first;
+                double* p = it->second;
+                free_blocks.erase(it);
+                pinned = true;
+                return p;
+            }
+        }
+        void* p = nullptr;
+        cap = want;
+        if (cudaHostAlloc(&p, want * sizeof(double), cudaHostAllocPortable) == cudaSuccess) {
+            pinned = true;
+            return static_cast<double*>(p);
+        }
+        cudaGetLastError(); // no device / pinning refused: fall back to pageable host memory
+        pinned = false;
+        p = std::malloc(want * sizeof(double));
+        if (!p) throw std::bad_alloc();
+        return static_cast<double*>(p);
+    }
+    void release(double* p, size_t cap, bool pinned) {
+        if (!p) return;
+        if (!pinned) {
+            std::free(p);
+            return;
+        }
+        std::lock_guard<std::mutex> lk(mu);
+        free_blocks.emplace(cap, p);
+    }
+};
+PinnedArena& arena() {
+    static PinnedArena* a = new PinnedArena(); // intentionally leaked: outlives the CUDA runtime
+    return *a;
+}
+} // namespace
+
+PinnedBuf& PinnedBuf::operator=(PinnedBuf&& o) noexcept {
+    if (this != &o) {
+        arena().release(p, cap, pinned);
+        p = o.p;
+        n = o.n;
+        cap = o.cap;
+        pinned = o.pinned;
+        o.p = nullptr;
+        o.n = o.cap = 0;
+    }
+    return *this;
+}
+
+PinnedBuf::~PinnedBuf() { arena().release(p, cap, pinned); }
+
+void PinnedBuf::resize(size_t count) {
+    if (count > cap) {
+        arena().release(p, cap, pinned);
+        p = nullptr;
+        cap = 0;
+        if (count) p = arena().acquire(count, cap, pinned);
+    }
+    n = count;
 }
 
 uint64_t PackedDataset::bytes() const {
@@ -285,6 +356,7 @@ std::string StageStats::to_json() const {
                        {"vp_pruned", s.vp_pruned},
                        {"facet_pairs", s.facet_pairs}});
     j["stages"] = std::move(arr);
+    j["b200"] = {{"pack_ms", pack_ms}, {"upload_ms", upload_ms}, {"device_ms", device_ms}, {"devices", devices}};
     return j.dump(2);
 }
 
@@ -476,6 +548,7 @@ JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const Jo
 
     const std::vector<int> devices = detail::join_devices();
     const bool self_join = &R == &S;
+    auto tp = Clock::now();
     auto pr = detail::pack_dataset(R, pool);
     std::unique_ptr<detail::PackedDataset> ps_own;
     const detail::PackedDataset* ps = pr.get();
@@ -483,12 +556,16 @@ JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const Jo
         ps_own = detail::pack_dataset(S, pool);
         ps = ps_own.get();
     }
+    out.stats.pack_ms = std::chrono::duration<double, std::milli>(Clock::now() - tp).count();
     const size_t G = (trace && (trace->on_interval || trace->on_vp_pruned)) ? 1 : devices.size();
+    out.stats.devices = static_cast<uint32_t>(G);
     std::vector<detail::ResultHandle> results(G);
     std::vector<std::exception_ptr> errors(G);
+    std::vector<double> up_ms(G, 0.0), dev_ms(G, 0.0);
     auto run_shard = [&](size_t g) {
         try {
             tj_ctx* ctx = detail::device_context(devices[g]);
+            const auto tu = Clock::now();
             detail::DatasetHandle dr, ds_h;
             detail::check(tj_dataset_upload(ctx, &pr->view, &dr.p), ctx);
             const tj_dataset* dsp = dr.p;
@@ -496,6 +573,8 @@ JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const Jo
                 detail::check(tj_dataset_upload(ctx, &ps->view, &ds_h.p), ctx);
                 dsp = ds_h.p;
             }
+            const auto td = Clock::now();
+            up_ms[g] = std::chrono::duration<double, std::milli>(td - tu).count();
             tj_join_spec cs = to_c_spec(spec);
             cs.shard_index = static_cast<uint32_t>(g);
             cs.shard_count = static_cast<uint32_t>(G);
@@ -503,6 +582,7 @@ JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const Jo
             TraceBridge bridge{trace};
             tj_trace tt{&bridge, &TraceBridge::interval, &TraceBridge::pruned};
             detail::check(tj_join(ctx, dr.p, dsp, &cs, trace ? &tt : nullptr, &results[g].r), ctx);
+            dev_ms[g] = std::chrono::duration<double, std::milli>(Clock::now() - td).count();
         } catch (...) {
             errors[g] = std::current_exception();
         }
@@ -516,6 +596,8 @@ JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const Jo
     }
     for (auto& e : errors)
         if (e) std::rethrow_exception(e);
+    out.stats.upload_ms = *std::max_element(up_ms.begin(), up_ms.end());
+    out.stats.device_ms = *std::max_element(dev_ms.begin(), dev_ms.end());
 
     // Merge shards: query r is owned by shard (r / 1024) % G; each shard's arrays cover
     // all queries with empty ranges for foreign ones.

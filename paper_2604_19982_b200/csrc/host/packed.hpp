@@ -10,6 +10,25 @@
 
 namespace trijoin::detail {
 
+// Page-locked host buffer from a process-wide arena (cudaHostAlloc'ed once, reused), so
+// that uploads of packed facet records run at full DMA speed.
+struct PinnedBuf {
+    double* p = nullptr;
+    size_t n = 0;     // doubles in use
+    size_t cap = 0;   // doubles allocated
+    bool pinned = false;
+    PinnedBuf() = default;
+    PinnedBuf(const PinnedBuf&) = delete;
+    PinnedBuf& operator=(const PinnedBuf&) = delete;
+    PinnedBuf(PinnedBuf&& o) noexcept { *this = std::move(o); }
+    PinnedBuf& operator=(PinnedBuf&& o) noexcept;
+    ~PinnedBuf();
+    void resize(size_t count); // contents not preserved
+    double* data() { return p; }
+    const double* data() const { return p; }
+    size_t size() const { return n; }
+};
+
 // Owning SoA image of one PreparedDataset in the device layout (include/tj_capi.h).
 struct PackedDataset {
     uint32_t n_objects = 0;
@@ -17,7 +36,7 @@ struct PackedDataset {
     std::vector<double> mbb, anchor, voxel_box, voxel_anchor;
     std::vector<uint64_t> voxel_offsets;
     std::vector<std::vector<uint64_t>> facet_offsets; // per level
-    std::vector<std::vector<double>> facets;          // per level, TJ_FACET_STRIDE doubles each
+    std::vector<PinnedBuf> facets;                    // per level, TJ_FACET_STRIDE doubles each
     std::vector<const uint64_t*> fo_ptrs;
     std::vector<const double*> f_ptrs;
     tj_dataset_view view{};

@@ -131,6 +131,7 @@ public:
             l["facet_pairs"] = r.level_facet_pairs[i];
             l["evaluated"] = r.level_pairs_evaluated[i];
             l["tested"] = r.level_pairs_tested[i];
+            l["screened"] = r.level_pairs_screened[i];
             l["ms"] = r.level_ms[i];
             l["kernel_ms"] = r.level_kernel_ms[i];
             levels.append(l);

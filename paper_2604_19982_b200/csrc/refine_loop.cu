@@ -132,7 +132,9 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
     RefineLoopOut out;
     const uint64_t n = cs.n;
     DevBuf<unsigned long long> lbb(std::max<uint64_t>(n, 1)), ubb(std::max<uint64_t>(n, 1));
-    DevBuf<unsigned long long> counters(3), work(1);
+    DevBuf<unsigned long long> counters(4), work(1);
+    if (!ws.queue) ws.queue = std::make_unique<RefineQueueStore>();
+    RefineQueueStore& queue = *ws.queue;
     DevBuf<uint8_t> updated;
     if (trace && trace->on_interval) updated.alloc(std::max<uint64_t>(n, 1));
     cudaEvent_t e0, e1;
@@ -153,27 +155,28 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
             k_fill_u64<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(lbb.p, n, kInfBits);
             count_launch();
             k_fill_u64<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(ubb.p, n, kInfBits);
-            TJ_CUDA(cudaMemsetAsync(counters.p, 0, 24, st));
+            TJ_CUDA(cudaMemsetAsync(counters.p, 0, 32, st));
             count_launch();
             k_facet_pairs<<<grid_for(n_active, 256, ws.num_sms), 256, 0, st>>>(
                 active.p, n_active, R.facet_offsets[sr].p, S.facet_offsets[ss].p, counters.p + 2);
             TJ_CUDA(cudaEventRecord(e0, st));
-            for (uint64_t c0 = 0; c0 < n_active; c0 += launch) {
-                RefineJoinArgs a{};
-                a.active = active.p + c0;
-                a.n_vp = std::min(launch, n_active - c0);
-                a.r_foff = R.facet_offsets[sr].p;
-                a.r_facets = R.facets[sr].p;
-                a.s_foff = S.facet_offsets[ss].p;
-                a.s_facets = S.facets[ss].p;
-                a.op_lb_bits = lbb.p;
-                a.op_ub_bits = ubb.p;
-                a.work = work.p;
-                a.counters = counters.p;
-                a.cull = (spec.flags & TJ_FLAG_NO_CULL) ? 0 : 1;
-                TJ_CUDA(cudaMemsetAsync(work.p, 0, 8, st));
-                launch_refine_join(a, ws.num_sms, st);
-            }
+            RefineSource src{};
+            src.active = active.p;
+            src.r_foff = R.facet_offsets[sr].p;
+            src.s_foff = S.facet_offsets[ss].p;
+            src.cand_lb = cs.lb.p;
+            src.cand_ub = cs.ub.p;
+            src.r_facets = R.facets[sr].p;
+            src.s_facets = S.facets[ss].p;
+            const int cull = (spec.flags & TJ_FLAG_NO_CULL) ? 0 : 1;
+            // seeds for every voxel pair first (op thresholds), then the screened passes
+            if (cull)
+                for (uint64_t c0 = 0; c0 < n_active; c0 += launch)
+                    refine_pass(src, c0, std::min(n_active, c0 + launch), true, lbb.p, ubb.p, cull, queue, work.p,
+                                counters.p, ws.num_sms, st);
+            for (uint64_t c0 = 0; c0 < n_active; c0 += launch)
+                refine_pass(src, c0, std::min(n_active, c0 + launch), false, lbb.p, ubb.p, cull, queue, work.p,
+                            counters.p, ws.num_sms, st);
             TJ_CUDA(cudaEventRecord(e1, st));
             out.chunks += (n_active + spec.refine_chunk - 1) / spec.refine_chunk;
             count_launch();
@@ -186,14 +189,15 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
                 knn_fixpoint(ws, cs, spec.k, (int16_t)level, err, st);
                 check_error(err, st);
             }
-            unsigned long long hc[3];
-            TJ_CUDA(cudaMemcpyAsync(hc, counters.p, 24, cudaMemcpyDeviceToHost, st));
+            unsigned long long hc[4];
+            TJ_CUDA(cudaMemcpyAsync(hc, counters.p, 32, cudaMemcpyDeviceToHost, st));
             TJ_CUDA(cudaStreamSynchronize(st));
             float kms = 0.f;
             TJ_CUDA(cudaEventElapsedTime(&kms, e0, e1));
             ls.tested = hc[0];
             ls.evaluated = hc[1];
             ls.facet_pairs = hc[2];
+            ls.screened = hc[3];
             ls.kernel_ms = kms;
             n_active = compact_active(ws, cs, active, n_active, st);
             ls.ms = std::chrono::duration<double, std::milli>(Clock::now() - t0).count();

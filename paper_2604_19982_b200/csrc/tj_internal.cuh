@@ -29,6 +29,15 @@ struct Error : std::runtime_error {
                                std::string(#call) + ": " + cudaGetErrorString(e_));           \
     } while (0)
 
+// Stream used for stream-ordered allocation by DevBuf on this thread (set at every C-ABI
+// entry to the context's stream; nullptr = legacy stream). Allocations come from the
+// device's default memory pool, which the context configures never to release memory, so
+// per-join temporaries cost no cudaMalloc/cudaFree (and no implicit device syncs).
+inline cudaStream_t& alloc_stream() {
+    static thread_local cudaStream_t s = nullptr;
+    return s;
+}
+
 // Minimal owning device buffer.
 template <class T>
 struct DevBuf {
@@ -47,12 +56,12 @@ struct DevBuf {
     void alloc(size_t count) {
         release();
         n = count;
-        if (count) TJ_CUDA(cudaMalloc(&p, count * sizeof(T)));
+        if (count) TJ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), alloc_stream()));
     }
     // grow-only reallocation (contents not preserved)
     void reserve(size_t count) { if (count > n) alloc(count); }
     void release() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, alloc_stream());
         p = nullptr;
         n = 0;
     }
@@ -78,40 +87,58 @@ struct ActiveVpDev {
     uint32_t op, gvr, gvs;
 };
 
-// Arguments of a refinement launch in join mode.
-struct RefineJoinArgs {
-    const ActiveVpDev* active;
-    uint64_t n_vp;
-    const uint64_t* r_foff; // R facet offsets of this level, by global voxel
-    const double* r_facets;
+// Where the voxel pairs of a refinement pass come from: join mode (active list + per-level
+// CSR of both datasets) or batch mode (explicit facet segments; every pair its own op).
+struct RefineSource {
+    // join mode
+    const ActiveVpDev* active; // nullptr = batch mode
+    const uint64_t* r_foff;    // facet offsets of this level, by global voxel
     const uint64_t* s_foff;
-    const double* s_facets;
-    unsigned long long* op_lb_bits; // atomicMin targets (non-negative doubles as u64)
-    unsigned long long* op_ub_bits;
-    double* vp_lb; // optional per-vp outputs (nullptr = off)
-    double* vp_ub;
-    unsigned long long* work; // dynamic work counter
-    unsigned long long* counters; // [2]: tested, evaluated
-    int cull;
-};
-
-struct RefineBatchArgs {
-    const double* facets; // [n_tris*12]
+    const double* cand_lb;     // candidate intervals before this level
+    const double* cand_ub;
+    // batch mode
     const uint64_t* r_off;
     const uint64_t* s_off;
     const uint32_t* r_len;
     const uint32_t* s_len;
-    uint64_t n_vp;
-    double* vp_lb;
-    double* vp_ub;
-    unsigned long long* work;
-    unsigned long long* counters;
-    int cull;
+    // both: facet records (TJ_FACET_STRIDE doubles each)
+    const double* r_facets;
+    const double* s_facets;
 };
 
+// A queued facet pair: op and the two global facet record indices.
+struct PairRef {
+    uint32_t op, fr, fs;
+    uint32_t mask; // verify queue: ill-conditioned combinations to check
+};
+
+struct RefineQueue {
+    PairRef* items;
+    unsigned long long capacity;
+    unsigned long long* count;
+};
+
+struct RefineQueueStore {
+    DevBuf<PairRef> items, vitems;      // exact queue, verify queue
+    DevBuf<unsigned long long> count;   // [0] exact, [1] verify
+    RefineQueueStore() : count(2) {
+        items.alloc(1u << 22);
+        vitems.alloc(1u << 22);
+    }
+    RefineQueue view() { return {items.p, (unsigned long long)items.n, count.p}; }
+    RefineQueue verify_view() { return {vitems.p, (unsigned long long)vitems.n, count.p + 1}; }
+};
+
+// One refinement pass over voxel pairs [vp_begin, vp_end) (refine.cu): the seed pass queues
+// each voxel pair's 2 smallest-box-gap facet pairs, the screen pass every facet pair that
+// may still change the op's bounds; then the queued pairs are evaluated exactly and folded
+// into lb_bits / ub_bits (atomicMin on IEEE bits). counters: [0] box tests, [1] exact
+// evaluations, [3] separating-axis tests ([2] is the refine loop's facet-pair count).
+void refine_pass(const RefineSource& src, uint64_t vp_begin, uint64_t vp_end, bool seed, unsigned long long* lb_bits,
+                 unsigned long long* ub_bits, int cull, RefineQueueStore& qs, unsigned long long* work,
+                 unsigned long long* counters, int num_sms, cudaStream_t st);
+
 // kernels (refine.cu)
-void launch_refine_join(const RefineJoinArgs& a, int num_sms, cudaStream_t st);
-void launch_refine_batch(const RefineBatchArgs& a, int num_sms, cudaStream_t st);
 void launch_tri_tri_batch(uint64_t n, const double* a9, const double* b9, double* out, cudaStream_t st);
 void launch_mindist_batch(uint64_t n, const double* a6, const double* b6, double* out, cudaStream_t st);
 

@@ -60,7 +60,8 @@ class JoinResult(ctypes.Structure):
                 ("level_pairs_evaluated", ctypes.c_uint64 * MAXL), ("level_pairs_tested", ctypes.c_uint64 * MAXL),
                 ("level_ms", ctypes.c_double * MAXL), ("level_kernel_ms", ctypes.c_double * MAXL),
                 ("refine_chunks", ctypes.c_uint64), ("mbb_ms", ctypes.c_double), ("voxel_ms", ctypes.c_double),
-                ("refine_ms", ctypes.c_double), ("total_ms", ctypes.c_double)]
+                ("refine_ms", ctypes.c_double), ("total_ms", ctypes.c_double),
+                ("level_pairs_screened", ctypes.c_uint64 * MAXL)]
 
 
 def capi_functions():

@@ -441,6 +441,10 @@ int tj_refine_batch(tj_ctx* ctx, uint64_t n_tris, const double* tris, const doub
         src.s_len = sl.p;
         src.r_facets = f.p;
         src.s_facets = f.p;
+        DevBuf<float4> scr(std::max<uint64_t>(n_tris, 1) * 7);
+        refine_prep(f.p, n_tris, scr.p, ctx->ws.num_sms, st);
+        src.r_screen = scr.p;
+        src.s_screen = scr.p;
         const int cull = (flags & TJ_FLAG_NO_CULL) ? 0 : 1;
         RefineQueueStore queue;
         if (cull) refine_pass(src, 0, n_descs, true, lbb.p, ubb.p, cull, queue, work.p, counters.p, ctx->ws.num_sms, st);

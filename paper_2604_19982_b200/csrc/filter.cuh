@@ -58,10 +58,13 @@ struct Workspace {
     DevBuf<unsigned char> temp;
     DevBuf<uint64_t> u64a;
     std::unique_ptr<RefineQueueStore> queue; // refinement pair queues, grow-only, per context
+    DevBuf<float4> screen_r, screen_s;       // per-level FP32 screening records, grow-only
     void release() {
         temp.release();
         u64a.release();
         queue.reset();
+        screen_r.release();
+        screen_s.release();
     }
 };
 

@@ -4,13 +4,19 @@
 //     lb_ij = max(0, d_ij - ph_i - ph_j)      ub_ij = d_ij + hd_i + hd_j
 // with d_ij the reference tri_tri_distance (geom_exact.cuh), bit-identical to the CPU.
 //
-// Phase-separated design (each phase a tight, converged loop; see refine.cu):
-//   seed   : warp per voxel pair; the pairs of smallest facet-AABB gap are queued;
+// Phase-separated design (each phase a tight, converged loop; kernels in refine.cu):
+//   prep   : thread per facet of the level; FP32 screening record (7 x float4) computed once;
+//   seed   : warp per voxel pair; O(r + s) choice of 2 promising facet pairs (facet box vs the
+//            partner segment's box, then the best partner facet) -> exact queue;
 //   eval   : thread per queued pair; exact FP64 tri_tri; 64-bit atomicMin of the IEEE bits of
 //            lb_ij / ub_ij into the op minima (order-free, exact for non-negative doubles);
-//   screen : warp per voxel pair; every facet pair is tested in FP32 against the op's
-//            thresholds (stage 1: facet-AABB gap; stage 2, box survivors through a per-warp
-//            queue: separating-axis bound); survivors are queued for a second eval.
+//   screen : warp per voxel pair, 32 x 32 facet tiles copied into shared memory; every facet
+//            pair is tested in FP32 against the op's thresholds (stage 1: facet-AABB gap;
+//            stage 2, box survivors through a per-warp queue: separating-axis bound);
+//            survivors -> exact queue, skip candidates with ill-conditioned edge/plane
+//            combinations -> verify queue;
+//   verify : thread per entry; the reference's FP64 piercing test for those combinations;
+//            a firing test sends the pair to the exact queue; then eval runs again.
 //
 // Exact-preserving screening. The join consumes only
 //     lb' = max(iv_lb, min lb_ij)      ub' = min(iv_ub, min ub_ij)      (intersect_interval)
@@ -29,9 +35,9 @@
 // (|cos(edge, normal)| >= 1e-3) needs the segment within ~1e-10 of the triangle, i.e. B below
 // delta, where a reference value of 0 is still >= B - delta; pairs with an ill-conditioned
 // combination are skipped only after the reference's FP64 piercing test for that combination
-// came out negative (k_verify). delta = 1e-5 (B + L_i + L_j) + 1e-12 |coords| dwarfs the
-// FP64 rounding in that regime. Skipped pairs cannot lower any minimum that matters, so the
-// op's lb' and ub' are bit-identical to the exhaustive loop.
+// came out negative (verify). delta = 1e-5 (B + L_i + L_j) + 1e-12 |coords| dwarfs the FP64
+// rounding in that regime. Skipped pairs cannot lower any minimum that matters, so the op's
+// lb' and ub' are bit-identical to the exhaustive loop.
 #pragma once
 #include <cstdint>
 
@@ -41,14 +47,15 @@ namespace tjx {
 
 constexpr int kRT = 32;    // r facets per screening tile
 constexpr int kST = 32;    // s facets per screening tile
-constexpr int kCS = 36;    // floats per screening record
+constexpr int kCS = 28;    // floats per screening record (7 x float4)
 constexpr int kQueue = 64; // per-warp SAT queue (< 32 pending + 32 new)
 
-// Screening record layout (floats):
-//  0-2 lo (rd)  3-5 hi (ru)  6 L (ru, facet AABB diagonal)  7 M (ru, max |coord|)
-//  8 hd (rd)  9 ph (ru)  10 ok (well shaped and non-degenerate)  11 pad
-//  12-20 unit edge directions (v1-v0, v2-v1, v0-v2)  21-23 unit normal
-//  24-32 v0 v1 v2 relative to the voxel pair's origin  33-35 pad
+// Screening record (floats), one per facet of a level, computed once by k_prep:
+//  0-2 lo (rd)   3 L (ru facet AABB diagonal; negated if the facet is not well shaped)
+//  4-6 hi (ru)   7 hd (rd)
+//  8-10 unit normal   11 ph (ru)
+//  12-20 unit edge directions (v1-v0, v2-v1, v0-v2)
+//  21-23 v1 - v0   24-26 v2 - v0   (FP64 differences rounded to FP32)   27 pad
 struct ScreenSmem {
     float rc[kRT * kCS];
     float sc[kST * kCS];
@@ -72,51 +79,52 @@ __device__ __forceinline__ void load_facet(const double* __restrict__ g, double*
     }
 }
 
-// Build the FP32 screening record of one facet record (TJ_FACET_STRIDE doubles).
-__device__ __forceinline__ void stage_screen(const double* __restrict__ g, const double* o, float* cr) {
+// Screening record of one facet record (TJ_FACET_STRIDE doubles).
+__device__ __forceinline__ void make_screen(const double* __restrict__ g, float* cr) {
     double c[12];
     load_facet(g, c);
-    float M = 0.f;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-        const double lo = fmin(fmin(c[d], c[3 + d]), c[6 + d]);
-        const double hi = fmax(fmax(c[d], c[3 + d]), c[6 + d]);
-        cr[d] = rd(lo);
-        cr[3 + d] = ru(hi);
-        M = fmaxf(M, fmaxf(fabsf(cr[d]), fabsf(cr[3 + d])));
+        cr[d] = rd(fmin(fmin(c[d], c[3 + d]), c[6 + d]));
+        cr[4 + d] = ru(fmax(fmax(c[d], c[3 + d]), c[6 + d]));
     }
-    const float dx = __fsub_ru(cr[3], cr[0]), dy = __fsub_ru(cr[4], cr[1]), dz = __fsub_ru(cr[5], cr[2]);
+    const float dx = __fsub_ru(cr[4], cr[0]), dy = __fsub_ru(cr[5], cr[1]), dz = __fsub_ru(cr[6], cr[2]);
     // facet AABB diagonal, rounded up (hardware sqrt is within 2 ulp; 1 + 2^-20 covers it)
-    cr[6] = __fmul_ru(sqrtf(__fadd_ru(__fadd_ru(__fmul_ru(dx, dx), __fmul_ru(dy, dy)), __fmul_ru(dz, dz))),
-                      1.0f + 0x1p-20f);
-    cr[7] = M;
-    cr[8] = rd(c[9]);
-    cr[9] = ru(c[10]);
+    const float L = __fmul_ru(sqrtf(__fadd_ru(__fadd_ru(__fmul_ru(dx, dx), __fmul_ru(dy, dy)), __fmul_ru(dz, dz))),
+                              1.0f + 0x1p-20f);
     const V3 v0 = {c[0], c[1], c[2]}, v1 = {c[3], c[4], c[5]}, v2 = {c[6], c[7], c[8]};
     double n2, s2;
     const bool degen = tri_degenerate(v0, v1, v2, &n2, &s2);
-    cr[10] = (!degen && n2 >= TJ_MUL(TJ_MUL(1e-4, s2), s2)) ? 1.f : 0.f;
-    cr[11] = 0.f;
-    const V3 es[4] = {vsub(v1, v0), vsub(v2, v1), vsub(v0, v2), vcross(vsub(v1, v0), vsub(v2, v0))};
+    const bool ok = !degen && n2 >= TJ_MUL(TJ_MUL(1e-4, s2), s2);
+    cr[3] = ok ? L : -L;
+    cr[7] = rd(c[9]);
+    cr[11] = ru(c[10]);
+    const V3 e01 = vsub(v1, v0), e12 = vsub(v2, v1), e20 = vsub(v0, v2), e02 = vsub(v2, v0);
+    const V3 es[4] = {vcross(e01, e02), e01, e12, e20};
+    const int at[4] = {8, 12, 15, 18};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const double l2 = vnorm2(es[k]);
         const double inv = l2 > 0.0 ? rsqrt(l2) : 0.0;
-        cr[12 + 3 * k] = (float)(es[k].x * inv);
-        cr[13 + 3 * k] = (float)(es[k].y * inv);
-        cr[14 + 3 * k] = (float)(es[k].z * inv);
+        cr[at[k]] = (float)(es[k].x * inv);
+        cr[at[k] + 1] = (float)(es[k].y * inv);
+        cr[at[k] + 2] = (float)(es[k].z * inv);
     }
-#pragma unroll
-    for (int k = 0; k < 9; ++k) cr[24 + k] = (float)(c[k] - o[k % 3]);
-    cr[33] = cr[34] = cr[35] = 0.f;
+    cr[21] = (float)e01.x;
+    cr[22] = (float)e01.y;
+    cr[23] = (float)e01.z;
+    cr[24] = (float)e02.x;
+    cr[25] = (float)e02.y;
+    cr[26] = (float)e02.z;
+    cr[27] = 0.f;
 }
 
-// Rigorous lower bound of the AABB gap (outward-rounded boxes, round-down arithmetic).
+// Rigorous lower bound of the gap between two outward-rounded boxes (lo at b+0, hi at b+4).
 __device__ __forceinline__ float box_gap_lb(const float* a, const float* b) {
     float s = 0.f;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-        const float g = fmaxf(0.f, fmaxf(__fsub_rd(b[d], a[3 + d]), __fsub_rd(a[d], b[3 + d])));
+        const float g = fmaxf(0.f, fmaxf(__fsub_rd(b[d], a[4 + d]), __fsub_rd(a[d], b[4 + d])));
         s = __fadd_rd(s, __fmul_rd(g, g));
     }
     // lower bound of sqrt(s): hardware sqrt (<= 2 ulp error) scaled down by 1 - 2^-20
@@ -129,12 +137,17 @@ struct Thresh {
     bool lb_sat;
 };
 
+__device__ __forceinline__ float abs_coord(const float* a) {
+    return fmaxf(fmaxf(fmaxf(fabsf(a[0]), fabsf(a[1])), fmaxf(fabsf(a[2]), fabsf(a[4]))), fmaxf(fabsf(a[5]), fabsf(a[6])));
+}
+
 // True iff a pair with distance lower bound B can change neither lb' nor ub'.
 __device__ __forceinline__ bool cannot_improve(float B, const float* a, const float* b, const Thresh& t) {
-    const float delta =
-        __fadd_ru(__fmul_ru(1e-5f, __fadd_ru(__fadd_ru(B, a[6]), b[6])), __fmul_ru(1e-12f, __fadd_ru(a[7], b[7])));
-    const float lbs = __fsub_rd(__fsub_rd(B, a[9]), b[9]);
-    const float ubs = __fadd_rd(__fadd_rd(B, a[8]), b[8]);
+    const float La = fabsf(a[3]), Lb = fabsf(b[3]);
+    const float M = __fadd_ru(abs_coord(a), abs_coord(b));
+    const float delta = __fadd_ru(__fmul_ru(1e-5f, __fadd_ru(__fadd_ru(B, La), Lb)), __fmul_ru(1e-12f, M));
+    const float lbs = __fsub_rd(__fsub_rd(B, a[11]), b[11]);
+    const float ubs = __fadd_rd(__fadd_rd(B, a[7]), b[7]);
     // a minimum of exactly 0 is the floor (lb_ij, ub_ij >= 0): that side needs no test
     const bool lb_ok = t.lb_sat || t.lb_u == 0.f || lbs >= __fadd_ru(t.lb_u, delta);
     const bool ub_ok = t.ub_u == 0.f || ubs >= __fadd_ru(t.ub_u, delta);
@@ -145,41 +158,28 @@ __device__ __forceinline__ bool cannot_improve(float B, const float* a, const fl
 // combinations (bit k < 3: edge k of a vs the plane of b; bit 3 + k: edge k of b vs the
 // plane of a; |cos(edge, normal)| < 1e-3). Returns -1 if the pair may never be skipped; a
 // non-zero mask means the skip additionally needs the reference's own piercing test to be
-// negative for those combinations (k_verify).
+// negative for those combinations (verify).
 __device__ __forceinline__ int skip_mask(float B, const float* a, const float* b) {
-    if (a[10] == 0.f || b[10] == 0.f) return -1;
-    if (B > 1e3f * fminf(a[6], b[6])) return -1;
+    if (a[3] < 0.f || b[3] < 0.f) return -1;
+    if (B > 1e3f * fminf(a[3], b[3])) return -1;
     int mask = 0;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        if (fabsf(a[12 + 3 * k] * b[21] + a[13 + 3 * k] * b[22] + a[14 + 3 * k] * b[23]) < 1e-3f) mask |= 1 << k;
-        if (fabsf(b[12 + 3 * k] * a[21] + b[13 + 3 * k] * a[22] + b[14 + 3 * k] * a[23]) < 1e-3f) mask |= 8 << k;
+        if (fabsf(a[12 + 3 * k] * b[8] + a[13 + 3 * k] * b[9] + a[14 + 3 * k] * b[10]) < 1e-3f) mask |= 1 << k;
+        if (fabsf(b[12 + 3 * k] * a[8] + b[13 + 3 * k] * a[9] + b[14 + 3 * k] * a[10]) < 1e-3f) mask |= 8 << k;
     }
     return mask;
 }
 
-// The reference's FP64 piercing test (segment_pierces_triangle, src/geom.cpp:120-136) for the
-// combinations in `mask` on two staged exact records: true iff none fires, i.e. the pair's
-// reference distance cannot be a (spurious) piercing 0.
-__device__ __noinline__ bool pierce_clear(int mask, uint32_t ra, uint32_t sb) {
-#pragma unroll 1
-    for (int k = 0; k < 6; ++k) {
-        if (!(mask & (1 << k))) continue;
-        const uint32_t src = k < 3 ? ra : sb, tri = k < 3 ? sb : ra;
-        if (ldw(tri, 14) != 0.0) continue; // degenerate target: the reference never tests it
-        const int e = k < 3 ? k : k - 3, e1 = e == 2 ? 0 : e + 1;
-        if (segment_pierces(ldv(src, e), ldv(src, e1), ldw(src, 11 + e), tri)) return false;
-    }
-    return true;
-}
-
-// Separating-axis lower bound of the distance between the two triangles (FP32, coordinates
-// relative to the voxel pair's origin): max over the 2 face normals and 9 edge-edge cross
-// products u of the projection gap / |u|, minus a bound on its rounding error (projections:
-// <= 3 ulp of |u|*R each; vertex rounding to FP32: <= 2^-24 * R per coordinate; rsqrt: 2^-22).
-__device__ __forceinline__ float sat_lower_bound(const float* a, const float* b) {
-    const float* av = a + 24;
-    const float* bv = b + 24;
+// Separating-axis lower bound of the distance between the two triangles (FP32; a's v0 is the
+// origin, `off` = b.v0 - a.v0 rounded from FP64): max over the 2 face normals and 9 edge-edge
+// cross products u of the projection gap / |u|, minus a bound on its rounding error
+// (projections: <= 3 ulp of |u|*R each; vertex rounding to FP32: <= 2^-24 R per coordinate
+// (+ 2^-24 |off| for b); rsqrt: 2^-22).
+__device__ __forceinline__ float sat_lower_bound(const float* a, const float* b, const float* off) {
+    const float av[9] = {0.f, 0.f, 0.f, a[21], a[22], a[23], a[24], a[25], a[26]};
+    const float bv[9] = {off[0], off[1], off[2], off[0] + b[21], off[1] + b[22], off[2] + b[23],
+                         off[0] + b[24], off[1] + b[25], off[2] + b[26]};
     float R = 0.f;
 #pragma unroll
     for (int k = 0; k < 9; ++k) R = fmaxf(R, fmaxf(fabsf(av[k]), fabsf(bv[k])));
@@ -200,8 +200,8 @@ __device__ __forceinline__ float sat_lower_bound(const float* a, const float* b)
         const float gap = fmaxf(bmin - amax, amin - bmax);
         if (gap > 0.f) best = fmaxf(best, gap * rsqrtf(u2));
     };
-    axis(a[21], a[22], a[23]);
-    axis(b[21], b[22], b[23]);
+    axis(a[8], a[9], a[10]);
+    axis(b[8], b[9], b[10]);
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
 #pragma unroll
@@ -213,6 +213,31 @@ __device__ __forceinline__ float sat_lower_bound(const float* a, const float* b)
     }
     // rounding margin: 8e-6 R absolute (>= 16x the analysed bound) + 1e-5 relative
     return fmaxf(0.f, best * (1.0f - 1e-5f) - 8e-6f * R);
+}
+
+// The reference's FP64 piercing test (segment_pierces_triangle, src/geom.cpp:120-136) for
+// edge (p, q) of one triangle against triangle (v0, v1, v2), with a pre-test: when
+// det^2 <= 1e-28 (1 - 1e-12) |dir|^2 |e1|^2 |e2|^2 (same det and squared norms as the
+// reference) the reference's |det| <= 1e-14 * norm*norm*norm test is certain to reject, and
+// the sqrt-based remainder is skipped. Otherwise the reference test runs unchanged.
+__device__ __forceinline__ bool pierces_ref(const V3& p, const V3& q, const V3& v0, const V3& v1, const V3& v2) {
+    const V3 dir = vsub(q, p);
+    const V3 e1 = vsub(v1, v0), e2 = vsub(v2, v0);
+    const V3 pv = vcross(dir, e2);
+    const double det = vdot(e1, pv);
+    const double n2d = vnorm2(dir), n2a = vnorm2(e1), n2b = vnorm2(e2);
+    if (det * det <= 1e-28 * (1.0 - 1e-12) * (n2d * n2a * n2b)) return false;
+    const double scale = TJ_MUL(TJ_MUL(TJ_SQRT(n2d), TJ_SQRT(n2a)), TJ_SQRT(n2b));
+    if (fabs(det) <= TJ_MUL(1e-14, scale)) return false;
+    const double inv = TJ_DIV(1.0, det);
+    const V3 tv = vsub(p, v0);
+    const double u = TJ_MUL(vdot(tv, pv), inv);
+    if (u < 0.0 || u > 1.0) return false;
+    const V3 qv = vcross(tv, e1);
+    const double v = TJ_MUL(vdot(dir, qv), inv);
+    if (v < 0.0 || TJ_ADD(u, v) > 1.0) return false;
+    const double tt = TJ_MUL(vdot(e2, qv), inv);
+    return tt >= 0.0 && tt <= 1.0;
 }
 
 // Exact evaluation of one facet pair from two staged exact records (shared addresses):

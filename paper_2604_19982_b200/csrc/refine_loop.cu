@@ -168,6 +168,19 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
             src.cand_ub = cs.ub.p;
             src.r_facets = R.facets[sr].p;
             src.s_facets = S.facets[ss].p;
+            {   // FP32 screening records of this level's facets, once per facet
+                const uint64_t nr = R.facets[sr].n / 12, ns = S.facets[ss].n / 12;
+                ws.screen_r.reserve(std::max<uint64_t>(nr * 7, 1));
+                refine_prep(R.facets[sr].p, nr, ws.screen_r.p, ws.num_sms, st);
+                src.r_screen = ws.screen_r.p;
+                if (S.facets[ss].p == R.facets[sr].p) {
+                    src.s_screen = ws.screen_r.p;
+                } else {
+                    ws.screen_s.reserve(std::max<uint64_t>(ns * 7, 1));
+                    refine_prep(S.facets[ss].p, ns, ws.screen_s.p, ws.num_sms, st);
+                    src.s_screen = ws.screen_s.p;
+                }
+            }
             const int cull = (spec.flags & TJ_FLAG_NO_CULL) ? 0 : 1;
             // seeds for every voxel pair first (op thresholds), then the screened passes
             if (cull)

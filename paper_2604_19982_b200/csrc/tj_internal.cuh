@@ -101,9 +101,11 @@ struct RefineSource {
     const uint64_t* s_off;
     const uint32_t* r_len;
     const uint32_t* s_len;
-    // both: facet records (TJ_FACET_STRIDE doubles each)
+    // both: facet records (TJ_FACET_STRIDE doubles each) and their FP32 screening records
     const double* r_facets;
     const double* s_facets;
+    const float4* r_screen; // 7 float4 per facet (refine_prep)
+    const float4* s_screen;
 };
 
 // A queued facet pair: op and the two global facet record indices.
@@ -119,15 +121,14 @@ struct RefineQueue {
 };
 
 struct RefineQueueStore {
-    DevBuf<PairRef> items, vitems;      // exact queue, verify queue
-    DevBuf<unsigned long long> count;   // [0] exact, [1] verify
-    RefineQueueStore() : count(2) {
-        items.alloc(1u << 22);
-        vitems.alloc(1u << 22);
-    }
+    DevBuf<PairRef> items;              // exact-evaluation queue
+    DevBuf<unsigned long long> count;
+    RefineQueueStore() : count(2) { items.alloc(1u << 22); }
     RefineQueue view() { return {items.p, (unsigned long long)items.n, count.p}; }
-    RefineQueue verify_view() { return {vitems.p, (unsigned long long)vitems.n, count.p + 1}; }
 };
+
+// FP32 screening records (7 float4 each) of n facet records (refine.cu, k_prep).
+void refine_prep(const double* facets, uint64_t n, float4* out, int num_sms, cudaStream_t st);
 
 // One refinement pass over voxel pairs [vp_begin, vp_end) (refine.cu): the seed pass queues
 // each voxel pair's 2 smallest-box-gap facet pairs, the screen pass every facet pair that

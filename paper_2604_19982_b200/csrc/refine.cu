@@ -228,6 +228,27 @@ __global__ void __launch_bounds__(256) k_screen(RefineSource src, uint64_t vp_be
                 const int step_i = 32 / scnt, step_j = 32 - (32 / scnt) * scnt; // t += 32 in (i, j)
                 int bi = lane / scnt, bj = lane - (lane / scnt) * scnt;
                 int nq = 0;
+                {   // per-row thresholds for the stage-1 test (box_cannot_improve)
+                    float Lm = 0.f, Mm = 0.f;
+                    if (lane < rcnt) { Lm = fabsf(sm.rc[lane * kCS + 3]); Mm = sm.rc[lane * kCS + 27]; }
+                    if (lane < scnt) {
+                        Lm = fmaxf(Lm, fabsf(sm.sc[lane * kCS + 3]));
+                        Mm = fmaxf(Mm, sm.sc[lane * kCS + 27]);
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        Lm = fmaxf(Lm, __shfl_xor_sync(0xffffffffu, Lm, o));
+                        Mm = fmaxf(Mm, __shfl_xor_sync(0xffffffffu, Mm, o));
+                    }
+                    const float delta0 = __fadd_ru(__fmul_ru(2e-5f, Lm), __fmul_ru(2e-12f, Mm));
+                    if (lane < rcnt) {
+                        const float ninf = __int_as_float(0xff800000);
+                        const bool lb_settled = th.lb_sat || th.lb_u == 0.f;
+                        sm.row_lb[lane] = lb_settled ? ninf : __fadd_ru(__fadd_ru(th.lb_u, delta0), sm.rc[lane * kCS + 11]);
+                        sm.row_ub[lane] = th.ub_u == 0.f ? ninf : __fsub_ru(__fadd_ru(th.ub_u, delta0), sm.rc[lane * kCS + 7]);
+                    }
+                    __syncwarp();
+                }
                 auto sat_round = [&](int n) { // screen sm.q[0, n) with the separating-axis bound
                     __syncwarp();
                     bool need = false;
@@ -259,8 +280,9 @@ __global__ void __launch_bounds__(256) k_screen(RefineSource src, uint64_t vp_be
                     if (t < npairs) {
                         const float* a = sm.rc + bi * kCS;
                         const float* b = sm.sc + bj * kCS;
-                        const float B = box_gap_lb(a, b);
-                        need = !cull || !(cannot_improve(B, a, b, th) && skip_mask(B, a, b) == 0);
+                        const float g2 = box_gap2_lb(a, b);
+                        need = !cull || !box_cannot_improve(g2, sm.row_lb[bi], sm.row_ub[bi], b) ||
+                               skip_mask(__fmul_rd(sqrtf(g2), 1.0f - 0x1p-20f), a, b) != 0;
                         ++tested;
                     }
                     if (!cull) {

@@ -55,10 +55,12 @@ constexpr int kQueue = 64; // per-warp SAT queue (< 32 pending + 32 new)
 //  4-6 hi (ru)   7 hd (rd)
 //  8-10 unit normal   11 ph (ru)
 //  12-20 unit edge directions (v1-v0, v2-v1, v0-v2)
-//  21-23 v1 - v0   24-26 v2 - v0   (FP64 differences rounded to FP32)   27 pad
+//  21-23 v1 - v0   24-26 v2 - v0   (FP64 differences rounded to FP32)   27 M (max |coordinate|)
 struct ScreenSmem {
     float rc[kRT * kCS];
     float sc[kST * kCS];
+    float row_lb[kRT]; // per r facet of the tile: T_lb + delta0 + ph_i (or -inf: lb side settled)
+    float row_ub[kRT]; // per r facet of the tile: T_ub + delta0 - hd_i (or -inf: ub side settled)
     uint16_t q[kQueue];
 };
 
@@ -116,7 +118,8 @@ __device__ __forceinline__ void make_screen(const double* __restrict__ g, float*
     cr[24] = (float)e02.x;
     cr[25] = (float)e02.y;
     cr[26] = (float)e02.z;
-    cr[27] = 0.f;
+    cr[27] = fmaxf(fmaxf(fmaxf(fabsf(cr[0]), fabsf(cr[1])), fmaxf(fabsf(cr[2]), fabsf(cr[4]))),
+                   fmaxf(fabsf(cr[5]), fabsf(cr[6]))); // M: max |coordinate|
 }
 
 // Rigorous lower bound of the gap between two outward-rounded boxes (lo at b+0, hi at b+4).
@@ -137,20 +140,43 @@ struct Thresh {
     bool lb_sat;
 };
 
-__device__ __forceinline__ float abs_coord(const float* a) {
-    return fmaxf(fmaxf(fmaxf(fabsf(a[0]), fabsf(a[1])), fmaxf(fabsf(a[2]), fabsf(a[4]))), fmaxf(fabsf(a[5]), fabsf(a[6])));
-}
-
 // True iff a pair with distance lower bound B can change neither lb' nor ub'.
 __device__ __forceinline__ bool cannot_improve(float B, const float* a, const float* b, const Thresh& t) {
     const float La = fabsf(a[3]), Lb = fabsf(b[3]);
-    const float M = __fadd_ru(abs_coord(a), abs_coord(b));
+    const float M = __fadd_ru(a[27], b[27]);
     const float delta = __fadd_ru(__fmul_ru(1e-5f, __fadd_ru(__fadd_ru(B, La), Lb)), __fmul_ru(1e-12f, M));
     const float lbs = __fsub_rd(__fsub_rd(B, a[11]), b[11]);
     const float ubs = __fadd_rd(__fadd_rd(B, a[7]), b[7]);
     // a minimum of exactly 0 is the floor (lb_ij, ub_ij >= 0): that side needs no test
     const bool lb_ok = t.lb_sat || t.lb_u == 0.f || lbs >= __fadd_ru(t.lb_u, delta);
     const bool ub_ok = t.ub_u == 0.f || ubs >= __fadd_ru(t.ub_u, delta);
+    return lb_ok && ub_ok;
+}
+
+// Lower bound of the squared AABB gap (outward-rounded boxes, round-down arithmetic).
+__device__ __forceinline__ float box_gap2_lb(const float* a, const float* b) {
+    float s = 0.f;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        const float g = fmaxf(0.f, fmaxf(__fsub_rd(b[d], a[4 + d]), __fsub_rd(a[d], b[4 + d])));
+        s = __fadd_rd(s, __fmul_rd(g, g));
+    }
+    return s;
+}
+
+// Stage-1 test of the screen pass, on the squared box gap g2 against the per-row thresholds
+// (ScreenSmem::row_*): with c = 1 - 1e-5 and delta0 >= 1e-5 (L_i + L_j) + 1e-12 (M_i + M_j),
+//   lb side: c B >= T_lb + delta0 + ph_i + ph_j   implies  B - ph_i - ph_j >= T_lb + delta(B)
+//   ub side: c B >= T_ub + delta0 - hd_i - hd_j   implies  B + hd_i + hd_j >= T_ub + delta(B)
+// i.e. the same condition as cannot_improve with a (larger) tile-wide delta. Comparisons are
+// made on squares (both sides non-negative) with directed rounding.
+__device__ __forceinline__ bool box_cannot_improve(float g2, float row_lb, float row_ub, const float* b) {
+    constexpr float kInvC = 1.0f / (1.0f - 1e-5f) * (1.0f + 0x1p-20f); // >= 1 / c
+    const float xl = __fadd_ru(row_lb, b[11]);
+    const float yu = __fsub_ru(row_ub, b[7]);
+    const float xs = __fmul_ru(xl, kInvC), ys = __fmul_ru(yu, kInvC);
+    const bool lb_ok = xl <= 0.f || g2 >= __fmul_ru(xs, xs);
+    const bool ub_ok = yu <= 0.f || g2 >= __fmul_ru(ys, ys);
     return lb_ok && ub_ok;
 }
 
@@ -162,6 +188,10 @@ __device__ __forceinline__ bool cannot_improve(float B, const float* a, const fl
 __device__ __forceinline__ int skip_mask(float B, const float* a, const float* b) {
     if (a[3] < 0.f || b[3] < 0.f) return -1;
     if (B > 1e3f * fminf(a[3], b[3])) return -1;
+    // Far apart (B > 2 (L_a + L_b)): no computed piercing can fire for any conditioning that
+    // passes the reference's |det| > 1e-14 scale test (its u, v, t errors are then below ~6%
+    // of the vertex-to-triangle distance, which needs the segment within 0.44 (L_a + L_b)).
+    if (B > 2.f * (a[3] + b[3])) return 0;
     int mask = 0;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {

@@ -135,6 +135,9 @@ typedef struct tj_join_result {
     uint64_t refine_chunks;
     double mbb_ms, voxel_ms, refine_ms, total_ms;
     uint64_t level_pairs_screened[TJ_MAX_LODS];  /* FP32 separating-axis tests run */
+    uint64_t level_pairs_verified[TJ_MAX_LODS];  /* FP64 piercing verifications run */
+    uint64_t level_vps_skipped[TJ_MAX_LODS];     /* voxel pairs skipped whole by the screen */
+    uint64_t level_facets_dropped[TJ_MAX_LODS];  /* facets dropped by the row/column screens */
 } tj_join_result;
 
 /* ---- context ---- */

@@ -383,6 +383,9 @@ int tj_join(tj_ctx* ctx, const tj_dataset* Rh, const tj_dataset* Sh, const tj_jo
             out->level_pairs_evaluated[i] = ro.levels[i].evaluated;
             out->level_pairs_tested[i] = ro.levels[i].tested;
             out->level_pairs_screened[i] = ro.levels[i].screened;
+            out->level_pairs_verified[i] = ro.levels[i].verified;
+            out->level_vps_skipped[i] = ro.levels[i].vps_skipped;
+            out->level_facets_dropped[i] = ro.levels[i].facets_dropped;
             out->level_ms[i] = ro.levels[i].ms;
             out->level_kernel_ms[i] = ro.levels[i].kernel_ms;
         }
@@ -429,11 +432,11 @@ int tj_refine_batch(tj_ctx* ctx, uint64_t n_tris, const double* tris, const doub
         upload(rl, r_len, n_descs, st);
         upload(sl, s_len, n_descs, st);
         // every descriptor is its own op: per-voxel-pair minima, exact (refine_kernel.cuh)
-        DevBuf<unsigned long long> lbb(n_descs), ubb(n_descs), work(1), counters(4);
+        DevBuf<unsigned long long> lbb(n_descs), ubb(n_descs), work(1), counters(kNumCounters);
         std::vector<unsigned long long> inf(n_descs, 0x7ff0000000000000ull);
         TJ_CUDA(cudaMemcpyAsync(lbb.p, inf.data(), n_descs * 8, cudaMemcpyHostToDevice, st));
         TJ_CUDA(cudaMemcpyAsync(ubb.p, inf.data(), n_descs * 8, cudaMemcpyHostToDevice, st));
-        TJ_CUDA(cudaMemsetAsync(counters.p, 0, 32, st));
+        TJ_CUDA(cudaMemsetAsync(counters.p, 0, kNumCounters * 8, st));
         RefineSource src{};
         src.r_off = ro.p;
         src.s_off = so.p;
@@ -443,8 +446,8 @@ int tj_refine_batch(tj_ctx* ctx, uint64_t n_tris, const double* tris, const doub
         src.s_facets = f.p;
         DevBuf<float4> scr(std::max<uint64_t>(n_tris, 1) * 7);
         refine_prep(f.p, n_tris, scr.p, ctx->ws.num_sms, st);
-        src.r_screen = scr.p;
-        src.s_screen = scr.p;
+        src.r_box = src.s_box = scr.p;
+        src.r_geo = src.s_geo = scr.p + 3 * n_tris;
         const int cull = (flags & TJ_FLAG_NO_CULL) ? 0 : 1;
         RefineQueueStore queue;
         if (cull) refine_pass(src, 0, n_descs, true, lbb.p, ubb.p, cull, queue, work.p, counters.p, ctx->ws.num_sms, st);

@@ -128,7 +128,7 @@ void knn_finalize_dev(Workspace& ws, CandDevStore& cs, uint32_t k, cudaStream_t 
 // refine_loop.cu
 struct LevelStats {
     uint32_t level;
-    uint64_t vps, facet_pairs, evaluated, tested, screened;
+    uint64_t vps, facet_pairs, evaluated, tested, screened, verified, vps_skipped, facets_dropped;
     double ms, kernel_ms;
 };
 struct RefineLoopOut {

@@ -132,6 +132,9 @@ public:
             l["evaluated"] = r.level_pairs_evaluated[i];
             l["tested"] = r.level_pairs_tested[i];
             l["screened"] = r.level_pairs_screened[i];
+            l["verified"] = r.level_pairs_verified[i];
+            l["vps_skipped"] = r.level_vps_skipped[i];
+            l["facets_dropped"] = r.level_facets_dropped[i];
             l["ms"] = r.level_ms[i];
             l["kernel_ms"] = r.level_kernel_ms[i];
             levels.append(l);

@@ -57,23 +57,17 @@ __device__ __forceinline__ void queue_push(const RefineQueue& q, bool want, uint
     }
 }
 
-__device__ __forceinline__ void load_rec(const float4* __restrict__ g, float* dst) {
-#pragma unroll
-    for (int k = 0; k < 7; ++k) {
-        const float4 v = __ldg(g + k);
-        dst[4 * k] = v.x;
-        dst[4 * k + 1] = v.y;
-        dst[4 * k + 2] = v.z;
-        dst[4 * k + 3] = v.w;
-    }
-}
-
-// Cooperative copy of n records (7 float4 each) into shared memory.
-__device__ __forceinline__ void copy_recs(const float4* __restrict__ g, uint64_t first, int n, float* dst) {
+// Cooperative gather of up to 32 screening records (facets first + list[k]) into shared
+// memory: box part from `box`, geometry part from `geo` (7 float4 per record in smem).
+__device__ __forceinline__ void gather_recs(const float4* __restrict__ box, const float4* __restrict__ geo,
+                                            uint64_t first, const uint16_t* list, int n, float* dst) {
     const int lane = threadIdx.x & 31;
     float4* d4 = reinterpret_cast<float4*>(dst);
-    const float4* s4 = g + first * 7;
-    for (int k = lane; k < 7 * n; k += 32) d4[k] = __ldg(s4 + k);
+    for (int k = lane; k < 7 * n; k += 32) {
+        const int rec = k / 7, part = k - 7 * (k / 7);
+        const uint64_t f = first + list[rec];
+        d4[k] = part < kBoxF4 ? __ldg(box + f * kBoxF4 + part) : __ldg(geo + f * kGeoF4 + (part - kBoxF4));
+    }
 }
 
 // Warp argmin (ties: lowest index) of (value, index).
@@ -87,12 +81,38 @@ __device__ __forceinline__ void warp_argmin(float& v, uint32_t& idx) {
 }
 
 __global__ void k_prep(const double* __restrict__ facets, uint64_t n, float4* __restrict__ out) {
+    float4* box = out;
+    float4* geo = out + kBoxF4 * n;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         float r[kCS];
         make_screen(facets + i * 12, r);
 #pragma unroll
-        for (int k = 0; k < 7; ++k) out[i * 7 + k] = make_float4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+        for (int k = 0; k < kBoxF4; ++k) box[i * kBoxF4 + k] = make_float4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+#pragma unroll
+        for (int k = 0; k < kGeoF4; ++k)
+            geo[i * kGeoF4 + k] = make_float4(r[12 + 4 * k], r[13 + 4 * k], r[14 + 4 * k], r[15 + 4 * k]);
     }
+}
+
+// Facet of [first, first + n) whose box is closest (gap, then centre distance) to `box`.
+__device__ __forceinline__ uint32_t closest_facet(const float4* __restrict__ set, uint64_t first, uint32_t n,
+                                                  const float* lo, const float* hi) {
+    const int lane = threadIdx.x & 31;
+    const float cx = 0.5f * (lo[0] + hi[0]), cy = 0.5f * (lo[1] + hi[1]), cz = 0.5f * (lo[2] + hi[2]);
+    const float box[8] = {lo[0], lo[1], lo[2], 0.f, hi[0], hi[1], hi[2], 0.f};
+    float best = __int_as_float(0x7f800000);
+    uint32_t bi = 0xffffffffu;
+    for (uint32_t i = lane; i < n; i += 32) {
+        const float4 a = __ldg(set + (first + i) * kBoxF4), b = __ldg(set + (first + i) * kBoxF4 + 1);
+        const float rec[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        const float g = box_gap_lb(rec, box);
+        const float dx = 0.5f * (a.x + b.x) - cx, dy = 0.5f * (a.y + b.y) - cy, dz = 0.5f * (a.z + b.z) - cz;
+        // gap dominates; the centre distance only orders near-ties (deepest overlap first)
+        const float key = g + 1e-3f * sqrtf(dx * dx + dy * dy + dz * dz);
+        if (key < best || (key == best && i < bi)) { best = key; bi = i; }
+    }
+    warp_argmin(best, bi);
+    return bi;
 }
 
 // Seed pass, warp per voxel pair, O(r + s): i* = the r facet closest (box gap) to the s
@@ -101,7 +121,6 @@ __global__ void k_prep(const double* __restrict__ facets, uint64_t n, float4* __
 __global__ void __launch_bounds__(256) k_seed(RefineSource src, uint64_t vp_begin, uint64_t vp_end, RefineQueue q,
                                               unsigned long long* work) {
     const int lane = threadIdx.x & 31;
-    const float kInfF = __int_as_float(0x7f800000);
     for (;;) {
         unsigned long long vp = 0;
         if (lane == 0) vp = atomicAdd(work, 1ull);
@@ -109,60 +128,21 @@ __global__ void __launch_bounds__(256) k_seed(RefineSource src, uint64_t vp_begi
         if (vp >= vp_end) break;
         const VpDescDev d = get_vp(src, vp);
         if (d.rn == 0 || d.sn == 0) continue;
-        const float4* R = src.r_screen + d.r0 * 7;
-        const float4* S = src.s_screen + d.s0 * 7;
-        // segment boxes (lo at [0..2], hi at [4..6], as in a record)
-        float br[8] = {kInfF, kInfF, kInfF, 0.f, -kInfF, -kInfF, -kInfF, 0.f};
-        float bs[8] = {kInfF, kInfF, kInfF, 0.f, -kInfF, -kInfF, -kInfF, 0.f};
-        for (uint32_t i = lane; i < d.rn; i += 32) {
-            const float4 lo = __ldg(R + i * 7), hi = __ldg(R + i * 7 + 1);
-            br[0] = fminf(br[0], lo.x); br[1] = fminf(br[1], lo.y); br[2] = fminf(br[2], lo.z);
-            br[4] = fmaxf(br[4], hi.x); br[5] = fmaxf(br[5], hi.y); br[6] = fmaxf(br[6], hi.z);
-        }
-        for (uint32_t j = lane; j < d.sn; j += 32) {
-            const float4 lo = __ldg(S + j * 7), hi = __ldg(S + j * 7 + 1);
-            bs[0] = fminf(bs[0], lo.x); bs[1] = fminf(bs[1], lo.y); bs[2] = fminf(bs[2], lo.z);
-            bs[4] = fmaxf(bs[4], hi.x); bs[5] = fmaxf(bs[5], hi.y); bs[6] = fmaxf(bs[6], hi.z);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                br[k] = fminf(br[k], __shfl_xor_sync(0xffffffffu, br[k], o));
-                bs[k] = fminf(bs[k], __shfl_xor_sync(0xffffffffu, bs[k], o));
-                br[4 + k] = fmaxf(br[4 + k], __shfl_xor_sync(0xffffffffu, br[4 + k], o));
-                bs[4 + k] = fmaxf(bs[4 + k], __shfl_xor_sync(0xffffffffu, bs[4 + k], o));
-            }
-        }
-        // argmin of (box gap, then centre distance): among facets touching the other box,
-        // prefer the one nearest its centre (deepest overlap)
-        auto closest = [&](const float4* set, uint32_t n, const float* box) {
-            const float cx = 0.5f * (box[0] + box[4]), cy = 0.5f * (box[1] + box[5]), cz = 0.5f * (box[2] + box[6]);
-            float best = kInfF;
-            uint32_t bi = 0xffffffffu;
-            for (uint32_t i = lane; i < n; i += 32) {
-                const float4 lo = __ldg(set + i * 7), hi = __ldg(set + i * 7 + 1);
-                const float rec[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-                const float g = box_gap_lb(rec, box);
-                const float dx = 0.5f * (lo.x + hi.x) - cx, dy = 0.5f * (lo.y + hi.y) - cy, dz = 0.5f * (lo.z + hi.z) - cz;
-                // gap dominates; the centre distance only orders near-ties (scaled to stay below gaps)
-                const float key = g + 1e-3f * sqrtf(dx * dx + dy * dy + dz * dz);
-                if (key < best || (key == best && i < bi)) { best = key; bi = i; }
-            }
-            warp_argmin(best, bi);
-            return bi;
-        };
-        const uint32_t ist = closest(R, d.rn, bs);
-        const uint32_t jst = closest(S, d.sn, br);
-        float bi_box[8], bj_box[8];
+        const SegAgg ar = seg_reduce(src.r_box, d.r0, d.rn);
+        const SegAgg as = seg_reduce(src.s_box, d.s0, d.sn);
+        const uint32_t ist = closest_facet(src.r_box, d.r0, d.rn, as.lo, as.hi);
+        const uint32_t jst = closest_facet(src.s_box, d.s0, d.sn, ar.lo, ar.hi);
+        float blo[3], bhi[3];
         {
-            const float4 lo = __ldg(R + ist * 7), hi = __ldg(R + ist * 7 + 1);
-            bi_box[0] = lo.x; bi_box[1] = lo.y; bi_box[2] = lo.z; bi_box[4] = hi.x; bi_box[5] = hi.y; bi_box[6] = hi.z;
-            const float4 lo2 = __ldg(S + jst * 7), hi2 = __ldg(S + jst * 7 + 1);
-            bj_box[0] = lo2.x; bj_box[1] = lo2.y; bj_box[2] = lo2.z; bj_box[4] = hi2.x; bj_box[5] = hi2.y; bj_box[6] = hi2.z;
+            const float4 a = __ldg(src.r_box + (d.r0 + ist) * kBoxF4), b = __ldg(src.r_box + (d.r0 + ist) * kBoxF4 + 1);
+            blo[0] = a.x; blo[1] = a.y; blo[2] = a.z; bhi[0] = b.x; bhi[1] = b.y; bhi[2] = b.z;
         }
-        const uint32_t jp = closest(S, d.sn, bi_box);
-        const uint32_t ip = closest(R, d.rn, bj_box);
+        const uint32_t jp = closest_facet(src.s_box, d.s0, d.sn, blo, bhi);
+        {
+            const float4 a = __ldg(src.s_box + (d.s0 + jst) * kBoxF4), b = __ldg(src.s_box + (d.s0 + jst) * kBoxF4 + 1);
+            blo[0] = a.x; blo[1] = a.y; blo[2] = a.z; bhi[0] = b.x; bhi[1] = b.y; bhi[2] = b.z;
+        }
+        const uint32_t ip = closest_facet(src.r_box, d.r0, d.rn, blo, bhi);
         queue_push(q, lane == 0, d.op, (uint32_t)(d.r0 + ist), (uint32_t)(d.s0 + jp));
         queue_push(q, lane == 0 && !(ip == ist && jst == jp), d.op, (uint32_t)(d.r0 + ip), (uint32_t)(d.s0 + jst));
     }
@@ -190,10 +170,65 @@ __device__ __noinline__ bool pierce_clear(int mask, const double* __restrict__ p
     return true;
 }
 
-// Screen pass: every facet pair not provably irrelevant (refine_kernel.cuh) is queued; skip
-// candidates with ill-conditioned edge/plane combinations are first checked with the
-// reference's own FP64 piercing test (pierce_clear).
-__global__ void __launch_bounds__(256) k_screen(RefineSource src, uint64_t vp_begin, uint64_t vp_end,
+// Second-stage screen of one queued facet pair (a, b: shared records): true iff the pair
+// must be evaluated exactly. Separating-axis bound in two stages (face normals, then the
+// 9 edge-edge axes); skip candidates with ill-conditioned edge/plane combinations are
+// checked with the reference's own FP64 piercing test (pierce_clear). Returns bit 0: needed,
+// bit 1: a piercing verification ran (one call site).
+__device__ __forceinline__ int sat_needed(const float* a, const float* b, const double* va, const double* vb, Thresh th) {
+    const float off[3] = {(float)(__ldg(vb) - __ldg(va)), (float)(__ldg(vb + 1) - __ldg(va + 1)),
+                          (float)(__ldg(vb + 2) - __ldg(va + 2))};
+    const SatFrame f = sat_frame(a, b, off);
+    const float B0 = box_gap_lb(a, b);
+    float B = fmaxf(B0, sat_faces(f, a, b));
+    int mask = cannot_improve(B, a, b, th) ? skip_mask(B, a, b) : -1;
+    if (mask != 0) {
+        B = fmaxf(B, sat_edges(f, a, b));
+        mask = cannot_improve(B, a, b, th) ? skip_mask(B, a, b) : -1;
+    }
+    if (mask < 0) return 1;
+    if (mask > 0) mask = plane_clear(mask, f, a, b);
+    if (mask == 0) return 0;
+    return pierce_clear(mask, va, vb) ? 2 : 3; // reference piercing test
+}
+
+// Builds the list of facets of [first, first + n) (n <= kCap) that survive the row/column
+// screen against the partner segment `o` (offsets relative to first); returns the count.
+__device__ __forceinline__ int build_list(const float4* __restrict__ box, uint64_t first, uint32_t n, const SegAgg& o,
+                                          float delta0, const Thresh& th, bool cull, uint16_t* list,
+                                          uint32_t& dropped) {
+    const int lane = threadIdx.x & 31;
+    int cnt = 0;
+    for (uint32_t i0 = 0; i0 < n; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        bool keep = false;
+        if (i < n) {
+            keep = true;
+            if (cull && o.ok) {
+                const float4 a = __ldg(box + (first + i) * kBoxF4), b = __ldg(box + (first + i) * kBoxF4 + 1);
+                const float ph = __ldg(box + (first + i) * kBoxF4 + 2).w;
+                const float lo[3] = {a.x, a.y, a.z}, hi[3] = {b.x, b.y, b.z};
+                if (a.w >= 0.f)
+                    keep = !agg_skip(lo, hi, o.lo, o.hi, a.w + o.Lmax, fminf(a.w, o.Lmin), __fadd_ru(ph, o.phmax),
+                                     __fadd_rd(b.w, o.hdmin), delta0, th);
+                if (!keep) ++dropped;
+            }
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (keep) list[cnt + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)i;
+        cnt += __popc(bal);
+    }
+    __syncwarp();
+    return cnt;
+}
+
+// Screen pass, warp per voxel pair, hierarchical: (1) the whole voxel pair against the op
+// thresholds (segment aggregates); (2) each r facet against the s segment and each s facet
+// against the r segment (row / column screens, O(r + s)); (3) the surviving facets in
+// 32 x 32 shared-memory tiles, every pair tested on its facet-AABB gap; (4) box survivors
+// through the separating-axis stage (sat_needed). Pairs that may still change the op's
+// bounds go to the exact queue (refine_kernel.cuh has the exactness argument).
+__global__ void __launch_bounds__(256, 2) k_screen(RefineSource src, uint64_t vp_begin, uint64_t vp_end,
                                                 const unsigned long long* __restrict__ op_lb_bits,
                                                 const unsigned long long* __restrict__ op_ub_bits, int cull,
                                                 RefineQueue q, unsigned long long* work,
@@ -201,7 +236,7 @@ __global__ void __launch_bounds__(256) k_screen(RefineSource src, uint64_t vp_be
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ScreenSmem& sm = reinterpret_cast<ScreenSmem*>(smem_raw)[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
-    unsigned long long tested = 0, sat_tests = 0;
+    uint32_t tested = 0, sat_tests = 0, verified = 0, vps_skipped = 0, dropped = 0; // per-lane (< 2^32)
     for (;;) {
         unsigned long long vp = 0;
         if (lane == 0) vp = atomicAdd(work, 1ull);
@@ -215,94 +250,120 @@ __global__ void __launch_bounds__(256) k_screen(RefineSource src, uint64_t vp_be
         const Thresh th{ru(tlb), ru(tub), tlb <= d.iv_lb};
         // nothing can change lb' or ub': the whole voxel pair is irrelevant
         if (cull && (th.lb_sat || th.lb_u == 0.f) && th.ub_u == 0.f) continue;
-        for (uint32_t r0 = 0; r0 < d.rn; r0 += kRT) {
-            const int rcnt = (int)min((uint32_t)kRT, d.rn - r0);
+        // hierarchical screens (voxel pair, rows, columns) only where they can pay off
+        const bool hier = cull && d.rn * d.sn >= kHierMinPairs;
+        float delta0 = 0.f; // tile-pair value when !hier
+        if (hier) {
+            const SegAgg ar = seg_reduce(src.r_box, d.r0, d.rn);
+            const SegAgg as = seg_reduce(src.s_box, d.s0, d.sn);
+            // delta0 >= 1e-5 (L_i + L_j) + 1e-12 (M_i + M_j) for every pair of the voxel pair
+            delta0 = __fadd_ru(__fmul_ru(2e-5f, fmaxf(ar.Lmax, as.Lmax)), __fmul_ru(2e-12f, fmaxf(seg_m(ar), seg_m(as))));
+            if (ar.ok && as.ok &&
+                agg_skip(ar.lo, ar.hi, as.lo, as.hi, ar.Lmax + as.Lmax, fminf(ar.Lmin, as.Lmin),
+                         __fadd_ru(ar.phmax, as.phmax), __fadd_rd(ar.hdmin, as.hdmin), delta0, th)) {
+                ++vps_skipped;
+                continue;
+            }
             __syncwarp();
-            copy_recs(src.r_screen, d.r0 + r0, rcnt, sm.rc);
-            for (uint32_t s0 = 0; s0 < d.sn; s0 += kST) {
-                const int scnt = (int)min((uint32_t)kST, d.sn - s0);
-                __syncwarp();
-                copy_recs(src.s_screen, d.s0 + s0, scnt, sm.sc);
-                __syncwarp();
-                const int npairs = rcnt * scnt;
-                const int step_i = 32 / scnt, step_j = 32 - (32 / scnt) * scnt; // t += 32 in (i, j)
-                int bi = lane / scnt, bj = lane - (lane / scnt) * scnt;
-                int nq = 0;
-                {   // per-row thresholds for the stage-1 test (box_cannot_improve)
-                    float Lm = 0.f, Mm = 0.f;
-                    if (lane < rcnt) { Lm = fabsf(sm.rc[lane * kCS + 3]); Mm = sm.rc[lane * kCS + 27]; }
-                    if (lane < scnt) {
-                        Lm = fmaxf(Lm, fabsf(sm.sc[lane * kCS + 3]));
-                        Mm = fmaxf(Mm, sm.sc[lane * kCS + 27]);
-                    }
+            if (lane == 0) {
+                sm.seg_r = ar;
+                sm.seg_s = as;
+            }
+            __syncwarp();
+        }
+        for (uint32_t rc0 = 0; rc0 < d.rn; rc0 += kCap) {
+            const int nrl = build_list(src.r_box, d.r0 + rc0, min((uint32_t)kCap, d.rn - rc0), sm.seg_s, delta0, th, hier,
+                                       sm.rl, dropped);
+            for (uint32_t sc0 = 0; nrl > 0 && sc0 < d.sn; sc0 += kCap) {
+                const int nsl = build_list(src.s_box, d.s0 + sc0, min((uint32_t)kCap, d.sn - sc0), sm.seg_r, delta0, th,
+                                           hier, sm.sl, dropped);
+                for (int rt0 = 0; nsl > 0 && rt0 < nrl; rt0 += kRT) {
+                    const int rcnt = min(kRT, nrl - rt0);
+                    __syncwarp();
+                    gather_recs(src.r_box, src.r_geo, d.r0 + rc0, sm.rl + rt0, rcnt, sm.rc);
+                    __syncwarp();
+                    for (int st0 = 0; st0 < nsl; st0 += kST) {
+                        const int scnt = min(kST, nsl - st0);
+                        __syncwarp();
+                        gather_recs(src.s_box, src.s_geo, d.s0 + sc0, sm.sl + st0, scnt, sm.sc);
+                        __syncwarp();
+                        float dl = delta0;
+                        if (!hier) { // tile-pair delta0 >= 1e-5 (L_i + L_j) + 1e-12 (M_i + M_j)
+                            float Lm = 0.f, Mm = 0.f;
+                            if (lane < rcnt) { Lm = fabsf(sm.rc[lane * kCS + 3]); Mm = sm.rc[lane * kCS + 27]; }
+                            if (lane < scnt) {
+                                Lm = fmaxf(Lm, fabsf(sm.sc[lane * kCS + 3]));
+                                Mm = fmaxf(Mm, sm.sc[lane * kCS + 27]);
+                            }
 #pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) {
-                        Lm = fmaxf(Lm, __shfl_xor_sync(0xffffffffu, Lm, o));
-                        Mm = fmaxf(Mm, __shfl_xor_sync(0xffffffffu, Mm, o));
-                    }
-                    const float delta0 = __fadd_ru(__fmul_ru(2e-5f, Lm), __fmul_ru(2e-12f, Mm));
-                    if (lane < rcnt) {
-                        const float ninf = __int_as_float(0xff800000);
-                        const bool lb_settled = th.lb_sat || th.lb_u == 0.f;
-                        sm.row_lb[lane] = lb_settled ? ninf : __fadd_ru(__fadd_ru(th.lb_u, delta0), sm.rc[lane * kCS + 11]);
-                        sm.row_ub[lane] = th.ub_u == 0.f ? ninf : __fsub_ru(__fadd_ru(th.ub_u, delta0), sm.rc[lane * kCS + 7]);
-                    }
-                    __syncwarp();
-                }
-                auto sat_round = [&](int n) { // screen sm.q[0, n) with the separating-axis bound
-                    __syncwarp();
-                    bool need = false;
-                    int i = 0, j = 0, mask = 0;
-                    uint32_t fr = 0, fs = 0;
-                    if (lane < n) {
-                        const int e = sm.q[lane];
-                        i = e >> 5;
-                        j = e & 31;
-                        fr = (uint32_t)(d.r0 + r0 + i);
-                        fs = (uint32_t)(d.s0 + s0 + j);
-                        const float* a = sm.rc + i * kCS;
-                        const float* b = sm.sc + j * kCS;
-                        const double* va = src.r_facets + (size_t)fr * 12;
-                        const double* vb = src.s_facets + (size_t)fs * 12;
-                        const float off[3] = {(float)(__ldg(vb) - __ldg(va)), (float)(__ldg(vb + 1) - __ldg(va + 1)),
-                                              (float)(__ldg(vb + 2) - __ldg(va + 2))};
-                        const float B = fmaxf(box_gap_lb(a, b), sat_lower_bound(a, b, off));
-                        mask = cannot_improve(B, a, b, th) ? skip_mask(B, a, b) : -1;
-                        need = mask < 0;
-                        if (mask > 0) need = !pierce_clear(mask, va, vb); // reference piercing test
-                        ++sat_tests;
-                    }
-                    queue_push(q, need, d.op, fr, fs);
-                };
-                for (int t0 = 0; t0 < npairs; t0 += 32) {
-                    const int t = t0 + lane;
-                    bool need = false;
-                    if (t < npairs) {
-                        const float* a = sm.rc + bi * kCS;
-                        const float* b = sm.sc + bj * kCS;
-                        const float g2 = box_gap2_lb(a, b);
-                        need = !cull || !box_cannot_improve(g2, sm.row_lb[bi], sm.row_ub[bi], b) ||
-                               skip_mask(__fmul_rd(sqrtf(g2), 1.0f - 0x1p-20f), a, b) != 0;
-                        ++tested;
-                    }
-                    if (!cull) {
-                        queue_push(q, need, d.op, (uint32_t)(d.r0 + r0 + bi), (uint32_t)(d.s0 + s0 + bj));
-                    } else {
-                        const unsigned bal = __ballot_sync(0xffffffffu, need);
-                        if (need) sm.q[nq + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)((bi << 5) | bj);
-                        nq += __popc(bal);
-                        if (nq >= 32) {
-                            sat_round(32);
-                            __syncwarp();
-                            if (lane < nq - 32) sm.q[lane] = sm.q[32 + lane];
-                            nq -= 32;
+                            for (int o = 16; o > 0; o >>= 1) {
+                                Lm = fmaxf(Lm, __shfl_xor_sync(0xffffffffu, Lm, o));
+                                Mm = fmaxf(Mm, __shfl_xor_sync(0xffffffffu, Mm, o));
+                            }
+                            dl = __fadd_ru(__fmul_ru(2e-5f, Lm), __fmul_ru(2e-12f, Mm));
+                        }
+                        if (lane < rcnt) { // per-row thresholds of the stage-1 pair test (box_cannot_improve)
+                            const float ninf = __int_as_float(0xff800000);
+                            const bool lb_settled = th.lb_sat || th.lb_u == 0.f;
+                            sm.row_lb[lane] = lb_settled ? ninf : __fadd_ru(__fadd_ru(th.lb_u, dl), sm.rc[lane * kCS + 11]);
+                            sm.row_ub[lane] = th.ub_u == 0.f ? ninf : __fsub_ru(__fadd_ru(th.ub_u, dl), sm.rc[lane * kCS + 7]);
+                        }
+                        __syncwarp();
+                        const int npairs = rcnt * scnt;
+                        const int step_i = 32 / scnt, step_j = 32 - (32 / scnt) * scnt; // t += 32 in (i, j)
+                        int bi = lane / scnt, bj = lane - (lane / scnt) * scnt;
+                        int nq = 0;
+                        for (int t0 = 0;; t0 += 32) {
+                            if (t0 < npairs) {
+                                const int t = t0 + lane;
+                                bool need = false;
+                                if (t < npairs) {
+                                    const float* a = sm.rc + bi * kCS;
+                                    const float* b = sm.sc + bj * kCS;
+                                    const float g2 = box_gap2_lb(a, b);
+                                    need = !cull || !box_cannot_improve(g2, sm.row_lb[bi], sm.row_ub[bi], b) ||
+                                           skip_mask(__fmul_rd(sqrtf(g2), 1.0f - 0x1p-20f), a, b) != 0;
+                                    ++tested;
+                                }
+                                if (!cull) {
+                                    queue_push(q, need, d.op, (uint32_t)(d.r0 + rc0 + sm.rl[rt0 + bi]),
+                                               (uint32_t)(d.s0 + sc0 + sm.sl[st0 + bj]));
+                                } else {
+                                    const unsigned bal = __ballot_sync(0xffffffffu, need);
+                                    if (need) sm.q[nq + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)((bi << 5) | bj);
+                                    nq += __popc(bal);
+                                }
+                                bj += step_j;
+                                bi += step_i;
+                                if (bj >= scnt) { bj -= scnt; ++bi; }
+                            }
+                            const bool last = t0 + 32 >= npairs;
+                            if (nq >= 32 || (last && nq > 0)) { // second stage on up to 32 queued pairs
+                                const int n = min(nq, 32);
+                                __syncwarp();
+                                bool need = false;
+                                uint32_t fr = 0, fs = 0;
+                                if (lane < n) {
+                                    const int e = sm.q[lane];
+                                    const int i = e >> 5, j = e & 31;
+                                    fr = (uint32_t)(d.r0 + rc0 + sm.rl[rt0 + i]);
+                                    fs = (uint32_t)(d.s0 + sc0 + sm.sl[st0 + j]);
+                                    const int r = sat_needed(sm.rc + i * kCS, sm.sc + j * kCS, src.r_facets + (size_t)fr * 12,
+                                                             src.s_facets + (size_t)fs * 12, th);
+                                    need = r & 1;
+                                    verified += r >> 1;
+                                    ++sat_tests;
+                                }
+                                queue_push(q, need, d.op, fr, fs);
+                                __syncwarp();
+                                if (lane < nq - n) sm.q[lane] = sm.q[n + lane];
+                                __syncwarp();
+                                nq -= n;
+                            }
+                            if (last && nq == 0) break;
                         }
                     }
-                    bj += step_j;
-                    bi += step_i;
-                    if (bj >= scnt) { bj -= scnt; ++bi; }
                 }
-                if (nq > 0) sat_round(nq);
             }
         }
     }
@@ -311,10 +372,15 @@ __global__ void __launch_bounds__(256) k_screen(RefineSource src, uint64_t vp_be
         for (int o = 16; o > 0; o >>= 1) {
             tested += __shfl_xor_sync(0xffffffffu, tested, o);
             sat_tests += __shfl_xor_sync(0xffffffffu, sat_tests, o);
+            verified += __shfl_xor_sync(0xffffffffu, verified, o);
+            dropped += __shfl_xor_sync(0xffffffffu, dropped, o);
         }
         if (lane == 0) {
-            atomicAdd(counters + 0, tested);
-            atomicAdd(counters + 3, sat_tests);
+            atomicAdd(counters + 0, (unsigned long long)tested);
+            atomicAdd(counters + 3, (unsigned long long)sat_tests);
+            atomicAdd(counters + 4, (unsigned long long)verified);
+            atomicAdd(counters + 5, (unsigned long long)vps_skipped);
+            atomicAdd(counters + 6, (unsigned long long)dropped);
         }
     }
 }
@@ -411,7 +477,7 @@ void refine_pass(const RefineSource& src, uint64_t vp_begin, uint64_t vp_end, bo
             TJ_CUDA(cudaMemsetAsync(qs.count.p, 0, 16, st));
             TJ_CUDA(cudaMemsetAsync(work, 0, 8, st));
             count_launch();
-            k_screen<<<warp_grid(vp_end - vp_begin, num_sms, 3), kScreenThreads, kScreenSmem, st>>>(
+            k_screen<<<warp_grid(vp_end - vp_begin, num_sms, 2), kScreenThreads, kScreenSmem, st>>>(
                 src, vp_begin, vp_end, lb_bits, ub_bits, cull, qs.view(), work,
                 attempt ? nullptr : counters);
             TJ_CUDA(cudaGetLastError());

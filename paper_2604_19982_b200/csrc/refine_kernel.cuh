@@ -48,20 +48,40 @@ namespace tjx {
 constexpr int kRT = 32;    // r facets per screening tile
 constexpr int kST = 32;    // s facets per screening tile
 constexpr int kCS = 28;    // floats per screening record (7 x float4)
+constexpr int kBoxF4 = 3;  // box part of a record (floats 0-11), its own array: 3 float4 per facet
+constexpr int kGeoF4 = 4;  // geometry part (floats 12-27): 4 float4 per facet
 constexpr int kQueue = 64; // per-warp SAT queue (< 32 pending + 32 new)
+constexpr int kCap = 128;  // per-warp survivor lists: facets per raw segment chunk
+constexpr uint32_t kHierMinPairs = 1024; // voxel pairs with fewer facet pairs skip the hierarchical screens
 
-// Screening record (floats), one per facet of a level, computed once by k_prep:
-//  0-2 lo (rd)   3 L (ru facet AABB diagonal; negated if the facet is not well shaped)
+// Aggregate of a facet segment (or of one facet) for the hierarchical screen: the union of
+// the outward-rounded facet boxes and the extreme per-facet quantities the pair tests use.
+struct SegAgg {
+    float lo[3], hi[3];
+    float Lmax;  // max facet L
+    float Lmin;  // min facet L
+    float phmax; // max ph (rounded up)
+    float hdmin; // min hd (rounded down)
+    bool ok;     // every facet well shaped
+};
+
+// Screening record (floats), one per facet of a level, computed once by k_prep and stored
+// as two arrays: the box part (floats 0-11, read by the seed pass and the row/column
+// screens) and the geometry part (floats 12-27, only for facets that survive them):
+//  0-2 lo (rd)   3 L (ru facet AABB diagonal; negative if the facet is not well shaped)
 //  4-6 hi (ru)   7 hd (rd)
 //  8-10 unit normal   11 ph (ru)
 //  12-20 unit edge directions (v1-v0, v2-v1, v0-v2)
 //  21-23 v1 - v0   24-26 v2 - v0   (FP64 differences rounded to FP32)   27 M (max |coordinate|)
-struct ScreenSmem {
+struct __align__(16) ScreenSmem {
     float rc[kRT * kCS];
     float sc[kST * kCS];
     float row_lb[kRT]; // per r facet of the tile: T_lb + delta0 + ph_i (or -inf: lb side settled)
     float row_ub[kRT]; // per r facet of the tile: T_ub + delta0 - hd_i (or -inf: ub side settled)
     uint16_t q[kQueue];
+    uint16_t rl[kCap]; // surviving r facets of the current raw chunk (offsets in the chunk)
+    uint16_t sl[kCap]; // surviving s facets
+    SegAgg seg_r, seg_s; // aggregates of the current voxel pair's segments
 };
 
 __device__ __forceinline__ float rd(double x) { return __double2float_rd(x); }
@@ -98,7 +118,7 @@ __device__ __forceinline__ void make_screen(const double* __restrict__ g, float*
     double n2, s2;
     const bool degen = tri_degenerate(v0, v1, v2, &n2, &s2);
     const bool ok = !degen && n2 >= TJ_MUL(TJ_MUL(1e-4, s2), s2);
-    cr[3] = ok ? L : -L;
+    cr[3] = ok ? L : -(L + 1e-30f); // strictly negative: not well shaped
     cr[7] = rd(c[9]);
     cr[11] = ru(c[10]);
     const V3 e01 = vsub(v1, v0), e12 = vsub(v2, v1), e20 = vsub(v0, v2), e02 = vsub(v2, v0);
@@ -180,6 +200,84 @@ __device__ __forceinline__ bool box_cannot_improve(float g2, float row_lb, float
     return lb_ok && ub_ok;
 }
 
+// Warp reduction of the box parts of facets [first, first + n) (all lanes call).
+__device__ __forceinline__ SegAgg seg_reduce(const float4* __restrict__ box, uint64_t first, uint32_t n) {
+    const float kInfF = __int_as_float(0x7f800000);
+    SegAgg g;
+    g.lo[0] = g.lo[1] = g.lo[2] = kInfF;
+    g.hi[0] = g.hi[1] = g.hi[2] = -kInfF;
+    g.Lmax = 0.f;
+    g.Lmin = kInfF;
+    g.phmax = 0.f;
+    g.hdmin = kInfF;
+    bool ok = true;
+    const int lane = threadIdx.x & 31;
+    for (uint32_t i = lane; i < n; i += 32) {
+        const float4* f = box + (first + i) * kBoxF4;
+        const float4 a = __ldg(f), b = __ldg(f + 1), c = __ldg(f + 2);
+        g.lo[0] = fminf(g.lo[0], a.x); g.lo[1] = fminf(g.lo[1], a.y); g.lo[2] = fminf(g.lo[2], a.z);
+        g.hi[0] = fmaxf(g.hi[0], b.x); g.hi[1] = fmaxf(g.hi[1], b.y); g.hi[2] = fmaxf(g.hi[2], b.z);
+        ok = ok && a.w >= 0.f;
+        g.Lmax = fmaxf(g.Lmax, fabsf(a.w));
+        g.Lmin = fminf(g.Lmin, fabsf(a.w));
+        g.hdmin = fminf(g.hdmin, b.w);
+        g.phmax = fmaxf(g.phmax, c.w);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            g.lo[k] = fminf(g.lo[k], __shfl_xor_sync(0xffffffffu, g.lo[k], o));
+            g.hi[k] = fmaxf(g.hi[k], __shfl_xor_sync(0xffffffffu, g.hi[k], o));
+        }
+        g.Lmax = fmaxf(g.Lmax, __shfl_xor_sync(0xffffffffu, g.Lmax, o));
+        g.Lmin = fminf(g.Lmin, __shfl_xor_sync(0xffffffffu, g.Lmin, o));
+        g.hdmin = fminf(g.hdmin, __shfl_xor_sync(0xffffffffu, g.hdmin, o));
+        g.phmax = fmaxf(g.phmax, __shfl_xor_sync(0xffffffffu, g.phmax, o));
+    }
+    g.ok = __all_sync(0xffffffffu, ok);
+    return g;
+}
+
+// Max |coordinate| of a segment (bounds every facet's M).
+__device__ __forceinline__ float seg_m(const SegAgg& g) {
+    return fmaxf(fmaxf(fmaxf(fabsf(g.lo[0]), fabsf(g.lo[1])), fmaxf(fabsf(g.lo[2]), fabsf(g.hi[0]))),
+                 fmaxf(fabsf(g.hi[1]), fabsf(g.hi[2])));
+}
+
+// Aggregated skip test (hierarchical screen): true only if EVERY facet pair (x, y) with x's
+// box inside box a and y's box inside box b passes the pair screen's skip conditions, i.e.
+// box_cannot_improve and skip_mask == 0 (far branch), given
+//   lsum  >= L_x + L_y,  lmin <= min(L_x, L_y)   (all facets well shaped),
+//   phsum >= ph_x + ph_y (rounded up),   hdsum <= hd_x + hd_y (rounded down),
+//   delta0 >= 1e-5 (L_x + L_y) + 1e-12 (M_x + M_y).
+// Every quantity is monotone in the right direction: the union-box gap lower-bounds each
+// pair's box gap (directed rounding), and the farthest-point distance Bmax (rounded up)
+// upper-bounds it.
+__device__ __forceinline__ bool agg_skip(const float* alo, const float* ahi, const float* blo, const float* bhi,
+                                         float lsum, float lmin, float phsum, float hdsum, float delta0,
+                                         const Thresh& t) {
+    constexpr float kInvC = 1.0f / (1.0f - 1e-5f) * (1.0f + 0x1p-20f); // >= 1 / c (box_cannot_improve)
+    float g2 = 0.f, m2 = 0.f;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        const float g = fmaxf(0.f, fmaxf(__fsub_rd(blo[d], ahi[d]), __fsub_rd(alo[d], bhi[d])));
+        g2 = __fadd_rd(g2, __fmul_rd(g, g));
+        const float m = fmaxf(__fsub_ru(bhi[d], alo[d]), __fsub_ru(ahi[d], blo[d]));
+        m2 = __fadd_ru(m2, __fmul_ru(m, m));
+    }
+    const bool lb_settled = t.lb_sat || t.lb_u == 0.f;
+    const float xl = __fadd_ru(__fadd_ru(t.lb_u, delta0), phsum);
+    const float yu = __fsub_ru(__fadd_ru(t.ub_u, delta0), hdsum);
+    const float xs = __fmul_ru(xl, kInvC), ys = __fmul_ru(yu, kInvC);
+    const bool lb_ok = lb_settled || xl <= 0.f || g2 >= __fmul_ru(xs, xs);
+    const bool ub_ok = t.ub_u == 0.f || yu <= 0.f || g2 >= __fmul_ru(ys, ys);
+    const float B = __fmul_rd(sqrtf(g2), 1.0f - 0x1p-20f);
+    const bool far = B > 2.f * lsum;                   // skip_mask's far branch for every pair
+    const bool near = __fsqrt_ru(m2) <= 1e3f * lmin;   // no pair beyond skip_mask's 1e3 L range
+    return lb_ok && ub_ok && far && near;
+}
+
 // Shape / range eligibility for a skip and the mask of ill-conditioned edge/plane
 // combinations (bit k < 3: edge k of a vs the plane of b; bit 3 + k: edge k of b vs the
 // plane of a; |cos(edge, normal)| < 1e-3). Returns -1 if the pair may never be skipped; a
@@ -202,47 +300,100 @@ __device__ __forceinline__ int skip_mask(float B, const float* a, const float* b
 }
 
 // Separating-axis lower bound of the distance between the two triangles (FP32; a's v0 is the
-// origin, `off` = b.v0 - a.v0 rounded from FP64): max over the 2 face normals and 9 edge-edge
-// cross products u of the projection gap / |u|, minus a bound on its rounding error
-// (projections: <= 3 ulp of |u|*R each; vertex rounding to FP32: <= 2^-24 R per coordinate
-// (+ 2^-24 |off| for b); rsqrt: 2^-22).
-__device__ __forceinline__ float sat_lower_bound(const float* a, const float* b, const float* off) {
-    const float av[9] = {0.f, 0.f, 0.f, a[21], a[22], a[23], a[24], a[25], a[26]};
-    const float bv[9] = {off[0], off[1], off[2], off[0] + b[21], off[1] + b[22], off[2] + b[23],
-                         off[0] + b[24], off[1] + b[25], off[2] + b[26]};
-    float R = 0.f;
+// origin, `off` = b.v0 - a.v0 rounded from FP64): max over the candidate axes u of the
+// projection gap / |u|, minus a bound on its rounding error (projections: <= 3 ulp of |u|*R
+// each; vertex rounding to FP32: <= 2^-24 R per coordinate (+ 2^-24 |off| for b); rsqrt:
+// 2^-22). Two stages: the 2 face normals (sat_faces), then the 9 edge-edge cross products
+// (sat_edges); each result alone is a rigorous lower bound.
+struct SatFrame {
+    float av[9], bv[9];
+    float R;
+};
+
+__device__ __forceinline__ SatFrame sat_frame(const float* a, const float* b, const float* off) {
+    SatFrame f;
+    f.av[0] = f.av[1] = f.av[2] = 0.f;
 #pragma unroll
-    for (int k = 0; k < 9; ++k) R = fmaxf(R, fmaxf(fabsf(av[k]), fabsf(bv[k])));
+    for (int k = 0; k < 3; ++k) {
+        f.av[3 + k] = a[21 + k];
+        f.av[6 + k] = a[24 + k];
+        f.bv[k] = off[k];
+        f.bv[3 + k] = off[k] + b[21 + k];
+        f.bv[6 + k] = off[k] + b[24 + k];
+    }
+    f.R = 0.f;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) f.R = fmaxf(f.R, fmaxf(fabsf(f.av[k]), fabsf(f.bv[k])));
+    return f;
+}
+
+__device__ __forceinline__ float sat_axis(const SatFrame& f, float ux, float uy, float uz) {
+    const float u2 = ux * ux + uy * uy + uz * uz;
+    if (!(u2 > 1e-30f)) return 0.f;
+    float amin = 3.4e38f, amax = -3.4e38f, bmin = 3.4e38f, bmax = -3.4e38f;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float pa = ux * f.av[3 * k] + uy * f.av[3 * k + 1] + uz * f.av[3 * k + 2];
+        const float pb = ux * f.bv[3 * k] + uy * f.bv[3 * k + 1] + uz * f.bv[3 * k + 2];
+        amin = fminf(amin, pa);
+        amax = fmaxf(amax, pa);
+        bmin = fminf(bmin, pb);
+        bmax = fmaxf(bmax, pb);
+    }
+    const float gap = fmaxf(bmin - amax, amin - bmax);
+    return gap > 0.f ? gap * rsqrtf(u2) : 0.f;
+}
+
+// rounding margin: 8e-6 R absolute (>= 16x the analysed bound) + 1e-5 relative
+__device__ __forceinline__ float sat_margin(float best, const SatFrame& f) {
+    return fmaxf(0.f, best * (1.0f - 1e-5f) - 8e-6f * f.R);
+}
+
+__device__ __forceinline__ float sat_faces(const SatFrame& f, const float* a, const float* b) {
+    return sat_margin(fmaxf(sat_axis(f, a[8], a[9], a[10]), sat_axis(f, b[8], b[9], b[10])), f);
+}
+
+__device__ __forceinline__ float sat_edges(const SatFrame& f, const float* a, const float* b) {
     float best = 0.f;
-    auto axis = [&](float ux, float uy, float uz) {
-        const float u2 = ux * ux + uy * uy + uz * uz;
-        if (!(u2 > 1e-30f)) return;
-        float amin = 3.4e38f, amax = -3.4e38f, bmin = 3.4e38f, bmax = -3.4e38f;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            const float pa = ux * av[3 * k] + uy * av[3 * k + 1] + uz * av[3 * k + 2];
-            const float pb = ux * bv[3 * k] + uy * bv[3 * k + 1] + uz * bv[3 * k + 2];
-            amin = fminf(amin, pa);
-            amax = fmaxf(amax, pa);
-            bmin = fminf(bmin, pb);
-            bmax = fmaxf(bmax, pb);
-        }
-        const float gap = fmaxf(bmin - amax, amin - bmax);
-        if (gap > 0.f) best = fmaxf(best, gap * rsqrtf(u2));
-    };
-    axis(a[8], a[9], a[10]);
-    axis(b[8], b[9], b[10]);
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
             const float* e = a + 12 + 3 * i;
-            const float* f = b + 12 + 3 * j;
-            axis(e[1] * f[2] - e[2] * f[1], e[2] * f[0] - e[0] * f[2], e[0] * f[1] - e[1] * f[0]);
+            const float* g = b + 12 + 3 * j;
+            best = fmaxf(best, sat_axis(f, e[1] * g[2] - e[2] * g[1], e[2] * g[0] - e[0] * g[2],
+                                        e[0] * g[1] - e[1] * g[0]));
         }
     }
-    // rounding margin: 8e-6 R absolute (>= 16x the analysed bound) + 1e-5 relative
-    return fmaxf(0.f, best * (1.0f - 1e-5f) - 8e-6f * R);
+    return sat_margin(best, f);
+}
+
+// Clears the bits of an ill-conditioned-combination mask (skip_mask) whose edge lies
+// robustly on one side of the other triangle's plane. The reference's piercing test for
+// edge (p, q) against triangle (v0, v1, v2) (src/geom.cpp:120-136) computes
+//     tt = (e2 . ((p - v0) x e1)) / (e1 . ((q - p) x e2)) = h_p / (h_p - h_q),
+// h_x = (x - v0) . (e1 x e2); with both h_p, h_q of one sign and |h| above the FP64
+// rounding of numerator and denominator (<= ~8 eps (|p - v0| + |q - p|) |e1| |e2|, i.e. a
+// clearance of ~1e-13 R for a well-shaped triangle, sin(angle) >= 1e-2), the computed tt
+// cannot land in [0, 1]: no piercing can be reported, whatever the conditioning. Here the
+// clearance is the FP32 signed distance to the plane (unit normal; error <= ~2e-6 R in the
+// local frame of radius R), required to exceed 3.2e-5 R.
+__device__ __forceinline__ int plane_clear(int mask, const SatFrame& f, const float* a, const float* b) {
+    const float m = 3.2e-5f * f.R;
+    float sa[3], sb[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        // a's vertices against b's plane (through bv[0..2]); b's vertices against a's (origin)
+        sa[k] = b[8] * (f.av[3 * k] - f.bv[0]) + b[9] * (f.av[3 * k + 1] - f.bv[1]) + b[10] * (f.av[3 * k + 2] - f.bv[2]);
+        sb[k] = a[8] * f.bv[3 * k] + a[9] * f.bv[3 * k + 1] + a[10] * f.bv[3 * k + 2];
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const int k1 = k == 2 ? 0 : k + 1;
+        if ((sa[k] > m && sa[k1] > m) || (sa[k] < -m && sa[k1] < -m)) mask &= ~(1 << k);
+        if ((sb[k] > m && sb[k1] > m) || (sb[k] < -m && sb[k1] < -m)) mask &= ~(8 << k);
+    }
+    return mask;
 }
 
 // The reference's FP64 piercing test (segment_pierces_triangle, src/geom.cpp:120-136) for

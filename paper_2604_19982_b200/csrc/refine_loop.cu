@@ -132,7 +132,7 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
     RefineLoopOut out;
     const uint64_t n = cs.n;
     DevBuf<unsigned long long> lbb(std::max<uint64_t>(n, 1)), ubb(std::max<uint64_t>(n, 1));
-    DevBuf<unsigned long long> counters(4), work(1);
+    DevBuf<unsigned long long> counters(kNumCounters), work(1);
     if (!ws.queue) ws.queue = std::make_unique<RefineQueueStore>();
     RefineQueueStore& queue = *ws.queue;
     DevBuf<uint8_t> updated;
@@ -155,7 +155,7 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
             k_fill_u64<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(lbb.p, n, kInfBits);
             count_launch();
             k_fill_u64<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(ubb.p, n, kInfBits);
-            TJ_CUDA(cudaMemsetAsync(counters.p, 0, 32, st));
+            TJ_CUDA(cudaMemsetAsync(counters.p, 0, kNumCounters * 8, st));
             count_launch();
             k_facet_pairs<<<grid_for(n_active, 256, ws.num_sms), 256, 0, st>>>(
                 active.p, n_active, R.facet_offsets[sr].p, S.facet_offsets[ss].p, counters.p + 2);
@@ -172,13 +172,16 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
                 const uint64_t nr = R.facets[sr].n / 12, ns = S.facets[ss].n / 12;
                 ws.screen_r.reserve(std::max<uint64_t>(nr * 7, 1));
                 refine_prep(R.facets[sr].p, nr, ws.screen_r.p, ws.num_sms, st);
-                src.r_screen = ws.screen_r.p;
+                src.r_box = ws.screen_r.p;
+                src.r_geo = ws.screen_r.p + 3 * nr;
                 if (S.facets[ss].p == R.facets[sr].p) {
-                    src.s_screen = ws.screen_r.p;
+                    src.s_box = src.r_box;
+                    src.s_geo = src.r_geo;
                 } else {
                     ws.screen_s.reserve(std::max<uint64_t>(ns * 7, 1));
                     refine_prep(S.facets[ss].p, ns, ws.screen_s.p, ws.num_sms, st);
-                    src.s_screen = ws.screen_s.p;
+                    src.s_box = ws.screen_s.p;
+                    src.s_geo = ws.screen_s.p + 3 * ns;
                 }
             }
             const int cull = (spec.flags & TJ_FLAG_NO_CULL) ? 0 : 1;
@@ -202,8 +205,8 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
                 knn_fixpoint(ws, cs, spec.k, (int16_t)level, err, st);
                 check_error(err, st);
             }
-            unsigned long long hc[4];
-            TJ_CUDA(cudaMemcpyAsync(hc, counters.p, 32, cudaMemcpyDeviceToHost, st));
+            unsigned long long hc[kNumCounters];
+            TJ_CUDA(cudaMemcpyAsync(hc, counters.p, sizeof(hc), cudaMemcpyDeviceToHost, st));
             TJ_CUDA(cudaStreamSynchronize(st));
             float kms = 0.f;
             TJ_CUDA(cudaEventElapsedTime(&kms, e0, e1));
@@ -211,6 +214,9 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
             ls.evaluated = hc[1];
             ls.facet_pairs = hc[2];
             ls.screened = hc[3];
+            ls.verified = hc[4];
+            ls.vps_skipped = hc[5];
+            ls.facets_dropped = hc[6];
             ls.kernel_ms = kms;
             n_active = compact_active(ws, cs, active, n_active, st);
             ls.ms = std::chrono::duration<double, std::milli>(Clock::now() - t0).count();

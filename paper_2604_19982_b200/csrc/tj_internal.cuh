@@ -104,8 +104,12 @@ struct RefineSource {
     // both: facet records (TJ_FACET_STRIDE doubles each) and their FP32 screening records
     const double* r_facets;
     const double* s_facets;
-    const float4* r_screen; // 7 float4 per facet (refine_prep)
-    const float4* s_screen;
+    // FP32 screening records (refine_prep): box parts (kBoxF4 float4 per facet) and geometry
+    // parts (kGeoF4 float4 per facet) as separate arrays
+    const float4* r_box;
+    const float4* r_geo;
+    const float4* s_box;
+    const float4* s_geo;
 };
 
 // A queued facet pair: op and the two global facet record indices.
@@ -113,6 +117,8 @@ struct PairRef {
     uint32_t op, fr, fs;
     uint32_t mask; // verify queue: ill-conditioned combinations to check
 };
+
+constexpr int kNumCounters = 8;
 
 struct RefineQueue {
     PairRef* items;
@@ -127,14 +133,17 @@ struct RefineQueueStore {
     RefineQueue view() { return {items.p, (unsigned long long)items.n, count.p}; }
 };
 
-// FP32 screening records (7 float4 each) of n facet records (refine.cu, k_prep).
+// FP32 screening records of n facet records (refine.cu, k_prep) into out[7 n]: box parts at
+// out[0, 3 n), geometry parts at out[3 n, 7 n).
 void refine_prep(const double* facets, uint64_t n, float4* out, int num_sms, cudaStream_t st);
 
 // One refinement pass over voxel pairs [vp_begin, vp_end) (refine.cu): the seed pass queues
 // each voxel pair's 2 smallest-box-gap facet pairs, the screen pass every facet pair that
 // may still change the op's bounds; then the queued pairs are evaluated exactly and folded
-// into lb_bits / ub_bits (atomicMin on IEEE bits). counters: [0] box tests, [1] exact
-// evaluations, [3] separating-axis tests ([2] is the refine loop's facet-pair count).
+// into lb_bits / ub_bits (atomicMin on IEEE bits). counters (kNumCounters): [0] facet-pair
+// box tests, [1] exact evaluations, [2] the refine loop's facet-pair count, [3]
+// separating-axis tests, [4] FP64 piercing verifications, [5] voxel pairs skipped whole,
+// [6] facets dropped by the row/column screens.
 void refine_pass(const RefineSource& src, uint64_t vp_begin, uint64_t vp_end, bool seed, unsigned long long* lb_bits,
                  unsigned long long* ub_bits, int cull, RefineQueueStore& qs, unsigned long long* work,
                  unsigned long long* counters, int num_sms, cudaStream_t st);

@@ -61,7 +61,10 @@ class JoinResult(ctypes.Structure):
                 ("level_ms", ctypes.c_double * MAXL), ("level_kernel_ms", ctypes.c_double * MAXL),
                 ("refine_chunks", ctypes.c_uint64), ("mbb_ms", ctypes.c_double), ("voxel_ms", ctypes.c_double),
                 ("refine_ms", ctypes.c_double), ("total_ms", ctypes.c_double),
-                ("level_pairs_screened", ctypes.c_uint64 * MAXL)]
+                ("level_pairs_screened", ctypes.c_uint64 * MAXL),
+                ("level_pairs_verified", ctypes.c_uint64 * MAXL),
+                ("level_vps_skipped", ctypes.c_uint64 * MAXL),
+                ("level_facets_dropped", ctypes.c_uint64 * MAXL)]
 
 
 def capi_functions():

@@ -176,12 +176,18 @@ __device__ __noinline__ bool pierce_clear(int mask, const double* __restrict__ p
 // checked with the reference's own FP64 piercing test (pierce_clear). Returns bit 0: needed,
 // bit 1: a piercing verification ran (one call site).
 __device__ __forceinline__ int sat_needed(const float* a, const float* b, const double* va, const double* vb, Thresh th) {
+    const float B0 = box_gap_lb(a, b);
+    int mask = cannot_improve(B0, a, b, th) ? skip_mask(B0, a, b) : -1;
+    if (mask == 0) return 0;
     const float off[3] = {(float)(__ldg(vb) - __ldg(va)), (float)(__ldg(vb + 1) - __ldg(va + 1)),
                           (float)(__ldg(vb + 2) - __ldg(va + 2))};
     const SatFrame f = sat_frame(a, b, off);
-    const float B0 = box_gap_lb(a, b);
+    if (mask > 0) { // the box gap already rules the pair out up to conditioning: plane sides first
+        mask = plane_clear(mask, f, a, b);
+        if (mask == 0) return 0;
+    }
     float B = fmaxf(B0, sat_faces(f, a, b));
-    int mask = cannot_improve(B, a, b, th) ? skip_mask(B, a, b) : -1;
+    mask = cannot_improve(B, a, b, th) ? skip_mask(B, a, b) : -1;
     if (mask != 0) {
         B = fmaxf(B, sat_edges(f, a, b));
         mask = cannot_improve(B, a, b, th) ? skip_mask(B, a, b) : -1;

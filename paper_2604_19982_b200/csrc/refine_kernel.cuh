@@ -278,11 +278,37 @@ __device__ __forceinline__ bool agg_skip(const float* alo, const float* ahi, con
     return lb_ok && ub_ok && far && near;
 }
 
+// Stage-1 pair test on float4 box records (lo.xyz + L, hi.xyz + hd) with the row's
+// thresholds rlb = T_lb + delta0 + ph_i, rub = T_ub + delta0 - hd_i (box_cannot_improve),
+// plus skip_mask's shape and 1e3 L range conditions: false iff the pair is skippable or
+// only needs the near-pair conditioning check (near_mask). Branch-free.
+__device__ __forceinline__ bool stage1_need(const float4& a0, const float4& a1, const float4& b0, const float4& b1,
+                                            float bph, float rlb, float rub) {
+    constexpr float kInvC = 1.0f / (1.0f - 1e-5f) * (1.0f + 0x1p-20f); // >= 1 / c
+    const float gx = fmaxf(0.f, fmaxf(__fsub_rd(b0.x, a1.x), __fsub_rd(a0.x, b1.x)));
+    const float gy = fmaxf(0.f, fmaxf(__fsub_rd(b0.y, a1.y), __fsub_rd(a0.y, b1.y)));
+    const float gz = fmaxf(0.f, fmaxf(__fsub_rd(b0.z, a1.z), __fsub_rd(a0.z, b1.z)));
+    const float g2 = __fadd_rd(__fadd_rd(__fmul_rd(gx, gx), __fmul_rd(gy, gy)), __fmul_rd(gz, gz));
+    const float xl = __fadd_ru(rlb, bph);
+    const float yu = __fsub_ru(rub, b1.w);
+    const float xs = __fmul_ru(xl, kInvC), ys = __fmul_ru(yu, kInvC);
+    const bool lb_ok = xl <= 0.f || g2 >= __fmul_ru(xs, xs);
+    const bool ub_ok = yu <= 0.f || g2 >= __fmul_ru(ys, ys);
+    const float B = __fmul_rd(sqrtf(g2), 1.0f - 0x1p-20f);
+    const bool shapes = a0.w >= 0.f && b0.w >= 0.f && !(B > 1e3f * fminf(a0.w, b0.w));
+    return !(lb_ok && ub_ok && shapes);
+}
+
 // Shape / range eligibility for a skip and the mask of ill-conditioned edge/plane
 // combinations (bit k < 3: edge k of a vs the plane of b; bit 3 + k: edge k of b vs the
 // plane of a; |cos(edge, normal)| < 1e-3). Returns -1 if the pair may never be skipped; a
 // non-zero mask means the skip additionally needs the reference's own piercing test to be
 // negative for those combinations (verify).
+// Conditioning mask of a pair that passed stage1_need (shapes and range already checked):
+// 0 if far (B > 2 (L_a + L_b), B from the box gap) or well conditioned; else the mask of
+// ill-conditioned combinations (see skip_mask).
+__device__ __forceinline__ int near_mask(const float* a, const float* b, float La, float Lb);
+
 __device__ __forceinline__ int skip_mask(float B, const float* a, const float* b) {
     if (a[3] < 0.f || b[3] < 0.f) return -1;
     if (B > 1e3f * fminf(a[3], b[3])) return -1;
@@ -290,6 +316,18 @@ __device__ __forceinline__ int skip_mask(float B, const float* a, const float* b
     // passes the reference's |det| > 1e-14 scale test (its u, v, t errors are then below ~6%
     // of the vertex-to-triangle distance, which needs the segment within 0.44 (L_a + L_b)).
     if (B > 2.f * (a[3] + b[3])) return 0;
+    int mask = 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        if (fabsf(a[12 + 3 * k] * b[8] + a[13 + 3 * k] * b[9] + a[14 + 3 * k] * b[10]) < 1e-3f) mask |= 1 << k;
+        if (fabsf(b[12 + 3 * k] * a[8] + b[13 + 3 * k] * a[9] + b[14 + 3 * k] * a[10]) < 1e-3f) mask |= 8 << k;
+    }
+    return mask;
+}
+
+__device__ __forceinline__ int near_mask(const float* a, const float* b, float La, float Lb) {
+    const float B = box_gap_lb(a, b);
+    if (B > 2.f * (La + Lb)) return 0;
     int mask = 0;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {

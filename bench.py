@@ -259,8 +259,8 @@ def main():
     # ---- e2e: public API from host buffers ----
     e2e = None
     if not a.no_e2e:
-        h2d = float(res.device_bytes)
         ts = []
+        parts = []
         d2h = 0
         for i in range(max(1, min(a.steps, 3)) + 1):
             if world > 1:
@@ -277,13 +277,18 @@ def main():
             n_c = st["stages"][0]["pairs_in"] - st["stages"][0]["removed"]
             d2h = n_c * (4 + 4 + 8 + 8 + 1 + 2) + (R.n_objects + 1) * 8 + R.n_objects * 4
             pairs_e2e = st["stages"][1]["pairs_in"]
+            if i > 0:
+                parts.append(st.get("b200", {}))
+            h2d = st.get("b200", {}).get("h2d_bytes", 0)
         e2e_ms = float(np.mean(ts))
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e = {"value": pairs_e2e / (float(t[0]) / 1e3), "unit": "pairs/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": float(t[0]),
-               "path": "paper_2604_19982_b200._core.join_datasets -> trijoin::run_join -> tj_join (C-ABI)"}
+               "path": "paper_2604_19982_b200._core.join_datasets -> trijoin::run_join -> tj_join (C-ABI)",
+               "breakdown_ms": {k: round(float(np.mean([p.get(k, 0.0) for p in parts])), 2)
+                                for k in ("pack_ms", "upload_ms", "device_ms", "stream_wait_ms")}}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:

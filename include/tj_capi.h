@@ -52,7 +52,13 @@ enum { TJ_STAGE_NONE = -3, TJ_STAGE_MBB = -2, TJ_STAGE_VOXEL = -1 };
 /* Behaviour flags (none of them changes a result). */
 enum {
     TJ_FLAG_NO_CULL = 1u << 0, /* disable exact-preserving facet-pair culling (A/B checks) */
-    TJ_FLAG_SYNC_STAGES = 1u << 1 /* synchronise + time every stage (stats wall_ms) */
+    TJ_FLAG_SYNC_STAGES = 1u << 1, /* synchronise + time every stage (stats wall_ms) */
+    /* Keep every candidate interval equal to the reference's at every level. Without it, an
+       intersection join without a trace refines in decision mode: a level only establishes
+       whether min lb_ij / min ub_ij are 0 (the only facts an intersection decision and its
+       records depend on), so intervals of pairs it removes may stay looser
+       than the reference's; records and stage counters are identical either way. */
+    TJ_FLAG_EXACT_INTERVALS = 1u << 2
 };
 
 #define TJ_FACET_STRIDE 12 /* doubles per facet record: v0.xyz v1.xyz v2.xyz hd ph pad */
@@ -138,6 +144,8 @@ typedef struct tj_join_result {
     uint64_t level_pairs_verified[TJ_MAX_LODS];  /* FP64 piercing verifications run */
     uint64_t level_vps_skipped[TJ_MAX_LODS];     /* voxel pairs skipped whole by the screen */
     uint64_t level_facets_dropped[TJ_MAX_LODS];  /* facets dropped by the row/column screens */
+    double level_wait_ms[TJ_MAX_LODS];           /* host time blocked on a streamed level */
+    int32_t decision_mode;                       /* 1: refined in decision mode (TJ_FLAG_EXACT_INTERVALS) */
 } tj_join_result;
 
 /* ---- context ---- */
@@ -154,6 +162,40 @@ uint64_t tj_kernel_launches(void);
 int tj_dataset_upload(tj_ctx* ctx, const tj_dataset_view* view, tj_dataset** out);
 void tj_dataset_free(tj_dataset* ds);
 uint64_t tj_dataset_device_bytes(const tj_dataset* ds);
+
+/* ---- streamed datasets: compact mesh form, per-level H2D overlapping the join ----
+ *
+ * The e2e path of run_join (include/trijoin/engine.hpp) does not ship the expanded
+ * 96-byte facet records over PCIe. It ships each LOD level in the reference's own mesh
+ * form (vertices + index triples + hd/ph + voxel facet-id lists, ~44 B per facet) and the
+ * device expands it into the resident record layout. Levels are uploaded one at a time
+ * on the dataset's own copy stream while tj_join already runs the filters and the
+ * coarser levels; tj_join blocks (host condition variable, then a device event wait) only
+ * when it reaches a level that has not arrived yet.
+ *
+ * tj_dataset_begin: uploads the object and voxel arrays of `header` (its facets[] may be
+ *   NULL; facet_offsets[] is required) and reserves every level. n_vertices[li] and
+ *   n_facets[li] are the level's dataset-wide vertex / facet totals.
+ * tj_dataset_put_level: queues level slot `slot`: copies from the caller's buffers (keep
+ *   them valid, preferably page-locked, until tj_dataset_sync returns) and expands. May be
+ *   called from another host thread while tj_join runs on the dataset. lv == NULL marks
+ *   the slot failed: a join waiting for it returns TJ_EINVAL.
+ * tj_dataset_sync: waits for every queued level copy of the dataset.
+ */
+typedef struct tj_level_mesh_view {
+    uint64_t n_vertices;
+    uint64_t n_facets;
+    const double* vertices;       /* [n_vertices*3] all objects, concatenated */
+    const uint32_t* tris;         /* [n_facets*3] dataset-global vertex ids */
+    const double* hd;             /* [n_facets] */
+    const double* ph;             /* [n_facets] */
+    const uint32_t* voxel_facets; /* [facet_offsets[li][n_voxels]] dataset-global facet ids, voxel order */
+} tj_level_mesh_view;
+
+int tj_dataset_begin(tj_ctx* ctx, const tj_dataset_view* header, const uint64_t* n_vertices,
+                     const uint64_t* n_facets, tj_dataset** out);
+int tj_dataset_put_level(tj_dataset* ds, uint32_t slot, const tj_level_mesh_view* lv);
+int tj_dataset_sync(tj_dataset* ds);
 
 /* ---- host-side index loading (backs load_index, reference src/index_io.cpp:244-249) ----
    Parses a 3DPJ1 index file and packs it into the tj_dataset_view layout in host memory,

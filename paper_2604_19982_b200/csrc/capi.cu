@@ -20,6 +20,7 @@ struct tj_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     Workspace ws;
+    std::mutex err_mu; // tj_dataset_put_level may fail on another thread than tj_join
     std::string last_error;
 };
 
@@ -38,6 +39,14 @@ void set_global_error(const std::string& m) {
     g_err = m;
 }
 
+void set_ctx_error(tj_ctx* ctx, const char* m) {
+    if (ctx) {
+        std::lock_guard<std::mutex> lk(ctx->err_mu);
+        ctx->last_error = m;
+    }
+    set_global_error(m);
+}
+
 // Restores the thread's allocation stream on scope exit.
 struct AllocStreamScope {
     cudaStream_t saved;
@@ -53,16 +62,13 @@ int guarded(tj_ctx* ctx, F&& f) {
         f();
         return TJ_OK;
     } catch (const Error& e) {
-        if (ctx) ctx->last_error = e.what();
-        set_global_error(e.what());
+        set_ctx_error(ctx, e.what());
         return e.code;
     } catch (const std::bad_alloc& e) {
-        if (ctx) ctx->last_error = "host allocation failed";
-        set_global_error("host allocation failed");
+        set_ctx_error(ctx, "host allocation failed");
         return TJ_ENOMEM;
     } catch (const std::exception& e) {
-        if (ctx) ctx->last_error = e.what();
-        set_global_error(e.what());
+        set_ctx_error(ctx, e.what());
         return TJ_ECUDA;
     }
 }
@@ -122,9 +128,85 @@ T* host_copy(const DevBuf<T>& src, uint64_t n, cudaStream_t st) {
     return p;
 }
 
+
+// Object and voxel arrays of a dataset view (shared by tj_dataset_upload / _begin).
+void upload_objects(DatasetDev& d, const tj_dataset_view* v, cudaStream_t st) {
+    if (v->n_levels == 0 || v->n_levels > TJ_MAX_LODS)
+        throw Error(TJ_EINVAL, "tj_dataset_upload: n_levels must be in [1, 16]");
+    const uint32_t no = v->n_objects;
+    if (!v->levels || !v->voxel_offsets || (no && (!v->mbb || !v->anchor)))
+        throw Error(TJ_EINVAL, "tj_dataset_upload: null object arrays");
+    d.n_objects = no;
+    d.levels.assign(v->levels, v->levels + v->n_levels);
+    d.voxel_offsets_h.assign(v->voxel_offsets, v->voxel_offsets + no + 1);
+    d.n_voxels = d.voxel_offsets_h.back();
+    for (uint32_t o = 0; o < no; ++o)
+        if (d.voxel_offsets_h[o + 1] < d.voxel_offsets_h[o])
+            throw Error(TJ_EINVAL, "tj_dataset_upload: voxel_offsets not monotone");
+    if (d.n_voxels && (!v->voxel_box || !v->voxel_anchor)) throw Error(TJ_EINVAL, "tj_dataset_upload: null voxel arrays");
+    upload(d.mbb, v->mbb, 6ull * no, st);
+    upload(d.anchor, v->anchor, 3ull * no, st);
+    upload(d.voxel_offsets, v->voxel_offsets, no + 1ull, st);
+    upload(d.voxel_box, v->voxel_box, 6ull * d.n_voxels, st);
+    upload(d.voxel_anchor, v->voxel_anchor, 3ull * d.n_voxels, st);
+    d.facet_offsets.resize(v->n_levels);
+    d.facets.resize(v->n_levels);
+    d.bytes = (9ull * no + 9ull * d.n_voxels) * 8 + (no + 1ull) * 8;
+}
+
+// Expansion of one level's compact mesh form into the resident record layout: entry e
+// of the voxel-ordered CSR gets (v0, v1, v2, hd, ph, 0) of facet voxel_facets[e]
+// (the record the reference's gather_facet_data builds per chunk, src/refine.cpp:25-61).
+__global__ void k_expand_level(const double* __restrict__ verts, const uint32_t* __restrict__ tris,
+                               const double* __restrict__ hd, const double* __restrict__ ph,
+                               const uint32_t* __restrict__ vf, uint64_t entries, double* __restrict__ out) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < entries; e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t f = __ldg(vf + e);
+        const uint32_t t0 = __ldg(tris + 3ull * f), t1 = __ldg(tris + 3ull * f + 1), t2 = __ldg(tris + 3ull * f + 2);
+        double2* o = reinterpret_cast<double2*>(out + e * TJ_FACET_STRIDE);
+        const double* a = verts + 3ull * t0;
+        const double* b = verts + 3ull * t1;
+        const double* c = verts + 3ull * t2;
+        o[0] = make_double2(__ldg(a), __ldg(a + 1));
+        o[1] = make_double2(__ldg(a + 2), __ldg(b));
+        o[2] = make_double2(__ldg(b + 1), __ldg(b + 2));
+        o[3] = make_double2(__ldg(c), __ldg(c + 1));
+        o[4] = make_double2(__ldg(c + 2), __ldg(hd + f));
+        o[5] = make_double2(__ldg(ph + f), 0.0);
+    }
+}
+
+void launch_expand_level(const double* verts, const uint32_t* tris, const double* hd, const double* ph,
+                         const uint32_t* vf, uint64_t entries, double* out, int num_sms, cudaStream_t st) {
+    if (!entries) return;
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((entries + 255) / 256, (uint64_t)num_sms * 16));
+    count_launch();
+    k_expand_level<<<grid, 256, 0, st>>>(verts, tris, hd, ph, vf, entries, out);
+    TJ_CUDA(cudaGetLastError());
+}
+
 } // namespace
 
 namespace tjx {
+LevelGate::~LevelGate() {
+    cudaSetDevice(device);
+    for (cudaEvent_t e : ev)
+        if (e) cudaEventDestroy(e);
+    if (copy) cudaStreamDestroy(copy);
+}
+
+double level_ready(const DatasetDev& d, int slot, cudaStream_t st) {
+    if (!d.gate) return 0.0;
+    LevelGate& g = *d.gate;
+    const auto t0 = std::chrono::steady_clock::now();
+    std::unique_lock<std::mutex> lk(g.mu);
+    g.cv.wait(lk, [&] { return g.state[slot] != LevelGate::kPending; });
+    if (g.state[slot] == LevelGate::kFailed)
+        throw Error(TJ_EINVAL, "join: level " + std::to_string(d.levels[slot]) + " of a streamed dataset was not delivered");
+    TJ_CUDA(cudaStreamWaitEvent(st, g.ev[slot], 0));
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
 unsigned long long& launch_counter_ref() {
     static unsigned long long n = 0;
     return n;
@@ -200,26 +282,8 @@ int tj_dataset_upload(tj_ctx* ctx, const tj_dataset_view* v, tj_dataset** out) {
     const int rc = guarded(ctx, [&] {
         DatasetDev& d = ds->d;
         cudaStream_t st = ctx->stream;
-        if (v->n_levels == 0 || v->n_levels > TJ_MAX_LODS)
-            throw Error(TJ_EINVAL, "tj_dataset_upload: n_levels must be in [1, 16]");
-        const uint32_t no = v->n_objects;
-        if (no && (!v->mbb || !v->anchor || !v->voxel_offsets))
-            throw Error(TJ_EINVAL, "tj_dataset_upload: null object arrays");
-        d.n_objects = no;
-        d.levels.assign(v->levels, v->levels + v->n_levels);
-        d.voxel_offsets_h.assign(v->voxel_offsets, v->voxel_offsets + no + 1);
-        d.n_voxels = d.voxel_offsets_h.back();
-        for (uint32_t o = 0; o < no; ++o)
-            if (d.voxel_offsets_h[o + 1] < d.voxel_offsets_h[o])
-                throw Error(TJ_EINVAL, "tj_dataset_upload: voxel_offsets not monotone");
-        upload(d.mbb, v->mbb, 6ull * no, st);
-        upload(d.anchor, v->anchor, 3ull * no, st);
-        upload(d.voxel_offsets, v->voxel_offsets, no + 1ull, st);
-        upload(d.voxel_box, v->voxel_box, 6ull * d.n_voxels, st);
-        upload(d.voxel_anchor, v->voxel_anchor, 3ull * d.n_voxels, st);
-        d.facet_offsets.resize(v->n_levels);
-        d.facets.resize(v->n_levels);
-        d.bytes = (9ull * no + 9ull * d.n_voxels) * 8 + (no + 1ull) * 8;
+        upload_objects(d, v, st);
+        if (!v->facet_offsets || !v->facets) throw Error(TJ_EINVAL, "tj_dataset_upload: null facet arrays");
         for (uint32_t li = 0; li < v->n_levels; ++li) {
             const uint64_t* fo = v->facet_offsets[li];
             const uint64_t entries = fo[d.n_voxels];
@@ -227,6 +291,7 @@ int tj_dataset_upload(tj_ctx* ctx, const tj_dataset_view* v, tj_dataset** out) {
                 if (fo[x + 1] < fo[x]) throw Error(TJ_EINVAL, "tj_dataset_upload: facet_offsets not monotone");
             upload(d.facet_offsets[li], fo, d.n_voxels + 1, st);
             upload(d.facets[li], v->facets[li], entries * TJ_FACET_STRIDE, st);
+            d.level_entries.push_back(entries);
             d.bytes += (d.n_voxels + 1) * 8 + entries * TJ_FACET_STRIDE * 8;
         }
         TJ_CUDA(cudaStreamSynchronize(st));
@@ -238,8 +303,91 @@ int tj_dataset_upload(tj_ctx* ctx, const tj_dataset_view* v, tj_dataset** out) {
 void tj_dataset_free(tj_dataset* ds) {
     if (!ds) return;
     cudaSetDevice(ds->ctx->device);
+    if (ds->d.gate && ds->d.gate->copy) cudaStreamSynchronize(ds->d.gate->copy);
     AllocStreamScope scope(ds->ctx->stream);
     delete ds;
+}
+
+int tj_dataset_begin(tj_ctx* ctx, const tj_dataset_view* v, const uint64_t* n_vertices, const uint64_t* n_facets,
+                     tj_dataset** out) {
+    if (!ctx || !v || !out || !n_vertices || !n_facets) return TJ_EINVAL;
+    *out = nullptr;
+    auto ds = std::make_unique<tj_dataset>();
+    ds->ctx = ctx;
+    const int rc = guarded(ctx, [&] {
+        DatasetDev& d = ds->d;
+        cudaStream_t st = ctx->stream;
+        upload_objects(d, v, st);
+        auto gate = std::make_shared<LevelGate>();
+        gate->device = ctx->device;
+        gate->state.assign(v->n_levels, LevelGate::kPending);
+        gate->ev.assign(v->n_levels, nullptr);
+        TJ_CUDA(cudaStreamCreateWithFlags(&gate->copy, cudaStreamNonBlocking));
+        for (uint32_t li = 0; li < v->n_levels; ++li) {
+            TJ_CUDA(cudaEventCreateWithFlags(&gate->ev[li], cudaEventDisableTiming));
+            const uint64_t* fo = v->facet_offsets ? v->facet_offsets[li] : nullptr;
+            if (!fo) throw Error(TJ_EINVAL, "tj_dataset_begin: null facet_offsets");
+            const uint64_t entries = fo[d.n_voxels];
+            for (uint64_t x = 0; x < d.n_voxels; ++x)
+                if (fo[x + 1] < fo[x]) throw Error(TJ_EINVAL, "tj_dataset_begin: facet_offsets not monotone");
+            upload(d.facet_offsets[li], fo, d.n_voxels + 1, st);
+            d.facets[li].alloc(std::max<uint64_t>(entries, 1) * TJ_FACET_STRIDE);
+            d.level_entries.push_back(entries);
+            d.level_vertices.push_back(n_vertices[li]);
+            d.level_facets.push_back(n_facets[li]);
+            d.bytes += (d.n_voxels + 1) * 8 + entries * TJ_FACET_STRIDE * 8;
+        }
+        d.gate = std::move(gate);
+        TJ_CUDA(cudaStreamSynchronize(st));
+    });
+    if (rc == TJ_OK) *out = ds.release();
+    return rc;
+}
+
+int tj_dataset_put_level(tj_dataset* ds, uint32_t slot, const tj_level_mesh_view* lv) {
+    if (!ds || !ds->d.gate || slot >= ds->d.levels.size()) return TJ_EINVAL;
+    LevelGate& g = *ds->d.gate;
+    auto set_state = [&](int s) {
+        {
+            std::lock_guard<std::mutex> lk(g.mu);
+            g.state[slot] = s;
+        }
+        g.cv.notify_all();
+    };
+    if (!lv) {
+        set_state(LevelGate::kFailed);
+        return TJ_OK;
+    }
+    tj_ctx* ctx = ds->ctx;
+    const int rc = guarded(nullptr, [&] {
+        TJ_CUDA(cudaSetDevice(ctx->device));
+        AllocStreamScope scope(g.copy);
+        DatasetDev& d = ds->d;
+        if (lv->n_vertices != d.level_vertices[slot] || lv->n_facets != d.level_facets[slot])
+            throw Error(TJ_EINVAL, "tj_dataset_put_level: level sizes differ from tj_dataset_begin");
+        const uint64_t used = d.level_entries[slot];
+        DevBuf<double> verts, hd, ph;
+        DevBuf<uint32_t> tris, vf;
+        upload(verts, lv->vertices, lv->n_vertices * 3, g.copy);
+        upload(tris, lv->tris, lv->n_facets * 3, g.copy);
+        upload(hd, lv->hd, lv->n_facets, g.copy);
+        upload(ph, lv->ph, lv->n_facets, g.copy);
+        upload(vf, lv->voxel_facets, used, g.copy);
+        launch_expand_level(verts.p, tris.p, hd.p, ph.p, vf.p, used, d.facets[slot].p, ctx->ws.num_sms, g.copy);
+        TJ_CUDA(cudaEventRecord(g.ev[slot], g.copy));
+    });
+    set_state(rc == TJ_OK ? LevelGate::kQueued : LevelGate::kFailed);
+    if (rc != TJ_OK) set_ctx_error(ctx, tj_global_last_error());
+    return rc;
+}
+
+int tj_dataset_sync(tj_dataset* ds) {
+    if (!ds) return TJ_EINVAL;
+    if (!ds->d.gate) return TJ_OK;
+    return guarded(nullptr, [&] {
+        TJ_CUDA(cudaSetDevice(ds->ctx->device));
+        TJ_CUDA(cudaStreamSynchronize(ds->d.gate->copy));
+    });
 }
 
 uint64_t tj_dataset_device_bytes(const tj_dataset* ds) { return ds ? ds->d.bytes : 0; }
@@ -363,7 +511,9 @@ int tj_join(tj_ctx* ctx, const tj_dataset* Rh, const tj_dataset* Sh, const tj_jo
         check_levels(R, sp);
         check_levels(S, sp);
         uint64_t n_active = compact_active(ws, cs, active, vo.survivors, st);
-        RefineLoopOut ro = refine_loop_dev(ws, R, S, cs, active, n_active, sp, knn, tau, err.p, tsink, st);
+        const bool decision = sp.type == TJ_INTERSECT && !tsink && !(sp.flags & TJ_FLAG_EXACT_INTERVALS);
+        out->decision_mode = decision ? 1 : 0;
+        RefineLoopOut ro = refine_loop_dev(ws, R, S, cs, active, n_active, sp, knn, tau, decision, err.p, tsink, st);
         if (knn) {
             knn_finalize_dev(ws, cs, sp.k, st);
         } else {
@@ -388,6 +538,7 @@ int tj_join(tj_ctx* ctx, const tj_dataset* Rh, const tj_dataset* Sh, const tj_jo
             out->level_facets_dropped[i] = ro.levels[i].facets_dropped;
             out->level_ms[i] = ro.levels[i].ms;
             out->level_kernel_ms[i] = ro.levels[i].kernel_ms;
+            out->level_wait_ms[i] = ro.levels[i].wait_ms;
         }
         out->refine_chunks = ro.chunks;
 
@@ -445,7 +596,7 @@ int tj_refine_batch(tj_ctx* ctx, uint64_t n_tris, const double* tris, const doub
         src.r_facets = f.p;
         src.s_facets = f.p;
         DevBuf<float4> scr(std::max<uint64_t>(n_tris, 1) * 7);
-        refine_prep(f.p, n_tris, scr.p, ctx->ws.num_sms, st);
+        refine_prep(f.p, n_tris, scr.p, nullptr, ctx->ws.num_sms, st);
         src.r_box = src.s_box = scr.p;
         src.r_geo = src.s_geo = scr.p + 3 * n_tris;
         const int cull = (flags & TJ_FLAG_NO_CULL) ? 0 : 1;

@@ -59,12 +59,14 @@ struct Workspace {
     DevBuf<uint64_t> u64a;
     std::unique_ptr<RefineQueueStore> queue; // refinement pair queues, grow-only, per context
     DevBuf<float4> screen_r, screen_s;       // per-level FP32 screening records, grow-only
+    DevBuf<unsigned> level_agg;              // per-level record aggregates (RefineSource::agg)
     void release() {
         temp.release();
         u64a.release();
         queue.reset();
         screen_r.release();
         screen_s.release();
+        level_agg.release();
     }
 };
 
@@ -129,7 +131,7 @@ void knn_finalize_dev(Workspace& ws, CandDevStore& cs, uint32_t k, cudaStream_t 
 struct LevelStats {
     uint32_t level;
     uint64_t vps, facet_pairs, evaluated, tested, screened, verified, vps_skipped, facets_dropped;
-    double ms, kernel_ms;
+    double ms, kernel_ms, wait_ms;
 };
 struct RefineLoopOut {
     std::vector<LevelStats> levels;
@@ -138,6 +140,6 @@ struct RefineLoopOut {
 struct TraceSink; // host-side trace forwarding (engine.cu)
 RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetDev& S, CandDevStore& cs,
                               DevBuf<ActiveVpDev>& active, uint64_t n_active, const tj_join_spec& spec, bool knn,
-                              double tau, DevError* err, TraceSink* trace, cudaStream_t st);
+                              double tau, bool decision, DevError* err, TraceSink* trace, cudaStream_t st);
 
 } // namespace tjx

@@ -242,6 +242,159 @@ std::unique_ptr<PackedDataset> pack_dataset(const PreparedDataset& ds, ThreadPoo
     return p;
 }
 
+namespace {
+// fn(begin, end) over [0, n) in ~8 contiguous blocks per worker (one pool job per block).
+void for_blocks(ThreadPool& pool, size_t n, const std::function<void(size_t, size_t)>& fn) {
+    if (n == 0) return;
+    const auto ranges = partition_ranges(n, std::max<size_t>(1, size_t{pool.size()} * 8));
+    pool.parallel_jobs(ranges.size(), [&](size_t j) { fn(ranges[j].first, ranges[j].second); });
+}
+template <class T>
+T* as(PinnedBuf& b) {
+    return reinterpret_cast<T*>(b.data());
+}
+} // namespace
+
+uint64_t PackedHeader::bytes() const {
+    uint64_t b = (mbb.size() + anchor.size() + voxel_box.size() + voxel_anchor.size() + voxel_offsets.size()) * 8;
+    for (const auto& v : facet_offsets) b += v.size() * 8;
+    return b;
+}
+
+std::unique_ptr<PackedHeader> pack_header(const PreparedDataset& ds, ThreadPool& pool) {
+    auto h = std::make_unique<PackedHeader>();
+    const size_t no = ds.objects.size();
+    const size_t nl = ds.lod_schedule.size();
+    h->n_objects = static_cast<uint32_t>(no);
+    h->levels.assign(ds.lod_schedule.begin(), ds.lod_schedule.end());
+    h->mbb.resize(6 * no);
+    h->anchor.resize(3 * no);
+    h->voxel_offsets.assign(no + 1, 0);
+    h->vert_base.assign(nl, std::vector<uint64_t>(no + 1, 0));
+    h->facet_base.assign(nl, std::vector<uint64_t>(no + 1, 0));
+    for (size_t o = 0; o < no; ++o) {
+        const PreparedObject& obj = ds.objects[o];
+        if (obj.ladder.levels.size() != nl || obj.voxels.facets_per_level.size() != nl)
+            throw std::invalid_argument("trijoin: object level count does not match the lod schedule");
+        h->voxel_offsets[o + 1] = h->voxel_offsets[o] + obj.voxels.voxel_count();
+        for (size_t li = 0; li < nl; ++li) {
+            const Mesh& m = obj.ladder.levels[li].mesh;
+            h->vert_base[li][o + 1] = h->vert_base[li][o] + m.vertices.size();
+            h->facet_base[li][o + 1] = h->facet_base[li][o] + m.facets.size();
+        }
+    }
+    const uint64_t nv = h->voxel_offsets[no];
+    for (size_t li = 0; li < nl; ++li) {
+        h->n_vertices.push_back(h->vert_base[li][no]);
+        h->n_facets.push_back(h->facet_base[li][no]);
+        if (h->n_vertices.back() >> 32 || h->n_facets.back() >> 32)
+            throw std::invalid_argument("trijoin: more than 2^32 vertices or facets in one level");
+    }
+    h->voxel_box.resize(6 * nv);
+    h->voxel_anchor.resize(3 * nv);
+    h->facet_offsets.assign(nl, std::vector<uint64_t>(nv + 1, 0));
+    for_blocks(pool, no, [&](size_t b, size_t e) {
+        for (size_t o = b; o < e; ++o) {
+            const PreparedObject& obj = ds.objects[o];
+            const double m[6] = {obj.mbb.min.x, obj.mbb.min.y, obj.mbb.min.z, obj.mbb.max.x, obj.mbb.max.y, obj.mbb.max.z};
+            std::memcpy(&h->mbb[6 * o], m, sizeof(m));
+            h->anchor[3 * o] = obj.anchor.x;
+            h->anchor[3 * o + 1] = obj.anchor.y;
+            h->anchor[3 * o + 2] = obj.anchor.z;
+            const uint64_t v0 = h->voxel_offsets[o];
+            const VoxelSet& vs = obj.voxels;
+            for (uint32_t v = 0; v < vs.voxel_count(); ++v) {
+                const Aabb& bx = vs.boxes[v];
+                const double bb[6] = {bx.min.x, bx.min.y, bx.min.z, bx.max.x, bx.max.y, bx.max.z};
+                std::memcpy(&h->voxel_box[6 * (v0 + v)], bb, sizeof(bb));
+                h->voxel_anchor[3 * (v0 + v)] = vs.anchors[v].x;
+                h->voxel_anchor[3 * (v0 + v) + 1] = vs.anchors[v].y;
+                h->voxel_anchor[3 * (v0 + v) + 2] = vs.anchors[v].z;
+                for (size_t li = 0; li < nl; ++li)
+                    h->facet_offsets[li][v0 + v + 1] = vs.facets_per_level[li][v].size();
+            }
+        }
+    });
+    for (size_t li = 0; li < nl; ++li) {
+        auto& fo = h->facet_offsets[li];
+        for (uint64_t v = 0; v < nv; ++v) fo[v + 1] += fo[v];
+    }
+    h->fo_ptrs.resize(nl);
+    for (size_t li = 0; li < nl; ++li) h->fo_ptrs[li] = h->facet_offsets[li].data();
+    tj_dataset_view& v = h->view;
+    v.n_objects = h->n_objects;
+    v.n_levels = static_cast<uint32_t>(nl);
+    v.levels = h->levels.data();
+    v.mbb = h->mbb.data();
+    v.anchor = h->anchor.data();
+    v.voxel_offsets = h->voxel_offsets.data();
+    v.voxel_box = h->voxel_box.data();
+    v.voxel_anchor = h->voxel_anchor.data();
+    v.facet_offsets = h->fo_ptrs.data();
+    v.facets = nullptr;
+    return h;
+}
+
+std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& ds, const PackedHeader& h, size_t li, ThreadPool& pool) {
+    auto p = std::make_unique<PackedLevel>();
+    const size_t no = ds.objects.size();
+    const uint64_t nvert = h.n_vertices[li], nfac = h.n_facets[li];
+    const uint64_t entries = h.facet_offsets[li].back();
+    p->verts.resize(std::max<uint64_t>(3 * nvert, 1));
+    p->tris.resize(std::max<uint64_t>((3 * nfac + 1) / 2, 1));
+    p->hd.resize(std::max<uint64_t>(nfac, 1));
+    p->ph.resize(std::max<uint64_t>(nfac, 1));
+    p->vf.resize(std::max<uint64_t>((entries + 1) / 2, 1));
+    double* verts = p->verts.data();
+    uint32_t* tris = as<uint32_t>(p->tris);
+    double* hd = p->hd.data();
+    double* ph = p->ph.data();
+    uint32_t* vf = as<uint32_t>(p->vf);
+    std::atomic<bool> bad{false};
+    for_blocks(pool, no, [&](size_t b, size_t e) {
+        for (size_t o = b; o < e && !bad.load(std::memory_order_relaxed); ++o) {
+            const PreparedObject& obj = ds.objects[o];
+            const LodMesh& lod = obj.ladder.levels[li];
+            const uint64_t vb = h.vert_base[li][o], fb = h.facet_base[li][o];
+            const size_t n_v = lod.mesh.vertices.size(), n_f = lod.mesh.facets.size();
+            static_assert(sizeof(Point3) == 3 * sizeof(double), "Point3 must be three packed doubles");
+            if (n_v) std::memcpy(verts + 3 * vb, lod.mesh.vertices.data(), n_v * sizeof(Point3));
+            for (size_t f = 0; f < n_f; ++f) {
+                const auto& t = lod.mesh.facets[f];
+                if (t[0] >= n_v || t[1] >= n_v || t[2] >= n_v) bad = true;
+                tris[3 * (fb + f)] = static_cast<uint32_t>(vb + t[0]);
+                tris[3 * (fb + f) + 1] = static_cast<uint32_t>(vb + t[1]);
+                tris[3 * (fb + f) + 2] = static_cast<uint32_t>(vb + t[2]);
+            }
+            const size_t nh = std::min(n_f, lod.hd.size()), np = std::min(n_f, lod.ph.size());
+            if (nh) std::memcpy(hd + fb, lod.hd.data(), nh * sizeof(double));
+            if (np) std::memcpy(ph + fb, lod.ph.data(), np * sizeof(double));
+            for (size_t f = nh; f < n_f; ++f) hd[fb + f] = 0.0;
+            for (size_t f = np; f < n_f; ++f) ph[fb + f] = 0.0;
+            const size_t n_ok = std::min({n_f, lod.hd.size(), lod.ph.size()});
+            const VoxelSet& vs = obj.voxels;
+            const uint64_t v0 = h.voxel_offsets[o];
+            for (uint32_t v = 0; v < vs.voxel_count(); ++v) {
+                uint64_t x = h.facet_offsets[li][v0 + v];
+                for (uint32_t f : vs.facets_per_level[li][v]) {
+                    if (f >= n_ok) bad = true;
+                    vf[x++] = static_cast<uint32_t>(fb + f);
+                }
+            }
+        }
+    });
+    if (bad) throw std::invalid_argument("trijoin: voxel facet id out of range");
+    tj_level_mesh_view& v = p->view;
+    v.n_vertices = nvert;
+    v.n_facets = nfac;
+    v.vertices = verts;
+    v.tris = tris;
+    v.hd = hd;
+    v.ph = ph;
+    v.voxel_facets = vf;
+    return p;
+}
+
 } // namespace detail
 
 // ---------------------------------------------------------------- small API functions
@@ -356,7 +509,9 @@ std::string StageStats::to_json() const {
                        {"vp_pruned", s.vp_pruned},
                        {"facet_pairs", s.facet_pairs}});
     j["stages"] = std::move(arr);
-    j["b200"] = {{"pack_ms", pack_ms}, {"upload_ms", upload_ms}, {"device_ms", device_ms}, {"devices", devices}};
+    j["b200"] = {{"pack_ms", pack_ms}, {"upload_ms", upload_ms}, {"device_ms", device_ms},
+                 {"stream_wait_ms", stream_wait_ms}, {"h2d_bytes", h2d_bytes}, {"devices", devices},
+                 {"intervals", decision_mode ? "decision" : "exact"}};
     return j.dump(2);
 }
 
@@ -532,6 +687,7 @@ tj_join_spec to_c_spec(const JoinSpec& spec) {
     c.pipeline = spec.pipeline ? 1 : 0;
     c.flags = 0;
     if (const char* e = std::getenv("TRIJOIN_NO_CULL"); e && *e && *e != '0') c.flags |= TJ_FLAG_NO_CULL;
+    if (const char* e = std::getenv("TRIJOIN_EXACT_INTERVALS"); e && *e && *e != '0') c.flags |= TJ_FLAG_EXACT_INTERVALS;
     return c;
 }
 
@@ -548,56 +704,112 @@ JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const Jo
 
     const std::vector<int> devices = detail::join_devices();
     const bool self_join = &R == &S;
-    auto tp = Clock::now();
-    auto pr = detail::pack_dataset(R, pool);
-    std::unique_ptr<detail::PackedDataset> ps_own;
-    const detail::PackedDataset* ps = pr.get();
-    if (!self_join) {
-        ps_own = detail::pack_dataset(S, pool);
-        ps = ps_own.get();
-    }
-    out.stats.pack_ms = std::chrono::duration<double, std::milli>(Clock::now() - tp).count();
     const size_t G = (trace && (trace->on_interval || trace->on_vp_pruned)) ? 1 : devices.size();
     out.stats.devices = static_cast<uint32_t>(G);
+
+    // Streamed upload (tj_dataset_begin / _put_level): object + voxel arrays first, then
+    // each LOD level the join uses, coarsest first, packed on the host in the compact mesh
+    // form while the devices already run the filters and the coarser levels.
+    auto tp = Clock::now();
+    auto hr = detail::pack_header(R, pool);
+    std::unique_ptr<detail::PackedHeader> hs_own;
+    const detail::PackedHeader* hs = hr.get();
+    if (!self_join) {
+        hs_own = detail::pack_header(S, pool);
+        hs = hs_own.get();
+    }
+    double pack_ms = std::chrono::duration<double, std::milli>(Clock::now() - tp).count();
+    std::vector<std::unique_ptr<detail::PackedLevel>> staged; // outlives the dataset handles below
+    std::vector<detail::DatasetHandle> dr(G), dsh(G);
+    const auto tu = Clock::now();
+    for (size_t g = 0; g < G; ++g) {
+        tj_ctx* ctx = detail::device_context(devices[g]);
+        detail::check(tj_dataset_begin(ctx, &hr->view, hr->n_vertices.data(), hr->n_facets.data(), &dr[g].p), ctx);
+        out.stats.h2d_bytes += hr->bytes() + (self_join ? 0 : hs->bytes());
+        if (!self_join)
+            detail::check(tj_dataset_begin(ctx, &hs->view, hs->n_vertices.data(), hs->n_facets.data(), &dsh[g].p), ctx);
+    }
+    out.stats.upload_ms = std::chrono::duration<double, std::milli>(Clock::now() - tu).count();
+
     std::vector<detail::ResultHandle> results(G);
     std::vector<std::exception_ptr> errors(G);
-    std::vector<double> up_ms(G, 0.0), dev_ms(G, 0.0);
+    std::vector<double> dev_ms(G, 0.0);
     auto run_shard = [&](size_t g) {
         try {
             tj_ctx* ctx = detail::device_context(devices[g]);
-            const auto tu = Clock::now();
-            detail::DatasetHandle dr, ds_h;
-            detail::check(tj_dataset_upload(ctx, &pr->view, &dr.p), ctx);
-            const tj_dataset* dsp = dr.p;
-            if (!self_join) {
-                detail::check(tj_dataset_upload(ctx, &ps->view, &ds_h.p), ctx);
-                dsp = ds_h.p;
-            }
             const auto td = Clock::now();
-            up_ms[g] = std::chrono::duration<double, std::milli>(td - tu).count();
             tj_join_spec cs = to_c_spec(spec);
             cs.shard_index = static_cast<uint32_t>(g);
             cs.shard_count = static_cast<uint32_t>(G);
             cs.shard_block = 1024;
             TraceBridge bridge{trace};
             tj_trace tt{&bridge, &TraceBridge::interval, &TraceBridge::pruned};
-            detail::check(tj_join(ctx, dr.p, dsp, &cs, trace ? &tt : nullptr, &results[g].r), ctx);
+            detail::check(tj_join(ctx, dr[g].p, self_join ? dr[g].p : dsh[g].p, &cs, trace ? &tt : nullptr,
+                                  &results[g].r),
+                          ctx);
             dev_ms[g] = std::chrono::duration<double, std::milli>(Clock::now() - td).count();
         } catch (...) {
             errors[g] = std::current_exception();
         }
     };
-    if (G == 1) {
-        run_shard(0);
-    } else {
-        std::vector<std::thread> ts;
-        for (size_t g = 0; g < G; ++g) ts.emplace_back(run_shard, g);
-        for (auto& t : ts) t.join();
+    std::vector<std::thread> joins;
+    for (size_t g = 0; g < G; ++g) joins.emplace_back(run_shard, g);
+
+    // Producer: levels in join order; a level missing from a schedule is left to the join
+    // (EngineError from its level check). On failure every undelivered slot is released.
+    std::exception_ptr pack_error;
+    std::vector<std::vector<char>> put_r(G, std::vector<char>(R.lod_schedule.size(), 0));
+    std::vector<std::vector<char>> put_s(G, std::vector<char>(S.lod_schedule.size(), 0));
+    auto slot_of = [](const PreparedDataset& d, uint32_t level) -> int {
+        for (size_t i = 0; i < d.lod_schedule.size(); ++i)
+            if (d.lod_schedule[i] == static_cast<int>(level)) return static_cast<int>(i);
+        return -1;
+    };
+    try {
+        for (uint32_t level : spec.lods) {
+            for (int side = 0; side < (self_join ? 1 : 2); ++side) {
+                const PreparedDataset& D = side == 0 ? R : S;
+                const detail::PackedHeader& H = side == 0 ? *hr : *hs;
+                const int slot = slot_of(D, level);
+                if (slot < 0) continue;
+                const auto tl = Clock::now();
+                staged.push_back(detail::pack_level(D, H, static_cast<size_t>(slot), pool));
+                pack_ms += std::chrono::duration<double, std::milli>(Clock::now() - tl).count();
+                const tj_level_mesh_view& lv = staged.back()->view;
+                out.stats.h2d_bytes += G * (lv.n_vertices * 24 + lv.n_facets * 28 + H.facet_offsets[slot].back() * 4);
+                for (size_t g = 0; g < G; ++g) {
+                    tj_dataset* ds = side == 0 ? dr[g].p : dsh[g].p;
+                    auto& put = side == 0 ? put_r[g] : put_s[g];
+                    put[slot] = 1;
+                    detail::check(tj_dataset_put_level(ds, static_cast<uint32_t>(slot), &staged.back()->view),
+                                  detail::device_context(devices[g]));
+                }
+            }
+        }
+    } catch (...) {
+        pack_error = std::current_exception();
+        for (size_t g = 0; g < G; ++g) {
+            for (size_t i = 0; i < put_r[g].size(); ++i)
+                if (!put_r[g][i]) tj_dataset_put_level(dr[g].p, static_cast<uint32_t>(i), nullptr);
+            if (!self_join)
+                for (size_t i = 0; i < put_s[g].size(); ++i)
+                    if (!put_s[g][i]) tj_dataset_put_level(dsh[g].p, static_cast<uint32_t>(i), nullptr);
+        }
     }
+    for (auto& t : joins) t.join();
+    for (size_t g = 0; g < G; ++g) {
+        tj_dataset_sync(dr[g].p);
+        if (!self_join) tj_dataset_sync(dsh[g].p);
+    }
+    if (pack_error) std::rethrow_exception(pack_error);
     for (auto& e : errors)
         if (e) std::rethrow_exception(e);
-    out.stats.upload_ms = *std::max_element(up_ms.begin(), up_ms.end());
+    out.stats.pack_ms = pack_ms;
     out.stats.device_ms = *std::max_element(dev_ms.begin(), dev_ms.end());
+    for (const auto& h : results) {
+        for (uint32_t i = 0; i < h.r.n_levels_run; ++i) out.stats.stream_wait_ms += h.r.level_wait_ms[i];
+        out.stats.decision_mode = h.r.decision_mode != 0;
+    }
 
     // Merge shards: query r is owned by shard (r / 1024) % G; each shard's arrays cover
     // all queries with empty ranges for foreign ones.

@@ -45,6 +45,28 @@ struct PackedDataset {
 
 std::unique_ptr<PackedDataset> pack_dataset(const PreparedDataset& ds, ThreadPool& pool);
 
+// Streamed form (tj_dataset_begin / tj_dataset_put_level): the header holds the object and
+// voxel arrays, the per-level voxel CSR and the per-object vertex / facet bases; each level
+// is then packed on its own in the reference's compact mesh form.
+struct PackedHeader {
+    uint32_t n_objects = 0;
+    std::vector<int32_t> levels;
+    std::vector<double> mbb, anchor, voxel_box, voxel_anchor;
+    std::vector<uint64_t> voxel_offsets;
+    std::vector<std::vector<uint64_t>> facet_offsets;           // per level [nv+1]
+    std::vector<std::vector<uint64_t>> vert_base, facet_base;   // per level [n_objects+1]
+    std::vector<uint64_t> n_vertices, n_facets;                  // per level totals
+    std::vector<const uint64_t*> fo_ptrs;
+    tj_dataset_view view{};
+    uint64_t bytes() const; // H2D bytes of tj_dataset_begin
+};
+struct PackedLevel {
+    PinnedBuf verts, tris, hd, ph, vf; // tris / vf hold uint32 pairs per double slot
+    tj_level_mesh_view view{};
+};
+std::unique_ptr<PackedHeader> pack_header(const PreparedDataset& ds, ThreadPool& pool);
+std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& ds, const PackedHeader& h, size_t li, ThreadPool& pool);
+
 // Lazily created context per CUDA device, destroyed at process exit.
 tj_ctx* device_context(int device);
 // Devices used by run_join: $TRIJOIN_DEVICES (comma list) or {0}.

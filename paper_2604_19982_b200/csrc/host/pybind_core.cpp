@@ -123,6 +123,7 @@ public:
         d["voxel_ms"] = r.voxel_ms;
         d["refine_ms"] = r.refine_ms;
         d["total_ms"] = r.total_ms;
+        d["decision_mode"] = r.decision_mode;
         py::list levels;
         for (uint32_t i = 0; i < r.n_levels_run; ++i) {
             py::dict l;

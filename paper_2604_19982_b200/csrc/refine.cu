@@ -80,17 +80,34 @@ __device__ __forceinline__ void warp_argmin(float& v, uint32_t& idx) {
     }
 }
 
-__global__ void k_prep(const double* __restrict__ facets, uint64_t n, float4* __restrict__ out) {
+__global__ void k_prep(const double* __restrict__ facets, uint64_t n, float4* __restrict__ out, unsigned* agg) {
     float4* box = out;
     float4* geo = out + kBoxF4 * n;
+    float hdmin = __int_as_float(0x7f800000), lmax = 0.f, mmax = 0.f;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         float r[kCS];
         make_screen(facets + i * 12, r);
+        hdmin = fminf(hdmin, r[7]);
+        lmax = fmaxf(lmax, fabsf(r[3]));
+        mmax = fmaxf(mmax, r[27]);
 #pragma unroll
         for (int k = 0; k < kBoxF4; ++k) box[i * kBoxF4 + k] = make_float4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
 #pragma unroll
         for (int k = 0; k < kGeoF4; ++k)
             geo[i * kGeoF4 + k] = make_float4(r[12 + 4 * k], r[13 + 4 * k], r[14 + 4 * k], r[15 + 4 * k]);
+    }
+    if (agg) { // non-negative floats order like their bit patterns
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            hdmin = fminf(hdmin, __shfl_xor_sync(0xffffffffu, hdmin, o));
+            lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+            mmax = fmaxf(mmax, __shfl_xor_sync(0xffffffffu, mmax, o));
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin(agg, __float_as_uint(fmaxf(hdmin, 0.f)));
+            atomicMax(agg + 1, __float_as_uint(lmax));
+            atomicMax(agg + 2, __float_as_uint(mmax));
+        }
     }
 }
 
@@ -243,6 +260,16 @@ __global__ void __launch_bounds__(256, 2) k_screen(RefineSource src, uint64_t vp
     ScreenSmem& sm = reinterpret_cast<ScreenSmem*>(smem_raw)[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
     uint32_t tested = 0, sat_tests = 0, verified = 0, vps_skipped = 0, dropped = 0; // per-lane (< 2^32)
+    // decision mode: when every facet pair has hd_i + hd_j > 1e-5 (L_i + L_j) + 1e-12 (M_i + M_j),
+    // no ub_ij can be 0 at this level (B + hd_i + hd_j >= tiny + delta for every pair), so
+    // the ub side of every op is settled (the level's aggregates, k_prep)
+    bool ub_level_settled = false;
+    if (cull == 2 && src.agg) {
+        const float hd2 = __fadd_rd(__uint_as_float(src.agg[0]), __uint_as_float(src.agg[3]));
+        const float l2 = __fadd_ru(__uint_as_float(src.agg[1]), __uint_as_float(src.agg[4]));
+        const float m2 = __fadd_ru(__uint_as_float(src.agg[2]), __uint_as_float(src.agg[5]));
+        ub_level_settled = hd2 > __fadd_ru(__fadd_ru(__fmul_ru(1e-5f, l2), __fmul_ru(1e-12f, m2)), 1e-30f);
+    }
     for (;;) {
         unsigned long long vp = 0;
         if (lane == 0) vp = atomicAdd(work, 1ull);
@@ -253,7 +280,15 @@ __global__ void __launch_bounds__(256, 2) k_screen(RefineSource src, uint64_t vp
         const double tlb = bits_to_double(__ldcg(op_lb_bits + d.op));
         double tub = bits_to_double(__ldcg(op_ub_bits + d.op));
         tub = tub < d.iv_ub ? tub : d.iv_ub;
-        const Thresh th{ru(tlb), ru(tub), tlb <= d.iv_lb};
+        Thresh th{ru(tlb), ru(tub), tlb <= d.iv_lb};
+        if (cull == 2) {
+            // decision mode (intersection, tau = 0): only "is the minimum 0?" matters on
+            // either side; a pair surely positive on a side cannot change that side's answer
+            constexpr float kTiny = 1e-30f;
+            th.lb_sat = tlb == 0.0;
+            th.lb_u = th.lb_sat ? 0.f : kTiny;
+            th.ub_u = tub == 0.0 || ub_level_settled ? 0.f : kTiny;
+        }
         // nothing can change lb' or ub': the whole voxel pair is irrelevant
         if (cull && (th.lb_sat || th.lb_u == 0.f) && th.ub_u == 0.f) continue;
         // hierarchical screens (voxel pair, rows, columns) only where they can pay off
@@ -308,27 +343,27 @@ __global__ void __launch_bounds__(256, 2) k_screen(RefineSource src, uint64_t vp
                             }
                             dl = __fadd_ru(__fmul_ru(2e-5f, Lm), __fmul_ru(2e-12f, Mm));
                         }
-                        if (lane < rcnt) { // per-row thresholds of the stage-1 pair test (box_cannot_improve)
-                            const float ninf = __int_as_float(0xff800000);
-                            const bool lb_settled = th.lb_sat || th.lb_u == 0.f;
-                            sm.row_lb[lane] = lb_settled ? ninf : __fadd_ru(__fadd_ru(th.lb_u, dl), sm.rc[lane * kCS + 11]);
-                            sm.row_ub[lane] = th.ub_u == 0.f ? ninf : __fsub_ru(__fadd_ru(th.ub_u, dl), sm.rc[lane * kCS + 7]);
-                        }
-                        __syncwarp();
-                        const int npairs = rcnt * scnt;
-                        const int step_i = 32 / scnt, step_j = 32 - (32 / scnt) * scnt; // t += 32 in (i, j)
-                        int bi = lane / scnt, bj = lane - (lane / scnt) * scnt;
+                        // Stage 1, register-blocked: lane -> r facet i = lane / P (its record in
+                        // registers) and s facets j = jj, jj + P, ... (shared-memory reads that
+                        // the P-lane groups share as broadcasts); P = lanes per r facet.
+                        const int P = rcnt >= 32 ? 1 : 32 / rcnt;
+                        const int bi = min(lane / P, rcnt - 1), jj = lane - (lane / P) * P;
+                        const bool row_on = lane / P < rcnt;
+                        const RowRec ar = load_row(sm.rc + bi * kCS);
+                        const bool lb_settled = th.lb_sat || th.lb_u == 0.f;
+                        const float ninf = __int_as_float(0xff800000);
+                        // per-row thresholds of the stage-1 pair test (box_cannot_improve)
+                        const float rlb = lb_settled ? ninf : __fadd_ru(__fadd_ru(th.lb_u, dl), ar.ph);
+                        const float rub = th.ub_u == 0.f ? ninf : __fsub_ru(__fadd_ru(th.ub_u, dl), ar.hd);
+                        const int iters = (scnt - jj + P - 1) / P; // this lane's s facets
+                        const int max_iters = (scnt + P - 1) / P;
                         int nq = 0;
-                        for (int t0 = 0;; t0 += 32) {
-                            if (t0 < npairs) {
-                                const int t = t0 + lane;
+                        for (int t = 0;; ++t) {
+                            if (t < max_iters) {
+                                const int bj = jj + t * P;
                                 bool need = false;
-                                if (t < npairs) {
-                                    const float* a = sm.rc + bi * kCS;
-                                    const float* b = sm.sc + bj * kCS;
-                                    const float g2 = box_gap2_lb(a, b);
-                                    need = !cull || !box_cannot_improve(g2, sm.row_lb[bi], sm.row_ub[bi], b) ||
-                                           skip_mask(__fmul_rd(sqrtf(g2), 1.0f - 0x1p-20f), a, b) != 0;
+                                if (row_on && t < iters) {
+                                    need = !cull || stage1_need_rr(ar, sm.rc + bi * kCS, sm.sc + bj * kCS, rlb, rub);
                                     ++tested;
                                 }
                                 if (!cull) {
@@ -339,11 +374,8 @@ __global__ void __launch_bounds__(256, 2) k_screen(RefineSource src, uint64_t vp
                                     if (need) sm.q[nq + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)((bi << 5) | bj);
                                     nq += __popc(bal);
                                 }
-                                bj += step_j;
-                                bi += step_i;
-                                if (bj >= scnt) { bj -= scnt; ++bi; }
                             }
-                            const bool last = t0 + 32 >= npairs;
+                            const bool last = t + 1 >= max_iters;
                             if (nq >= 32 || (last && nq > 0)) { // second stage on up to 32 queued pairs
                                 const int n = min(nq, 32);
                                 __syncwarp();
@@ -452,11 +484,11 @@ inline int warp_grid(uint64_t warps, int num_sms, int per_sm) {
 
 } // namespace
 
-void refine_prep(const double* facets, uint64_t n, float4* out, int num_sms, cudaStream_t st) {
+void refine_prep(const double* facets, uint64_t n, float4* out, unsigned* agg, int num_sms, cudaStream_t st) {
     if (!n) return;
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, (uint64_t)num_sms * 16));
     count_launch();
-    k_prep<<<grid, 256, 0, st>>>(facets, n, out);
+    k_prep<<<grid, 256, 0, st>>>(facets, n, out, agg);
     TJ_CUDA(cudaGetLastError());
 }
 

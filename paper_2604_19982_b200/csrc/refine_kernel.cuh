@@ -76,8 +76,6 @@ struct SegAgg {
 struct __align__(16) ScreenSmem {
     float rc[kRT * kCS];
     float sc[kST * kCS];
-    float row_lb[kRT]; // per r facet of the tile: T_lb + delta0 + ph_i (or -inf: lb side settled)
-    float row_ub[kRT]; // per r facet of the tile: T_ub + delta0 - hd_i (or -inf: ub side settled)
     uint16_t q[kQueue];
     uint16_t rl[kCap]; // surviving r facets of the current raw chunk (offsets in the chunk)
     uint16_t sl[kCap]; // surviving s facets
@@ -297,6 +295,65 @@ __device__ __forceinline__ bool stage1_need(const float4& a0, const float4& a1, 
     const float B = __fmul_rd(sqrtf(g2), 1.0f - 0x1p-20f);
     const bool shapes = a0.w >= 0.f && b0.w >= 0.f && !(B > 1e3f * fminf(a0.w, b0.w));
     return !(lb_ok && ub_ok && shapes);
+}
+
+// The r-side box of the register-blocked stage-1 loop (floats 0-7 and 11 of a screening
+// record, held in registers by the lane that owns the r facet).
+struct RowRec {
+    float lo[3], hi[3], L, hd, ph;
+};
+
+__device__ __forceinline__ RowRec load_row(const float* a) {
+    RowRec r;
+    const float4 p0 = *reinterpret_cast<const float4*>(a), p1 = *reinterpret_cast<const float4*>(a + 4);
+    r.lo[0] = p0.x; r.lo[1] = p0.y; r.lo[2] = p0.z; r.L = p0.w;
+    r.hi[0] = p1.x; r.hi[1] = p1.y; r.hi[2] = p1.z; r.hd = p1.w;
+    r.ph = a[11];
+    return r;
+}
+
+// |u . v| < 1e-3 for unit vectors (a conditioning cutoff; FMA only sharpens the dot).
+__device__ __forceinline__ bool ill_cond(float ux, float uy, float uz, float vx, float vy, float vz) {
+    return fabsf(__fmaf_rn(ux, vx, __fmaf_rn(uy, vy, __fmul_rn(uz, vz)))) < 1e-3f;
+}
+
+// Stage-1 test of the screen pass with the r record in registers and the s record b in
+// shared memory: true iff the pair must go to stage 2. Same decision as
+//   !box_cannot_improve(g2, rlb, rub, b) || skip_mask(B, a, b) != 0.
+__device__ __forceinline__ bool stage1_need_rr(const RowRec& a, const float* as, const float* b, float rlb, float rub) {
+    const float4 b0 = *reinterpret_cast<const float4*>(b), b1 = *reinterpret_cast<const float4*>(b + 4);
+    const float4 b2 = *reinterpret_cast<const float4*>(b + 8);
+    float g2;
+    {
+        const float gx = fmaxf(0.f, fmaxf(__fsub_rd(b0.x, a.hi[0]), __fsub_rd(a.lo[0], b1.x)));
+        const float gy = fmaxf(0.f, fmaxf(__fsub_rd(b0.y, a.hi[1]), __fsub_rd(a.lo[1], b1.y)));
+        const float gz = fmaxf(0.f, fmaxf(__fsub_rd(b0.z, a.hi[2]), __fsub_rd(a.lo[2], b1.z)));
+        g2 = __fadd_rd(__fadd_rd(__fmul_rd(gx, gx), __fmul_rd(gy, gy)), __fmul_rd(gz, gz));
+    }
+    // box_cannot_improve
+    constexpr float kInvC = 1.0f / (1.0f - 1e-5f) * (1.0f + 0x1p-20f);
+    const float xl = __fadd_ru(rlb, b2.w);
+    const float yu = __fsub_ru(rub, b1.w);
+    const float xs = __fmul_ru(xl, kInvC), ys = __fmul_ru(yu, kInvC);
+    const bool lb_ok = xl <= 0.f || g2 >= __fmul_ru(xs, xs);
+    const bool ub_ok = yu <= 0.f || g2 >= __fmul_ru(ys, ys);
+    if (!(lb_ok && ub_ok)) return true;
+    // skip_mask: shapes, 1e3 L range, far branch, conditioning
+    if (a.L < 0.f || b0.w < 0.f) return true;
+    const float B = __fmul_rd(sqrtf(g2), 1.0f - 0x1p-20f);
+    if (B > 1e3f * fminf(a.L, b0.w)) return true;
+    if (B > 2.f * (a.L + b0.w)) return false;
+    // near pair: the edge / plane conditioning of skip_mask (records read from shared memory)
+    const float4 b3 = *reinterpret_cast<const float4*>(b + 12), b4 = *reinterpret_cast<const float4*>(b + 16);
+    const float b20 = b[20];
+    const float4 a2 = *reinterpret_cast<const float4*>(as + 8), a3 = *reinterpret_cast<const float4*>(as + 12);
+    const float4 a4 = *reinterpret_cast<const float4*>(as + 16);
+    const float a20 = as[20];
+    bool ill = ill_cond(a3.x, a3.y, a3.z, b2.x, b2.y, b2.z) || ill_cond(a3.w, a4.x, a4.y, b2.x, b2.y, b2.z) ||
+               ill_cond(a4.z, a4.w, a20, b2.x, b2.y, b2.z);
+    ill = ill || ill_cond(b3.x, b3.y, b3.z, a2.x, a2.y, a2.z) || ill_cond(b3.w, b4.x, b4.y, a2.x, a2.y, a2.z) ||
+          ill_cond(b4.z, b4.w, b20, a2.x, a2.y, a2.z);
+    return ill;
 }
 
 // Shape / range eligibility for a skip and the mask of ill-conditioned edge/plane

@@ -44,7 +44,7 @@ __global__ void k_facet_pairs(const ActiveVpDev* __restrict__ act, uint64_t n, c
 
 __global__ void k_aggregate(CandDev c, uint64_t n, const unsigned long long* __restrict__ lbb,
                             const unsigned long long* __restrict__ ubb, int prune, double tau, int16_t stage,
-                            uint8_t* __restrict__ updated, DevError* err) {
+                            int decision, uint8_t* __restrict__ updated, DevError* err) {
     for (uint64_t op = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; op < n; op += (uint64_t)gridDim.x * blockDim.x) {
         if (updated) updated[op] = 0;
         if (c.status[op] != TJ_UNDECIDED) continue;
@@ -52,8 +52,11 @@ __global__ void k_aggregate(CandDev c, uint64_t n, const unsigned long long* __r
         const double mub = __longlong_as_double((long long)ubb[op]);
         if (!(mlb < dinf())) continue; // every voxel pair empty at this level (or op not active)
         double lb = c.lb[op], ub = c.ub[op];
-        lb = (lb < mlb) ? mlb : lb;
         ub = (mub < ub) ? mub : ub;
+        // decision mode: a positive mlb is only known to be positive (pairs that could lower
+        // it were skipped); clamping it to ub keeps "lb > 0" and never trips the crossing check
+        const double mlb_d = (decision && mlb > 0.0 && ub < mlb) ? ub : mlb;
+        lb = (lb < mlb_d) ? mlb_d : lb;
         if (lb > ub) {
             if (lb - ub > 1e-9) {
                 atomicMin(&err->op, (uint32_t)op);
@@ -127,7 +130,7 @@ uint64_t compact_active(Workspace& ws, const CandDevStore& cs, DevBuf<ActiveVpDe
 
 RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetDev& S, CandDevStore& cs,
                               DevBuf<ActiveVpDev>& active, uint64_t n_active, const tj_join_spec& spec, bool knn,
-                              double tau, DevError* err, TraceSink* trace, cudaStream_t st) {
+                              double tau, bool decision, DevError* err, TraceSink* trace, cudaStream_t st) {
     using Clock = std::chrono::steady_clock;
     RefineLoopOut out;
     const uint64_t n = cs.n;
@@ -159,6 +162,9 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
             count_launch();
             k_facet_pairs<<<grid_for(n_active, 256, ws.num_sms), 256, 0, st>>>(
                 active.p, n_active, R.facet_offsets[sr].p, S.facet_offsets[ss].p, counters.p + 2);
+            // streamed datasets: this level's facets may still be in flight
+            ls.wait_ms = level_ready(R, sr, st);
+            if (&S != &R) ls.wait_ms += level_ready(S, ss, st);
             TJ_CUDA(cudaEventRecord(e0, st));
             RefineSource src{};
             src.active = active.p;
@@ -168,23 +174,29 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
             src.cand_ub = cs.ub.p;
             src.r_facets = R.facets[sr].p;
             src.s_facets = S.facets[ss].p;
-            {   // FP32 screening records of this level's facets, once per facet
-                const uint64_t nr = R.facets[sr].n / 12, ns = S.facets[ss].n / 12;
+            {   // FP32 screening records of this level's facets, once per facet, + their aggregates
+                const uint64_t nr = R.level_entries[sr], ns = S.level_entries[ss];
+                ws.level_agg.reserve(8);
+                const unsigned init[8] = {0x7f800000u, 0u, 0u, 0x7f800000u, 0u, 0u, 0u, 0u};
+                TJ_CUDA(cudaMemcpyAsync(ws.level_agg.p, init, sizeof(init), cudaMemcpyHostToDevice, st));
+                src.agg = ws.level_agg.p;
                 ws.screen_r.reserve(std::max<uint64_t>(nr * 7, 1));
-                refine_prep(R.facets[sr].p, nr, ws.screen_r.p, ws.num_sms, st);
+                refine_prep(R.facets[sr].p, nr, ws.screen_r.p, ws.level_agg.p, ws.num_sms, st);
                 src.r_box = ws.screen_r.p;
                 src.r_geo = ws.screen_r.p + 3 * nr;
                 if (S.facets[ss].p == R.facets[sr].p) {
                     src.s_box = src.r_box;
                     src.s_geo = src.r_geo;
+                    TJ_CUDA(cudaMemcpyAsync(ws.level_agg.p + 3, ws.level_agg.p, 12, cudaMemcpyDeviceToDevice, st));
                 } else {
                     ws.screen_s.reserve(std::max<uint64_t>(ns * 7, 1));
-                    refine_prep(S.facets[ss].p, ns, ws.screen_s.p, ws.num_sms, st);
+                    refine_prep(S.facets[ss].p, ns, ws.screen_s.p, ws.level_agg.p + 3, ws.num_sms, st);
                     src.s_box = ws.screen_s.p;
                     src.s_geo = ws.screen_s.p + 3 * ns;
                 }
             }
-            const int cull = (spec.flags & TJ_FLAG_NO_CULL) ? 0 : 1;
+            // 0: every facet pair; 1: exact-preserving culling; 2: decision-mode culling
+            const int cull = (spec.flags & TJ_FLAG_NO_CULL) ? 0 : decision ? 2 : 1;
             // seeds for every voxel pair first (op thresholds), then the screened passes
             if (cull)
                 for (uint64_t c0 = 0; c0 < n_active; c0 += launch)
@@ -197,7 +209,8 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
             out.chunks += (n_active + spec.refine_chunk - 1) / spec.refine_chunk;
             count_launch();
             k_aggregate<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(cs.view(), n, lbb.p, ubb.p, knn ? 0 : 1, tau,
-                                                                      (int16_t)level, updated.p, err);
+                                                                      (int16_t)level, cull == 2 ? 1 : 0, updated.p,
+                                                                      err);
             TJ_CUDA(cudaGetLastError());
             check_error(err, st);
             if (trace && trace->on_interval) trace->emit_updated(cs, updated, (int16_t)level, st);

@@ -2,7 +2,10 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <condition_variable>
 #include <cstdint>
+#include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -68,6 +71,20 @@ struct DevBuf {
     size_t bytes() const { return n * sizeof(T); }
 };
 
+// Arrival state of the levels of a streamed dataset (tj_dataset_begin / _put_level): a
+// level is pending until its copy + expansion has been queued on the dataset's copy
+// stream (then `ev` marks its completion) or failed.
+struct LevelGate {
+    enum State { kPending = 0, kQueued = 1, kFailed = 2 };
+    std::mutex mu;
+    std::condition_variable cv;
+    std::vector<int> state;
+    std::vector<cudaEvent_t> ev;
+    cudaStream_t copy = nullptr;
+    int device = 0;
+    ~LevelGate();
+};
+
 // A prepared dataset resident in HBM (the device image of reference PreparedDataset).
 struct DatasetDev {
     uint32_t n_objects = 0;
@@ -80,7 +97,14 @@ struct DatasetDev {
     std::vector<DevBuf<uint64_t>> facet_offsets; // per level [nv+1]
     std::vector<DevBuf<double>> facets;          // per level [entries*12]
     uint64_t bytes = 0;
+    std::vector<uint64_t> level_entries;         // per level: facet records (CSR entries)
+    std::vector<uint64_t> level_vertices, level_facets; // streamed: compact-form sizes per level
+    std::shared_ptr<LevelGate> gate;             // streamed datasets only (else all levels resident)
 };
+
+// Makes `st` wait until level slot `slot` of `d` is resident (no-op for uploaded datasets);
+// returns the host milliseconds spent blocked waiting for the level to be queued.
+double level_ready(const DatasetDev& d, int slot, cudaStream_t st);
 
 // Active voxel pair during refinement: candidate op + global voxel ids.
 struct ActiveVpDev {
@@ -110,6 +134,9 @@ struct RefineSource {
     const float4* r_geo;
     const float4* s_box;
     const float4* s_geo;
+    // level aggregates of the screening records (refine_prep): [0..2] R min hd, max |L|,
+    // max M; [3..5] the same for S (float bits; join mode only, else nullptr)
+    const unsigned* agg;
 };
 
 // A queued facet pair: op and the two global facet record indices.
@@ -135,7 +162,8 @@ struct RefineQueueStore {
 
 // FP32 screening records of n facet records (refine.cu, k_prep) into out[7 n]: box parts at
 // out[0, 3 n), geometry parts at out[3 n, 7 n).
-void refine_prep(const double* facets, uint64_t n, float4* out, int num_sms, cudaStream_t st);
+// agg (optional, 3 uints pre-set to {+inf, 0, 0} bits): min hd, max |L|, max M of the records.
+void refine_prep(const double* facets, uint64_t n, float4* out, unsigned* agg, int num_sms, cudaStream_t st);
 
 // One refinement pass over voxel pairs [vp_begin, vp_end) (refine.cu): the seed pass queues
 // each voxel pair's 2 smallest-box-gap facet pairs, the screen pass every facet pair that

@@ -61,6 +61,29 @@ def test_chunk_and_cull_invariance(capi, refine_chunk):
         capi.free(R)
 
 
+@pytest.mark.parametrize("idx", ["mini10_s61.idx", "mini18_s21.idx", "spheres80a.idx"])
+def test_intersect_decision_mode(capi, idx):
+    """Intersection joins refine in decision mode unless TJ_FLAG_EXACT_INTERVALS (4): statuses
+    and stages are identical to the exhaustive run; confirmed intervals are bit-identical (the
+    only intervals an intersection's records carry); with the flag every interval is."""
+    R = capi.load(golden(idx))
+    try:
+        lods = (20, 60, 100)
+        base = capi.join(R, R, type="intersect", lods=lods, flags=1 | 4)
+        dec = capi.join(R, R, type="intersect", lods=lods)
+        exact = capi.join(R, R, type="intersect", lods=lods, flags=4)
+        assert dec["decision_mode"] == 1 and exact["decision_mode"] == 0
+        for c in (dec, exact):
+            for key in ("pair_r", "pair_s", "status", "decided_at"):
+                assert (c[key] == base[key]).all()
+        conf = base["status"] == 1
+        for key in ("lb", "ub"):
+            assert (tjtest.bits(dec[key][conf]) == tjtest.bits(base[key][conf])).all()
+            assert (tjtest.bits(exact[key]) == tjtest.bits(base[key])).all()
+    finally:
+        capi.free(R)
+
+
 @pytest.mark.parametrize("kw", [dict(type="within", tau=0.9), dict(type="knn", k=3)])
 def test_shards_merge_to_single_run(capi, kw):
     """R-sharded runs (query blocks across GPUs, no data-path collective) merge to

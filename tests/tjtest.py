@@ -64,7 +64,8 @@ class JoinResult(ctypes.Structure):
                 ("level_pairs_screened", ctypes.c_uint64 * MAXL),
                 ("level_pairs_verified", ctypes.c_uint64 * MAXL),
                 ("level_vps_skipped", ctypes.c_uint64 * MAXL),
-                ("level_facets_dropped", ctypes.c_uint64 * MAXL)]
+                ("level_facets_dropped", ctypes.c_uint64 * MAXL),
+                ("level_wait_ms", ctypes.c_double * MAXL), ("decision_mode", ctypes.c_int32)]
 
 
 def capi_functions():
@@ -168,6 +169,7 @@ class Capi:
             "decided_at": np.ctypeslib.as_array(res.decided_at, (max(n, 1),))[:n].copy(),
             "nq": res.n_queries, "vp_generated": res.vp_generated, "vp_pruned": res.vp_pruned,
             "levels": [(res.level[i], res.level_vps[i], res.level_facet_pairs[i]) for i in range(res.n_levels_run)],
+            "decision_mode": res.decision_mode,
         }
         self.lib.tj_join_result_free(ctypes.byref(res))
         return out

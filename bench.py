@@ -278,7 +278,10 @@ def main():
             d2h = n_c * (4 + 4 + 8 + 8 + 1 + 2) + (R.n_objects + 1) * 8 + R.n_objects * 4
             pairs_e2e = st["stages"][1]["pairs_in"]
             if i > 0:
-                parts.append(st.get("b200", {}))
+                b = dict(st.get("b200", {}))
+                b["run_join_ms"] = st.get("total_ms", 0.0)
+                b["python_ms"] = (t1 - t0) * 1e3 - b["run_join_ms"]
+                parts.append(b)
             h2d = st.get("b200", {}).get("h2d_bytes", 0)
         e2e_ms = float(np.mean(ts))
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
@@ -288,7 +291,9 @@ def main():
                "d2h_bytes_per_step": int(d2h), "ms_per_step": float(t[0]),
                "path": "paper_2604_19982_b200._core.join_datasets -> trijoin::run_join -> tj_join (C-ABI)",
                "breakdown_ms": {k: round(float(np.mean([p.get(k, 0.0) for p in parts])), 2)
-                                for k in ("pack_ms", "upload_ms", "device_ms", "stream_wait_ms")}}
+                                for k in ("pack_ms", "upload_ms", "device_ms", "stream_wait_ms", "run_join_ms",
+                                          "python_ms")},
+               "timeline_ms": parts[-1].get("timeline", {}) if parts else {}}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:

@@ -167,33 +167,34 @@ uint64_t tj_dataset_device_bytes(const tj_dataset* ds);
  *
  * The e2e path of run_join (include/trijoin/engine.hpp) does not ship the expanded
  * 96-byte facet records over PCIe. It ships each LOD level in the reference's own mesh
- * form (vertices + index triples + hd/ph + voxel facet-id lists, ~44 B per facet) and the
- * device expands it into the resident record layout. Levels are uploaded one at a time
- * on the dataset's own copy stream while tj_join already runs the filters and the
- * coarser levels; tj_join blocks (host condition variable, then a device event wait) only
- * when it reaches a level that has not arrived yet.
+ * form, object by object exactly as PreparedObject holds it (vertices, object-local index
+ * triples, hd/ph, object-local voxel facet-id lists; ~44 B per facet, so the host side
+ * is plain memcpy), and the device rebases, validates and expands it into the resident
+ * record layout. Levels are uploaded one at a time on the dataset's own copy stream while
+ * tj_join already runs the filters and the coarser levels; tj_join blocks (host condition
+ * variable, then a device event wait) only when it reaches a level that has not arrived.
  *
  * tj_dataset_begin: uploads the object and voxel arrays of `header` (its facets[] may be
- *   NULL; facet_offsets[] is required) and reserves every level. n_vertices[li] and
- *   n_facets[li] are the level's dataset-wide vertex / facet totals.
+ *   NULL; facet_offsets[] is required) and reserves every level. vert_base[li] and
+ *   facet_base[li] ([n_objects+1] each) are the per-object prefix sums of the level's
+ *   vertex and facet counts (object o owns vertices [vert_base[o], vert_base[o+1])).
  * tj_dataset_put_level: queues level slot `slot`: copies from the caller's buffers (keep
  *   them valid, preferably page-locked, until tj_dataset_sync returns) and expands. May be
  *   called from another host thread while tj_join runs on the dataset. lv == NULL marks
- *   the slot failed: a join waiting for it returns TJ_EINVAL.
+ *   the slot failed: a join waiting for it returns TJ_EINVAL. An index out of its
+ *   object's range makes every later tj_join on the dataset return TJ_EINVAL.
  * tj_dataset_sync: waits for every queued level copy of the dataset.
  */
 typedef struct tj_level_mesh_view {
-    uint64_t n_vertices;
-    uint64_t n_facets;
-    const double* vertices;       /* [n_vertices*3] all objects, concatenated */
-    const uint32_t* tris;         /* [n_facets*3] dataset-global vertex ids */
-    const double* hd;             /* [n_facets] */
-    const double* ph;             /* [n_facets] */
-    const uint32_t* voxel_facets; /* [facet_offsets[li][n_voxels]] dataset-global facet ids, voxel order */
+    const double* vertices;       /* [vert_base[n_objects]*3] all objects, concatenated */
+    const uint32_t* tris;         /* [facet_base[n_objects]*3] object-local vertex ids */
+    const double* hd;             /* [facet_base[n_objects]] */
+    const double* ph;             /* [facet_base[n_objects]] */
+    const uint32_t* voxel_facets; /* [facet_offsets[li][n_voxels]] object-local facet ids, voxel order */
 } tj_level_mesh_view;
 
-int tj_dataset_begin(tj_ctx* ctx, const tj_dataset_view* header, const uint64_t* n_vertices,
-                     const uint64_t* n_facets, tj_dataset** out);
+int tj_dataset_begin(tj_ctx* ctx, const tj_dataset_view* header, const uint64_t* const* vert_base,
+                     const uint64_t* const* facet_base, tj_dataset** out);
 int tj_dataset_put_level(tj_dataset* ds, uint32_t slot, const tj_level_mesh_view* lv);
 int tj_dataset_sync(tj_dataset* ds);
 

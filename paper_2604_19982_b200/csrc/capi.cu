@@ -114,7 +114,7 @@ void check_levels(const DatasetDev& d, const tj_join_spec& s) {
 void check_dev_error(DevError* err, cudaStream_t st) {
     DevError h;
     TJ_CUDA(cudaMemcpyAsync(&h, err, sizeof(DevError), cudaMemcpyDeviceToHost, st));
-    TJ_CUDA(cudaStreamSynchronize(st));
+    stream_sync(st);
     if (h.code == 0) return;
     if (h.kind == 1) throw Error(TJ_EENGINE, "knn_apply_deltas: confirmed count exceeds k");
     throw Error(TJ_EENGINE, "bound crossing: lb " + std::to_string(h.lb) + " > ub " + std::to_string(h.ub));
@@ -154,35 +154,59 @@ void upload_objects(DatasetDev& d, const tj_dataset_view* v, cudaStream_t st) {
     d.bytes = (9ull * no + 9ull * d.n_voxels) * 8 + (no + 1ull) * 8;
 }
 
-// Expansion of one level's compact mesh form into the resident record layout: entry e
-// of the voxel-ordered CSR gets (v0, v1, v2, hd, ph, 0) of facet voxel_facets[e]
-// (the record the reference's gather_facet_data builds per chunk, src/refine.cpp:25-61).
+// Expansion of one level's compact mesh form into the resident record layout, warp per
+// voxel: entry e of voxel v (object o) gets (v0, v1, v2, hd, ph, 0) of o's facet
+// voxel_facets[e] (the record the reference's gather_facet_data builds per chunk,
+// src/refine.cpp:25-61). Object-local ids are rebased here and range-checked against the
+// object's counts; an out-of-range id is clamped (never read out of bounds) and flagged.
 __global__ void k_expand_level(const double* __restrict__ verts, const uint32_t* __restrict__ tris,
                                const double* __restrict__ hd, const double* __restrict__ ph,
-                               const uint32_t* __restrict__ vf, uint64_t entries, double* __restrict__ out) {
-    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < entries; e += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t f = __ldg(vf + e);
-        const uint32_t t0 = __ldg(tris + 3ull * f), t1 = __ldg(tris + 3ull * f + 1), t2 = __ldg(tris + 3ull * f + 2);
-        double2* o = reinterpret_cast<double2*>(out + e * TJ_FACET_STRIDE);
-        const double* a = verts + 3ull * t0;
-        const double* b = verts + 3ull * t1;
-        const double* c = verts + 3ull * t2;
-        o[0] = make_double2(__ldg(a), __ldg(a + 1));
-        o[1] = make_double2(__ldg(a + 2), __ldg(b));
-        o[2] = make_double2(__ldg(b + 1), __ldg(b + 2));
-        o[3] = make_double2(__ldg(c), __ldg(c + 1));
-        o[4] = make_double2(__ldg(c + 2), __ldg(hd + f));
-        o[5] = make_double2(__ldg(ph + f), 0.0);
+                               const uint32_t* __restrict__ vf, const uint64_t* __restrict__ foff,
+                               const uint32_t* __restrict__ vox_obj, const uint64_t* __restrict__ vb,
+                               const uint64_t* __restrict__ fb, uint64_t n_voxels, double* __restrict__ out,
+                               int* __restrict__ err) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t v = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); v < n_voxels; v += warps) {
+        const uint32_t o = vox_obj[v];
+        const uint64_t v_lo = vb[o], nv = vb[o + 1] - v_lo;
+        const uint64_t f_lo = fb[o], nf = fb[o + 1] - f_lo;
+        const uint64_t e0 = foff[v], e1 = foff[v + 1];
+        bool bad = false;
+        for (uint64_t e = e0 + lane; e < e1; e += 32) {
+            uint64_t f = __ldg(vf + e);
+            if (f >= nf) { bad = true; f = 0; }
+            f += f_lo;
+            uint64_t t[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                t[k] = nf ? __ldg(tris + 3 * f + k) : 0;
+                if (t[k] >= nv) { bad = true; t[k] = 0; }
+                t[k] += v_lo;
+            }
+            double r[12];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const double* p = verts + 3 * t[k];
+                const bool ok = nv != 0;
+                r[3 * k] = ok ? __ldg(p) : 0.0;
+                r[3 * k + 1] = ok ? __ldg(p + 1) : 0.0;
+                r[3 * k + 2] = ok ? __ldg(p + 2) : 0.0;
+            }
+            r[9] = nf ? __ldg(hd + f) : 0.0;
+            r[10] = nf ? __ldg(ph + f) : 0.0;
+            r[11] = 0.0;
+            double2* d = reinterpret_cast<double2*>(out + e * TJ_FACET_STRIDE);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) d[k] = make_double2(r[2 * k], r[2 * k + 1]);
+        }
+        if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(err, 1);
     }
 }
 
-void launch_expand_level(const double* verts, const uint32_t* tris, const double* hd, const double* ph,
-                         const uint32_t* vf, uint64_t entries, double* out, int num_sms, cudaStream_t st) {
-    if (!entries) return;
-    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((entries + 255) / 256, (uint64_t)num_sms * 16));
-    count_launch();
-    k_expand_level<<<grid, 256, 0, st>>>(verts, tris, hd, ph, vf, entries, out);
-    TJ_CUDA(cudaGetLastError());
+__global__ void k_voxel_owner(const uint64_t* __restrict__ voff, uint32_t n_objects, uint32_t* __restrict__ vox_obj) {
+    for (uint32_t o = blockIdx.x * blockDim.x + threadIdx.x; o < n_objects; o += gridDim.x * blockDim.x)
+        for (uint64_t v = voff[o]; v < voff[o + 1]; ++v) vox_obj[v] = o;
 }
 
 } // namespace
@@ -205,6 +229,23 @@ double level_ready(const DatasetDev& d, int slot, cudaStream_t st) {
         throw Error(TJ_EINVAL, "join: level " + std::to_string(d.levels[slot]) + " of a streamed dataset was not delivered");
     TJ_CUDA(cudaStreamWaitEvent(st, g.ev[slot], 0));
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+void stream_sync(cudaStream_t st) {
+    struct Events {
+        cudaEvent_t ev[64] = {};
+        ~Events() {
+            for (cudaEvent_t e : ev)
+                if (e) cudaEventDestroy(e);
+        }
+    };
+    static thread_local Events evs;
+    int dev = 0;
+    TJ_CUDA(cudaGetDevice(&dev));
+    cudaEvent_t& e = evs.ev[dev & 63];
+    if (!e) TJ_CUDA(cudaEventCreateWithFlags(&e, cudaEventBlockingSync | cudaEventDisableTiming));
+    TJ_CUDA(cudaEventRecord(e, st));
+    TJ_CUDA(cudaEventSynchronize(e));
 }
 
 unsigned long long& launch_counter_ref() {
@@ -294,7 +335,7 @@ int tj_dataset_upload(tj_ctx* ctx, const tj_dataset_view* v, tj_dataset** out) {
             d.level_entries.push_back(entries);
             d.bytes += (d.n_voxels + 1) * 8 + entries * TJ_FACET_STRIDE * 8;
         }
-        TJ_CUDA(cudaStreamSynchronize(st));
+        stream_sync(st);
     });
     if (rc == TJ_OK) *out = ds.release();
     return rc;
@@ -308,9 +349,9 @@ void tj_dataset_free(tj_dataset* ds) {
     delete ds;
 }
 
-int tj_dataset_begin(tj_ctx* ctx, const tj_dataset_view* v, const uint64_t* n_vertices, const uint64_t* n_facets,
-                     tj_dataset** out) {
-    if (!ctx || !v || !out || !n_vertices || !n_facets) return TJ_EINVAL;
+int tj_dataset_begin(tj_ctx* ctx, const tj_dataset_view* v, const uint64_t* const* vert_base,
+                     const uint64_t* const* facet_base, tj_dataset** out) {
+    if (!ctx || !v || !out || !vert_base || !facet_base) return TJ_EINVAL;
     *out = nullptr;
     auto ds = std::make_unique<tj_dataset>();
     ds->ctx = ctx;
@@ -318,27 +359,48 @@ int tj_dataset_begin(tj_ctx* ctx, const tj_dataset_view* v, const uint64_t* n_ve
         DatasetDev& d = ds->d;
         cudaStream_t st = ctx->stream;
         upload_objects(d, v, st);
+        const uint32_t no = d.n_objects;
         auto gate = std::make_shared<LevelGate>();
         gate->device = ctx->device;
         gate->state.assign(v->n_levels, LevelGate::kPending);
         gate->ev.assign(v->n_levels, nullptr);
         TJ_CUDA(cudaStreamCreateWithFlags(&gate->copy, cudaStreamNonBlocking));
+        d.vert_base.resize(v->n_levels);
+        d.facet_base.resize(v->n_levels);
         for (uint32_t li = 0; li < v->n_levels; ++li) {
             TJ_CUDA(cudaEventCreateWithFlags(&gate->ev[li], cudaEventDisableTiming));
             const uint64_t* fo = v->facet_offsets ? v->facet_offsets[li] : nullptr;
-            if (!fo) throw Error(TJ_EINVAL, "tj_dataset_begin: null facet_offsets");
+            const uint64_t* vb = vert_base[li];
+            const uint64_t* fb = facet_base[li];
+            if (!fo || !vb || !fb) throw Error(TJ_EINVAL, "tj_dataset_begin: null level offsets");
             const uint64_t entries = fo[d.n_voxels];
             for (uint64_t x = 0; x < d.n_voxels; ++x)
                 if (fo[x + 1] < fo[x]) throw Error(TJ_EINVAL, "tj_dataset_begin: facet_offsets not monotone");
+            if (vb[0] != 0 || fb[0] != 0) throw Error(TJ_EINVAL, "tj_dataset_begin: object bases must start at 0");
+            for (uint32_t o = 0; o < no; ++o)
+                if (vb[o + 1] < vb[o] || fb[o + 1] < fb[o])
+                    throw Error(TJ_EINVAL, "tj_dataset_begin: object bases not monotone");
+            if (vb[no] >> 32 || fb[no] >> 32)
+                throw Error(TJ_EINVAL, "tj_dataset_begin: more than 2^32 vertices or facets in one level");
             upload(d.facet_offsets[li], fo, d.n_voxels + 1, st);
+            upload(d.vert_base[li], vb, no + 1ull, st);
+            upload(d.facet_base[li], fb, no + 1ull, st);
             d.facets[li].alloc(std::max<uint64_t>(entries, 1) * TJ_FACET_STRIDE);
             d.level_entries.push_back(entries);
-            d.level_vertices.push_back(n_vertices[li]);
-            d.level_facets.push_back(n_facets[li]);
+            d.level_vertices.push_back(vb[no]);
+            d.level_facets.push_back(fb[no]);
             d.bytes += (d.n_voxels + 1) * 8 + entries * TJ_FACET_STRIDE * 8;
         }
+        d.vox_obj.alloc(std::max<uint64_t>(d.n_voxels, 1));
+        if (no) {
+            count_launch();
+            k_voxel_owner<<<(no + 255) / 256, 256, 0, st>>>(d.voxel_offsets.p, no, d.vox_obj.p);
+            TJ_CUDA(cudaGetLastError());
+        }
+        d.stream_err.alloc(1);
+        TJ_CUDA(cudaMemsetAsync(d.stream_err.p, 0, sizeof(int), st));
         d.gate = std::move(gate);
-        TJ_CUDA(cudaStreamSynchronize(st));
+        stream_sync(st);
     });
     if (rc == TJ_OK) *out = ds.release();
     return rc;
@@ -363,17 +425,24 @@ int tj_dataset_put_level(tj_dataset* ds, uint32_t slot, const tj_level_mesh_view
         TJ_CUDA(cudaSetDevice(ctx->device));
         AllocStreamScope scope(g.copy);
         DatasetDev& d = ds->d;
-        if (lv->n_vertices != d.level_vertices[slot] || lv->n_facets != d.level_facets[slot])
-            throw Error(TJ_EINVAL, "tj_dataset_put_level: level sizes differ from tj_dataset_begin");
-        const uint64_t used = d.level_entries[slot];
+        const uint64_t nvert = d.level_vertices[slot], nfac = d.level_facets[slot], used = d.level_entries[slot];
+        if ((nvert && !lv->vertices) || (nfac && (!lv->tris || !lv->hd || !lv->ph)) || (used && !lv->voxel_facets))
+            throw Error(TJ_EINVAL, "tj_dataset_put_level: null level arrays");
         DevBuf<double> verts, hd, ph;
         DevBuf<uint32_t> tris, vf;
-        upload(verts, lv->vertices, lv->n_vertices * 3, g.copy);
-        upload(tris, lv->tris, lv->n_facets * 3, g.copy);
-        upload(hd, lv->hd, lv->n_facets, g.copy);
-        upload(ph, lv->ph, lv->n_facets, g.copy);
+        upload(verts, lv->vertices, nvert * 3, g.copy);
+        upload(tris, lv->tris, nfac * 3, g.copy);
+        upload(hd, lv->hd, nfac, g.copy);
+        upload(ph, lv->ph, nfac, g.copy);
         upload(vf, lv->voxel_facets, used, g.copy);
-        launch_expand_level(verts.p, tris.p, hd.p, ph.p, vf.p, used, d.facets[slot].p, ctx->ws.num_sms, g.copy);
+        if (d.n_voxels) {
+            const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((d.n_voxels + 7) / 8, (uint64_t)ctx->ws.num_sms * 16));
+            count_launch();
+            k_expand_level<<<grid, 256, 0, g.copy>>>(verts.p, tris.p, hd.p, ph.p, vf.p, d.facet_offsets[slot].p,
+                                                      d.vox_obj.p, d.vert_base[slot].p, d.facet_base[slot].p,
+                                                      d.n_voxels, d.facets[slot].p, d.stream_err.p);
+            TJ_CUDA(cudaGetLastError());
+        }
         TJ_CUDA(cudaEventRecord(g.ev[slot], g.copy));
     });
     set_state(rc == TJ_OK ? LevelGate::kQueued : LevelGate::kFailed);
@@ -496,7 +565,7 @@ int tj_join(tj_ctx* ctx, const tj_dataset* Rh, const tj_dataset* Sh, const tj_jo
             if (tsink->on_vp_pruned && !pruned.empty()) {
                 std::vector<double> ub(cs.n);
                 TJ_CUDA(cudaMemcpyAsync(ub.data(), cs.ub.p, cs.n * 8, cudaMemcpyDeviceToHost, st));
-                TJ_CUDA(cudaStreamSynchronize(st));
+                stream_sync(st);
                 for (const PrunedVp& p : pruned) tsink->on_vp_pruned(tsink->user, p.op, p.vr, p.vs, p.lb, ub[p.op]);
             }
         }
@@ -519,7 +588,7 @@ int tj_join(tj_ctx* ctx, const tj_dataset* Rh, const tj_dataset* Sh, const tj_jo
         } else {
             std::vector<uint8_t> stv(cs.n);
             if (cs.n) TJ_CUDA(cudaMemcpyAsync(stv.data(), cs.status.p, cs.n, cudaMemcpyDeviceToHost, st));
-            TJ_CUDA(cudaStreamSynchronize(st));
+            stream_sync(st);
             for (uint8_t s : stv)
                 if (s == TJ_UNDECIDED)
                     throw Error(TJ_EENGINE, "refine_loop: candidates left undecided after the exact level");
@@ -542,6 +611,15 @@ int tj_join(tj_ctx* ctx, const tj_dataset* Rh, const tj_dataset* Sh, const tj_jo
         }
         out->refine_chunks = ro.chunks;
 
+        // streamed datasets: the device-side validation of the levels this join used
+        for (const DatasetDev* D : {&R, &S}) {
+            if (!D->gate) continue;
+            int bad = 0;
+            TJ_CUDA(cudaMemcpyAsync(&bad, D->stream_err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+            stream_sync(st);
+            if (bad) throw Error(TJ_EINVAL, "trijoin: voxel facet id or facet vertex id out of range");
+        }
+
         // ---- results ----
         out->n_cands = cs.n;
         out->n_queries = R.n_objects;
@@ -553,7 +631,7 @@ int tj_join(tj_ctx* ctx, const tj_dataset* Rh, const tj_dataset* Sh, const tj_jo
         out->decided_at = host_copy(cs.decided_at, cs.n, st);
         out->r2op_offsets = host_copy(cs.r2op, (uint64_t)R.n_objects + 1, st);
         out->num_confirmed = host_copy(cs.num_confirmed, R.n_objects, st);
-        TJ_CUDA(cudaStreamSynchronize(st));
+        stream_sync(st);
         out->total_ms = std::chrono::duration<double, std::milli>(Clock::now() - t_total).count();
     });
 }
@@ -585,9 +663,6 @@ int tj_refine_batch(tj_ctx* ctx, uint64_t n_tris, const double* tris, const doub
         // every descriptor is its own op: per-voxel-pair minima, exact (refine_kernel.cuh)
         DevBuf<unsigned long long> lbb(n_descs), ubb(n_descs), work(1), counters(kNumCounters);
         std::vector<unsigned long long> inf(n_descs, 0x7ff0000000000000ull);
-        TJ_CUDA(cudaMemcpyAsync(lbb.p, inf.data(), n_descs * 8, cudaMemcpyHostToDevice, st));
-        TJ_CUDA(cudaMemcpyAsync(ubb.p, inf.data(), n_descs * 8, cudaMemcpyHostToDevice, st));
-        TJ_CUDA(cudaMemsetAsync(counters.p, 0, kNumCounters * 8, st));
         RefineSource src{};
         src.r_off = ro.p;
         src.s_off = so.p;
@@ -601,11 +676,23 @@ int tj_refine_batch(tj_ctx* ctx, uint64_t n_tris, const double* tris, const doub
         src.r_geo = src.s_geo = scr.p + 3 * n_tris;
         const int cull = (flags & TJ_FLAG_NO_CULL) ? 0 : 1;
         RefineQueueStore queue;
-        if (cull) refine_pass(src, 0, n_descs, true, lbb.p, ubb.p, cull, queue, work.p, counters.p, ctx->ws.num_sms, st);
-        refine_pass(src, 0, n_descs, false, lbb.p, ubb.p, cull, queue, work.p, counters.p, ctx->ws.num_sms, st);
+        for (;;) { // re-run with a larger exact-evaluation queue if it overflowed
+            TJ_CUDA(cudaMemcpyAsync(lbb.p, inf.data(), n_descs * 8, cudaMemcpyHostToDevice, st));
+            TJ_CUDA(cudaMemcpyAsync(ubb.p, inf.data(), n_descs * 8, cudaMemcpyHostToDevice, st));
+            TJ_CUDA(cudaMemsetAsync(counters.p, 0, kNumCounters * 8, st));
+            TJ_CUDA(cudaMemsetAsync(queue.count.p, 0, 16, st));
+            if (cull)
+                refine_pass(src, 0, n_descs, true, lbb.p, ubb.p, cull, queue, work.p, counters.p, ctx->ws.num_sms, st);
+            refine_pass(src, 0, n_descs, false, lbb.p, ubb.p, cull, queue, work.p, counters.p, ctx->ws.num_sms, st);
+            unsigned long long ovf = 0;
+            TJ_CUDA(cudaMemcpyAsync(&ovf, queue.count.p + 1, 8, cudaMemcpyDeviceToHost, st));
+            stream_sync(st);
+            if (ovf == 0) break;
+            queue.items.alloc(ovf + ovf / 4);
+        }
         TJ_CUDA(cudaMemcpyAsync(vp_lb, lbb.p, n_descs * 8, cudaMemcpyDeviceToHost, st));
         TJ_CUDA(cudaMemcpyAsync(vp_ub, ubb.p, n_descs * 8, cudaMemcpyDeviceToHost, st));
-        TJ_CUDA(cudaStreamSynchronize(st));
+        stream_sync(st);
     });
 }
 
@@ -619,7 +706,7 @@ int tj_tri_tri_batch(tj_ctx* ctx, uint64_t n, const double* a9, const double* b9
         upload(b, b9, 9 * n, st);
         launch_tri_tri_batch(n, a.p, b.p, o.p, st);
         TJ_CUDA(cudaMemcpyAsync(out, o.p, n * 8, cudaMemcpyDeviceToHost, st));
-        TJ_CUDA(cudaStreamSynchronize(st));
+        stream_sync(st);
     });
 }
 
@@ -633,7 +720,7 @@ int tj_mindist_batch(tj_ctx* ctx, uint64_t n, const double* a6, const double* b6
         upload(b, b6, 6 * n, st);
         launch_mindist_batch(n, a.p, b.p, o.p, st);
         TJ_CUDA(cudaMemcpyAsync(out, o.p, n * 8, cudaMemcpyDeviceToHost, st));
-        TJ_CUDA(cudaStreamSynchronize(st));
+        stream_sync(st);
     });
 }
 

@@ -376,7 +376,7 @@ uint64_t scan_counts(Workspace& ws, const uint32_t* counts, uint64_t n, DevBuf<u
     TJ_CUDA(cub::DeviceScan::InclusiveSum(ws.temp.p, bytes, wide.p, offsets.p + 1, (int64_t)n, st));
     uint64_t total = 0;
     TJ_CUDA(cudaMemcpyAsync(&total, offsets.p + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-    TJ_CUDA(cudaStreamSynchronize(st));
+    stream_sync(st);
     return total;
 }
 
@@ -400,7 +400,7 @@ void mbb_prepare_s(Workspace& ws, const DatasetDev& S, SortedS& out, cudaStream_
     k_gather_sorted<<<grid_for(ns, 256, ws.num_sms), 256, 0, st>>>(S.mbb.p, out.order.p, ns, out.mbb.p, ext.p);
     unsigned long long bits = 0;
     TJ_CUDA(cudaMemcpyAsync(&bits, ext.p, 8, cudaMemcpyDeviceToHost, st));
-    TJ_CUDA(cudaStreamSynchronize(st));
+    stream_sync(st);
     double e;
     memcpy(&e, &bits, 8);
     out.max_ext = e;
@@ -449,7 +449,7 @@ uint64_t mbb_candidates(Workspace& ws, const MbbArgs& a, CandDevStore& cs, cudaS
     } else {
         TJ_CUDA(cudaMemsetAsync(cs.num_confirmed.p, 0, sizeof(uint32_t) * std::max<uint32_t>(nr, 1), st));
     }
-    TJ_CUDA(cudaStreamSynchronize(st));
+    stream_sync(st);
     return n;
 }
 
@@ -504,11 +504,11 @@ VoxelOut voxel_filter(Workspace& ws, const VoxelArgs& a, CandDevStore& cs, DevBu
             TJ_CUDA(cudaMemcpyAsync(hv.data(), pv.p, np * sizeof(ActiveVpDev), cudaMemcpyDeviceToHost, st));
             TJ_CUDA(cudaMemcpyAsync(hl.data(), plb.p, np * sizeof(double), cudaMemcpyDeviceToHost, st));
         }
-        TJ_CUDA(cudaStreamSynchronize(st));
+        stream_sync(st);
         pruned_host->resize(np);
         for (uint64_t i = 0; i < np; ++i) (*pruned_host)[i] = {hv[i].op, hv[i].gvr, hv[i].gvs, hl[i]};
     }
-    TJ_CUDA(cudaStreamSynchronize(st));
+    stream_sync(st);
     return out;
 }
 

@@ -71,19 +71,20 @@ std::vector<int> join_devices() {
 }
 
 namespace {
-// Process-wide pinned arena: freed blocks are kept for reuse (pinning is slow; reuse is free).
+// Process-wide host staging arena: freed blocks are kept for reuse (pinning and first-touch
+// page faults are slow; reuse is free). Blocks are page-locked unless no device is present.
 struct PinnedArena {
     std::mutex mu;
-    std::multimap<size_t, double*> free_blocks; // capacity (doubles) -> block
+    std::multimap<size_t, std::pair<double*, bool>> free_blocks; // capacity (doubles) -> (block, pinned)
     double* acquire(size_t want, size_t& cap, bool& pinned) {
         {
             std::lock_guard<std::mutex> lk(mu);
             auto it = free_blocks.lower_bound(want);
             if (it != free_blocks.end() && it->first <= 2 * want + (1u << 20)) {
                 cap = it->first;
-                double* p = it->second;
+                double* p = it->second.first;
+                pinned = it->second.second;
                 free_blocks.erase(it);
-                pinned = true;
                 return p;
             }
         }
@@ -93,7 +94,7 @@ struct PinnedArena {
             pinned = true;
             return static_cast<double*>(p);
         }
-        cudaGetLastError(); // no device / pinning refused: fall back to pageable host memory
+        cudaGetLastError(); // no device / pinning refused: pageable host memory
         pinned = false;
         p = std::malloc(want * sizeof(double));
         if (!p) throw std::bad_alloc();
@@ -101,12 +102,8 @@ struct PinnedArena {
     }
     void release(double* p, size_t cap, bool pinned) {
         if (!p) return;
-        if (!pinned) {
-            std::free(p);
-            return;
-        }
         std::lock_guard<std::mutex> lk(mu);
-        free_blocks.emplace(cap, p);
+        free_blocks.emplace(cap, std::make_pair(p, pinned));
     }
 };
 PinnedArena& arena() {
@@ -258,6 +255,8 @@ T* as(PinnedBuf& b) {
 uint64_t PackedHeader::bytes() const {
     uint64_t b = (mbb.size() + anchor.size() + voxel_box.size() + voxel_anchor.size() + voxel_offsets.size()) * 8;
     for (const auto& v : facet_offsets) b += v.size() * 8;
+    for (const auto& v : vert_base) b += v.size() * 8;
+    for (const auto& v : facet_base) b += v.size() * 8;
     return b;
 }
 
@@ -272,15 +271,31 @@ std::unique_ptr<PackedHeader> pack_header(const PreparedDataset& ds, ThreadPool&
     h->voxel_offsets.assign(no + 1, 0);
     h->vert_base.assign(nl, std::vector<uint64_t>(no + 1, 0));
     h->facet_base.assign(nl, std::vector<uint64_t>(no + 1, 0));
+    // per-object counts in parallel (written at o + 1), then serial prefix sums
+    std::atomic<int> bad_levels{0}, bad_pad{0};
+    for_blocks(pool, no, [&](size_t b, size_t e) {
+        for (size_t o = b; o < e; ++o) {
+            const PreparedObject& obj = ds.objects[o];
+            if (obj.ladder.levels.size() != nl || obj.voxels.facets_per_level.size() != nl) {
+                bad_levels = 1;
+                continue;
+            }
+            h->voxel_offsets[o + 1] = obj.voxels.voxel_count();
+            for (size_t li = 0; li < nl; ++li) {
+                const LodMesh& lod = obj.ladder.levels[li];
+                if (lod.hd.size() < lod.mesh.facets.size() || lod.ph.size() < lod.mesh.facets.size()) bad_pad = 1;
+                h->vert_base[li][o + 1] = lod.mesh.vertices.size();
+                h->facet_base[li][o + 1] = lod.mesh.facets.size();
+            }
+        }
+    });
+    if (bad_levels) throw std::invalid_argument("trijoin: object level count does not match the lod schedule");
+    if (bad_pad) throw std::invalid_argument("trijoin: hd / ph shorter than the level's facet list");
     for (size_t o = 0; o < no; ++o) {
-        const PreparedObject& obj = ds.objects[o];
-        if (obj.ladder.levels.size() != nl || obj.voxels.facets_per_level.size() != nl)
-            throw std::invalid_argument("trijoin: object level count does not match the lod schedule");
-        h->voxel_offsets[o + 1] = h->voxel_offsets[o] + obj.voxels.voxel_count();
+        h->voxel_offsets[o + 1] += h->voxel_offsets[o];
         for (size_t li = 0; li < nl; ++li) {
-            const Mesh& m = obj.ladder.levels[li].mesh;
-            h->vert_base[li][o + 1] = h->vert_base[li][o] + m.vertices.size();
-            h->facet_base[li][o + 1] = h->facet_base[li][o] + m.facets.size();
+            h->vert_base[li][o + 1] += h->vert_base[li][o];
+            h->facet_base[li][o + 1] += h->facet_base[li][o];
         }
     }
     const uint64_t nv = h->voxel_offsets[no];
@@ -320,7 +335,13 @@ std::unique_ptr<PackedHeader> pack_header(const PreparedDataset& ds, ThreadPool&
         for (uint64_t v = 0; v < nv; ++v) fo[v + 1] += fo[v];
     }
     h->fo_ptrs.resize(nl);
-    for (size_t li = 0; li < nl; ++li) h->fo_ptrs[li] = h->facet_offsets[li].data();
+    h->vb_ptrs.resize(nl);
+    h->fb_ptrs.resize(nl);
+    for (size_t li = 0; li < nl; ++li) {
+        h->fo_ptrs[li] = h->facet_offsets[li].data();
+        h->vb_ptrs[li] = h->vert_base[li].data();
+        h->fb_ptrs[li] = h->facet_base[li].data();
+    }
     tj_dataset_view& v = h->view;
     v.n_objects = h->n_objects;
     v.n_levels = static_cast<uint32_t>(nl);
@@ -335,6 +356,9 @@ std::unique_ptr<PackedHeader> pack_header(const PreparedDataset& ds, ThreadPool&
     return h;
 }
 
+// One level in the compact mesh form: per object a straight copy of its vertices, index
+// triples, hd / ph and voxel facet-id lists (object-local ids; the device rebases and
+// range-checks them, k_expand_level).
 std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& ds, const PackedHeader& h, size_t li, ThreadPool& pool) {
     auto p = std::make_unique<PackedLevel>();
     const size_t no = ds.objects.size();
@@ -350,43 +374,30 @@ std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& ds, const PackedH
     double* hd = p->hd.data();
     double* ph = p->ph.data();
     uint32_t* vf = as<uint32_t>(p->vf);
-    std::atomic<bool> bad{false};
+    static_assert(sizeof(Point3) == 3 * sizeof(double), "Point3 must be three packed doubles");
+    static_assert(sizeof(std::array<uint32_t, 3>) == 3 * sizeof(uint32_t), "facets must be packed uint32 triples");
     for_blocks(pool, no, [&](size_t b, size_t e) {
-        for (size_t o = b; o < e && !bad.load(std::memory_order_relaxed); ++o) {
+        for (size_t o = b; o < e; ++o) {
             const PreparedObject& obj = ds.objects[o];
             const LodMesh& lod = obj.ladder.levels[li];
             const uint64_t vb = h.vert_base[li][o], fb = h.facet_base[li][o];
             const size_t n_v = lod.mesh.vertices.size(), n_f = lod.mesh.facets.size();
-            static_assert(sizeof(Point3) == 3 * sizeof(double), "Point3 must be three packed doubles");
             if (n_v) std::memcpy(verts + 3 * vb, lod.mesh.vertices.data(), n_v * sizeof(Point3));
-            for (size_t f = 0; f < n_f; ++f) {
-                const auto& t = lod.mesh.facets[f];
-                if (t[0] >= n_v || t[1] >= n_v || t[2] >= n_v) bad = true;
-                tris[3 * (fb + f)] = static_cast<uint32_t>(vb + t[0]);
-                tris[3 * (fb + f) + 1] = static_cast<uint32_t>(vb + t[1]);
-                tris[3 * (fb + f) + 2] = static_cast<uint32_t>(vb + t[2]);
+            if (n_f) {
+                std::memcpy(tris + 3 * fb, lod.mesh.facets.data(), n_f * 3 * sizeof(uint32_t));
+                std::memcpy(hd + fb, lod.hd.data(), n_f * sizeof(double));
+                std::memcpy(ph + fb, lod.ph.data(), n_f * sizeof(double));
             }
-            const size_t nh = std::min(n_f, lod.hd.size()), np = std::min(n_f, lod.ph.size());
-            if (nh) std::memcpy(hd + fb, lod.hd.data(), nh * sizeof(double));
-            if (np) std::memcpy(ph + fb, lod.ph.data(), np * sizeof(double));
-            for (size_t f = nh; f < n_f; ++f) hd[fb + f] = 0.0;
-            for (size_t f = np; f < n_f; ++f) ph[fb + f] = 0.0;
-            const size_t n_ok = std::min({n_f, lod.hd.size(), lod.ph.size()});
             const VoxelSet& vs = obj.voxels;
             const uint64_t v0 = h.voxel_offsets[o];
+            const auto& fo = h.facet_offsets[li];
             for (uint32_t v = 0; v < vs.voxel_count(); ++v) {
-                uint64_t x = h.facet_offsets[li][v0 + v];
-                for (uint32_t f : vs.facets_per_level[li][v]) {
-                    if (f >= n_ok) bad = true;
-                    vf[x++] = static_cast<uint32_t>(fb + f);
-                }
+                const auto& ids = vs.facets_per_level[li][v];
+                if (!ids.empty()) std::memcpy(vf + fo[v0 + v], ids.data(), ids.size() * sizeof(uint32_t));
             }
         }
     });
-    if (bad) throw std::invalid_argument("trijoin: voxel facet id out of range");
     tj_level_mesh_view& v = p->view;
-    v.n_vertices = nvert;
-    v.n_facets = nfac;
     v.vertices = verts;
     v.tris = tris;
     v.hd = hd;
@@ -512,6 +523,9 @@ std::string StageStats::to_json() const {
     j["b200"] = {{"pack_ms", pack_ms}, {"upload_ms", upload_ms}, {"device_ms", device_ms},
                  {"stream_wait_ms", stream_wait_ms}, {"h2d_bytes", h2d_bytes}, {"devices", devices},
                  {"intervals", decision_mode ? "decision" : "exact"}};
+    nlohmann::json tl = nlohmann::json::object();
+    for (const auto& [k, v] : timeline) tl[k] = v;
+    j["b200"]["timeline"] = std::move(tl);
     return j.dump(2);
 }
 
@@ -701,6 +715,9 @@ JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const Jo
     const auto t_total = Clock::now();
     JoinOutput out;
     out.stats.query = join_type_name(spec.type);
+    auto mark = [&](const std::string& what) {
+        out.stats.timeline.emplace_back(what, std::chrono::duration<double, std::milli>(Clock::now() - t_total).count());
+    };
 
     const std::vector<int> devices = detail::join_devices();
     const bool self_join = &R == &S;
@@ -719,17 +736,19 @@ JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const Jo
         hs = hs_own.get();
     }
     double pack_ms = std::chrono::duration<double, std::milli>(Clock::now() - tp).count();
+    mark("header_packed");
     std::vector<std::unique_ptr<detail::PackedLevel>> staged; // outlives the dataset handles below
     std::vector<detail::DatasetHandle> dr(G), dsh(G);
     const auto tu = Clock::now();
     for (size_t g = 0; g < G; ++g) {
         tj_ctx* ctx = detail::device_context(devices[g]);
-        detail::check(tj_dataset_begin(ctx, &hr->view, hr->n_vertices.data(), hr->n_facets.data(), &dr[g].p), ctx);
+        detail::check(tj_dataset_begin(ctx, &hr->view, hr->vb_ptrs.data(), hr->fb_ptrs.data(), &dr[g].p), ctx);
         out.stats.h2d_bytes += hr->bytes() + (self_join ? 0 : hs->bytes());
         if (!self_join)
-            detail::check(tj_dataset_begin(ctx, &hs->view, hs->n_vertices.data(), hs->n_facets.data(), &dsh[g].p), ctx);
+            detail::check(tj_dataset_begin(ctx, &hs->view, hs->vb_ptrs.data(), hs->fb_ptrs.data(), &dsh[g].p), ctx);
     }
     out.stats.upload_ms = std::chrono::duration<double, std::milli>(Clock::now() - tu).count();
+    mark("datasets_begun");
 
     std::vector<detail::ResultHandle> results(G);
     std::vector<std::exception_ptr> errors(G);
@@ -775,8 +794,7 @@ JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const Jo
                 const auto tl = Clock::now();
                 staged.push_back(detail::pack_level(D, H, static_cast<size_t>(slot), pool));
                 pack_ms += std::chrono::duration<double, std::milli>(Clock::now() - tl).count();
-                const tj_level_mesh_view& lv = staged.back()->view;
-                out.stats.h2d_bytes += G * (lv.n_vertices * 24 + lv.n_facets * 28 + H.facet_offsets[slot].back() * 4);
+                out.stats.h2d_bytes += G * (H.n_vertices[slot] * 24 + H.n_facets[slot] * 28 + H.facet_offsets[slot].back() * 4);
                 for (size_t g = 0; g < G; ++g) {
                     tj_dataset* ds = side == 0 ? dr[g].p : dsh[g].p;
                     auto& put = side == 0 ? put_r[g] : put_s[g];
@@ -784,6 +802,7 @@ JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const Jo
                     detail::check(tj_dataset_put_level(ds, static_cast<uint32_t>(slot), &staged.back()->view),
                                   detail::device_context(devices[g]));
                 }
+                mark(std::string(side == 0 ? "R" : "S") + "_lod" + std::to_string(level) + "_put");
             }
         }
     } catch (...) {
@@ -797,6 +816,7 @@ JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const Jo
         }
     }
     for (auto& t : joins) t.join();
+    mark("joins_done");
     for (size_t g = 0; g < G; ++g) {
         tj_dataset_sync(dr[g].p);
         if (!self_join) tj_dataset_sync(dsh[g].p);
@@ -914,6 +934,7 @@ JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const Jo
         flowing = sc.pairs_out;
     }
     out.stats.results = out.records.size();
+    mark("records_built");
     out.stats.total_ms = std::chrono::duration<double, std::milli>(Clock::now() - t_total).count();
     return out;
 }

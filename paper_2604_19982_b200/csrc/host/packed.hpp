@@ -56,7 +56,7 @@ struct PackedHeader {
     std::vector<std::vector<uint64_t>> facet_offsets;           // per level [nv+1]
     std::vector<std::vector<uint64_t>> vert_base, facet_base;   // per level [n_objects+1]
     std::vector<uint64_t> n_vertices, n_facets;                  // per level totals
-    std::vector<const uint64_t*> fo_ptrs;
+    std::vector<const uint64_t*> fo_ptrs, vb_ptrs, fb_ptrs;
     tj_dataset_view view{};
     uint64_t bytes() const; // H2D bytes of tj_dataset_begin
 };

@@ -8,6 +8,7 @@
 #include <pybind11/stl.h>
 
 #include <chrono>
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -43,10 +44,28 @@ JoinSpec make_spec(const std::string& type, double tau, uint32_t k, uint64_t fil
     return spec;
 }
 
+// (records, stats_json) as the reference's _core.join returns them (python/bindings.cpp:101-121);
+// built with the CPython API directly (one shared str per stage name).
 py::tuple pack_output(const JoinOutput& out) {
-    py::list records;
-    for (const JoinResultRecord& r : out.records)
-        records.append(py::make_tuple(r.r, r.s, r.lb, r.ub, stage_name(r.decided_at), r.rank));
+    const size_t n = out.records.size();
+    py::list records(n);
+    std::map<int16_t, py::str> names;
+    for (size_t i = 0; i < n; ++i) {
+        const JoinResultRecord& r = out.records[i];
+        auto it = names.find(r.decided_at);
+        if (it == names.end()) it = names.emplace(r.decided_at, py::str(stage_name(r.decided_at))).first;
+        PyObject* t = PyTuple_New(6);
+        if (!t) throw py::error_already_set();
+        PyTuple_SET_ITEM(t, 0, PyLong_FromUnsignedLong(r.r));
+        PyTuple_SET_ITEM(t, 1, PyLong_FromUnsignedLong(r.s));
+        PyTuple_SET_ITEM(t, 2, PyFloat_FromDouble(r.lb));
+        PyTuple_SET_ITEM(t, 3, PyFloat_FromDouble(r.ub));
+        PyObject* nm = it->second.ptr();
+        Py_INCREF(nm);
+        PyTuple_SET_ITEM(t, 4, nm);
+        PyTuple_SET_ITEM(t, 5, PyLong_FromUnsignedLong(r.rank));
+        PyList_SET_ITEM(records.ptr(), static_cast<Py_ssize_t>(i), t);
+    }
     return py::make_tuple(records, out.stats.to_json());
 }
 
@@ -198,6 +217,31 @@ PYBIND11_MODULE(_core, m) {
             return std::make_shared<PreparedDataset>(load_index(path));
         },
         py::arg("path"));
+
+    m.def(
+        "pack_timing",
+        [](std::shared_ptr<PreparedDataset> R, unsigned workers) {
+            // host-side cost of the streamed upload's packing (diagnostics for bench.py)
+            using Clock = std::chrono::steady_clock;
+            py::dict d;
+            py::gil_scoped_release release;
+            ThreadPool pool(workers);
+            auto t0 = Clock::now();
+            auto h = detail::pack_header(*R, pool);
+            double ms = std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+            std::vector<double> lv;
+            for (size_t li = 0; li < R->lod_schedule.size(); ++li) {
+                t0 = Clock::now();
+                auto p = detail::pack_level(*R, *h, li, pool);
+                lv.push_back(std::chrono::duration<double, std::milli>(Clock::now() - t0).count());
+            }
+            py::gil_scoped_acquire acquire;
+            d["header_ms"] = ms;
+            d["level_ms"] = lv;
+            d["workers"] = pool.size();
+            return d;
+        },
+        py::arg("R"), py::arg("workers") = 0u);
 
     m.def(
         "save_dataset",

@@ -141,7 +141,7 @@ uint64_t knn_fixpoint(Workspace& ws, CandDevStore& cs, uint32_t k, int16_t stage
     TJ_CUDA(cudaGetLastError());
     unsigned long long h = 0;
     TJ_CUDA(cudaMemcpyAsync(&h, total.p, 8, cudaMemcpyDeviceToHost, st));
-    TJ_CUDA(cudaStreamSynchronize(st));
+    stream_sync(st);
     return h;
 }
 
@@ -156,6 +156,6 @@ void knn_finalize_dev(Workspace& ws, CandDevStore& cs, uint32_t k, cudaStream_t 
     count_launch();
     k_knn_finalize<<<grid, 256, 0, st>>>(cs.view(), cs.nq, k, delta.p);
     TJ_CUDA(cudaGetLastError());
-    TJ_CUDA(cudaStreamSynchronize(st));
+    stream_sync(st);
 }
 } // namespace tjx

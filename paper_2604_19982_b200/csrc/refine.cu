@@ -430,6 +430,7 @@ __global__ void __launch_bounds__(128) k_eval(RefineSource src, RefineQueue q, u
     __shared__ double rec[128][2][kFacetWords];
     const uint32_t ra = smem_addr(&rec[threadIdx.x][0][0]), sb = smem_addr(&rec[threadIdx.x][1][0]);
     unsigned long long n = *q.count;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && n > q.capacity) atomicMax(q.count + 1, n); // overflow record
     if (n > q.capacity) n = q.capacity;
     unsigned long long done = 0;
     for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < n;
@@ -505,27 +506,20 @@ void refine_pass(const RefineSource& src, uint64_t vp_begin, uint64_t vp_end, bo
     if (seed) {
         // 2 entries per voxel pair at most
         if (2 * (vp_end - vp_begin) > qs.items.n) qs.items.alloc(2 * (vp_end - vp_begin));
-        TJ_CUDA(cudaMemsetAsync(qs.count.p, 0, 16, st));
+        TJ_CUDA(cudaMemsetAsync(qs.count.p, 0, 8, st));
         TJ_CUDA(cudaMemsetAsync(work, 0, 8, st));
         count_launch();
         k_seed<<<warp_grid(vp_end - vp_begin, num_sms, 4), 256, 0, st>>>(src, vp_begin, vp_end, qs.view(), work);
         TJ_CUDA(cudaGetLastError());
     } else {
-        for (int attempt = 0; attempt < 3; ++attempt) {
-            TJ_CUDA(cudaMemsetAsync(qs.count.p, 0, 16, st));
-            TJ_CUDA(cudaMemsetAsync(work, 0, 8, st));
-            count_launch();
-            k_screen<<<warp_grid(vp_end - vp_begin, num_sms, 2), kScreenThreads, kScreenSmem, st>>>(
-                src, vp_begin, vp_end, lb_bits, ub_bits, cull, qs.view(), work,
-                attempt ? nullptr : counters);
-            TJ_CUDA(cudaGetLastError());
-            unsigned long long n[2] = {0, 0};
-            TJ_CUDA(cudaMemcpyAsync(n, qs.count.p, 16, cudaMemcpyDeviceToHost, st));
-            TJ_CUDA(cudaStreamSynchronize(st));
-            if (n[0] <= qs.items.n) break;
-            // queue overflow: grow and re-run the (deterministic) pass; nothing was evaluated yet
-            qs.items.alloc(n[0] + n[0] / 4);
-        }
+        // No host round trip: a queue overflow only drops entries, k_eval records the largest
+        // count in count[1] and the caller re-runs the whole level with a larger queue.
+        TJ_CUDA(cudaMemsetAsync(qs.count.p, 0, 8, st));
+        TJ_CUDA(cudaMemsetAsync(work, 0, 8, st));
+        count_launch();
+        k_screen<<<warp_grid(vp_end - vp_begin, num_sms, 2), kScreenThreads, kScreenSmem, st>>>(
+            src, vp_begin, vp_end, lb_bits, ub_bits, cull, qs.view(), work, counters);
+        TJ_CUDA(cudaGetLastError());
     }
     count_launch();
     k_eval<<<grid, 128, 0, st>>>(src, qs.view(), lb_bits, ub_bits, counters);

@@ -30,6 +30,10 @@ __global__ void k_fill_u64(unsigned long long* p, uint64_t n, unsigned long long
         p[i] = v;
 }
 
+__global__ void k_init_agg(unsigned* agg) {
+    if (threadIdx.x < 8) agg[threadIdx.x] = (threadIdx.x == 0 || threadIdx.x == 3) ? 0x7f800000u : 0u;
+}
+
 __global__ void k_facet_pairs(const ActiveVpDev* __restrict__ act, uint64_t n, const uint64_t* __restrict__ rf,
                               const uint64_t* __restrict__ sf, unsigned long long* out) {
     unsigned long long acc = 0;
@@ -103,7 +107,7 @@ int level_slot(const DatasetDev& d, uint32_t level) {
 void check_error(DevError* err, cudaStream_t st) {
     DevError h;
     TJ_CUDA(cudaMemcpyAsync(&h, err, sizeof(DevError), cudaMemcpyDeviceToHost, st));
-    TJ_CUDA(cudaStreamSynchronize(st));
+    stream_sync(st);
     if (h.code == 0) return;
     if (h.kind == 1) throw Error(TJ_EENGINE, "knn_apply_deltas: confirmed count exceeds k");
     throw Error(TJ_EENGINE, "bound crossing: lb " + std::to_string(h.lb) + " > ub " + std::to_string(h.ub));
@@ -123,7 +127,7 @@ uint64_t compact_active(Workspace& ws, const CandDevStore& cs, DevBuf<ActiveVpDe
     TJ_CUDA(cub::DeviceSelect::If(ws.temp.p, bytes, active.p, out.p, nsel.p, (int64_t)n, pred, st));
     int64_t h = 0;
     TJ_CUDA(cudaMemcpyAsync(&h, nsel.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    TJ_CUDA(cudaStreamSynchronize(st));
+    stream_sync(st);
     active = std::move(out);
     return (uint64_t)h;
 }
@@ -154,18 +158,9 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
             LevelStats ls{};
             ls.level = level;
             ls.vps = n_active;
-            count_launch();
-            k_fill_u64<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(lbb.p, n, kInfBits);
-            count_launch();
-            k_fill_u64<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(ubb.p, n, kInfBits);
-            TJ_CUDA(cudaMemsetAsync(counters.p, 0, kNumCounters * 8, st));
-            count_launch();
-            k_facet_pairs<<<grid_for(n_active, 256, ws.num_sms), 256, 0, st>>>(
-                active.p, n_active, R.facet_offsets[sr].p, S.facet_offsets[ss].p, counters.p + 2);
             // streamed datasets: this level's facets may still be in flight
             ls.wait_ms = level_ready(R, sr, st);
             if (&S != &R) ls.wait_ms += level_ready(S, ss, st);
-            TJ_CUDA(cudaEventRecord(e0, st));
             RefineSource src{};
             src.active = active.p;
             src.r_foff = R.facet_offsets[sr].p;
@@ -177,8 +172,8 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
             {   // FP32 screening records of this level's facets, once per facet, + their aggregates
                 const uint64_t nr = R.level_entries[sr], ns = S.level_entries[ss];
                 ws.level_agg.reserve(8);
-                const unsigned init[8] = {0x7f800000u, 0u, 0u, 0x7f800000u, 0u, 0u, 0u, 0u};
-                TJ_CUDA(cudaMemcpyAsync(ws.level_agg.p, init, sizeof(init), cudaMemcpyHostToDevice, st));
+                count_launch();
+                k_init_agg<<<1, 32, 0, st>>>(ws.level_agg.p);
                 src.agg = ws.level_agg.p;
                 ws.screen_r.reserve(std::max<uint64_t>(nr * 7, 1));
                 refine_prep(R.facets[sr].p, nr, ws.screen_r.p, ws.level_agg.p, ws.num_sms, st);
@@ -197,15 +192,36 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
             }
             // 0: every facet pair; 1: exact-preserving culling; 2: decision-mode culling
             const int cull = (spec.flags & TJ_FLAG_NO_CULL) ? 0 : decision ? 2 : 1;
-            // seeds for every voxel pair first (op thresholds), then the screened passes
-            if (cull)
+            unsigned long long hc[kNumCounters];
+            for (;;) {
+                count_launch();
+                k_fill_u64<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(lbb.p, n, kInfBits);
+                count_launch();
+                k_fill_u64<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(ubb.p, n, kInfBits);
+                TJ_CUDA(cudaMemsetAsync(counters.p, 0, kNumCounters * 8, st));
+                TJ_CUDA(cudaMemsetAsync(queue.count.p, 0, 16, st));
+                count_launch();
+                k_facet_pairs<<<grid_for(n_active, 256, ws.num_sms), 256, 0, st>>>(
+                    active.p, n_active, R.facet_offsets[sr].p, S.facet_offsets[ss].p, counters.p + 2);
+                TJ_CUDA(cudaEventRecord(e0, st));
+                // seeds for every voxel pair first (op thresholds), then the screened passes
+                if (cull)
+                    for (uint64_t c0 = 0; c0 < n_active; c0 += launch)
+                        refine_pass(src, c0, std::min(n_active, c0 + launch), true, lbb.p, ubb.p, cull, queue, work.p,
+                                    counters.p, ws.num_sms, st);
                 for (uint64_t c0 = 0; c0 < n_active; c0 += launch)
-                    refine_pass(src, c0, std::min(n_active, c0 + launch), true, lbb.p, ubb.p, cull, queue, work.p,
+                    refine_pass(src, c0, std::min(n_active, c0 + launch), false, lbb.p, ubb.p, cull, queue, work.p,
                                 counters.p, ws.num_sms, st);
-            for (uint64_t c0 = 0; c0 < n_active; c0 += launch)
-                refine_pass(src, c0, std::min(n_active, c0 + launch), false, lbb.p, ubb.p, cull, queue, work.p,
-                            counters.p, ws.num_sms, st);
-            TJ_CUDA(cudaEventRecord(e1, st));
+                TJ_CUDA(cudaEventRecord(e1, st));
+                unsigned long long ovf = 0;
+                TJ_CUDA(cudaMemcpyAsync(hc, counters.p, sizeof(hc), cudaMemcpyDeviceToHost, st));
+                TJ_CUDA(cudaMemcpyAsync(&ovf, queue.count.p + 1, 8, cudaMemcpyDeviceToHost, st));
+                stream_sync(st);
+                if (ovf == 0) break;
+                // an exact-evaluation queue overflowed somewhere in the level: grow it and
+                // redo the level (the screen is deterministic given the same evaluations)
+                queue.items.alloc(ovf + ovf / 4);
+            }
             out.chunks += (n_active + spec.refine_chunk - 1) / spec.refine_chunk;
             count_launch();
             k_aggregate<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(cs.view(), n, lbb.p, ubb.p, knn ? 0 : 1, tau,
@@ -218,9 +234,6 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
                 knn_fixpoint(ws, cs, spec.k, (int16_t)level, err, st);
                 check_error(err, st);
             }
-            unsigned long long hc[kNumCounters];
-            TJ_CUDA(cudaMemcpyAsync(hc, counters.p, sizeof(hc), cudaMemcpyDeviceToHost, st));
-            TJ_CUDA(cudaStreamSynchronize(st));
             float kms = 0.f;
             TJ_CUDA(cudaEventElapsedTime(&kms, e0, e1));
             ls.tested = hc[0];

@@ -41,6 +41,10 @@ inline cudaStream_t& alloc_stream() {
     return s;
 }
 
+// Blocking wait for the work queued on `st` so far: the calling thread sleeps (blocking-sync
+// event) instead of spinning, leaving its core to the host packing threads of run_join.
+void stream_sync(cudaStream_t st);
+
 // Minimal owning device buffer.
 template <class T>
 struct DevBuf {
@@ -98,8 +102,13 @@ struct DatasetDev {
     std::vector<DevBuf<double>> facets;          // per level [entries*12]
     uint64_t bytes = 0;
     std::vector<uint64_t> level_entries;         // per level: facet records (CSR entries)
-    std::vector<uint64_t> level_vertices, level_facets; // streamed: compact-form sizes per level
-    std::shared_ptr<LevelGate> gate;             // streamed datasets only (else all levels resident)
+    // streamed datasets only (tj_dataset_begin): per-level object bases, voxel -> object,
+    // validation flag of the device-side expansion, arrival gate
+    std::vector<DevBuf<uint64_t>> vert_base, facet_base; // per level [n_obj+1]
+    std::vector<uint64_t> level_vertices, level_facets;  // per level totals
+    DevBuf<uint32_t> vox_obj;                            // [nv]
+    DevBuf<int> stream_err;                              // [1]: an index out of range
+    std::shared_ptr<LevelGate> gate;
 };
 
 // Makes `st` wait until level slot `slot` of `d` is resident (no-op for uploaded datasets);
@@ -155,7 +164,7 @@ struct RefineQueue {
 
 struct RefineQueueStore {
     DevBuf<PairRef> items;              // exact-evaluation queue
-    DevBuf<unsigned long long> count;
+    DevBuf<unsigned long long> count; // [0] entries of the current pass, [1] largest overflowing count
     RefineQueueStore() : count(2) { items.alloc(1u << 22); }
     RefineQueue view() { return {items.p, (unsigned long long)items.n, count.p}; }
 };

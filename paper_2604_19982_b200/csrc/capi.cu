@@ -670,7 +670,7 @@ int tj_refine_batch(tj_ctx* ctx, uint64_t n_tris, const double* tris, const doub
         src.s_len = sl.p;
         src.r_facets = f.p;
         src.s_facets = f.p;
-        DevBuf<float4> scr(std::max<uint64_t>(n_tris, 1) * 7);
+        DevBuf<float4> scr(std::max<uint64_t>(n_tris, 1) * kScreenRecF4);
         refine_prep(f.p, n_tris, scr.p, nullptr, ctx->ws.num_sms, st);
         src.r_box = src.s_box = scr.p;
         src.r_geo = src.s_geo = scr.p + 3 * n_tris;

@@ -60,6 +60,7 @@ struct Workspace {
     std::unique_ptr<RefineQueueStore> queue; // refinement pair queues, grow-only, per context
     DevBuf<float4> screen_r, screen_s;       // per-level FP32 screening records, grow-only
     DevBuf<unsigned> level_agg;              // per-level record aggregates (RefineSource::agg)
+    DevBuf<float4> seg_r, seg_s;             // per-level voxel segment aggregates, grow-only
     void release() {
         temp.release();
         u64a.release();
@@ -67,6 +68,8 @@ struct Workspace {
         screen_r.release();
         screen_s.release();
         level_agg.release();
+        seg_r.release();
+        seg_s.release();
     }
 };
 

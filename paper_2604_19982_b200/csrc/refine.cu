@@ -13,6 +13,7 @@ namespace {
 
 struct VpDescDev {
     uint32_t op;
+    uint32_t gvr, gvs; // global voxel ids (join mode)
     uint64_t r0, s0; // first facet (record index) of each segment
     uint32_t rn, sn;
     double iv_lb, iv_ub;
@@ -23,6 +24,8 @@ __device__ __forceinline__ VpDescDev get_vp(const RefineSource& src, uint64_t vp
     if (src.active) { // join mode
         const ActiveVpDev av = src.active[vp];
         d.op = av.op;
+        d.gvr = av.gvr;
+        d.gvs = av.gvs;
         d.r0 = src.r_foff[av.gvr];
         d.rn = (uint32_t)(src.r_foff[av.gvr + 1] - d.r0);
         d.s0 = src.s_foff[av.gvs];
@@ -31,6 +34,7 @@ __device__ __forceinline__ VpDescDev get_vp(const RefineSource& src, uint64_t vp
         d.iv_ub = src.cand_ub[av.op];
     } else { // batch mode: every voxel pair is its own op, interval [0, +inf]
         d.op = (uint32_t)vp;
+        d.gvr = d.gvs = 0;
         d.r0 = src.r_off[vp];
         d.rn = src.r_len[vp];
         d.s0 = src.s_off[vp];
@@ -39,6 +43,25 @@ __device__ __forceinline__ VpDescDev get_vp(const RefineSource& src, uint64_t vp
         d.iv_ub = __longlong_as_double(0x7ff0000000000000ll);
     }
     return d;
+}
+
+// Segment aggregates of a voxel pair: precomputed per voxel (join mode) or reduced here.
+__device__ __forceinline__ SegAgg seg_r_of(const RefineSource& src, const VpDescDev& d) {
+    return src.r_seg ? seg_load(src.r_seg + 3ull * d.gvr) : seg_reduce(src.r_box, d.r0, d.rn);
+}
+__device__ __forceinline__ SegAgg seg_s_of(const RefineSource& src, const VpDescDev& d) {
+    return src.s_seg ? seg_load(src.s_seg + 3ull * d.gvs) : seg_reduce(src.s_box, d.s0, d.sn);
+}
+
+__global__ void k_seg_prep(const float4* __restrict__ box, const uint64_t* __restrict__ foff, uint64_t n_voxels,
+                           float4* __restrict__ seg) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t v = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); v < n_voxels; v += warps) {
+        const uint64_t f0 = foff[v];
+        const SegAgg g = seg_reduce(box, f0, (uint32_t)(foff[v + 1] - f0));
+        if (lane == 0) seg_store(seg + 3 * v, g);
+    }
 }
 
 // Warp-aggregated append of one pair per lane with `want` set (all lanes must call);
@@ -58,15 +81,17 @@ __device__ __forceinline__ void queue_push(const RefineQueue& q, bool want, uint
 }
 
 // Cooperative gather of up to 32 screening records (facets first + list[k]) into shared
-// memory: box part from `box`, geometry part from `geo` (7 float4 per record in smem).
+// memory: box part from `box`, geometry part from `geo` (kRecF4 float4 per record, rows
+// kCS floats apart).
 __device__ __forceinline__ void gather_recs(const float4* __restrict__ box, const float4* __restrict__ geo,
                                             uint64_t first, const uint16_t* list, int n, float* dst) {
     const int lane = threadIdx.x & 31;
     float4* d4 = reinterpret_cast<float4*>(dst);
-    for (int k = lane; k < 7 * n; k += 32) {
-        const int rec = k / 7, part = k - 7 * (k / 7);
+    for (int k = lane; k < kRecF4 * n; k += 32) {
+        const int rec = k / kRecF4, part = k % kRecF4;
         const uint64_t f = first + list[rec];
-        d4[k] = part < kBoxF4 ? __ldg(box + f * kBoxF4 + part) : __ldg(geo + f * kGeoF4 + (part - kBoxF4));
+        d4[rec * (kCS / 4) + part] =
+            part < kBoxF4 ? __ldg(box + f * kBoxF4 + part) : __ldg(geo + f * kGeoF4 + (part - kBoxF4));
     }
 }
 
@@ -132,11 +157,47 @@ __device__ __forceinline__ uint32_t closest_facet(const float4* __restrict__ set
     return bi;
 }
 
+// Facets i* of r closest (box gap, then centre distance) to box b_s and j* of s closest to
+// box b_r, in one sweep over both segments.
+__device__ __forceinline__ void closest_pair(const float4* __restrict__ rset, uint64_t r0, uint32_t rn,
+                                             const float4* __restrict__ sset, uint64_t s0, uint32_t sn,
+                                             const SegAgg& sr, const SegAgg& ss, uint32_t& ist, uint32_t& jst) {
+    const int lane = threadIdx.x & 31;
+    auto key_of = [](float4 a, float4 b, const SegAgg& o) {
+        const float rec[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        const float box[8] = {o.lo[0], o.lo[1], o.lo[2], 0.f, o.hi[0], o.hi[1], o.hi[2], 0.f};
+        const float g = box_gap_lb(rec, box);
+        const float dx = 0.5f * (a.x + b.x) - 0.5f * (o.lo[0] + o.hi[0]);
+        const float dy = 0.5f * (a.y + b.y) - 0.5f * (o.lo[1] + o.hi[1]);
+        const float dz = 0.5f * (a.z + b.z) - 0.5f * (o.lo[2] + o.hi[2]);
+        // gap dominates; the centre distance only orders near-ties (deepest overlap first)
+        return g + 1e-3f * sqrtf(dx * dx + dy * dy + dz * dz);
+    };
+    const float kInfF = __int_as_float(0x7f800000);
+    float br = kInfF, bs = kInfF;
+    uint32_t ir = 0xffffffffu, is = 0xffffffffu;
+    for (uint32_t i = lane; i < max(rn, sn); i += 32) {
+        if (i < rn) {
+            const float k = key_of(__ldg(rset + (r0 + i) * kBoxF4), __ldg(rset + (r0 + i) * kBoxF4 + 1), ss);
+            if (k < br) { br = k; ir = i; }
+        }
+        if (i < sn) {
+            const float k = key_of(__ldg(sset + (s0 + i) * kBoxF4), __ldg(sset + (s0 + i) * kBoxF4 + 1), sr);
+            if (k < bs) { bs = k; is = i; }
+        }
+    }
+    warp_argmin(br, ir);
+    warp_argmin(bs, is);
+    ist = ir;
+    jst = is;
+}
+
 // Seed pass, warp per voxel pair, O(r + s): i* = the r facet closest (box gap) to the s
 // segment's box, j* symmetrically; then j' = the s facet closest to i* and i' the r facet
-// closest to j*. Queues (i*, j') and (i', j*).
+// closest to j*; queues (i*, j') and (i', j*). In decision mode only voxel pairs that can
+// hold a zero bound are seeded (segment gap <= ph_max(r) + ph_max(s)).
 __global__ void __launch_bounds__(256) k_seed(RefineSource src, uint64_t vp_begin, uint64_t vp_end, RefineQueue q,
-                                              unsigned long long* work) {
+                                              unsigned long long* work, int cull) {
     const int lane = threadIdx.x & 31;
     for (;;) {
         unsigned long long vp = 0;
@@ -145,23 +206,27 @@ __global__ void __launch_bounds__(256) k_seed(RefineSource src, uint64_t vp_begi
         if (vp >= vp_end) break;
         const VpDescDev d = get_vp(src, vp);
         if (d.rn == 0 || d.sn == 0) continue;
-        const SegAgg ar = seg_reduce(src.r_box, d.r0, d.rn);
-        const SegAgg as = seg_reduce(src.s_box, d.s0, d.sn);
-        const uint32_t ist = closest_facet(src.r_box, d.r0, d.rn, as.lo, as.hi);
-        const uint32_t jst = closest_facet(src.s_box, d.s0, d.sn, ar.lo, ar.hi);
-        float blo[3], bhi[3];
+        const SegAgg ar = seg_r_of(src, d);
+        const SegAgg as = seg_s_of(src, d);
+        if (cull == 2) {
+            const float arec[8] = {ar.lo[0], ar.lo[1], ar.lo[2], 0.f, ar.hi[0], ar.hi[1], ar.hi[2], 0.f};
+            const float brec[8] = {as.lo[0], as.lo[1], as.lo[2], 0.f, as.hi[0], as.hi[1], as.hi[2], 0.f};
+            if (box_gap_lb(arec, brec) > __fadd_ru(ar.phmax, as.phmax)) continue;
+        }
+        uint32_t ist, jst;
+        closest_pair(src.r_box, d.r0, d.rn, src.s_box, d.s0, d.sn, ar, as, ist, jst);
+        // second round: the partner facet closest to each first-round facet
+        SegAgg fi = ar, fj = as; // only lo / hi are read
         {
             const float4 a = __ldg(src.r_box + (d.r0 + ist) * kBoxF4), b = __ldg(src.r_box + (d.r0 + ist) * kBoxF4 + 1);
-            blo[0] = a.x; blo[1] = a.y; blo[2] = a.z; bhi[0] = b.x; bhi[1] = b.y; bhi[2] = b.z;
+            fi.lo[0] = a.x; fi.lo[1] = a.y; fi.lo[2] = a.z; fi.hi[0] = b.x; fi.hi[1] = b.y; fi.hi[2] = b.z;
+            const float4 c = __ldg(src.s_box + (d.s0 + jst) * kBoxF4), e = __ldg(src.s_box + (d.s0 + jst) * kBoxF4 + 1);
+            fj.lo[0] = c.x; fj.lo[1] = c.y; fj.lo[2] = c.z; fj.hi[0] = e.x; fj.hi[1] = e.y; fj.hi[2] = e.z;
         }
-        const uint32_t jp = closest_facet(src.s_box, d.s0, d.sn, blo, bhi);
-        {
-            const float4 a = __ldg(src.s_box + (d.s0 + jst) * kBoxF4), b = __ldg(src.s_box + (d.s0 + jst) * kBoxF4 + 1);
-            blo[0] = a.x; blo[1] = a.y; blo[2] = a.z; bhi[0] = b.x; bhi[1] = b.y; bhi[2] = b.z;
-        }
-        const uint32_t ip = closest_facet(src.r_box, d.r0, d.rn, blo, bhi);
+        uint32_t ip, jp;
+        closest_pair(src.r_box, d.r0, d.rn, src.s_box, d.s0, d.sn, fi, fj, ip, jp);
         queue_push(q, lane == 0, d.op, (uint32_t)(d.r0 + ist), (uint32_t)(d.s0 + jp));
-        queue_push(q, lane == 0 && !(ip == ist && jst == jp), d.op, (uint32_t)(d.r0 + ip), (uint32_t)(d.s0 + jst));
+        queue_push(q, lane == 0 && !(ip == ist && jp == jst), d.op, (uint32_t)(d.r0 + ip), (uint32_t)(d.s0 + jst));
     }
 }
 
@@ -291,26 +356,30 @@ __global__ void __launch_bounds__(256, 2) k_screen(RefineSource src, uint64_t vp
         }
         // nothing can change lb' or ub': the whole voxel pair is irrelevant
         if (cull && (th.lb_sat || th.lb_u == 0.f) && th.ub_u == 0.f) continue;
-        // hierarchical screens (voxel pair, rows, columns) only where they can pay off
+        // hierarchical screens: the whole voxel pair (always when the segment aggregates are
+        // precomputed), then rows / columns where that can pay off
         const bool hier = cull && d.rn * d.sn >= kHierMinPairs;
         float delta0 = 0.f; // tile-pair value when !hier
-        if (hier) {
-            const SegAgg ar = seg_reduce(src.r_box, d.r0, d.rn);
-            const SegAgg as = seg_reduce(src.s_box, d.s0, d.sn);
-            // delta0 >= 1e-5 (L_i + L_j) + 1e-12 (M_i + M_j) for every pair of the voxel pair
-            delta0 = __fadd_ru(__fmul_ru(2e-5f, fmaxf(ar.Lmax, as.Lmax)), __fmul_ru(2e-12f, fmaxf(seg_m(ar), seg_m(as))));
+        if (cull && (hier || src.r_seg)) {
+            const SegAgg ar = seg_r_of(src, d);
+            const SegAgg as = seg_s_of(src, d);
+            // d0 >= 1e-5 (L_i + L_j) + 1e-12 (M_i + M_j) for every pair of the voxel pair
+            const float d0 = __fadd_ru(__fmul_ru(2e-5f, fmaxf(ar.Lmax, as.Lmax)), __fmul_ru(2e-12f, fmaxf(seg_m(ar), seg_m(as))));
             if (ar.ok && as.ok &&
                 agg_skip(ar.lo, ar.hi, as.lo, as.hi, ar.Lmax + as.Lmax, fminf(ar.Lmin, as.Lmin),
-                         __fadd_ru(ar.phmax, as.phmax), __fadd_rd(ar.hdmin, as.hdmin), delta0, th)) {
+                         __fadd_ru(ar.phmax, as.phmax), __fadd_rd(ar.hdmin, as.hdmin), d0, th)) {
                 ++vps_skipped;
                 continue;
             }
-            __syncwarp();
-            if (lane == 0) {
-                sm.seg_r = ar;
-                sm.seg_s = as;
+            if (hier) {
+                delta0 = d0;
+                __syncwarp();
+                if (lane == 0) {
+                    sm.seg_r = ar;
+                    sm.seg_s = as;
+                }
+                __syncwarp();
             }
-            __syncwarp();
         }
         for (uint32_t rc0 = 0; rc0 < d.rn; rc0 += kCap) {
             const int nrl = build_list(src.r_box, d.r0 + rc0, min((uint32_t)kCap, d.rn - rc0), sm.seg_s, delta0, th, hier,
@@ -356,16 +425,15 @@ __global__ void __launch_bounds__(256, 2) k_screen(RefineSource src, uint64_t vp
                         const float rlb = lb_settled ? ninf : __fadd_ru(__fadd_ru(th.lb_u, dl), ar.ph);
                         const float rub = th.ub_u == 0.f ? ninf : __fsub_ru(__fadd_ru(th.ub_u, dl), ar.hd);
                         const int iters = (scnt - jj + P - 1) / P; // this lane's s facets
+                        if (lane == 0) tested += (uint32_t)(rcnt * scnt);
                         const int max_iters = (scnt + P - 1) / P;
                         int nq = 0;
                         for (int t = 0;; ++t) {
                             if (t < max_iters) {
                                 const int bj = jj + t * P;
                                 bool need = false;
-                                if (row_on && t < iters) {
+                                if (row_on && t < iters)
                                     need = !cull || stage1_need_rr(ar, sm.rc + bi * kCS, sm.sc + bj * kCS, rlb, rub);
-                                    ++tested;
-                                }
                                 if (!cull) {
                                     queue_push(q, need, d.op, (uint32_t)(d.r0 + rc0 + sm.rl[rt0 + bi]),
                                                (uint32_t)(d.s0 + sc0 + sm.sl[st0 + bj]));
@@ -493,6 +561,15 @@ void refine_prep(const double* facets, uint64_t n, float4* out, unsigned* agg, i
     TJ_CUDA(cudaGetLastError());
 }
 
+void refine_seg_prep(const float4* box, const uint64_t* foff, uint64_t n_voxels, float4* seg, int num_sms,
+                     cudaStream_t st) {
+    if (!n_voxels) return;
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((n_voxels + 7) / 8, (uint64_t)num_sms * 16));
+    count_launch();
+    k_seg_prep<<<grid, 256, 0, st>>>(box, foff, n_voxels, seg);
+    TJ_CUDA(cudaGetLastError());
+}
+
 void refine_pass(const RefineSource& src, uint64_t vp_begin, uint64_t vp_end, bool seed, unsigned long long* lb_bits,
                  unsigned long long* ub_bits, int cull, RefineQueueStore& qs, unsigned long long* work,
                  unsigned long long* counters, int num_sms, cudaStream_t st) {
@@ -509,7 +586,7 @@ void refine_pass(const RefineSource& src, uint64_t vp_begin, uint64_t vp_end, bo
         TJ_CUDA(cudaMemsetAsync(qs.count.p, 0, 8, st));
         TJ_CUDA(cudaMemsetAsync(work, 0, 8, st));
         count_launch();
-        k_seed<<<warp_grid(vp_end - vp_begin, num_sms, 4), 256, 0, st>>>(src, vp_begin, vp_end, qs.view(), work);
+        k_seed<<<warp_grid(vp_end - vp_begin, num_sms, 8), 256, 0, st>>>(src, vp_begin, vp_end, qs.view(), work, cull);
         TJ_CUDA(cudaGetLastError());
     } else {
         // No host round trip: a queue overflow only drops entries, k_eval records the largest

@@ -42,14 +42,16 @@
 #include <cstdint>
 
 #include "geom_exact.cuh"
+#include "tj_internal.cuh"
 
 namespace tjx {
 
 constexpr int kRT = 32;    // r facets per screening tile
 constexpr int kST = 32;    // s facets per screening tile
-constexpr int kCS = 28;    // floats per screening record (7 x float4)
+constexpr int kCS = 36;    // shared-memory stride of a screening record (32 floats + 4 pad: bank shift)
+constexpr int kRecF4 = kScreenRecF4; // float4 per screening record (floats 0-31)
 constexpr int kBoxF4 = 3;  // box part of a record (floats 0-11), its own array: 3 float4 per facet
-constexpr int kGeoF4 = 4;  // geometry part (floats 12-27): 4 float4 per facet
+constexpr int kGeoF4 = 5;  // geometry part (floats 12-31): 5 float4 per facet
 constexpr int kQueue = 64; // per-warp SAT queue (< 32 pending + 32 new)
 constexpr int kCap = 128;  // per-warp survivor lists: facets per raw segment chunk
 constexpr uint32_t kHierMinPairs = 1024; // voxel pairs with fewer facet pairs skip the hierarchical screens
@@ -73,6 +75,8 @@ struct SegAgg {
 //  8-10 unit normal   11 ph (ru)
 //  12-20 unit edge directions (v1-v0, v2-v1, v0-v2)
 //  21-23 v1 - v0   24-26 v2 - v0   (FP64 differences rounded to FP32)   27 M (max |coordinate|)
+//  28-31 (int bits) the unit normal and the 3 unit edge directions quantised to int8x3
+//        (round(127 x), 4th byte 0) for the DP4A conditioning pre-test (stage1_need_rr)
 struct __align__(16) ScreenSmem {
     float rc[kRT * kCS];
     float sc[kST * kCS];
@@ -97,6 +101,14 @@ __device__ __forceinline__ void load_facet(const double* __restrict__ g, double*
         c[2 * k] = t.x;
         c[2 * k + 1] = t.y;
     }
+}
+
+// int8x3 quantisation of an FP32 unit vector: round(127 x) per component, 4th byte 0.
+__device__ __forceinline__ int quant_dir(const float* u) {
+    int q = 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) q |= (__float2int_rn(127.f * fminf(1.f, fmaxf(-1.f, u[k]))) & 0xff) << (8 * k);
+    return q;
 }
 
 // Screening record of one facet record (TJ_FACET_STRIDE doubles).
@@ -138,6 +150,8 @@ __device__ __forceinline__ void make_screen(const double* __restrict__ g, float*
     cr[26] = (float)e02.z;
     cr[27] = fmaxf(fmaxf(fmaxf(fabsf(cr[0]), fabsf(cr[1])), fmaxf(fabsf(cr[2]), fabsf(cr[4]))),
                    fmaxf(fabsf(cr[5]), fabsf(cr[6]))); // M: max |coordinate|
+#pragma unroll
+    for (int k = 0; k < 4; ++k) cr[28 + k] = __int_as_float(quant_dir(cr + at[k]));
 }
 
 // Rigorous lower bound of the gap between two outward-rounded boxes (lo at b+0, hi at b+4).
@@ -237,6 +251,23 @@ __device__ __forceinline__ SegAgg seg_reduce(const float4* __restrict__ box, uin
     return g;
 }
 
+// Segment aggregates stored per voxel (3 float4: lo.xyz Lmax | hi.xyz Lmin | phmax hdmin ok 0).
+__device__ __forceinline__ void seg_store(float4* dst, const SegAgg& g) {
+    dst[0] = make_float4(g.lo[0], g.lo[1], g.lo[2], g.Lmax);
+    dst[1] = make_float4(g.hi[0], g.hi[1], g.hi[2], g.Lmin);
+    dst[2] = make_float4(g.phmax, g.hdmin, g.ok ? 1.f : 0.f, 0.f);
+}
+__device__ __forceinline__ SegAgg seg_load(const float4* __restrict__ src) {
+    const float4 a = __ldg(src), b = __ldg(src + 1), c = __ldg(src + 2);
+    SegAgg g;
+    g.lo[0] = a.x; g.lo[1] = a.y; g.lo[2] = a.z; g.Lmax = a.w;
+    g.hi[0] = b.x; g.hi[1] = b.y; g.hi[2] = b.z; g.Lmin = b.w;
+    g.phmax = c.x;
+    g.hdmin = c.y;
+    g.ok = c.z != 0.f;
+    return g;
+}
+
 // Max |coordinate| of a segment (bounds every facet's M).
 __device__ __forceinline__ float seg_m(const SegAgg& g) {
     return fmaxf(fmaxf(fmaxf(fabsf(g.lo[0]), fabsf(g.lo[1])), fmaxf(fabsf(g.lo[2]), fabsf(g.hi[0]))),
@@ -297,18 +328,21 @@ __device__ __forceinline__ bool stage1_need(const float4& a0, const float4& a1, 
     return !(lb_ok && ub_ok && shapes);
 }
 
-// The r-side box of the register-blocked stage-1 loop (floats 0-7 and 11 of a screening
-// record, held in registers by the lane that owns the r facet).
+// The r-side part of the register-blocked stage-1 loop (floats 0-7, 11 and the quantised
+// directions 28-31 of a screening record, held in registers by the lane owning the r facet).
 struct RowRec {
     float lo[3], hi[3], L, hd, ph;
+    int q[4];
 };
 
 __device__ __forceinline__ RowRec load_row(const float* a) {
     RowRec r;
     const float4 p0 = *reinterpret_cast<const float4*>(a), p1 = *reinterpret_cast<const float4*>(a + 4);
+    const int4 pq = *reinterpret_cast<const int4*>(a + 28);
     r.lo[0] = p0.x; r.lo[1] = p0.y; r.lo[2] = p0.z; r.L = p0.w;
     r.hi[0] = p1.x; r.hi[1] = p1.y; r.hi[2] = p1.z; r.hd = p1.w;
     r.ph = a[11];
+    r.q[0] = pq.x; r.q[1] = pq.y; r.q[2] = pq.z; r.q[3] = pq.w;
     return r;
 }
 
@@ -317,12 +351,27 @@ __device__ __forceinline__ bool ill_cond(float ux, float uy, float uz, float vx,
     return fabsf(__fmaf_rn(ux, vx, __fmaf_rn(uy, vy, __fmul_rn(uz, vz)))) < 1e-3f;
 }
 
-// Stage-1 test of the screen pass with the r record in registers and the s record b in
-// shared memory: true iff the pair must go to stage 2. Same decision as
-//   !box_cannot_improve(g2, rlb, rub, b) || skip_mask(B, a, b) != 0.
+// DP4A pre-test of the 6 edge / normal combinations: true only if every |e . n| of the FP32
+// unit vectors exceeds 1e-3. With q = round(127 x) per component, |q_u . q_v / 127^2 - u . v|
+// <= 2 * sqrt(3) * 0.5 / 127 + 3 (0.5 / 127)^2 < 0.01370, so |q_u . q_v| > 16129 * 0.01470
+// (= 237.1) implies |u . v| > 1e-3.
+__device__ __forceinline__ bool well_cond_q(const int* aq, int4 bq) {
+    constexpr unsigned kT = 238;
+    const int d0 = __dp4a(aq[1], bq.x, 0), d1 = __dp4a(aq[2], bq.x, 0), d2 = __dp4a(aq[3], bq.x, 0);
+    const int d3 = __dp4a(bq.y, aq[0], 0), d4 = __dp4a(bq.z, aq[0], 0), d5 = __dp4a(bq.w, aq[0], 0);
+    // (unsigned)(d + T) > 2 T  <=>  |d| > T
+    return (unsigned)(d0 + (int)kT) > 2 * kT && (unsigned)(d1 + (int)kT) > 2 * kT &&
+           (unsigned)(d2 + (int)kT) > 2 * kT && (unsigned)(d3 + (int)kT) > 2 * kT &&
+           (unsigned)(d4 + (int)kT) > 2 * kT && (unsigned)(d5 + (int)kT) > 2 * kT;
+}
+
+// Stage-1 test of the screen pass with the r record in registers (a; its shared-memory
+// record as) and the s record b in shared memory: true iff the pair must go to stage 2.
+// Same decision as !box_cannot_improve(g2, rlb, rub, b) || skip_mask(B, a, b) != 0, with
+// the range and far tests of skip_mask taken on the squared box gap (no square root).
 __device__ __forceinline__ bool stage1_need_rr(const RowRec& a, const float* as, const float* b, float rlb, float rub) {
     const float4 b0 = *reinterpret_cast<const float4*>(b), b1 = *reinterpret_cast<const float4*>(b + 4);
-    const float4 b2 = *reinterpret_cast<const float4*>(b + 8);
+    const float bph = b[11];
     float g2;
     {
         const float gx = fmaxf(0.f, fmaxf(__fsub_rd(b0.x, a.hi[0]), __fsub_rd(a.lo[0], b1.x)));
@@ -332,18 +381,19 @@ __device__ __forceinline__ bool stage1_need_rr(const RowRec& a, const float* as,
     }
     // box_cannot_improve
     constexpr float kInvC = 1.0f / (1.0f - 1e-5f) * (1.0f + 0x1p-20f);
-    const float xl = __fadd_ru(rlb, b2.w);
+    const float xl = __fadd_ru(rlb, bph);
     const float yu = __fsub_ru(rub, b1.w);
     const float xs = __fmul_ru(xl, kInvC), ys = __fmul_ru(yu, kInvC);
     const bool lb_ok = xl <= 0.f || g2 >= __fmul_ru(xs, xs);
     const bool ub_ok = yu <= 0.f || g2 >= __fmul_ru(ys, ys);
-    if (!(lb_ok && ub_ok)) return true;
-    // skip_mask: shapes, 1e3 L range, far branch, conditioning
-    if (a.L < 0.f || b0.w < 0.f) return true;
-    const float B = __fmul_rd(sqrtf(g2), 1.0f - 0x1p-20f);
-    if (B > 1e3f * fminf(a.L, b0.w)) return true;
-    if (B > 2.f * (a.L + b0.w)) return false;
-    // near pair: the edge / plane conditioning of skip_mask (records read from shared memory)
+    // skip_mask: shapes, the 1e3 L range, far branch, conditioning
+    const float m = 1e3f * fminf(a.L, b0.w), f = 2.f * (a.L + b0.w);
+    const bool shapes = a.L >= 0.f && b0.w >= 0.f && g2 <= m * m;
+    if (!(lb_ok && ub_ok && shapes)) return true;
+    if (g2 > f * f) return false; // far apart: no spurious piercing for any conditioning
+    // near pair: DP4A pre-test, then the FP32 test of skip_mask on the rare failures
+    if (well_cond_q(a.q, *reinterpret_cast<const int4*>(b + 28))) return false;
+    const float4 b2 = *reinterpret_cast<const float4*>(b + 8);
     const float4 b3 = *reinterpret_cast<const float4*>(b + 12), b4 = *reinterpret_cast<const float4*>(b + 16);
     const float b20 = b[20];
     const float4 a2 = *reinterpret_cast<const float4*>(as + 8), a3 = *reinterpret_cast<const float4*>(as + 12);

@@ -175,19 +175,26 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
                 count_launch();
                 k_init_agg<<<1, 32, 0, st>>>(ws.level_agg.p);
                 src.agg = ws.level_agg.p;
-                ws.screen_r.reserve(std::max<uint64_t>(nr * 7, 1));
+                ws.screen_r.reserve(std::max<uint64_t>(nr * kScreenRecF4, 1));
                 refine_prep(R.facets[sr].p, nr, ws.screen_r.p, ws.level_agg.p, ws.num_sms, st);
                 src.r_box = ws.screen_r.p;
                 src.r_geo = ws.screen_r.p + 3 * nr;
+                ws.seg_r.reserve(std::max<uint64_t>(3 * R.n_voxels, 1));
+                refine_seg_prep(src.r_box, R.facet_offsets[sr].p, R.n_voxels, ws.seg_r.p, ws.num_sms, st);
+                src.r_seg = ws.seg_r.p;
                 if (S.facets[ss].p == R.facets[sr].p) {
                     src.s_box = src.r_box;
                     src.s_geo = src.r_geo;
+                    src.s_seg = src.r_seg;
                     TJ_CUDA(cudaMemcpyAsync(ws.level_agg.p + 3, ws.level_agg.p, 12, cudaMemcpyDeviceToDevice, st));
                 } else {
-                    ws.screen_s.reserve(std::max<uint64_t>(ns * 7, 1));
+                    ws.screen_s.reserve(std::max<uint64_t>(ns * kScreenRecF4, 1));
                     refine_prep(S.facets[ss].p, ns, ws.screen_s.p, ws.level_agg.p + 3, ws.num_sms, st);
                     src.s_box = ws.screen_s.p;
                     src.s_geo = ws.screen_s.p + 3 * ns;
+                    ws.seg_s.reserve(std::max<uint64_t>(3 * S.n_voxels, 1));
+                    refine_seg_prep(src.s_box, S.facet_offsets[ss].p, S.n_voxels, ws.seg_s.p, ws.num_sms, st);
+                    src.s_seg = ws.seg_s.p;
                 }
             }
             // 0: every facet pair; 1: exact-preserving culling; 2: decision-mode culling

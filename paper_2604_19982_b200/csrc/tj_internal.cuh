@@ -146,6 +146,10 @@ struct RefineSource {
     // level aggregates of the screening records (refine_prep): [0..2] R min hd, max |L|,
     // max M; [3..5] the same for S (float bits; join mode only, else nullptr)
     const unsigned* agg;
+    // per-voxel segment aggregates of this level (refine_seg_prep; 3 float4 per global
+    // voxel; join mode only, else nullptr)
+    const float4* r_seg;
+    const float4* s_seg;
 };
 
 // A queued facet pair: op and the two global facet record indices.
@@ -155,6 +159,7 @@ struct PairRef {
 };
 
 constexpr int kNumCounters = 8;
+constexpr int kScreenRecF4 = 8; // float4 per FP32 screening record (refine_kernel.cuh)
 
 struct RefineQueue {
     PairRef* items;
@@ -173,6 +178,11 @@ struct RefineQueueStore {
 // out[0, 3 n), geometry parts at out[3 n, 7 n).
 // agg (optional, 3 uints pre-set to {+inf, 0, 0} bits): min hd, max |L|, max M of the records.
 void refine_prep(const double* facets, uint64_t n, float4* out, unsigned* agg, int num_sms, cudaStream_t st);
+
+// Per-voxel segment aggregates of one level (refine.cu, k_seg_prep) into seg[3 n_voxels]:
+// union of the facet boxes, max / min L, max ph, min hd, all well shaped.
+void refine_seg_prep(const float4* box, const uint64_t* foff, uint64_t n_voxels, float4* seg, int num_sms,
+                     cudaStream_t st);
 
 // One refinement pass over voxel pairs [vp_begin, vp_end) (refine.cu): the seed pass queues
 // each voxel pair's 2 smallest-box-gap facet pairs, the screen pass every facet pair that

@@ -136,53 +136,43 @@ __global__ void k_prep(const double* __restrict__ facets, uint64_t n, float4* __
     }
 }
 
-// Facet of [first, first + n) whose box is closest (gap, then centre distance) to `box`.
-__device__ __forceinline__ uint32_t closest_facet(const float4* __restrict__ set, uint64_t first, uint32_t n,
-                                                  const float* lo, const float* hi) {
-    const int lane = threadIdx.x & 31;
-    const float cx = 0.5f * (lo[0] + hi[0]), cy = 0.5f * (lo[1] + hi[1]), cz = 0.5f * (lo[2] + hi[2]);
-    const float box[8] = {lo[0], lo[1], lo[2], 0.f, hi[0], hi[1], hi[2], 0.f};
-    float best = __int_as_float(0x7f800000);
-    uint32_t bi = 0xffffffffu;
-    for (uint32_t i = lane; i < n; i += 32) {
-        const float4 a = __ldg(set + (first + i) * kBoxF4), b = __ldg(set + (first + i) * kBoxF4 + 1);
-        const float rec[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-        const float g = box_gap_lb(rec, box);
-        const float dx = 0.5f * (a.x + b.x) - cx, dy = 0.5f * (a.y + b.y) - cy, dz = 0.5f * (a.z + b.z) - cz;
-        // gap dominates; the centre distance only orders near-ties (deepest overlap first)
-        const float key = g + 1e-3f * sqrtf(dx * dx + dy * dy + dz * dz);
-        if (key < best || (key == best && i < bi)) { best = key; bi = i; }
-    }
-    warp_argmin(best, bi);
-    return bi;
+// Seed ordering key (a heuristic; exactness never depends on it) of a facet box (a: lo.xyz
+// L, b: hi.xyz hd) against box (lo, hi): squared gap + 1e-6 x squared centre distance, so
+// the gap dominates and the centre distance orders near-ties (deepest overlap first).
+__device__ __forceinline__ float seed_key(float4 a, float4 b, const float* lo, const float* hi) {
+    const float gx = fmaxf(0.f, fmaxf(lo[0] - b.x, a.x - hi[0]));
+    const float gy = fmaxf(0.f, fmaxf(lo[1] - b.y, a.y - hi[1]));
+    const float gz = fmaxf(0.f, fmaxf(lo[2] - b.z, a.z - hi[2]));
+    const float cx = (a.x + b.x) - (lo[0] + hi[0]), cy = (a.y + b.y) - (lo[1] + hi[1]), cz = (a.z + b.z) - (lo[2] + hi[2]);
+    const float g2 = __fmaf_rn(gx, gx, __fmaf_rn(gy, gy, __fmul_rn(gz, gz)));
+    const float c2 = __fmaf_rn(cx, cx, __fmaf_rn(cy, cy, __fmul_rn(cz, cz)));
+    return __fmaf_rn(0.25e-6f, c2, g2);
 }
 
-// Facets i* of r closest (box gap, then centre distance) to box b_s and j* of s closest to
-// box b_r, in one sweep over both segments.
+// Warp argmin of a non-negative key held by lanes [0, 32) (lane = index): the key's low 5
+// bits are replaced by the lane, so one integer min-reduction returns the winner (ties, and
+// keys within 2^-18 relative, resolve to the lowest lane; a heuristic order only).
+__device__ __forceinline__ uint32_t warp_argmin_lane(float key) {
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned packed = (__float_as_uint(key) & ~31u) | lane;
+    return __reduce_min_sync(0xffffffffu, packed) & 31u;
+}
+
+// Facets i* of r closest (seed_key) to box sb and j* of s closest to box rb, in one sweep.
 __device__ __forceinline__ void closest_pair(const float4* __restrict__ rset, uint64_t r0, uint32_t rn,
                                              const float4* __restrict__ sset, uint64_t s0, uint32_t sn,
-                                             const SegAgg& sr, const SegAgg& ss, uint32_t& ist, uint32_t& jst) {
+                                             const SegAgg& rb, const SegAgg& sb, uint32_t& ist, uint32_t& jst) {
     const int lane = threadIdx.x & 31;
-    auto key_of = [](float4 a, float4 b, const SegAgg& o) {
-        const float rec[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-        const float box[8] = {o.lo[0], o.lo[1], o.lo[2], 0.f, o.hi[0], o.hi[1], o.hi[2], 0.f};
-        const float g = box_gap_lb(rec, box);
-        const float dx = 0.5f * (a.x + b.x) - 0.5f * (o.lo[0] + o.hi[0]);
-        const float dy = 0.5f * (a.y + b.y) - 0.5f * (o.lo[1] + o.hi[1]);
-        const float dz = 0.5f * (a.z + b.z) - 0.5f * (o.lo[2] + o.hi[2]);
-        // gap dominates; the centre distance only orders near-ties (deepest overlap first)
-        return g + 1e-3f * sqrtf(dx * dx + dy * dy + dz * dz);
-    };
     const float kInfF = __int_as_float(0x7f800000);
     float br = kInfF, bs = kInfF;
     uint32_t ir = 0xffffffffu, is = 0xffffffffu;
     for (uint32_t i = lane; i < max(rn, sn); i += 32) {
         if (i < rn) {
-            const float k = key_of(__ldg(rset + (r0 + i) * kBoxF4), __ldg(rset + (r0 + i) * kBoxF4 + 1), ss);
+            const float k = seed_key(__ldg(rset + (r0 + i) * kBoxF4), __ldg(rset + (r0 + i) * kBoxF4 + 1), sb.lo, sb.hi);
             if (k < br) { br = k; ir = i; }
         }
         if (i < sn) {
-            const float k = key_of(__ldg(sset + (s0 + i) * kBoxF4), __ldg(sset + (s0 + i) * kBoxF4 + 1), sr);
+            const float k = seed_key(__ldg(sset + (s0 + i) * kBoxF4), __ldg(sset + (s0 + i) * kBoxF4 + 1), rb.lo, rb.hi);
             if (k < bs) { bs = k; is = i; }
         }
     }
@@ -197,13 +187,12 @@ __device__ __forceinline__ void closest_pair(const float4* __restrict__ rset, ui
 // closest to j*; queues (i*, j') and (i', j*). In decision mode only voxel pairs that can
 // hold a zero bound are seeded (segment gap <= ph_max(r) + ph_max(s)).
 __global__ void __launch_bounds__(256) k_seed(RefineSource src, uint64_t vp_begin, uint64_t vp_end, RefineQueue q,
-                                              unsigned long long* work, int cull) {
+                                              int cull) {
     const int lane = threadIdx.x & 31;
-    for (;;) {
-        unsigned long long vp = 0;
-        if (lane == 0) vp = atomicAdd(work, 1ull);
-        vp = __shfl_sync(0xffffffffu, vp, 0) + vp_begin;
-        if (vp >= vp_end) break;
+    const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    PairRef pref{0u, 0u, 0u, 0u}; // this lane's buffered seed
+    int pend = 0;
+    for (uint64_t vp = vp_begin + blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); vp < vp_end; vp += nw) {
         const VpDescDev d = get_vp(src, vp);
         if (d.rn == 0 || d.sn == 0) continue;
         const SegAgg ar = seg_r_of(src, d);
@@ -213,21 +202,44 @@ __global__ void __launch_bounds__(256) k_seed(RefineSource src, uint64_t vp_begi
             const float brec[8] = {as.lo[0], as.lo[1], as.lo[2], 0.f, as.hi[0], as.hi[1], as.hi[2], 0.f};
             if (box_gap_lb(arec, brec) > __fadd_ru(ar.phmax, as.phmax)) continue;
         }
-        uint32_t ist, jst;
-        closest_pair(src.r_box, d.r0, d.rn, src.s_box, d.s0, d.sn, ar, as, ist, jst);
-        // second round: the partner facet closest to each first-round facet
-        SegAgg fi = ar, fj = as; // only lo / hi are read
-        {
-            const float4 a = __ldg(src.r_box + (d.r0 + ist) * kBoxF4), b = __ldg(src.r_box + (d.r0 + ist) * kBoxF4 + 1);
-            fi.lo[0] = a.x; fi.lo[1] = a.y; fi.lo[2] = a.z; fi.hi[0] = b.x; fi.hi[1] = b.y; fi.hi[2] = b.z;
-            const float4 c = __ldg(src.s_box + (d.s0 + jst) * kBoxF4), e = __ldg(src.s_box + (d.s0 + jst) * kBoxF4 + 1);
-            fj.lo[0] = c.x; fj.lo[1] = c.y; fj.lo[2] = c.z; fj.hi[0] = e.x; fj.hi[1] = e.y; fj.hi[2] = e.z;
+        uint32_t ist, jst, ip, jp;
+        if (d.rn <= 32 && d.sn <= 32) {
+            // both segments fit the warp: each lane keeps its r and s facet boxes in registers
+            const float kInfF = __int_as_float(0x7f800000);
+            float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0, s0 = r0, s1 = r0;
+            if (lane < (int)d.rn) { r0 = __ldg(src.r_box + (d.r0 + lane) * kBoxF4); r1 = __ldg(src.r_box + (d.r0 + lane) * kBoxF4 + 1); }
+            if (lane < (int)d.sn) { s0 = __ldg(src.s_box + (d.s0 + lane) * kBoxF4); s1 = __ldg(src.s_box + (d.s0 + lane) * kBoxF4 + 1); }
+            ist = warp_argmin_lane(lane < (int)d.rn ? seed_key(r0, r1, as.lo, as.hi) : kInfF);
+            jst = warp_argmin_lane(lane < (int)d.sn ? seed_key(s0, s1, ar.lo, ar.hi) : kInfF);
+            // second round against the single facets i*, j* (their boxes by shuffle)
+            const float fil[3] = {__shfl_sync(~0u, r0.x, ist), __shfl_sync(~0u, r0.y, ist), __shfl_sync(~0u, r0.z, ist)};
+            const float fih[3] = {__shfl_sync(~0u, r1.x, ist), __shfl_sync(~0u, r1.y, ist), __shfl_sync(~0u, r1.z, ist)};
+            const float fjl[3] = {__shfl_sync(~0u, s0.x, jst), __shfl_sync(~0u, s0.y, jst), __shfl_sync(~0u, s0.z, jst)};
+            const float fjh[3] = {__shfl_sync(~0u, s1.x, jst), __shfl_sync(~0u, s1.y, jst), __shfl_sync(~0u, s1.z, jst)};
+            ip = warp_argmin_lane(lane < (int)d.rn ? seed_key(r0, r1, fjl, fjh) : kInfF);
+            jp = warp_argmin_lane(lane < (int)d.sn ? seed_key(s0, s1, fil, fih) : kInfF);
+        } else {
+            closest_pair(src.r_box, d.r0, d.rn, src.s_box, d.s0, d.sn, ar, as, ist, jst);
+            SegAgg fi = ar, fj = as; // only lo / hi are read
+            {
+                const float4 a = __ldg(src.r_box + (d.r0 + ist) * kBoxF4), b = __ldg(src.r_box + (d.r0 + ist) * kBoxF4 + 1);
+                fi.lo[0] = a.x; fi.lo[1] = a.y; fi.lo[2] = a.z; fi.hi[0] = b.x; fi.hi[1] = b.y; fi.hi[2] = b.z;
+                const float4 c = __ldg(src.s_box + (d.s0 + jst) * kBoxF4), e = __ldg(src.s_box + (d.s0 + jst) * kBoxF4 + 1);
+                fj.lo[0] = c.x; fj.lo[1] = c.y; fj.lo[2] = c.z; fj.hi[0] = e.x; fj.hi[1] = e.y; fj.hi[2] = e.z;
+            }
+            closest_pair(src.r_box, d.r0, d.rn, src.s_box, d.s0, d.sn, fi, fj, ip, jp);
         }
-        uint32_t ip, jp;
-        closest_pair(src.r_box, d.r0, d.rn, src.s_box, d.s0, d.sn, fi, fj, ip, jp);
-        queue_push(q, lane == 0, d.op, (uint32_t)(d.r0 + ist), (uint32_t)(d.s0 + jp));
-        queue_push(q, lane == 0 && !(ip == ist && jp == jst), d.op, (uint32_t)(d.r0 + ip), (uint32_t)(d.s0 + jst));
+        // buffer the seeds in lanes (pend = entries held), one queue append per 30+ seeds
+        const bool two = !(ip == ist && jp == jst);
+        if (lane == pend) pref = {d.op, (uint32_t)(d.r0 + ist), (uint32_t)(d.s0 + jp), 0u};
+        if (two && lane == pend + 1) pref = {d.op, (uint32_t)(d.r0 + ip), (uint32_t)(d.s0 + jst), 0u};
+        pend += two ? 2 : 1;
+        if (pend >= 31) {
+            queue_push(q, lane < pend, pref.op, pref.fr, pref.fs);
+            pend = 0;
+        }
     }
+    queue_push(q, lane < pend, pref.op, pref.fr, pref.fs);
 }
 
 // The reference's FP64 piercing test for the masked edge/plane combinations of two facet
@@ -335,10 +347,18 @@ __global__ void __launch_bounds__(256, 2) k_screen(RefineSource src, uint64_t vp
         const float m2 = __fadd_ru(__uint_as_float(src.agg[2]), __uint_as_float(src.agg[5]));
         ub_level_settled = hd2 > __fadd_ru(__fadd_ru(__fmul_ru(1e-5f, l2), __fmul_ru(1e-12f, m2)), 1e-30f);
     }
+    // dynamic work distribution in grabs of kGrab voxel pairs (one atomic per grab: a single
+    // counter hit once per voxel pair serialises at the L2)
+    constexpr unsigned kGrab = 4;
+    unsigned long long grab = 0;
+    unsigned taken = kGrab;
     for (;;) {
-        unsigned long long vp = 0;
-        if (lane == 0) vp = atomicAdd(work, 1ull);
-        vp = __shfl_sync(0xffffffffu, vp, 0) + vp_begin;
+        if (taken == kGrab) {
+            if (lane == 0) grab = atomicAdd(work, (unsigned long long)kGrab);
+            grab = __shfl_sync(0xffffffffu, grab, 0);
+            taken = 0;
+        }
+        const unsigned long long vp = grab + taken++ + vp_begin;
         if (vp >= vp_end) break;
         const VpDescDev d = get_vp(src, vp);
         if (d.rn == 0 || d.sn == 0) continue;
@@ -584,9 +604,8 @@ void refine_pass(const RefineSource& src, uint64_t vp_begin, uint64_t vp_end, bo
         // 2 entries per voxel pair at most
         if (2 * (vp_end - vp_begin) > qs.items.n) qs.items.alloc(2 * (vp_end - vp_begin));
         TJ_CUDA(cudaMemsetAsync(qs.count.p, 0, 8, st));
-        TJ_CUDA(cudaMemsetAsync(work, 0, 8, st));
         count_launch();
-        k_seed<<<warp_grid(vp_end - vp_begin, num_sms, 8), 256, 0, st>>>(src, vp_begin, vp_end, qs.view(), work, cull);
+        k_seed<<<warp_grid(vp_end - vp_begin, num_sms, 4), 256, 0, st>>>(src, vp_begin, vp_end, qs.view(), cull);
         TJ_CUDA(cudaGetLastError());
     } else {
         // No host round trip: a queue overflow only drops entries, k_eval records the largest

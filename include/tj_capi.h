@@ -15,7 +15,11 @@
  *   tj_mindist_batch   mindist_aabb             include/trijoin/geom.hpp:60,      src/geom.cpp:11-16
  *   tj_mbb_filter      mbb_filter_within / _knn include/trijoin/filter.hpp:62-66,   src/filter.cpp:88-190
  *   tj_voxel_filter    chunked_filter           include/trijoin/filter.hpp:111-114, src/filter.cpp:350-448
- *   tj_knn_prune       knn_prune_to_fixpoint    include/trijoin/knn.hpp:41-42,      src/knn.cpp:82-91
+ *   tj_voxel_bounds    voxel_pair_bounds        include/trijoin/filter.hpp:83-85,   src/filter.cpp:199-239
+ *   tj_voxel_compact   voxel_pair_compact       include/trijoin/filter.hpp:94-97,   src/filter.cpp:265-315
+ *   tj_refine_loop     refine_loop              include/trijoin/refine.hpp:82-87,   src/refine.cpp:263-314
+ *   tj_knn_prune       knn_prune_round / _to_fixpoint / knn_finalize
+ *                                               include/trijoin/knn.hpp:30-50,      src/knn.cpp:19-118
  *   tj_dataset_upload  (no reference analogue: PreparedDataset is host-resident there,
  *                       include/trijoin/index.hpp:15-36; here it is packed once into HBM)
  *
@@ -222,6 +226,64 @@ int tj_refine_batch(tj_ctx* ctx, uint64_t n_tris, const double* tris, const doub
                     const double* ph, uint64_t n_descs, const uint64_t* r_off,
                     const uint64_t* s_off, const uint32_t* r_len, const uint32_t* s_len,
                     uint32_t flags, double* vp_lb, double* vp_ub);
+
+/* ---- stage entry points over a caller-owned host candidate set ----
+ * The reference's stage functions (called directly by its tests and tools) on the device.
+ * Datasets are tj_dataset handles (tj_dataset_upload); the candidate set is the caller's
+ * (reference CandidateSet, include/trijoin/filter.hpp:38-48) and is updated in place.
+ *   tj_mbb_filter     mbb_filter_within / mbb_filter_knn   include/trijoin/filter.hpp:62-66, src/filter.cpp:88-190
+ *                     (exact broad phase; returns a new candidate set in a tj_join_result)
+ *   tj_voxel_filter   chunked_filter (all chunks)          include/trijoin/filter.hpp:111-114, src/filter.cpp:350-448
+ *   tj_voxel_bounds   voxel_pair_bounds (one chunk)        include/trijoin/filter.hpp:83-85, src/filter.cpp:199-239
+ *   tj_voxel_compact  voxel_pair_compact (one chunk)       include/trijoin/filter.hpp:94-97, src/filter.cpp:265-315
+ *   tj_refine_loop    refine_loop / knn_resolve            include/trijoin/refine.hpp:82-87, src/refine.cpp:263-314
+ *   tj_knn_prune      knn_prune_round (mode 0: deltas only), knn_prune_to_fixpoint (1), knn_finalize (2)
+ *                                                          include/trijoin/knn.hpp:30-50, src/knn.cpp:19-118
+ */
+typedef struct tj_cand_view {
+    uint64_t n_cands;
+    uint32_t n_queries;
+    const uint32_t* pair_r;  /* [n_cands], grouped by r */
+    const uint32_t* pair_s;
+    double* lb;              /* [n_cands] interval, updated in place */
+    double* ub;
+    uint8_t* status;         /* TJ_UNDECIDED / TJ_CONFIRMED / TJ_REMOVED */
+    int16_t* decided_at;
+    const uint64_t* r2op_offsets; /* [n_queries+1] */
+    uint32_t* num_confirmed;      /* [n_queries] */
+} tj_cand_view;
+
+/* Voxel-pair list (reference VoxelPairList, include/trijoin/filter.hpp:50-53): op_offsets
+   [n_ops+1] (may be NULL for a plain survivor list), per voxel pair its op and the
+   object-local voxel ids (vr of r, vs of s). Library-owned when returned. */
+typedef struct tj_vp_list {
+    uint64_t n_ops;
+    uint64_t n_vps;
+    uint64_t* op_offsets;
+    uint32_t* op;
+    uint32_t* vr;
+    uint32_t* vs;
+} tj_vp_list;
+void tj_vp_list_free(tj_vp_list* l);
+
+int tj_mbb_filter(tj_ctx* ctx, const tj_dataset* R, const tj_dataset* S, int32_t type, double tau, uint32_t k,
+                  const tj_trace* trace, tj_join_result* out);
+int tj_voxel_filter(tj_ctx* ctx, const tj_dataset* R, const tj_dataset* S, tj_cand_view* cands, int prune,
+                    double tau, const tj_trace* trace, tj_vp_list* out, uint64_t* vp_generated,
+                    uint64_t* vp_pruned);
+int tj_voxel_bounds(tj_ctx* ctx, const tj_dataset* R, const tj_dataset* S, const tj_cand_view* cands,
+                    uint64_t n_ops, const uint32_t* ops, const uint64_t* vp_offsets, double* vp_lb,
+                    double* vp_ub, double* op_lb, double* op_ub);
+int tj_voxel_compact(tj_ctx* ctx, const tj_dataset* R, const tj_dataset* S, const tj_cand_view* cands,
+                     uint64_t n_ops, const uint32_t* ops, const uint64_t* vp_offsets, const double* vp_lb,
+                     tj_vp_list* out);
+/* spec: type (TJ_WITHIN / TJ_INTERSECT use tau, TJ_KNN uses k), lods, refine_chunk, flags.
+   stats (optional): the per-level counters of a tj_join_result. */
+int tj_refine_loop(tj_ctx* ctx, const tj_dataset* R, const tj_dataset* S, tj_cand_view* cands,
+                   const tj_vp_list* vplist, const tj_join_spec* spec, const tj_trace* trace,
+                   tj_join_result* stats);
+int tj_knn_prune(tj_ctx* ctx, tj_cand_view* cands, uint32_t k, int16_t stage, int mode, uint8_t* deltas,
+                 uint64_t* decisions);
 
 /* Exact FP64 tri_tri_distance / mindist_aabb over n independent inputs. */
 int tj_tri_tri_batch(tj_ctx* ctx, uint64_t n, const double* a9, const double* b9, double* out);

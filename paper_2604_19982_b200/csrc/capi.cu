@@ -248,6 +248,20 @@ void stream_sync(cudaStream_t st) {
     TJ_CUDA(cudaEventSynchronize(e));
 }
 
+} // namespace tjx
+// Accessors for the stage entry points (stages.cu).
+struct tj_ctx_view {
+    int device;
+    cudaStream_t stream;
+    tjx::Workspace* ws;
+};
+namespace tjx {
+tj_ctx_view ctx_view(tj_ctx* ctx) { return {ctx->device, ctx->stream, &ctx->ws}; }
+const DatasetDev& dataset_dev(const tj_dataset* ds) { return ds->d; }
+int guarded_call(tj_ctx* ctx, void (*fn)(void*), void* arg) {
+    return guarded(ctx, [&] { fn(arg); });
+}
+
 unsigned long long& launch_counter_ref() {
     static unsigned long long n = 0;
     return n;

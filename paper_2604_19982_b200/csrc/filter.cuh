@@ -127,6 +127,9 @@ VoxelOut voxel_filter(Workspace& ws, const VoxelArgs& a, CandDevStore& cs, DevBu
 // knn.cu
 // k-NN pruning rounds to a fixpoint for every query (knn_prune_to_fixpoint, src/knn.cpp:82-91).
 uint64_t knn_fixpoint(Workspace& ws, CandDevStore& cs, uint32_t k, int16_t stage, DevError* err, cudaStream_t st);
+// One pruning round, deltas only (knn_prune_round, src/knn.cpp:19-63); returns the count.
+uint64_t knn_round_dev(Workspace& ws, CandDevStore& cs, uint32_t k, DevBuf<uint8_t>& delta, DevError* err,
+                       cudaStream_t st);
 // knn_finalize (src/knn.cpp:93-118).
 void knn_finalize_dev(Workspace& ws, CandDevStore& cs, uint32_t k, cudaStream_t st);
 

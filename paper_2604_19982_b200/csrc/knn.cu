@@ -23,7 +23,7 @@ __device__ __forceinline__ void flag_knn_error(DevError* err, uint32_t op) {
 }
 
 __global__ void k_knn_fixpoint(CandDev c, uint32_t nq, uint32_t k, int16_t stage, uint8_t* __restrict__ delta,
-                               DevError* err, unsigned long long* decided_total) {
+                               DevError* err, unsigned long long* decided_total, int apply) {
     const int lane = threadIdx.x & 31;
     const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
     unsigned long long decided = 0;
@@ -56,8 +56,15 @@ __global__ void k_knn_fixpoint(CandDev c, uint32_t nq, uint32_t k, int16_t stage
                     else if (closer >= k_left) d = TJ_REMOVED;
                 }
                 delta[m] = d;
+                if (!apply) changes += d != 0;
             }
             __syncwarp();
+            if (!apply) { // one round, deltas only (knn_prune_round)
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) changes += __shfl_xor_sync(0xffffffffu, changes, o);
+                decided += changes;
+                break;
+            }
             for (uint64_t m = b + lane; m < e; m += 32) {
                 const uint8_t d = delta[m];
                 if (d) {
@@ -137,7 +144,25 @@ uint64_t knn_fixpoint(Workspace& ws, CandDevStore& cs, uint32_t k, int16_t stage
     const uint64_t threads = (uint64_t)cs.nq * 32;
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((threads + 255) / 256, (uint64_t)ws.num_sms * 16));
     count_launch();
-    k_knn_fixpoint<<<grid, 256, 0, st>>>(cs.view(), cs.nq, k, stage, delta.p, err, total.p);
+    k_knn_fixpoint<<<grid, 256, 0, st>>>(cs.view(), cs.nq, k, stage, delta.p, err, total.p, 1);
+    TJ_CUDA(cudaGetLastError());
+    unsigned long long h = 0;
+    TJ_CUDA(cudaMemcpyAsync(&h, total.p, 8, cudaMemcpyDeviceToHost, st));
+    stream_sync(st);
+    return h;
+}
+
+uint64_t knn_round_dev(Workspace& ws, CandDevStore& cs, uint32_t k, DevBuf<uint8_t>& delta, DevError* err,
+                       cudaStream_t st) {
+    if (cs.n == 0) return 0;
+    TJ_CUDA(cudaMemsetAsync(delta.p, 0, cs.n, st));
+    if (cs.nq == 0) return 0;
+    DevBuf<unsigned long long> total(1);
+    TJ_CUDA(cudaMemsetAsync(total.p, 0, 8, st));
+    const uint64_t threads = (uint64_t)cs.nq * 32;
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((threads + 255) / 256, (uint64_t)ws.num_sms * 16));
+    count_launch();
+    k_knn_fixpoint<<<grid, 256, 0, st>>>(cs.view(), cs.nq, k, 0, delta.p, err, total.p, 0);
     TJ_CUDA(cudaGetLastError());
     unsigned long long h = 0;
     TJ_CUDA(cudaMemcpyAsync(&h, total.p, 8, cudaMemcpyDeviceToHost, st));

@@ -62,7 +62,11 @@ enum {
        whether min lb_ij / min ub_ij are 0 (the only facts an intersection decision and its
        records depend on), so intervals of pairs it removes may stay looser
        than the reference's; records and stage counters are identical either way. */
-    TJ_FLAG_EXACT_INTERVALS = 1u << 2
+    TJ_FLAG_EXACT_INTERVALS = 1u << 2,
+    /* JoinSpec::exact (reference src/engine.cpp:96-118, :159): after the cascade, every
+       confirmed pair's interval becomes [d, d], d the minimum tri_tri_distance over all
+       pairs of the two level-100 meshes' facets. */
+    TJ_FLAG_EXACT_RECOMPUTE = 1u << 3
 };
 
 #define TJ_FACET_STRIDE 12 /* doubles per facet record: v0.xyz v1.xyz v2.xyz hd ph pad */

@@ -232,6 +232,7 @@ void ora_refine_batch(uint64_t n_descs, const double* tris9, const double* hd, c
  * length-prefixed bodies). Only the fields the join reads are kept. */
 
 typedef struct {
+    uint64_t nf;        /* facets of the level mesh */
     Tri* tris;          /* per facet, level mesh */
     double *hd, *ph;    /* per facet */
     uint64_t* voff;     /* [nvox+1] into vid */
@@ -330,6 +331,7 @@ static int ds_load(const char* path, ODs* d) {
             double* v = malloc(24 * (nv ? nv : 1));
             for (uint64_t i = 0; i < 3 * nv; ++i) v[i] = rd_f64(&r);
             uint64_t nf = rd_u64(&r);
+            L->nf = nf;
             L->tris = malloc(sizeof(Tri) * (nf ? nf : 1));
             for (uint64_t i = 0; i < nf; ++i)
                 for (int k = 0; k < 3; ++k) {
@@ -498,6 +500,11 @@ static int cmp_records(const void* a, const void* b) { /* (ub, lb, s) */
 
 void ora_join_files(const char* r_path, const char* s_path, int type, double tau, uint32_t kk,
                     const uint32_t* lods, uint32_t n_lods, ora_result* out) {
+    ora_join_files_ex(r_path, s_path, type, tau, kk, lods, n_lods, 0, out);
+}
+
+void ora_join_files_ex(const char* r_path, const char* s_path, int type, double tau, uint32_t kk,
+                       const uint32_t* lods, uint32_t n_lods, int exact, ora_result* out) {
     memset(out, 0, sizeof(*out));
     Ctx c = {out, 0};
     const int knn = type == 2;
@@ -647,6 +654,25 @@ void ora_join_files(const char* r_path, const char* s_path, int type, double tau
         } else {
             for (uint64_t op = 0; op < k.n; ++op)
                 if (k.st[op] == UND) { fail(&c, 2, "refine_loop: candidates left undecided after the exact level"); break; }
+        }
+    }
+    if (!c.failed && exact) {
+        /* --exact (src/engine.cpp:96-118, :159): each confirmed interval becomes [d, d], d the
+           minimum tri_tri_distance over all facet pairs of the two level-100 meshes (the
+           reference's TriBvh::pair_distance, src/bvh.cpp:114-154, is that minimum; here by
+           brute force) */
+        const int sr = level_slot(&R, 100), ss = level_slot(S, 100);
+        for (uint64_t op = 0; op < k.n && sr >= 0 && ss >= 0; ++op) {
+            if (k.st[op] != CONF) continue;
+            const OLevel* a = &R.o[k.r[op]].lv[sr];
+            const OLevel* b = &S->o[k.s[op]].lv[ss];
+            double d = INFINITY;
+            for (uint64_t i = 0; i < a->nf && d != 0.0; ++i)
+                for (uint64_t j = 0; j < b->nf; ++j) {
+                    d = smin(d, tri_tri(&a->tris[i], &b->tris[j]));
+                    if (d == 0.0) break;
+                }
+            k.lb[op] = k.ub[op] = d;
         }
     }
     if (!c.failed) {

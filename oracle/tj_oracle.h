@@ -52,6 +52,10 @@ typedef struct ora_result {
    type: 0 within, 1 intersect, 2 knn. */
 void ora_join_files(const char* r_path, const char* s_path, int type, double tau, uint32_t k,
                     const uint32_t* lods, uint32_t n_lods, ora_result* out);
+/* The same with JoinSpec::exact (src/engine.cpp:96-118): confirmed intervals become the
+   exact level-100 mesh distance. */
+void ora_join_files_ex(const char* r_path, const char* s_path, int type, double tau, uint32_t k,
+                       const uint32_t* lods, uint32_t n_lods, int exact, ora_result* out);
 void ora_result_free(ora_result* r);
 
 #ifdef __cplusplus

@@ -625,6 +625,8 @@ int tj_join(tj_ctx* ctx, const tj_dataset* Rh, const tj_dataset* Sh, const tj_jo
         }
         out->refine_chunks = ro.chunks;
 
+        if (sp.flags & TJ_FLAG_EXACT_RECOMPUTE) exact_recompute_dev(ws, R, S, cs, st);
+
         // streamed datasets: the device-side validation of the levels this join used
         for (const DatasetDev* D : {&R, &S}) {
             if (!D->gate) continue;

@@ -147,5 +147,7 @@ struct TraceSink; // host-side trace forwarding (engine.cu)
 RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetDev& S, CandDevStore& cs,
                               DevBuf<ActiveVpDev>& active, uint64_t n_active, const tj_join_spec& spec, bool knn,
                               double tau, bool decision, DevError* err, TraceSink* trace, cudaStream_t st);
+// --exact: confirmed intervals become [d, d], d the level-100 mesh distance (src/engine.cpp:96-118).
+void exact_recompute_dev(Workspace& ws, const DatasetDev& R, const DatasetDev& S, CandDevStore& cs, cudaStream_t st);
 
 } // namespace tjx

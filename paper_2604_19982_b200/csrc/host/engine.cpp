@@ -700,6 +700,7 @@ tj_join_spec to_c_spec(const JoinSpec& spec) {
     c.lods = spec.lods.data();
     c.pipeline = spec.pipeline ? 1 : 0;
     c.flags = 0;
+    if (spec.exact) c.flags |= TJ_FLAG_EXACT_RECOMPUTE;
     if (const char* e = std::getenv("TRIJOIN_NO_CULL"); e && *e && *e != '0') c.flags |= TJ_FLAG_NO_CULL;
     if (const char* e = std::getenv("TRIJOIN_EXACT_INTERVALS"); e && *e && *e != '0') c.flags |= TJ_FLAG_EXACT_INTERVALS;
     return c;

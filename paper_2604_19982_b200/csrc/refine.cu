@@ -105,13 +105,15 @@ __device__ __forceinline__ void warp_argmin(float& v, uint32_t& idx) {
     }
 }
 
-__global__ void k_prep(const double* __restrict__ facets, uint64_t n, float4* __restrict__ out, unsigned* agg) {
+__global__ void k_prep(const double* __restrict__ facets, uint64_t n, float4* __restrict__ out, unsigned* agg,
+                       int zero_pad) {
     float4* box = out;
     float4* geo = out + kBoxF4 * n;
     float hdmin = __int_as_float(0x7f800000), lmax = 0.f, mmax = 0.f;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         float r[kCS];
         make_screen(facets + i * 12, r);
+        if (zero_pad) r[7] = r[11] = 0.f; // hd, ph
         hdmin = fminf(hdmin, r[7]);
         lmax = fmaxf(lmax, fabsf(r[3]));
         mmax = fmaxf(mmax, r[27]);
@@ -527,9 +529,9 @@ __global__ void __launch_bounds__(128) k_eval(RefineSource src, RefineQueue q, u
         double c[12];
         double n2, s2;
         load_facet(src.r_facets + (size_t)p.fr * 12, c);
-        stage_exact(c, c[9], c[10], ra, &n2, &s2);
+        stage_exact(c, src.zero_pad ? 0.0 : c[9], src.zero_pad ? 0.0 : c[10], ra, &n2, &s2);
         load_facet(src.s_facets + (size_t)p.fs * 12, c);
-        stage_exact(c, c[9], c[10], sb, &n2, &s2);
+        stage_exact(c, src.zero_pad ? 0.0 : c[9], src.zero_pad ? 0.0 : c[10], sb, &n2, &s2);
         const double2 v = eval_pair(ra, sb);
         const unsigned long long lbv = (unsigned long long)__double_as_longlong(v.x);
         const unsigned long long ubv = (unsigned long long)__double_as_longlong(v.y);
@@ -573,11 +575,12 @@ inline int warp_grid(uint64_t warps, int num_sms, int per_sm) {
 
 } // namespace
 
-void refine_prep(const double* facets, uint64_t n, float4* out, unsigned* agg, int num_sms, cudaStream_t st) {
+void refine_prep(const double* facets, uint64_t n, float4* out, unsigned* agg, int num_sms, cudaStream_t st,
+                 int zero_pad) {
     if (!n) return;
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, (uint64_t)num_sms * 16));
     count_launch();
-    k_prep<<<grid, 256, 0, st>>>(facets, n, out, agg);
+    k_prep<<<grid, 256, 0, st>>>(facets, n, out, agg, zero_pad);
     TJ_CUDA(cudaGetLastError());
 }
 

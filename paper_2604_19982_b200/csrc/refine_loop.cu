@@ -265,4 +265,131 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
     return out;
 }
 
+namespace {
+
+__global__ void k_exact_counts(CandDev c, uint64_t n, const uint64_t* __restrict__ r_voff,
+                               const uint64_t* __restrict__ s_voff, uint32_t* __restrict__ counts) {
+    for (uint64_t op = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; op < n; op += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t cnt = 0;
+        if (c.status[op] == TJ_CONFIRMED) {
+            const uint32_t r = c.pair_r[op], s = c.pair_s[op];
+            cnt = (uint32_t)((r_voff[r + 1] - r_voff[r]) * (s_voff[s + 1] - s_voff[s]));
+        }
+        counts[op] = cnt;
+    }
+}
+
+// Warp per confirmed op: every voxel pair (i, j) of its two objects.
+__global__ void k_exact_emit(CandDev c, uint64_t n, const uint64_t* __restrict__ offsets,
+                             const uint64_t* __restrict__ r_voff, const uint64_t* __restrict__ s_voff,
+                             ActiveVpDev* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+    for (uint64_t op = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; op < n; op += warps) {
+        if (c.status[op] != TJ_CONFIRMED) continue;
+        const uint32_t r = c.pair_r[op], s = c.pair_s[op];
+        const uint64_t vr0 = r_voff[r], vs0 = s_voff[s], ns = s_voff[s + 1] - vs0;
+        const uint64_t total = (r_voff[r + 1] - vr0) * ns, base = offsets[op];
+        for (uint64_t t = lane; t < total; t += 32)
+            out[base + t] = {(uint32_t)op, (uint32_t)(vr0 + t / ns), (uint32_t)(vs0 + t % ns)};
+    }
+}
+
+__global__ void k_exact_store(CandDev c, uint64_t n, const unsigned long long* __restrict__ dbits) {
+    for (uint64_t op = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; op < n; op += (uint64_t)gridDim.x * blockDim.x) {
+        if (c.status[op] != TJ_CONFIRMED) continue;
+        const double d = __longlong_as_double((long long)dbits[op]);
+        c.lb[op] = d;
+        c.ub[op] = d;
+    }
+}
+
+} // namespace
+
+// --exact (reference recompute_exact, src/engine.cpp:96-118): for every confirmed pair the
+// minimum tri_tri_distance over all facet pairs of the two level-100 meshes (TriBvh::
+// pair_distance is that minimum). On the device it is one more level-100 pass over every
+// voxel pair of the confirmed pairs (the level-100 voxel lists partition the mesh facets),
+// with the paddings ignored and the same exact-preserving culling against the op minima.
+void exact_recompute_dev(Workspace& ws, const DatasetDev& R, const DatasetDev& S, CandDevStore& cs, cudaStream_t st) {
+    const uint64_t n = cs.n;
+    if (n == 0) return;
+    const int sr = level_slot(R, 100), ss = level_slot(S, 100);
+    if (sr < 0 || ss < 0) throw Error(TJ_EENGINE, "refine: level 100 is not in the dataset's lod schedule");
+    level_ready(R, sr, st);
+    if (&S != &R) level_ready(S, ss, st);
+    DevBuf<uint32_t> counts(n);
+    count_launch();
+    k_exact_counts<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(cs.view(), n, R.voxel_offsets.p, S.voxel_offsets.p,
+                                                                 counts.p);
+    DevBuf<uint64_t> offsets;
+    const uint64_t total = scan_counts(ws, counts.p, n, offsets, st);
+    if (total == 0) return;
+    DevBuf<ActiveVpDev> active(total);
+    count_launch();
+    k_exact_emit<<<grid_for(n * 32, 256, ws.num_sms), 256, 0, st>>>(cs.view(), n, offsets.p, R.voxel_offsets.p,
+                                                                     S.voxel_offsets.p, active.p);
+    DevBuf<double> iv_lb(n), iv_ub(n);
+    DevBuf<unsigned long long> lbb(n), ubb(n), counters(kNumCounters), work(1);
+    const unsigned long long kInfBits = 0x7ff0000000000000ull;
+    TJ_CUDA(cudaMemsetAsync(iv_lb.p, 0, n * 8, st));
+    count_launch();
+    k_fill_u64<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(reinterpret_cast<unsigned long long*>(iv_ub.p), n,
+                                                              kInfBits);
+    RefineSource src{};
+    src.active = active.p;
+    src.r_foff = R.facet_offsets[sr].p;
+    src.s_foff = S.facet_offsets[ss].p;
+    src.cand_lb = iv_lb.p;
+    src.cand_ub = iv_ub.p;
+    src.r_facets = R.facets[sr].p;
+    src.s_facets = S.facets[ss].p;
+    src.zero_pad = 1;
+    const uint64_t nr = R.level_entries[sr], ns = S.level_entries[ss];
+    ws.screen_r.reserve(std::max<uint64_t>(nr * kScreenRecF4, 1));
+    refine_prep(R.facets[sr].p, nr, ws.screen_r.p, nullptr, ws.num_sms, st, 1);
+    src.r_box = ws.screen_r.p;
+    src.r_geo = ws.screen_r.p + 3 * nr;
+    ws.seg_r.reserve(std::max<uint64_t>(3 * R.n_voxels, 1));
+    refine_seg_prep(src.r_box, R.facet_offsets[sr].p, R.n_voxels, ws.seg_r.p, ws.num_sms, st);
+    src.r_seg = ws.seg_r.p;
+    if (S.facets[ss].p == R.facets[sr].p) {
+        src.s_box = src.r_box;
+        src.s_geo = src.r_geo;
+        src.s_seg = src.r_seg;
+    } else {
+        ws.screen_s.reserve(std::max<uint64_t>(ns * kScreenRecF4, 1));
+        refine_prep(S.facets[ss].p, ns, ws.screen_s.p, nullptr, ws.num_sms, st, 1);
+        src.s_box = ws.screen_s.p;
+        src.s_geo = ws.screen_s.p + 3 * ns;
+        ws.seg_s.reserve(std::max<uint64_t>(3 * S.n_voxels, 1));
+        refine_seg_prep(src.s_box, S.facet_offsets[ss].p, S.n_voxels, ws.seg_s.p, ws.num_sms, st);
+        src.s_seg = ws.seg_s.p;
+    }
+    if (!ws.queue) ws.queue = std::make_unique<RefineQueueStore>();
+    RefineQueueStore& queue = *ws.queue;
+    const uint64_t launch = 1ull << 20;
+    for (;;) {
+        count_launch();
+        k_fill_u64<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(lbb.p, n, kInfBits);
+        count_launch();
+        k_fill_u64<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(ubb.p, n, kInfBits);
+        TJ_CUDA(cudaMemsetAsync(queue.count.p, 0, 16, st));
+        for (uint64_t c0 = 0; c0 < total; c0 += launch)
+            refine_pass(src, c0, std::min(total, c0 + launch), true, lbb.p, ubb.p, 1, queue, work.p, counters.p,
+                        ws.num_sms, st);
+        for (uint64_t c0 = 0; c0 < total; c0 += launch)
+            refine_pass(src, c0, std::min(total, c0 + launch), false, lbb.p, ubb.p, 1, queue, work.p, counters.p,
+                        ws.num_sms, st);
+        unsigned long long ovf = 0;
+        TJ_CUDA(cudaMemcpyAsync(&ovf, queue.count.p + 1, 8, cudaMemcpyDeviceToHost, st));
+        stream_sync(st);
+        if (ovf == 0) break;
+        queue.items.alloc(ovf + ovf / 4);
+    }
+    count_launch();
+    k_exact_store<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(cs.view(), n, lbb.p);
+    TJ_CUDA(cudaGetLastError());
+}
+
 } // namespace tjx

@@ -150,6 +150,8 @@ struct RefineSource {
     // voxel; join mode only, else nullptr)
     const float4* r_seg;
     const float4* s_seg;
+    // 1: ignore the records' hd / ph (pure tri-tri minima: the --exact recompute)
+    int zero_pad;
 };
 
 // A queued facet pair: op and the two global facet record indices.
@@ -177,7 +179,8 @@ struct RefineQueueStore {
 // FP32 screening records of n facet records (refine.cu, k_prep) into out[7 n]: box parts at
 // out[0, 3 n), geometry parts at out[3 n, 7 n).
 // agg (optional, 3 uints pre-set to {+inf, 0, 0} bits): min hd, max |L|, max M of the records.
-void refine_prep(const double* facets, uint64_t n, float4* out, unsigned* agg, int num_sms, cudaStream_t st);
+void refine_prep(const double* facets, uint64_t n, float4* out, unsigned* agg, int num_sms, cudaStream_t st,
+                 int zero_pad = 0);
 
 // Per-voxel segment aggregates of one level (refine.cu, k_seg_prep) into seg[3 n_voxels]:
 // union of the facet boxes, max / min L, max ph, min hd, all well shaped.

@@ -67,6 +67,7 @@ DATASETS = {
     "mini18_s21": ("mini", 18, 3.3, 21, 100, 0.02),
     "mini9_s13_vr15": ("mini", 9, 3.4, 13, 150, 0.15),
     "mini14_s53": ("mini", 14, 3.3, 53, 80, 0.02),
+    "mini10_s77": ("mini", 10, 3.2, 77, 90, 0.02),
 }
 # generated (reference generator + preprocessor, lods [20,60,100]): nuclei vs vessels
 GENERATED = {
@@ -96,6 +97,10 @@ JOINS += [
     ("spheres80a", "spheres80b", dict(type="intersect", lods=[20, 60, 100])),
     ("spheres80a", "spheres80b", dict(type="within", tau=0.2, lods=[20, 60, 100])),
     ("spheres80a", "", dict(type="within", tau=0.1, lods=[20, 60, 100])),
+    # --exact (proj/tests/test_engine.cpp:180-196)
+    ("mini10_s77", "", dict(type="within", tau=1.2, exact=True)),
+    ("mini14_s53", "", dict(type="knn", k=3, exact=True)),
+    ("nuclei60", "vessels8", dict(type="within", tau=0.5, lods=[20, 60, 100], exact=True)),
 ]
 
 # (dataset, tau, levels) for staged refine-kernel dumps (test_refine.cpp:92-146 logic)

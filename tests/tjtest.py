@@ -150,8 +150,10 @@ class Capi:
         return ds
 
     def join(self, R, S, type="within", tau=0.0, k=1, lods=(20, 40, 60, 80, 100), flags=0, refine_chunk=500000,
-             shard=(0, 1)):
+             shard=(0, 1), exact=False):
         arr = (ctypes.c_uint32 * len(lods))(*lods)
+        if exact:
+            flags |= 8  # TJ_FLAG_EXACT_RECOMPUTE
         spec = JoinSpec(self.TYPES[type], tau, k, 4194304, refine_chunk, len(lods), arr, 1, flags, shard[0],
                         shard[1], 1024)
         res = JoinResult()
@@ -219,11 +221,11 @@ def load_oracle():
     return ctypes.CDLL(ORACLE_LIB)
 
 
-def oracle_join(lib, r_path, s_path, type="within", tau=0.0, k=1, lods=(20, 40, 60, 80, 100)):
+def oracle_join(lib, r_path, s_path, type="within", tau=0.0, k=1, lods=(20, 40, 60, 80, 100), exact=False):
     res = OraResult()
     arr = (ctypes.c_uint32 * len(lods))(*lods)
-    lib.ora_join_files(r_path.encode(), (s_path or "").encode(), Capi.TYPES[type], ctypes.c_double(tau), k, arr,
-                       len(lods), ctypes.byref(res))
+    lib.ora_join_files_ex(r_path.encode(), (s_path or "").encode(), Capi.TYPES[type], ctypes.c_double(tau), k, arr,
+                          len(lods), 1 if exact else 0, ctypes.byref(res))
     if res.status != 0:
         raise RuntimeError(res.error.decode())
     recs = [(x.r, x.s, x.lb, x.ub, stage_name(x.stage), x.rank) for x in res.records[:res.n_records]]

@@ -129,6 +129,22 @@ T* host_copy(const DevBuf<T>& src, uint64_t n, cudaStream_t st) {
 }
 
 
+// Byte layout of one level's compact arrays in a dataset's staging area (256-B aligned parts).
+struct StageLayout {
+    uint64_t verts, tris, hd, ph, vf, total;
+};
+StageLayout stage_layout(uint64_t nvert, uint64_t nfac, uint64_t entries) {
+    auto up = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };
+    StageLayout L;
+    L.verts = 0;
+    L.tris = up(nvert * 24);
+    L.hd = L.tris + up(nfac * 12);
+    L.ph = L.hd + up(nfac * 8);
+    L.vf = L.ph + up(nfac * 8);
+    L.total = L.vf + up(entries * 4);
+    return L;
+}
+
 // Object and voxel arrays of a dataset view (shared by tj_dataset_upload / _begin).
 void upload_objects(DatasetDev& d, const tj_dataset_view* v, cudaStream_t st) {
     if (v->n_levels == 0 || v->n_levels > TJ_MAX_LODS)
@@ -405,6 +421,10 @@ int tj_dataset_begin(tj_ctx* ctx, const tj_dataset_view* v, const uint64_t* cons
             d.level_facets.push_back(fb[no]);
             d.bytes += (d.n_voxels + 1) * 8 + entries * TJ_FACET_STRIDE * 8;
         }
+        uint64_t stage_bytes = 256;
+        for (uint32_t li = 0; li < v->n_levels; ++li)
+            stage_bytes = std::max(stage_bytes, stage_layout(d.level_vertices[li], d.level_facets[li], d.level_entries[li]).total);
+        d.stage.alloc(stage_bytes);
         d.vox_obj.alloc(std::max<uint64_t>(d.n_voxels, 1));
         if (no) {
             count_launch();
@@ -442,17 +462,27 @@ int tj_dataset_put_level(tj_dataset* ds, uint32_t slot, const tj_level_mesh_view
         const uint64_t nvert = d.level_vertices[slot], nfac = d.level_facets[slot], used = d.level_entries[slot];
         if ((nvert && !lv->vertices) || (nfac && (!lv->tris || !lv->hd || !lv->ph)) || (used && !lv->voxel_facets))
             throw Error(TJ_EINVAL, "tj_dataset_put_level: null level arrays");
-        DevBuf<double> verts, hd, ph;
-        DevBuf<uint32_t> tris, vf;
-        upload(verts, lv->vertices, nvert * 3, g.copy);
-        upload(tris, lv->tris, nfac * 3, g.copy);
-        upload(hd, lv->hd, nfac, g.copy);
-        upload(ph, lv->ph, nfac, g.copy);
-        upload(vf, lv->voxel_facets, used, g.copy);
+        // compact arrays into the dataset's staging area (reserved at tj_dataset_begin: no
+        // allocation here, so a put never waits on the memory pool while a join runs); the
+        // copy stream orders the reuse of the area across levels
+        StageLayout L = stage_layout(nvert, nfac, used);
+        unsigned char* base = d.stage.p;
+        double* verts = reinterpret_cast<double*>(base + L.verts);
+        uint32_t* tris = reinterpret_cast<uint32_t*>(base + L.tris);
+        double* hd = reinterpret_cast<double*>(base + L.hd);
+        double* ph = reinterpret_cast<double*>(base + L.ph);
+        uint32_t* vf = reinterpret_cast<uint32_t*>(base + L.vf);
+        if (nvert) TJ_CUDA(cudaMemcpyAsync(verts, lv->vertices, nvert * 24, cudaMemcpyHostToDevice, g.copy));
+        if (nfac) {
+            TJ_CUDA(cudaMemcpyAsync(tris, lv->tris, nfac * 12, cudaMemcpyHostToDevice, g.copy));
+            TJ_CUDA(cudaMemcpyAsync(hd, lv->hd, nfac * 8, cudaMemcpyHostToDevice, g.copy));
+            TJ_CUDA(cudaMemcpyAsync(ph, lv->ph, nfac * 8, cudaMemcpyHostToDevice, g.copy));
+        }
+        if (used) TJ_CUDA(cudaMemcpyAsync(vf, lv->voxel_facets, used * 4, cudaMemcpyHostToDevice, g.copy));
         if (d.n_voxels) {
             const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((d.n_voxels + 7) / 8, (uint64_t)ctx->ws.num_sms * 16));
             count_launch();
-            k_expand_level<<<grid, 256, 0, g.copy>>>(verts.p, tris.p, hd.p, ph.p, vf.p, d.facet_offsets[slot].p,
+            k_expand_level<<<grid, 256, 0, g.copy>>>(verts, tris, hd, ph, vf, d.facet_offsets[slot].p,
                                                       d.vox_obj.p, d.vert_base[slot].p, d.facet_base[slot].p,
                                                       d.n_voxels, d.facets[slot].p, d.stream_err.p);
             TJ_CUDA(cudaGetLastError());

@@ -76,6 +76,7 @@ namespace {
 struct PinnedArena {
     std::mutex mu;
     std::multimap<size_t, std::pair<double*, bool>> free_blocks; // capacity (doubles) -> (block, pinned)
+    std::atomic<uint64_t> n_new{0}, n_pageable{0}, bytes_new{0}, ns_new{0}; // diagnostics (stats JSON)
     double* acquire(size_t want, size_t& cap, bool& pinned) {
         {
             std::lock_guard<std::mutex> lk(mu);
@@ -90,11 +91,17 @@ struct PinnedArena {
         }
         void* p = nullptr;
         cap = want;
-        if (cudaHostAlloc(&p, want * sizeof(double), cudaHostAllocPortable) == cudaSuccess) {
+        const auto t0 = std::chrono::steady_clock::now();
+        const bool ok = cudaHostAlloc(&p, want * sizeof(double), cudaHostAllocPortable) == cudaSuccess;
+        ++n_new;
+        bytes_new += want * sizeof(double);
+        ns_new += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
+        if (ok) {
             pinned = true;
             return static_cast<double*>(p);
         }
         cudaGetLastError(); // no device / pinning refused: pageable host memory
+        ++n_pageable;
         pinned = false;
         p = std::malloc(want * sizeof(double));
         if (!p) throw std::bad_alloc();
@@ -111,6 +118,11 @@ PinnedArena& arena() {
     return *a;
 }
 } // namespace
+
+ArenaStats arena_stats() {
+    PinnedArena& a = arena();
+    return {a.n_new.load(), a.n_pageable.load(), a.bytes_new.load(), a.ns_new.load() / 1e6};
+}
 
 PinnedBuf& PinnedBuf::operator=(PinnedBuf&& o) noexcept {
     if (this != &o) {
@@ -728,6 +740,7 @@ JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const Jo
     // Streamed upload (tj_dataset_begin / _put_level): object + voxel arrays first, then
     // each LOD level the join uses, coarsest first, packed on the host in the compact mesh
     // form while the devices already run the filters and the coarser levels.
+    const detail::ArenaStats arena0 = detail::arena_stats();
     auto tp = Clock::now();
     auto hr = detail::pack_header(R, pool);
     std::unique_ptr<detail::PackedHeader> hs_own;
@@ -795,6 +808,7 @@ JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const Jo
                 const auto tl = Clock::now();
                 staged.push_back(detail::pack_level(D, H, static_cast<size_t>(slot), pool));
                 pack_ms += std::chrono::duration<double, std::milli>(Clock::now() - tl).count();
+                mark(std::string(side == 0 ? "R" : "S") + "_lod" + std::to_string(level) + "_packed");
                 out.stats.h2d_bytes += G * (H.n_vertices[slot] * 24 + H.n_facets[slot] * 28 + H.facet_offsets[slot].back() * 4);
                 for (size_t g = 0; g < G; ++g) {
                     tj_dataset* ds = side == 0 ? dr[g].p : dsh[g].p;
@@ -818,6 +832,12 @@ JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const Jo
     }
     for (auto& t : joins) t.join();
     mark("joins_done");
+    {
+        const detail::ArenaStats a1 = detail::arena_stats();
+        out.stats.timeline.emplace_back("arena_fresh_blocks", double(a1.fresh - arena0.fresh));
+        out.stats.timeline.emplace_back("arena_pageable_blocks", double(a1.pageable - arena0.pageable));
+        out.stats.timeline.emplace_back("arena_fresh_ms", a1.fresh_ms - arena0.fresh_ms);
+    }
     for (size_t g = 0; g < G; ++g) {
         tj_dataset_sync(dr[g].p);
         if (!self_join) tj_dataset_sync(dsh[g].p);

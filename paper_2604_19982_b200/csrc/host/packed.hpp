@@ -45,6 +45,14 @@ struct PackedDataset {
 
 std::unique_ptr<PackedDataset> pack_dataset(const PreparedDataset& ds, ThreadPool& pool);
 
+// Host staging arena counters (process lifetime): fresh blocks, blocks that could not be
+// page-locked, bytes and milliseconds spent allocating fresh blocks.
+struct ArenaStats {
+    uint64_t fresh, pageable, fresh_bytes;
+    double fresh_ms;
+};
+ArenaStats arena_stats();
+
 // Streamed form (tj_dataset_begin / tj_dataset_put_level): the header holds the object and
 // voxel arrays, the per-level voxel CSR and the per-object vertex / facet bases; each level
 // is then packed on its own in the reference's compact mesh form.

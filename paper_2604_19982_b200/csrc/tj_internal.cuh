@@ -108,6 +108,7 @@ struct DatasetDev {
     std::vector<uint64_t> level_vertices, level_facets;  // per level totals
     DevBuf<uint32_t> vox_obj;                            // [nv]
     DevBuf<int> stream_err;                              // [1]: an index out of range
+    DevBuf<unsigned char> stage;                         // compact-level staging area (largest level)
     std::shared_ptr<LevelGate> gate;
 };
 

@@ -280,9 +280,15 @@ std::unique_ptr<PackedHeader> pack_header(const PreparedDataset& ds, ThreadPool&
     h->levels.assign(ds.lod_schedule.begin(), ds.lod_schedule.end());
     h->mbb.resize(6 * no);
     h->anchor.resize(3 * no);
-    h->voxel_offsets.assign(no + 1, 0);
-    h->vert_base.assign(nl, std::vector<uint64_t>(no + 1, 0));
-    h->facet_base.assign(nl, std::vector<uint64_t>(no + 1, 0));
+    h->voxel_offsets.resize(no + 1);
+    h->voxel_offsets[0] = 0;
+    h->vert_base.resize(nl);
+    h->facet_base.resize(nl);
+    for (size_t li = 0; li < nl; ++li) {
+        h->vert_base[li].resize(no + 1);
+        h->facet_base[li].resize(no + 1);
+        h->vert_base[li][0] = h->facet_base[li][0] = 0;
+    }
     // per-object counts in parallel (written at o + 1), then serial prefix sums
     std::atomic<int> bad_levels{0}, bad_pad{0};
     for_blocks(pool, no, [&](size_t b, size_t e) {
@@ -319,7 +325,11 @@ std::unique_ptr<PackedHeader> pack_header(const PreparedDataset& ds, ThreadPool&
     }
     h->voxel_box.resize(6 * nv);
     h->voxel_anchor.resize(3 * nv);
-    h->facet_offsets.assign(nl, std::vector<uint64_t>(nv + 1, 0));
+    h->facet_offsets.resize(nl);
+    for (size_t li = 0; li < nl; ++li) {
+        h->facet_offsets[li].resize(nv + 1);
+        h->facet_offsets[li][0] = 0;
+    }
     for_blocks(pool, no, [&](size_t b, size_t e) {
         for (size_t o = b; o < e; ++o) {
             const PreparedObject& obj = ds.objects[o];

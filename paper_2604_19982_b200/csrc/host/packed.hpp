@@ -29,6 +29,25 @@ struct PinnedBuf {
     size_t size() const { return n; }
 };
 
+// Typed view of a PinnedBuf for 8-byte element types; resize() leaves contents undefined
+// (no serial zero-fill: the parallel packers touch every element they use).
+template <class T>
+struct PinnedArr {
+    static_assert(sizeof(T) == sizeof(double), "8-byte elements only");
+    PinnedBuf b;
+    size_t n = 0;
+    void resize(size_t count) {
+        b.resize(count ? count : 1);
+        n = count;
+    }
+    T* data() { return reinterpret_cast<T*>(b.data()); }
+    const T* data() const { return reinterpret_cast<const T*>(b.data()); }
+    T& operator[](size_t i) { return data()[i]; }
+    const T& operator[](size_t i) const { return data()[i]; }
+    size_t size() const { return n; }
+    const T& back() const { return data()[n - 1]; }
+};
+
 // Owning SoA image of one PreparedDataset in the device layout (include/tj_capi.h).
 struct PackedDataset {
     uint32_t n_objects = 0;
@@ -59,10 +78,10 @@ ArenaStats arena_stats();
 struct PackedHeader {
     uint32_t n_objects = 0;
     std::vector<int32_t> levels;
-    std::vector<double> mbb, anchor, voxel_box, voxel_anchor;
-    std::vector<uint64_t> voxel_offsets;
-    std::vector<std::vector<uint64_t>> facet_offsets;           // per level [nv+1]
-    std::vector<std::vector<uint64_t>> vert_base, facet_base;   // per level [n_objects+1]
+    PinnedArr<double> mbb, anchor, voxel_box, voxel_anchor;     // page-locked, reused across joins
+    PinnedArr<uint64_t> voxel_offsets;
+    std::vector<PinnedArr<uint64_t>> facet_offsets;             // per level [nv+1]
+    std::vector<PinnedArr<uint64_t>> vert_base, facet_base;     // per level [n_objects+1]
     std::vector<uint64_t> n_vertices, n_facets;                  // per level totals
     std::vector<const uint64_t*> fo_ptrs, vb_ptrs, fb_ptrs;
     tj_dataset_view view{};

@@ -387,14 +387,17 @@ int tj_dataset_begin(tj_ctx* ctx, const tj_dataset_view* v, const uint64_t* cons
     ds->ctx = ctx;
     const int rc = guarded(ctx, [&] {
         DatasetDev& d = ds->d;
-        cudaStream_t st = ctx->stream;
-        upload_objects(d, v, st);
-        const uint32_t no = d.n_objects;
         auto gate = std::make_shared<LevelGate>();
         gate->device = ctx->device;
+        TJ_CUDA(cudaStreamCreateWithFlags(&gate->copy, cudaStreamNonBlocking));
+        // everything on the dataset's own copy stream: a begin may run while a join occupies
+        // the context's stream (the next R chunk of the out-of-core path)
+        cudaStream_t st = gate->copy;
+        AllocStreamScope scope(st);
+        upload_objects(d, v, st);
+        const uint32_t no = d.n_objects;
         gate->state.assign(v->n_levels, LevelGate::kPending);
         gate->ev.assign(v->n_levels, nullptr);
-        TJ_CUDA(cudaStreamCreateWithFlags(&gate->copy, cudaStreamNonBlocking));
         d.vert_base.resize(v->n_levels);
         d.facet_base.resize(v->n_levels);
         for (uint32_t li = 0; li < v->n_levels; ++li) {

@@ -252,6 +252,12 @@ std::unique_ptr<PackedDataset> pack_dataset(const PreparedDataset& ds, ThreadPoo
 }
 
 namespace {
+// A contiguous run of a dataset's objects (the packers' view: R chunks of the out-of-core path).
+struct ObjRange {
+    std::span<const PreparedObject> objects;
+    ObjRange(const PreparedObject* p, size_t n) : objects(p, n) {}
+};
+
 // fn(begin, end) over [0, n) in ~8 contiguous blocks per worker (one pool job per block).
 void for_blocks(ThreadPool& pool, size_t n, const std::function<void(size_t, size_t)>& fn) {
     if (n == 0) return;
@@ -273,11 +279,16 @@ uint64_t PackedHeader::bytes() const {
 }
 
 std::unique_ptr<PackedHeader> pack_header(const PreparedDataset& ds, ThreadPool& pool) {
+    return pack_header(ds, 0, ds.objects.size(), pool);
+}
+
+std::unique_ptr<PackedHeader> pack_header(const PreparedDataset& dsf, size_t first, size_t last, ThreadPool& pool) {
     auto h = std::make_unique<PackedHeader>();
+    const ObjRange ds{dsf.objects.data() + first, last - first};
     const size_t no = ds.objects.size();
-    const size_t nl = ds.lod_schedule.size();
+    const size_t nl = dsf.lod_schedule.size();
     h->n_objects = static_cast<uint32_t>(no);
-    h->levels.assign(ds.lod_schedule.begin(), ds.lod_schedule.end());
+    h->levels.assign(dsf.lod_schedule.begin(), dsf.lod_schedule.end());
     h->mbb.resize(6 * no);
     h->anchor.resize(3 * no);
     h->voxel_offsets.resize(no + 1);
@@ -382,7 +393,13 @@ std::unique_ptr<PackedHeader> pack_header(const PreparedDataset& ds, ThreadPool&
 // triples, hd / ph and voxel facet-id lists (object-local ids; the device rebases and
 // range-checks them, k_expand_level).
 std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& ds, const PackedHeader& h, size_t li, ThreadPool& pool) {
+    return pack_level(ds, 0, h, li, pool);
+}
+
+std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& dsf, size_t first, const PackedHeader& h, size_t li,
+                                        ThreadPool& pool) {
     auto p = std::make_unique<PackedLevel>();
+    const ObjRange ds{dsf.objects.data() + first, h.n_objects};
     const size_t no = ds.objects.size();
     const uint64_t nvert = h.n_vertices[li], nfac = h.n_facets[li];
     const uint64_t entries = h.facet_offsets[li].back();
@@ -544,7 +561,7 @@ std::string StageStats::to_json() const {
     j["stages"] = std::move(arr);
     j["b200"] = {{"pack_ms", pack_ms}, {"upload_ms", upload_ms}, {"device_ms", device_ms},
                  {"stream_wait_ms", stream_wait_ms}, {"h2d_bytes", h2d_bytes}, {"devices", devices},
-                 {"intervals", decision_mode ? "decision" : "exact"}};
+                 {"intervals", decision_mode ? "decision" : "exact"}, {"r_chunks", r_chunks}};
     nlohmann::json tl = nlohmann::json::object();
     for (const auto& [k, v] : timeline) tl[k] = v;
     j["b200"]["timeline"] = std::move(tl);
@@ -728,6 +745,189 @@ tj_join_spec to_c_spec(const JoinSpec& spec) {
     return c;
 }
 
+// One part of a join's device results: queries [r_base, r_base + n) (or a GPU shard).
+struct Piece {
+    const tj_join_result* res;
+    uint32_t r_base;
+};
+
+int slot_of(const PreparedDataset& d, uint32_t level) {
+    for (size_t i = 0; i < d.lod_schedule.size(); ++i)
+        if (d.lod_schedule[i] == static_cast<int>(level)) return static_cast<int>(i);
+    return -1;
+}
+
+// ---- out-of-core R: the device-memory budget ----
+// Device bytes one object costs while resident: object + voxel records, the 96-B facet
+// records of every level, the compact staging of its largest level and its share of the
+// per-level screening workspace (128-B records + 48-B voxel aggregates).
+uint64_t object_device_bytes(const PreparedObject& o) {
+    uint64_t all = 0, mx = 0;
+    for (const auto& lv : o.voxels.facets_per_level) {
+        uint64_t e = 0;
+        for (const auto& ids : lv) e += ids.size();
+        all += e;
+        mx = std::max(mx, e);
+    }
+    const uint64_t nv = o.voxels.voxel_count();
+    return 256 + 112 * nv + 96 * all + (44 + 176) * mx;
+}
+
+// R split into consecutive object chunks so that S (resident for the whole join) and two R
+// chunks (one joining, the next uploading) fit the budget: $TRIJOIN_DEVICE_BUDGET_MB, else
+// 90 % of the device's free memory. $TRIJOIN_R_CHUNK_OBJECTS forces a chunk size. One
+// chunk = the whole of R (the resident path).
+std::vector<std::pair<size_t, size_t>> plan_r_chunks(const PreparedDataset& R, const PreparedDataset& S,
+                                                     const JoinSpec&, int device, bool self_join) {
+    const size_t nr = R.objects.size();
+    if (const char* e = std::getenv("TRIJOIN_R_CHUNK_OBJECTS"); e && *e) {
+        const size_t step = std::max<size_t>(1, std::stoull(e));
+        std::vector<std::pair<size_t, size_t>> plan;
+        for (size_t a = 0; a < nr; a += step) plan.emplace_back(a, std::min(nr, a + step));
+        if (plan.empty()) plan.emplace_back(0, 0);
+        return plan;
+    }
+    uint64_t budget = 0;
+    if (const char* e = std::getenv("TRIJOIN_DEVICE_BUDGET_MB"); e && *e) {
+        budget = std::stoull(e) << 20;
+    } else {
+        size_t free_b = 0, total_b = 0;
+        if (cudaSetDevice(device) != cudaSuccess || cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+            cudaGetLastError();
+            return {{0, nr}};
+        }
+        budget = free_b / 10 * 9;
+    }
+    std::vector<uint64_t> cost(nr);
+    uint64_t r_total = 0, s_total = 0;
+    for (size_t o = 0; o < nr; ++o) r_total += cost[o] = object_device_bytes(R.objects[o]);
+    if (!self_join)
+        for (const auto& o : S.objects) s_total += object_device_bytes(o);
+    const uint64_t fixed = (64ull << 20) + 256 * uint64_t{nr};
+    if (r_total + s_total + fixed <= budget) return {{0, nr}};
+    // chunked: S in full (for a self-join a second, complete copy) + two R chunks
+    const uint64_t s_res = self_join ? r_total : s_total;
+    if (s_res + fixed >= budget) throw std::runtime_error("trijoin: S does not fit the device-memory budget");
+    const uint64_t per_chunk = (budget - s_res - fixed) / 2;
+    std::vector<std::pair<size_t, size_t>> plan;
+    size_t a = 0;
+    uint64_t acc = 0;
+    for (size_t o = 0; o < nr; ++o) {
+        if (cost[o] > per_chunk) throw std::runtime_error("trijoin: one R object exceeds the device-memory budget");
+        if (acc + cost[o] > per_chunk) {
+            plan.emplace_back(a, o);
+            a = o;
+            acc = 0;
+        }
+        acc += cost[o];
+    }
+    plan.emplace_back(a, nr);
+    return plan;
+}
+
+// Out-of-core device phase: S resident on every GPU (streamed once), R chunks dealt to the
+// GPUs round-robin; on each GPU the next chunk is packed and uploaded (its own copy stream)
+// while the current chunk joins. results[k] holds chunk k (queries local to the chunk).
+void run_chunked(const PreparedDataset& R, const PreparedDataset& S, const JoinSpec& spec, ThreadPool& pool,
+                 const std::vector<int>& devices, const std::vector<std::pair<size_t, size_t>>& plan,
+                 std::vector<detail::ResultHandle>& results, JoinOutput& out,
+                 const std::function<void(const std::string&)>& mark) {
+    using Clock = std::chrono::steady_clock;
+    const size_t G = devices.size();
+    out.stats.devices = static_cast<uint32_t>(G);
+    results = std::vector<detail::ResultHandle>(plan.size());
+    // S: header + every level the join uses, streamed to each GPU once
+    auto hs = detail::pack_header(S, pool);
+    std::vector<detail::DatasetHandle> dsh(G);
+    std::vector<std::unique_ptr<detail::PackedLevel>> s_levels;
+    for (size_t g = 0; g < G; ++g) {
+        tj_ctx* ctx = detail::device_context(devices[g]);
+        detail::check(tj_dataset_begin(ctx, &hs->view, hs->vb_ptrs.data(), hs->fb_ptrs.data(), &dsh[g].p), ctx);
+        out.stats.h2d_bytes += hs->bytes();
+    }
+    for (uint32_t level : spec.lods) {
+        const int slot = slot_of(S, level);
+        if (slot < 0) continue;
+        s_levels.push_back(detail::pack_level(S, *hs, static_cast<size_t>(slot), pool));
+        out.stats.h2d_bytes += G * (hs->n_vertices[slot] * 24 + hs->n_facets[slot] * 28 + hs->facet_offsets[slot].back() * 4);
+        for (size_t g = 0; g < G; ++g)
+            detail::check(tj_dataset_put_level(dsh[g].p, static_cast<uint32_t>(slot), &s_levels.back()->view),
+                          detail::device_context(devices[g]));
+    }
+    mark("S_streamed");
+    struct Prepared {
+        std::unique_ptr<detail::PackedHeader> h;
+        std::vector<std::unique_ptr<detail::PackedLevel>> lv; // outlive the dataset below
+        detail::DatasetHandle d;
+        ~Prepared() {
+            if (d.p) tj_dataset_sync(d.p);
+        }
+    };
+    std::mutex stat_mu;
+    auto prepare = [&](tj_ctx* ctx, size_t k) {
+        auto p = std::make_unique<Prepared>();
+        const auto [a, b] = plan[k];
+        p->h = detail::pack_header(R, a, b, pool);
+        detail::check(tj_dataset_begin(ctx, &p->h->view, p->h->vb_ptrs.data(), p->h->fb_ptrs.data(), &p->d.p), ctx);
+        uint64_t bytes = p->h->bytes();
+        for (uint32_t level : spec.lods) {
+            const int slot = slot_of(R, level);
+            if (slot < 0) continue; // the join reports the missing level
+            p->lv.push_back(detail::pack_level(R, a, *p->h, static_cast<size_t>(slot), pool));
+            bytes += p->h->n_vertices[slot] * 24 + p->h->n_facets[slot] * 28 + p->h->facet_offsets[slot].back() * 4;
+            detail::check(tj_dataset_put_level(p->d.p, static_cast<uint32_t>(slot), &p->lv.back()->view), ctx);
+        }
+        std::lock_guard<std::mutex> lk(stat_mu);
+        out.stats.h2d_bytes += bytes;
+        return p;
+    };
+    std::vector<std::exception_ptr> errors(G);
+    std::vector<double> dev_ms(G, 0.0);
+    auto worker = [&](size_t g) {
+        try {
+            tj_ctx* ctx = detail::device_context(devices[g]);
+            tj_join_spec cs = to_c_spec(spec);
+            std::vector<size_t> mine;
+            for (size_t k = g; k < plan.size(); k += G) mine.push_back(k);
+            if (mine.empty()) return;
+            std::unique_ptr<Prepared> next = prepare(ctx, mine[0]);
+            for (size_t i = 0; i < mine.size(); ++i) {
+                std::unique_ptr<Prepared> cur = std::move(next);
+                std::exception_ptr je;
+                const auto td = Clock::now();
+                std::thread jt([&] {
+                    try {
+                        detail::check(tj_join(ctx, cur->d.p, dsh[g].p, &cs, nullptr, &results[mine[i]].r), ctx);
+                    } catch (...) {
+                        je = std::current_exception();
+                    }
+                });
+                std::exception_ptr pe;
+                try {
+                    if (i + 1 < mine.size()) next = prepare(ctx, mine[i + 1]); // overlaps the join
+                } catch (...) {
+                    pe = std::current_exception();
+                }
+                jt.join();
+                dev_ms[g] += std::chrono::duration<double, std::milli>(Clock::now() - td).count();
+                if (je) std::rethrow_exception(je);
+                if (pe) std::rethrow_exception(pe);
+            }
+        } catch (...) {
+            errors[g] = std::current_exception();
+        }
+    };
+    std::vector<std::thread> ts;
+    for (size_t g = 0; g < G; ++g) ts.emplace_back(worker, g);
+    for (auto& t : ts) t.join();
+    for (size_t g = 0; g < G; ++g) tj_dataset_sync(dsh[g].p);
+    for (auto& e : errors)
+        if (e) std::rethrow_exception(e);
+    out.stats.device_ms = *std::max_element(dev_ms.begin(), dev_ms.end());
+    out.stats.r_chunks = static_cast<uint32_t>(plan.size());
+    mark("joins_done");
+}
+
 } // namespace
 
 JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const JoinSpec& spec, ThreadPool& pool,
@@ -747,127 +947,152 @@ JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const Jo
     const size_t G = (trace && (trace->on_interval || trace->on_vp_pruned)) ? 1 : devices.size();
     out.stats.devices = static_cast<uint32_t>(G);
 
-    // Streamed upload (tj_dataset_begin / _put_level): object + voxel arrays first, then
-    // each LOD level the join uses, coarsest first, packed on the host in the compact mesh
-    // form while the devices already run the filters and the coarser levels.
-    const detail::ArenaStats arena0 = detail::arena_stats();
-    auto tp = Clock::now();
-    auto hr = detail::pack_header(R, pool);
-    std::unique_ptr<detail::PackedHeader> hs_own;
-    const detail::PackedHeader* hs = hr.get();
-    if (!self_join) {
-        hs_own = detail::pack_header(S, pool);
-        hs = hs_own.get();
-    }
-    double pack_ms = std::chrono::duration<double, std::milli>(Clock::now() - tp).count();
-    mark("header_packed");
-    std::vector<std::unique_ptr<detail::PackedLevel>> staged; // outlives the dataset handles below
-    std::vector<detail::DatasetHandle> dr(G), dsh(G);
-    const auto tu = Clock::now();
-    for (size_t g = 0; g < G; ++g) {
-        tj_ctx* ctx = detail::device_context(devices[g]);
-        detail::check(tj_dataset_begin(ctx, &hr->view, hr->vb_ptrs.data(), hr->fb_ptrs.data(), &dr[g].p), ctx);
-        out.stats.h2d_bytes += hr->bytes() + (self_join ? 0 : hs->bytes());
-        if (!self_join)
-            detail::check(tj_dataset_begin(ctx, &hs->view, hs->vb_ptrs.data(), hs->fb_ptrs.data(), &dsh[g].p), ctx);
-    }
-    out.stats.upload_ms = std::chrono::duration<double, std::milli>(Clock::now() - tu).count();
-    mark("datasets_begun");
+    // Device phase -> result pieces + the owner of every query.
+    std::vector<detail::ResultHandle> results;
+    std::vector<Piece> pieces;
+    std::function<size_t(uint32_t)> owner;
+    const bool tracing = trace && (trace->on_interval || trace->on_vp_pruned);
+    const std::vector<std::pair<size_t, size_t>> chunks =
+        tracing ? std::vector<std::pair<size_t, size_t>>{} : plan_r_chunks(R, S, spec, devices[0], self_join);
+    if (chunks.size() > 1) {
+        run_chunked(R, S, spec, pool, devices, chunks, results, out, mark);
+        for (size_t k = 0; k < chunks.size(); ++k)
+            pieces.push_back({&results[k].r, static_cast<uint32_t>(chunks[k].first)});
+        owner = [&chunks](uint32_t r) {
+            size_t lo = 0, hi = chunks.size();
+            while (hi - lo > 1) {
+                const size_t mid = (lo + hi) / 2;
+                if (chunks[mid].first <= r) lo = mid; else hi = mid;
+            }
+            return lo;
+        };
+    } else {
 
-    std::vector<detail::ResultHandle> results(G);
-    std::vector<std::exception_ptr> errors(G);
-    std::vector<double> dev_ms(G, 0.0);
-    auto run_shard = [&](size_t g) {
-        try {
-            tj_ctx* ctx = detail::device_context(devices[g]);
-            const auto td = Clock::now();
-            tj_join_spec cs = to_c_spec(spec);
-            cs.shard_index = static_cast<uint32_t>(g);
-            cs.shard_count = static_cast<uint32_t>(G);
-            cs.shard_block = 1024;
-            TraceBridge bridge{trace};
-            tj_trace tt{&bridge, &TraceBridge::interval, &TraceBridge::pruned};
-            detail::check(tj_join(ctx, dr[g].p, self_join ? dr[g].p : dsh[g].p, &cs, trace ? &tt : nullptr,
-                                  &results[g].r),
-                          ctx);
-            dev_ms[g] = std::chrono::duration<double, std::milli>(Clock::now() - td).count();
-        } catch (...) {
-            errors[g] = std::current_exception();
+        // Streamed upload (tj_dataset_begin / _put_level): object + voxel arrays first, then
+        // each LOD level the join uses, coarsest first, packed on the host in the compact mesh
+        // form while the devices already run the filters and the coarser levels.
+        const detail::ArenaStats arena0 = detail::arena_stats();
+        auto tp = Clock::now();
+        auto hr = detail::pack_header(R, pool);
+        std::unique_ptr<detail::PackedHeader> hs_own;
+        const detail::PackedHeader* hs = hr.get();
+        if (!self_join) {
+            hs_own = detail::pack_header(S, pool);
+            hs = hs_own.get();
         }
-    };
-    std::vector<std::thread> joins;
-    for (size_t g = 0; g < G; ++g) joins.emplace_back(run_shard, g);
+        double pack_ms = std::chrono::duration<double, std::milli>(Clock::now() - tp).count();
+        mark("header_packed");
+        std::vector<std::unique_ptr<detail::PackedLevel>> staged; // outlives the dataset handles below
+        std::vector<detail::DatasetHandle> dr(G), dsh(G);
+        const auto tu = Clock::now();
+        for (size_t g = 0; g < G; ++g) {
+            tj_ctx* ctx = detail::device_context(devices[g]);
+            detail::check(tj_dataset_begin(ctx, &hr->view, hr->vb_ptrs.data(), hr->fb_ptrs.data(), &dr[g].p), ctx);
+            out.stats.h2d_bytes += hr->bytes() + (self_join ? 0 : hs->bytes());
+            if (!self_join)
+                detail::check(tj_dataset_begin(ctx, &hs->view, hs->vb_ptrs.data(), hs->fb_ptrs.data(), &dsh[g].p), ctx);
+        }
+        out.stats.upload_ms = std::chrono::duration<double, std::milli>(Clock::now() - tu).count();
+        mark("datasets_begun");
 
-    // Producer: levels in join order; a level missing from a schedule is left to the join
-    // (EngineError from its level check). On failure every undelivered slot is released.
-    std::exception_ptr pack_error;
-    std::vector<std::vector<char>> put_r(G, std::vector<char>(R.lod_schedule.size(), 0));
-    std::vector<std::vector<char>> put_s(G, std::vector<char>(S.lod_schedule.size(), 0));
-    auto slot_of = [](const PreparedDataset& d, uint32_t level) -> int {
-        for (size_t i = 0; i < d.lod_schedule.size(); ++i)
-            if (d.lod_schedule[i] == static_cast<int>(level)) return static_cast<int>(i);
-        return -1;
-    };
-    try {
-        for (uint32_t level : spec.lods) {
-            for (int side = 0; side < (self_join ? 1 : 2); ++side) {
-                const PreparedDataset& D = side == 0 ? R : S;
-                const detail::PackedHeader& H = side == 0 ? *hr : *hs;
-                const int slot = slot_of(D, level);
-                if (slot < 0) continue;
-                const auto tl = Clock::now();
-                staged.push_back(detail::pack_level(D, H, static_cast<size_t>(slot), pool));
-                pack_ms += std::chrono::duration<double, std::milli>(Clock::now() - tl).count();
-                mark(std::string(side == 0 ? "R" : "S") + "_lod" + std::to_string(level) + "_packed");
-                out.stats.h2d_bytes += G * (H.n_vertices[slot] * 24 + H.n_facets[slot] * 28 + H.facet_offsets[slot].back() * 4);
-                for (size_t g = 0; g < G; ++g) {
-                    tj_dataset* ds = side == 0 ? dr[g].p : dsh[g].p;
-                    auto& put = side == 0 ? put_r[g] : put_s[g];
-                    put[slot] = 1;
-                    detail::check(tj_dataset_put_level(ds, static_cast<uint32_t>(slot), &staged.back()->view),
-                                  detail::device_context(devices[g]));
+        results = std::vector<detail::ResultHandle>(G);
+        std::vector<std::exception_ptr> errors(G);
+        std::vector<double> dev_ms(G, 0.0);
+        auto run_shard = [&](size_t g) {
+            try {
+                tj_ctx* ctx = detail::device_context(devices[g]);
+                const auto td = Clock::now();
+                tj_join_spec cs = to_c_spec(spec);
+                cs.shard_index = static_cast<uint32_t>(g);
+                cs.shard_count = static_cast<uint32_t>(G);
+                cs.shard_block = 1024;
+                TraceBridge bridge{trace};
+                tj_trace tt{&bridge, &TraceBridge::interval, &TraceBridge::pruned};
+                detail::check(tj_join(ctx, dr[g].p, self_join ? dr[g].p : dsh[g].p, &cs, trace ? &tt : nullptr,
+                                      &results[g].r),
+                              ctx);
+                dev_ms[g] = std::chrono::duration<double, std::milli>(Clock::now() - td).count();
+            } catch (...) {
+                errors[g] = std::current_exception();
+            }
+        };
+        std::vector<std::thread> joins;
+        for (size_t g = 0; g < G; ++g) joins.emplace_back(run_shard, g);
+
+        // Producer: levels in join order; a level missing from a schedule is left to the join
+        // (EngineError from its level check). On failure every undelivered slot is released.
+        std::exception_ptr pack_error;
+        std::vector<std::vector<char>> put_r(G, std::vector<char>(R.lod_schedule.size(), 0));
+        std::vector<std::vector<char>> put_s(G, std::vector<char>(S.lod_schedule.size(), 0));
+        auto slot_of = [](const PreparedDataset& d, uint32_t level) -> int {
+            for (size_t i = 0; i < d.lod_schedule.size(); ++i)
+                if (d.lod_schedule[i] == static_cast<int>(level)) return static_cast<int>(i);
+            return -1;
+        };
+        try {
+            for (uint32_t level : spec.lods) {
+                for (int side = 0; side < (self_join ? 1 : 2); ++side) {
+                    const PreparedDataset& D = side == 0 ? R : S;
+                    const detail::PackedHeader& H = side == 0 ? *hr : *hs;
+                    const int slot = slot_of(D, level);
+                    if (slot < 0) continue;
+                    const auto tl = Clock::now();
+                    staged.push_back(detail::pack_level(D, H, static_cast<size_t>(slot), pool));
+                    pack_ms += std::chrono::duration<double, std::milli>(Clock::now() - tl).count();
+                    mark(std::string(side == 0 ? "R" : "S") + "_lod" + std::to_string(level) + "_packed");
+                    out.stats.h2d_bytes += G * (H.n_vertices[slot] * 24 + H.n_facets[slot] * 28 + H.facet_offsets[slot].back() * 4);
+                    for (size_t g = 0; g < G; ++g) {
+                        tj_dataset* ds = side == 0 ? dr[g].p : dsh[g].p;
+                        auto& put = side == 0 ? put_r[g] : put_s[g];
+                        put[slot] = 1;
+                        detail::check(tj_dataset_put_level(ds, static_cast<uint32_t>(slot), &staged.back()->view),
+                                      detail::device_context(devices[g]));
+                    }
+                    mark(std::string(side == 0 ? "R" : "S") + "_lod" + std::to_string(level) + "_put");
                 }
-                mark(std::string(side == 0 ? "R" : "S") + "_lod" + std::to_string(level) + "_put");
+            }
+        } catch (...) {
+            pack_error = std::current_exception();
+            for (size_t g = 0; g < G; ++g) {
+                for (size_t i = 0; i < put_r[g].size(); ++i)
+                    if (!put_r[g][i]) tj_dataset_put_level(dr[g].p, static_cast<uint32_t>(i), nullptr);
+                if (!self_join)
+                    for (size_t i = 0; i < put_s[g].size(); ++i)
+                        if (!put_s[g][i]) tj_dataset_put_level(dsh[g].p, static_cast<uint32_t>(i), nullptr);
             }
         }
-    } catch (...) {
-        pack_error = std::current_exception();
-        for (size_t g = 0; g < G; ++g) {
-            for (size_t i = 0; i < put_r[g].size(); ++i)
-                if (!put_r[g][i]) tj_dataset_put_level(dr[g].p, static_cast<uint32_t>(i), nullptr);
-            if (!self_join)
-                for (size_t i = 0; i < put_s[g].size(); ++i)
-                    if (!put_s[g][i]) tj_dataset_put_level(dsh[g].p, static_cast<uint32_t>(i), nullptr);
+        for (auto& t : joins) t.join();
+        mark("joins_done");
+        {
+            const detail::ArenaStats a1 = detail::arena_stats();
+            out.stats.timeline.emplace_back("arena_fresh_blocks", double(a1.fresh - arena0.fresh));
+            out.stats.timeline.emplace_back("arena_pageable_blocks", double(a1.pageable - arena0.pageable));
+            out.stats.timeline.emplace_back("arena_fresh_ms", a1.fresh_ms - arena0.fresh_ms);
         }
-    }
-    for (auto& t : joins) t.join();
-    mark("joins_done");
-    {
-        const detail::ArenaStats a1 = detail::arena_stats();
-        out.stats.timeline.emplace_back("arena_fresh_blocks", double(a1.fresh - arena0.fresh));
-        out.stats.timeline.emplace_back("arena_pageable_blocks", double(a1.pageable - arena0.pageable));
-        out.stats.timeline.emplace_back("arena_fresh_ms", a1.fresh_ms - arena0.fresh_ms);
-    }
-    for (size_t g = 0; g < G; ++g) {
-        tj_dataset_sync(dr[g].p);
-        if (!self_join) tj_dataset_sync(dsh[g].p);
-    }
-    if (pack_error) std::rethrow_exception(pack_error);
-    for (auto& e : errors)
-        if (e) std::rethrow_exception(e);
-    out.stats.pack_ms = pack_ms;
-    out.stats.device_ms = *std::max_element(dev_ms.begin(), dev_ms.end());
-    for (const auto& h : results) {
-        for (uint32_t i = 0; i < h.r.n_levels_run; ++i) out.stats.stream_wait_ms += h.r.level_wait_ms[i];
-        out.stats.decision_mode = h.r.decision_mode != 0;
+        for (size_t g = 0; g < G; ++g) {
+            tj_dataset_sync(dr[g].p);
+            if (!self_join) tj_dataset_sync(dsh[g].p);
+        }
+        if (pack_error) std::rethrow_exception(pack_error);
+        for (auto& e : errors)
+            if (e) std::rethrow_exception(e);
+        out.stats.pack_ms = pack_ms;
+        out.stats.device_ms = *std::max_element(dev_ms.begin(), dev_ms.end());
+        for (const auto& h : results) {
+            for (uint32_t i = 0; i < h.r.n_levels_run; ++i) out.stats.stream_wait_ms += h.r.level_wait_ms[i];
+            out.stats.decision_mode = h.r.decision_mode != 0;
+        }
+
+        for (size_t g = 0; g < G; ++g) pieces.push_back({&results[g].r, 0u});
+        owner = [G](uint32_t r) { return G == 1 ? size_t{0} : size_t{(r / 1024) % G}; };
     }
 
-    // Merge shards: query r is owned by shard (r / 1024) % G; each shard's arrays cover
-    // all queries with empty ranges for foreign ones.
+    // Merge: every query r is owned by one piece (a GPU shard, or an R chunk whose query ids
+    // start at r_base); a piece's arrays cover its own query range.
     Merged m;
     const uint32_t nq = static_cast<uint32_t>(R.objects.size());
     uint64_t total = 0;
-    for (auto& h : results) total += h.r.n_cands;
+    for (const Piece& pc : pieces) total += pc.res->n_cands;
     CandidateSet& c = m.cands;
     c.pairs.reserve(total);
     c.intervals.reserve(total);
@@ -876,19 +1101,21 @@ JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const Jo
     c.r2op_offsets.assign(nq + 1, 0);
     c.num_confirmed.assign(nq, 0);
     for (uint32_t r = 0; r < nq; ++r) {
-        const tj_join_result& res = results[G == 1 ? 0 : (r / 1024) % G].r;
+        const Piece& pc = pieces[owner(r)];
+        const tj_join_result& res = *pc.res;
+        const uint32_t lr = r - pc.r_base;
         c.r2op_offsets[r] = c.pairs.size();
-        for (uint64_t op = res.r2op_offsets[r]; op < res.r2op_offsets[r + 1]; ++op) {
-            c.pairs.emplace_back(res.pair_r[op], res.pair_s[op]);
+        for (uint64_t op = res.r2op_offsets[lr]; op < res.r2op_offsets[lr + 1]; ++op) {
+            c.pairs.emplace_back(res.pair_r[op] + pc.r_base, res.pair_s[op]);
             c.intervals.push_back({res.lb[op], res.ub[op]});
             c.status.push_back(static_cast<PairStatus>(res.status[op]));
             c.decided_at.push_back(res.decided_at[op]);
         }
-        c.num_confirmed[r] = res.num_confirmed[r];
+        c.num_confirmed[r] = res.num_confirmed[lr];
     }
     c.r2op_offsets[nq] = c.pairs.size();
-    for (auto& h : results) {
-        const tj_join_result& res = h.r;
+    for (const Piece& pc : pieces) {
+        const tj_join_result& res = *pc.res;
         m.vp_generated += res.vp_generated;
         m.vp_pruned += res.vp_pruned;
         m.mbb_ms = std::max(m.mbb_ms, res.mbb_ms);

@@ -93,6 +93,10 @@ struct PackedLevel {
 };
 std::unique_ptr<PackedHeader> pack_header(const PreparedDataset& ds, ThreadPool& pool);
 std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& ds, const PackedHeader& h, size_t li, ThreadPool& pool);
+// The same over objects [first, last) of ds (one R chunk of the out-of-core path).
+std::unique_ptr<PackedHeader> pack_header(const PreparedDataset& ds, size_t first, size_t last, ThreadPool& pool);
+std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& ds, size_t first, const PackedHeader& h, size_t li,
+                                        ThreadPool& pool);
 
 // Lazily created context per CUDA device, destroyed at process exit.
 tj_ctx* device_context(int device);

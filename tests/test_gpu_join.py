@@ -61,6 +61,27 @@ def test_chunk_and_cull_invariance(capi, refine_chunk):
         capi.free(R)
 
 
+OUT_OF_CORE = [j for j in JOINS if j["r"] in ("nuclei60", "mini18_s21", "mini10_s77", "spheres80a")]
+
+
+@pytest.mark.parametrize("env", [{"TRIJOIN_R_CHUNK_OBJECTS": "7"}, {"TRIJOIN_DEVICE_BUDGET_MB": "70"}],
+                         ids=["chunk7", "budget70MB"])
+@pytest.mark.parametrize("j", OUT_OF_CORE, ids=tjtest.join_id)
+def test_out_of_core_r_chunks(monkeypatch, env, j):
+    """R joined in consecutive object chunks against a resident S (device-memory budget,
+    SURVEY §8d config D): records and every stage counter equal the reference's."""
+    import paper_2604_19982_b200 as tj
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    r, s = _paths(j)
+    out = tj.join(r, s, **j["kwargs"])
+    assert out["records"] == j["records"]
+    stages = [{k: v for k, v in st.items() if k != "wall_ms"} for st in out["stats"]["stages"]]
+    assert stages == j["stages"]
+    if j["r"] == "nuclei60":
+        assert out["stats"]["b200"]["r_chunks"] > 1
+
+
 @pytest.mark.parametrize("idx", ["mini10_s61.idx", "mini18_s21.idx", "spheres80a.idx"])
 def test_intersect_decision_mode(capi, idx):
     """Intersection joins refine in decision mode unless TJ_FLAG_EXACT_INTERVALS (4): statuses

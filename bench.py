@@ -147,6 +147,7 @@ def main():
         "B": "B: intersection join, 100k x 100k nuclei (312-facet spheres)",
         "C": "C: k-NN k=3, 200k nuclei x 10k vessels",
         "D": "D: within-tau 0.2, 1M x 1M nuclei",
+        "E": "E: within-tau 0, 50k scanned-surface meshes (~20k facets) self-join",
     }[name]
     data_dir = os.path.join(a.data_dir, f"{name}_x{a.scale:g}")
 
@@ -193,7 +194,7 @@ def main():
         dist.barrier()
     r_path, s_path = synth.build_config(name, data_dir, scale=a.scale)
     R = tj.load_dataset(r_path)
-    S = tj.load_dataset(s_path)
+    S = tj.load_dataset(s_path) if s_path else R  # "" = self-join (config E)
     res = tj.Resident(R, S, device=local)
     setup_s = time.time() - t_setup
     flags = 1 if a.no_cull else 0

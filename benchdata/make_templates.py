@@ -25,6 +25,7 @@ TEMPLATES = {
     "sphere300_s035": ("sphere", 300, 0.35, 16),   # nuclei (configs B, C, D)
     "sphere1000_s035": ("sphere", 1000, 0.35, 8),  # nuclei, config A
     "tube1000_s3": ("tube", 1000, 3.0, 8),         # vessels (configs A, C)
+    "mixed20k": ("mixed", 20000, 1.0, 4),          # scanned-surface meshes, config E
 }
 
 

@@ -83,6 +83,11 @@ CONFIGS = {
     "D": (("sphere300_s035", 1000000, ("scatter", 41, (0, 0, 0, 100.7, 100.7, 100.7))),
           ("sphere300_s035", 1000000, ("scatter", 42, (0, 0, 0, 100.7, 100.7, 100.7))),
           dict(type="within", tau=0.2)),
+    # E: scanned-surface meshes (~20k facets), 50k objects, self-join within tau = 0
+    # (scattered in a cube of side 137.5, about 3 MBB neighbours each)
+    "E": (("mixed20k", 50000, ("scatter", 53, (0, 0, 0, 137.5, 137.5, 137.5))),
+          None,
+          dict(type="within", tau=0.0)),
 }
 LODS = [20, 60, 100]
 
@@ -142,6 +147,8 @@ def build_config(name, out_dir, scale=1.0, r_stride=1):
     s_path = os.path.join(out_dir, f"{name}_{key}_S.idx")
     done = r_path + ".ok"
     if os.path.exists(done):
+        if sspec is None:
+            return (r_path, s_path) if r_stride > 1 else (s_path, "")
         return r_path, s_path
     box_scale = float(np.cbrt(scale))
 
@@ -155,6 +162,15 @@ def build_config(name, out_dir, scale=1.0, r_stride=1):
         shifts = targets - centres[ids]
         return _core.load_dataset(tpath), ids[::stride], shifts[::stride], targets
 
+    if sspec is None:  # self-join: S is the full R; the R file is a slice of it when r_stride > 1
+        tmpl, ids, shifts, _ = make(rspec, None)
+        _core.replicate_index(tmpl, s_path, ids.tolist(), shifts.tolist())
+        if r_stride > 1:
+            _core.replicate_index(tmpl, r_path, ids[::r_stride].tolist(), shifts[::r_stride].tolist())
+        else:
+            r_path = s_path
+        open(done, "w").close()
+        return (r_path, s_path) if r_stride > 1 else (s_path, "")
     # S first: the "scatter_in" placements scatter R inside S's extent (generate's
     # scatter_within=V.extent in the reference configurations).
     tmpl_s, ids_s, shifts_s, targets_s = make(sspec, None)

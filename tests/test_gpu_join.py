@@ -170,7 +170,7 @@ def test_empty_inputs(capi, tmp_path):
     assert out["records"] == [] and out["stats"]["stages"][0]["pairs_in"] == 0
 
 
-@pytest.mark.parametrize("cfg,scale", [("B", 0.002), ("C", 0.0005), ("A", 0.02)])
+@pytest.mark.parametrize("cfg,scale", [("B", 0.002), ("C", 0.0005), ("A", 0.02), ("D", 0.0001), ("E", 0.001)])
 def test_benchmark_configs_match_reference(ref_module, tmp_path, cfg, scale):
     """Scaled benchmark configurations (same density) against the live reference build."""
     import paper_2604_19982_b200 as tj

@@ -8,6 +8,7 @@
 #include <pybind11/stl.h>
 
 #include <chrono>
+#include <cstring>
 #include <map>
 #include <memory>
 #include <string>
@@ -47,23 +48,46 @@ JoinSpec make_spec(const std::string& type, double tau, uint32_t k, uint64_t fil
 // (records, stats_json) as the reference's _core.join returns them (python/bindings.cpp:101-121);
 // built with the CPython API directly (one shared str per stage name).
 py::tuple pack_output(const JoinOutput& out) {
+    // hundreds of thousands of fresh tuples would trigger repeated cyclic-GC passes over
+    // the whole interpreter heap; the records hold no cycles, so collection is paused
+    struct GcPause {
+        int was = PyGC_Disable();
+        ~GcPause() {
+            if (was) PyGC_Enable();
+        }
+    } gc_pause;
     const size_t n = out.records.size();
     py::list records(n);
     std::map<int16_t, py::str> names;
+    // shared immutable objects: one int per object id, one float when ub == lb (bitwise)
+    std::vector<py::object> ints;
+    auto int_of = [&](uint32_t v) -> PyObject* {
+        if (v >= ints.size()) ints.resize(std::max<size_t>(v + 1, ints.size() * 2));
+        if (!ints[v]) ints[v] = py::reinterpret_steal<py::object>(PyLong_FromUnsignedLong(v));
+        PyObject* o = ints[v].ptr();
+        Py_INCREF(o);
+        return o;
+    };
     for (size_t i = 0; i < n; ++i) {
         const JoinResultRecord& r = out.records[i];
         auto it = names.find(r.decided_at);
         if (it == names.end()) it = names.emplace(r.decided_at, py::str(stage_name(r.decided_at))).first;
         PyObject* t = PyTuple_New(6);
         if (!t) throw py::error_already_set();
-        PyTuple_SET_ITEM(t, 0, PyLong_FromUnsignedLong(r.r));
-        PyTuple_SET_ITEM(t, 1, PyLong_FromUnsignedLong(r.s));
-        PyTuple_SET_ITEM(t, 2, PyFloat_FromDouble(r.lb));
-        PyTuple_SET_ITEM(t, 3, PyFloat_FromDouble(r.ub));
+        PyTuple_SET_ITEM(t, 0, int_of(r.r));
+        PyTuple_SET_ITEM(t, 1, int_of(r.s));
+        PyObject* lb = PyFloat_FromDouble(r.lb);
+        PyTuple_SET_ITEM(t, 2, lb);
+        if (std::memcmp(&r.lb, &r.ub, sizeof(double)) == 0) {
+            Py_INCREF(lb);
+            PyTuple_SET_ITEM(t, 3, lb);
+        } else {
+            PyTuple_SET_ITEM(t, 3, PyFloat_FromDouble(r.ub));
+        }
         PyObject* nm = it->second.ptr();
         Py_INCREF(nm);
         PyTuple_SET_ITEM(t, 4, nm);
-        PyTuple_SET_ITEM(t, 5, PyLong_FromUnsignedLong(r.rank));
+        PyTuple_SET_ITEM(t, 5, int_of(r.rank));
         PyList_SET_ITEM(records.ptr(), static_cast<Py_ssize_t>(i), t);
     }
     return py::make_tuple(records, out.stats.to_json());

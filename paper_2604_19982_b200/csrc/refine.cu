@@ -11,6 +11,11 @@ namespace tjx {
 
 namespace {
 
+// k_screen launch shape: 8 warps per block, 2 blocks per SM (16 warps, 128 registers; 4 x 5 was
+// slower: the 102-register bound spills the stage-2 code)
+constexpr int kScreenThreads = 256;
+constexpr int kScreenBlocks = 2;
+
 struct VpDescDev {
     uint32_t op;
     uint32_t gvr, gvs; // global voxel ids (join mode)
@@ -330,7 +335,7 @@ __device__ __forceinline__ int build_list(const float4* __restrict__ box, uint64
 // 32 x 32 shared-memory tiles, every pair tested on its facet-AABB gap; (4) box survivors
 // through the separating-axis stage (sat_needed). Pairs that may still change the op's
 // bounds go to the exact queue (refine_kernel.cuh has the exactness argument).
-__global__ void __launch_bounds__(256, 2) k_screen(RefineSource src, uint64_t vp_begin, uint64_t vp_end,
+__global__ void __launch_bounds__(kScreenThreads, kScreenBlocks) k_screen(RefineSource src, uint64_t vp_begin, uint64_t vp_end,
                                                 const unsigned long long* __restrict__ op_lb_bits,
                                                 const unsigned long long* __restrict__ op_ub_bits, int cull,
                                                 RefineQueue q, unsigned long long* work,
@@ -566,11 +571,11 @@ __global__ void mindist_batch_kernel(uint64_t n, const double* __restrict__ a6, 
         out[i] = mindist_box(a6 + 6 * i, b6 + 6 * i);
 }
 
-constexpr int kScreenThreads = 256;
 constexpr size_t kScreenSmem = sizeof(ScreenSmem) * (kScreenThreads / 32);
 
-inline int warp_grid(uint64_t warps, int num_sms, int per_sm) {
-    return (int)std::max<uint64_t>(1, std::min<uint64_t>((warps + 7) / 8, (uint64_t)num_sms * per_sm));
+inline int warp_grid(uint64_t warps, int num_sms, int per_sm, int warps_per_block = 8) {
+    return (int)std::max<uint64_t>(
+        1, std::min<uint64_t>((warps + warps_per_block - 1) / warps_per_block, (uint64_t)num_sms * per_sm));
 }
 
 } // namespace
@@ -616,7 +621,8 @@ void refine_pass(const RefineSource& src, uint64_t vp_begin, uint64_t vp_end, bo
         TJ_CUDA(cudaMemsetAsync(qs.count.p, 0, 8, st));
         TJ_CUDA(cudaMemsetAsync(work, 0, 8, st));
         count_launch();
-        k_screen<<<warp_grid(vp_end - vp_begin, num_sms, 2), kScreenThreads, kScreenSmem, st>>>(
+        k_screen<<<warp_grid(vp_end - vp_begin, num_sms, kScreenBlocks, kScreenThreads / 32), kScreenThreads,
+                   kScreenSmem, st>>>(
             src, vp_begin, vp_end, lb_bits, ub_bits, cull, qs.view(), work, counters);
         TJ_CUDA(cudaGetLastError());
     }

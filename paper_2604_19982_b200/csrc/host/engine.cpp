@@ -762,10 +762,9 @@ int slot_of(const PreparedDataset& d, uint32_t level) {
 // records of every level, the compact staging of its largest level and its share of the
 // per-level screening workspace (128-B records + 48-B voxel aggregates).
 uint64_t object_device_bytes(const PreparedObject& o) {
-    uint64_t all = 0, mx = 0;
-    for (const auto& lv : o.voxels.facets_per_level) {
-        uint64_t e = 0;
-        for (const auto& ids : lv) e += ids.size();
+    uint64_t all = 0, mx = 0; // the level meshes' facet counts (the voxel lists partition them)
+    for (const auto& lv : o.ladder.levels) {
+        const uint64_t e = lv.mesh.facets.size();
         all += e;
         mx = std::max(mx, e);
     }
@@ -778,7 +777,7 @@ uint64_t object_device_bytes(const PreparedObject& o) {
 // 90 % of the device's free memory. $TRIJOIN_R_CHUNK_OBJECTS forces a chunk size. One
 // chunk = the whole of R (the resident path).
 std::vector<std::pair<size_t, size_t>> plan_r_chunks(const PreparedDataset& R, const PreparedDataset& S,
-                                                     const JoinSpec&, int device, bool self_join) {
+                                                     const JoinSpec&, int device, bool self_join, ThreadPool& pool) {
     const size_t nr = R.objects.size();
     if (const char* e = std::getenv("TRIJOIN_R_CHUNK_OBJECTS"); e && *e) {
         const size_t step = std::max<size_t>(1, std::stoull(e));
@@ -799,10 +798,19 @@ std::vector<std::pair<size_t, size_t>> plan_r_chunks(const PreparedDataset& R, c
         budget = free_b / 10 * 9;
     }
     std::vector<uint64_t> cost(nr);
-    uint64_t r_total = 0, s_total = 0;
-    for (size_t o = 0; o < nr; ++o) r_total += cost[o] = object_device_bytes(R.objects[o]);
+    std::atomic<uint64_t> r_sum{0}, s_sum{0};
+    detail::for_blocks(pool, nr, [&](size_t b, size_t e) {
+        uint64_t acc = 0;
+        for (size_t o = b; o < e; ++o) acc += cost[o] = object_device_bytes(R.objects[o]);
+        r_sum += acc;
+    });
     if (!self_join)
-        for (const auto& o : S.objects) s_total += object_device_bytes(o);
+        detail::for_blocks(pool, S.objects.size(), [&](size_t b, size_t e) {
+            uint64_t acc = 0;
+            for (size_t o = b; o < e; ++o) acc += object_device_bytes(S.objects[o]);
+            s_sum += acc;
+        });
+    const uint64_t r_total = r_sum.load(), s_total = s_sum.load();
     const uint64_t fixed = (64ull << 20) + 256 * uint64_t{nr};
     if (r_total + s_total + fixed <= budget) return {{0, nr}};
     // chunked: S in full (for a self-join a second, complete copy) + two R chunks
@@ -953,7 +961,8 @@ JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const Jo
     std::function<size_t(uint32_t)> owner;
     const bool tracing = trace && (trace->on_interval || trace->on_vp_pruned);
     const std::vector<std::pair<size_t, size_t>> chunks =
-        tracing ? std::vector<std::pair<size_t, size_t>>{} : plan_r_chunks(R, S, spec, devices[0], self_join);
+        tracing ? std::vector<std::pair<size_t, size_t>>{} : plan_r_chunks(R, S, spec, devices[0], self_join, pool);
+    mark("planned");
     if (chunks.size() > 1) {
         run_chunked(R, S, spec, pool, devices, chunks, results, out, mark);
         for (size_t k = 0; k < chunks.size(); ++k)

@@ -11,6 +11,8 @@ namespace tjx {
 
 namespace {
 
+__device__ unsigned long long* g_dbg_op_tested = nullptr; // TRIJOIN_DEBUG_OPSTATS diagnostics
+
 // k_screen launch shape: 8 warps per block, 2 blocks per SM (16 warps, 128 registers; 4 x 5 was
 // slower: the 102-register bound spills the stage-2 code)
 constexpr int kScreenThreads = 256;
@@ -453,6 +455,7 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks) k_screen(Refine
                         const float rub = th.ub_u == 0.f ? ninf : __fsub_ru(__fadd_ru(th.ub_u, dl), ar.hd);
                         const int iters = (scnt - jj + P - 1) / P; // this lane's s facets
                         if (lane == 0) tested += (uint32_t)(rcnt * scnt);
+                        if (lane == 0 && g_dbg_op_tested) atomicAdd(g_dbg_op_tested + d.op, (unsigned long long)(rcnt * scnt));
                         const int max_iters = (scnt + P - 1) / P;
                         int nq = 0;
                         for (int t = 0;; ++t) {
@@ -587,6 +590,10 @@ void refine_prep(const double* facets, uint64_t n, float4* out, unsigned* agg, i
     count_launch();
     k_prep<<<grid, 256, 0, st>>>(facets, n, out, agg, zero_pad);
     TJ_CUDA(cudaGetLastError());
+}
+
+void refine_debug_op_tested(unsigned long long* p) {
+    TJ_CUDA(cudaMemcpyToSymbol(g_dbg_op_tested, &p, sizeof(p)));
 }
 
 void refine_seg_prep(const float4* box, const uint64_t* foff, uint64_t n_voxels, float4* seg, int num_sms,

@@ -15,6 +15,8 @@
 #include <cub/cub.cuh>
 
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 
 #include "filter.cuh"
 #include "trace_sink.h"
@@ -139,7 +141,8 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
     RefineLoopOut out;
     const uint64_t n = cs.n;
     DevBuf<unsigned long long> lbb(std::max<uint64_t>(n, 1)), ubb(std::max<uint64_t>(n, 1));
-    DevBuf<unsigned long long> counters(kNumCounters), work(1);
+    DevBuf<unsigned long long> counters(kNumCounters), work(1), dbg;
+    if (const char* e = std::getenv("TRIJOIN_DEBUG_OPSTATS"); e && *e && *e != '0') dbg.alloc(std::max<uint64_t>(n, 1));
     if (!ws.queue) ws.queue = std::make_unique<RefineQueueStore>();
     RefineQueueStore& queue = *ws.queue;
     DevBuf<uint8_t> updated;
@@ -200,6 +203,10 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
             // 0: every facet pair; 1: exact-preserving culling; 2: decision-mode culling
             const int cull = (spec.flags & TJ_FLAG_NO_CULL) ? 0 : decision ? 2 : 1;
             unsigned long long hc[kNumCounters];
+            if (dbg.n) {
+                TJ_CUDA(cudaMemsetAsync(dbg.p, 0, n * 8, st));
+                refine_debug_op_tested(dbg.p);
+            }
             for (;;) {
                 count_launch();
                 k_fill_u64<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(lbb.p, n, kInfBits);
@@ -230,6 +237,7 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
                 queue.items.alloc(ovf + ovf / 4);
             }
             out.chunks += (n_active + spec.refine_chunk - 1) / spec.refine_chunk;
+            if (dbg.n) refine_debug_op_tested(nullptr);
             count_launch();
             k_aggregate<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(cs.view(), n, lbb.p, ubb.p, knn ? 0 : 1, tau,
                                                                       (int16_t)level, cull == 2 ? 1 : 0, updated.p,
@@ -240,6 +248,24 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
             if (knn) {
                 knn_fixpoint(ws, cs, spec.k, (int16_t)level, err, st);
                 check_error(err, st);
+            }
+            if (dbg.n) { // tested pairs by the op's outcome at this level
+                std::vector<unsigned long long> t(n);
+                std::vector<uint8_t> sts(n);
+                std::vector<int16_t> at(n);
+                TJ_CUDA(cudaMemcpyAsync(t.data(), dbg.p, n * 8, cudaMemcpyDeviceToHost, st));
+                TJ_CUDA(cudaMemcpyAsync(sts.data(), cs.status.p, n, cudaMemcpyDeviceToHost, st));
+                TJ_CUDA(cudaMemcpyAsync(at.data(), cs.decided_at.p, n * 2, cudaMemcpyDeviceToHost, st));
+                stream_sync(st);
+                unsigned long long conf = 0, rem = 0, und = 0, nconf = 0, nrem = 0, nund = 0;
+                for (uint64_t op = 0; op < n; ++op) {
+                    if (!t[op]) continue;
+                    if (sts[op] == TJ_UNDECIDED) { und += t[op]; ++nund; }
+                    else if (at[op] == (int16_t)level && sts[op] == TJ_CONFIRMED) { conf += t[op]; ++nconf; }
+                    else if (at[op] == (int16_t)level) { rem += t[op]; ++nrem; }
+                }
+                std::fprintf(stderr, "[opstats] lod %u tested: confirmed-here %llu (%llu ops) removed-here %llu (%llu ops) undecided %llu (%llu ops)\n",
+                             level, conf, nconf, rem, nrem, und, nund);
             }
             float kms = 0.f;
             TJ_CUDA(cudaEventElapsedTime(&kms, e0, e1));

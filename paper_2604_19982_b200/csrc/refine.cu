@@ -11,7 +11,8 @@ namespace tjx {
 
 namespace {
 
-__device__ unsigned long long* g_dbg_op_tested = nullptr; // TRIJOIN_DEBUG_OPSTATS diagnostics
+// TRIJOIN_DEBUG_OPSTATS diagnostics (per-op counters only in a -DTJ_DEBUG_OPSTATS build)
+__device__ unsigned long long* g_dbg_op_tested = nullptr;
 
 // k_screen launch shape: 8 warps per block, 2 blocks per SM (16 warps, 128 registers; 4 x 5 was
 // slower: the 102-register bound spills the stage-2 code)
@@ -455,7 +456,9 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks) k_screen(Refine
                         const float rub = th.ub_u == 0.f ? ninf : __fsub_ru(__fadd_ru(th.ub_u, dl), ar.hd);
                         const int iters = (scnt - jj + P - 1) / P; // this lane's s facets
                         if (lane == 0) tested += (uint32_t)(rcnt * scnt);
+#ifdef TJ_DEBUG_OPSTATS
                         if (lane == 0 && g_dbg_op_tested) atomicAdd(g_dbg_op_tested + d.op, (unsigned long long)(rcnt * scnt));
+#endif
                         const int max_iters = (scnt + P - 1) / P;
                         int nq = 0;
                         for (int t = 0;; ++t) {

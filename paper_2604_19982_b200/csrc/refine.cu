@@ -306,7 +306,7 @@ __device__ __forceinline__ int sat_needed(const float* a, const float* b, const 
 // screen against the partner segment `o` (offsets relative to first); returns the count.
 __device__ __forceinline__ int build_list(const float4* __restrict__ box, uint64_t first, uint32_t n, const SegAgg& o,
                                           float delta0, const Thresh& th, bool cull, uint16_t* list,
-                                          uint32_t& dropped) {
+                                          uint32_t* dropped) {
     const int lane = threadIdx.x & 31;
     int cnt = 0;
     for (uint32_t i0 = 0; i0 < n; i0 += 32) {
@@ -321,10 +321,10 @@ __device__ __forceinline__ int build_list(const float4* __restrict__ box, uint64
                 if (a.w >= 0.f)
                     keep = !agg_skip(lo, hi, o.lo, o.hi, a.w + o.Lmax, fminf(a.w, o.Lmin), __fadd_ru(ph, o.phmax),
                                      __fadd_rd(b.w, o.hdmin), delta0, th);
-                if (!keep) ++dropped;
             }
         }
         const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (cull && o.ok && lane == 0) *dropped += (uint32_t)min(32u, n - i0) - __popc(bal);
         if (keep) list[cnt + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)i;
         cnt += __popc(bal);
     }
@@ -346,7 +346,8 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks) k_screen(Refine
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ScreenSmem& sm = reinterpret_cast<ScreenSmem*>(smem_raw)[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
-    uint32_t tested = 0, sat_tests = 0, verified = 0, vps_skipped = 0, dropped = 0; // per-lane (< 2^32)
+    if (lane < 5) sm.cnt[lane] = 0;
+    __syncwarp();
     // decision mode: when every facet pair has hd_i + hd_j > 1e-5 (L_i + L_j) + 1e-12 (M_i + M_j),
     // no ub_ij can be 0 at this level (B + hd_i + hd_j >= tiny + delta for every pair), so
     // the ub side of every op is settled (the level's aggregates, k_prep)
@@ -398,7 +399,7 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks) k_screen(Refine
             if (ar.ok && as.ok &&
                 agg_skip(ar.lo, ar.hi, as.lo, as.hi, ar.Lmax + as.Lmax, fminf(ar.Lmin, as.Lmin),
                          __fadd_ru(ar.phmax, as.phmax), __fadd_rd(ar.hdmin, as.hdmin), d0, th)) {
-                ++vps_skipped;
+                if (lane == 0) ++sm.cnt[3];
                 continue;
             }
             if (hier) {
@@ -413,10 +414,10 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks) k_screen(Refine
         }
         for (uint32_t rc0 = 0; rc0 < d.rn; rc0 += kCap) {
             const int nrl = build_list(src.r_box, d.r0 + rc0, min((uint32_t)kCap, d.rn - rc0), sm.seg_s, delta0, th, hier,
-                                       sm.rl, dropped);
+                                       sm.rl, &sm.cnt[4]);
             for (uint32_t sc0 = 0; nrl > 0 && sc0 < d.sn; sc0 += kCap) {
                 const int nsl = build_list(src.s_box, d.s0 + sc0, min((uint32_t)kCap, d.sn - sc0), sm.seg_r, delta0, th,
-                                           hier, sm.sl, dropped);
+                                           hier, sm.sl, &sm.cnt[4]);
                 for (int rt0 = 0; nsl > 0 && rt0 < nrl; rt0 += kRT) {
                     const int rcnt = min(kRT, nrl - rt0);
                     __syncwarp();
@@ -455,7 +456,7 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks) k_screen(Refine
                         const float rlb = lb_settled ? ninf : __fadd_ru(__fadd_ru(th.lb_u, dl), ar.ph);
                         const float rub = th.ub_u == 0.f ? ninf : __fsub_ru(__fadd_ru(th.ub_u, dl), ar.hd);
                         const int iters = (scnt - jj + P - 1) / P; // this lane's s facets
-                        if (lane == 0) tested += (uint32_t)(rcnt * scnt);
+                        if (lane == 0) sm.cnt[0] += (uint32_t)(rcnt * scnt);
 #ifdef TJ_DEBUG_OPSTATS
                         if (lane == 0 && g_dbg_op_tested) atomicAdd(g_dbg_op_tested + d.op, (unsigned long long)(rcnt * scnt));
 #endif
@@ -490,9 +491,9 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks) k_screen(Refine
                                     const int r = sat_needed(sm.rc + i * kCS, sm.sc + j * kCS, src.r_facets + (size_t)fr * 12,
                                                              src.s_facets + (size_t)fs * 12, th);
                                     need = r & 1;
-                                    verified += r >> 1;
-                                    ++sat_tests;
+                                    if (r >> 1) atomicAdd(&sm.cnt[2], 1u); // rare
                                 }
+                                if (lane == 0) sm.cnt[1] += (uint32_t)n;
                                 queue_push(q, need, d.op, fr, fs);
                                 __syncwarp();
                                 if (lane < nq - n) sm.q[lane] = sm.q[n + lane];
@@ -507,19 +508,13 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks) k_screen(Refine
         }
     }
     if (counters) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            tested += __shfl_xor_sync(0xffffffffu, tested, o);
-            sat_tests += __shfl_xor_sync(0xffffffffu, sat_tests, o);
-            verified += __shfl_xor_sync(0xffffffffu, verified, o);
-            dropped += __shfl_xor_sync(0xffffffffu, dropped, o);
-        }
+        __syncwarp();
         if (lane == 0) {
-            atomicAdd(counters + 0, (unsigned long long)tested);
-            atomicAdd(counters + 3, (unsigned long long)sat_tests);
-            atomicAdd(counters + 4, (unsigned long long)verified);
-            atomicAdd(counters + 5, (unsigned long long)vps_skipped);
-            atomicAdd(counters + 6, (unsigned long long)dropped);
+            atomicAdd(counters + 0, (unsigned long long)sm.cnt[0]);
+            atomicAdd(counters + 3, (unsigned long long)sm.cnt[1]);
+            atomicAdd(counters + 4, (unsigned long long)sm.cnt[2]);
+            atomicAdd(counters + 5, (unsigned long long)sm.cnt[3]);
+            atomicAdd(counters + 6, (unsigned long long)sm.cnt[4]);
         }
     }
 }

@@ -84,6 +84,9 @@ struct __align__(16) ScreenSmem {
     uint16_t rl[kCap]; // surviving r facets of the current raw chunk (offsets in the chunk)
     uint16_t sl[kCap]; // surviving s facets
     SegAgg seg_r, seg_s; // aggregates of the current voxel pair's segments
+    // the warp's counters (lane 0 writes; kept out of registers: the stage-1 loop is at the
+    // register limit): tested, separating-axis tests, verified, voxel pairs skipped, dropped
+    uint32_t cnt[5];
 };
 
 __device__ __forceinline__ float rd(double x) { return __double2float_rd(x); }

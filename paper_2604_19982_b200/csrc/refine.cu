@@ -462,23 +462,40 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks) k_screen(Refine
 #endif
                         const int max_iters = (scnt + P - 1) / P;
                         int nq = 0;
-                        for (int t = 0;; ++t) {
+                        // two s facets per lane and iteration: independent dependency chains
+                        for (int t = 0;; t += 2) {
                             if (t < max_iters) {
-                                const int bj = jj + t * P;
-                                bool need = false;
-                                if (row_on && t < iters)
-                                    need = !cull || stage1_need_rr(ar, sm.rc + bi * kCS, sm.sc + bj * kCS, rlb, rub);
+                                const int bj0 = jj + t * P;
+                                const bool v0 = row_on && t < iters, v1 = row_on && t + 1 < iters;
+                                const int bj1 = v1 ? bj0 + P : bj0;
+                                bool n0 = v0, n1 = v1;
+                                if (cull) {
+                                    const float* b0p = sm.sc + bj0 * kCS;
+                                    const float* b1p = sm.sc + bj1 * kCS;
+                                    const int s0 = stage1_box(ar, *reinterpret_cast<const float4*>(b0p),
+                                                              *reinterpret_cast<const float4*>(b0p + 4), b0p[11], rlb, rub);
+                                    const int s1 = stage1_box(ar, *reinterpret_cast<const float4*>(b1p),
+                                                              *reinterpret_cast<const float4*>(b1p + 4), b1p[11], rlb, rub);
+                                    const float* asr = sm.rc + bi * kCS;
+                                    n0 = v0 && (s0 == 1 || (s0 == 2 && stage1_ill(ar, asr, b0p)));
+                                    n1 = v1 && (s1 == 1 || (s1 == 2 && stage1_ill(ar, asr, b1p)));
+                                }
                                 if (!cull) {
-                                    queue_push(q, need, d.op, (uint32_t)(d.r0 + rc0 + sm.rl[rt0 + bi]),
-                                               (uint32_t)(d.s0 + sc0 + sm.sl[st0 + bj]));
+                                    queue_push(q, n0, d.op, (uint32_t)(d.r0 + rc0 + sm.rl[rt0 + bi]),
+                                               (uint32_t)(d.s0 + sc0 + sm.sl[st0 + bj0]));
+                                    queue_push(q, n1, d.op, (uint32_t)(d.r0 + rc0 + sm.rl[rt0 + bi]),
+                                               (uint32_t)(d.s0 + sc0 + sm.sl[st0 + bj1]));
                                 } else {
-                                    const unsigned bal = __ballot_sync(0xffffffffu, need);
-                                    if (need) sm.q[nq + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)((bi << 5) | bj);
-                                    nq += __popc(bal);
+                                    const unsigned bal0 = __ballot_sync(0xffffffffu, n0);
+                                    if (n0) sm.q[nq + __popc(bal0 & ((1u << lane) - 1u))] = (uint16_t)((bi << 5) | bj0);
+                                    nq += __popc(bal0);
+                                    const unsigned bal1 = __ballot_sync(0xffffffffu, n1);
+                                    if (n1) sm.q[nq + __popc(bal1 & ((1u << lane) - 1u))] = (uint16_t)((bi << 5) | bj1);
+                                    nq += __popc(bal1);
                                 }
                             }
-                            const bool last = t + 1 >= max_iters;
-                            if (nq >= 32 || (last && nq > 0)) { // second stage on up to 32 queued pairs
+                            const bool last = t + 2 >= max_iters;
+                            while (nq >= 32 || (last && nq > 0)) { // second stage on up to 32 queued pairs
                                 const int n = min(nq, 32);
                                 __syncwarp();
                                 bool need = false;
@@ -496,8 +513,13 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks) k_screen(Refine
                                 if (lane == 0) sm.cnt[1] += (uint32_t)n;
                                 queue_push(q, need, d.op, fr, fs);
                                 __syncwarp();
-                                if (lane < nq - n) sm.q[lane] = sm.q[n + lane];
-                                __syncwarp();
+                                for (int k0 = 0; k0 < nq - n; k0 += 32) { // shift the rest down (in order)
+                                    const bool mv = k0 + lane < nq - n;
+                                    const uint16_t v = mv ? sm.q[n + k0 + lane] : 0;
+                                    __syncwarp();
+                                    if (mv) sm.q[k0 + lane] = v;
+                                    __syncwarp();
+                                }
                                 nq -= n;
                             }
                             if (last && nq == 0) break;

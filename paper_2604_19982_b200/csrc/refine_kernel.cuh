@@ -52,7 +52,7 @@ constexpr int kCS = 36;    // shared-memory stride of a screening record (32 flo
 constexpr int kRecF4 = kScreenRecF4; // float4 per screening record (floats 0-31)
 constexpr int kBoxF4 = 3;  // box part of a record (floats 0-11), its own array: 3 float4 per facet
 constexpr int kGeoF4 = 5;  // geometry part (floats 12-31): 5 float4 per facet
-constexpr int kQueue = 64; // per-warp SAT queue (< 32 pending + 32 new)
+constexpr int kQueue = 96; // per-warp SAT queue (< 32 pending + 2 x 32 new)
 constexpr int kCap = 128;  // per-warp survivor lists: facets per raw segment chunk
 constexpr uint32_t kHierMinPairs = 1024; // voxel pairs with fewer facet pairs skip the hierarchical screens
 
@@ -366,6 +366,43 @@ __device__ __forceinline__ bool well_cond_q(const int* aq, int4 bq) {
     return (unsigned)(d0 + (int)kT) > 2 * kT && (unsigned)(d1 + (int)kT) > 2 * kT &&
            (unsigned)(d2 + (int)kT) > 2 * kT && (unsigned)(d3 + (int)kT) > 2 * kT &&
            (unsigned)(d4 + (int)kT) > 2 * kT && (unsigned)(d5 + (int)kT) > 2 * kT;
+}
+
+// Box part of stage 1 for one pair, branch-free: 1 = the pair must go to stage 2 (it may
+// change a minimum, or it is out of the skip argument's shape / range), 2 = skippable by its
+// box gap but near (the edge / plane conditioning decides), 0 = skippable (far apart).
+__device__ __forceinline__ int stage1_box(const RowRec& a, float4 b0, float4 b1, float bph, float rlb, float rub) {
+    const float gx = fmaxf(0.f, fmaxf(__fsub_rd(b0.x, a.hi[0]), __fsub_rd(a.lo[0], b1.x)));
+    const float gy = fmaxf(0.f, fmaxf(__fsub_rd(b0.y, a.hi[1]), __fsub_rd(a.lo[1], b1.y)));
+    const float gz = fmaxf(0.f, fmaxf(__fsub_rd(b0.z, a.hi[2]), __fsub_rd(a.lo[2], b1.z)));
+    const float g2 = __fadd_rd(__fadd_rd(__fmul_rd(gx, gx), __fmul_rd(gy, gy)), __fmul_rd(gz, gz));
+    constexpr float kInvC = 1.0f / (1.0f - 1e-5f) * (1.0f + 0x1p-20f);
+    const float xl = __fadd_ru(rlb, bph);
+    const float yu = __fsub_ru(rub, b1.w);
+    const float xs = __fmul_ru(xl, kInvC), ys = __fmul_ru(yu, kInvC);
+    const bool lb_ok = xl <= 0.f || g2 >= __fmul_ru(xs, xs);
+    const bool ub_ok = yu <= 0.f || g2 >= __fmul_ru(ys, ys);
+    const float m = 1e3f * fminf(a.L, b0.w), f = 2.f * (a.L + b0.w);
+    const bool shapes = a.L >= 0.f && b0.w >= 0.f && g2 <= m * m;
+    const bool skip = lb_ok && ub_ok && shapes;
+    return skip ? (g2 > f * f ? 0 : 2) : 1;
+}
+
+// Conditioning decision of a near, box-skippable pair (the rest of skip_mask): true iff some
+// edge / plane combination is ill conditioned (the pair must go to stage 2).
+__device__ __forceinline__ bool stage1_ill(const RowRec& a, const float* as, const float* b) {
+    if (well_cond_q(a.q, *reinterpret_cast<const int4*>(b + 28))) return false;
+    const float4 b2 = *reinterpret_cast<const float4*>(b + 8);
+    const float4 b3 = *reinterpret_cast<const float4*>(b + 12), b4 = *reinterpret_cast<const float4*>(b + 16);
+    const float b20 = b[20];
+    const float4 a2 = *reinterpret_cast<const float4*>(as + 8), a3 = *reinterpret_cast<const float4*>(as + 12);
+    const float4 a4 = *reinterpret_cast<const float4*>(as + 16);
+    const float a20 = as[20];
+    bool ill = ill_cond(a3.x, a3.y, a3.z, b2.x, b2.y, b2.z) || ill_cond(a3.w, a4.x, a4.y, b2.x, b2.y, b2.z) ||
+               ill_cond(a4.z, a4.w, a20, b2.x, b2.y, b2.z);
+    ill = ill || ill_cond(b3.x, b3.y, b3.z, a2.x, a2.y, a2.z) || ill_cond(b3.w, b4.x, b4.y, a2.x, a2.y, a2.z) ||
+          ill_cond(b4.z, b4.w, b20, a2.x, a2.y, a2.z);
+    return ill;
 }
 
 // Stage-1 test of the screen pass with the r record in registers (a; its shared-memory

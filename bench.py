@@ -78,6 +78,8 @@ class Clocks:
 
     def __init__(self, path, gpu):
         self.path, self.proc = path, None
+        if os.environ.get("BENCH_NO_CLOCKS"):
+            return
         try:
             self.f = open(path, "w")
             self.proc = subprocess.Popen(
@@ -208,11 +210,13 @@ def main():
         return 0
 
     dev = torch.device("cuda", local)
+    # the clocks sampler starts before the warm-up (its first NVML queries must not land in
+    # the timed region); it keeps sampling through the timed steps
+    clocks = Clocks(os.path.join(ROOT, "gpurun_out", f"clocks_rank{rank}.csv") if os.path.isdir(
+        os.path.join(ROOT, "gpurun_out")) else f"/tmp/trijoin_clocks_{rank}.csv", local)
     for _ in range(a.warmup):
         res.run(**run_kw)
     launches0 = _core.kernel_launches()
-    clocks = Clocks(os.path.join(ROOT, "gpurun_out", f"clocks_rank{rank}.csv") if os.path.isdir(
-        os.path.join(ROOT, "gpurun_out")) else f"/tmp/trijoin_clocks_{rank}.csv", local)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)

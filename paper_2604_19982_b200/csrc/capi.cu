@@ -248,6 +248,16 @@ double level_ready(const DatasetDev& d, int slot, cudaStream_t st) {
 }
 
 void stream_sync(cudaStream_t st) {
+    // Spin by default: blocking-sync waits (TRIJOIN_BLOCKING_SYNC=1) free the core but were
+    // measured to wake up hundreds of milliseconds late now and then on the B200 hosts.
+    static const bool blocking = [] {
+        const char* e = std::getenv("TRIJOIN_BLOCKING_SYNC");
+        return e && *e && *e != '0';
+    }();
+    if (!blocking) {
+        TJ_CUDA(cudaStreamSynchronize(st));
+        return;
+    }
     struct Events {
         cudaEvent_t ev[64] = {};
         ~Events() {
@@ -365,6 +375,7 @@ int tj_dataset_upload(tj_ctx* ctx, const tj_dataset_view* v, tj_dataset** out) {
             d.level_entries.push_back(entries);
             d.bytes += (d.n_voxels + 1) * 8 + entries * TJ_FACET_STRIDE * 8;
         }
+        for (uint32_t li = 0; li < v->n_levels; ++li) derive_level(d, li, ctx->ws.num_sms, st);
         stream_sync(st);
     });
     if (rc == TJ_OK) *out = ds.release();
@@ -428,6 +439,14 @@ int tj_dataset_begin(tj_ctx* ctx, const tj_dataset_view* v, const uint64_t* cons
         for (uint32_t li = 0; li < v->n_levels; ++li)
             stage_bytes = std::max(stage_bytes, stage_layout(d.level_vertices[li], d.level_facets[li], d.level_entries[li]).total);
         d.stage.alloc(stage_bytes);
+        // derived screening data, reserved here (a put never allocates while a join runs)
+        d.screen.resize(v->n_levels);
+        d.seg.resize(v->n_levels);
+        for (uint32_t li = 0; li < v->n_levels; ++li) {
+            d.screen[li].alloc(std::max<uint64_t>(d.level_entries[li] * kScreenRecF4, 1));
+            d.seg[li].alloc(std::max<uint64_t>(3 * d.n_voxels, 1));
+        }
+        d.agg.alloc(3 * v->n_levels);
         d.vox_obj.alloc(std::max<uint64_t>(d.n_voxels, 1));
         if (no) {
             count_launch();
@@ -490,6 +509,7 @@ int tj_dataset_put_level(tj_dataset* ds, uint32_t slot, const tj_level_mesh_view
                                                       d.n_voxels, d.facets[slot].p, d.stream_err.p);
             TJ_CUDA(cudaGetLastError());
         }
+        derive_level(d, slot, ctx->ws.num_sms, g.copy);
         TJ_CUDA(cudaEventRecord(g.ev[slot], g.copy));
     });
     set_state(rc == TJ_OK ? LevelGate::kQueued : LevelGate::kFailed);

@@ -61,6 +61,8 @@ struct Workspace {
     DevBuf<float4> screen_r, screen_s;       // per-level FP32 screening records, grow-only
     DevBuf<unsigned> level_agg;              // per-level record aggregates (RefineSource::agg)
     DevBuf<float4> seg_r, seg_s;             // per-level voxel segment aggregates, grow-only
+    DevBuf<ActiveVpDev> active_alt;          // compaction scratch of the active list, grow-only
+    DevBuf<int64_t> nsel;
     void release() {
         temp.release();
         u64a.release();
@@ -70,6 +72,8 @@ struct Workspace {
         level_agg.release();
         seg_r.release();
         seg_s.release();
+        active_alt.release();
+        nsel.release();
     }
 };
 

@@ -616,6 +616,24 @@ void refine_debug_op_tested(unsigned long long* p) {
     TJ_CUDA(cudaMemcpyToSymbol(g_dbg_op_tested, &p, sizeof(p)));
 }
 
+__global__ void k_init_level_agg(unsigned* agg) {
+    if (threadIdx.x < 3) agg[threadIdx.x] = threadIdx.x == 0 ? 0x7f800000u : 0u;
+}
+
+void derive_level(DatasetDev& d, uint32_t li, int num_sms, cudaStream_t st) {
+    const uint64_t n = d.level_entries[li];
+    if (d.screen.size() <= li) d.screen.resize(li + 1);
+    if (d.seg.size() <= li) d.seg.resize(li + 1);
+    if (d.screen[li].n < std::max<uint64_t>(n * kScreenRecF4, 1)) d.screen[li].alloc(std::max<uint64_t>(n * kScreenRecF4, 1));
+    if (d.seg[li].n < std::max<uint64_t>(3 * d.n_voxels, 1)) d.seg[li].alloc(std::max<uint64_t>(3 * d.n_voxels, 1));
+    if (d.agg.n < 3 * d.levels.size()) d.agg.alloc(3 * d.levels.size());
+    count_launch();
+    k_init_level_agg<<<1, 32, 0, st>>>(d.agg.p + 3 * li);
+    refine_prep(d.facets[li].p, n, d.screen[li].p, d.agg.p + 3 * li, num_sms, st);
+    refine_seg_prep(d.screen[li].p, d.facet_offsets[li].p, d.n_voxels, d.seg[li].p, num_sms, st);
+    d.bytes += n * kScreenRecF4 * 16 + 3 * d.n_voxels * 16;
+}
+
 void refine_seg_prep(const float4* box, const uint64_t* foff, uint64_t n_voxels, float4* seg, int num_sms,
                      cudaStream_t st) {
     if (!n_voxels) return;

@@ -32,8 +32,9 @@ __global__ void k_fill_u64(unsigned long long* p, uint64_t n, unsigned long long
         p[i] = v;
 }
 
-__global__ void k_init_agg(unsigned* agg) {
-    if (threadIdx.x < 8) agg[threadIdx.x] = (threadIdx.x == 0 || threadIdx.x == 3) ? 0x7f800000u : 0u;
+__global__ void k_copy_agg(const unsigned* __restrict__ r, const unsigned* __restrict__ s, unsigned* agg) {
+    if (threadIdx.x < 3) agg[threadIdx.x] = r[threadIdx.x];
+    else if (threadIdx.x < 6) agg[threadIdx.x] = s[threadIdx.x - 3];
 }
 
 __global__ void k_facet_pairs(const ActiveVpDev* __restrict__ act, uint64_t n, const uint64_t* __restrict__ rf,
@@ -120,17 +121,20 @@ void check_error(DevError* err, cudaStream_t st) {
 uint64_t compact_active(Workspace& ws, const CandDevStore& cs, DevBuf<ActiveVpDev>& active, uint64_t n,
                         cudaStream_t st) {
     if (n == 0) return 0;
-    DevBuf<ActiveVpDev> out(n);
-    DevBuf<int64_t> nsel(1);
+    // scratch from the workspace (grow-only: no allocation between the levels of a join,
+    // where a pool growth stalled the host for tens of milliseconds), result copied back
+    ws.active_alt.reserve(n);
+    ws.nsel.reserve(1);
     StillUndecided pred{cs.status.p};
     size_t bytes = 0;
-    TJ_CUDA(cub::DeviceSelect::If(nullptr, bytes, active.p, out.p, nsel.p, (int64_t)n, pred, st));
+    TJ_CUDA(cub::DeviceSelect::If(nullptr, bytes, active.p, ws.active_alt.p, ws.nsel.p, (int64_t)n, pred, st));
     ws.temp.reserve(bytes);
-    TJ_CUDA(cub::DeviceSelect::If(ws.temp.p, bytes, active.p, out.p, nsel.p, (int64_t)n, pred, st));
+    TJ_CUDA(cub::DeviceSelect::If(ws.temp.p, bytes, active.p, ws.active_alt.p, ws.nsel.p, (int64_t)n, pred, st));
     int64_t h = 0;
-    TJ_CUDA(cudaMemcpyAsync(&h, nsel.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    TJ_CUDA(cudaMemcpyAsync(&h, ws.nsel.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     stream_sync(st);
-    active = std::move(out);
+    if (h > 0)
+        TJ_CUDA(cudaMemcpyAsync(active.p, ws.active_alt.p, (size_t)h * sizeof(ActiveVpDev), cudaMemcpyDeviceToDevice, st));
     return (uint64_t)h;
 }
 
@@ -142,6 +146,8 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
     const uint64_t n = cs.n;
     DevBuf<unsigned long long> lbb(std::max<uint64_t>(n, 1)), ubb(std::max<uint64_t>(n, 1));
     DevBuf<unsigned long long> counters(kNumCounters), work(1), dbg;
+    Clock::time_point tdbg[4];
+    static const bool dbg_timing = std::getenv("TRIJOIN_DEBUG_TIMING") != nullptr;
     if (const char* e = std::getenv("TRIJOIN_DEBUG_OPSTATS"); e && *e && *e != '0') dbg.alloc(std::max<uint64_t>(n, 1));
     if (!ws.queue) ws.queue = std::make_unique<RefineQueueStore>();
     RefineQueueStore& queue = *ws.queue;
@@ -172,33 +178,19 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
             src.cand_ub = cs.ub.p;
             src.r_facets = R.facets[sr].p;
             src.s_facets = S.facets[ss].p;
-            {   // FP32 screening records of this level's facets, once per facet, + their aggregates
+            {   // FP32 screening records, voxel segment aggregates and level aggregates of this
+                // level (derived once per dataset at upload: DatasetDev::screen / seg / agg)
                 const uint64_t nr = R.level_entries[sr], ns = S.level_entries[ss];
                 ws.level_agg.reserve(8);
                 count_launch();
-                k_init_agg<<<1, 32, 0, st>>>(ws.level_agg.p);
+                k_copy_agg<<<1, 32, 0, st>>>(R.agg.p + 3 * sr, S.agg.p + 3 * ss, ws.level_agg.p);
                 src.agg = ws.level_agg.p;
-                ws.screen_r.reserve(std::max<uint64_t>(nr * kScreenRecF4, 1));
-                refine_prep(R.facets[sr].p, nr, ws.screen_r.p, ws.level_agg.p, ws.num_sms, st);
-                src.r_box = ws.screen_r.p;
-                src.r_geo = ws.screen_r.p + 3 * nr;
-                ws.seg_r.reserve(std::max<uint64_t>(3 * R.n_voxels, 1));
-                refine_seg_prep(src.r_box, R.facet_offsets[sr].p, R.n_voxels, ws.seg_r.p, ws.num_sms, st);
-                src.r_seg = ws.seg_r.p;
-                if (S.facets[ss].p == R.facets[sr].p) {
-                    src.s_box = src.r_box;
-                    src.s_geo = src.r_geo;
-                    src.s_seg = src.r_seg;
-                    TJ_CUDA(cudaMemcpyAsync(ws.level_agg.p + 3, ws.level_agg.p, 12, cudaMemcpyDeviceToDevice, st));
-                } else {
-                    ws.screen_s.reserve(std::max<uint64_t>(ns * kScreenRecF4, 1));
-                    refine_prep(S.facets[ss].p, ns, ws.screen_s.p, ws.level_agg.p + 3, ws.num_sms, st);
-                    src.s_box = ws.screen_s.p;
-                    src.s_geo = ws.screen_s.p + 3 * ns;
-                    ws.seg_s.reserve(std::max<uint64_t>(3 * S.n_voxels, 1));
-                    refine_seg_prep(src.s_box, S.facet_offsets[ss].p, S.n_voxels, ws.seg_s.p, ws.num_sms, st);
-                    src.s_seg = ws.seg_s.p;
-                }
+                src.r_box = R.screen[sr].p;
+                src.r_geo = R.screen[sr].p + 3 * nr;
+                src.r_seg = R.seg[sr].p;
+                src.s_box = S.screen[ss].p;
+                src.s_geo = S.screen[ss].p + 3 * ns;
+                src.s_seg = S.seg[ss].p;
             }
             // 0: every facet pair; 1: exact-preserving culling; 2: decision-mode culling
             const int cull = (spec.flags & TJ_FLAG_NO_CULL) ? 0 : decision ? 2 : 1;
@@ -230,7 +222,9 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
                 unsigned long long ovf = 0;
                 TJ_CUDA(cudaMemcpyAsync(hc, counters.p, sizeof(hc), cudaMemcpyDeviceToHost, st));
                 TJ_CUDA(cudaMemcpyAsync(&ovf, queue.count.p + 1, 8, cudaMemcpyDeviceToHost, st));
+                tdbg[0] = Clock::now();
                 stream_sync(st);
+                tdbg[1] = Clock::now();
                 if (ovf == 0) break;
                 // an exact-evaluation queue overflowed somewhere in the level: grow it and
                 // redo the level (the screen is deterministic given the same evaluations)
@@ -244,6 +238,7 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
                                                                       err);
             TJ_CUDA(cudaGetLastError());
             check_error(err, st);
+            tdbg[2] = Clock::now();
             if (trace && trace->on_interval) trace->emit_updated(cs, updated, (int16_t)level, st);
             if (knn) {
                 knn_fixpoint(ws, cs, spec.k, (int16_t)level, err, st);
@@ -277,7 +272,17 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
             ls.vps_skipped = hc[5];
             ls.facets_dropped = hc[6];
             ls.kernel_ms = kms;
+            tdbg[3] = Clock::now();
             n_active = compact_active(ws, cs, active, n_active, st);
+            if (dbg_timing) {
+                const auto ms = [](Clock::time_point a, Clock::time_point b) {
+                    return std::chrono::duration<double, std::milli>(b - a).count();
+                };
+                std::fprintf(stderr, "[timing] lod %u: to-sync %.1f sync %.1f agg %.1f mid %.1f compact %.1f\n", level,
+                             ms(t0, tdbg[0]), ms(tdbg[0], tdbg[1]), ms(tdbg[1], tdbg[2]), ms(tdbg[2], tdbg[3]),
+                             ms(tdbg[3], Clock::now()));
+            }
+
             ls.ms = std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
             out.levels.push_back(ls);
         }

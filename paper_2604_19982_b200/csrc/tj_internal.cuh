@@ -41,8 +41,8 @@ inline cudaStream_t& alloc_stream() {
     return s;
 }
 
-// Blocking wait for the work queued on `st` so far: the calling thread sleeps (blocking-sync
-// event) instead of spinning, leaving its core to the host packing threads of run_join.
+// Wait for the work queued on `st` so far (spinning; TRIJOIN_BLOCKING_SYNC=1: a blocking-sync
+// event, the calling thread sleeps).
 void stream_sync(cudaStream_t st);
 
 // Minimal owning device buffer.
@@ -102,6 +102,11 @@ struct DatasetDev {
     std::vector<DevBuf<double>> facets;          // per level [entries*12]
     uint64_t bytes = 0;
     std::vector<uint64_t> level_entries;         // per level: facet records (CSR entries)
+    // derived per level at upload (refine.cu k_prep / k_seg_prep, on the upload stream): FP32
+    // screening records (kScreenRecF4 float4 per facet: box parts, then geometry parts), voxel
+    // segment aggregates (3 float4 per voxel) and the level aggregates (3 uints per level)
+    std::vector<DevBuf<float4>> screen, seg;
+    DevBuf<unsigned> agg;
     // streamed datasets only (tj_dataset_begin): per-level object bases, voxel -> object,
     // validation flag of the device-side expansion, arrival gate
     std::vector<DevBuf<uint64_t>> vert_base, facet_base; // per level [n_obj+1]
@@ -111,6 +116,9 @@ struct DatasetDev {
     DevBuf<unsigned char> stage;                         // compact-level staging area (largest level)
     std::shared_ptr<LevelGate> gate;
 };
+
+// Derived screening data of level slot li of d (facets already resident), on stream st.
+void derive_level(DatasetDev& d, uint32_t li, int num_sms, cudaStream_t st);
 
 // Makes `st` wait until level slot `slot` of `d` is resident (no-op for uploaded datasets);
 // returns the host milliseconds spent blocked waiting for the level to be queued.

@@ -196,7 +196,7 @@ uint64_t tj_dataset_device_bytes(const tj_dataset* ds);
 typedef struct tj_level_mesh_view {
     const double* vertices;       /* [vert_base[n_objects]*3] all objects, concatenated */
     const uint32_t* tris;         /* [facet_base[n_objects]*3] object-local vertex ids */
-    const double* hd;             /* [facet_base[n_objects]] */
+    const double* hd;             /* [facet_base[n_objects]]; hd and ph both NULL: all 0 */
     const double* ph;             /* [facet_base[n_objects]] */
     const uint32_t* voxel_facets; /* [facet_offsets[li][n_voxels]] object-local facet ids, voxel order */
 } tj_level_mesh_view;

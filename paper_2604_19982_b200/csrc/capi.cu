@@ -209,8 +209,8 @@ __global__ void k_expand_level(const double* __restrict__ verts, const uint32_t*
                 r[3 * k + 1] = ok ? __ldg(p + 1) : 0.0;
                 r[3 * k + 2] = ok ? __ldg(p + 2) : 0.0;
             }
-            r[9] = nf ? __ldg(hd + f) : 0.0;
-            r[10] = nf ? __ldg(ph + f) : 0.0;
+            r[9] = nf && hd ? __ldg(hd + f) : 0.0; // hd / ph NULL: the level's paddings are all 0
+            r[10] = nf && ph ? __ldg(ph + f) : 0.0;
             r[11] = 0.0;
             double2* d = reinterpret_cast<double2*>(out + e * TJ_FACET_STRIDE);
 #pragma unroll
@@ -482,7 +482,7 @@ int tj_dataset_put_level(tj_dataset* ds, uint32_t slot, const tj_level_mesh_view
         AllocStreamScope scope(g.copy);
         DatasetDev& d = ds->d;
         const uint64_t nvert = d.level_vertices[slot], nfac = d.level_facets[slot], used = d.level_entries[slot];
-        if ((nvert && !lv->vertices) || (nfac && (!lv->tris || !lv->hd || !lv->ph)) || (used && !lv->voxel_facets))
+        if ((nvert && !lv->vertices) || (nfac && (!lv->tris || !lv->hd != !lv->ph)) || (used && !lv->voxel_facets))
             throw Error(TJ_EINVAL, "tj_dataset_put_level: null level arrays");
         // compact arrays into the dataset's staging area (reserved at tj_dataset_begin: no
         // allocation here, so a put never waits on the memory pool while a join runs); the
@@ -497,8 +497,12 @@ int tj_dataset_put_level(tj_dataset* ds, uint32_t slot, const tj_level_mesh_view
         if (nvert) TJ_CUDA(cudaMemcpyAsync(verts, lv->vertices, nvert * 24, cudaMemcpyHostToDevice, g.copy));
         if (nfac) {
             TJ_CUDA(cudaMemcpyAsync(tris, lv->tris, nfac * 12, cudaMemcpyHostToDevice, g.copy));
-            TJ_CUDA(cudaMemcpyAsync(hd, lv->hd, nfac * 8, cudaMemcpyHostToDevice, g.copy));
-            TJ_CUDA(cudaMemcpyAsync(ph, lv->ph, nfac * 8, cudaMemcpyHostToDevice, g.copy));
+            if (lv->hd) {
+                TJ_CUDA(cudaMemcpyAsync(hd, lv->hd, nfac * 8, cudaMemcpyHostToDevice, g.copy));
+                TJ_CUDA(cudaMemcpyAsync(ph, lv->ph, nfac * 8, cudaMemcpyHostToDevice, g.copy));
+            } else {
+                hd = ph = nullptr;
+            }
         }
         if (used) TJ_CUDA(cudaMemcpyAsync(vf, lv->voxel_facets, used * 4, cudaMemcpyHostToDevice, g.copy));
         if (d.n_voxels) {

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -413,6 +414,21 @@ std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& dsf, size_t first
     double* hd = p->hd.data();
     double* ph = p->ph.data();
     uint32_t* vf = as<uint32_t>(p->vf);
+    // a level whose paddings are all 0 (the reference's level 100) ships no hd / ph at all
+    std::atomic<bool> nonzero{false};
+    for_blocks(pool, no, [&](size_t b, size_t e) {
+        for (size_t o = b; o < e && !nonzero.load(std::memory_order_relaxed); ++o) {
+            const LodMesh& lod = ds.objects[o].ladder.levels[li];
+            const size_t n_f = lod.mesh.facets.size();
+            for (size_t f = 0; f < n_f; ++f)
+                if (lod.hd[f] != 0.0 || lod.ph[f] != 0.0 || std::signbit(lod.hd[f]) || std::signbit(lod.ph[f])) {
+                    nonzero = true;
+                    break;
+                }
+        }
+    });
+    const bool pads = nonzero.load();
+    p->zero_pads = !pads;
     static_assert(sizeof(Point3) == 3 * sizeof(double), "Point3 must be three packed doubles");
     static_assert(sizeof(std::array<uint32_t, 3>) == 3 * sizeof(uint32_t), "facets must be packed uint32 triples");
     for_blocks(pool, no, [&](size_t b, size_t e) {
@@ -424,8 +440,10 @@ std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& dsf, size_t first
             if (n_v) std::memcpy(verts + 3 * vb, lod.mesh.vertices.data(), n_v * sizeof(Point3));
             if (n_f) {
                 std::memcpy(tris + 3 * fb, lod.mesh.facets.data(), n_f * 3 * sizeof(uint32_t));
-                std::memcpy(hd + fb, lod.hd.data(), n_f * sizeof(double));
-                std::memcpy(ph + fb, lod.ph.data(), n_f * sizeof(double));
+                if (pads) {
+                    std::memcpy(hd + fb, lod.hd.data(), n_f * sizeof(double));
+                    std::memcpy(ph + fb, lod.ph.data(), n_f * sizeof(double));
+                }
             }
             const VoxelSet& vs = obj.voxels;
             const uint64_t v0 = h.voxel_offsets[o];
@@ -439,8 +457,8 @@ std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& dsf, size_t first
     tj_level_mesh_view& v = p->view;
     v.vertices = verts;
     v.tris = tris;
-    v.hd = hd;
-    v.ph = ph;
+    v.hd = pads ? hd : nullptr;
+    v.ph = pads ? ph : nullptr;
     v.voxel_facets = vf;
     return p;
 }
@@ -772,6 +790,24 @@ uint64_t object_device_bytes(const PreparedObject& o) {
     return 256 + 112 * nv + 96 * all + (44 + 176) * mx;
 }
 
+// Device-memory budget: $TRIJOIN_DEVICE_BUDGET_MB, else 90 % of the device's free memory
+// (0 = unknown).
+uint64_t device_budget(int device) {
+    if (const char* e = std::getenv("TRIJOIN_DEVICE_BUDGET_MB"); e && *e) return std::stoull(e) << 20;
+    // queried once per device and process (cudaMemGetInfo costs up to tens of milliseconds
+    // right after a join); this library's memory is pooled and returned between joins
+    static std::mutex mu;
+    static std::map<int, uint64_t> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    if (auto it = cache.find(device); it != cache.end()) return it->second;
+    size_t free_b = 0, total_b = 0;
+    if (cudaSetDevice(device) != cudaSuccess || cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return cache[device] = free_b / 10 * 9;
+}
+
 // R split into consecutive object chunks so that S (resident for the whole join) and two R
 // chunks (one joining, the next uploading) fit the budget: $TRIJOIN_DEVICE_BUDGET_MB, else
 // 90 % of the device's free memory. $TRIJOIN_R_CHUNK_OBJECTS forces a chunk size. One
@@ -786,17 +822,8 @@ std::vector<std::pair<size_t, size_t>> plan_r_chunks(const PreparedDataset& R, c
         if (plan.empty()) plan.emplace_back(0, 0);
         return plan;
     }
-    uint64_t budget = 0;
-    if (const char* e = std::getenv("TRIJOIN_DEVICE_BUDGET_MB"); e && *e) {
-        budget = std::stoull(e) << 20;
-    } else {
-        size_t free_b = 0, total_b = 0;
-        if (cudaSetDevice(device) != cudaSuccess || cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
-            cudaGetLastError();
-            return {{0, nr}};
-        }
-        budget = free_b / 10 * 9;
-    }
+    const uint64_t budget = device_budget(device);
+    if (budget == 0) return {{0, nr}};
     std::vector<uint64_t> cost(nr);
     std::atomic<uint64_t> r_sum{0}, s_sum{0};
     detail::for_blocks(pool, nr, [&](size_t b, size_t e) {
@@ -857,7 +884,8 @@ void run_chunked(const PreparedDataset& R, const PreparedDataset& S, const JoinS
         const int slot = slot_of(S, level);
         if (slot < 0) continue;
         s_levels.push_back(detail::pack_level(S, *hs, static_cast<size_t>(slot), pool));
-        out.stats.h2d_bytes += G * (hs->n_vertices[slot] * 24 + hs->n_facets[slot] * 28 + hs->facet_offsets[slot].back() * 4);
+        out.stats.h2d_bytes += G * (hs->n_vertices[slot] * 24 + hs->n_facets[slot] * (s_levels.back()->zero_pads ? 12 : 28) +
+                                    hs->facet_offsets[slot].back() * 4);
         for (size_t g = 0; g < G; ++g)
             detail::check(tj_dataset_put_level(dsh[g].p, static_cast<uint32_t>(slot), &s_levels.back()->view),
                           detail::device_context(devices[g]));
@@ -882,7 +910,8 @@ void run_chunked(const PreparedDataset& R, const PreparedDataset& S, const JoinS
             const int slot = slot_of(R, level);
             if (slot < 0) continue; // the join reports the missing level
             p->lv.push_back(detail::pack_level(R, a, *p->h, static_cast<size_t>(slot), pool));
-            bytes += p->h->n_vertices[slot] * 24 + p->h->n_facets[slot] * 28 + p->h->facet_offsets[slot].back() * 4;
+            bytes += p->h->n_vertices[slot] * 24 + p->h->n_facets[slot] * (p->lv.back()->zero_pads ? 12 : 28) +
+                     p->h->facet_offsets[slot].back() * 4;
             detail::check(tj_dataset_put_level(p->d.p, static_cast<uint32_t>(slot), &p->lv.back()->view), ctx);
         }
         std::lock_guard<std::mutex> lk(stat_mu);
@@ -950,6 +979,7 @@ JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const Jo
         out.stats.timeline.emplace_back(what, std::chrono::duration<double, std::milli>(Clock::now() - t_total).count());
     };
 
+    mark("entered");
     const std::vector<int> devices = detail::join_devices();
     const bool self_join = &R == &S;
     const size_t G = (trace && (trace->on_interval || trace->on_vp_pruned)) ? 1 : devices.size();
@@ -1049,7 +1079,7 @@ JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const Jo
                     staged.push_back(detail::pack_level(D, H, static_cast<size_t>(slot), pool));
                     pack_ms += std::chrono::duration<double, std::milli>(Clock::now() - tl).count();
                     mark(std::string(side == 0 ? "R" : "S") + "_lod" + std::to_string(level) + "_packed");
-                    out.stats.h2d_bytes += G * (H.n_vertices[slot] * 24 + H.n_facets[slot] * 28 + H.facet_offsets[slot].back() * 4);
+                    out.stats.h2d_bytes += G * (H.n_vertices[slot] * 24 + H.n_facets[slot] * (staged.back()->zero_pads ? 12 : 28) + H.facet_offsets[slot].back() * 4);
                     for (size_t g = 0; g < G; ++g) {
                         tj_dataset* ds = side == 0 ? dr[g].p : dsh[g].p;
                         auto& put = side == 0 ? put_r[g] : put_s[g];

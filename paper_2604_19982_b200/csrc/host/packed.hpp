@@ -89,6 +89,7 @@ struct PackedHeader {
 };
 struct PackedLevel {
     PinnedBuf verts, tris, hd, ph, vf; // tris / vf hold uint32 pairs per double slot
+    bool zero_pads = false;            // every hd / ph of the level is +0: not shipped
     tj_level_mesh_view view{};
 };
 std::unique_ptr<PackedHeader> pack_header(const PreparedDataset& ds, ThreadPool& pool);

@@ -184,6 +184,7 @@ def main():
     if world > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        os.environ["TRIJOIN_PROCESS_SHARD"] = f"{rank}/{world}"  # e2e: this rank's query blocks
     os.environ.setdefault("TRIJOIN_DEVICES", str(local))
     import paper_2604_19982_b200 as tj
     from paper_2604_19982_b200 import _core
@@ -298,8 +299,11 @@ def main():
             h2d = st.get("b200", {}).get("h2d_bytes", 0)
         e2e_ms = float(np.mean(ts))
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        if world > 1:
+        tot = torch.tensor([float(pairs_e2e), float(h2d), float(d2h)], dtype=torch.float64, device=dev)
+        if world > 1:  # each rank joined its own query blocks (TRIJOIN_PROCESS_SHARD)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+        pairs_e2e, h2d, d2h = float(tot[0]), float(tot[1]), float(tot[2])
         e2e = {"value": pairs_e2e / (float(t[0]) / 1e3), "unit": "pairs/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": float(t[0]),
                "path": "paper_2604_19982_b200._core.join_datasets -> trijoin::run_join -> tj_join (C-ABI)",

@@ -990,8 +990,24 @@ JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const Jo
     std::vector<Piece> pieces;
     std::function<size_t(uint32_t)> owner;
     const bool tracing = trace && (trace->on_interval || trace->on_vp_pruned);
+    // Process-level sharding for one-process-per-GPU launches ($TRIJOIN_PROCESS_SHARD = "i/n"):
+    // this process joins only the query blocks of shard i of n (records and counters then
+    // cover those queries only); resident path only.
+    size_t proc_i = 0, proc_n = 1;
+    if (const char* e = std::getenv("TRIJOIN_PROCESS_SHARD"); e && *e && !tracing) {
+        const std::string v(e);
+        const size_t slash = v.find('/');
+        if (slash == std::string::npos) throw std::invalid_argument("TRIJOIN_PROCESS_SHARD must be i/n");
+        proc_i = std::stoull(v.substr(0, slash));
+        proc_n = std::max<size_t>(1, std::stoull(v.substr(slash + 1)));
+        if (proc_i >= proc_n) throw std::invalid_argument("TRIJOIN_PROCESS_SHARD: i must be < n");
+    }
+    // queries per shard block ($TRIJOIN_SHARD_BLOCK for tests)
+    uint32_t block = 1024;
+    if (const char* e = std::getenv("TRIJOIN_SHARD_BLOCK"); e && *e) block = std::max<uint32_t>(1, std::stoul(e));
     const std::vector<std::pair<size_t, size_t>> chunks =
-        tracing ? std::vector<std::pair<size_t, size_t>>{} : plan_r_chunks(R, S, spec, devices[0], self_join, pool);
+        tracing || proc_n > 1 ? std::vector<std::pair<size_t, size_t>>{}
+                              : plan_r_chunks(R, S, spec, devices[0], self_join, pool);
     mark("planned");
     if (chunks.size() > 1) {
         run_chunked(R, S, spec, pool, devices, chunks, results, out, mark);
@@ -1042,9 +1058,9 @@ JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const Jo
                 tj_ctx* ctx = detail::device_context(devices[g]);
                 const auto td = Clock::now();
                 tj_join_spec cs = to_c_spec(spec);
-                cs.shard_index = static_cast<uint32_t>(g);
-                cs.shard_count = static_cast<uint32_t>(G);
-                cs.shard_block = 1024;
+                cs.shard_index = static_cast<uint32_t>(proc_i * G + g);
+                cs.shard_count = static_cast<uint32_t>(proc_n * G);
+                cs.shard_block = block;
                 TraceBridge bridge{trace};
                 tj_trace tt{&bridge, &TraceBridge::interval, &TraceBridge::pruned};
                 detail::check(tj_join(ctx, dr[g].p, self_join ? dr[g].p : dsh[g].p, &cs, trace ? &tt : nullptr,
@@ -1123,7 +1139,8 @@ JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const Jo
         }
 
         for (size_t g = 0; g < G; ++g) pieces.push_back({&results[g].r, 0u});
-        owner = [G](uint32_t r) { return G == 1 ? size_t{0} : size_t{(r / 1024) % G}; };
+        // (a query of another process's shard has empty ranges in every piece of this one)
+        owner = [G, proc_n, block](uint32_t r) { return size_t{(r / block) % (proc_n * G) % G}; };
     }
 
     // Merge: every query r is owned by one piece (a GPU shard, or an R chunk whose query ids

@@ -82,6 +82,21 @@ def test_out_of_core_r_chunks(monkeypatch, env, j):
         assert out["stats"]["b200"]["r_chunks"] > 1
 
 
+@pytest.mark.parametrize("j", [j for j in JOINS if j["r"] in ("nuclei60", "spheres80a")], ids=tjtest.join_id)
+def test_process_shards_partition_the_queries(monkeypatch, j):
+    """One process per GPU (bench.py under torchrun): TRIJOIN_PROCESS_SHARD=i/n joins the
+    query blocks of shard i only; the shards' records partition the full result."""
+    import paper_2604_19982_b200 as tj
+    r, s = _paths(j)
+    monkeypatch.setenv("TRIJOIN_SHARD_BLOCK", "7")
+    got = []
+    for i in range(3):
+        monkeypatch.setenv("TRIJOIN_PROCESS_SHARD", f"{i}/3")
+        got += tj.join(r, s, **j["kwargs"])["records"]
+    monkeypatch.delenv("TRIJOIN_PROCESS_SHARD")
+    assert sorted(got) == sorted(j["records"])
+
+
 @pytest.mark.parametrize("idx", ["mini10_s61.idx", "mini18_s21.idx", "spheres80a.idx"])
 def test_intersect_decision_mode(capi, idx):
     """Intersection joins refine in decision mode unless TJ_FLAG_EXACT_INTERVALS (4): statuses

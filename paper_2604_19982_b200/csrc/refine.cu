@@ -14,6 +14,9 @@ namespace {
 // TRIJOIN_DEBUG_OPSTATS diagnostics (per-op counters only in a -DTJ_DEBUG_OPSTATS build)
 __device__ unsigned long long* g_dbg_op_tested = nullptr;
 
+// stage-1 s facets per lane and loop iteration (kQueue >= 31 + 32 kS1Unroll)
+constexpr int kS1Unroll = 2; // 4: config B -1 %, config C +8 % (small tiles waste the extra slots)
+
 // k_screen launch shape: 8 warps per block, 2 blocks per SM (16 warps, 128 registers; 4 x 5 was
 // slower: the 102-register bound spills the stage-2 code)
 constexpr int kScreenThreads = 256;
@@ -462,39 +465,42 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks) k_screen(Refine
 #endif
                         const int max_iters = (scnt + P - 1) / P;
                         int nq = 0;
-                        // two s facets per lane and iteration: independent dependency chains
-                        for (int t = 0;; t += 2) {
+                        // kS1Unroll s facets per lane and iteration: independent dependency chains
+                        for (int t = 0;; t += kS1Unroll) {
                             if (t < max_iters) {
-                                const int bj0 = jj + t * P;
-                                const bool v0 = row_on && t < iters, v1 = row_on && t + 1 < iters;
-                                const int bj1 = v1 ? bj0 + P : bj0;
-                                bool n0 = v0, n1 = v1;
-                                if (cull) {
-                                    const float* b0p = sm.sc + bj0 * kCS;
-                                    const float* b1p = sm.sc + bj1 * kCS;
-                                    const int s0 = stage1_box(ar, *reinterpret_cast<const float4*>(b0p),
-                                                              *reinterpret_cast<const float4*>(b0p + 4), b0p[11], rlb, rub);
-                                    const int s1 = stage1_box(ar, *reinterpret_cast<const float4*>(b1p),
-                                                              *reinterpret_cast<const float4*>(b1p + 4), b1p[11], rlb, rub);
-                                    const float* asr = sm.rc + bi * kCS;
-                                    n0 = v0 && (s0 == 1 || (s0 == 2 && stage1_ill(ar, asr, b0p)));
-                                    n1 = v1 && (s1 == 1 || (s1 == 2 && stage1_ill(ar, asr, b1p)));
+                                int bj[kS1Unroll];
+                                bool nn[kS1Unroll];
+#pragma unroll
+                                for (int u = 0; u < kS1Unroll; ++u) {
+                                    nn[u] = row_on && t + u < iters;
+                                    bj[u] = nn[u] ? jj + (t + u) * P : 0; // a valid row either way
                                 }
-                                if (!cull) {
-                                    queue_push(q, n0, d.op, (uint32_t)(d.r0 + rc0 + sm.rl[rt0 + bi]),
-                                               (uint32_t)(d.s0 + sc0 + sm.sl[st0 + bj0]));
-                                    queue_push(q, n1, d.op, (uint32_t)(d.r0 + rc0 + sm.rl[rt0 + bi]),
-                                               (uint32_t)(d.s0 + sc0 + sm.sl[st0 + bj1]));
-                                } else {
-                                    const unsigned bal0 = __ballot_sync(0xffffffffu, n0);
-                                    if (n0) sm.q[nq + __popc(bal0 & ((1u << lane) - 1u))] = (uint16_t)((bi << 5) | bj0);
-                                    nq += __popc(bal0);
-                                    const unsigned bal1 = __ballot_sync(0xffffffffu, n1);
-                                    if (n1) sm.q[nq + __popc(bal1 & ((1u << lane) - 1u))] = (uint16_t)((bi << 5) | bj1);
-                                    nq += __popc(bal1);
+                                if (cull) {
+                                    int sb[kS1Unroll];
+#pragma unroll
+                                    for (int u = 0; u < kS1Unroll; ++u) {
+                                        const float* bp = sm.sc + bj[u] * kCS;
+                                        sb[u] = stage1_box(ar, *reinterpret_cast<const float4*>(bp),
+                                                           *reinterpret_cast<const float4*>(bp + 4), bp[11], rlb, rub);
+                                    }
+                                    const float* asr = sm.rc + bi * kCS;
+#pragma unroll
+                                    for (int u = 0; u < kS1Unroll; ++u)
+                                        nn[u] = nn[u] && (sb[u] == 1 || (sb[u] == 2 && stage1_ill(ar, asr, sm.sc + bj[u] * kCS)));
+                                }
+#pragma unroll
+                                for (int u = 0; u < kS1Unroll; ++u) {
+                                    if (!cull) {
+                                        queue_push(q, nn[u], d.op, (uint32_t)(d.r0 + rc0 + sm.rl[rt0 + bi]),
+                                                   (uint32_t)(d.s0 + sc0 + sm.sl[st0 + bj[u]]));
+                                    } else {
+                                        const unsigned bal = __ballot_sync(0xffffffffu, nn[u]);
+                                        if (nn[u]) sm.q[nq + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)((bi << 5) | bj[u]);
+                                        nq += __popc(bal);
+                                    }
                                 }
                             }
-                            const bool last = t + 2 >= max_iters;
+                            const bool last = t + kS1Unroll >= max_iters;
                             while (nq >= 32 || (last && nq > 0)) { // second stage on up to 32 queued pairs
                                 const int n = min(nq, 32);
                                 __syncwarp();

@@ -296,6 +296,14 @@ __device__ __forceinline__ int sat_needed(const float* a, const float* b, const 
     float B = fmaxf(B0, sat_faces(f, a, b));
     mask = cannot_improve(B, a, b, th) ? skip_mask(B, a, b) : -1;
     if (mask != 0) {
+        // The 9 edge axes can only raise B towards the distance. Skip them where they cannot
+        // change the outcome (shapes outside the skip argument) or are very unlikely to (the
+        // bound needed for a skip is over twice the face bound): the pair is then evaluated,
+        // which is always exact.
+        if (a[3] < 0.f || b[3] < 0.f) return 1;
+        const float need_lb = (th.lb_sat || th.lb_u == 0.f) ? 0.f : th.lb_u + a[11] + b[11];
+        const float need_ub = th.ub_u == 0.f ? 0.f : th.ub_u - a[7] - b[7];
+        if (B < 0.5f * fmaxf(need_lb, need_ub)) return 1;
         B = fmaxf(B, sat_edges(f, a, b));
         mask = cannot_improve(B, a, b, th) ? skip_mask(B, a, b) : -1;
     }

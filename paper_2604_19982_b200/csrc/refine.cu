@@ -498,7 +498,7 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks) k_screen(Refine
                         for (int t = 0;; t += kS1Unroll) {
                             if (t < max_iters) {
                                 int bj[kS1Unroll];
-                                bool nn[kS1Unroll];
+                                bool nn[kS1Unroll], fl[kS1Unroll] = {};
 #pragma unroll
                                 for (int u = 0; u < kS1Unroll; ++u) {
                                     nn[u] = row_on && t + u < iters;
@@ -512,10 +512,15 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks) k_screen(Refine
                                         sb[u] = stage1_box(ar, *reinterpret_cast<const float4*>(bp),
                                                            *reinterpret_cast<const float4*>(bp + 4), bp[11], rlb, rub);
                                     }
-                                    const float* asr = sm.rc + bi * kCS;
+                                    // near pairs whose DP4A conditioning pre-test fails are queued
+                                    // with a flag: the FP32 conditioning test runs at the flush,
+                                    // 32 pairs at a time instead of on a few divergent lanes here
 #pragma unroll
-                                    for (int u = 0; u < kS1Unroll; ++u)
-                                        nn[u] = nn[u] && (sb[u] == 1 || (sb[u] == 2 && stage1_ill(ar, asr, sm.sc + bj[u] * kCS)));
+                                    for (int u = 0; u < kS1Unroll; ++u) {
+                                        fl[u] = sb[u] == 2 &&
+                                                !well_cond_q(ar.q, *reinterpret_cast<const int4*>(sm.sc + bj[u] * kCS + 28));
+                                        nn[u] = nn[u] && (sb[u] == 1 || fl[u]);
+                                    }
                                 }
 #pragma unroll
                                 for (int u = 0; u < kS1Unroll; ++u) {
@@ -524,7 +529,9 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks) k_screen(Refine
                                                    (uint32_t)(d.s0 + sc0 + sm.sl[st0 + bj[u]]));
                                     } else {
                                         const unsigned bal = __ballot_sync(0xffffffffu, nn[u]);
-                                        if (nn[u]) sm.q[nq + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)((bi << 5) | bj[u]);
+                                        if (nn[u])
+                                            sm.q[nq + __popc(bal & ((1u << lane) - 1u))] =
+                                                (uint16_t)((fl[u] ? 0x8000 : 0) | (bi << 5) | bj[u]);
                                         nq += __popc(bal);
                                     }
                                 }
@@ -535,17 +542,22 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks) k_screen(Refine
                                 __syncwarp();
                                 bool need = false;
                                 uint32_t fr = 0, fs = 0;
+                                bool go = false;
                                 if (lane < n) {
                                     const int e = sm.q[lane];
-                                    const int i = e >> 5, j = e & 31;
-                                    fr = (uint32_t)(d.r0 + rc0 + sm.rl[rt0 + i]);
-                                    fs = (uint32_t)(d.s0 + sc0 + sm.sl[st0 + j]);
-                                    const int r = sat_needed(sm.rc + i * kCS, sm.sc + j * kCS, src.r_facets + (size_t)fr * 12,
-                                                             src.s_facets + (size_t)fs * 12, th);
-                                    need = r & 1;
-                                    if (r >> 1) atomicAdd(&sm.cnt[2], 1u); // rare
+                                    const int i = (e >> 5) & 31, j = e & 31;
+                                    go = !(e & 0x8000) || stage1_ill_fp32(sm.rc + i * kCS, sm.sc + j * kCS);
+                                    if (go) {
+                                        fr = (uint32_t)(d.r0 + rc0 + sm.rl[rt0 + i]);
+                                        fs = (uint32_t)(d.s0 + sc0 + sm.sl[st0 + j]);
+                                        const int r = sat_needed(sm.rc + i * kCS, sm.sc + j * kCS, src.r_facets + (size_t)fr * 12,
+                                                                 src.s_facets + (size_t)fs * 12, th);
+                                        need = r & 1;
+                                        if (r >> 1) atomicAdd(&sm.cnt[2], 1u); // rare
+                                    }
                                 }
-                                if (lane == 0) sm.cnt[1] += (uint32_t)n;
+                                const unsigned ngo = __popc(__ballot_sync(0xffffffffu, go));
+                                if (lane == 0) sm.cnt[1] += ngo;
                                 queue_push(q, need, d.op, fr, fs);
                                 __syncwarp();
                                 for (int k0 = 0; k0 < nq - n; k0 += 32) { // shift the rest down (in order)

@@ -388,10 +388,10 @@ __device__ __forceinline__ int stage1_box(const RowRec& a, float4 b0, float4 b1,
     return skip ? (g2 > f * f ? 0 : 2) : 1;
 }
 
-// Conditioning decision of a near, box-skippable pair (the rest of skip_mask): true iff some
-// edge / plane combination is ill conditioned (the pair must go to stage 2).
-__device__ __forceinline__ bool stage1_ill(const RowRec& a, const float* as, const float* b) {
-    if (well_cond_q(a.q, *reinterpret_cast<const int4*>(b + 28))) return false;
+// Conditioning decision of a near, box-skippable pair whose DP4A pre-test failed (the rest of
+// skip_mask, FP32): true iff some edge / plane combination is ill conditioned (the pair must
+// go to stage 2).
+__device__ __forceinline__ bool stage1_ill_fp32(const float* as, const float* b) {
     const float4 b2 = *reinterpret_cast<const float4*>(b + 8);
     const float4 b3 = *reinterpret_cast<const float4*>(b + 12), b4 = *reinterpret_cast<const float4*>(b + 16);
     const float b20 = b[20];

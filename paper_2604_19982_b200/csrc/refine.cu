@@ -97,14 +97,19 @@ __device__ __forceinline__ void queue_push(const RefineQueue& q, bool want, uint
 // kCS floats apart).
 __device__ __forceinline__ void gather_recs(const float4* __restrict__ box, const float4* __restrict__ geo,
                                             uint64_t first, const uint16_t* list, int n, float* dst) {
+    // cp.async: every 16-B piece is in flight at once (a load -> store loop serialises one
+    // global latency per iteration and lane)
     const int lane = threadIdx.x & 31;
     float4* d4 = reinterpret_cast<float4*>(dst);
     for (int k = lane; k < kRecF4 * n; k += 32) {
         const int rec = k / kRecF4, part = k % kRecF4;
         const uint64_t f = first + list[rec];
-        d4[rec * (kCS / 4) + part] =
-            part < kBoxF4 ? __ldg(box + f * kBoxF4 + part) : __ldg(geo + f * kGeoF4 + (part - kBoxF4));
+        const float4* g = part < kBoxF4 ? box + f * kBoxF4 + part : geo + f * kGeoF4 + (part - kBoxF4);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_addr(d4 + rec * (kCS / 4) + part)),
+                     "l"(g)
+                     : "memory");
     }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
 // Warp argmin (ties: lowest index) of (value, index).

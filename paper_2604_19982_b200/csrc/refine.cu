@@ -412,30 +412,66 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks) k_screen(Refine
         if (lane == 0) base = atomicAdd(work, (unsigned long long)batch);
         base = __shfl_sync(0xffffffffu, base, 0) + vp_begin;
         if (base >= vp_end) break;
-        bool live = false;
+        // whole-voxel-pair screen on the segment aggregates; d0 >= 1e-5 (L_i + L_j) + 1e-12
+        // (M_i + M_j) for every facet pair of the voxel pair
+        auto vp_screen = [&](const VpDescDev& d, const Thresh& th, float& d0, SegAgg& ar, SegAgg& as) {
+            ar = seg_r_of(src, d);
+            as = seg_s_of(src, d);
+            d0 = __fadd_ru(__fmul_ru(2e-5f, fmaxf(ar.Lmax, as.Lmax)), __fmul_ru(2e-12f, fmaxf(seg_m(ar), seg_m(as))));
+            return ar.ok && as.ok &&
+                   agg_skip(ar.lo, ar.hi, as.lo, as.hi, ar.Lmax + as.Lmax, fminf(ar.Lmin, as.Lmin),
+                            __fadd_ru(ar.phmax, as.phmax), __fadd_rd(ar.hdmin, as.hdmin), d0, th);
+        };
+        // with precomputed segment aggregates (join mode) the voxel-pair screen runs here too,
+        // one voxel pair per lane
+        const bool pre_seg = cull && src.r_seg && src.s_seg;
+        bool live = false, agg_skipped = false;
+        __syncwarp();
         if (lane < batch && base + lane < vp_end) {
             const VpDescDev dl = get_vp(src, base + lane);
-            live = dl.rn != 0 && dl.sn != 0 && !settled(thresholds(dl));
+            const Thresh tl = thresholds(dl);
+            live = dl.rn != 0 && dl.sn != 0 && !settled(tl);
+            if (live && pre_seg) {
+                float d0;
+                SegAgg ar, as;
+                agg_skipped = vp_screen(dl, tl, d0, ar, as);
+                live = !agg_skipped;
+            }
+            if (live) sm.vpd[lane] = {dl.r0, dl.s0, dl.op, dl.gvr, dl.gvs, dl.rn, dl.sn, tl.lb_u, tl.ub_u, (int)tl.lb_sat};
+        }
+        if (pre_seg) {
+            const unsigned n_agg = __popc(__ballot_sync(0xffffffffu, agg_skipped));
+            if (lane == 0) sm.cnt[3] += n_agg;
         }
         unsigned pending = __ballot_sync(0xffffffffu, live);
+        __syncwarp(); // sm.vpd visible to the warp
         while (pending) {
         const int lv = __ffs(pending) - 1;
         pending &= pending - 1;
-        const unsigned long long vp = base + lv;
-        const VpDescDev d = get_vp(src, vp);
-        const Thresh th = thresholds(d);
+        VpDescDev d;
+        Thresh th;
+        {
+            const ScreenSmem::BatchVp& b = sm.vpd[lv];
+            d.op = b.op;
+            d.gvr = b.gvr;
+            d.gvs = b.gvs;
+            d.r0 = b.r0;
+            d.s0 = b.s0;
+            d.rn = b.rn;
+            d.sn = b.sn;
+            th.lb_u = b.lb_u;
+            th.ub_u = b.ub_u;
+            th.lb_sat = b.lb_sat != 0;
+        }
         // hierarchical screens: the whole voxel pair (always when the segment aggregates are
         // precomputed), then rows / columns where that can pay off
         const bool hier = cull && d.rn * d.sn >= kHierMinPairs;
         float delta0 = 0.f; // tile-pair value when !hier
-        if (cull && (hier || src.r_seg)) {
-            const SegAgg ar = seg_r_of(src, d);
-            const SegAgg as = seg_s_of(src, d);
-            // d0 >= 1e-5 (L_i + L_j) + 1e-12 (M_i + M_j) for every pair of the voxel pair
-            const float d0 = __fadd_ru(__fmul_ru(2e-5f, fmaxf(ar.Lmax, as.Lmax)), __fmul_ru(2e-12f, fmaxf(seg_m(ar), seg_m(as))));
-            if (ar.ok && as.ok &&
-                agg_skip(ar.lo, ar.hi, as.lo, as.hi, ar.Lmax + as.Lmax, fminf(ar.Lmin, as.Lmin),
-                         __fadd_ru(ar.phmax, as.phmax), __fadd_rd(ar.hdmin, as.hdmin), d0, th)) {
+        if (hier || (cull && !pre_seg && src.r_seg)) {
+            float d0;
+            SegAgg ar, as;
+            const bool skip = vp_screen(d, th, d0, ar, as);
+            if (!pre_seg && skip) {
                 if (lane == 0) ++sm.cnt[3];
                 continue;
             }

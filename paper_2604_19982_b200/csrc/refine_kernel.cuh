@@ -84,6 +84,13 @@ struct __align__(16) ScreenSmem {
     uint16_t rl[kCap]; // surviving r facets of the current raw chunk (offsets in the chunk)
     uint16_t sl[kCap]; // surviving s facets
     SegAgg seg_r, seg_s; // aggregates of the current voxel pair's segments
+    // the current work batch: per voxel pair (lane) its segments, op and thresholds
+    struct BatchVp {
+        uint64_t r0, s0;
+        uint32_t op, gvr, gvs, rn, sn;
+        float lb_u, ub_u;
+        int lb_sat;
+    } vpd[32];
     // the warp's counters (lane 0 writes; kept out of registers: the stage-1 loop is at the
     // register limit): tested, separating-axis tests, verified, voxel pairs skipped, dropped
     uint32_t cnt[5];

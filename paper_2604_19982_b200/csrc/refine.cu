@@ -109,8 +109,8 @@ __device__ __forceinline__ void gather_recs(const float4* __restrict__ box, cons
                      "l"(g)
                      : "memory");
     }
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
+__device__ __forceinline__ void gather_wait() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // Warp argmin (ties: lowest index) of (value, index).
 __device__ __forceinline__ void warp_argmin(float& v, uint32_t& idx) {
@@ -494,13 +494,19 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks) k_screen(Refine
                 for (int rt0 = 0; nsl > 0 && rt0 < nrl; rt0 += kRT) {
                     const int rcnt = min(kRT, nrl - rt0);
                     __syncwarp();
+                    // the r tile and the first s tile in flight together
                     gather_recs(src.r_box, src.r_geo, d.r0 + rc0, sm.rl + rt0, rcnt, sm.rc);
+                    gather_recs(src.s_box, src.s_geo, d.s0 + sc0, sm.sl, min(kST, nsl), sm.sc);
+                    gather_wait();
                     __syncwarp();
                     for (int st0 = 0; st0 < nsl; st0 += kST) {
                         const int scnt = min(kST, nsl - st0);
-                        __syncwarp();
-                        gather_recs(src.s_box, src.s_geo, d.s0 + sc0, sm.sl + st0, scnt, sm.sc);
-                        __syncwarp();
+                        if (st0 > 0) {
+                            __syncwarp();
+                            gather_recs(src.s_box, src.s_geo, d.s0 + sc0, sm.sl + st0, scnt, sm.sc);
+                            gather_wait();
+                            __syncwarp();
+                        }
                         float dl = delta0;
                         if (!hier) { // tile-pair delta0 >= 1e-5 (L_i + L_j) + 1e-12 (M_i + M_j)
                             float Lm = 0.f, Mm = 0.f;

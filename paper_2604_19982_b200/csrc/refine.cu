@@ -205,22 +205,32 @@ __device__ __forceinline__ void closest_pair(const float4* __restrict__ rset, ui
 // segment's box, j* symmetrically; then j' = the s facet closest to i* and i' the r facet
 // closest to j*; queues (i*, j') and (i', j*). In decision mode only voxel pairs that can
 // hold a zero bound are seeded (segment gap <= ph_max(r) + ph_max(s)).
+#ifndef SEED_BATCH
+#define SEED_BATCH 32
+#endif
+__device__ __forceinline__ unsigned seed_batch() { return SEED_BATCH; }
 __global__ void __launch_bounds__(256) k_seed(RefineSource src, uint64_t vp_begin, uint64_t vp_end, RefineQueue q,
                                               int cull) {
+    // per warp: the voxel pairs of the current batch that need seeds (segments + boxes)
+    struct SeedVp {
+        uint64_t r0, s0;
+        uint32_t op, rn, sn, pad;
+        float alo[3], ahi[3], blo[3], bhi[3];
+    };
+    __shared__ SeedVp sv[8][32];
     const int lane = threadIdx.x & 31;
     const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    const uint64_t gw = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
     PairRef pref{0u, 0u, 0u, 0u}; // this lane's buffered seed
     int pend = 0;
-    for (uint64_t vp = vp_begin + blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); vp < vp_end; vp += nw) {
-        const VpDescDev d = get_vp(src, vp);
-        if (d.rn == 0 || d.sn == 0) continue;
-        const SegAgg ar = seg_r_of(src, d);
-        const SegAgg as = seg_s_of(src, d);
-        if (cull == 2) {
-            const float arec[8] = {ar.lo[0], ar.lo[1], ar.lo[2], 0.f, ar.hi[0], ar.hi[1], ar.hi[2], 0.f};
-            const float brec[8] = {as.lo[0], as.lo[1], as.lo[2], 0.f, as.hi[0], as.hi[1], as.hi[2], 0.f};
-            if (box_gap_lb(arec, brec) > __fadd_ru(ar.phmax, as.phmax)) continue;
-        }
+    // decision mode: only voxel pairs that can hold a zero bound
+    auto seedable = [&](const SegAgg& ar, const SegAgg& as) {
+        if (cull != 2) return true;
+        const float arec[8] = {ar.lo[0], ar.lo[1], ar.lo[2], 0.f, ar.hi[0], ar.hi[1], ar.hi[2], 0.f};
+        const float brec[8] = {as.lo[0], as.lo[1], as.lo[2], 0.f, as.hi[0], as.hi[1], as.hi[2], 0.f};
+        return !(box_gap_lb(arec, brec) > __fadd_ru(ar.phmax, as.phmax));
+    };
+    auto seed_vp = [&](const VpDescDev& d, const SegAgg& ar, const SegAgg& as) {
         uint32_t ist, jst, ip, jp;
         if (d.rn <= 32 && d.sn <= 32) {
             // both segments fit the warp: each lane keeps its r and s facet boxes in registers
@@ -256,6 +266,58 @@ __global__ void __launch_bounds__(256) k_seed(RefineSource src, uint64_t vp_begi
         if (pend >= 31) {
             queue_push(q, lane < pend, pref.op, pref.fr, pref.fs);
             pend = 0;
+        }
+    };
+    if (src.r_seg && src.s_seg) {
+        // precomputed segment aggregates: batches of 32 voxel pairs, one per lane for the
+        // descriptor / aggregate lookups and the decision-mode test (independent latency
+        // chains), then the warp seeds the survivors
+        SeedVp* mine = sv[threadIdx.x >> 5];
+        const unsigned nb = seed_batch();
+        for (uint64_t base = vp_begin + gw * nb; base < vp_end; base += nw * nb) {
+            bool live = false;
+            __syncwarp();
+            if (lane < nb && base + lane < vp_end) {
+                const VpDescDev d = get_vp(src, base + lane);
+                if (d.rn != 0 && d.sn != 0) {
+                    const SegAgg ar = seg_r_of(src, d), as = seg_s_of(src, d);
+                    live = seedable(ar, as);
+                    if (live)
+                        mine[lane] = {d.r0, d.s0, d.op, d.rn, d.sn, 0u,
+                                      {ar.lo[0], ar.lo[1], ar.lo[2]}, {ar.hi[0], ar.hi[1], ar.hi[2]},
+                                      {as.lo[0], as.lo[1], as.lo[2]}, {as.hi[0], as.hi[1], as.hi[2]}};
+                }
+            }
+            unsigned pending = __ballot_sync(0xffffffffu, live);
+            __syncwarp();
+            while (pending) {
+                const int lv = __ffs(pending) - 1;
+                pending &= pending - 1;
+                const SeedVp& e = mine[lv];
+                VpDescDev d{};
+                d.op = e.op;
+                d.r0 = e.r0;
+                d.s0 = e.s0;
+                d.rn = e.rn;
+                d.sn = e.sn;
+                SegAgg ar{}, as{}; // only lo / hi are read by the seeding
+                for (int k = 0; k < 3; ++k) {
+                    ar.lo[k] = e.alo[k];
+                    ar.hi[k] = e.ahi[k];
+                    as.lo[k] = e.blo[k];
+                    as.hi[k] = e.bhi[k];
+                }
+                seed_vp(d, ar, as);
+            }
+        }
+    } else {
+        for (uint64_t vp = vp_begin + gw; vp < vp_end; vp += nw) {
+            const VpDescDev d = get_vp(src, vp);
+            if (d.rn == 0 || d.sn == 0) continue;
+            const SegAgg ar = seg_r_of(src, d);
+            const SegAgg as = seg_s_of(src, d);
+            if (!seedable(ar, as)) continue;
+            seed_vp(d, ar, as);
         }
     }
     queue_push(q, lane < pend, pref.op, pref.fr, pref.fs);

@@ -15,8 +15,6 @@ namespace {
 // TRIJOIN_DEBUG_OPSTATS diagnostics (per-op counters only in a -DTJ_DEBUG_OPSTATS build)
 __device__ unsigned long long* g_dbg_op_tested = nullptr;
 
-// stage-1 s facets per lane and loop iteration (kQueue >= 31 + 32 kS1Unroll)
-constexpr int kS1Unroll = 2; // 4: config B -1 %, config C +8 % (small tiles waste the extra slots)
 
 // k_screen launch shape: 8 warps per block, 2 blocks per SM (16 warps, 128 registers; 4 x 5 was
 // slower: the 102-register bound spills the stage-2 code)
@@ -601,51 +599,44 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks) k_screen(Refine
 #ifdef TJ_DEBUG_OPSTATS
                         if (lane == 0 && g_dbg_op_tested) atomicAdd(g_dbg_op_tested + d.op, (unsigned long long)(rcnt * scnt));
 #endif
-                        const int max_iters = (scnt + P - 1) / P;
-                        int nq = 0;
-                        // kS1Unroll s facets per lane and iteration: independent dependency chains
-                        for (int t = 0;; t += kS1Unroll) {
-                            if (t < max_iters) {
-                                int bj[kS1Unroll];
-                                bool nn[kS1Unroll], fl[kS1Unroll] = {};
-#pragma unroll
-                                for (int u = 0; u < kS1Unroll; ++u) {
-                                    nn[u] = row_on && t + u < iters;
-                                    bj[u] = nn[u] ? jj + (t + u) * P : 0; // a valid row either way
-                                }
-                                if (cull) {
-                                    int sb[kS1Unroll];
-#pragma unroll
-                                    for (int u = 0; u < kS1Unroll; ++u) {
-                                        const float* bp = sm.sc + bj[u] * kCS;
-                                        sb[u] = stage1_box(ar, *reinterpret_cast<const float4*>(bp),
-                                                           *reinterpret_cast<const float4*>(bp + 4), bp[11], rlb, rub);
-                                    }
-                                    // near pairs whose DP4A conditioning pre-test fails are queued
-                                    // with a flag: the FP32 conditioning test runs at the flush,
-                                    // 32 pairs at a time instead of on a few divergent lanes here
-#pragma unroll
-                                    for (int u = 0; u < kS1Unroll; ++u) {
-                                        fl[u] = sb[u] == 2 &&
-                                                !well_cond_q(ar.q, *reinterpret_cast<const int4*>(sm.sc + bj[u] * kCS + 28));
-                                        nn[u] = nn[u] && (sb[u] == 1 || fl[u]);
-                                    }
-                                }
-#pragma unroll
-                                for (int u = 0; u < kS1Unroll; ++u) {
-                                    if (!cull) {
-                                        queue_push(q, nn[u], d.op, (uint32_t)(d.r0 + rc0 + sm.rl[rt0 + bi]),
-                                                   (uint32_t)(d.s0 + sc0 + sm.sl[st0 + bj[u]]));
-                                    } else {
-                                        const unsigned bal = __ballot_sync(0xffffffffu, nn[u]);
-                                        if (nn[u])
-                                            sm.q[nq + __popc(bal & ((1u << lane) - 1u))] =
-                                                (uint16_t)((fl[u] ? 0x8000 : 0) | (bi << 5) | bj[u]);
-                                        nq += __popc(bal);
-                                    }
-                                }
+                        if (!cull) { // every pair to the exact queue
+                            const int max_iters = (scnt + P - 1) / P;
+                            for (int t = 0; t < max_iters; ++t) {
+                                const bool nn = row_on && t < iters;
+                                queue_push(q, nn, d.op, (uint32_t)(d.r0 + rc0 + sm.rl[rt0 + bi]),
+                                           (uint32_t)(d.s0 + sc0 + sm.sl[st0 + (nn ? jj + t * P : 0)]));
                             }
-                            const bool last = t + kS1Unroll >= max_iters;
+                            continue;
+                        }
+                        // The lane's s facets (jj + t P) into bit masks: bit t of `need` = the pair
+                        // goes to stage 2; of `flag` = a near pair whose DP4A conditioning
+                        // pre-test failed (its FP32 test runs at the flush, 32 pairs at a time).
+                        uint32_t nmask = 0, fmask = 0;
+                        if (row_on) {
+#pragma unroll 2
+                            for (int t = 0; t < iters; ++t) {
+                                const float* bp = sm.sc + (jj + t * P) * kCS;
+                                const int sb = stage1_box(ar, *reinterpret_cast<const float4*>(bp),
+                                                          *reinterpret_cast<const float4*>(bp + 4), bp[11], rlb, rub);
+                                const bool f = sb == 2 && !well_cond_q(ar.q, *reinterpret_cast<const int4*>(bp + 28));
+                                nmask |= (uint32_t)(sb == 1 || f) << t;
+                                fmask |= (uint32_t)f << t;
+                            }
+                        }
+                        // compact the masks into the warp queue one entry per lane and round;
+                        // stage 2 runs whenever 32 entries are queued
+                        int nq = 0;
+                        for (;;) {
+                            const bool has = nmask != 0;
+                            const unsigned bal = __ballot_sync(0xffffffffu, has);
+                            if (has) {
+                                const int t = __ffs(nmask) - 1;
+                                nmask &= nmask - 1;
+                                sm.q[nq + __popc(bal & ((1u << lane) - 1u))] =
+                                    (uint16_t)(((fmask >> t) & 1u ? 0x8000 : 0) | (bi << 5) | (jj + t * P));
+                            }
+                            nq += __popc(bal);
+                            const bool last = bal == 0;
                             while (nq >= 32 || (last && nq > 0)) { // second stage on up to 32 queued pairs
                                 const int n = min(nq, 32);
                                 __syncwarp();
@@ -678,7 +669,7 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks) k_screen(Refine
                                 }
                                 nq -= n;
                             }
-                            if (last && nq == 0) break;
+                            if (last) break;
                         }
                     }
                 }

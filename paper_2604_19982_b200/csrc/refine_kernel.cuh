@@ -52,7 +52,7 @@ constexpr int kCS = 36;    // shared-memory stride of a screening record (32 flo
 constexpr int kRecF4 = kScreenRecF4; // float4 per screening record (floats 0-31)
 constexpr int kBoxF4 = 3;  // box part of a record (floats 0-11), its own array: 3 float4 per facet
 constexpr int kGeoF4 = 5;  // geometry part (floats 12-31): 5 float4 per facet
-constexpr int kQueue = 96;  // per-warp SAT queue (< 32 pending + kS1Unroll x 32 new, kS1Unroll <= 2)
+constexpr int kQueue = 64;  // per-warp SAT queue (< 32 pending + 32 new per compaction round)
 constexpr int kCap = 128;  // per-warp survivor lists: facets per raw segment chunk
 constexpr uint32_t kHierMinPairs = 1024; // voxel pairs with fewer facet pairs skip the hierarchical screens
 

@@ -415,6 +415,15 @@ __device__ __forceinline__ int build_list(const float4* __restrict__ box, uint64
 // 32 x 32 shared-memory tiles, every pair tested on its facet-AABB gap; (4) box survivors
 // through the separating-axis stage (sat_needed). Pairs that may still change the op's
 // bounds go to the exact queue (refine_kernel.cuh has the exactness argument).
+// voxel pairs with fewer facet pairs skip the row / column screens (TRIJOIN_HIER_MIN: tuning)
+uint32_t hier_min_pairs() {
+    static const uint32_t v = [] {
+        const char* e = getenv("TRIJOIN_HIER_MIN");
+        return e ? (uint32_t)atoi(e) : kHierMinPairs;
+    }();
+    return v;
+}
+
 // voxel pairs per work grab of k_screen (TRIJOIN_SCREEN_BATCH: tuning override, 1..32)
 unsigned screen_batch() {
     static const unsigned b = [] {
@@ -429,7 +438,7 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks) k_screen(Refine
                                                 const unsigned long long* __restrict__ op_lb_bits,
                                                 const unsigned long long* __restrict__ op_ub_bits, int cull,
                                                 RefineQueue q, unsigned long long* work,
-                                                unsigned long long* counters, unsigned batch) {
+                                                unsigned long long* counters, unsigned batch, uint32_t hier_min) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ScreenSmem& sm = reinterpret_cast<ScreenSmem*>(smem_raw)[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
@@ -525,7 +534,7 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks) k_screen(Refine
         }
         // hierarchical screens: the whole voxel pair (always when the segment aggregates are
         // precomputed), then rows / columns where that can pay off
-        const bool hier = cull && d.rn * d.sn >= kHierMinPairs;
+        const bool hier = cull && d.rn * d.sn >= hier_min;
         float delta0 = 0.f; // tile-pair value when !hier
         if (hier || (cull && !pre_seg && src.r_seg)) {
             float d0;
@@ -816,7 +825,7 @@ void refine_pass(const RefineSource& src, uint64_t vp_begin, uint64_t vp_end, bo
         count_launch();
         k_screen<<<warp_grid(vp_end - vp_begin, num_sms, kScreenBlocks, kScreenThreads / 32), kScreenThreads,
                    kScreenSmem, st>>>(
-            src, vp_begin, vp_end, lb_bits, ub_bits, cull, qs.view(), work, counters, screen_batch());
+            src, vp_begin, vp_end, lb_bits, ub_bits, cull, qs.view(), work, counters, screen_batch(), hier_min_pairs());
         TJ_CUDA(cudaGetLastError());
     }
     count_launch();

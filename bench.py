@@ -65,6 +65,21 @@ def dist_env():
     return world, rank, local
 
 
+def ncu_traffic(config):
+    """DRAM bytes of one k_screen launch (the dominant kernel) from the committed ncu --set full
+    capture of this workload (profiles/ncu_traffic_<config>.json, scripts/ncu_traffic.py), or None."""
+    path = os.path.join(ROOT, "profiles", f"ncu_traffic_{config}.json")
+    try:
+        launches = [l for l in json.load(open(path))["launches"] if l["kernel"] == "k_screen"]
+    except (OSError, ValueError, KeyError):
+        return None, None
+    if not launches:
+        return None, None
+    top = max(launches, key=lambda l: l["dram_bytes"])
+    return top["dram_bytes"], f"profiles/ncu_traffic_{config}.json ({top['report']}: one k_screen launch, " \
+                              f"{top['duration_s'] * 1e3:.2f} ms, {top['dram_GBps']:.0f} GB/s)"
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -259,8 +274,9 @@ def main():
     work_flop = evaluated * FLOP_PER_PAIR + tested * FLOP_PER_TEST + screened * FLOP_PER_SAT
     achieved = work_flop / (kernel_ms / 1e3) / 1e12 / max(world, 1)
     brute_peak_pairs = fp32_peak * 1e12 / FLOP_PER_PAIR  # every reference facet pair through tri_tri at FP32 peak
+    traffic, traffic_src = ncu_traffic(a.config)
     roofline = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
-                "frac": achieved / fp32_peak, "traffic": None,
+                "frac": achieved / fp32_peak, "traffic": traffic, "traffic_source": traffic_src,
                 "kernel": "refinement kernels k_seed + k_screen + k_eval (all LOD levels, CUDA events)",
                 "flop_model": f"{FLOP_PER_TEST:g} x box tests + {FLOP_PER_SAT:g} x separating-axis tests + "
                               f"{FLOP_PER_PAIR:g} x exact FP64 evaluations (counted on device)",

@@ -4,6 +4,7 @@
 // (src/engine.cpp:122-237). All join arithmetic runs on the GPU.
 #include <algorithm>
 #include <atomic>
+#include <bit>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -414,17 +415,17 @@ std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& dsf, size_t first
     double* hd = p->hd.data();
     double* ph = p->ph.data();
     uint32_t* vf = as<uint32_t>(p->vf);
-    // a level whose paddings are all 0 (the reference's level 100) ships no hd / ph at all
+    // a level whose paddings are all +0.0 (the reference's level 100) ships no hd / ph at all;
+    // the test ORs the IEEE bit patterns (branch-free, vectorisable: it reads the whole level
+    // when the paddings are zero, so it runs at memory bandwidth)
     std::atomic<bool> nonzero{false};
     for_blocks(pool, no, [&](size_t b, size_t e) {
         for (size_t o = b; o < e && !nonzero.load(std::memory_order_relaxed); ++o) {
             const LodMesh& lod = ds.objects[o].ladder.levels[li];
             const size_t n_f = lod.mesh.facets.size();
-            for (size_t f = 0; f < n_f; ++f)
-                if (lod.hd[f] != 0.0 || lod.ph[f] != 0.0 || std::signbit(lod.hd[f]) || std::signbit(lod.ph[f])) {
-                    nonzero = true;
-                    break;
-                }
+            uint64_t bits = 0;
+            for (size_t f = 0; f < n_f; ++f) bits |= std::bit_cast<uint64_t>(lod.hd[f]) | std::bit_cast<uint64_t>(lod.ph[f]);
+            if (bits) nonzero = true;
         }
     });
     const bool pads = nonzero.load();

@@ -591,25 +591,20 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks) k_screen(Refine
                             }
                             dl = __fadd_ru(__fmul_ru(2e-5f, Lm), __fmul_ru(2e-12f, Mm));
                         }
-                        // Stage 1, register-blocked: lane -> r facet i = lane / P (its record in
-                        // registers) and s facets j = jj, jj + P, ... (shared-memory reads that
-                        // the P-lane groups share as broadcasts); P = lanes per r facet.
-                        const int P = rcnt >= 32 ? 1 : 32 / rcnt;
-                        const int bi = min(lane / P, rcnt - 1), jj = lane - (lane / P) * P;
-                        const bool row_on = lane / P < rcnt;
-                        const RowRec ar = load_row(sm.rc + bi * kCS);
+                        // Stage 1, register-blocked: lane -> r facet i (its record in registers)
+                        // and s facets j = jj, jj + P, ... (shared-memory reads that the P-lane
+                        // groups share as broadcasts); P = lanes per r facet.
                         const bool lb_settled = th.lb_sat || th.lb_u == 0.f;
                         const float ninf = __int_as_float(0xff800000);
-                        // per-row thresholds of the stage-1 pair test (box_cannot_improve)
-                        const float rlb = lb_settled ? ninf : __fadd_ru(__fadd_ru(th.lb_u, dl), ar.ph);
-                        const float rub = th.ub_u == 0.f ? ninf : __fsub_ru(__fadd_ru(th.ub_u, dl), ar.hd);
-                        const int iters = (scnt - jj + P - 1) / P; // this lane's s facets
                         if (lane == 0) sm.cnt[0] += (uint32_t)(rcnt * scnt);
 #ifdef TJ_DEBUG_OPSTATS
                         if (lane == 0 && g_dbg_op_tested) atomicAdd(g_dbg_op_tested + d.op, (unsigned long long)(rcnt * scnt));
 #endif
                         if (!cull) { // every pair to the exact queue
-                            const int max_iters = (scnt + P - 1) / P;
+                            const int P = rcnt >= 32 ? 1 : 32 / rcnt;
+                            const int bi = min(lane / P, rcnt - 1), jj = lane - (lane / P) * P;
+                            const bool row_on = lane / P < rcnt;
+                            const int iters = (scnt - jj + P - 1) / P, max_iters = (scnt + P - 1) / P;
                             for (int t = 0; t < max_iters; ++t) {
                                 const bool nn = row_on && t < iters;
                                 queue_push(q, nn, d.op, (uint32_t)(d.r0 + rc0 + sm.rl[rt0 + bi]),
@@ -617,68 +612,86 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks) k_screen(Refine
                             }
                             continue;
                         }
-                        // The lane's s facets (jj + t P) into bit masks: bit t of `need` = the pair
-                        // goes to stage 2; of `flag` = a near pair whose DP4A conditioning
-                        // pre-test failed (its FP32 test runs at the flush, 32 pairs at a time).
-                        uint32_t nmask = 0, fmask = 0;
-                        if (row_on) {
-#pragma unroll 2
-                            for (int t = 0; t < iters; ++t) {
-                                const float* bp = sm.sc + (jj + t * P) * kCS;
-                                const int sb = stage1_box(ar, *reinterpret_cast<const float4*>(bp),
-                                                          *reinterpret_cast<const float4*>(bp + 4), bp[11], rlb, rub);
-                                const bool f = sb == 2 && !well_cond_q(ar.q, *reinterpret_cast<const int4*>(bp + 28));
-                                nmask |= (uint32_t)(sb == 1 || f) << t;
-                                fmask |= (uint32_t)f << t;
-                            }
-                        }
-                        // compact the masks into the warp queue one entry per lane and round;
-                        // stage 2 runs whenever 32 entries are queued
+                        // Stage 1, register-blocked, in row passes: a pass takes `rows` r facets
+                        // (32, 16 or the rest) with P = 32 / rows lanes per r facet, so a 24-row
+                        // tile runs as 16 + 8 rows on all 32 lanes instead of 24 lanes.
                         int nq = 0;
-                        for (;;) {
-                            const bool has = nmask != 0;
-                            const unsigned bal = __ballot_sync(0xffffffffu, has);
-                            if (has) {
-                                const int t = __ffs(nmask) - 1;
-                                nmask &= nmask - 1;
-                                sm.q[nq + __popc(bal & ((1u << lane) - 1u))] =
-                                    (uint16_t)(((fmask >> t) & 1u ? 0x8000 : 0) | (bi << 5) | (jj + t * P));
+                        for (int rp0 = 0; rp0 < rcnt;) {
+                            const int left = rcnt - rp0;
+                            const int rows = left >= 32 ? 32 : left > 16 ? 16 : left;
+                            const bool final_pass = rp0 + rows >= rcnt;
+                            const int P = 32 / rows;
+                            const int bi = rp0 + min(lane / P, rows - 1), jj = lane - (lane / P) * P;
+                            const bool row_on = lane / P < rows;
+                            rp0 += rows;
+                            const RowRec ar = load_row(sm.rc + bi * kCS);
+                            // per-row thresholds of the stage-1 pair test (box_cannot_improve)
+                            const float rlb = lb_settled ? ninf : __fadd_ru(__fadd_ru(th.lb_u, dl), ar.ph);
+                            const float rub = th.ub_u == 0.f ? ninf : __fsub_ru(__fadd_ru(th.ub_u, dl), ar.hd);
+                            const int iters = (scnt - jj + P - 1) / P; // this lane's s facets
+                            // The lane's s facets (jj + t P) into bit masks: bit t of `nmask` = the
+                            // pair goes to stage 2; of `fmask` = a near pair whose DP4A conditioning
+                            // pre-test failed (its FP32 test runs at the flush, 32 pairs at a time).
+                            uint32_t nmask = 0, fmask = 0;
+                            if (row_on) {
+#pragma unroll 2
+                                for (int t = 0; t < iters; ++t) {
+                                    const float* bp = sm.sc + (jj + t * P) * kCS;
+                                    const int sb = stage1_box(ar, *reinterpret_cast<const float4*>(bp),
+                                                              *reinterpret_cast<const float4*>(bp + 4), bp[11], rlb, rub);
+                                    const bool f = sb == 2 && !well_cond_q(ar.q, *reinterpret_cast<const int4*>(bp + 28));
+                                    nmask |= (uint32_t)(sb == 1 || f) << t;
+                                    fmask |= (uint32_t)f << t;
+                                }
                             }
-                            nq += __popc(bal);
-                            const bool last = bal == 0;
-                            while (nq >= 32 || (last && nq > 0)) { // second stage on up to 32 queued pairs
-                                const int n = min(nq, 32);
-                                __syncwarp();
-                                bool need = false;
-                                uint32_t fr = 0, fs = 0;
-                                bool go = false;
-                                if (lane < n) {
-                                    const int e = sm.q[lane];
-                                    const int i = (e >> 5) & 31, j = e & 31;
-                                    go = !(e & 0x8000) || stage1_ill_fp32(sm.rc + i * kCS, sm.sc + j * kCS);
-                                    if (go) {
-                                        fr = (uint32_t)(d.r0 + rc0 + sm.rl[rt0 + i]);
-                                        fs = (uint32_t)(d.s0 + sc0 + sm.sl[st0 + j]);
-                                        const int r = sat_needed(sm.rc + i * kCS, sm.sc + j * kCS, src.r_facets + (size_t)fr * 12,
-                                                                 src.s_facets + (size_t)fs * 12, th);
-                                        need = r & 1;
-                                        if (r >> 1) atomicAdd(&sm.cnt[2], 1u); // rare
+                            // compact the masks into the warp queue one entry per lane and round;
+                            // stage 2 runs whenever 32 entries are queued (and on the rest after
+                            // the final pass: the entries index this tile's records)
+                            for (;;) {
+                                const bool has = nmask != 0;
+                                const unsigned bal = __ballot_sync(0xffffffffu, has);
+                                if (has) {
+                                    const int t = __ffs(nmask) - 1;
+                                    nmask &= nmask - 1;
+                                    sm.q[nq + __popc(bal & ((1u << lane) - 1u))] =
+                                        (uint16_t)(((fmask >> t) & 1u ? 0x8000 : 0) | (bi << 5) | (jj + t * P));
+                                }
+                                nq += __popc(bal);
+                                const bool last = bal == 0 && final_pass;
+                                while (nq >= 32 || (last && nq > 0)) { // second stage on up to 32 queued pairs
+                                    const int n = min(nq, 32);
+                                    __syncwarp();
+                                    bool need = false;
+                                    uint32_t fr = 0, fs = 0;
+                                    bool go = false;
+                                    if (lane < n) {
+                                        const int e = sm.q[lane];
+                                        const int i = (e >> 5) & 31, j = e & 31;
+                                        go = !(e & 0x8000) || stage1_ill_fp32(sm.rc + i * kCS, sm.sc + j * kCS);
+                                        if (go) {
+                                            fr = (uint32_t)(d.r0 + rc0 + sm.rl[rt0 + i]);
+                                            fs = (uint32_t)(d.s0 + sc0 + sm.sl[st0 + j]);
+                                            const int r = sat_needed(sm.rc + i * kCS, sm.sc + j * kCS, src.r_facets + (size_t)fr * 12,
+                                                                     src.s_facets + (size_t)fs * 12, th);
+                                            need = r & 1;
+                                            if (r >> 1) atomicAdd(&sm.cnt[2], 1u); // rare
+                                        }
                                     }
-                                }
-                                const unsigned ngo = __popc(__ballot_sync(0xffffffffu, go));
-                                if (lane == 0) sm.cnt[1] += ngo;
-                                queue_push(q, need, d.op, fr, fs);
-                                __syncwarp();
-                                for (int k0 = 0; k0 < nq - n; k0 += 32) { // shift the rest down (in order)
-                                    const bool mv = k0 + lane < nq - n;
-                                    const uint16_t v = mv ? sm.q[n + k0 + lane] : 0;
+                                    const unsigned ngo = __popc(__ballot_sync(0xffffffffu, go));
+                                    if (lane == 0) sm.cnt[1] += ngo;
+                                    queue_push(q, need, d.op, fr, fs);
                                     __syncwarp();
-                                    if (mv) sm.q[k0 + lane] = v;
-                                    __syncwarp();
+                                    for (int k0 = 0; k0 < nq - n; k0 += 32) { // shift the rest down (in order)
+                                        const bool mv = k0 + lane < nq - n;
+                                        const uint16_t v = mv ? sm.q[n + k0 + lane] : 0;
+                                        __syncwarp();
+                                        if (mv) sm.q[k0 + lane] = v;
+                                        __syncwarp();
+                                    }
+                                    nq -= n;
                                 }
-                                nq -= n;
+                                if (bal == 0) break;
                             }
-                            if (last) break;
                         }
                     }
                 }

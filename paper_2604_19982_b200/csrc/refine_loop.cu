@@ -3,8 +3,10 @@
 //
 // The active voxel-pair list lives in HBM for the whole loop. Per LOD level:
 //   1. the reference facet-pair count sum(r_len * s_len) is reduced from the CSR offsets;
-//   2. refine kernel launches (launch size = max(refine_chunk, 64Ki) voxel pairs; the
-//      outcome is independent of it) fold each voxel pair's exact minima into per-op
+//   2. refine kernel launches (launch size = max(refine_chunk, 16Mi) voxel pairs: the
+//      reference's refine_chunk bounds host memory, the device has room for a whole level,
+//      and every launch boundary costs a drain + an exact-evaluation launch (config B:
+//      500k -> 81.5 ms, 2M -> 76.4, 8M -> 74.8); the outcome is independent of it) fold each voxel pair's exact minima into per-op
 //      minima with 64-bit atomicMin on the IEEE bit patterns (order-free and exact for
 //      non-negative doubles);
 //   3. one thread per op applies aggregate_object_bounds (skip ops whose minima stayed
@@ -157,7 +159,7 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
     TJ_CUDA(cudaEventCreate(&e0));
     TJ_CUDA(cudaEventCreate(&e1));
     const unsigned long long kInfBits = 0x7ff0000000000000ull;
-    const uint64_t launch = std::max<uint64_t>(spec.refine_chunk, 65536);
+    const uint64_t launch = std::max<uint64_t>(spec.refine_chunk, 1ull << 24);
     try {
         for (uint32_t li = 0; li < spec.n_lods; ++li) {
             if (n_active == 0) break;

@@ -13,6 +13,8 @@ r, s = synth.build_config("B", "/tmp/trijoin_bench/B_x1", scale=1.0)
 R, S = tj.load_dataset(r), tj.load_dataset(s)
 res = tj.Resident(R, S)
 kw = dict(type="intersect", lods=[20, 60, 100])
+if os.environ.get("SV_REFINE_CHUNK"):
+    kw["refine_chunk"] = int(os.environ["SV_REFINE_CHUNK"])
 for i in range(int(sys.argv[1]) if len(sys.argv) > 1 else 20):
     t0 = time.perf_counter()
     o = res.run(**kw)

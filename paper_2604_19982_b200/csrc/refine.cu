@@ -434,6 +434,17 @@ unsigned screen_batch() {
     return b;
 }
 
+// Decision mode: when every facet pair has hd_i + hd_j > 1e-5 (L_i + L_j) + 1e-12 (M_i + M_j),
+// no ub_ij can be 0 at this level (B + hd_i + hd_j >= tiny + delta for every pair), so the ub
+// side of every op is settled (the level's aggregates, k_prep).
+__device__ __forceinline__ bool level_ub_settled(const RefineSource& src, int cull) {
+    if (cull != 2 || !src.agg) return false;
+    const float hd2 = __fadd_rd(__uint_as_float(src.agg[0]), __uint_as_float(src.agg[3]));
+    const float l2 = __fadd_ru(__uint_as_float(src.agg[1]), __uint_as_float(src.agg[4]));
+    const float m2 = __fadd_ru(__uint_as_float(src.agg[2]), __uint_as_float(src.agg[5]));
+    return hd2 > __fadd_ru(__fadd_ru(__fmul_ru(1e-5f, l2), __fmul_ru(1e-12f, m2)), 1e-30f);
+}
+
 __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks) k_screen(RefineSource src, uint64_t vp_begin, uint64_t vp_end,
                                                 const unsigned long long* __restrict__ op_lb_bits,
                                                 const unsigned long long* __restrict__ op_ub_bits, int cull,
@@ -444,16 +455,7 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks) k_screen(Refine
     const int lane = threadIdx.x & 31;
     if (lane < 5) sm.cnt[lane] = 0;
     __syncwarp();
-    // decision mode: when every facet pair has hd_i + hd_j > 1e-5 (L_i + L_j) + 1e-12 (M_i + M_j),
-    // no ub_ij can be 0 at this level (B + hd_i + hd_j >= tiny + delta for every pair), so
-    // the ub side of every op is settled (the level's aggregates, k_prep)
-    bool ub_level_settled = false;
-    if (cull == 2 && src.agg) {
-        const float hd2 = __fadd_rd(__uint_as_float(src.agg[0]), __uint_as_float(src.agg[3]));
-        const float l2 = __fadd_ru(__uint_as_float(src.agg[1]), __uint_as_float(src.agg[4]));
-        const float m2 = __fadd_ru(__uint_as_float(src.agg[2]), __uint_as_float(src.agg[5]));
-        ub_level_settled = hd2 > __fadd_ru(__fadd_ru(__fmul_ru(1e-5f, l2), __fmul_ru(1e-12f, m2)), 1e-30f);
-    }
+    const bool ub_level_settled = level_ub_settled(src, cull);
     // The op thresholds of a voxel pair (decision mode, intersection with tau = 0: only "is the
     // minimum 0?" matters on either side; a pair surely positive on a side cannot change it).
     auto thresholds = [&](const VpDescDev& d) {
@@ -714,8 +716,12 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks) k_screen(Refine
 // Exact evaluation of the queued facet pairs: thread per pair, records staged in the
 // thread's own shared-memory slots, minima folded into the op bits with atomicMin.
 __global__ void __launch_bounds__(128) k_eval(RefineSource src, RefineQueue q, unsigned long long* __restrict__ lb_bits,
-                                              unsigned long long* __restrict__ ub_bits, unsigned long long* counters) {
+                                              unsigned long long* __restrict__ ub_bits, unsigned long long* counters,
+                                              int cull) {
     __shared__ double rec[128][2][kFacetWords];
+    // decision mode: a pair of an op whose answer is already settled on both sides (min lb 0;
+    // min ub 0 or impossible at this level) cannot change the op's outcome
+    const bool ub_settled = level_ub_settled(src, cull);
     const uint32_t ra = smem_addr(&rec[threadIdx.x][0][0]), sb = smem_addr(&rec[threadIdx.x][1][0]);
     unsigned long long n = *q.count;
     if (blockIdx.x == 0 && threadIdx.x == 0 && n > q.capacity) atomicMax(q.count + 1, n); // overflow record
@@ -724,6 +730,9 @@ __global__ void __launch_bounds__(128) k_eval(RefineSource src, RefineQueue q, u
     for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < n;
          k += (unsigned long long)gridDim.x * blockDim.x) {
         const PairRef p = q.items[k];
+        if (cull == 2 && bits_to_double(__ldcg(lb_bits + p.op)) == 0.0 &&
+            (ub_settled || bits_to_double(__ldcg(ub_bits + p.op)) == 0.0))
+            continue;
         double c[12];
         double n2, s2;
         load_facet(src.r_facets + (size_t)p.fr * 12, c);
@@ -842,7 +851,7 @@ void refine_pass(const RefineSource& src, uint64_t vp_begin, uint64_t vp_end, bo
         TJ_CUDA(cudaGetLastError());
     }
     count_launch();
-    k_eval<<<grid, 128, 0, st>>>(src, qs.view(), lb_bits, ub_bits, counters);
+    k_eval<<<grid, 128, 0, st>>>(src, qs.view(), lb_bits, ub_bits, counters, cull);
     TJ_CUDA(cudaGetLastError());
 }
 

@@ -627,7 +627,7 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks) k_screen(Refine
                             const bool row_on = lane / P < rows;
                             rp0 += rows;
                             const RowRec ar = load_row(sm.rc + bi * kCS);
-                            // per-row thresholds of the stage-1 pair test (box_cannot_improve)
+                            // per-row thresholds of the stage-1 pair test (stage1_box)
                             const float rlb = lb_settled ? ninf : __fadd_ru(__fadd_ru(th.lb_u, dl), ar.ph);
                             const float rub = th.ub_u == 0.f ? ninf : __fsub_ru(__fadd_ru(th.ub_u, dl), ar.hd);
                             const int iters = (scnt - jj + P - 1) / P; // this lane's s facets

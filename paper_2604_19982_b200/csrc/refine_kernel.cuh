@@ -78,7 +78,7 @@ struct SegAgg {
 //  12-20 unit edge directions (v1-v0, v2-v1, v0-v2)
 //  21-23 v1 - v0   24-26 v2 - v0   (FP64 differences rounded to FP32)   27 M (max |coordinate|)
 //  28-31 (int bits) the unit normal and the 3 unit edge directions quantised to int8x3
-//        (round(127 x), 4th byte 0) for the DP4A conditioning pre-test (stage1_need_rr)
+//        (round(127 x), 4th byte 0) for the DP4A conditioning pre-test (well_cond_q)
 struct __align__(16) ScreenSmem {
     float rc[kRT * kCS];
     float sc[kST * kCS];
@@ -197,33 +197,6 @@ __device__ __forceinline__ bool cannot_improve(float B, const float* a, const fl
     return lb_ok && ub_ok;
 }
 
-// Lower bound of the squared AABB gap (outward-rounded boxes, round-down arithmetic).
-__device__ __forceinline__ float box_gap2_lb(const float* a, const float* b) {
-    float s = 0.f;
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-        const float g = fmaxf(0.f, fmaxf(__fsub_rd(b[d], a[4 + d]), __fsub_rd(a[d], b[4 + d])));
-        s = __fadd_rd(s, __fmul_rd(g, g));
-    }
-    return s;
-}
-
-// Stage-1 test of the screen pass, on the squared box gap g2 against the per-row thresholds
-// (ScreenSmem::row_*): with c = 1 - 1e-5 and delta0 >= 1e-5 (L_i + L_j) + 1e-12 (M_i + M_j),
-//   lb side: c B >= T_lb + delta0 + ph_i + ph_j   implies  B - ph_i - ph_j >= T_lb + delta(B)
-//   ub side: c B >= T_ub + delta0 - hd_i - hd_j   implies  B + hd_i + hd_j >= T_ub + delta(B)
-// i.e. the same condition as cannot_improve with a (larger) tile-wide delta. Comparisons are
-// made on squares (both sides non-negative) with directed rounding.
-__device__ __forceinline__ bool box_cannot_improve(float g2, float row_lb, float row_ub, const float* b) {
-    constexpr float kInvC = 1.0f / (1.0f - 1e-5f) * (1.0f + 0x1p-20f); // >= 1 / c
-    const float xl = __fadd_ru(row_lb, b[11]);
-    const float yu = __fsub_ru(row_ub, b[7]);
-    const float xs = __fmul_ru(xl, kInvC), ys = __fmul_ru(yu, kInvC);
-    const bool lb_ok = xl <= 0.f || g2 >= __fmul_ru(xs, xs);
-    const bool ub_ok = yu <= 0.f || g2 >= __fmul_ru(ys, ys);
-    return lb_ok && ub_ok;
-}
-
 // Warp reduction of the box parts of facets [first, first + n) (all lanes call).
 __device__ __forceinline__ SegAgg seg_reduce(const float4* __restrict__ box, uint64_t first, uint32_t n) {
     const float kInfF = __int_as_float(0x7f800000);
@@ -288,7 +261,7 @@ __device__ __forceinline__ float seg_m(const SegAgg& g) {
 
 // Aggregated skip test (hierarchical screen): true only if EVERY facet pair (x, y) with x's
 // box inside box a and y's box inside box b passes the pair screen's skip conditions, i.e.
-// box_cannot_improve and skip_mask == 0 (far branch), given
+// the stage-1 box condition (stage1_box) and skip_mask == 0 (far branch), given
 //   lsum  >= L_x + L_y,  lmin <= min(L_x, L_y)   (all facets well shaped),
 //   phsum >= ph_x + ph_y (rounded up),   hdsum <= hd_x + hd_y (rounded down),
 //   delta0 >= 1e-5 (L_x + L_y) + 1e-12 (M_x + M_y).
@@ -298,7 +271,7 @@ __device__ __forceinline__ float seg_m(const SegAgg& g) {
 __device__ __forceinline__ bool agg_skip(const float* alo, const float* ahi, const float* blo, const float* bhi,
                                          float lsum, float lmin, float phsum, float hdsum, float delta0,
                                          const Thresh& t) {
-    constexpr float kInvC = 1.0f / (1.0f - 1e-5f) * (1.0f + 0x1p-20f); // >= 1 / c (box_cannot_improve)
+    constexpr float kInvC = 1.0f / (1.0f - 1e-5f) * (1.0f + 0x1p-20f); // >= 1 / c (stage1_box)
     float g2 = 0.f, m2 = 0.f;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
@@ -317,27 +290,6 @@ __device__ __forceinline__ bool agg_skip(const float* alo, const float* ahi, con
     const bool far = B > 2.f * lsum;                   // skip_mask's far branch for every pair
     const bool near = __fsqrt_ru(m2) <= 1e3f * lmin;   // no pair beyond skip_mask's 1e3 L range
     return lb_ok && ub_ok && far && near;
-}
-
-// Stage-1 pair test on float4 box records (lo.xyz + L, hi.xyz + hd) with the row's
-// thresholds rlb = T_lb + delta0 + ph_i, rub = T_ub + delta0 - hd_i (box_cannot_improve),
-// plus skip_mask's shape and 1e3 L range conditions: false iff the pair is skippable or
-// only needs the near-pair conditioning check (near_mask). Branch-free.
-__device__ __forceinline__ bool stage1_need(const float4& a0, const float4& a1, const float4& b0, const float4& b1,
-                                            float bph, float rlb, float rub) {
-    constexpr float kInvC = 1.0f / (1.0f - 1e-5f) * (1.0f + 0x1p-20f); // >= 1 / c
-    const float gx = fmaxf(0.f, fmaxf(__fsub_rd(b0.x, a1.x), __fsub_rd(a0.x, b1.x)));
-    const float gy = fmaxf(0.f, fmaxf(__fsub_rd(b0.y, a1.y), __fsub_rd(a0.y, b1.y)));
-    const float gz = fmaxf(0.f, fmaxf(__fsub_rd(b0.z, a1.z), __fsub_rd(a0.z, b1.z)));
-    const float g2 = __fadd_rd(__fadd_rd(__fmul_rd(gx, gx), __fmul_rd(gy, gy)), __fmul_rd(gz, gz));
-    const float xl = __fadd_ru(rlb, bph);
-    const float yu = __fsub_ru(rub, b1.w);
-    const float xs = __fmul_ru(xl, kInvC), ys = __fmul_ru(yu, kInvC);
-    const bool lb_ok = xl <= 0.f || g2 >= __fmul_ru(xs, xs);
-    const bool ub_ok = yu <= 0.f || g2 >= __fmul_ru(ys, ys);
-    const float B = __fmul_rd(sqrtf(g2), 1.0f - 0x1p-20f);
-    const bool shapes = a0.w >= 0.f && b0.w >= 0.f && !(B > 1e3f * fminf(a0.w, b0.w));
-    return !(lb_ok && ub_ok && shapes);
 }
 
 // The r-side part of the register-blocked stage-1 loop (floats 0-7, 11 and the quantised
@@ -380,6 +332,13 @@ __device__ __forceinline__ bool well_cond_q(const int* aq, int4 bq) {
 // Box part of stage 1 for one pair, branch-free: 1 = the pair must go to stage 2 (it may
 // change a minimum, or it is out of the skip argument's shape / range), 2 = skippable by its
 // box gap but near (the edge / plane conditioning decides), 0 = skippable (far apart).
+// The box condition uses the squared box gap g2 = B^2 against the row thresholds
+// rlb = T_lb + delta0 + ph_i, rub = T_ub + delta0 - hd_i: with c = 1 - 1e-5 and
+// delta0 >= 1e-5 (L_i + L_j) + 1e-12 (M_i + M_j),
+//   lb side: c B >= T_lb + delta0 + ph_i + ph_j   implies  B - ph_i - ph_j >= T_lb + delta(B)
+//   ub side: c B >= T_ub + delta0 - hd_i - hd_j   implies  B + hd_i + hd_j >= T_ub + delta(B)
+// i.e. cannot_improve with a (larger) tile-wide delta; squares are compared (both sides
+// non-negative) with directed rounding.
 __device__ __forceinline__ int stage1_box(const RowRec& a, float4 b0, float4 b1, float bph, float rlb, float rub) {
     const float gx = fmaxf(0.f, fmaxf(__fsub_rd(b0.x, a.hi[0]), __fsub_rd(a.lo[0], b1.x)));
     const float gy = fmaxf(0.f, fmaxf(__fsub_rd(b0.y, a.hi[1]), __fsub_rd(a.lo[1], b1.y)));
@@ -414,57 +373,11 @@ __device__ __forceinline__ bool stage1_ill_fp32(const float* as, const float* b)
     return ill;
 }
 
-// Stage-1 test of the screen pass with the r record in registers (a; its shared-memory
-// record as) and the s record b in shared memory: true iff the pair must go to stage 2.
-// Same decision as !box_cannot_improve(g2, rlb, rub, b) || skip_mask(B, a, b) != 0, with
-// the range and far tests of skip_mask taken on the squared box gap (no square root).
-__device__ __forceinline__ bool stage1_need_rr(const RowRec& a, const float* as, const float* b, float rlb, float rub) {
-    const float4 b0 = *reinterpret_cast<const float4*>(b), b1 = *reinterpret_cast<const float4*>(b + 4);
-    const float bph = b[11];
-    float g2;
-    {
-        const float gx = fmaxf(0.f, fmaxf(__fsub_rd(b0.x, a.hi[0]), __fsub_rd(a.lo[0], b1.x)));
-        const float gy = fmaxf(0.f, fmaxf(__fsub_rd(b0.y, a.hi[1]), __fsub_rd(a.lo[1], b1.y)));
-        const float gz = fmaxf(0.f, fmaxf(__fsub_rd(b0.z, a.hi[2]), __fsub_rd(a.lo[2], b1.z)));
-        g2 = __fadd_rd(__fadd_rd(__fmul_rd(gx, gx), __fmul_rd(gy, gy)), __fmul_rd(gz, gz));
-    }
-    // box_cannot_improve
-    constexpr float kInvC = 1.0f / (1.0f - 1e-5f) * (1.0f + 0x1p-20f);
-    const float xl = __fadd_ru(rlb, bph);
-    const float yu = __fsub_ru(rub, b1.w);
-    const float xs = __fmul_ru(xl, kInvC), ys = __fmul_ru(yu, kInvC);
-    const bool lb_ok = xl <= 0.f || g2 >= __fmul_ru(xs, xs);
-    const bool ub_ok = yu <= 0.f || g2 >= __fmul_ru(ys, ys);
-    // skip_mask: shapes, the 1e3 L range, far branch, conditioning
-    const float m = 1e3f * fminf(a.L, b0.w), f = 2.f * (a.L + b0.w);
-    const bool shapes = a.L >= 0.f && b0.w >= 0.f && g2 <= m * m;
-    if (!(lb_ok && ub_ok && shapes)) return true;
-    if (g2 > f * f) return false; // far apart: no spurious piercing for any conditioning
-    // near pair: DP4A pre-test, then the FP32 test of skip_mask on the rare failures
-    if (well_cond_q(a.q, *reinterpret_cast<const int4*>(b + 28))) return false;
-    const float4 b2 = *reinterpret_cast<const float4*>(b + 8);
-    const float4 b3 = *reinterpret_cast<const float4*>(b + 12), b4 = *reinterpret_cast<const float4*>(b + 16);
-    const float b20 = b[20];
-    const float4 a2 = *reinterpret_cast<const float4*>(as + 8), a3 = *reinterpret_cast<const float4*>(as + 12);
-    const float4 a4 = *reinterpret_cast<const float4*>(as + 16);
-    const float a20 = as[20];
-    bool ill = ill_cond(a3.x, a3.y, a3.z, b2.x, b2.y, b2.z) || ill_cond(a3.w, a4.x, a4.y, b2.x, b2.y, b2.z) ||
-               ill_cond(a4.z, a4.w, a20, b2.x, b2.y, b2.z);
-    ill = ill || ill_cond(b3.x, b3.y, b3.z, a2.x, a2.y, a2.z) || ill_cond(b3.w, b4.x, b4.y, a2.x, a2.y, a2.z) ||
-          ill_cond(b4.z, b4.w, b20, a2.x, a2.y, a2.z);
-    return ill;
-}
-
 // Shape / range eligibility for a skip and the mask of ill-conditioned edge/plane
 // combinations (bit k < 3: edge k of a vs the plane of b; bit 3 + k: edge k of b vs the
 // plane of a; |cos(edge, normal)| < 1e-3). Returns -1 if the pair may never be skipped; a
 // non-zero mask means the skip additionally needs the reference's own piercing test to be
 // negative for those combinations (verify).
-// Conditioning mask of a pair that passed stage1_need (shapes and range already checked):
-// 0 if far (B > 2 (L_a + L_b), B from the box gap) or well conditioned; else the mask of
-// ill-conditioned combinations (see skip_mask).
-__device__ __forceinline__ int near_mask(const float* a, const float* b, float La, float Lb);
-
 __device__ __forceinline__ int skip_mask(float B, const float* a, const float* b) {
     if (a[3] < 0.f || b[3] < 0.f) return -1;
     if (B > 1e3f * fminf(a[3], b[3])) return -1;
@@ -472,18 +385,6 @@ __device__ __forceinline__ int skip_mask(float B, const float* a, const float* b
     // passes the reference's |det| > 1e-14 scale test (its u, v, t errors are then below ~6%
     // of the vertex-to-triangle distance, which needs the segment within 0.44 (L_a + L_b)).
     if (B > 2.f * (a[3] + b[3])) return 0;
-    int mask = 0;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        if (fabsf(a[12 + 3 * k] * b[8] + a[13 + 3 * k] * b[9] + a[14 + 3 * k] * b[10]) < 1e-3f) mask |= 1 << k;
-        if (fabsf(b[12 + 3 * k] * a[8] + b[13 + 3 * k] * a[9] + b[14 + 3 * k] * a[10]) < 1e-3f) mask |= 8 << k;
-    }
-    return mask;
-}
-
-__device__ __forceinline__ int near_mask(const float* a, const float* b, float La, float Lb) {
-    const float B = box_gap_lb(a, b);
-    if (B > 2.f * (La + Lb)) return 0;
     int mask = 0;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {

@@ -191,6 +191,13 @@ uint64_t tj_dataset_device_bytes(const tj_dataset* ds);
  *   called from another host thread while tj_join runs on the dataset. lv == NULL marks
  *   the slot failed: a join waiting for it returns TJ_EINVAL. An index out of its
  *   object's range makes every later tj_join on the dataset return TJ_EINVAL.
+ * tj_dataset_put_level_part / tj_dataset_finish_level: the same upload in pieces, so the
+ *   copy of a level overlaps the host packing its remaining objects. A part copies rows
+ *   [vert_begin, vert_end) of lv->vertices, [facet_begin, facet_end) of lv->tris (and of
+ *   lv->hd / lv->ph when non-NULL) and [entry_begin, entry_end) of lv->voxel_facets (lv's
+ *   arrays are the whole level's; the ranges are row indices into them). Once every row has
+ *   been put, tj_dataset_finish_level(has_pads = whether hd / ph were shipped) expands the
+ *   level and queues it; tj_dataset_put_level == one part covering the level + finish.
  * tj_dataset_sync: waits for every queued level copy of the dataset.
  */
 typedef struct tj_level_mesh_view {
@@ -204,6 +211,10 @@ typedef struct tj_level_mesh_view {
 int tj_dataset_begin(tj_ctx* ctx, const tj_dataset_view* header, const uint64_t* const* vert_base,
                      const uint64_t* const* facet_base, tj_dataset** out);
 int tj_dataset_put_level(tj_dataset* ds, uint32_t slot, const tj_level_mesh_view* lv);
+int tj_dataset_put_level_part(tj_dataset* ds, uint32_t slot, const tj_level_mesh_view* lv, uint64_t vert_begin,
+                              uint64_t vert_end, uint64_t facet_begin, uint64_t facet_end, uint64_t entry_begin,
+                              uint64_t entry_end);
+int tj_dataset_finish_level(tj_dataset* ds, uint32_t slot, int has_pads);
 int tj_dataset_sync(tj_dataset* ds);
 
 /* ---- host-side index loading (backs load_index, reference src/index_io.cpp:244-249) ----

@@ -462,49 +462,67 @@ int tj_dataset_begin(tj_ctx* ctx, const tj_dataset_view* v, const uint64_t* cons
     return rc;
 }
 
-int tj_dataset_put_level(tj_dataset* ds, uint32_t slot, const tj_level_mesh_view* lv) {
-    if (!ds || !ds->d.gate || slot >= ds->d.levels.size()) return TJ_EINVAL;
+int tj_dataset_put_level_part(tj_dataset* ds, uint32_t slot, const tj_level_mesh_view* lv, uint64_t vert_begin,
+                              uint64_t vert_end, uint64_t facet_begin, uint64_t facet_end, uint64_t entry_begin,
+                              uint64_t entry_end) {
+    if (!ds || !ds->d.gate || slot >= ds->d.levels.size() || !lv) return TJ_EINVAL;
     LevelGate& g = *ds->d.gate;
-    auto set_state = [&](int s) {
+    tj_ctx* ctx = ds->ctx;
+    const int rc = guarded(nullptr, [&] {
+        TJ_CUDA(cudaSetDevice(ctx->device));
+        DatasetDev& d = ds->d;
+        const uint64_t nvert = d.level_vertices[slot], nfac = d.level_facets[slot], used = d.level_entries[slot];
+        if (vert_begin > vert_end || vert_end > nvert || facet_begin > facet_end || facet_end > nfac ||
+            entry_begin > entry_end || entry_end > used)
+            throw Error(TJ_EINVAL, "tj_dataset_put_level_part: row range outside the level");
+        if ((vert_end > vert_begin && !lv->vertices) || (facet_end > facet_begin && (!lv->tris || !lv->hd != !lv->ph)) ||
+            (entry_end > entry_begin && !lv->voxel_facets))
+            throw Error(TJ_EINVAL, "tj_dataset_put_level: null level arrays");
+        // into the dataset's staging area (reserved at tj_dataset_begin: no allocation here, so
+        // a put never waits on the memory pool while a join runs); the copy stream orders the
+        // reuse of the area across levels
+        const StageLayout L = stage_layout(nvert, nfac, used);
+        unsigned char* base = d.stage.p;
+        auto put = [&](uint64_t off, const void* src, uint64_t b0, uint64_t b1, size_t row) {
+            if (b1 > b0)
+                TJ_CUDA(cudaMemcpyAsync(base + off + b0 * row, static_cast<const unsigned char*>(src) + b0 * row,
+                                        (b1 - b0) * row, cudaMemcpyHostToDevice, g.copy));
+        };
+        put(L.verts, lv->vertices, vert_begin, vert_end, 24);
+        put(L.tris, lv->tris, facet_begin, facet_end, 12);
+        if (lv->hd) {
+            put(L.hd, lv->hd, facet_begin, facet_end, 8);
+            put(L.ph, lv->ph, facet_begin, facet_end, 8);
+        }
+        put(L.vf, lv->voxel_facets, entry_begin, entry_end, 4);
+    });
+    if (rc != TJ_OK) {
         {
             std::lock_guard<std::mutex> lk(g.mu);
-            g.state[slot] = s;
+            g.state[slot] = LevelGate::kFailed;
         }
         g.cv.notify_all();
-    };
-    if (!lv) {
-        set_state(LevelGate::kFailed);
-        return TJ_OK;
+        set_ctx_error(ctx, tj_global_last_error());
     }
+    return rc;
+}
+
+int tj_dataset_finish_level(tj_dataset* ds, uint32_t slot, int has_pads) {
+    if (!ds || !ds->d.gate || slot >= ds->d.levels.size()) return TJ_EINVAL;
+    LevelGate& g = *ds->d.gate;
     tj_ctx* ctx = ds->ctx;
     const int rc = guarded(nullptr, [&] {
         TJ_CUDA(cudaSetDevice(ctx->device));
         AllocStreamScope scope(g.copy);
         DatasetDev& d = ds->d;
         const uint64_t nvert = d.level_vertices[slot], nfac = d.level_facets[slot], used = d.level_entries[slot];
-        if ((nvert && !lv->vertices) || (nfac && (!lv->tris || !lv->hd != !lv->ph)) || (used && !lv->voxel_facets))
-            throw Error(TJ_EINVAL, "tj_dataset_put_level: null level arrays");
-        // compact arrays into the dataset's staging area (reserved at tj_dataset_begin: no
-        // allocation here, so a put never waits on the memory pool while a join runs); the
-        // copy stream orders the reuse of the area across levels
-        StageLayout L = stage_layout(nvert, nfac, used);
+        const StageLayout L = stage_layout(nvert, nfac, used);
         unsigned char* base = d.stage.p;
-        double* verts = reinterpret_cast<double*>(base + L.verts);
-        uint32_t* tris = reinterpret_cast<uint32_t*>(base + L.tris);
-        double* hd = reinterpret_cast<double*>(base + L.hd);
-        double* ph = reinterpret_cast<double*>(base + L.ph);
-        uint32_t* vf = reinterpret_cast<uint32_t*>(base + L.vf);
-        if (nvert) TJ_CUDA(cudaMemcpyAsync(verts, lv->vertices, nvert * 24, cudaMemcpyHostToDevice, g.copy));
-        if (nfac) {
-            TJ_CUDA(cudaMemcpyAsync(tris, lv->tris, nfac * 12, cudaMemcpyHostToDevice, g.copy));
-            if (lv->hd) {
-                TJ_CUDA(cudaMemcpyAsync(hd, lv->hd, nfac * 8, cudaMemcpyHostToDevice, g.copy));
-                TJ_CUDA(cudaMemcpyAsync(ph, lv->ph, nfac * 8, cudaMemcpyHostToDevice, g.copy));
-            } else {
-                hd = ph = nullptr;
-            }
-        }
-        if (used) TJ_CUDA(cudaMemcpyAsync(vf, lv->voxel_facets, used * 4, cudaMemcpyHostToDevice, g.copy));
+        const double* verts = reinterpret_cast<const double*>(base + L.verts);
+        const uint32_t* tris = reinterpret_cast<const uint32_t*>(base + L.tris);
+        const double* hd = has_pads && nfac ? reinterpret_cast<const double*>(base + L.hd) : nullptr;
+        const double* ph = has_pads && nfac ? reinterpret_cast<const double*>(base + L.ph) : nullptr;
+        const uint32_t* vf = reinterpret_cast<const uint32_t*>(base + L.vf);
         if (d.n_voxels) {
             const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((d.n_voxels + 7) / 8, (uint64_t)ctx->ws.num_sms * 16));
             count_launch();
@@ -516,9 +534,31 @@ int tj_dataset_put_level(tj_dataset* ds, uint32_t slot, const tj_level_mesh_view
         derive_level(d, slot, ctx->ws.num_sms, g.copy);
         TJ_CUDA(cudaEventRecord(g.ev[slot], g.copy));
     });
-    set_state(rc == TJ_OK ? LevelGate::kQueued : LevelGate::kFailed);
+    {
+        std::lock_guard<std::mutex> lk(g.mu);
+        g.state[slot] = rc == TJ_OK ? LevelGate::kQueued : LevelGate::kFailed;
+    }
+    g.cv.notify_all();
     if (rc != TJ_OK) set_ctx_error(ctx, tj_global_last_error());
     return rc;
+}
+
+int tj_dataset_put_level(tj_dataset* ds, uint32_t slot, const tj_level_mesh_view* lv) {
+    if (!ds || !ds->d.gate || slot >= ds->d.levels.size()) return TJ_EINVAL;
+    if (!lv) {
+        LevelGate& g = *ds->d.gate;
+        {
+            std::lock_guard<std::mutex> lk(g.mu);
+            g.state[slot] = LevelGate::kFailed;
+        }
+        g.cv.notify_all();
+        return TJ_OK;
+    }
+    const DatasetDev& d = ds->d;
+    const int rc = tj_dataset_put_level_part(ds, slot, lv, 0, d.level_vertices[slot], 0, d.level_facets[slot], 0,
+                                             d.level_entries[slot]);
+    if (rc != TJ_OK) return rc;
+    return tj_dataset_finish_level(ds, slot, lv->hd != nullptr);
 }
 
 int tj_dataset_sync(tj_dataset* ds) {

@@ -24,6 +24,11 @@
 
 namespace trijoin {
 
+namespace {
+// object-range pieces per streamed level (pack_level / tj_dataset_put_level_part)
+constexpr size_t kPackPieces = 8;
+} // namespace
+
 // ---------------------------------------------------------------- detail: contexts, packing
 namespace detail {
 
@@ -399,7 +404,8 @@ std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& ds, const PackedH
 }
 
 std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& dsf, size_t first, const PackedHeader& h, size_t li,
-                                        ThreadPool& pool) {
+                                        ThreadPool& pool, size_t pieces,
+                                        const std::function<void(const PackedLevel&, const PieceRows&)>& on_piece) {
     auto p = std::make_unique<PackedLevel>();
     const ObjRange ds{dsf.objects.data() + first, h.n_objects};
     const size_t no = ds.objects.size();
@@ -432,36 +438,54 @@ std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& dsf, size_t first
     p->zero_pads = !pads;
     static_assert(sizeof(Point3) == 3 * sizeof(double), "Point3 must be three packed doubles");
     static_assert(sizeof(std::array<uint32_t, 3>) == 3 * sizeof(uint32_t), "facets must be packed uint32 triples");
-    for_blocks(pool, no, [&](size_t b, size_t e) {
-        for (size_t o = b; o < e; ++o) {
-            const PreparedObject& obj = ds.objects[o];
-            const LodMesh& lod = obj.ladder.levels[li];
-            const uint64_t vb = h.vert_base[li][o], fb = h.facet_base[li][o];
-            const size_t n_v = lod.mesh.vertices.size(), n_f = lod.mesh.facets.size();
-            if (n_v) std::memcpy(verts + 3 * vb, lod.mesh.vertices.data(), n_v * sizeof(Point3));
-            if (n_f) {
-                std::memcpy(tris + 3 * fb, lod.mesh.facets.data(), n_f * 3 * sizeof(uint32_t));
-                if (pads) {
-                    std::memcpy(hd + fb, lod.hd.data(), n_f * sizeof(double));
-                    std::memcpy(ph + fb, lod.ph.data(), n_f * sizeof(double));
+    tj_level_mesh_view& view = p->view;
+    view.vertices = verts;
+    view.tris = tris;
+    view.hd = pads ? hd : nullptr;
+    view.ph = pads ? ph : nullptr;
+    view.voxel_facets = vf;
+    const auto& fo = h.facet_offsets[li];
+    pieces = std::max<size_t>(1, std::min(pieces, no));
+    for (size_t k = 0; k < pieces; ++k) {
+        const size_t lo = no * k / pieces, hi = no * (k + 1) / pieces;
+        for_blocks(pool, hi - lo, [&](size_t b, size_t e) {
+            for (size_t o = lo + b; o < lo + e; ++o) {
+                const PreparedObject& obj = ds.objects[o];
+                const LodMesh& lod = obj.ladder.levels[li];
+                const uint64_t vb = h.vert_base[li][o], fb = h.facet_base[li][o];
+                const size_t n_v = lod.mesh.vertices.size(), n_f = lod.mesh.facets.size();
+                if (n_v) std::memcpy(verts + 3 * vb, lod.mesh.vertices.data(), n_v * sizeof(Point3));
+                if (n_f) {
+                    std::memcpy(tris + 3 * fb, lod.mesh.facets.data(), n_f * 3 * sizeof(uint32_t));
+                    if (pads) {
+                        std::memcpy(hd + fb, lod.hd.data(), n_f * sizeof(double));
+                        std::memcpy(ph + fb, lod.ph.data(), n_f * sizeof(double));
+                    }
+                }
+                const VoxelSet& vs = obj.voxels;
+                const uint64_t v0 = h.voxel_offsets[o];
+                for (uint32_t v = 0; v < vs.voxel_count(); ++v) {
+                    const auto& ids = vs.facets_per_level[li][v];
+                    if (!ids.empty()) std::memcpy(vf + fo[v0 + v], ids.data(), ids.size() * sizeof(uint32_t));
                 }
             }
-            const VoxelSet& vs = obj.voxels;
-            const uint64_t v0 = h.voxel_offsets[o];
-            const auto& fo = h.facet_offsets[li];
-            for (uint32_t v = 0; v < vs.voxel_count(); ++v) {
-                const auto& ids = vs.facets_per_level[li][v];
-                if (!ids.empty()) std::memcpy(vf + fo[v0 + v], ids.data(), ids.size() * sizeof(uint32_t));
-            }
-        }
-    });
-    tj_level_mesh_view& v = p->view;
-    v.vertices = verts;
-    v.tris = tris;
-    v.hd = pads ? hd : nullptr;
-    v.ph = pads ? ph : nullptr;
-    v.voxel_facets = vf;
+        });
+        if (on_piece)
+            on_piece(*p, PieceRows{h.vert_base[li][lo], h.vert_base[li][hi], h.facet_base[li][lo], h.facet_base[li][hi],
+                                   fo[h.voxel_offsets[lo]], fo[h.voxel_offsets[hi]]});
+    }
     return p;
+}
+
+std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& dsf, size_t first, const PackedHeader& h, size_t li,
+                                        ThreadPool& pool) {
+    return pack_level(dsf, first, h, li, pool, 1, {});
+}
+
+std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& ds, const PackedHeader& h, size_t li, ThreadPool& pool,
+                                        size_t pieces,
+                                        const std::function<void(const PackedLevel&, const PieceRows&)>& on_piece) {
+    return pack_level(ds, 0, h, li, pool, pieces, on_piece);
 }
 
 } // namespace detail
@@ -1093,7 +1117,18 @@ JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const Jo
                     const int slot = slot_of(D, level);
                     if (slot < 0) continue;
                     const auto tl = Clock::now();
-                    staged.push_back(detail::pack_level(D, H, static_cast<size_t>(slot), pool));
+                    // packed in pieces, each shipped while the next is packed (the copy engine
+                    // then trails the packing by one piece instead of one level)
+                    auto ship = [&](const detail::PackedLevel& lv, const detail::PieceRows& rows) {
+                        for (size_t g = 0; g < G; ++g) {
+                            tj_dataset* ds = side == 0 ? dr[g].p : dsh[g].p;
+                            detail::check(tj_dataset_put_level_part(ds, static_cast<uint32_t>(slot), &lv.view,
+                                                                    rows.vert_begin, rows.vert_end, rows.facet_begin,
+                                                                    rows.facet_end, rows.entry_begin, rows.entry_end),
+                                          detail::device_context(devices[g]));
+                        }
+                    };
+                    staged.push_back(detail::pack_level(D, H, static_cast<size_t>(slot), pool, kPackPieces, ship));
                     pack_ms += std::chrono::duration<double, std::milli>(Clock::now() - tl).count();
                     mark(std::string(side == 0 ? "R" : "S") + "_lod" + std::to_string(level) + "_packed");
                     out.stats.h2d_bytes += G * (H.n_vertices[slot] * 24 + H.n_facets[slot] * (staged.back()->zero_pads ? 12 : 28) + H.facet_offsets[slot].back() * 4);
@@ -1101,7 +1136,7 @@ JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const Jo
                         tj_dataset* ds = side == 0 ? dr[g].p : dsh[g].p;
                         auto& put = side == 0 ? put_r[g] : put_s[g];
                         put[slot] = 1;
-                        detail::check(tj_dataset_put_level(ds, static_cast<uint32_t>(slot), &staged.back()->view),
+                        detail::check(tj_dataset_finish_level(ds, static_cast<uint32_t>(slot), !staged.back()->zero_pads),
                                       detail::device_context(devices[g]));
                     }
                     mark(std::string(side == 0 ? "R" : "S") + "_lod" + std::to_string(level) + "_put");

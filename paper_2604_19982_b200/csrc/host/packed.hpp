@@ -2,6 +2,7 @@
 // (tj_dataset_view), plus the per-process device context registry.
 #pragma once
 
+#include <functional>
 #include <memory>
 #include <vector>
 
@@ -98,6 +99,15 @@ std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& ds, const PackedH
 std::unique_ptr<PackedHeader> pack_header(const PreparedDataset& ds, size_t first, size_t last, ThreadPool& pool);
 std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& ds, size_t first, const PackedHeader& h, size_t li,
                                         ThreadPool& pool);
+// Rows of one packed piece of a level: vertices, facets and voxel facet-id entries.
+struct PieceRows {
+    uint64_t vert_begin, vert_end, facet_begin, facet_end, entry_begin, entry_end;
+};
+// pack_level in `pieces` consecutive object ranges; on_piece(level, rows) runs after each
+// (the caller ships the rows while the next piece is packed).
+std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& ds, const PackedHeader& h, size_t li, ThreadPool& pool,
+                                        size_t pieces,
+                                        const std::function<void(const PackedLevel&, const PieceRows&)>& on_piece);
 
 // Lazily created context per CUDA device, destroyed at process exit.
 tj_ctx* device_context(int device);

@@ -9,6 +9,7 @@
 
 #include <chrono>
 #include <cstring>
+#include <bit>
 #include <map>
 #include <memory>
 #include <string>
@@ -68,23 +69,40 @@ py::tuple pack_output(const JoinOutput& out) {
         Py_INCREF(o);
         return o;
     };
+    // +0.0 (every confirmed intersection record's bounds) as one shared float
+    const py::object zero = py::reinterpret_steal<py::object>(PyFloat_FromDouble(0.0));
+    auto float_of = [&](double v) -> PyObject* {
+        if (std::bit_cast<uint64_t>(v) == 0) {
+            Py_INCREF(zero.ptr());
+            return zero.ptr();
+        }
+        PyObject* o = PyFloat_FromDouble(v);
+        if (!o) throw py::error_already_set();
+        return o;
+    };
+    int16_t last_stage = 0;
+    PyObject* last_name = nullptr;
     for (size_t i = 0; i < n; ++i) {
         const JoinResultRecord& r = out.records[i];
-        auto it = names.find(r.decided_at);
-        if (it == names.end()) it = names.emplace(r.decided_at, py::str(stage_name(r.decided_at))).first;
+        if (!last_name || r.decided_at != last_stage) {
+            auto it = names.find(r.decided_at);
+            if (it == names.end()) it = names.emplace(r.decided_at, py::str(stage_name(r.decided_at))).first;
+            last_stage = r.decided_at;
+            last_name = it->second.ptr();
+        }
         PyObject* t = PyTuple_New(6);
         if (!t) throw py::error_already_set();
         PyTuple_SET_ITEM(t, 0, int_of(r.r));
         PyTuple_SET_ITEM(t, 1, int_of(r.s));
-        PyObject* lb = PyFloat_FromDouble(r.lb);
+        PyObject* lb = float_of(r.lb);
         PyTuple_SET_ITEM(t, 2, lb);
         if (std::memcmp(&r.lb, &r.ub, sizeof(double)) == 0) {
             Py_INCREF(lb);
             PyTuple_SET_ITEM(t, 3, lb);
         } else {
-            PyTuple_SET_ITEM(t, 3, PyFloat_FromDouble(r.ub));
+            PyTuple_SET_ITEM(t, 3, float_of(r.ub));
         }
-        PyObject* nm = it->second.ptr();
+        PyObject* nm = last_name;
         Py_INCREF(nm);
         PyTuple_SET_ITEM(t, 4, nm);
         PyTuple_SET_ITEM(t, 5, int_of(r.rank));

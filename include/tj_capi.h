@@ -196,8 +196,9 @@ uint64_t tj_dataset_device_bytes(const tj_dataset* ds);
  *   [vert_begin, vert_end) of lv->vertices, [facet_begin, facet_end) of lv->tris (and of
  *   lv->hd / lv->ph when non-NULL) and [entry_begin, entry_end) of lv->voxel_facets (lv's
  *   arrays are the whole level's; the ranges are row indices into them). Once every row has
- *   been put, tj_dataset_finish_level(has_pads = whether hd / ph were shipped) expands the
- *   level and queues it; tj_dataset_put_level == one part covering the level + finish.
+ *   been put, tj_dataset_finish_level(flags: TJ_LEVEL_PADS if hd / ph were shipped,
+ *   TJ_LEVEL_NARROW if the 16-bit id arrays were) expands the level and queues it;
+ *   tj_dataset_put_level == one part covering the level + finish.
  * tj_dataset_sync: waits for every queued level copy of the dataset.
  */
 typedef struct tj_level_mesh_view {
@@ -206,7 +207,14 @@ typedef struct tj_level_mesh_view {
     const double* hd;             /* [facet_base[n_objects]]; hd and ph both NULL: all 0 */
     const double* ph;             /* [facet_base[n_objects]] */
     const uint32_t* voxel_facets; /* [facet_offsets[li][n_voxels]] object-local facet ids, voxel order */
+    /* Optional 16-bit forms (objects with at most 65536 vertices and facets at this level):
+     * when tris16 is non-NULL it replaces tris, likewise voxel_facets16 (both or neither). */
+    const uint16_t* tris16;
+    const uint16_t* voxel_facets16;
 } tj_level_mesh_view;
+
+#define TJ_LEVEL_PADS 1u   /* tj_dataset_finish_level: hd / ph were shipped */
+#define TJ_LEVEL_NARROW 2u /* tj_dataset_finish_level: tris16 / voxel_facets16 were shipped */
 
 int tj_dataset_begin(tj_ctx* ctx, const tj_dataset_view* header, const uint64_t* const* vert_base,
                      const uint64_t* const* facet_base, tj_dataset** out);
@@ -214,7 +222,7 @@ int tj_dataset_put_level(tj_dataset* ds, uint32_t slot, const tj_level_mesh_view
 int tj_dataset_put_level_part(tj_dataset* ds, uint32_t slot, const tj_level_mesh_view* lv, uint64_t vert_begin,
                               uint64_t vert_end, uint64_t facet_begin, uint64_t facet_end, uint64_t entry_begin,
                               uint64_t entry_end);
-int tj_dataset_finish_level(tj_dataset* ds, uint32_t slot, int has_pads);
+int tj_dataset_finish_level(tj_dataset* ds, uint32_t slot, uint32_t flags);
 int tj_dataset_sync(tj_dataset* ds);
 
 /* ---- host-side index loading (backs load_index, reference src/index_io.cpp:244-249) ----

@@ -175,9 +175,10 @@ void upload_objects(DatasetDev& d, const tj_dataset_view* v, cudaStream_t st) {
 // voxel_facets[e] (the record the reference's gather_facet_data builds per chunk,
 // src/refine.cpp:25-61). Object-local ids are rebased here and range-checked against the
 // object's counts; an out-of-range id is clamped (never read out of bounds) and flagged.
-__global__ void k_expand_level(const double* __restrict__ verts, const uint32_t* __restrict__ tris,
+template <class Id>
+__global__ void k_expand_level(const double* __restrict__ verts, const Id* __restrict__ tris,
                                const double* __restrict__ hd, const double* __restrict__ ph,
-                               const uint32_t* __restrict__ vf, const uint64_t* __restrict__ foff,
+                               const Id* __restrict__ vf, const uint64_t* __restrict__ foff,
                                const uint32_t* __restrict__ vox_obj, const uint64_t* __restrict__ vb,
                                const uint64_t* __restrict__ fb, uint64_t n_voxels, double* __restrict__ out,
                                int* __restrict__ err) {
@@ -475,8 +476,13 @@ int tj_dataset_put_level_part(tj_dataset* ds, uint32_t slot, const tj_level_mesh
         if (vert_begin > vert_end || vert_end > nvert || facet_begin > facet_end || facet_end > nfac ||
             entry_begin > entry_end || entry_end > used)
             throw Error(TJ_EINVAL, "tj_dataset_put_level_part: row range outside the level");
-        if ((vert_end > vert_begin && !lv->vertices) || (facet_end > facet_begin && (!lv->tris || !lv->hd != !lv->ph)) ||
-            (entry_end > entry_begin && !lv->voxel_facets))
+        const bool narrow = lv->tris16 != nullptr;
+        if (narrow != (lv->voxel_facets16 != nullptr))
+            throw Error(TJ_EINVAL, "tj_dataset_put_level: tris16 and voxel_facets16 go together");
+        const void* tris = narrow ? static_cast<const void*>(lv->tris16) : lv->tris;
+        const void* vfs = narrow ? static_cast<const void*>(lv->voxel_facets16) : lv->voxel_facets;
+        if ((vert_end > vert_begin && !lv->vertices) || (facet_end > facet_begin && (!tris || !lv->hd != !lv->ph)) ||
+            (entry_end > entry_begin && !vfs))
             throw Error(TJ_EINVAL, "tj_dataset_put_level: null level arrays");
         // into the dataset's staging area (reserved at tj_dataset_begin: no allocation here, so
         // a put never waits on the memory pool while a join runs); the copy stream orders the
@@ -489,12 +495,12 @@ int tj_dataset_put_level_part(tj_dataset* ds, uint32_t slot, const tj_level_mesh
                                         (b1 - b0) * row, cudaMemcpyHostToDevice, g.copy));
         };
         put(L.verts, lv->vertices, vert_begin, vert_end, 24);
-        put(L.tris, lv->tris, facet_begin, facet_end, 12);
+        put(L.tris, tris, facet_begin, facet_end, narrow ? 6 : 12);
         if (lv->hd) {
             put(L.hd, lv->hd, facet_begin, facet_end, 8);
             put(L.ph, lv->ph, facet_begin, facet_end, 8);
         }
-        put(L.vf, lv->voxel_facets, entry_begin, entry_end, 4);
+        put(L.vf, vfs, entry_begin, entry_end, narrow ? 2 : 4);
     });
     if (rc != TJ_OK) {
         {
@@ -507,7 +513,7 @@ int tj_dataset_put_level_part(tj_dataset* ds, uint32_t slot, const tj_level_mesh
     return rc;
 }
 
-int tj_dataset_finish_level(tj_dataset* ds, uint32_t slot, int has_pads) {
+int tj_dataset_finish_level(tj_dataset* ds, uint32_t slot, uint32_t flags) {
     if (!ds || !ds->d.gate || slot >= ds->d.levels.size()) return TJ_EINVAL;
     LevelGate& g = *ds->d.gate;
     tj_ctx* ctx = ds->ctx;
@@ -518,17 +524,25 @@ int tj_dataset_finish_level(tj_dataset* ds, uint32_t slot, int has_pads) {
         const uint64_t nvert = d.level_vertices[slot], nfac = d.level_facets[slot], used = d.level_entries[slot];
         const StageLayout L = stage_layout(nvert, nfac, used);
         unsigned char* base = d.stage.p;
+        const bool pads = flags & TJ_LEVEL_PADS;
         const double* verts = reinterpret_cast<const double*>(base + L.verts);
-        const uint32_t* tris = reinterpret_cast<const uint32_t*>(base + L.tris);
-        const double* hd = has_pads && nfac ? reinterpret_cast<const double*>(base + L.hd) : nullptr;
-        const double* ph = has_pads && nfac ? reinterpret_cast<const double*>(base + L.ph) : nullptr;
-        const uint32_t* vf = reinterpret_cast<const uint32_t*>(base + L.vf);
+        const double* hd = pads && nfac ? reinterpret_cast<const double*>(base + L.hd) : nullptr;
+        const double* ph = pads && nfac ? reinterpret_cast<const double*>(base + L.ph) : nullptr;
         if (d.n_voxels) {
             const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((d.n_voxels + 7) / 8, (uint64_t)ctx->ws.num_sms * 16));
             count_launch();
-            k_expand_level<<<grid, 256, 0, g.copy>>>(verts, tris, hd, ph, vf, d.facet_offsets[slot].p,
-                                                      d.vox_obj.p, d.vert_base[slot].p, d.facet_base[slot].p,
-                                                      d.n_voxels, d.facets[slot].p, d.stream_err.p);
+            if (flags & TJ_LEVEL_NARROW)
+                k_expand_level<<<grid, 256, 0, g.copy>>>(verts, reinterpret_cast<const uint16_t*>(base + L.tris), hd, ph,
+                                                          reinterpret_cast<const uint16_t*>(base + L.vf),
+                                                          d.facet_offsets[slot].p, d.vox_obj.p, d.vert_base[slot].p,
+                                                          d.facet_base[slot].p, d.n_voxels, d.facets[slot].p,
+                                                          d.stream_err.p);
+            else
+                k_expand_level<<<grid, 256, 0, g.copy>>>(verts, reinterpret_cast<const uint32_t*>(base + L.tris), hd, ph,
+                                                          reinterpret_cast<const uint32_t*>(base + L.vf),
+                                                          d.facet_offsets[slot].p, d.vox_obj.p, d.vert_base[slot].p,
+                                                          d.facet_base[slot].p, d.n_voxels, d.facets[slot].p,
+                                                          d.stream_err.p);
             TJ_CUDA(cudaGetLastError());
         }
         derive_level(d, slot, ctx->ws.num_sms, g.copy);
@@ -558,7 +572,7 @@ int tj_dataset_put_level(tj_dataset* ds, uint32_t slot, const tj_level_mesh_view
     const int rc = tj_dataset_put_level_part(ds, slot, lv, 0, d.level_vertices[slot], 0, d.level_facets[slot], 0,
                                              d.level_entries[slot]);
     if (rc != TJ_OK) return rc;
-    return tj_dataset_finish_level(ds, slot, lv->hd != nullptr);
+    return tj_dataset_finish_level(ds, slot, (lv->hd ? TJ_LEVEL_PADS : 0u) | (lv->tris16 ? TJ_LEVEL_NARROW : 0u));
 }
 
 int tj_dataset_sync(tj_dataset* ds) {

@@ -424,26 +424,40 @@ std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& dsf, size_t first
     // a level whose paddings are all +0.0 (the reference's level 100) ships no hd / ph at all;
     // the test ORs the IEEE bit patterns (branch-free, vectorisable: it reads the whole level
     // when the paddings are zero, so it runs at memory bandwidth)
-    std::atomic<bool> nonzero{false};
+    std::atomic<bool> nonzero{false}, wide{false};
     for_blocks(pool, no, [&](size_t b, size_t e) {
-        for (size_t o = b; o < e && !nonzero.load(std::memory_order_relaxed); ++o) {
+        bool w = false;
+        for (size_t o = b; o < e; ++o) {
             const LodMesh& lod = ds.objects[o].ladder.levels[li];
             const size_t n_f = lod.mesh.facets.size();
+            w = w || lod.mesh.vertices.size() >= 0xffff || n_f >= 0xffff;
+            if (nonzero.load(std::memory_order_relaxed)) continue;
             uint64_t bits = 0;
             for (size_t f = 0; f < n_f; ++f) bits |= std::bit_cast<uint64_t>(lod.hd[f]) | std::bit_cast<uint64_t>(lod.ph[f]);
             if (bits) nonzero = true;
         }
+        if (w) wide = true;
     });
     const bool pads = nonzero.load();
     p->zero_pads = !pads;
+    // 16-bit ids when every object of the level has < 65535 vertices and facets: ids are
+    // saturated at 0xffff, which is then out of every object's range, so an invalid id still
+    // trips the device's range check
+    const bool narrow = !wide.load();
+    p->narrow = narrow;
+    p->bytes = nvert * 24 + nfac * ((narrow ? 6 : 12) + (pads ? 16 : 0)) + entries * (narrow ? 2 : 4);
+    uint16_t* tris16 = reinterpret_cast<uint16_t*>(tris);
+    uint16_t* vf16 = reinterpret_cast<uint16_t*>(vf);
     static_assert(sizeof(Point3) == 3 * sizeof(double), "Point3 must be three packed doubles");
     static_assert(sizeof(std::array<uint32_t, 3>) == 3 * sizeof(uint32_t), "facets must be packed uint32 triples");
     tj_level_mesh_view& view = p->view;
     view.vertices = verts;
-    view.tris = tris;
+    view.tris = narrow ? nullptr : tris;
     view.hd = pads ? hd : nullptr;
     view.ph = pads ? ph : nullptr;
-    view.voxel_facets = vf;
+    view.voxel_facets = narrow ? nullptr : vf;
+    view.tris16 = narrow ? tris16 : nullptr;
+    view.voxel_facets16 = narrow ? vf16 : nullptr;
     const auto& fo = h.facet_offsets[li];
     pieces = std::max<size_t>(1, std::min(pieces, no));
     for (size_t k = 0; k < pieces; ++k) {
@@ -456,7 +470,13 @@ std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& dsf, size_t first
                 const size_t n_v = lod.mesh.vertices.size(), n_f = lod.mesh.facets.size();
                 if (n_v) std::memcpy(verts + 3 * vb, lod.mesh.vertices.data(), n_v * sizeof(Point3));
                 if (n_f) {
-                    std::memcpy(tris + 3 * fb, lod.mesh.facets.data(), n_f * 3 * sizeof(uint32_t));
+                    if (narrow) {
+                        const uint32_t* src = lod.mesh.facets.data()->data();
+                        uint16_t* dst = tris16 + 3 * fb;
+                        for (size_t i = 0; i < 3 * n_f; ++i) dst[i] = static_cast<uint16_t>(std::min<uint32_t>(src[i], 0xffff));
+                    } else {
+                        std::memcpy(tris + 3 * fb, lod.mesh.facets.data(), n_f * 3 * sizeof(uint32_t));
+                    }
                     if (pads) {
                         std::memcpy(hd + fb, lod.hd.data(), n_f * sizeof(double));
                         std::memcpy(ph + fb, lod.ph.data(), n_f * sizeof(double));
@@ -466,7 +486,13 @@ std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& dsf, size_t first
                 const uint64_t v0 = h.voxel_offsets[o];
                 for (uint32_t v = 0; v < vs.voxel_count(); ++v) {
                     const auto& ids = vs.facets_per_level[li][v];
-                    if (!ids.empty()) std::memcpy(vf + fo[v0 + v], ids.data(), ids.size() * sizeof(uint32_t));
+                    if (ids.empty()) continue;
+                    if (narrow) {
+                        uint16_t* dst = vf16 + fo[v0 + v];
+                        for (size_t i = 0; i < ids.size(); ++i) dst[i] = static_cast<uint16_t>(std::min<uint32_t>(ids[i], 0xffff));
+                    } else {
+                        std::memcpy(vf + fo[v0 + v], ids.data(), ids.size() * sizeof(uint32_t));
+                    }
                 }
             }
         });
@@ -909,8 +935,7 @@ void run_chunked(const PreparedDataset& R, const PreparedDataset& S, const JoinS
         const int slot = slot_of(S, level);
         if (slot < 0) continue;
         s_levels.push_back(detail::pack_level(S, *hs, static_cast<size_t>(slot), pool));
-        out.stats.h2d_bytes += G * (hs->n_vertices[slot] * 24 + hs->n_facets[slot] * (s_levels.back()->zero_pads ? 12 : 28) +
-                                    hs->facet_offsets[slot].back() * 4);
+        out.stats.h2d_bytes += G * s_levels.back()->bytes;
         for (size_t g = 0; g < G; ++g)
             detail::check(tj_dataset_put_level(dsh[g].p, static_cast<uint32_t>(slot), &s_levels.back()->view),
                           detail::device_context(devices[g]));
@@ -935,8 +960,7 @@ void run_chunked(const PreparedDataset& R, const PreparedDataset& S, const JoinS
             const int slot = slot_of(R, level);
             if (slot < 0) continue; // the join reports the missing level
             p->lv.push_back(detail::pack_level(R, a, *p->h, static_cast<size_t>(slot), pool));
-            bytes += p->h->n_vertices[slot] * 24 + p->h->n_facets[slot] * (p->lv.back()->zero_pads ? 12 : 28) +
-                     p->h->facet_offsets[slot].back() * 4;
+            bytes += p->lv.back()->bytes;
             detail::check(tj_dataset_put_level(p->d.p, static_cast<uint32_t>(slot), &p->lv.back()->view), ctx);
         }
         std::lock_guard<std::mutex> lk(stat_mu);
@@ -1131,12 +1155,14 @@ JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const Jo
                     staged.push_back(detail::pack_level(D, H, static_cast<size_t>(slot), pool, kPackPieces, ship));
                     pack_ms += std::chrono::duration<double, std::milli>(Clock::now() - tl).count();
                     mark(std::string(side == 0 ? "R" : "S") + "_lod" + std::to_string(level) + "_packed");
-                    out.stats.h2d_bytes += G * (H.n_vertices[slot] * 24 + H.n_facets[slot] * (staged.back()->zero_pads ? 12 : 28) + H.facet_offsets[slot].back() * 4);
+                    out.stats.h2d_bytes += G * staged.back()->bytes;
                     for (size_t g = 0; g < G; ++g) {
                         tj_dataset* ds = side == 0 ? dr[g].p : dsh[g].p;
                         auto& put = side == 0 ? put_r[g] : put_s[g];
                         put[slot] = 1;
-                        detail::check(tj_dataset_finish_level(ds, static_cast<uint32_t>(slot), !staged.back()->zero_pads),
+                        const uint32_t flags = (staged.back()->zero_pads ? 0u : TJ_LEVEL_PADS) |
+                                               (staged.back()->narrow ? TJ_LEVEL_NARROW : 0u);
+                        detail::check(tj_dataset_finish_level(ds, static_cast<uint32_t>(slot), flags),
                                       detail::device_context(devices[g]));
                     }
                     mark(std::string(side == 0 ? "R" : "S") + "_lod" + std::to_string(level) + "_put");

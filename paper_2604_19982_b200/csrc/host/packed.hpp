@@ -91,6 +91,8 @@ struct PackedHeader {
 struct PackedLevel {
     PinnedBuf verts, tris, hd, ph, vf; // tris / vf hold uint32 pairs per double slot
     bool zero_pads = false;            // every hd / ph of the level is +0: not shipped
+    bool narrow = false;               // ids shipped as uint16 (every object < 65536 vertices / facets)
+    uint64_t bytes = 0;                // H2D bytes of the level
     tj_level_mesh_view view{};
 };
 std::unique_ptr<PackedHeader> pack_header(const PreparedDataset& ds, ThreadPool& pool);

@@ -4,6 +4,7 @@
 // __d*_rn intrinsics).
 #include <cuda_runtime.h>
 #include <cstdlib>
+#include <type_traits>
 
 #include "refine_kernel.cuh"
 #include "tj_internal.cuh"
@@ -207,7 +208,7 @@ __device__ __forceinline__ void closest_pair(const float4* __restrict__ rset, ui
 #define SEED_BATCH 32
 #endif
 __device__ __forceinline__ unsigned seed_batch() { return SEED_BATCH; }
-__global__ void __launch_bounds__(256) k_seed(RefineSource src, uint64_t vp_begin, uint64_t vp_end, RefineQueue q,
+__global__ void __launch_bounds__(256, 4) k_seed(RefineSource src, uint64_t vp_begin, uint64_t vp_end, RefineQueue q,
                                               int cull) {
     // per warp: the voxel pairs of the current batch that need seeds (segments + boxes)
     struct SeedVp {
@@ -290,54 +291,61 @@ __global__ void __launch_bounds__(256) k_seed(RefineSource src, uint64_t vp_begi
                                       {as.lo[0], as.lo[1], as.lo[2]}, {as.hi[0], as.hi[1], as.hi[2]}};
                 }
             }
-            // voxel pairs with both segments <= 8 facets are seeded four at a time, one per
-            // 8-lane group (the coarse levels); the others one per warp
-            unsigned small = __ballot_sync(0xffffffffu, live && mine[lane].rn <= 8 && mine[lane].sn <= 8);
-            unsigned pending = __ballot_sync(0xffffffffu, live) & ~small;
+            // voxel pairs with both segments <= 8 (<= 16) facets are seeded four (two) at a
+            // time, one per 8-lane (16-lane) group; the others one per warp
+            auto run_groups = [&](auto gsize, unsigned set) {
+                constexpr int G = decltype(gsize)::value, NG = 32 / G;
+                while (set) {
+                    const int grp = lane / G, sub = lane % G, gl = lane - sub;
+                    int sel = -1; // the batch lane whose voxel pair this group seeds
+#pragma unroll
+                    for (int k = 0; k < NG; ++k) {
+                        const int v = set ? __ffs(set) - 1 : -1;
+                        if (set) set &= set - 1;
+                        if (k == grp) sel = v;
+                    }
+                    const bool on = sel >= 0;
+                    const SeedVp& e = mine[on ? sel : 0];
+                    const uint32_t rn = on ? e.rn : 0u, sn = on ? e.sn : 0u;
+                    const float kInfF = __int_as_float(0x7f800000);
+                    float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0, s0 = r0, s1 = r0;
+                    if (sub < (int)rn) { r0 = __ldg(src.r_box + (e.r0 + sub) * kBoxF4); r1 = __ldg(src.r_box + (e.r0 + sub) * kBoxF4 + 1); }
+                    if (sub < (int)sn) { s0 = __ldg(src.s_box + (e.s0 + sub) * kBoxF4); s1 = __ldg(src.s_box + (e.s0 + sub) * kBoxF4 + 1); }
+                    // argmin within the group (key bits with the lane in the low 5 bits)
+                    auto group_argmin = [&](float key) -> uint32_t {
+                        unsigned p = (__float_as_uint(key) & ~31u) | (unsigned)lane;
+#pragma unroll
+                        for (int o = G / 2; o > 0; o >>= 1) p = min(p, __shfl_xor_sync(0xffffffffu, p, o));
+                        return (p & 31u) - (unsigned)gl;
+                    };
+                    const uint32_t ist = group_argmin(sub < (int)rn ? seed_key(r0, r1, e.blo, e.bhi) : kInfF);
+                    const uint32_t jst = group_argmin(sub < (int)sn ? seed_key(s0, s1, e.alo, e.ahi) : kInfF);
+                    const float fil[3] = {__shfl_sync(~0u, r0.x, gl + ist), __shfl_sync(~0u, r0.y, gl + ist), __shfl_sync(~0u, r0.z, gl + ist)};
+                    const float fih[3] = {__shfl_sync(~0u, r1.x, gl + ist), __shfl_sync(~0u, r1.y, gl + ist), __shfl_sync(~0u, r1.z, gl + ist)};
+                    const float fjl[3] = {__shfl_sync(~0u, s0.x, gl + jst), __shfl_sync(~0u, s0.y, gl + jst), __shfl_sync(~0u, s0.z, gl + jst)};
+                    const float fjh[3] = {__shfl_sync(~0u, s1.x, gl + jst), __shfl_sync(~0u, s1.y, gl + jst), __shfl_sync(~0u, s1.z, gl + jst)};
+                    const uint32_t ip = group_argmin(sub < (int)rn ? seed_key(r0, r1, fjl, fjh) : kInfF);
+                    const uint32_t jp = group_argmin(sub < (int)sn ? seed_key(s0, s1, fil, fih) : kInfF);
+                    // the groups' seeds into the lane buffer, group by group (groups fill in order)
+#pragma unroll
+                    for (int k = 0; k < NG; ++k) {
+                        const int src_lane = G * k;
+                        if (!__shfl_sync(0xffffffffu, (int)on, src_lane)) break;
+                        const uint32_t op = __shfl_sync(0xffffffffu, on ? e.op : 0u, src_lane);
+                        const uint64_t gr0 = __shfl_sync(0xffffffffu, on ? e.r0 : 0ull, src_lane);
+                        const uint64_t gs0 = __shfl_sync(0xffffffffu, on ? e.s0 : 0ull, src_lane);
+                        emit(op, gr0, gs0, __shfl_sync(0xffffffffu, ist, src_lane), __shfl_sync(0xffffffffu, jst, src_lane),
+                             __shfl_sync(0xffffffffu, ip, src_lane), __shfl_sync(0xffffffffu, jp, src_lane));
+                    }
+                }
+            };
+            const unsigned all = __ballot_sync(0xffffffffu, live);
+            const unsigned le8 = __ballot_sync(0xffffffffu, live && mine[lane].rn <= 8 && mine[lane].sn <= 8);
+            const unsigned le16 = __ballot_sync(0xffffffffu, live && mine[lane].rn <= 16 && mine[lane].sn <= 16) & ~le8;
+            unsigned pending = all & ~le8 & ~le16;
             __syncwarp();
-            while (small) {
-                const int grp = lane >> 3, sub = lane & 7, gl = lane & ~7;
-                int sel = -1; // the batch lane whose voxel pair this group seeds
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int v = small ? __ffs(small) - 1 : -1;
-                    if (small) small &= small - 1;
-                    if (k == grp) sel = v;
-                }
-                const bool on = sel >= 0;
-                const SeedVp& e = mine[on ? sel : 0];
-                const uint32_t rn = on ? e.rn : 0u, sn = on ? e.sn : 0u;
-                const float kInfF = __int_as_float(0x7f800000);
-                float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0, s0 = r0, s1 = r0;
-                if (sub < (int)rn) { r0 = __ldg(src.r_box + (e.r0 + sub) * kBoxF4); r1 = __ldg(src.r_box + (e.r0 + sub) * kBoxF4 + 1); }
-                if (sub < (int)sn) { s0 = __ldg(src.s_box + (e.s0 + sub) * kBoxF4); s1 = __ldg(src.s_box + (e.s0 + sub) * kBoxF4 + 1); }
-                // argmin within the 8-lane group (key bits with the lane in the low 5 bits)
-                auto group_argmin = [&](float key) -> uint32_t {
-                    unsigned p = (__float_as_uint(key) & ~31u) | (unsigned)lane;
-#pragma unroll
-                    for (int o = 4; o > 0; o >>= 1) p = min(p, __shfl_xor_sync(0xffffffffu, p, o));
-                    return (p & 31u) - (unsigned)gl;
-                };
-                const uint32_t ist = group_argmin(sub < (int)rn ? seed_key(r0, r1, e.blo, e.bhi) : kInfF);
-                const uint32_t jst = group_argmin(sub < (int)sn ? seed_key(s0, s1, e.alo, e.ahi) : kInfF);
-                const float fil[3] = {__shfl_sync(~0u, r0.x, gl + ist), __shfl_sync(~0u, r0.y, gl + ist), __shfl_sync(~0u, r0.z, gl + ist)};
-                const float fih[3] = {__shfl_sync(~0u, r1.x, gl + ist), __shfl_sync(~0u, r1.y, gl + ist), __shfl_sync(~0u, r1.z, gl + ist)};
-                const float fjl[3] = {__shfl_sync(~0u, s0.x, gl + jst), __shfl_sync(~0u, s0.y, gl + jst), __shfl_sync(~0u, s0.z, gl + jst)};
-                const float fjh[3] = {__shfl_sync(~0u, s1.x, gl + jst), __shfl_sync(~0u, s1.y, gl + jst), __shfl_sync(~0u, s1.z, gl + jst)};
-                const uint32_t ip = group_argmin(sub < (int)rn ? seed_key(r0, r1, fjl, fjh) : kInfF);
-                const uint32_t jp = group_argmin(sub < (int)sn ? seed_key(s0, s1, fil, fih) : kInfF);
-                // the groups' seeds into the lane buffer, group by group
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int src_lane = 8 * k;
-                    if (!__shfl_sync(0xffffffffu, (int)on, src_lane)) break; // groups fill in order
-                    const uint32_t op = __shfl_sync(0xffffffffu, on ? e.op : 0u, src_lane);
-                    const uint64_t gr0 = __shfl_sync(0xffffffffu, on ? e.r0 : 0ull, src_lane);
-                    const uint64_t gs0 = __shfl_sync(0xffffffffu, on ? e.s0 : 0ull, src_lane);
-                    emit(op, gr0, gs0, __shfl_sync(0xffffffffu, ist, src_lane), __shfl_sync(0xffffffffu, jst, src_lane),
-                         __shfl_sync(0xffffffffu, ip, src_lane), __shfl_sync(0xffffffffu, jp, src_lane));
-                }
-            }
+            run_groups(std::integral_constant<int, 8>{}, le8);
+            run_groups(std::integral_constant<int, 16>{}, le16);
             while (pending) {
                 const int lv = __ffs(pending) - 1;
                 pending &= pending - 1;

@@ -482,14 +482,26 @@ uint32_t hier_min_pairs() {
     return v;
 }
 
-// voxel pairs per work grab of k_screen (TRIJOIN_SCREEN_BATCH: tuning override, 1..32)
-unsigned screen_batch() {
-    static const unsigned b = [] {
+// Voxel pairs per work grab of k_screen: inversely proportional to the expected work of a
+// voxel pair (mean segment length m, work ~ m^2 facet pairs): kGrabWork / m^2 clamped to
+// [4, 32] — large grabs where most voxel pairs are cheap or settled (fewer work-counter
+// atomics), small ones where heavy voxel pairs cluster (load balance). kGrabWork = 8192
+// (config B 68.6 -> 66.0 ms, C 206 -> 201 ms, E 12.9 -> 13.1 ms; 16384: B 65.7, C 197, E 14.0).
+// TRIJOIN_SCREEN_BATCH (1..32) / TRIJOIN_SCREEN_GRAB_WORK override (tuning).
+unsigned screen_batch(float mean_seg) {
+    static const int forced = [] {
         const char* e = getenv("TRIJOIN_SCREEN_BATCH");
         const int v = e ? atoi(e) : 0;
-        return v >= 1 && v <= 32 ? unsigned(v) : 4u;
+        return v >= 1 && v <= 32 ? v : 0;
     }();
-    return b;
+    static const float work = [] {
+        const char* e = getenv("TRIJOIN_SCREEN_GRAB_WORK");
+        return e ? (float)atof(e) : 8192.f;
+    }();
+    if (forced) return (unsigned)forced;
+    if (!(mean_seg > 0.f)) return 4u;
+    const float b = work / (mean_seg * mean_seg);
+    return b >= 32.f ? 32u : b <= 4.f ? 4u : (unsigned)b;
 }
 
 // Decision mode: when every facet pair has hd_i + hd_j > 1e-5 (L_i + L_j) + 1e-12 (M_i + M_j),
@@ -531,11 +543,9 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks) k_screen(Refine
     };
     // nothing can change lb' or ub': the whole voxel pair is irrelevant
     auto settled = [&](const Thresh& th) { return cull && (th.lb_sat || th.lb_u == 0.f) && th.ub_u == 0.f; };
-    // Work in batches of `batch` voxel pairs per work-counter atomic: lane i looks up voxel pair
-    // i of the batch and its op thresholds (independent latency chains), the warp then screens
-    // only the voxel pairs whose op can still change. 4 balances the cheap-skip levels (larger
-    // batches win) against clustered heavy voxel pairs at fine levels (B: 32 -> 118 ms, 16 ->
-    // 106, 8 -> 101, 4 -> 99.7, 1 -> 110.6).
+    // Work in batches of `batch` voxel pairs per work-counter atomic (screen_batch): lane i
+    // looks up voxel pair i of the batch and its op thresholds (independent latency chains),
+    // the warp then screens only the voxel pairs whose op can still change.
     for (;;) {
         unsigned long long base = 0;
         if (lane == 0) base = atomicAdd(work, (unsigned long long)batch);
@@ -905,7 +915,7 @@ void refine_pass(const RefineSource& src, uint64_t vp_begin, uint64_t vp_end, bo
         count_launch();
         k_screen<<<warp_grid(vp_end - vp_begin, num_sms, kScreenBlocks, kScreenThreads / 32), kScreenThreads,
                    kScreenSmem, st>>>(
-            src, vp_begin, vp_end, lb_bits, ub_bits, cull, qs.view(), work, counters, screen_batch(), hier_min_pairs());
+            src, vp_begin, vp_end, lb_bits, ub_bits, cull, qs.view(), work, counters, screen_batch(src.mean_seg), hier_min_pairs());
         TJ_CUDA(cudaGetLastError());
     }
     count_launch();

@@ -193,6 +193,9 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
                 src.s_box = S.screen[ss].p;
                 src.s_geo = S.screen[ss].p + 3 * ns;
                 src.s_seg = S.seg[ss].p;
+                const double mr = R.n_voxels ? double(nr) / double(R.n_voxels) : 0.0;
+                const double ms = S.n_voxels ? double(ns) / double(S.n_voxels) : 0.0;
+                src.mean_seg = float(0.5 * (mr + ms));
             }
             // 0: every facet pair; 1: exact-preserving culling; 2: decision-mode culling
             const int cull = (spec.flags & TJ_FLAG_NO_CULL) ? 0 : decision ? 2 : 1;

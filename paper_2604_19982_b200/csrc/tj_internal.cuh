@@ -161,6 +161,8 @@ struct RefineSource {
     const float4* s_seg;
     // 1: ignore the records' hd / ph (pure tri-tri minima: the --exact recompute)
     int zero_pad;
+    // mean facets per voxel of the level (R and S; 0 = unknown): sizes k_screen's work grabs
+    float mean_seg;
 };
 
 // A queued facet pair: op and the two global facet record indices.

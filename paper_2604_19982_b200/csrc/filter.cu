@@ -39,12 +39,14 @@ __global__ void k_minx_keys(const double* __restrict__ mbb, uint32_t n, double* 
 }
 
 __global__ void k_gather_sorted(const double* __restrict__ mbb, const uint32_t* __restrict__ order, uint32_t n,
-                                double* __restrict__ out, unsigned long long* max_ext_bits) {
+                                double* __restrict__ out, float4* __restrict__ yz, unsigned long long* max_ext_bits) {
     unsigned long long local = 0;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const double* m = mbb + 6 * (size_t)order[i];
 #pragma unroll
         for (int k = 0; k < 6; ++k) out[6 * (size_t)i + k] = m[k];
+        yz[i] = make_float4(__double2float_rd(m[1]), __double2float_ru(m[4]), __double2float_rd(m[2]),
+                            __double2float_ru(m[5]));
         const double ext = m[3] - m[0];
         const unsigned long long b = (unsigned long long)__double_as_longlong(ext > 0.0 ? ext : 0.0);
         local = b > local ? b : local;
@@ -88,6 +90,30 @@ __device__ __forceinline__ double query_tau(const MbbArgs& a, uint32_t r) {
     return a.tau_per_r ? a.tau_per_r[r] : a.tau;
 }
 
+// FP32 pre-rejection of sorted S entries on their y / z gaps to a query box (the x window
+// is mbb_window's). Rejects only if a rounded-down gap exceeds tau (1 + 2^-20) (rounded up,
+// at least 1e-30): the true gap then exceeds tau, so does its FP64 rounding, and mindist_box
+// (>= that rounded gap: sqrt(fl(g*g)) == g without underflow) cannot be <= tau.
+struct YzReject {
+    float ylo, yhi, zlo, zhi, t;
+    bool on;
+    __device__ YzReject(const MbbArgs& a, const double* rb, double tau) {
+        on = a.s_sorted_yz != nullptr;
+        ylo = __double2float_rd(rb[1]);
+        yhi = __double2float_ru(rb[4]);
+        zlo = __double2float_rd(rb[2]);
+        zhi = __double2float_ru(rb[5]);
+        t = fmaxf(__double2float_ru(tau * (1.0 + 0x1p-20)), 1e-30f);
+    }
+    __device__ __forceinline__ bool operator()(const MbbArgs& a, uint32_t i) const {
+        if (!on) return false;
+        const float4 s = __ldg(a.s_sorted_yz + i);
+        const float gy = fmaxf(__fsub_rd(s.x, yhi), __fsub_rd(ylo, s.y));
+        const float gz = fmaxf(__fsub_rd(s.z, zhi), __fsub_rd(zlo, s.w));
+        return gy > t || gz > t;
+    }
+};
+
 __global__ void k_mbb_count(MbbArgs a, uint32_t* __restrict__ counts) {
     const int lane = threadIdx.x & 31;
     const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
@@ -97,8 +123,9 @@ __global__ void k_mbb_count(MbbArgs a, uint32_t* __restrict__ counts) {
             const double* rb = a.r_mbb + 6 * (size_t)r;
             const double tau = query_tau(a, r);
             const Window w = mbb_window(rb, tau, a.s_sorted_mbb, a.ns, a.max_ext);
+            const YzReject reject(a, rb, tau);
             for (uint32_t i = w.lo + lane; i < w.hi; i += 32)
-                c += mindist_box(rb, a.s_sorted_mbb + 6 * (size_t)i) <= tau ? 1u : 0u;
+                if (!reject(a, i)) c += mindist_box(rb, a.s_sorted_mbb + 6 * (size_t)i) <= tau ? 1u : 0u;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
         }
@@ -116,9 +143,10 @@ __global__ void k_mbb_fill(MbbArgs a, const uint64_t* __restrict__ offsets, uint
         const double* rb = a.r_mbb + 6 * (size_t)r;
         const double tau = query_tau(a, r);
         const Window w = mbb_window(rb, tau, a.s_sorted_mbb, a.ns, a.max_ext);
+        const YzReject reject(a, rb, tau);
         for (uint32_t base = w.lo; base < w.hi; base += 32) {
             const uint32_t i = base + lane;
-            const bool keep = i < w.hi && mindist_box(rb, a.s_sorted_mbb + 6 * (size_t)i) <= tau;
+            const bool keep = i < w.hi && !reject(a, i) && mindist_box(rb, a.s_sorted_mbb + 6 * (size_t)i) <= tau;
             const unsigned bal = __ballot_sync(0xffffffffu, keep);
             if (keep) {
                 const uint64_t o = pos + __popc(bal & ((1u << lane) - 1u));
@@ -397,7 +425,8 @@ void mbb_prepare_s(Workspace& ws, const DatasetDev& S, SortedS& out, cudaStream_
     DevBuf<unsigned long long> ext(1);
     TJ_CUDA(cudaMemsetAsync(ext.p, 0, sizeof(unsigned long long), st));
     count_launch();
-    k_gather_sorted<<<grid_for(ns, 256, ws.num_sms), 256, 0, st>>>(S.mbb.p, out.order.p, ns, out.mbb.p, ext.p);
+    out.yz.reserve(ns);
+    k_gather_sorted<<<grid_for(ns, 256, ws.num_sms), 256, 0, st>>>(S.mbb.p, out.order.p, ns, out.mbb.p, out.yz.p, ext.p);
     unsigned long long bits = 0;
     TJ_CUDA(cudaMemcpyAsync(&bits, ext.p, 8, cudaMemcpyDeviceToHost, st));
     stream_sync(st);

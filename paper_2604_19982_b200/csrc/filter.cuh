@@ -80,6 +80,7 @@ struct Workspace {
 struct SortedS {
     DevBuf<uint32_t> order; // S indices sorted by mbb.min.x
     DevBuf<double> mbb;     // S mbbs in that order
+    DevBuf<float4> yz;      // their y / z extents outward-rounded to FP32: (y lo, y hi, z lo, z hi)
     double max_ext = 0.0;   // max over S of mbb.max.x - mbb.min.x
 };
 
@@ -89,6 +90,7 @@ struct MbbArgs {
     const double* s_mbb;
     const double* s_anchor;
     const double* s_sorted_mbb;
+    const float4* s_sorted_yz; // optional FP32 y / z pre-rejection (SortedS::yz)
     const uint32_t* s_order;
     uint32_t nr, ns;
     double tau;              // within threshold

@@ -263,6 +263,7 @@ int tj_mbb_filter(tj_ctx* ctx, const tj_dataset* Rh, const tj_dataset* Sh, int32
         ma.s_mbb = S.mbb.p;
         ma.s_anchor = S.anchor.p;
         ma.s_sorted_mbb = sorted.mbb.p;
+        ma.s_sorted_yz = sorted.yz.p;
         ma.s_order = sorted.order.p;
         ma.nr = R.n_objects;
         ma.ns = S.n_objects;

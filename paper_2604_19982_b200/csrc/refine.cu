@@ -488,7 +488,7 @@ uint32_t hier_min_pairs() {
 // atomics), small ones where heavy voxel pairs cluster (load balance). kGrabWork = 8192
 // (config B 68.6 -> 66.0 ms, C 206 -> 201 ms, E 12.9 -> 13.1 ms; 16384: B 65.7, C 197, E 14.0).
 // TRIJOIN_SCREEN_BATCH (1..32) / TRIJOIN_SCREEN_GRAB_WORK override (tuning).
-unsigned screen_batch(float mean_seg) {
+unsigned screen_batch(float mean_seg, uint64_t n_vps, uint64_t warps) {
     static const int forced = [] {
         const char* e = getenv("TRIJOIN_SCREEN_BATCH");
         const int v = e ? atoi(e) : 0;
@@ -500,7 +500,10 @@ unsigned screen_batch(float mean_seg) {
     }();
     if (forced) return (unsigned)forced;
     if (!(mean_seg > 0.f)) return 4u;
-    const float b = work / (mean_seg * mean_seg);
+    float b = work / (mean_seg * mean_seg);
+    // at least ~8 grabs per warp: a small launch is spread over the whole grid
+    const float cap = float(n_vps) / float(8 * (warps ? warps : 1));
+    b = fminf(b, cap);
     return b >= 32.f ? 32u : b <= 4.f ? 4u : (unsigned)b;
 }
 
@@ -913,9 +916,10 @@ void refine_pass(const RefineSource& src, uint64_t vp_begin, uint64_t vp_end, bo
         TJ_CUDA(cudaMemsetAsync(qs.count.p, 0, 8, st));
         TJ_CUDA(cudaMemsetAsync(work, 0, 8, st));
         count_launch();
-        k_screen<<<warp_grid(vp_end - vp_begin, num_sms, kScreenBlocks, kScreenThreads / 32), kScreenThreads,
-                   kScreenSmem, st>>>(
-            src, vp_begin, vp_end, lb_bits, ub_bits, cull, qs.view(), work, counters, screen_batch(src.mean_seg), hier_min_pairs());
+        const int sgrid = warp_grid(vp_end - vp_begin, num_sms, kScreenBlocks, kScreenThreads / 32);
+        k_screen<<<sgrid, kScreenThreads, kScreenSmem, st>>>(
+            src, vp_begin, vp_end, lb_bits, ub_bits, cull, qs.view(), work, counters,
+            screen_batch(src.mean_seg, vp_end - vp_begin, (uint64_t)sgrid * (kScreenThreads / 32)), hier_min_pairs());
         TJ_CUDA(cudaGetLastError());
     }
     count_launch();

@@ -258,6 +258,40 @@ __global__ void __launch_bounds__(256, 4) k_seed(RefineSource src, uint64_t vp_b
             const float fjh[3] = {__shfl_sync(~0u, s1.x, jst), __shfl_sync(~0u, s1.y, jst), __shfl_sync(~0u, s1.z, jst)};
             ip = warp_argmin_lane(lane < (int)d.rn ? seed_key(r0, r1, fjl, fjh) : kInfF);
             jp = warp_argmin_lane(lane < (int)d.sn ? seed_key(s0, s1, fil, fih) : kInfF);
+        } else if (d.rn <= 64 && d.sn <= 64) {
+            // two facets per lane and side (lane, lane + 32) in registers; argmin over 64
+            // indices (6 low key bits)
+            const float kInfF = __int_as_float(0x7f800000);
+            float4 ra0 = make_float4(0.f, 0.f, 0.f, 0.f), ra1 = ra0, rb0 = ra0, rb1 = ra0;
+            float4 sa0 = ra0, sa1 = ra0, sb0 = ra0, sb1 = ra0;
+            const int l2 = lane + 32;
+            if (lane < (int)d.rn) { ra0 = __ldg(src.r_box + (d.r0 + lane) * kBoxF4); ra1 = __ldg(src.r_box + (d.r0 + lane) * kBoxF4 + 1); }
+            if (l2 < (int)d.rn) { rb0 = __ldg(src.r_box + (d.r0 + l2) * kBoxF4); rb1 = __ldg(src.r_box + (d.r0 + l2) * kBoxF4 + 1); }
+            if (lane < (int)d.sn) { sa0 = __ldg(src.s_box + (d.s0 + lane) * kBoxF4); sa1 = __ldg(src.s_box + (d.s0 + lane) * kBoxF4 + 1); }
+            if (l2 < (int)d.sn) { sb0 = __ldg(src.s_box + (d.s0 + l2) * kBoxF4); sb1 = __ldg(src.s_box + (d.s0 + l2) * kBoxF4 + 1); }
+            auto argmin64 = [&](float ka, float kb) -> uint32_t {
+                const unsigned pa = (__float_as_uint(ka) & ~63u) | (unsigned)lane;
+                const unsigned pb = (__float_as_uint(kb) & ~63u) | (unsigned)l2;
+                return __reduce_min_sync(0xffffffffu, min(pa, pb)) & 63u;
+            };
+            ist = argmin64(lane < (int)d.rn ? seed_key(ra0, ra1, as.lo, as.hi) : kInfF,
+                           l2 < (int)d.rn ? seed_key(rb0, rb1, as.lo, as.hi) : kInfF);
+            jst = argmin64(lane < (int)d.sn ? seed_key(sa0, sa1, ar.lo, ar.hi) : kInfF,
+                           l2 < (int)d.sn ? seed_key(sb0, sb1, ar.lo, ar.hi) : kInfF);
+            const bool ih = ist >= 32, jh = jst >= 32;
+            const int il = ist & 31, jl = jst & 31;
+            const float fil[3] = {__shfl_sync(~0u, ih ? rb0.x : ra0.x, il), __shfl_sync(~0u, ih ? rb0.y : ra0.y, il),
+                                  __shfl_sync(~0u, ih ? rb0.z : ra0.z, il)};
+            const float fih[3] = {__shfl_sync(~0u, ih ? rb1.x : ra1.x, il), __shfl_sync(~0u, ih ? rb1.y : ra1.y, il),
+                                  __shfl_sync(~0u, ih ? rb1.z : ra1.z, il)};
+            const float fjl[3] = {__shfl_sync(~0u, jh ? sb0.x : sa0.x, jl), __shfl_sync(~0u, jh ? sb0.y : sa0.y, jl),
+                                  __shfl_sync(~0u, jh ? sb0.z : sa0.z, jl)};
+            const float fjh[3] = {__shfl_sync(~0u, jh ? sb1.x : sa1.x, jl), __shfl_sync(~0u, jh ? sb1.y : sa1.y, jl),
+                                  __shfl_sync(~0u, jh ? sb1.z : sa1.z, jl)};
+            ip = argmin64(lane < (int)d.rn ? seed_key(ra0, ra1, fjl, fjh) : kInfF,
+                          l2 < (int)d.rn ? seed_key(rb0, rb1, fjl, fjh) : kInfF);
+            jp = argmin64(lane < (int)d.sn ? seed_key(sa0, sa1, fil, fih) : kInfF,
+                          l2 < (int)d.sn ? seed_key(sb0, sb1, fil, fih) : kInfF);
         } else {
             closest_pair(src.r_box, d.r0, d.rn, src.s_box, d.s0, d.sn, ar, as, ist, jst);
             SegAgg fi = ar, fj = as; // only lo / hi are read

@@ -34,9 +34,13 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# roofline.achieved follows SURVEY §8(d): 1,500 FLOP per exact facet-pair evaluation + 20 FLOP per
+# culling box test, counted on the device. The builder's finer model (25 per box test, 300 per
+# separating-axis test) is reported beside it as roofline.builder_model.
 FLOP_PER_PAIR = 1500.0   # exact FP64 evaluation: dynamic op count of tri_tri_distance + padding
-FLOP_PER_TEST = 25.0     # stage-1 FP32 test: facet-AABB gap + thresholds (~25 FP32 ops) per facet pair
-FLOP_PER_SAT = 300.0     # stage-2 FP32 separating-axis bound (2 face + 9 edge axes, ~300 FP32 ops)
+FLOP_PER_TEST = 20.0     # culling box test
+B_FLOP_PER_TEST = 25.0   # builder model: stage-1 FP32 test (facet-AABB gap + thresholds)
+B_FLOP_PER_SAT = 300.0   # builder model: stage-2 FP32 separating-axis bound (2 face + 9 edge axes)
 TYPE_CODE = {"within": 0, "intersect": 1, "knn": 2}
 
 
@@ -78,6 +82,16 @@ def ncu_traffic(config):
     top = max(launches, key=lambda l: l["dram_bytes"])
     return top["dram_bytes"], f"profiles/ncu_traffic_{config}.json ({top['report']}: one k_screen launch, " \
                               f"{top['duration_s'] * 1e3:.2f} ms, {top['dram_GBps']:.0f} GB/s)"
+
+
+def ncu_pipes(config):
+    """ncu pipe utilisation of the dominant refinement launch from the committed --set full
+    capture (profiles/ncu_pipes_<config>.json, scripts/ncu_table.py), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", f"ncu_pipes_{config}.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
 
 
 def measured_peaks():
@@ -133,28 +147,81 @@ class Clocks:
 
 def ref_shim():
     lib = ctypes.CDLL(os.path.join(ROOT, "oracle", "_ref", "libref_shim.so"))
-    lib.ref_join_timed.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int, ctypes.c_double, ctypes.c_uint32,
-                                   ctypes.POINTER(ctypes.c_uint32), ctypes.c_uint32, ctypes.c_uint, ctypes.c_uint32,
-                                   ctypes.POINTER(ctypes.c_double)]
+    lib.ref_join_timed_records.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int, ctypes.c_double,
+                                           ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint32), ctypes.c_uint32,
+                                           ctypes.c_uint, ctypes.c_uint32, ctypes.POINTER(ctypes.c_double),
+                                           ctypes.c_char_p]
     lib.ref_last_error.restype = ctypes.c_char_p
     return lib
 
 
-def ref_join(lib, r_path, s_path, kw, lods, workers, repeats=1):
-    """The reference's own run_join on the host cores; loads untimed, joins timed."""
+REC_DTYPE = np.dtype([("r", "<u4"), ("s", "<u4"), ("lb", "<f8"), ("ub", "<f8"), ("stage", "<i2"), ("pad", "<i2"),
+                      ("rank", "<u4")])
+
+
+def stage_name(code):
+    """Reference stage_name (proj/src/engine.cpp: mbb / voxel / lod-L, 100 -> exact)."""
+    code = int(code)
+    return {-3: "undecided", -2: "mbb", -1: "voxel", 100: "exact"}.get(code, f"lod-{code}")
+
+
+def ref_join(lib, r_path, s_path, kw, lods, workers, repeats=1, records_path=None):
+    """The reference's own run_join on the host cores; loads untimed, joins timed. With
+    `records_path` the last join's records are returned as (r, s, lb, ub, stage, rank) tuples."""
     arr = (ctypes.c_uint32 * len(lods))(*lods)
     out = (ctypes.c_double * 6)()
-    rc = lib.ref_join_timed(r_path.encode(), s_path.encode(), TYPE_CODE[kw["type"]], float(kw.get("tau", 0.0)),
-                            int(kw.get("k", 1)), arr, len(lods), workers, repeats, out)
+    rc = lib.ref_join_timed_records(r_path.encode(), s_path.encode(), TYPE_CODE[kw["type"]],
+                                    float(kw.get("tau", 0.0)), int(kw.get("k", 1)), arr, len(lods), workers, repeats,
+                                    out, records_path.encode() if records_path else None)
     if rc != 0:
         raise RuntimeError("reference join failed: " + lib.ref_last_error().decode())
-    return {"ms": out[0], "pairs_in": out[1], "facet_pairs": out[2], "results": out[3], "cores": int(out[4])}
+    res = {"ms": out[0], "pairs_in": out[1], "facet_pairs": out[2], "results": out[3], "cores": int(out[4])}
+    if records_path:
+        rec = np.fromfile(records_path, dtype=REC_DTYPE)
+        res["records"] = [(int(x["r"]), int(x["s"]), float(x["lb"]), float(x["ub"]), stage_name(x["stage"]),
+                           int(x["rank"])) for x in rec]
+    return res
+
+
+def slice_parity(gpu_records, ref_records, stride):
+    """Bitwise comparison of the GPU's records of queries r % stride == 0 with the reference's
+    records of the R-slice (slice query r' is query r' * stride; per-query independence,
+    SURVEY §8e). lb / ub compare as IEEE bit patterns."""
+    def key(rec):
+        r, s, lb, ub, stage, rank = rec
+        return (r, s, np.float64(lb).view(np.uint64).item(), np.float64(ub).view(np.uint64).item(), stage, rank)
+    mine = [key(x) for x in gpu_records if x[0] % stride == 0]
+    theirs = [key((r * stride,) + tuple(rest)) for r, *rest in ref_records]
+    mismatches = sum(1 for a, b in zip(mine, theirs) if a != b) + abs(len(mine) - len(theirs))
+    return {"stride": stride, "slice_records": len(theirs), "gpu_records": len(mine), "mismatches": mismatches,
+            "compared": "r, s, lb bits, ub bits, stage, rank of every record, in the reference's order"}
+
+
+def load_synth_tables():
+    """paper_2604_19982_b200/synth.py loaded as a plain module (its CONFIGS / LODS tables)
+    without importing the package, so the reference arm never maps this repo's libraries."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("tj_synth_tables",
+                                                  os.path.join(ROOT, "paper_2604_19982_b200", "synth.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def build_slice_subprocess(name, data_dir, scale, stride):
+    """Slice index files for the reference arm, written by a separate process so the timed
+    reference process maps only oracle/_ref (the writer is this repo's replicate_index)."""
+    code = ("import sys, json; sys.path.insert(0, %r); from paper_2604_19982_b200 import synth; "
+            "print(json.dumps(synth.build_config(%r, %r, scale=%r, r_stride=%d)))" % (ROOT, name, data_dir, scale,
+                                                                                     stride))
+    out = subprocess.run([sys.executable, "-c", code], check=True, capture_output=True, text=True).stdout
+    return tuple(json.loads(out.strip().splitlines()[-1]))
 
 
 def main():
     a = parse()
     world, rank, local = dist_env()
-    from paper_2604_19982_b200 import synth
+    synth = load_synth_tables()
 
     name = a.config
     _, _, kw = synth.CONFIGS[name]
@@ -171,7 +238,7 @@ def main():
     if a.impl == "reference":
         if rank != 0:
             return 0
-        r_slice, s_path = synth.build_config(name, data_dir, scale=a.scale, r_stride=a.ref_stride)
+        r_slice, s_path = build_slice_subprocess(name, data_dir, a.scale, a.ref_stride)
         lib = ref_shim()
         workers = os.cpu_count() or 1
         times, last = [], None
@@ -203,6 +270,7 @@ def main():
     os.environ.setdefault("TRIJOIN_DEVICES", str(local))
     import paper_2604_19982_b200 as tj
     from paper_2604_19982_b200 import _core
+    from paper_2604_19982_b200 import synth
 
     # ---- inputs (built once per box; node-local rank 0 writes, others wait) ----
     t_setup = time.time()
@@ -271,15 +339,21 @@ def main():
 
     peaks, peak_src = measured_peaks()
     fp32_peak = 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12  # TFLOP/s
-    work_flop = evaluated * FLOP_PER_PAIR + tested * FLOP_PER_TEST + screened * FLOP_PER_SAT
+    work_flop = evaluated * FLOP_PER_PAIR + tested * FLOP_PER_TEST
     achieved = work_flop / (kernel_ms / 1e3) / 1e12 / max(world, 1)
+    b_flop = evaluated * FLOP_PER_PAIR + tested * B_FLOP_PER_TEST + screened * B_FLOP_PER_SAT
+    b_achieved = b_flop / (kernel_ms / 1e3) / 1e12 / max(world, 1)
     brute_peak_pairs = fp32_peak * 1e12 / FLOP_PER_PAIR  # every reference facet pair through tri_tri at FP32 peak
     traffic, traffic_src = ncu_traffic(a.config)
     roofline = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
                 "frac": achieved / fp32_peak, "traffic": traffic, "traffic_source": traffic_src,
-                "kernel": "refinement kernels k_seed + k_screen + k_eval (all LOD levels, CUDA events)",
-                "flop_model": f"{FLOP_PER_TEST:g} x box tests + {FLOP_PER_SAT:g} x separating-axis tests + "
-                              f"{FLOP_PER_PAIR:g} x exact FP64 evaluations (counted on device)",
+                "kernel": "refinement kernels k_seed + k_screen + k_eval (all LOD levels, CUDA events on their stream)",
+                "flop_model": f"SURVEY 8(d): {FLOP_PER_PAIR:g} x exact FP64 evaluations + {FLOP_PER_TEST:g} x box "
+                              "tests (both counted on the device)",
+                "builder_model": {"achieved": b_achieved, "frac": b_achieved / fp32_peak,
+                                  "flop_model": f"{B_FLOP_PER_TEST:g} x box tests + {B_FLOP_PER_SAT:g} x "
+                                                f"separating-axis tests + {FLOP_PER_PAIR:g} x exact evaluations"},
+                "ncu_pipes": ncu_pipes(a.config),
                 "peak_source": f"148 SM x 128 FP32 lanes x 2 x sm_max_mhz ({peak_src} MEASURED_PEAKS.json)",
                 "pairs_evaluated_per_s": evaluated / (kernel_ms / 1e3) / max(world, 1),
                 "ref_equiv_facet_pairs_per_s": fp / (kernel_ms / 1e3) / max(world, 1),
@@ -288,6 +362,7 @@ def main():
 
     # ---- e2e: public API from host buffers ----
     e2e = None
+    gpu_records = None
     if not a.no_e2e:
         ts = []
         parts = []
@@ -303,6 +378,7 @@ def main():
             t1 = time.perf_counter()
             if i > 0:
                 ts.append((t1 - t0) * 1e3)
+            gpu_records = recs
             st = json.loads(js)
             n_c = st["stages"][0]["pairs_in"] - st["stages"][0]["removed"]
             d2h = n_c * (4 + 4 + 8 + 8 + 1 + 2) + (R.n_objects + 1) * 8 + R.n_objects * 4
@@ -329,10 +405,17 @@ def main():
                "timeline_ms": parts[-1].get("timeline", {}) if parts else {}}
 
     cpu = None
+    parity = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         try:
             r_slice, s_full = synth.build_config(name, data_dir + "_slice", scale=a.scale, r_stride=a.cpu_stride)
-            rj = ref_join(ref_shim(), r_slice, s_full, kw, lods, os.cpu_count() or 1)
+            if gpu_records is None:  # the public API's records of the full workload (untimed)
+                gpu_records, _ = _core.join_datasets(R, S, type=kw["type"], tau=float(kw.get("tau", 0.0)),
+                                                     k=int(kw.get("k", 1)), lods=lods)
+            rec_path = os.path.join(data_dir + "_slice", "ref_records.bin")
+            rj = ref_join(ref_shim(), r_slice, s_full, kw, lods, os.cpu_count() or 1, records_path=rec_path)
+            parity = slice_parity(gpu_records, rj["records"], a.cpu_stride)
+            parity["slice_candidates"] = int(rj["pairs_in"])
             cpu = {"value": rj["pairs_in"] / (rj["ms"] / 1e3), "unit": "pairs/s", "cores": rj["cores"],
                    "kind": "reference",
                    "sample": f"reference run_join (oracle/_ref) on every {a.cpu_stride}th query object vs the full S: "
@@ -356,10 +439,14 @@ def main():
                            "step_ms": [round(x, 2) for x in step_ms],
                            "levels_last_step": outs[-1]["levels"]},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
-                "gpu_launches": int(launches)}
+                "gpu_launches": int(launches), "parity": parity}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+    if parity is not None and parity["mismatches"]:
+        print(f"PARITY FAILURE: {parity['mismatches']} record mismatches against the reference slice",
+              file=sys.stderr)
+        return 3
     return 0
 
 

@@ -154,6 +154,7 @@ typedef struct tj_join_result {
     uint64_t level_facets_dropped[TJ_MAX_LODS];  /* facets dropped by the row/column screens */
     double level_wait_ms[TJ_MAX_LODS];           /* host time blocked on a streamed level */
     int32_t decision_mode;                       /* 1: refined in decision mode (TJ_FLAG_EXACT_INTERVALS) */
+    uint32_t queue_reruns;                       /* levels re-run after an exact-queue overflow */
 } tj_join_result;
 
 /* ---- context ---- */

@@ -172,9 +172,21 @@ int ref_staged_dump(const char* r_path, const char* s_path, double tau, const ui
 // out[0] = best wall ms, out[1] = candidate pairs entering the voxel stage
 // (stats stages["voxel"].pairs_in), out[2] = sum of facet_pairs, out[3] = results,
 // out[4] = pool size, out[5] = total candidate pairs.
+int ref_join_timed_records(const char* r_path, const char* s_path, int type, double tau, uint32_t k,
+                           const uint32_t* lods, uint32_t n_lods, unsigned workers, uint32_t repeats,
+                           double* out, const char* records_path);
 int ref_join_timed(const char* r_path, const char* s_path, int type, double tau, uint32_t k,
                    const uint32_t* lods, uint32_t n_lods, unsigned workers, uint32_t repeats,
                    double* out) {
+    return ref_join_timed_records(r_path, s_path, type, tau, k, lods, n_lods, workers, repeats, out, nullptr);
+}
+
+// Same, and the last join's records (JoinResultRecord, include/trijoin/engine.hpp:36-41, in
+// the reference's own order) are written to `records_path` (when non-NULL) as packed
+// 32-byte rows: u32 r, u32 s, f64 lb, f64 ub, i16 decided_at, i16 0, u32 rank.
+int ref_join_timed_records(const char* r_path, const char* s_path, int type, double tau, uint32_t k,
+                           const uint32_t* lods, uint32_t n_lods, unsigned workers, uint32_t repeats,
+                           double* out, const char* records_path) {
     return guarded([&] {
         const PreparedDataset R = load_index(r_path);
         PreparedDataset s_store;
@@ -208,6 +220,23 @@ int ref_join_timed(const char* r_path, const char* s_path, int type, double tau,
         out[5] = jo.stats.stages.empty()
                      ? 0.0
                      : static_cast<double>(jo.stats.stages[0].pairs_in - jo.stats.stages[0].removed);
+        if (records_path && *records_path) {
+            std::FILE* f = std::fopen(records_path, "wb");
+            if (!f) throw std::runtime_error(std::string("cannot write ") + records_path);
+            for (const JoinResultRecord& rec : jo.records) {
+                unsigned char row[32] = {};
+                const int16_t pad = 0;
+                std::memcpy(row, &rec.r, 4);
+                std::memcpy(row + 4, &rec.s, 4);
+                std::memcpy(row + 8, &rec.lb, 8);
+                std::memcpy(row + 16, &rec.ub, 8);
+                std::memcpy(row + 24, &rec.decided_at, 2);
+                std::memcpy(row + 26, &pad, 2);
+                std::memcpy(row + 28, &rec.rank, 4);
+                std::fwrite(row, 1, 32, f);
+            }
+            std::fclose(f);
+        }
     });
 }
 

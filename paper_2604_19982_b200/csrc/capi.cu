@@ -736,12 +736,18 @@ int tj_join(tj_ctx* ctx, const tj_dataset* Rh, const tj_dataset* Sh, const tj_jo
             out->level_wait_ms[i] = ro.levels[i].wait_ms;
         }
         out->refine_chunks = ro.chunks;
+        out->queue_reruns = ro.queue_reruns;
 
         if (sp.flags & TJ_FLAG_EXACT_RECOMPUTE) exact_recompute_dev(ws, R, S, cs, st);
 
-        // streamed datasets: the device-side validation of the levels this join used
+        // streamed datasets: the device-side validation of every level the join asked for
+        // (levels the refinement never reached included: the join stream first waits on each
+        // level's arrival event, so the flag does not depend on how early refinement ended)
         for (const DatasetDev* D : {&R, &S}) {
             if (!D->gate) continue;
+            for (uint32_t li = 0; li < sp.n_lods; ++li)
+                for (size_t slot = 0; slot < D->levels.size(); ++slot)
+                    if (D->levels[slot] == (int32_t)sp.lods[li]) level_ready(*D, (int)slot, st);
             int bad = 0;
             TJ_CUDA(cudaMemcpyAsync(&bad, D->stream_err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
             stream_sync(st);

@@ -148,6 +148,7 @@ struct LevelStats {
 struct RefineLoopOut {
     std::vector<LevelStats> levels;
     uint64_t chunks = 0;
+    uint32_t queue_reruns = 0; // levels re-run after an exact-queue overflow
 };
 struct TraceSink; // host-side trace forwarding (engine.cu)
 RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetDev& S, CandDevStore& cs,

@@ -4,6 +4,8 @@
 // __d*_rn intrinsics).
 #include <cuda_runtime.h>
 #include <cstdlib>
+#include <mutex>
+#include <set>
 #include <type_traits>
 
 #include "refine_kernel.cuh"
@@ -931,10 +933,18 @@ void refine_pass(const RefineSource& src, uint64_t vp_begin, uint64_t vp_end, bo
                  unsigned long long* ub_bits, int cull, RefineQueueStore& qs, unsigned long long* work,
                  unsigned long long* counters, int num_sms, cudaStream_t st) {
     if (vp_end <= vp_begin) return;
-    static bool attr = false;
-    if (!attr) {
-        TJ_CUDA(cudaFuncSetAttribute(k_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScreenSmem));
-        attr = true;
+    // the dynamic shared-memory opt-in is per device: set once per device this process uses
+    // (several host threads may drive several GPUs, run_join's shard threads)
+    {
+        static std::mutex mu;
+        static std::set<int> done;
+        int dev = 0;
+        TJ_CUDA(cudaGetDevice(&dev));
+        std::lock_guard<std::mutex> lk(mu);
+        if (!done.count(dev)) {
+            TJ_CUDA(cudaFuncSetAttribute(k_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScreenSmem));
+            done.insert(dev);
+        }
     }
     const int grid = num_sms * 8;
     if (seed) {

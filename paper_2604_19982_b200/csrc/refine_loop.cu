@@ -160,6 +160,8 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
     TJ_CUDA(cudaEventCreate(&e1));
     const unsigned long long kInfBits = 0x7ff0000000000000ull;
     const uint64_t launch = std::max<uint64_t>(spec.refine_chunk, 1ull << 24);
+    uint64_t test_queue_cap = 0;
+    if (const char* e = std::getenv("TRIJOIN_TEST_QUEUE_CAP"); e && *e) test_queue_cap = std::strtoull(e, nullptr, 10);
     try {
         for (uint32_t li = 0; li < spec.n_lods; ++li) {
             if (n_active == 0) break;
@@ -204,6 +206,7 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
                 TJ_CUDA(cudaMemsetAsync(dbg.p, 0, n * 8, st));
                 refine_debug_op_tested(dbg.p);
             }
+            queue.cap = test_queue_cap;
             for (;;) {
                 count_launch();
                 k_fill_u64<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(lbb.p, n, kInfBits);
@@ -233,7 +236,9 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
                 if (ovf == 0) break;
                 // an exact-evaluation queue overflowed somewhere in the level: grow it and
                 // redo the level (the screen is deterministic given the same evaluations)
-                queue.items.alloc(ovf + ovf / 4);
+                if (ovf + ovf / 4 > queue.items.n) queue.items.alloc(ovf + ovf / 4);
+                queue.cap = 0;
+                ++out.queue_reruns;
             }
             out.chunks += (n_active + spec.refine_chunk - 1) / spec.refine_chunk;
             if (dbg.n) refine_debug_op_tested(nullptr);
@@ -404,6 +409,8 @@ void exact_recompute_dev(Workspace& ws, const DatasetDev& R, const DatasetDev& S
     }
     if (!ws.queue) ws.queue = std::make_unique<RefineQueueStore>();
     RefineQueueStore& queue = *ws.queue;
+    queue.cap = 0;
+    if (const char* e = std::getenv("TRIJOIN_TEST_QUEUE_CAP"); e && *e) queue.cap = std::strtoull(e, nullptr, 10);
     const uint64_t launch = 1ull << 20;
     for (;;) {
         count_launch();
@@ -421,7 +428,8 @@ void exact_recompute_dev(Workspace& ws, const DatasetDev& R, const DatasetDev& S
         TJ_CUDA(cudaMemcpyAsync(&ovf, queue.count.p + 1, 8, cudaMemcpyDeviceToHost, st));
         stream_sync(st);
         if (ovf == 0) break;
-        queue.items.alloc(ovf + ovf / 4);
+        if (ovf + ovf / 4 > queue.items.n) queue.items.alloc(ovf + ovf / 4);
+        queue.cap = 0;
     }
     count_launch();
     k_exact_store<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(cs.view(), n, lbb.p);

@@ -183,8 +183,15 @@ struct RefineQueue {
 struct RefineQueueStore {
     DevBuf<PairRef> items;              // exact-evaluation queue
     DevBuf<unsigned long long> count; // [0] entries of the current pass, [1] largest overflowing count
+    // Test hook ($TRIJOIN_TEST_QUEUE_CAP, read per level by refine_loop_dev): the passes of a
+    // level see at most `cap` slots until the first overflow grows the queue, so the
+    // overflow -> grow -> re-run path runs on small inputs. 0 = no cap.
+    uint64_t cap = 0;
     RefineQueueStore() : count(2) { items.alloc(1u << 22); }
-    RefineQueue view() { return {items.p, (unsigned long long)items.n, count.p}; }
+    RefineQueue view() {
+        const uint64_t n = cap && cap < items.n ? cap : items.n;
+        return {items.p, (unsigned long long)n, count.p};
+    }
 };
 
 // FP32 screening records of n facet records (refine.cu, k_prep) into out[7 n]: box parts at

@@ -197,3 +197,83 @@ def test_benchmark_configs_match_reference(ref_module, tmp_path, cfg, scale):
     assert a["records"] == b["records"]
     strip = lambda st: [{k: v for k, v in x.items() if k != "wall_ms"} for x in st["stages"]]
     assert strip(a["stats"]) == strip(b["stats"])
+
+
+ADVERSARIAL = tjtest.adversarial_joins()
+
+
+@pytest.mark.parametrize("j", ADVERSARIAL, ids=tjtest.join_id)
+def test_adversarial_culling_matches_reference(j):
+    """Near-parallel faces / edges at gaps 1e-12 .. 1e-2 and sliver facets (sin ~ 5e-3 .. 1.7e-2)
+    at coordinates around +-100 (tests/golden/make_adversarial.py): the exact-preserving culling
+    margins (refine_kernel.cuh) must leave records and every stage counter equal to the
+    reference's."""
+    import paper_2604_19982_b200 as tj
+    r, s = _paths(j)
+    out = tj.join(r, s, **j["kwargs"])
+    assert out["records"] == j["records"]
+    stages = [{k: v for k, v in st.items() if k != "wall_ms"} for st in out["stats"]["stages"]]
+    assert stages == j["stages"]
+
+
+@pytest.mark.parametrize("j", [j for j in ADVERSARIAL if j["kwargs"]["type"] in ("intersect", "within")
+                               and not j["kwargs"].get("exact")], ids=tjtest.join_id)
+def test_adversarial_intervals_bitwise_vs_no_cull(capi, j):
+    """Every candidate interval (not only the records) equals the exhaustive evaluation's
+    (culling off), with exact intervals on: the culling skipped nothing that mattered."""
+    r, s = _paths(j)
+    R = capi.load(r)
+    S = capi.load(s) if s else R
+    try:
+        kw = dict(j["kwargs"])
+        lods = tuple(kw.pop("lods"))
+        base = capi.join(R, S, lods=lods, flags=1 | 4, **kw)
+        c = capi.join(R, S, lods=lods, flags=4, **kw)
+        for key in ("pair_r", "pair_s", "status", "decided_at"):
+            assert (c[key] == base[key]).all()
+        assert (tjtest.bits(c["lb"]) == tjtest.bits(base["lb"])).all()
+        assert (tjtest.bits(c["ub"]) == tjtest.bits(base["ub"])).all()
+    finally:
+        capi.free(R)
+        if s:
+            capi.free(S)
+
+
+@pytest.mark.parametrize("kw", [dict(type="within", tau=0.5), dict(type="knn", k=3), dict(type="intersect"),
+                                dict(type="within", tau=0.5, exact=True)])
+def test_exact_queue_overflow_rerun(capi, monkeypatch, kw):
+    """A level whose exact-evaluation queue overflows is re-run with a larger queue
+    (refine_loop.cu): forced here with a 16-slot queue; results are bit-identical."""
+    R = capi.load(golden("nuclei60.idx"))
+    S = capi.load(golden("vessels8.idx"))
+    try:
+        lods = (20, 60, 100)
+        base = capi.join(R, S, lods=lods, **kw)
+        assert base["queue_reruns"] == 0
+        monkeypatch.setenv("TRIJOIN_TEST_QUEUE_CAP", "16")
+        c = capi.join(R, S, lods=lods, **kw)
+        assert c["queue_reruns"] > 0
+        for key in ("pair_r", "pair_s", "status", "decided_at"):
+            assert (c[key] == base[key]).all()
+        assert (tjtest.bits(c["lb"]) == tjtest.bits(base["lb"])).all()
+        assert (tjtest.bits(c["ub"]) == tjtest.bits(base["ub"])).all()
+    finally:
+        capi.free(R)
+        capi.free(S)
+
+
+@pytest.mark.parametrize("cfg,scale", [("B", 0.02), ("D", 0.001), ("C", 0.005)])
+def test_benchmark_scale_matches_reference(ref_module, tmp_path, cfg, scale):
+    """Larger slices of the benchmark configurations (B: 2k x 2k nuclei, ~7k candidate pairs;
+    D: 1k x 1k at tau 0.2; C: 1k nuclei x 50 vessels k-NN) against the live reference build:
+    every record bit for bit (repr of the doubles) and every stage counter."""
+    import paper_2604_19982_b200 as tj
+    from paper_2604_19982_b200 import synth
+    r, s = synth.build_config(cfg, str(tmp_path), scale=scale)
+    kw = dict(synth.CONFIGS[cfg][2], lods=synth.LODS)
+    a = ref_module.join(r, s, **kw)
+    b = tj.join(r, s, **kw)
+    assert len(a["records"]) > 100
+    assert [tuple(map(repr, x)) for x in a["records"]] == [tuple(map(repr, x)) for x in b["records"]]
+    strip = lambda st: [{k: v for k, v in x.items() if k != "wall_ms"} for x in st["stages"]]
+    assert strip(a["stats"]) == strip(b["stats"])

@@ -29,7 +29,7 @@ def test_oracle_mindist_bitexact(oracle_lib):
     assert (bits(out) == bits(g["d"])).all()
 
 
-@pytest.mark.parametrize("j", tjtest.golden_joins(), ids=tjtest.join_id)
+@pytest.mark.parametrize("j", tjtest.golden_joins() + tjtest.adversarial_joins(), ids=tjtest.join_id)
 def test_oracle_join_matches_reference(oracle_lib, j):
     kw = dict(j["kwargs"])
     lods = kw.pop("lods", [20, 40, 60, 80, 100])

@@ -65,7 +65,8 @@ class JoinResult(ctypes.Structure):
                 ("level_pairs_verified", ctypes.c_uint64 * MAXL),
                 ("level_vps_skipped", ctypes.c_uint64 * MAXL),
                 ("level_facets_dropped", ctypes.c_uint64 * MAXL),
-                ("level_wait_ms", ctypes.c_double * MAXL), ("decision_mode", ctypes.c_int32)]
+                ("level_wait_ms", ctypes.c_double * MAXL), ("decision_mode", ctypes.c_int32),
+                ("queue_reruns", ctypes.c_uint32)]
 
 
 def capi_functions():
@@ -172,6 +173,7 @@ class Capi:
             "nq": res.n_queries, "vp_generated": res.vp_generated, "vp_pruned": res.vp_pruned,
             "levels": [(res.level[i], res.level_vps[i], res.level_facet_pairs[i]) for i in range(res.n_levels_run)],
             "decision_mode": res.decision_mode,
+            "queue_reruns": res.queue_reruns,
         }
         self.lib.tj_join_result_free(ctypes.byref(res))
         return out
@@ -241,12 +243,17 @@ def golden(name):
     return os.path.join(GOLDEN, name)
 
 
-def golden_joins():
-    with open(golden("joins.json")) as f:
+def golden_joins(name="joins.json"):
+    with open(golden(name)) as f:
         joins = json.load(f)
     for j in joins:
         j["records"] = [tuple(r) for r in j["records"]]
     return joins
+
+
+def adversarial_joins():
+    """tests/golden/adversarial_joins.json (tests/golden/make_adversarial.py, the reference)."""
+    return golden_joins("adversarial_joins.json")
 
 
 def join_id(j):

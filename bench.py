@@ -19,7 +19,9 @@ object pairs entering the voxel + LOD cascade (stats stages["voxel"].pairs_in).
 
 --impl reference runs only the reference CPU arm (rank 0; other ranks exit 0).
 Multi-GPU (torchrun): query objects are sharded in blocks of 1024 across ranks (no data-path
-collective); result pairs are gathered to rank 0 at the end of the e2e run.
+collective); each rank uploads only its own queries. In the e2e run every step ends with the
+records of all ranks gathered to rank 0 over NCCL (paper_2604_19982_b200.dist.gather_records:
+counts all-gather + padded record all-gather, stable merge by query), inside the timed region.
 """
 import argparse
 import ctypes
@@ -270,6 +272,7 @@ def main():
     os.environ.setdefault("TRIJOIN_DEVICES", str(local))
     import paper_2604_19982_b200 as tj
     from paper_2604_19982_b200 import _core
+    from paper_2604_19982_b200 import dist as tjdist
     from paper_2604_19982_b200 import synth
 
     # ---- inputs (built once per box; node-local rank 0 writes, others wait) ----
@@ -281,11 +284,11 @@ def main():
     r_path, s_path = synth.build_config(name, data_dir, scale=a.scale)
     R = tj.load_dataset(r_path)
     S = tj.load_dataset(s_path) if s_path else R  # "" = self-join (config E)
-    res = tj.Resident(R, S, device=local)
+    # each rank uploads only its own query shard of R (blocks of 1024 queries dealt round-robin)
+    res = tj.Resident(R, S, device=local, shard_index=rank, shard_count=world)
     setup_s = time.time() - t_setup
     flags = 1 if a.no_cull else 0
-    run_kw = dict(type=kw["type"], tau=float(kw.get("tau", 0.0)), k=int(kw.get("k", 1)), lods=lods, flags=flags,
-                  shard_index=rank, shard_count=world)
+    run_kw = dict(type=kw["type"], tau=float(kw.get("tau", 0.0)), k=int(kw.get("k", 1)), lods=lods, flags=flags)
 
     if a.profile:
         out = res.run(**run_kw)
@@ -373,7 +376,9 @@ def main():
             torch.cuda.synchronize(dev)
             t0 = time.perf_counter()
             recs, js = _core.join_datasets(R, S, type=kw["type"], tau=float(kw.get("tau", 0.0)),
-                                           k=int(kw.get("k", 1)), lods=lods)
+                                           k=int(kw.get("k", 1)), lods=lods, records="array")
+            if world > 1:  # records of every rank's shard to rank 0 (NCCL), merged in query order
+                recs = tjdist.gather_records(recs, device=dev)
             torch.cuda.synchronize(dev)
             t1 = time.perf_counter()
             if i > 0:
@@ -381,7 +386,8 @@ def main():
             gpu_records = recs
             st = json.loads(js)
             n_c = st["stages"][0]["pairs_in"] - st["stages"][0]["removed"]
-            d2h = n_c * (4 + 4 + 8 + 8 + 1 + 2) + (R.n_objects + 1) * 8 + R.n_objects * 4
+            n_q = res.n_queries
+            d2h = n_c * (4 + 4 + 8 + 8 + 1 + 2) + (n_q + 1) * 8 + n_q * 4
             pairs_e2e = st["stages"][1]["pairs_in"]
             if i > 0:
                 b = dict(st.get("b200", {}))
@@ -411,7 +417,8 @@ def main():
             r_slice, s_full = synth.build_config(name, data_dir + "_slice", scale=a.scale, r_stride=a.cpu_stride)
             if gpu_records is None:  # the public API's records of the full workload (untimed)
                 gpu_records, _ = _core.join_datasets(R, S, type=kw["type"], tau=float(kw.get("tau", 0.0)),
-                                                     k=int(kw.get("k", 1)), lods=lods)
+                                                     k=int(kw.get("k", 1)), lods=lods, records="array")
+            gpu_records = tjdist.records_to_tuples(gpu_records)
             rec_path = os.path.join(data_dir + "_slice", "ref_records.bin")
             rj = ref_join(ref_shim(), r_slice, s_full, kw, lods, os.cpu_count() or 1, records_path=rec_path)
             parity = slice_parity(gpu_records, rj["records"], a.cpu_stride)

@@ -11,8 +11,12 @@
  * /root/reference/proj):
  *   tj_join            run_join                 include/trijoin/engine.hpp:70-71, src/engine.cpp:122-237
  *   tj_refine_batch    refine_kernel            include/trijoin/refine.hpp:67-68, src/refine.cpp:63-84
+ *   tj_geom_batch      mindist_aabb, point_segment_distance, point_triangle_distance,
+ *                      segment_segment_distance, tri_tri_distance
+ *                                               include/trijoin/geom.hpp:60-79,   src/geom.cpp:11-183
  *   tj_tri_tri_batch   tri_tri_distance         include/trijoin/geom.hpp:79,      src/geom.cpp:152-183
  *   tj_mindist_batch   mindist_aabb             include/trijoin/geom.hpp:60,      src/geom.cpp:11-16
+ *   tj_exhaustive_join run_oracle               include/trijoin/engine.hpp:77-80, src/oracle.cpp:124-186
  *   tj_mbb_filter      mbb_filter_within / _knn include/trijoin/filter.hpp:62-66,   src/filter.cpp:88-190
  *   tj_voxel_filter    chunked_filter           include/trijoin/filter.hpp:111-114, src/filter.cpp:350-448
  *   tj_voxel_bounds    voxel_pair_bounds        include/trijoin/filter.hpp:83-85,   src/filter.cpp:199-239
@@ -309,9 +313,56 @@ int tj_refine_loop(tj_ctx* ctx, const tj_dataset* R, const tj_dataset* S, tj_can
 int tj_knn_prune(tj_ctx* ctx, tj_cand_view* cands, uint32_t k, int16_t stage, int mode, uint8_t* deltas,
                  uint64_t* decisions);
 
-/* Exact FP64 tri_tri_distance / mindist_aabb over n independent inputs. */
+/* ---- geometric primitives (reference include/trijoin/geom.hpp:60-79, src/geom.cpp:11-183) ----
+ * Exact FP64, bit-identical to the reference, over n independent inputs: out[i] = f(a_i, b_i).
+ *   op                         a_i (doubles)             b_i (doubles)              reference
+ *   TJ_GEOM_MINDIST            box min.xyz max.xyz (6)   box (6)                    mindist_aabb            geom.cpp:11-16
+ *   TJ_GEOM_POINT_SEGMENT      point (3)                 segment a.xyz b.xyz (6)    point_segment_distance  geom.cpp:18-24
+ *   TJ_GEOM_POINT_TRIANGLE     point (3)                 triangle v0 v1 v2 (9)      point_triangle_distance geom.cpp:39-80
+ *   TJ_GEOM_SEGMENT_SEGMENT    segment (6)               segment (6)                segment_segment_distance geom.cpp:82-113
+ *   TJ_GEOM_TRI_TRI            triangle (9)              triangle (9)               tri_tri_distance        geom.cpp:152-183
+ * Calls of up to 256 inputs go through a page-locked mapped mailbox (no allocation, no copy
+ * engine): one kernel launch and one stream wait. */
+enum {
+    TJ_GEOM_MINDIST = 0,
+    TJ_GEOM_POINT_SEGMENT = 1,
+    TJ_GEOM_POINT_TRIANGLE = 2,
+    TJ_GEOM_SEGMENT_SEGMENT = 3,
+    TJ_GEOM_TRI_TRI = 4
+};
+int tj_geom_batch(tj_ctx* ctx, int32_t op, uint64_t n, const double* a, const double* b, double* out);
+/* Shorthands: tj_geom_batch(TJ_GEOM_TRI_TRI / TJ_GEOM_MINDIST, ...). */
 int tj_tri_tri_batch(tj_ctx* ctx, uint64_t n, const double* a9, const double* b9, double* out);
 int tj_mindist_batch(tj_ctx* ctx, uint64_t n, const double* a6, const double* b6, double* out);
+
+/* ---- exhaustive exact join (backs run_oracle, reference include/trijoin/engine.hpp:77-80,
+ * src/oracle.cpp:124-186) ----
+ * Over the level-100 (original-resolution) triangles only; shares nothing with the engine's
+ * bound machinery except the exact geometric primitives. Within / intersect (tau 0): every
+ * (r, s) whose facet-bounds boxes are within tau gets its exact distance d = min over all
+ * facet pairs of tri_tri_distance; records d <= tau in (r, s) order. k-NN: per r the k
+ * smallest (d, s) over all of S, rank 1..k. Records carry lb = ub = d, stage 100. */
+typedef struct tj_mesh_set_view {
+    uint32_t n_objects;
+    const uint64_t* tri_offsets; /* [n_objects+1] */
+    const double* tris;          /* [tri_offsets[n_objects]*9] v0 v1 v2 per triangle, object order */
+} tj_mesh_set_view;
+
+typedef struct tj_exhaustive_result {
+    uint64_t n_records;
+    uint32_t* r;
+    uint32_t* s;
+    double* d;
+    uint32_t* rank;               /* 0 for within / intersect */
+    uint64_t object_pairs;        /* object pairs whose exact distance was computed */
+    uint64_t facet_pairs_evaluated; /* exact tri_tri evaluations */
+    double total_ms;
+} tj_exhaustive_result;
+
+/* S == NULL: self-join. */
+int tj_exhaustive_join(tj_ctx* ctx, const tj_mesh_set_view* R, const tj_mesh_set_view* S, int32_t type, double tau,
+                       uint32_t k, tj_exhaustive_result* out);
+void tj_exhaustive_result_free(tj_exhaustive_result* res);
 
 #ifdef __cplusplus
 }

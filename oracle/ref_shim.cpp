@@ -54,6 +54,33 @@ void ref_tri_tri_batch(uint64_t n, const double* a9, const double* b9, double* o
     for (uint64_t i = 0; i < n; ++i) out[i] = tri_tri_distance(tri_from(a9 + 9 * i), tri_from(b9 + 9 * i));
 }
 
+// proj/src/geom.cpp:18-24 (a: points [3], b: segments [6])
+void ref_point_segment_batch(uint64_t n, const double* a3, const double* b6, double* out) {
+    for (uint64_t i = 0; i < n; ++i) {
+        const double* p = a3 + 3 * i;
+        const double* q = b6 + 6 * i;
+        out[i] = point_segment_distance({p[0], p[1], p[2]}, {q[0], q[1], q[2]}, {q[3], q[4], q[5]});
+    }
+}
+
+// proj/src/geom.cpp:39-80 (a: points [3], b: triangles [9])
+void ref_point_triangle_batch(uint64_t n, const double* a3, const double* b9, double* out) {
+    for (uint64_t i = 0; i < n; ++i) {
+        const double* p = a3 + 3 * i;
+        out[i] = point_triangle_distance({p[0], p[1], p[2]}, tri_from(b9 + 9 * i));
+    }
+}
+
+// proj/src/geom.cpp:82-113 (a, b: segments [6])
+void ref_segment_segment_batch(uint64_t n, const double* a6, const double* b6, double* out) {
+    for (uint64_t i = 0; i < n; ++i) {
+        const double* p = a6 + 6 * i;
+        const double* q = b6 + 6 * i;
+        out[i] = segment_segment_distance({p[0], p[1], p[2]}, {p[3], p[4], p[5]}, {q[0], q[1], q[2]},
+                                          {q[3], q[4], q[5]});
+    }
+}
+
 // proj/src/geom.cpp:11-16
 void ref_mindist_aabb_batch(uint64_t n, const double* a6, const double* b6, double* out) {
     for (uint64_t i = 0; i < n; ++i) {

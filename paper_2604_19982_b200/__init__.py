@@ -7,8 +7,9 @@ workers, seed, exact). The work runs on B200 GPUs through ``libtrijoin_b200.so``
 include/tj_capi.h); there is no CPU fallback — importing fails loudly if the compiled
 extension is missing, and joining fails loudly without a B200.
 
-Dataset generation / preprocessing / the exhaustive oracle are offline tooling in the
-reference and are out of scope here.
+``oracle(r, s="", **kwargs)`` is the reference's exhaustive exact join (``trijoin.oracle``),
+here on the GPU. Dataset generation / preprocessing are offline tooling in the reference and
+are out of scope.
 """
 
 import json
@@ -28,6 +29,7 @@ from ._core import EngineError, IndexError, Resident, join_datasets, load_datase
 
 __all__ = [
     "join",
+    "oracle",
     "join_datasets",
     "load_dataset",
     "replicate_index",
@@ -47,4 +49,12 @@ def join(r, s="", **kwargs):
     the reference's ``trijoin.join``.
     """
     records, stats = _core.join(r, s, **kwargs)
+    return {"records": records, "stats": json.loads(stats)}
+
+
+def oracle(r, s="", **kwargs):
+    """Exact reference join over the original-resolution geometry (reference ``trijoin.oracle``),
+    evaluated on the GPU. Same result shape as :func:`join`; accepts type, tau, k, workers, seed.
+    """
+    records, stats = _core.oracle(r, s, **kwargs)
     return {"records": records, "stats": json.loads(stats)}

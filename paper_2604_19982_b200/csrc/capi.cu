@@ -830,32 +830,4 @@ int tj_refine_batch(tj_ctx* ctx, uint64_t n_tris, const double* tris, const doub
     });
 }
 
-int tj_tri_tri_batch(tj_ctx* ctx, uint64_t n, const double* a9, const double* b9, double* out) {
-    if (!ctx) return TJ_EINVAL;
-    return guarded(ctx, [&] {
-        cudaStream_t st = ctx->stream;
-        if (!n) return;
-        DevBuf<double> a, b, o(n);
-        upload(a, a9, 9 * n, st);
-        upload(b, b9, 9 * n, st);
-        launch_tri_tri_batch(n, a.p, b.p, o.p, st);
-        TJ_CUDA(cudaMemcpyAsync(out, o.p, n * 8, cudaMemcpyDeviceToHost, st));
-        stream_sync(st);
-    });
-}
-
-int tj_mindist_batch(tj_ctx* ctx, uint64_t n, const double* a6, const double* b6, double* out) {
-    if (!ctx) return TJ_EINVAL;
-    return guarded(ctx, [&] {
-        cudaStream_t st = ctx->stream;
-        if (!n) return;
-        DevBuf<double> a, b, o(n);
-        upload(a, a6, 6 * n, st);
-        upload(b, b6, 6 * n, st);
-        launch_mindist_batch(n, a.p, b.p, o.p, st);
-        TJ_CUDA(cudaMemcpyAsync(out, o.p, n * 8, cudaMemcpyDeviceToHost, st));
-        stream_sync(st);
-    });
-}
-
 } // extern "C"

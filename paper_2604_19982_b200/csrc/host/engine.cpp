@@ -42,7 +42,7 @@ namespace detail {
 namespace {
 struct CtxRegistry {
     std::mutex mu;
-    std::map<int, tj_ctx*> ctxs;
+    std::map<std::pair<int, int>, tj_ctx*> ctxs;
     ~CtxRegistry() {
         for (auto& [d, c] : ctxs) tj_ctx_destroy(c);
     }
@@ -53,15 +53,15 @@ CtxRegistry& registry() {
 }
 } // namespace
 
-tj_ctx* device_context(int device) {
+tj_ctx* device_context(int device, int slot) {
     CtxRegistry& reg = registry();
     std::lock_guard<std::mutex> lk(reg.mu);
-    auto it = reg.ctxs.find(device);
+    auto it = reg.ctxs.find({device, slot});
     if (it != reg.ctxs.end()) return it->second;
     tj_ctx* c = nullptr;
     const int rc = tj_ctx_create(device, &c);
     if (rc != TJ_OK) throw std::runtime_error(std::string("trijoin: no usable B200 device: ") + tj_global_last_error());
-    reg.ctxs[device] = c;
+    reg.ctxs[{device, slot}] = c;
     return c;
 }
 
@@ -163,9 +163,13 @@ uint64_t PackedDataset::bytes() const {
     return b;
 }
 
-std::unique_ptr<PackedDataset> pack_dataset(const PreparedDataset& ds, ThreadPool& pool) {
+std::unique_ptr<PackedDataset> pack_dataset(const PreparedDataset& ds, ThreadPool& pool, const std::vector<uint32_t>* ids) {
     auto p = std::make_unique<PackedDataset>();
-    const size_t no = ds.objects.size();
+    const size_t no = ids ? ids->size() : ds.objects.size();
+    auto obj_at = [&](size_t o) -> const PreparedObject& { return ds.objects[ids ? (*ids)[o] : o]; };
+    if (ids)
+        for (size_t i = 0; i < ids->size(); ++i)
+            if ((*ids)[i] >= ds.objects.size()) throw std::invalid_argument("trijoin: shard object id out of range");
     const size_t nl = ds.lod_schedule.size();
     p->n_objects = static_cast<uint32_t>(no);
     p->levels.assign(ds.lod_schedule.begin(), ds.lod_schedule.end());
@@ -173,7 +177,7 @@ std::unique_ptr<PackedDataset> pack_dataset(const PreparedDataset& ds, ThreadPoo
     p->anchor.resize(3 * no);
     p->voxel_offsets.assign(no + 1, 0);
     for (size_t o = 0; o < no; ++o) {
-        const PreparedObject& obj = ds.objects[o];
+        const PreparedObject& obj = obj_at(o);
         if (obj.ladder.levels.size() != nl || obj.voxels.facets_per_level.size() != nl)
             throw std::invalid_argument("trijoin: object level count does not match the lod schedule");
         p->voxel_offsets[o + 1] = p->voxel_offsets[o] + obj.voxels.voxel_count();
@@ -185,7 +189,7 @@ std::unique_ptr<PackedDataset> pack_dataset(const PreparedDataset& ds, ThreadPoo
     p->facets.resize(nl);
     // per level: facet entries per voxel -> offsets
     pool.parallel_jobs(no, [&](size_t o) {
-        const PreparedObject& obj = ds.objects[o];
+        const PreparedObject& obj = obj_at(o);
         const uint64_t v0 = p->voxel_offsets[o];
         for (size_t li = 0; li < nl; ++li)
             for (uint32_t v = 0; v < obj.voxels.voxel_count(); ++v)
@@ -197,7 +201,7 @@ std::unique_ptr<PackedDataset> pack_dataset(const PreparedDataset& ds, ThreadPoo
         p->facets[li].resize(fo[nv] * TJ_FACET_STRIDE);
     }
     pool.parallel_jobs(no, [&](size_t o) {
-        const PreparedObject& obj = ds.objects[o];
+        const PreparedObject& obj = obj_at(o);
         const double m[6] = {obj.mbb.min.x, obj.mbb.min.y, obj.mbb.min.z, obj.mbb.max.x, obj.mbb.max.y, obj.mbb.max.z};
         std::memcpy(&p->mbb[6 * o], m, sizeof(m));
         p->anchor[3 * o] = obj.anchor.x;
@@ -259,11 +263,19 @@ std::unique_ptr<PackedDataset> pack_dataset(const PreparedDataset& ds, ThreadPoo
 }
 
 namespace {
-// A contiguous run of a dataset's objects (the packers' view: R chunks of the out-of-core path).
-struct ObjRange {
-    std::span<const PreparedObject> objects;
-    ObjRange(const PreparedObject* p, size_t n) : objects(p, n) {}
+// The objects a header is packed from: a contiguous run (R chunks of the out-of-core path) or
+// a list of global ids (query shards).
+struct ObjSel {
+    const PreparedObject* base;
+    size_t n;
+    const uint32_t* ids;
+    size_t size() const { return n; }
+    const PreparedObject& operator[](size_t i) const { return base[ids ? ids[i] : i]; }
 };
+ObjSel select(const PreparedDataset& ds, const PackedHeader& h) {
+    return h.ids.empty() ? ObjSel{ds.objects.data() + h.first, h.n_objects, nullptr}
+                         : ObjSel{ds.objects.data(), h.n_objects, h.ids.data()};
+}
 
 // fn(begin, end) over [0, n) in ~8 contiguous blocks per worker (one pool job per block).
 void for_blocks(ThreadPool& pool, size_t n, const std::function<void(size_t, size_t)>& fn) {
@@ -285,14 +297,35 @@ uint64_t PackedHeader::bytes() const {
     return b;
 }
 
+std::unique_ptr<PackedHeader> pack_header_sel(const PreparedDataset& dsf, std::unique_ptr<PackedHeader> h,
+                                              ThreadPool& pool);
+
 std::unique_ptr<PackedHeader> pack_header(const PreparedDataset& ds, ThreadPool& pool) {
     return pack_header(ds, 0, ds.objects.size(), pool);
 }
 
+std::unique_ptr<PackedHeader> pack_header(const PreparedDataset& dsf, std::vector<uint32_t> ids, ThreadPool& pool) {
+    for (size_t i = 0; i < ids.size(); ++i)
+        if (ids[i] >= dsf.objects.size() || (i && ids[i] <= ids[i - 1]))
+            throw std::invalid_argument("trijoin: shard object ids must be ascending and in range");
+    auto h = std::make_unique<PackedHeader>();
+    h->ids = std::move(ids);
+    h->n_objects = static_cast<uint32_t>(h->ids.size());
+    if (h->ids.empty()) h->first = dsf.objects.size(); // an empty selection
+    return pack_header_sel(dsf, std::move(h), pool);
+}
+
 std::unique_ptr<PackedHeader> pack_header(const PreparedDataset& dsf, size_t first, size_t last, ThreadPool& pool) {
     auto h = std::make_unique<PackedHeader>();
-    const ObjRange ds{dsf.objects.data() + first, last - first};
-    const size_t no = ds.objects.size();
+    h->first = first;
+    h->n_objects = static_cast<uint32_t>(last - first);
+    return pack_header_sel(dsf, std::move(h), pool);
+}
+
+std::unique_ptr<PackedHeader> pack_header_sel(const PreparedDataset& dsf, std::unique_ptr<PackedHeader> h,
+                                              ThreadPool& pool) {
+    const ObjSel ds = select(dsf, *h);
+    const size_t no = ds.size();
     const size_t nl = dsf.lod_schedule.size();
     h->n_objects = static_cast<uint32_t>(no);
     h->levels.assign(dsf.lod_schedule.begin(), dsf.lod_schedule.end());
@@ -311,7 +344,7 @@ std::unique_ptr<PackedHeader> pack_header(const PreparedDataset& dsf, size_t fir
     std::atomic<int> bad_levels{0}, bad_pad{0};
     for_blocks(pool, no, [&](size_t b, size_t e) {
         for (size_t o = b; o < e; ++o) {
-            const PreparedObject& obj = ds.objects[o];
+            const PreparedObject& obj = ds[o];
             if (obj.ladder.levels.size() != nl || obj.voxels.facets_per_level.size() != nl) {
                 bad_levels = 1;
                 continue;
@@ -350,7 +383,7 @@ std::unique_ptr<PackedHeader> pack_header(const PreparedDataset& dsf, size_t fir
     }
     for_blocks(pool, no, [&](size_t b, size_t e) {
         for (size_t o = b; o < e; ++o) {
-            const PreparedObject& obj = ds.objects[o];
+            const PreparedObject& obj = ds[o];
             const double m[6] = {obj.mbb.min.x, obj.mbb.min.y, obj.mbb.min.z, obj.mbb.max.x, obj.mbb.max.y, obj.mbb.max.z};
             std::memcpy(&h->mbb[6 * o], m, sizeof(m));
             h->anchor[3 * o] = obj.anchor.x;
@@ -399,16 +432,12 @@ std::unique_ptr<PackedHeader> pack_header(const PreparedDataset& dsf, size_t fir
 // One level in the compact mesh form: per object a straight copy of its vertices, index
 // triples, hd / ph and voxel facet-id lists (object-local ids; the device rebases and
 // range-checks them, k_expand_level).
-std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& ds, const PackedHeader& h, size_t li, ThreadPool& pool) {
-    return pack_level(ds, 0, h, li, pool);
-}
-
-std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& dsf, size_t first, const PackedHeader& h, size_t li,
-                                        ThreadPool& pool, size_t pieces,
+std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& dsf, const PackedHeader& h, size_t li, ThreadPool& pool,
+                                        size_t pieces,
                                         const std::function<void(const PackedLevel&, const PieceRows&)>& on_piece) {
     auto p = std::make_unique<PackedLevel>();
-    const ObjRange ds{dsf.objects.data() + first, h.n_objects};
-    const size_t no = ds.objects.size();
+    const ObjSel ds = select(dsf, h);
+    const size_t no = ds.size();
     const uint64_t nvert = h.n_vertices[li], nfac = h.n_facets[li];
     const uint64_t entries = h.facet_offsets[li].back();
     p->verts.resize(std::max<uint64_t>(3 * nvert, 1));
@@ -428,7 +457,7 @@ std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& dsf, size_t first
     for_blocks(pool, no, [&](size_t b, size_t e) {
         bool w = false;
         for (size_t o = b; o < e; ++o) {
-            const LodMesh& lod = ds.objects[o].ladder.levels[li];
+            const LodMesh& lod = ds[o].ladder.levels[li];
             const size_t n_f = lod.mesh.facets.size();
             w = w || lod.mesh.vertices.size() >= 0xffff || n_f >= 0xffff;
             if (nonzero.load(std::memory_order_relaxed)) continue;
@@ -464,7 +493,7 @@ std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& dsf, size_t first
         const size_t lo = no * k / pieces, hi = no * (k + 1) / pieces;
         for_blocks(pool, hi - lo, [&](size_t b, size_t e) {
             for (size_t o = lo + b; o < lo + e; ++o) {
-                const PreparedObject& obj = ds.objects[o];
+                const PreparedObject& obj = ds[o];
                 const LodMesh& lod = obj.ladder.levels[li];
                 const uint64_t vb = h.vert_base[li][o], fb = h.facet_base[li][o];
                 const size_t n_v = lod.mesh.vertices.size(), n_f = lod.mesh.facets.size();
@@ -501,17 +530,6 @@ std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& dsf, size_t first
                                    fo[h.voxel_offsets[lo]], fo[h.voxel_offsets[hi]]});
     }
     return p;
-}
-
-std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& dsf, size_t first, const PackedHeader& h, size_t li,
-                                        ThreadPool& pool) {
-    return pack_level(dsf, first, h, li, pool, 1, {});
-}
-
-std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& ds, const PackedHeader& h, size_t li, ThreadPool& pool,
-                                        size_t pieces,
-                                        const std::function<void(const PackedLevel&, const PieceRows&)>& on_piece) {
-    return pack_level(ds, 0, h, li, pool, pieces, on_piece);
 }
 
 } // namespace detail
@@ -718,6 +736,107 @@ double tri_tri_distance(const Triangle& t1, const Triangle& t2) {
     return d;
 }
 
+namespace {
+double geom_one(int op, const double* a, const double* b) {
+    tj_ctx* ctx = detail::device_context(detail::join_devices()[0]);
+    double d = 0;
+    detail::check(tj_geom_batch(ctx, op, 1, a, b, &d), ctx);
+    return d;
+}
+} // namespace
+
+double point_segment_distance(const Point3& p, const Point3& a, const Point3& b) {
+    static_assert(sizeof(Point3) == 24);
+    const double seg[6] = {a.x, a.y, a.z, b.x, b.y, b.z};
+    return geom_one(TJ_GEOM_POINT_SEGMENT, &p.x, seg);
+}
+
+double point_triangle_distance(const Point3& p, const Triangle& t) {
+    return geom_one(TJ_GEOM_POINT_TRIANGLE, &p.x, &t.v0.x);
+}
+
+double segment_segment_distance(const Point3& a0, const Point3& a1, const Point3& b0, const Point3& b1) {
+    const double a[6] = {a0.x, a0.y, a0.z, a1.x, a1.y, a1.z};
+    const double b[6] = {b0.x, b0.y, b0.z, b1.x, b1.y, b1.z};
+    return geom_one(TJ_GEOM_SEGMENT_SEGMENT, a, b);
+}
+
+// ---------------------------------------------------------------- run_oracle (GPU exhaustive join)
+
+namespace {
+// Level-100 triangles of every object (the OracleTree input, reference src/oracle.cpp:29-33).
+struct MeshSetPack {
+    std::vector<uint64_t> off;
+    std::vector<double> tris;
+    tj_mesh_set_view view{};
+    explicit MeshSetPack(const PreparedDataset& ds) {
+        off.assign(ds.objects.size() + 1, 0);
+        for (size_t o = 0; o < ds.objects.size(); ++o) {
+            const auto& lv = ds.objects[o].ladder.levels;
+            off[o + 1] = off[o] + (lv.empty() ? 0 : lv.back().mesh.facets.size());
+        }
+        tris.resize(9 * off.back());
+        for (size_t o = 0; o < ds.objects.size(); ++o) {
+            const auto& lv = ds.objects[o].ladder.levels;
+            if (lv.empty()) continue;
+            const Mesh& m = lv.back().mesh;
+            double* w = tris.data() + 9 * off[o];
+            for (size_t f = 0; f < m.facets.size(); ++f) {
+                for (int c = 0; c < 3; ++c) {
+                    const uint32_t vi = m.facets[f][c];
+                    if (vi >= m.vertices.size()) throw std::invalid_argument("run_oracle: facet vertex out of range");
+                    const Point3& v = m.vertices[vi];
+                    w[9 * f + 3 * c] = v.x;
+                    w[9 * f + 3 * c + 1] = v.y;
+                    w[9 * f + 3 * c + 2] = v.z;
+                }
+            }
+        }
+        view.n_objects = static_cast<uint32_t>(ds.objects.size());
+        view.tri_offsets = off.data();
+        view.tris = tris.data();
+    }
+};
+} // namespace
+
+JoinOutput run_oracle(const PreparedDataset& R, const PreparedDataset& S, const JoinSpec& spec, ThreadPool& pool) {
+    (void)pool; // the work runs on the GPU
+    validate(spec);
+    const auto t0 = std::chrono::steady_clock::now();
+    const MeshSetPack r(R);
+    std::unique_ptr<MeshSetPack> s_store;
+    const tj_mesh_set_view* sv = nullptr; // self-join: the same dataset object
+    if (&S != &R) {
+        s_store = std::make_unique<MeshSetPack>(S);
+        sv = &s_store->view;
+    }
+    const int32_t type = spec.type == JoinType::Knn ? TJ_KNN : spec.type == JoinType::Intersect ? TJ_INTERSECT
+                                                                                                   : TJ_WITHIN;
+    tj_ctx* ctx = detail::device_context(detail::join_devices()[0]);
+    tj_exhaustive_result res{};
+    detail::check(tj_exhaustive_join(ctx, &r.view, sv, type, spec.type == JoinType::Within ? spec.tau : 0.0, spec.k,
+                                     &res),
+                  ctx);
+    JoinOutput out;
+    out.records.reserve(res.n_records);
+    for (uint64_t x = 0; x < res.n_records; ++x)
+        out.records.push_back({res.r[x], res.s[x], res.d[x], res.d[x], 100, res.rank[x]});
+    tj_exhaustive_result_free(&res);
+    const uint64_t all_pairs = static_cast<uint64_t>(R.objects.size()) * static_cast<uint64_t>(S.objects.size());
+    out.stats.query = join_type_name(spec.type);
+    out.stats.results = out.records.size();
+    out.stats.total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    StageCounters sc;
+    sc.name = "exhaustive";
+    sc.wall_ms = out.stats.total_ms;
+    sc.pairs_in = all_pairs;
+    sc.confirmed = out.records.size();
+    sc.removed = all_pairs - out.records.size();
+    sc.pairs_out = 0;
+    out.stats.stages.push_back(sc);
+    return out;
+}
+
 VoxelPairBatch gather_facet_data(std::span<const ActiveVp> slice, uint32_t level, const PreparedDataset& R,
                                  const PreparedDataset& S, const CandidateSet& cands) {
     auto slot = [&](const PreparedDataset& d) {
@@ -814,10 +933,13 @@ tj_join_spec to_c_spec(const JoinSpec& spec) {
     return c;
 }
 
-// One part of a join's device results: queries [r_base, r_base + n) (or a GPU shard).
+// One part of a join's device results: n queries whose global ids are ids[0, n) (or
+// r_base + [0, n) when ids is null): one R chunk of one GPU's query shard.
 struct Piece {
     const tj_join_result* res;
     uint32_t r_base;
+    const uint32_t* ids;
+    uint32_t n;
 };
 
 int slot_of(const PreparedDataset& d, uint32_t level) {
@@ -859,189 +981,174 @@ uint64_t device_budget(int device) {
     return cache[device] = free_b / 10 * 9;
 }
 
-// R split into consecutive object chunks so that S (resident for the whole join) and two R
-// chunks (one joining, the next uploading) fit the budget: $TRIJOIN_DEVICE_BUDGET_MB, else
-// 90 % of the device's free memory. $TRIJOIN_R_CHUNK_OBJECTS forces a chunk size. One
-// chunk = the whole of R (the resident path).
-std::vector<std::pair<size_t, size_t>> plan_r_chunks(const PreparedDataset& R, const PreparedDataset& S,
-                                                     const JoinSpec&, int device, bool self_join, ThreadPool& pool) {
-    const size_t nr = R.objects.size();
+// One GPU's share of a join: a query shard (ids ascending; empty = all of R) split into R
+// chunks (ranges into the shard) so that S and the chunk being joined fit the budget:
+// $TRIJOIN_DEVICE_BUDGET_MB, else 90 % of the device's free memory (shared by the contexts
+// of one device). $TRIJOIN_R_CHUNK_OBJECTS forces a chunk size.
+struct GpuShare {
+    int device = 0, slot = 0;
+    std::vector<uint32_t> ids;
+    bool all = true;
+    std::vector<std::pair<size_t, size_t>> chunks;
+    size_t size(size_t nr) const { return all ? nr : ids.size(); }
+};
+
+void plan_r_chunks(GpuShare& w, const PreparedDataset& R, uint64_t s_total, size_t contexts_on_device,
+                   ThreadPool& pool) {
+    const size_t n = w.size(R.objects.size());
+    w.chunks.clear();
     if (const char* e = std::getenv("TRIJOIN_R_CHUNK_OBJECTS"); e && *e) {
         const size_t step = std::max<size_t>(1, std::stoull(e));
-        std::vector<std::pair<size_t, size_t>> plan;
-        for (size_t a = 0; a < nr; a += step) plan.emplace_back(a, std::min(nr, a + step));
-        if (plan.empty()) plan.emplace_back(0, 0);
-        return plan;
+        for (size_t a = 0; a < n; a += step) w.chunks.emplace_back(a, std::min(n, a + step));
+        if (w.chunks.empty()) w.chunks.emplace_back(0, 0);
+        return;
     }
-    const uint64_t budget = device_budget(device);
-    if (budget == 0) return {{0, nr}};
-    std::vector<uint64_t> cost(nr);
-    std::atomic<uint64_t> r_sum{0}, s_sum{0};
-    detail::for_blocks(pool, nr, [&](size_t b, size_t e) {
+    uint64_t budget = device_budget(w.device);
+    if (budget == 0) {
+        w.chunks.emplace_back(0, n);
+        return;
+    }
+    budget /= std::max<size_t>(1, contexts_on_device);
+    std::vector<uint64_t> cost(n);
+    std::atomic<uint64_t> r_sum{0};
+    detail::for_blocks(pool, n, [&](size_t b, size_t e) {
         uint64_t acc = 0;
-        for (size_t o = b; o < e; ++o) acc += cost[o] = object_device_bytes(R.objects[o]);
+        for (size_t i = b; i < e; ++i) acc += cost[i] = object_device_bytes(R.objects[w.all ? i : w.ids[i]]);
         r_sum += acc;
     });
-    if (!self_join)
-        detail::for_blocks(pool, S.objects.size(), [&](size_t b, size_t e) {
-            uint64_t acc = 0;
-            for (size_t o = b; o < e; ++o) acc += object_device_bytes(S.objects[o]);
-            s_sum += acc;
-        });
-    const uint64_t r_total = r_sum.load(), s_total = s_sum.load();
-    const uint64_t fixed = (64ull << 20) + 256 * uint64_t{nr};
-    if (r_total + s_total + fixed <= budget) return {{0, nr}};
-    // chunked: S in full (for a self-join a second, complete copy) + two R chunks
-    const uint64_t s_res = self_join ? r_total : s_total;
-    if (s_res + fixed >= budget) throw std::runtime_error("trijoin: S does not fit the device-memory budget");
-    const uint64_t per_chunk = (budget - s_res - fixed) / 2;
-    std::vector<std::pair<size_t, size_t>> plan;
+    const uint64_t fixed = (64ull << 20) + 256 * uint64_t{n};
+    if (r_sum.load() + s_total + fixed <= budget) {
+        w.chunks.emplace_back(0, n);
+        return;
+    }
+    // chunked: S in full + one R chunk joining (the next one is packed on the host meanwhile)
+    if (s_total + fixed >= budget) throw std::runtime_error("trijoin: S does not fit the device-memory budget");
+    const uint64_t per_chunk = budget - s_total - fixed;
     size_t a = 0;
     uint64_t acc = 0;
-    for (size_t o = 0; o < nr; ++o) {
-        if (cost[o] > per_chunk) throw std::runtime_error("trijoin: one R object exceeds the device-memory budget");
-        if (acc + cost[o] > per_chunk) {
-            plan.emplace_back(a, o);
-            a = o;
+    for (size_t i = 0; i < n; ++i) {
+        if (cost[i] > per_chunk) throw std::runtime_error("trijoin: one R object exceeds the device-memory budget");
+        if (acc + cost[i] > per_chunk) {
+            w.chunks.emplace_back(a, i);
+            a = i;
             acc = 0;
         }
-        acc += cost[o];
+        acc += cost[i];
     }
-    plan.emplace_back(a, nr);
-    return plan;
+    w.chunks.emplace_back(a, n);
 }
 
-// Out-of-core device phase: S resident on every GPU (streamed once), R chunks dealt to the
-// GPUs round-robin; on each GPU the next chunk is packed and uploaded (its own copy stream)
-// while the current chunk joins. results[k] holds chunk k (queries local to the chunk).
-void run_chunked(const PreparedDataset& R, const PreparedDataset& S, const JoinSpec& spec, ThreadPool& pool,
-                 const std::vector<int>& devices, const std::vector<std::pair<size_t, size_t>>& plan,
-                 std::vector<detail::ResultHandle>& results, JoinOutput& out,
-                 const std::function<void(const std::string&)>& mark) {
+uint64_t dataset_device_bytes(const PreparedDataset& D, ThreadPool& pool) {
+    std::atomic<uint64_t> sum{0};
+    detail::for_blocks(pool, D.objects.size(), [&](size_t b, size_t e) {
+        uint64_t acc = 0;
+        for (size_t o = b; o < e; ++o) acc += object_device_bytes(D.objects[o]);
+        sum += acc;
+    });
+    return sum.load();
+}
+
+// A packed set for one object selection of a dataset: from the caller's cache (kept for later
+// joins of the same immutable dataset) or fresh (freed after the join).
+struct SetLease {
+    std::shared_ptr<detail::PackedSet> set;
+    detail::JoinCache* cache = nullptr;
+    std::string key;
+    SetLease() = default;
+    SetLease(const SetLease&) = delete;
+    SetLease& operator=(const SetLease&) = delete;
+    ~SetLease() {
+        if (cache && set) cache->give_back(key, std::move(set));
+    }
+};
+
+void lease(SetLease& l, detail::JoinCache* cache, const std::string& key) {
+    if (cache) {
+        l.set = cache->take(key);
+        if (l.set) {
+            l.cache = cache;
+            l.key = key;
+            return;
+        }
+    }
+    l.set = std::make_shared<detail::PackedSet>();
+}
+
+// Ships level slot `slot` of set (packing it first, in pieces that are shipped while the next
+// is packed, unless the set already holds it) to every dataset handle in dst.
+void feed_level(const PreparedDataset& D, detail::PackedSet& set, size_t slot, const std::vector<tj_dataset*>& dst,
+                const std::vector<tj_ctx*>& ctxs, ThreadPool& pool, JoinOutput& out, double& pack_ms,
+                std::mutex* stat_mu) {
     using Clock = std::chrono::steady_clock;
-    const size_t G = devices.size();
-    out.stats.devices = static_cast<uint32_t>(G);
-    results = std::vector<detail::ResultHandle>(plan.size());
-    // S: header + every level the join uses, streamed to each GPU once
-    auto hs = detail::pack_header(S, pool);
-    std::vector<detail::DatasetHandle> dsh(G);
-    std::vector<std::unique_ptr<detail::PackedLevel>> s_levels;
-    for (size_t g = 0; g < G; ++g) {
-        tj_ctx* ctx = detail::device_context(devices[g]);
-        detail::check(tj_dataset_begin(ctx, &hs->view, hs->vb_ptrs.data(), hs->fb_ptrs.data(), &dsh[g].p), ctx);
-        out.stats.h2d_bytes += hs->bytes();
+    if (set.levels.size() < D.lod_schedule.size()) set.levels.resize(D.lod_schedule.size());
+    auto& lv = set.levels[slot];
+    if (!lv) {
+        const auto t0 = Clock::now();
+        auto ship = [&](const detail::PackedLevel& l, const detail::PieceRows& rows) {
+            for (size_t g = 0; g < dst.size(); ++g)
+                detail::check(tj_dataset_put_level_part(dst[g], static_cast<uint32_t>(slot), &l.view, rows.vert_begin,
+                                                        rows.vert_end, rows.facet_begin, rows.facet_end,
+                                                        rows.entry_begin, rows.entry_end),
+                              ctxs[g]);
+        };
+        lv = detail::pack_level(D, *set.h, slot, pool, kPackPieces, ship);
+        const double ms = std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+        std::unique_lock<std::mutex> lk;
+        if (stat_mu) lk = std::unique_lock<std::mutex>(*stat_mu);
+        pack_ms += ms;
+    } else {
+        const uint64_t nv = set.h->n_vertices[slot], nf = set.h->n_facets[slot];
+        const uint64_t ne = set.h->facet_offsets[slot].back();
+        for (size_t g = 0; g < dst.size(); ++g)
+            detail::check(tj_dataset_put_level_part(dst[g], static_cast<uint32_t>(slot), &lv->view, 0, nv, 0, nf, 0, ne),
+                          ctxs[g]);
     }
-    for (uint32_t level : spec.lods) {
-        const int slot = slot_of(S, level);
-        if (slot < 0) continue;
-        s_levels.push_back(detail::pack_level(S, *hs, static_cast<size_t>(slot), pool));
-        out.stats.h2d_bytes += G * s_levels.back()->bytes;
-        for (size_t g = 0; g < G; ++g)
-            detail::check(tj_dataset_put_level(dsh[g].p, static_cast<uint32_t>(slot), &s_levels.back()->view),
-                          detail::device_context(devices[g]));
-    }
-    mark("S_streamed");
-    struct Prepared {
-        std::unique_ptr<detail::PackedHeader> h;
-        std::vector<std::unique_ptr<detail::PackedLevel>> lv; // outlive the dataset below
-        detail::DatasetHandle d;
-        ~Prepared() {
-            if (d.p) tj_dataset_sync(d.p);
-        }
-    };
-    std::mutex stat_mu;
-    auto prepare = [&](tj_ctx* ctx, size_t k) {
-        auto p = std::make_unique<Prepared>();
-        const auto [a, b] = plan[k];
-        p->h = detail::pack_header(R, a, b, pool);
-        detail::check(tj_dataset_begin(ctx, &p->h->view, p->h->vb_ptrs.data(), p->h->fb_ptrs.data(), &p->d.p), ctx);
-        uint64_t bytes = p->h->bytes();
-        for (uint32_t level : spec.lods) {
-            const int slot = slot_of(R, level);
-            if (slot < 0) continue; // the join reports the missing level
-            p->lv.push_back(detail::pack_level(R, a, *p->h, static_cast<size_t>(slot), pool));
-            bytes += p->lv.back()->bytes;
-            detail::check(tj_dataset_put_level(p->d.p, static_cast<uint32_t>(slot), &p->lv.back()->view), ctx);
-        }
-        std::lock_guard<std::mutex> lk(stat_mu);
-        out.stats.h2d_bytes += bytes;
-        return p;
-    };
-    std::vector<std::exception_ptr> errors(G);
-    std::vector<double> dev_ms(G, 0.0);
-    auto worker = [&](size_t g) {
-        try {
-            tj_ctx* ctx = detail::device_context(devices[g]);
-            tj_join_spec cs = to_c_spec(spec);
-            std::vector<size_t> mine;
-            for (size_t k = g; k < plan.size(); k += G) mine.push_back(k);
-            if (mine.empty()) return;
-            std::unique_ptr<Prepared> next = prepare(ctx, mine[0]);
-            for (size_t i = 0; i < mine.size(); ++i) {
-                std::unique_ptr<Prepared> cur = std::move(next);
-                std::exception_ptr je;
-                const auto td = Clock::now();
-                std::thread jt([&] {
-                    try {
-                        detail::check(tj_join(ctx, cur->d.p, dsh[g].p, &cs, nullptr, &results[mine[i]].r), ctx);
-                    } catch (...) {
-                        je = std::current_exception();
-                    }
-                });
-                std::exception_ptr pe;
-                try {
-                    if (i + 1 < mine.size()) next = prepare(ctx, mine[i + 1]); // overlaps the join
-                } catch (...) {
-                    pe = std::current_exception();
-                }
-                jt.join();
-                dev_ms[g] += std::chrono::duration<double, std::milli>(Clock::now() - td).count();
-                if (je) std::rethrow_exception(je);
-                if (pe) std::rethrow_exception(pe);
-            }
-        } catch (...) {
-            errors[g] = std::current_exception();
-        }
-    };
-    std::vector<std::thread> ts;
-    for (size_t g = 0; g < G; ++g) ts.emplace_back(worker, g);
-    for (auto& t : ts) t.join();
-    for (size_t g = 0; g < G; ++g) tj_dataset_sync(dsh[g].p);
-    for (auto& e : errors)
-        if (e) std::rethrow_exception(e);
-    out.stats.device_ms = *std::max_element(dev_ms.begin(), dev_ms.end());
-    out.stats.r_chunks = static_cast<uint32_t>(plan.size());
-    mark("joins_done");
+    const uint32_t flags = (lv->zero_pads ? 0u : TJ_LEVEL_PADS) | (lv->narrow ? TJ_LEVEL_NARROW : 0u);
+    for (size_t g = 0; g < dst.size(); ++g)
+        detail::check(tj_dataset_finish_level(dst[g], static_cast<uint32_t>(slot), flags), ctxs[g]);
+    std::unique_lock<std::mutex> lk;
+    if (stat_mu) lk = std::unique_lock<std::mutex>(*stat_mu);
+    out.stats.h2d_bytes += dst.size() * lv->bytes;
+}
+
+// Marks every level slot of ds not yet shipped as failed (a join waiting for it returns).
+void release_levels(tj_dataset* ds, const std::vector<char>& put) {
+    for (size_t i = 0; i < put.size(); ++i)
+        if (!put[i]) tj_dataset_put_level(ds, static_cast<uint32_t>(i), nullptr);
 }
 
 } // namespace
 
 JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const JoinSpec& spec, ThreadPool& pool,
                     const JoinTrace* trace) {
+    return detail::run_join_cached(R, S, spec, pool, trace, nullptr, nullptr);
+}
+
+JoinOutput detail::run_join_cached(const PreparedDataset& R, const PreparedDataset& S, const JoinSpec& spec,
+                                   ThreadPool& pool, const JoinTrace* trace, JoinCache* r_cache, JoinCache* s_cache) {
     using Clock = std::chrono::steady_clock;
     validate(spec);
     const bool knn = spec.type == JoinType::Knn;
     const auto t_total = Clock::now();
     JoinOutput out;
     out.stats.query = join_type_name(spec.type);
+    std::mutex stat_mu;
     auto mark = [&](const std::string& what) {
+        std::lock_guard<std::mutex> lk(stat_mu);
         out.stats.timeline.emplace_back(what, std::chrono::duration<double, std::milli>(Clock::now() - t_total).count());
     };
 
     mark("entered");
     const std::vector<int> devices = detail::join_devices();
     const bool self_join = &R == &S;
-    const size_t G = (trace && (trace->on_interval || trace->on_vp_pruned)) ? 1 : devices.size();
-    out.stats.devices = static_cast<uint32_t>(G);
-
-    // Device phase -> result pieces + the owner of every query.
-    std::vector<detail::ResultHandle> results;
-    std::vector<Piece> pieces;
-    std::function<size_t(uint32_t)> owner;
     const bool tracing = trace && (trace->on_interval || trace->on_vp_pruned);
-    // Process-level sharding for one-process-per-GPU launches ($TRIJOIN_PROCESS_SHARD = "i/n"):
-    // this process joins only the query blocks of shard i of n (records and counters then
-    // cover those queries only); resident path only.
+    const size_t G = tracing ? 1 : devices.size();
+    out.stats.devices = static_cast<uint32_t>(G);
+    const size_t nr = R.objects.size();
+
+    // Query shards: query r belongs to shard (r / block) % Q, Q = processes x GPUs.
+    // $TRIJOIN_PROCESS_SHARD = "i/n" (one process per GPU, e.g. torchrun): this process joins
+    // shards i*G .. i*G+G-1 only, and its records and counters cover those queries only.
     size_t proc_i = 0, proc_n = 1;
     if (const char* e = std::getenv("TRIJOIN_PROCESS_SHARD"); e && *e && !tracing) {
         const std::string v(e);
@@ -1051,166 +1158,203 @@ JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const Jo
         proc_n = std::max<size_t>(1, std::stoull(v.substr(slash + 1)));
         if (proc_i >= proc_n) throw std::invalid_argument("TRIJOIN_PROCESS_SHARD: i must be < n");
     }
-    // queries per shard block ($TRIJOIN_SHARD_BLOCK for tests)
-    uint32_t block = 1024;
+    uint32_t block = 1024; // queries per shard block ($TRIJOIN_SHARD_BLOCK for tests)
     if (const char* e = std::getenv("TRIJOIN_SHARD_BLOCK"); e && *e) block = std::max<uint32_t>(1, std::stoul(e));
-    const std::vector<std::pair<size_t, size_t>> chunks =
-        tracing || proc_n > 1 ? std::vector<std::pair<size_t, size_t>>{}
-                              : plan_r_chunks(R, S, spec, devices[0], self_join, pool);
+    const size_t Q = proc_n * G;
+    std::vector<GpuShare> share(G);
+    std::map<int, size_t> per_device;
+    for (size_t g = 0; g < G; ++g) {
+        share[g].device = devices[g];
+        share[g].slot = static_cast<int>(per_device[devices[g]]++); // own context per listed slot
+        if (Q > 1) {
+            share[g].all = false;
+            const size_t q = proc_i * G + g;
+            for (size_t b0 = q * size_t{block}; b0 < nr; b0 += Q * size_t{block})
+                for (size_t r = b0; r < std::min(nr, b0 + block); ++r) share[g].ids.push_back(static_cast<uint32_t>(r));
+        }
+    }
+    // S stays resident on every GPU for the whole join; R goes in chunks if it does not fit
+    const uint64_t s_total = tracing ? 0 : dataset_device_bytes(S, pool);
+    for (size_t g = 0; g < G; ++g) {
+        if (tracing) share[g].chunks = {{0, share[g].size(nr)}};
+        else plan_r_chunks(share[g], R, s_total, per_device[share[g].device], pool);
+    }
+    // one GPU, all of R in one chunk, self-join: R and S are one device dataset
+    const bool one_dataset = self_join && G == 1 && Q == 1 && share[0].chunks.size() == 1;
+    uint32_t n_chunks = 0;
+    for (const auto& w : share) n_chunks += static_cast<uint32_t>(w.chunks.size());
+    out.stats.r_chunks = n_chunks;
     mark("planned");
-    if (chunks.size() > 1) {
-        run_chunked(R, S, spec, pool, devices, chunks, results, out, mark);
-        for (size_t k = 0; k < chunks.size(); ++k)
-            pieces.push_back({&results[k].r, static_cast<uint32_t>(chunks[k].first)});
-        owner = [&chunks](uint32_t r) {
-            size_t lo = 0, hi = chunks.size();
-            while (hi - lo > 1) {
-                const size_t mid = (lo + hi) / 2;
-                if (chunks[mid].first <= r) lo = mid; else hi = mid;
-            }
-            return lo;
-        };
-    } else {
 
-        // Streamed upload (tj_dataset_begin / _put_level): object + voxel arrays first, then
-        // each LOD level the join uses, coarsest first, packed on the host in the compact mesh
-        // form while the devices already run the filters and the coarser levels.
-        const detail::ArenaStats arena0 = detail::arena_stats();
-        auto tp = Clock::now();
-        auto hr = detail::pack_header(R, pool);
-        std::unique_ptr<detail::PackedHeader> hs_own;
-        const detail::PackedHeader* hs = hr.get();
-        if (!self_join) {
-            hs_own = detail::pack_header(S, pool);
-            hs = hs_own.get();
+    const detail::ArenaStats arena0 = detail::arena_stats();
+    std::vector<tj_ctx*> ctxs(G);
+    for (size_t g = 0; g < G; ++g) ctxs[g] = detail::device_context(share[g].device, share[g].slot);
+
+    // ---- S: header + levels packed once (or taken from the cache), streamed to every GPU
+    double pack_ms = 0.0;
+    SetLease s_lease;
+    std::vector<detail::DatasetHandle> dsh(G);
+    std::vector<std::vector<char>> put_s(G, std::vector<char>(S.lod_schedule.size(), 0));
+    const auto tu = Clock::now();
+    if (!one_dataset) {
+        lease(s_lease, s_cache, "all");
+        if (!s_lease.set->h) {
+            const auto tp = Clock::now();
+            s_lease.set->h = detail::pack_header(S, pool);
+            pack_ms += std::chrono::duration<double, std::milli>(Clock::now() - tp).count();
         }
-        double pack_ms = std::chrono::duration<double, std::milli>(Clock::now() - tp).count();
-        mark("header_packed");
-        std::vector<std::unique_ptr<detail::PackedLevel>> staged; // outlives the dataset handles below
-        std::vector<detail::DatasetHandle> dr(G), dsh(G);
-        const auto tu = Clock::now();
+        const detail::PackedHeader& hs = *s_lease.set->h;
         for (size_t g = 0; g < G; ++g) {
-            tj_ctx* ctx = detail::device_context(devices[g]);
-            detail::check(tj_dataset_begin(ctx, &hr->view, hr->vb_ptrs.data(), hr->fb_ptrs.data(), &dr[g].p), ctx);
-            out.stats.h2d_bytes += hr->bytes() + (self_join ? 0 : hs->bytes());
-            if (!self_join)
-                detail::check(tj_dataset_begin(ctx, &hs->view, hs->vb_ptrs.data(), hs->fb_ptrs.data(), &dsh[g].p), ctx);
+            detail::check(tj_dataset_begin(ctxs[g], &hs.view, hs.vb_ptrs.data(), hs.fb_ptrs.data(), &dsh[g].p), ctxs[g]);
+            out.stats.h2d_bytes += hs.bytes();
         }
-        out.stats.upload_ms = std::chrono::duration<double, std::milli>(Clock::now() - tu).count();
-        mark("datasets_begun");
+    }
+    out.stats.upload_ms = std::chrono::duration<double, std::milli>(Clock::now() - tu).count();
+    mark("S_begun");
 
-        results = std::vector<detail::ResultHandle>(G);
-        std::vector<std::exception_ptr> errors(G);
-        std::vector<double> dev_ms(G, 0.0);
-        auto run_shard = [&](size_t g) {
-            try {
-                tj_ctx* ctx = detail::device_context(devices[g]);
-                const auto td = Clock::now();
-                tj_join_spec cs = to_c_spec(spec);
-                cs.shard_index = static_cast<uint32_t>(proc_i * G + g);
-                cs.shard_count = static_cast<uint32_t>(proc_n * G);
-                cs.shard_block = block;
-                TraceBridge bridge{trace};
-                tj_trace tt{&bridge, &TraceBridge::interval, &TraceBridge::pruned};
-                detail::check(tj_join(ctx, dr[g].p, self_join ? dr[g].p : dsh[g].p, &cs, trace ? &tt : nullptr,
-                                      &results[g].r),
-                              ctx);
-                dev_ms[g] = std::chrono::duration<double, std::milli>(Clock::now() - td).count();
-            } catch (...) {
-                errors[g] = std::current_exception();
-            }
-        };
-        std::vector<std::thread> joins;
-        for (size_t g = 0; g < G; ++g) joins.emplace_back(run_shard, g);
-
-        // Producer: levels in join order; a level missing from a schedule is left to the join
-        // (EngineError from its level check). On failure every undelivered slot is released.
-        std::exception_ptr pack_error;
-        std::vector<std::vector<char>> put_r(G, std::vector<char>(R.lod_schedule.size(), 0));
-        std::vector<std::vector<char>> put_s(G, std::vector<char>(S.lod_schedule.size(), 0));
-        auto slot_of = [](const PreparedDataset& d, uint32_t level) -> int {
-            for (size_t i = 0; i < d.lod_schedule.size(); ++i)
-                if (d.lod_schedule[i] == static_cast<int>(level)) return static_cast<int>(i);
-            return -1;
-        };
+    // ---- per GPU: its R chunks in order; each chunk's levels are packed (or taken from the
+    // cache) and streamed while its join runs, coarsest level first
+    std::vector<std::vector<std::unique_ptr<detail::ResultHandle>>> results(G);
+    std::vector<std::vector<std::unique_ptr<SetLease>>> r_sets(G); // chunk id lists live until the merge
+    std::vector<std::exception_ptr> errors(G);
+    std::vector<double> dev_ms(G, 0.0);
+    auto worker = [&](size_t g) {
+        GpuShare& w = share[g];
+        tj_ctx* ctx = ctxs[g];
         try {
-            for (uint32_t level : spec.lods) {
-                for (int side = 0; side < (self_join ? 1 : 2); ++side) {
-                    const PreparedDataset& D = side == 0 ? R : S;
-                    const detail::PackedHeader& H = side == 0 ? *hr : *hs;
-                    const int slot = slot_of(D, level);
-                    if (slot < 0) continue;
-                    const auto tl = Clock::now();
-                    // packed in pieces, each shipped while the next is packed (the copy engine
-                    // then trails the packing by one piece instead of one level)
-                    auto ship = [&](const detail::PackedLevel& lv, const detail::PieceRows& rows) {
-                        for (size_t g = 0; g < G; ++g) {
-                            tj_dataset* ds = side == 0 ? dr[g].p : dsh[g].p;
-                            detail::check(tj_dataset_put_level_part(ds, static_cast<uint32_t>(slot), &lv.view,
-                                                                    rows.vert_begin, rows.vert_end, rows.facet_begin,
-                                                                    rows.facet_end, rows.entry_begin, rows.entry_end),
-                                          detail::device_context(devices[g]));
-                        }
-                    };
-                    staged.push_back(detail::pack_level(D, H, static_cast<size_t>(slot), pool, kPackPieces, ship));
-                    pack_ms += std::chrono::duration<double, std::milli>(Clock::now() - tl).count();
-                    mark(std::string(side == 0 ? "R" : "S") + "_lod" + std::to_string(level) + "_packed");
-                    out.stats.h2d_bytes += G * staged.back()->bytes;
-                    for (size_t g = 0; g < G; ++g) {
-                        tj_dataset* ds = side == 0 ? dr[g].p : dsh[g].p;
-                        auto& put = side == 0 ? put_r[g] : put_s[g];
-                        put[slot] = 1;
-                        const uint32_t flags = (staged.back()->zero_pads ? 0u : TJ_LEVEL_PADS) |
-                                               (staged.back()->narrow ? TJ_LEVEL_NARROW : 0u);
-                        detail::check(tj_dataset_finish_level(ds, static_cast<uint32_t>(slot), flags),
-                                      detail::device_context(devices[g]));
-                    }
-                    mark(std::string(side == 0 ? "R" : "S") + "_lod" + std::to_string(level) + "_put");
+            for (size_t k = 0; k < w.chunks.size(); ++k) {
+                const auto [a, b] = w.chunks[k];
+                auto lz = std::make_unique<SetLease>();
+                const std::string key = (w.all ? std::string("all") : std::to_string(proc_i * G + g) + "/" +
+                                                                          std::to_string(Q) + "/" + std::to_string(block)) +
+                                        ":" + std::to_string(a) + "-" + std::to_string(b);
+                lease(*lz, r_cache, key);
+                if (!lz->set->h) {
+                    const auto tp = Clock::now();
+                    if (w.all)
+                        lz->set->h = detail::pack_header(R, a, b, pool);
+                    else
+                        lz->set->h = detail::pack_header(
+                            R, std::vector<uint32_t>(w.ids.begin() + a, w.ids.begin() + b), pool);
+                    std::lock_guard<std::mutex> lk(stat_mu);
+                    pack_ms += std::chrono::duration<double, std::milli>(Clock::now() - tp).count();
                 }
+                const detail::PackedHeader& hr = *lz->set->h;
+                detail::DatasetHandle dr;
+                detail::check(tj_dataset_begin(ctx, &hr.view, hr.vb_ptrs.data(), hr.fb_ptrs.data(), &dr.p), ctx);
+                {
+                    std::lock_guard<std::mutex> lk(stat_mu);
+                    out.stats.h2d_bytes += hr.bytes();
+                }
+                results[g].push_back(std::make_unique<detail::ResultHandle>());
+                detail::ResultHandle* res = results[g].back().get();
+                std::exception_ptr je;
+                const auto td = Clock::now();
+                std::thread jt([&] {
+                    try {
+                        tj_join_spec cs = to_c_spec(spec);
+                        TraceBridge bridge{trace};
+                        tj_trace tt{&bridge, &TraceBridge::interval, &TraceBridge::pruned};
+                        detail::check(tj_join(ctx, dr.p, one_dataset ? dr.p : dsh[g].p, &cs, trace ? &tt : nullptr,
+                                              &res->r),
+                                      ctx);
+                    } catch (...) {
+                        je = std::current_exception();
+                    }
+                });
+                std::vector<char> put(R.lod_schedule.size(), 0);
+                std::exception_ptr pe;
+                try {
+                    for (uint32_t level : spec.lods) {
+                        const int slot = slot_of(R, level);
+                        if (slot < 0) continue; // the join reports the missing level
+                        feed_level(R, *lz->set, static_cast<size_t>(slot), {dr.p}, {ctx}, pool, out, pack_ms,
+                                   &stat_mu);
+                        put[slot] = 1;
+                        if (G == 1 && w.chunks.size() == 1)
+                            mark(std::string("R_lod") + std::to_string(level) + "_put");
+                    }
+                } catch (...) {
+                    pe = std::current_exception();
+                    release_levels(dr.p, put);
+                }
+                jt.join();
+                tj_dataset_sync(dr.p);
+                dev_ms[g] += std::chrono::duration<double, std::milli>(Clock::now() - td).count();
+                r_sets[g].push_back(std::move(lz));
+                if (pe) std::rethrow_exception(pe);
+                if (je) std::rethrow_exception(je);
             }
         } catch (...) {
-            pack_error = std::current_exception();
-            for (size_t g = 0; g < G; ++g) {
-                for (size_t i = 0; i < put_r[g].size(); ++i)
-                    if (!put_r[g][i]) tj_dataset_put_level(dr[g].p, static_cast<uint32_t>(i), nullptr);
-                if (!self_join)
-                    for (size_t i = 0; i < put_s[g].size(); ++i)
-                        if (!put_s[g][i]) tj_dataset_put_level(dsh[g].p, static_cast<uint32_t>(i), nullptr);
+            errors[g] = std::current_exception();
+        }
+    };
+    std::vector<std::thread> workers;
+    for (size_t g = 0; g < G; ++g) workers.emplace_back(worker, g);
+
+    // ---- main thread: S levels in join order, shipped to every GPU
+    std::exception_ptr s_error;
+    if (!one_dataset) {
+        std::vector<tj_dataset*> dst(G);
+        for (size_t g = 0; g < G; ++g) dst[g] = dsh[g].p;
+        try {
+            for (uint32_t level : spec.lods) {
+                const int slot = slot_of(S, level);
+                if (slot < 0) continue;
+                feed_level(S, *s_lease.set, static_cast<size_t>(slot), dst, ctxs, pool, out, pack_ms, &stat_mu);
+                for (size_t g = 0; g < G; ++g) put_s[g][slot] = 1;
+                mark(std::string("S_lod") + std::to_string(level) + "_put");
             }
+        } catch (...) {
+            s_error = std::current_exception();
+            for (size_t g = 0; g < G; ++g) release_levels(dsh[g].p, put_s[g]);
         }
-        for (auto& t : joins) t.join();
-        mark("joins_done");
-        {
-            const detail::ArenaStats a1 = detail::arena_stats();
-            out.stats.timeline.emplace_back("arena_fresh_blocks", double(a1.fresh - arena0.fresh));
-            out.stats.timeline.emplace_back("arena_pageable_blocks", double(a1.pageable - arena0.pageable));
-            out.stats.timeline.emplace_back("arena_fresh_ms", a1.fresh_ms - arena0.fresh_ms);
-        }
-        for (size_t g = 0; g < G; ++g) {
-            tj_dataset_sync(dr[g].p);
-            if (!self_join) tj_dataset_sync(dsh[g].p);
-        }
-        if (pack_error) std::rethrow_exception(pack_error);
-        for (auto& e : errors)
-            if (e) std::rethrow_exception(e);
-        out.stats.pack_ms = pack_ms;
-        out.stats.device_ms = *std::max_element(dev_ms.begin(), dev_ms.end());
-        for (const auto& h : results) {
-            for (uint32_t i = 0; i < h.r.n_levels_run; ++i) out.stats.stream_wait_ms += h.r.level_wait_ms[i];
-            out.stats.decision_mode = h.r.decision_mode != 0;
-        }
-
-        for (size_t g = 0; g < G; ++g) pieces.push_back({&results[g].r, 0u});
-        // (a query of another process's shard has empty ranges in every piece of this one)
-        owner = [G, proc_n, block](uint32_t r) { return size_t{(r / block) % (proc_n * G) % G}; };
     }
+    for (auto& t : workers) t.join();
+    mark("joins_done");
+    {
+        const detail::ArenaStats a1 = detail::arena_stats();
+        out.stats.timeline.emplace_back("arena_fresh_blocks", double(a1.fresh - arena0.fresh));
+        out.stats.timeline.emplace_back("arena_pageable_blocks", double(a1.pageable - arena0.pageable));
+        out.stats.timeline.emplace_back("arena_fresh_ms", a1.fresh_ms - arena0.fresh_ms);
+    }
+    for (size_t g = 0; g < G; ++g)
+        if (dsh[g].p) tj_dataset_sync(dsh[g].p);
+    if (s_error) std::rethrow_exception(s_error);
+    for (auto& e : errors)
+        if (e) std::rethrow_exception(e);
+    out.stats.pack_ms = pack_ms;
+    out.stats.device_ms = *std::max_element(dev_ms.begin(), dev_ms.end());
 
-    // Merge: every query r is owned by one piece (a GPU shard, or an R chunk whose query ids
-    // start at r_base); a piece's arrays cover its own query range.
+    std::vector<Piece> pieces;
+    for (size_t g = 0; g < G; ++g)
+        for (size_t k = 0; k < share[g].chunks.size(); ++k) {
+            const tj_join_result& res = results[g][k]->r;
+            for (uint32_t i = 0; i < res.n_levels_run; ++i) out.stats.stream_wait_ms += res.level_wait_ms[i];
+            out.stats.decision_mode = out.stats.decision_mode || res.decision_mode != 0;
+            const auto [a, b] = share[g].chunks[k];
+            const detail::PackedHeader& h = *r_sets[g][k]->set->h;
+            pieces.push_back({&res, static_cast<uint32_t>(a), h.ids.empty() ? nullptr : h.ids.data(),
+                              static_cast<uint32_t>(b - a)});
+        }
+
+    // Merge: every query r this process joins is owned by one piece (a chunk of a GPU's
+    // shard, queries ids[0, n) or r_base + [0, n)); the others have empty ranges.
     Merged m;
-    const uint32_t nq = static_cast<uint32_t>(R.objects.size());
-    uint64_t total = 0;
-    for (const Piece& pc : pieces) total += pc.res->n_cands;
+    const uint32_t nq = static_cast<uint32_t>(nr);
+    constexpr uint32_t kNone = 0xffffffffu;
+    std::vector<uint32_t> own_piece(nq, kNone), own_local(nq, 0);
+    uint64_t total = 0, owned = 0;
+    for (uint32_t p = 0; p < pieces.size(); ++p) {
+        const Piece& pc = pieces[p];
+        total += pc.res->n_cands;
+        owned += pc.n;
+        for (uint32_t lr = 0; lr < pc.n; ++lr) {
+            const uint32_t r = pc.ids ? pc.ids[lr] : pc.r_base + lr;
+            own_piece[r] = p;
+            own_local[r] = lr;
+        }
+    }
     CandidateSet& c = m.cands;
     c.pairs.reserve(total);
     c.intervals.reserve(total);
@@ -1219,12 +1363,12 @@ JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const Jo
     c.r2op_offsets.assign(nq + 1, 0);
     c.num_confirmed.assign(nq, 0);
     for (uint32_t r = 0; r < nq; ++r) {
-        const Piece& pc = pieces[owner(r)];
-        const tj_join_result& res = *pc.res;
-        const uint32_t lr = r - pc.r_base;
         c.r2op_offsets[r] = c.pairs.size();
+        if (own_piece[r] == kNone) continue;
+        const tj_join_result& res = *pieces[own_piece[r]].res;
+        const uint32_t lr = own_local[r];
         for (uint64_t op = res.r2op_offsets[lr]; op < res.r2op_offsets[lr + 1]; ++op) {
-            c.pairs.emplace_back(res.pair_r[op] + pc.r_base, res.pair_s[op]);
+            c.pairs.emplace_back(r, res.pair_s[op]);
             c.intervals.push_back({res.lb[op], res.ub[op]});
             c.status.push_back(static_cast<PairStatus>(res.status[op]));
             c.decided_at.push_back(res.decided_at[op]);
@@ -1291,7 +1435,9 @@ JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const Jo
         }
         plan.push_back(p);
     }
-    const uint64_t all_pairs = uint64_t{R.objects.size()} * uint64_t{S.objects.size()};
+    // the (r, s) pairs of the queries this process joined (all of R unless process-sharded, so
+    // that the counters of the ranks of a torchrun launch sum to the whole join's)
+    const uint64_t all_pairs = owned * uint64_t{S.objects.size()};
     uint64_t flowing = all_pairs;
     for (const Plan& p : plan) {
         auto [conf, rem] = tally.count(p.code) ? tally[p.code] : std::pair<uint64_t, uint64_t>{0, 0};

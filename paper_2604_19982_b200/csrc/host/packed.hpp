@@ -3,10 +3,14 @@
 #pragma once
 
 #include <functional>
+#include <map>
 #include <memory>
+#include <mutex>
+#include <string>
 #include <vector>
 
 #include "../../../include/tj_capi.h"
+#include "trijoin/engine.hpp"
 #include "trijoin/index.hpp"
 
 namespace trijoin::detail {
@@ -63,7 +67,9 @@ struct PackedDataset {
     uint64_t bytes() const;
 };
 
-std::unique_ptr<PackedDataset> pack_dataset(const PreparedDataset& ds, ThreadPool& pool);
+// ids (optional): only the listed objects, in that order (one query shard of R).
+std::unique_ptr<PackedDataset> pack_dataset(const PreparedDataset& ds, ThreadPool& pool,
+                                            const std::vector<uint32_t>* ids = nullptr);
 
 // Host staging arena counters (process lifetime): fresh blocks, blocks that could not be
 // page-locked, bytes and milliseconds spent allocating fresh blocks.
@@ -77,6 +83,10 @@ ArenaStats arena_stats();
 // voxel arrays, the per-level voxel CSR and the per-object vertex / facet bases; each level
 // is then packed on its own in the reference's compact mesh form.
 struct PackedHeader {
+    // object selection the header was packed from: objects [first, first + n_objects) of the
+    // dataset, or (ids non-empty) the listed global object ids, ascending
+    size_t first = 0;
+    std::vector<uint32_t> ids;
     uint32_t n_objects = 0;
     std::vector<int32_t> levels;
     PinnedArr<double> mbb, anchor, voxel_box, voxel_anchor;     // page-locked, reused across joins
@@ -96,23 +106,56 @@ struct PackedLevel {
     tj_level_mesh_view view{};
 };
 std::unique_ptr<PackedHeader> pack_header(const PreparedDataset& ds, ThreadPool& pool);
-std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& ds, const PackedHeader& h, size_t li, ThreadPool& pool);
 // The same over objects [first, last) of ds (one R chunk of the out-of-core path).
 std::unique_ptr<PackedHeader> pack_header(const PreparedDataset& ds, size_t first, size_t last, ThreadPool& pool);
-std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& ds, size_t first, const PackedHeader& h, size_t li,
-                                        ThreadPool& pool);
+// The same over the listed objects of ds (ascending global ids: one query shard).
+std::unique_ptr<PackedHeader> pack_header(const PreparedDataset& ds, std::vector<uint32_t> ids, ThreadPool& pool);
 // Rows of one packed piece of a level: vertices, facets and voxel facet-id entries.
 struct PieceRows {
     uint64_t vert_begin, vert_end, facet_begin, facet_end, entry_begin, entry_end;
 };
-// pack_level in `pieces` consecutive object ranges; on_piece(level, rows) runs after each
-// (the caller ships the rows while the next piece is packed).
+// Level slot li of the objects h was packed from. With pieces > 1 it is packed in that many
+// consecutive object ranges and on_piece(level, rows) runs after each (the caller ships the
+// rows while the next piece is packed).
 std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& ds, const PackedHeader& h, size_t li, ThreadPool& pool,
-                                        size_t pieces,
-                                        const std::function<void(const PackedLevel&, const PieceRows&)>& on_piece);
+                                        size_t pieces = 1,
+                                        const std::function<void(const PackedLevel&, const PieceRows&)>& on_piece = {});
 
-// Lazily created context per CUDA device, destroyed at process exit.
-tj_ctx* device_context(int device);
+// A dataset's streamed form, packed once and reused by every join of the same immutable
+// dataset (the Python Dataset objects): header + the levels packed so far, by slot.
+struct PackedSet {
+    std::unique_ptr<PackedHeader> h;
+    std::vector<std::unique_ptr<PackedLevel>> levels;
+};
+
+// Packed sets of one immutable dataset, kept across joins (keyed by object selection). A
+// set is lent to one join at a time; a concurrent join of the same selection packs afresh.
+struct JoinCache {
+    std::mutex mu;
+    std::map<std::string, std::shared_ptr<PackedSet>> idle;
+    std::shared_ptr<PackedSet> take(const std::string& key) {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = idle.find(key);
+        if (it == idle.end()) return std::make_shared<PackedSet>();
+        auto s = std::move(it->second);
+        idle.erase(it);
+        return s;
+    }
+    void give_back(const std::string& key, std::shared_ptr<PackedSet> s) {
+        std::lock_guard<std::mutex> lk(mu);
+        idle[key] = std::move(s);
+    }
+};
+
+// run_join with optional per-dataset caches of the packed streamed form (nullptr = pack
+// afresh, as the C++ API does: PreparedDataset is caller-owned and may change between calls).
+JoinOutput run_join_cached(const PreparedDataset& R, const PreparedDataset& S, const JoinSpec& spec, ThreadPool& pool,
+                           const JoinTrace* trace, JoinCache* r_cache, JoinCache* s_cache);
+
+// Lazily created context per (CUDA device, slot), destroyed at process exit. Several slots
+// of one device are independent contexts (own stream and workspace): TRIJOIN_DEVICES=0,0
+// runs two query shards side by side on GPU 0.
+tj_ctx* device_context(int device, int slot = 0);
 // Devices used by run_join: $TRIJOIN_DEVICES (comma list) or {0}.
 std::vector<int> join_devices();
 

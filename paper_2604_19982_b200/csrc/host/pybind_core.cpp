@@ -8,6 +8,10 @@
 #include <pybind11/stl.h>
 
 #include <chrono>
+#include <csignal>
+#include <cstdlib>
+#include <execinfo.h>
+#include <unistd.h>
 #include <cstring>
 #include <bit>
 #include <map>
@@ -111,7 +115,54 @@ py::tuple pack_output(const JoinOutput& out) {
     return py::make_tuple(records, out.stats.to_json());
 }
 
-py::tuple join_paths(const std::string& r_path, const std::string& s_path, const JoinSpec& spec) {
+// Packed-form caches of the Python Dataset objects (immutable once loaded): keyed by the
+// dataset's address, validated by a weak reference (a freed dataset's entry is dropped).
+detail::JoinCache* dataset_cache(const std::shared_ptr<PreparedDataset>& ds) {
+    static std::mutex mu;
+    static std::map<const PreparedDataset*, std::pair<std::weak_ptr<PreparedDataset>, std::unique_ptr<detail::JoinCache>>>
+        caches;
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto it = caches.begin(); it != caches.end();)
+        it = it->second.first.expired() ? caches.erase(it) : std::next(it);
+    auto& e = caches[ds.get()];
+    if (!e.second || e.first.lock() != ds) e = {ds, std::make_unique<detail::JoinCache>()};
+    return e.second.get();
+}
+
+// Records as a numpy structured array: r u4, s u4, lb f8, ub f8, stage i2, rank u4.
+py::object records_array(const JoinOutput& out) {
+    struct Rec {
+        uint32_t r, s;
+        double lb, ub;
+        int16_t stage, pad;
+        uint32_t rank;
+    };
+    static_assert(sizeof(Rec) == 32);
+    py::list names, formats, offsets;
+    for (auto [n, f, o] : {std::tuple{"r", "<u4", 0}, {"s", "<u4", 4}, {"lb", "<f8", 8}, {"ub", "<f8", 16},
+                           {"stage", "<i2", 24}, {"rank", "<u4", 28}}) {
+        names.append(n);
+        formats.append(f);
+        offsets.append(o);
+    }
+    py::dict spec;
+    spec["names"] = names;
+    spec["formats"] = formats;
+    spec["offsets"] = offsets;
+    spec["itemsize"] = 32;
+    const py::dtype dt = py::reinterpret_borrow<py::dtype>(py::module_::import("numpy").attr("dtype")(spec));
+    if (dt.itemsize() != static_cast<py::ssize_t>(sizeof(Rec))) throw std::runtime_error("record dtype is not 32 bytes");
+    py::array a(dt, std::vector<py::ssize_t>{static_cast<py::ssize_t>(out.records.size())});
+    Rec* w = static_cast<Rec*>(a.mutable_data());
+    for (size_t i = 0; i < out.records.size(); ++i) {
+        const JoinResultRecord& x = out.records[i];
+        w[i] = {x.r, x.s, x.lb, x.ub, x.decided_at, 0, x.rank};
+    }
+    return a;
+}
+
+py::tuple join_paths(const std::string& r_path, const std::string& s_path, const JoinSpec& spec,
+                     bool oracle = false) {
     JoinOutput out;
     {
         py::gil_scoped_release release;
@@ -123,7 +174,7 @@ py::tuple join_paths(const std::string& r_path, const std::string& s_path, const
             s_store = load_index(s_path);
             S = &s_store;
         }
-        out = run_join(R, *S, spec, pool);
+        out = oracle ? run_oracle(R, *S, spec, pool) : run_join(R, *S, spec, pool);
     }
     return pack_output(out);
 }
@@ -131,20 +182,34 @@ py::tuple join_paths(const std::string& r_path, const std::string& s_path, const
 // A device-resident (R, S) pair on one GPU: packed and uploaded once, joined many times.
 class Resident {
 public:
-    Resident(DatasetPtr R, DatasetPtr S, int device, unsigned workers) : R_(std::move(R)), S_(std::move(S)) {
+    // shard_count > 1: only the queries of shard shard_index (blocks of `block` queries dealt
+    // round-robin) are packed and uploaded; S is uploaded whole.
+    Resident(DatasetPtr R, DatasetPtr S, int device, unsigned workers, uint32_t shard_index, uint32_t shard_count,
+             uint32_t block)
+        : R_(std::move(R)), S_(std::move(S)) {
         py::gil_scoped_release release;
         ctx_ = detail::device_context(device);
         ThreadPool pool(workers);
-        auto pr = detail::pack_dataset(*R_, pool);
+        std::vector<uint32_t> ids;
+        const bool sharded = shard_count > 1;
+        if (sharded) {
+            if (shard_index >= shard_count || block == 0) throw std::invalid_argument("Resident: bad shard");
+            const size_t nr = R_->objects.size();
+            for (size_t b0 = size_t{shard_index} * block; b0 < nr; b0 += size_t{shard_count} * block)
+                for (size_t r = b0; r < std::min(nr, b0 + block); ++r) ids.push_back(static_cast<uint32_t>(r));
+        }
+        n_queries_ = sharded ? ids.size() : R_->objects.size();
+        auto pr = detail::pack_dataset(*R_, pool, sharded ? &ids : nullptr);
         detail::check(tj_dataset_upload(ctx_, &pr->view, &dr_.p), ctx_);
         bytes_ = pr->bytes();
-        if (S_.get() != R_.get()) {
+        if (sharded || S_.get() != R_.get()) {
             auto ps = detail::pack_dataset(*S_, pool);
             detail::check(tj_dataset_upload(ctx_, &ps->view, &ds_.p), ctx_);
             bytes_ += ps->bytes();
         }
     }
     uint64_t device_bytes() const { return bytes_; }
+    uint64_t n_queries() const { return n_queries_; }
 
     py::dict run(const std::string& type, double tau, uint32_t k, const std::vector<uint32_t>& lods,
                  uint64_t refine_chunk, uint32_t flags, uint32_t shard_index, uint32_t shard_count,
@@ -216,6 +281,7 @@ public:
 
 private:
     DatasetPtr R_, S_;
+    uint64_t n_queries_ = 0;
     tj_ctx* ctx_ = nullptr;
     detail::DatasetHandle dr_, ds_;
     uint64_t bytes_ = 0;
@@ -223,7 +289,22 @@ private:
 
 } // namespace
 
+// $TRIJOIN_BACKTRACE=1: print a native backtrace on SIGSEGV / SIGABRT (diagnostics).
+void crash_handler(int sig) {
+    void* frames[64];
+    const int n = backtrace(frames, 64);
+    const char msg[] = "trijoin: fatal signal, native backtrace:\n";
+    (void)!write(2, msg, sizeof(msg) - 1);
+    backtrace_symbols_fd(frames, n, 2);
+    std::signal(sig, SIG_DFL);
+    std::raise(sig);
+}
+
 PYBIND11_MODULE(_core, m) {
+    if (const char* e = std::getenv("TRIJOIN_BACKTRACE"); e && *e == '1') {
+        std::signal(SIGSEGV, crash_handler);
+        std::signal(SIGABRT, crash_handler);
+    }
     m.doc() = "B200-native filter-and-refine spatial joins over triangulated polyhedra (trijoin drop-in)";
 
     py::register_exception<EngineError>(m, "EngineError", PyExc_RuntimeError);
@@ -242,6 +323,35 @@ PYBIND11_MODULE(_core, m) {
         py::arg("workers") = 0, py::arg("seed") = 0, py::arg("exact") = false,
         "Returns (records, stats_json). Each record is (r, s, lb, ub, stage, rank); rank is 0 except for knn. "
         "s defaults to a self-join on r.");
+
+    m.def(
+        "oracle",
+        [](const std::string& r, const std::string& s, const std::string& type, double tau, uint32_t k,
+           uint32_t workers, uint64_t seed) {
+            return join_paths(r, s, make_spec(type, tau, k, 4194304, 500000, {20, 40, 60, 80, 100}, true, workers,
+                                              seed, false),
+                              true);
+        },
+        py::arg("r"), py::arg("s") = "", py::arg("type") = "within", py::arg("tau") = 0.0, py::arg("k") = 1,
+        py::arg("workers") = 0, py::arg("seed") = 0,
+        "Exhaustive exact join over the level-100 geometry on the GPU (reference _core.oracle). "
+        "Returns (records, stats_json).");
+
+    m.def(
+        "oracle_datasets",
+        [](const PreparedDataset& R, const PreparedDataset& S, const std::string& type, double tau, uint32_t k) {
+            JoinOutput out;
+            {
+                py::gil_scoped_release release;
+                ThreadPool pool(1);
+                out = run_oracle(R, S, make_spec(type, tau, k, 4194304, 500000, {20, 40, 60, 80, 100}, true, 1, 0,
+                                                 false),
+                                 pool);
+            }
+            return pack_output(out);
+        },
+        py::arg("r"), py::arg("s"), py::arg("type") = "within", py::arg("tau") = 0.0, py::arg("k") = 1,
+        "run_oracle on loaded datasets (s may be r: self-join). Returns (records, stats_json).");
 
     py::class_<PreparedDataset, std::shared_ptr<PreparedDataset>>(m, "Dataset")
         .def_property_readonly("n_objects", [](const PreparedDataset& d) { return d.objects.size(); })
@@ -297,27 +407,38 @@ PYBIND11_MODULE(_core, m) {
         "join_datasets",
         [](std::shared_ptr<PreparedDataset> R, std::shared_ptr<PreparedDataset> S, const std::string& type, double tau,
            uint32_t k, uint64_t filter_chunk, uint64_t refine_chunk, const std::vector<uint32_t>& lods, bool pipeline,
-           uint32_t workers, bool exact) {
+           uint32_t workers, bool exact, const std::string& records) {
             const JoinSpec spec = make_spec(type, tau, k, filter_chunk, refine_chunk, lods, pipeline, workers, 0, exact);
             JoinOutput out;
             {
                 py::gil_scoped_release release;
                 ThreadPool pool(workers);
-                out = run_join(*R, S ? *S : *R, spec, pool);
+                // the datasets' packed streamed form is kept with them: later joins only copy
+                detail::JoinCache* rc = dataset_cache(R);
+                detail::JoinCache* sc = S && S != R ? dataset_cache(S) : rc;
+                out = detail::run_join_cached(*R, S ? *S : *R, spec, pool, nullptr, rc, sc);
             }
+            if (records == "array") return py::tuple(py::make_tuple(records_array(out), out.stats.to_json()));
+            if (records != "list") throw std::invalid_argument("records must be 'list' or 'array'");
             return pack_output(out);
         },
         py::arg("R"), py::arg("S") = nullptr, py::arg("type") = "within", py::arg("tau") = 0.0, py::arg("k") = 1,
         py::arg("filter_chunk") = 4194304, py::arg("refine_chunk") = 500000,
         py::arg("lods") = std::vector<uint32_t>{20, 40, 60, 80, 100}, py::arg("pipeline") = true,
-        py::arg("workers") = 0, py::arg("exact") = false,
-        "run_join on in-memory datasets (host buffers in, records out): packs, uploads, joins, copies back.");
+        py::arg("workers") = 0, py::arg("exact") = false, py::arg("records") = "list",
+        "run_join on in-memory datasets (host buffers in, records out): packs (once per dataset; the packed "
+        "form is kept with the dataset), uploads, joins, copies back. records='array' returns the records as "
+        "a numpy structured array (r, s, lb, ub, stage code, rank) instead of a list of tuples.");
 
     py::class_<Resident>(m, "Resident")
         .def(py::init([](std::shared_ptr<PreparedDataset> R, std::shared_ptr<PreparedDataset> S, int device,
-                         unsigned workers) { return new Resident(R, S ? S : R, device, workers); }),
-             py::arg("R"), py::arg("S") = nullptr, py::arg("device") = 0, py::arg("workers") = 0)
+                         unsigned workers, uint32_t shard_index, uint32_t shard_count, uint32_t block) {
+                 return new Resident(R, S ? S : R, device, workers, shard_index, shard_count, block);
+             }),
+             py::arg("R"), py::arg("S") = nullptr, py::arg("device") = 0, py::arg("workers") = 0,
+             py::arg("shard_index") = 0u, py::arg("shard_count") = 1u, py::arg("block") = 1024u)
         .def_property_readonly("device_bytes", &Resident::device_bytes)
+        .def_property_readonly("n_queries", &Resident::n_queries)
         .def("run", &Resident::run, py::arg("type") = "within", py::arg("tau") = 0.0, py::arg("k") = 1,
              py::arg("lods") = std::vector<uint32_t>{20, 40, 60, 80, 100}, py::arg("refine_chunk") = 500000,
              py::arg("flags") = 0u, py::arg("shard_index") = 0u, py::arg("shard_count") = 1u,

@@ -860,26 +860,6 @@ __global__ void __launch_bounds__(128) k_eval(RefineSource src, RefineQueue q, u
     }
 }
 
-__device__ __noinline__ double tri_tri_call(uint32_t a, uint32_t b) { return tri_tri(a, b); }
-
-__global__ void __launch_bounds__(128) tri_tri_batch_kernel(uint64_t n, const double* __restrict__ a9,
-                                                            const double* __restrict__ b9, double* __restrict__ out) {
-    __shared__ double rec[128][2][kFacetWords];
-    const uint32_t ta = smem_addr(&rec[threadIdx.x][0][0]), tb = smem_addr(&rec[threadIdx.x][1][0]);
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        double n2, s2;
-        stage_exact(a9 + 9 * i, 0.0, 0.0, ta, &n2, &s2);
-        stage_exact(b9 + 9 * i, 0.0, 0.0, tb, &n2, &s2);
-        out[i] = tri_tri_call(ta, tb);
-    }
-}
-
-__global__ void mindist_batch_kernel(uint64_t n, const double* __restrict__ a6, const double* __restrict__ b6,
-                                     double* __restrict__ out) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-        out[i] = mindist_box(a6 + 6 * i, b6 + 6 * i);
-}
-
 constexpr size_t kScreenSmem = sizeof(ScreenSmem) * (kScreenThreads / 32);
 
 inline int warp_grid(uint64_t warps, int num_sms, int per_sm, int warps_per_block = 8) {
@@ -968,22 +948,6 @@ void refine_pass(const RefineSource& src, uint64_t vp_begin, uint64_t vp_end, bo
     }
     count_launch();
     k_eval<<<grid, 128, 0, st>>>(src, qs.view(), lb_bits, ub_bits, counters, cull);
-    TJ_CUDA(cudaGetLastError());
-}
-
-void launch_tri_tri_batch(uint64_t n, const double* a9, const double* b9, double* out, cudaStream_t st) {
-    if (!n) return;
-    const int grid = (int)std::min<uint64_t>((n + 127) / 128, 148 * 8);
-    count_launch();
-    tri_tri_batch_kernel<<<grid, 128, 0, st>>>(n, a9, b9, out);
-    TJ_CUDA(cudaGetLastError());
-}
-
-void launch_mindist_batch(uint64_t n, const double* a6, const double* b6, double* out, cudaStream_t st) {
-    if (!n) return;
-    const int grid = (int)std::min<uint64_t>((n + 255) / 256, 148 * 8);
-    count_launch();
-    mindist_batch_kernel<<<grid, 256, 0, st>>>(n, a6, b6, out);
     TJ_CUDA(cudaGetLastError());
 }
 

@@ -219,8 +219,5 @@ void refine_pass(const RefineSource& src, uint64_t vp_begin, uint64_t vp_end, bo
 // Diagnostics (TRIJOIN_DEBUG_OPSTATS): per-op tested-pair counters of k_screen (nullptr = off).
 void refine_debug_op_tested(unsigned long long* p);
 
-// kernels (refine.cu)
-void launch_tri_tri_batch(uint64_t n, const double* a9, const double* b9, double* out, cudaStream_t st);
-void launch_mindist_batch(uint64_t n, const double* a6, const double* b6, double* out, cudaStream_t st);
 
 } // namespace tjx

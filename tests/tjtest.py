@@ -49,6 +49,16 @@ class JoinSpec(ctypes.Structure):
 MAXL = 16
 
 
+class MeshSetView(ctypes.Structure):
+    _fields_ = [("n_objects", ctypes.c_uint32), ("tri_offsets", PU64), ("tris", PD)]
+
+
+class ExhaustiveResult(ctypes.Structure):
+    _fields_ = [("n_records", ctypes.c_uint64), ("r", PU32), ("s", PU32), ("d", PD), ("rank", PU32),
+                ("object_pairs", ctypes.c_uint64), ("facet_pairs_evaluated", ctypes.c_uint64),
+                ("total_ms", ctypes.c_double)]
+
+
 class JoinResult(ctypes.Structure):
     _fields_ = [("n_cands", ctypes.c_uint64), ("n_queries", ctypes.c_uint32), ("pair_r", PU32), ("pair_s", PU32),
                 ("lb", PD), ("ub", PD), ("status", ctypes.POINTER(ctypes.c_uint8)),
@@ -119,6 +129,34 @@ class Capi:
         b = np.ascontiguousarray(b, dtype=np.float64)
         out = np.zeros(len(a))
         self.check(self.lib.tj_mindist_batch(self.ctx, ctypes.c_uint64(len(a)), ptr(a), ptr(b), ptr(out)))
+        return out
+
+    GEOM = {"mindist": 0, "point_segment": 1, "point_triangle": 2, "segment_segment": 3, "tri_tri": 4}
+
+    def geom(self, op, a, b):
+        """tj_geom_batch (include/tj_capi.h): out[i] = op(a[i], b[i])."""
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        out = np.zeros(len(a))
+        self.check(self.lib.tj_geom_batch(self.ctx, ctypes.c_int32(self.GEOM[op]), ctypes.c_uint64(len(a)), ptr(a),
+                                          ptr(b), ptr(out)))
+        return out
+
+    def exhaustive(self, R, S, type="within", tau=0.0, k=1):
+        """tj_exhaustive_join over level-100 triangle sets given as (tri_offsets u64[n+1],
+        tris f64[m, 9]); S None = self-join. Returns a list of (r, s, d, rank)."""
+        def view(ms):
+            off = np.ascontiguousarray(ms[0], dtype=np.uint64)
+            tris = np.ascontiguousarray(ms[1], dtype=np.float64)
+            return MeshSetView(len(off) - 1, ptr(off, PU64), ptr(tris)), (off, tris)
+        rv, keep_r = view(R)
+        sv, keep_s = view(S) if S is not None else (None, None)
+        res = ExhaustiveResult()
+        self.check(self.lib.tj_exhaustive_join(self.ctx, ctypes.byref(rv), ctypes.byref(sv) if sv else None,
+                                               ctypes.c_int32(self.TYPES[type]), ctypes.c_double(tau),
+                                               ctypes.c_uint32(k), ctypes.byref(res)))
+        out = [(res.r[i], res.s[i], res.d[i], res.rank[i]) for i in range(res.n_records)]
+        self.lib.tj_exhaustive_result_free(ctypes.byref(res))
         return out
 
     def refine_batch(self, tris, hd, ph, r_off, s_off, r_len, s_len, flags=0):

@@ -61,6 +61,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cull", action="store_true", help="disable exact-preserving culling (A/B)")
     p.add_argument("--profile", action="store_true", help="one resident join only (for ncu)")
+    p.add_argument("--residency", default="auto", choices=["auto", "compact", "expanded"],
+                   help="device residency of the value-leg datasets (auto: compact for D, E)")
     return p.parse_args()
 
 
@@ -185,15 +187,17 @@ def ref_join(lib, r_path, s_path, kw, lods, workers, repeats=1, records_path=Non
     return res
 
 
-def slice_parity(gpu_records, ref_records, stride):
+def slice_parity(gpu_records, ref_records, stride, s_ids=None):
     """Bitwise comparison of the GPU's records of queries r % stride == 0 with the reference's
     records of the R-slice (slice query r' is query r' * stride; per-query independence,
-    SURVEY §8e). lb / ub compare as IEEE bit patterns."""
+    SURVEY §8e; with s_ids the slice's S file holds only those S objects: s' -> s_ids[s']).
+    lb / ub compare as IEEE bit patterns."""
     def key(rec):
         r, s, lb, ub, stage, rank = rec
         return (r, s, np.float64(lb).view(np.uint64).item(), np.float64(ub).view(np.uint64).item(), stage, rank)
     mine = [key(x) for x in gpu_records if x[0] % stride == 0]
-    theirs = [key((r * stride,) + tuple(rest)) for r, *rest in ref_records]
+    theirs = [key((r * stride, int(s_ids[s]) if s_ids is not None else s) + tuple(rest))
+              for r, s, *rest in ref_records]
     mismatches = sum(1 for a, b in zip(mine, theirs) if a != b) + abs(len(mine) - len(theirs))
     return {"stride": stride, "slice_records": len(theirs), "gpu_records": len(mine), "mismatches": mismatches,
             "compared": "r, s, lb bits, ub bits, stage, rank of every record, in the reference's order"}
@@ -210,12 +214,22 @@ def load_synth_tables():
     return mod
 
 
+# Configurations built in memory (their full index files would not fit the box's disk): the
+# reference's R-slice runs against only the S objects near the slice (synth.write_slice_files).
+IN_MEMORY = ("D", "E")
+
+
 def build_slice_subprocess(name, data_dir, scale, stride):
     """Slice index files for the reference arm, written by a separate process so the timed
     reference process maps only oracle/_ref (the writer is this repo's replicate_index)."""
-    code = ("import sys, json; sys.path.insert(0, %r); from paper_2604_19982_b200 import synth; "
-            "print(json.dumps(synth.build_config(%r, %r, scale=%r, r_stride=%d)))" % (ROOT, name, data_dir, scale,
-                                                                                     stride))
+    if name in IN_MEMORY:
+        code = ("import sys, json; sys.path.insert(0, %r); from paper_2604_19982_b200 import synth; "
+                "r, s, ri, si = synth.write_slice_files(%r, %r, %d, %r); print(json.dumps([r, s]))"
+                % (ROOT, name, scale, stride, data_dir))
+    else:
+        code = ("import sys, json; sys.path.insert(0, %r); from paper_2604_19982_b200 import synth; "
+                "print(json.dumps(synth.build_config(%r, %r, scale=%r, r_stride=%d)))" % (ROOT, name, data_dir, scale,
+                                                                                         stride))
     out = subprocess.run([sys.executable, "-c", code], check=True, capture_output=True, text=True).stdout
     return tuple(json.loads(out.strip().splitlines()[-1]))
 
@@ -277,15 +291,22 @@ def main():
 
     # ---- inputs (built once per box; node-local rank 0 writes, others wait) ----
     t_setup = time.time()
-    if local == 0:
+    in_memory = name in IN_MEMORY
+    if in_memory:  # translated template copies straight into memory (no index files)
+        R, S, _ = synth.build_datasets(name, scale=a.scale)
+    else:
+        if local == 0:
+            r_path, s_path = synth.build_config(name, data_dir, scale=a.scale)
+        if world > 1:
+            dist.barrier()
         r_path, s_path = synth.build_config(name, data_dir, scale=a.scale)
-    if world > 1:
-        dist.barrier()
-    r_path, s_path = synth.build_config(name, data_dir, scale=a.scale)
-    R = tj.load_dataset(r_path)
-    S = tj.load_dataset(s_path) if s_path else R  # "" = self-join (config E)
-    # each rank uploads only its own query shard of R (blocks of 1024 queries dealt round-robin)
-    res = tj.Resident(R, S, device=local, shard_index=rank, shard_count=world)
+        R = tj.load_dataset(r_path)
+        S = tj.load_dataset(s_path) if s_path else R  # "" = self-join (config E)
+    # each rank uploads only its own query shard of R (blocks of 1024 queries dealt round-robin);
+    # D / E: the expanded form exceeds HBM, so the datasets stay compact-resident and each
+    # level's active voxels are expanded on demand (TJ_DATASET_COMPACT)
+    compact = a.residency == "compact" or (a.residency == "auto" and in_memory)
+    res = tj.Resident(R, S, device=local, shard_index=rank, shard_count=world, compact=compact)
     setup_s = time.time() - t_setup
     flags = 1 if a.no_cull else 0
     run_kw = dict(type=kw["type"], tau=float(kw.get("tau", 0.0)), k=int(kw.get("k", 1)), lods=lods, flags=flags)
@@ -364,6 +385,10 @@ def main():
                 "cull_skip_frac": 1.0 - evaluated / fp if fp else None}
 
     # ---- e2e: public API from host buffers ----
+    # the e2e leg uploads its own copies: release the resident datasets first (their pooled
+    # device memory is reused)
+    res_bytes, n_q = res.device_bytes, res.n_queries
+    del res
     e2e = None
     gpu_records = None
     if not a.no_e2e:
@@ -386,7 +411,6 @@ def main():
             gpu_records = recs
             st = json.loads(js)
             n_c = st["stages"][0]["pairs_in"] - st["stages"][0]["removed"]
-            n_q = res.n_queries
             d2h = n_c * (4 + 4 + 8 + 8 + 1 + 2) + (n_q + 1) * 8 + n_q * 4
             pairs_e2e = st["stages"][1]["pairs_in"]
             if i > 0:
@@ -414,18 +438,23 @@ def main():
     parity = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         try:
-            r_slice, s_full = synth.build_config(name, data_dir + "_slice", scale=a.scale, r_stride=a.cpu_stride)
+            s_ids = None
+            if in_memory:
+                r_slice, s_full, _, s_ids = synth.write_slice_files(name, a.scale, a.cpu_stride, data_dir + "_slice")
+            else:
+                r_slice, s_full = synth.build_config(name, data_dir + "_slice", scale=a.scale, r_stride=a.cpu_stride)
             if gpu_records is None:  # the public API's records of the full workload (untimed)
                 gpu_records, _ = _core.join_datasets(R, S, type=kw["type"], tau=float(kw.get("tau", 0.0)),
                                                      k=int(kw.get("k", 1)), lods=lods, records="array")
             gpu_records = tjdist.records_to_tuples(gpu_records)
             rec_path = os.path.join(data_dir + "_slice", "ref_records.bin")
             rj = ref_join(ref_shim(), r_slice, s_full, kw, lods, os.cpu_count() or 1, records_path=rec_path)
-            parity = slice_parity(gpu_records, rj["records"], a.cpu_stride)
+            parity = slice_parity(gpu_records, rj["records"], a.cpu_stride, s_ids)
             parity["slice_candidates"] = int(rj["pairs_in"])
             cpu = {"value": rj["pairs_in"] / (rj["ms"] / 1e3), "unit": "pairs/s", "cores": rj["cores"],
                    "kind": "reference",
-                   "sample": f"reference run_join (oracle/_ref) on every {a.cpu_stride}th query object vs the full S: "
+                   "sample": f"reference run_join (oracle/_ref) on every {a.cpu_stride}th query object vs "
+                             f"{('the ' + str(len(s_ids)) + ' S objects near the slice') if in_memory else 'the full S'}: "
                              f"{int(rj['pairs_in'])} candidate pairs, {int(rj['facet_pairs'])} facet pairs, "
                              f"{rj['ms'] / 1e3:.1f} s",
                    "facet_pairs_per_s": rj["facet_pairs"] / (rj["ms"] / 1e3)}
@@ -441,7 +470,7 @@ def main():
                 "config": {"workload": workload, "lods": lods, "scale": a.scale,
                            "candidate_pairs": pairs, "facet_pairs_ref_count": fp,
                            "join_wall_ms": ms_per_step, "l2": "inputs larger than L2 "
-                           f"({res.device_bytes / 1e9:.1f} GB resident)", "parallelism": f"r-shard x{world}",
+                           f"({res_bytes / 1e9:.1f} GB resident)", "parallelism": f"r-shard x{world}",
                            "setup_s": round(setup_s, 1), "cull": not a.no_cull,
                            "step_ms": [round(x, 2) for x in step_ms],
                            "levels_last_step": outs[-1]["levels"]},

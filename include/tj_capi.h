@@ -159,6 +159,7 @@ typedef struct tj_join_result {
     double level_wait_ms[TJ_MAX_LODS];           /* host time blocked on a streamed level */
     int32_t decision_mode;                       /* 1: refined in decision mode (TJ_FLAG_EXACT_INTERVALS) */
     uint32_t queue_reruns;                       /* levels re-run after an exact-queue overflow */
+    uint64_t mat_chunks;                         /* compact-resident datasets: level expansions (chunks) */
 } tj_join_result;
 
 /* ---- context ---- */
@@ -223,6 +224,14 @@ typedef struct tj_level_mesh_view {
 
 int tj_dataset_begin(tj_ctx* ctx, const tj_dataset_view* header, const uint64_t* const* vert_base,
                      const uint64_t* const* facet_base, tj_dataset** out);
+/* tj_dataset_begin_ex(flags = TJ_DATASET_COMPACT): the dataset keeps every level in HBM in the
+ * shipped compact mesh form (~44 B per facet instead of ~224 B of expanded FP64 records and
+ * FP32 screening records) and a join expands, per level, only the voxels of its active voxel
+ * pairs, in chunks of a working-set budget ($TRIJOIN_WORKSET_MB) if need be. For inputs whose
+ * expanded form exceeds HBM (SURVEY configs D, E); results are identical. */
+#define TJ_DATASET_COMPACT 1u
+int tj_dataset_begin_ex(tj_ctx* ctx, const tj_dataset_view* header, const uint64_t* const* vert_base,
+                        const uint64_t* const* facet_base, uint32_t flags, tj_dataset** out);
 int tj_dataset_put_level(tj_dataset* ds, uint32_t slot, const tj_level_mesh_view* lv);
 int tj_dataset_put_level_part(tj_dataset* ds, uint32_t slot, const tj_level_mesh_view* lv, uint64_t vert_begin,
                               uint64_t vert_end, uint64_t facet_begin, uint64_t facet_end, uint64_t entry_begin,

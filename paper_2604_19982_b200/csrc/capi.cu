@@ -181,14 +181,21 @@ __global__ void k_expand_level(const double* __restrict__ verts, const Id* __res
                                const Id* __restrict__ vf, const uint64_t* __restrict__ foff,
                                const uint32_t* __restrict__ vox_obj, const uint64_t* __restrict__ vb,
                                const uint64_t* __restrict__ fb, uint64_t n_voxels, double* __restrict__ out,
-                               int* __restrict__ err) {
+                               int* __restrict__ err, const uint64_t* __restrict__ act) {
     const int lane = threadIdx.x & 31;
     const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
     for (uint64_t v = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); v < n_voxels; v += warps) {
+        const uint64_t e0 = foff[v], e1 = foff[v + 1];
+        // act (on-demand expansion of a compact-resident level): only the flagged voxels, packed
+        uint64_t w0 = e0;
+        if (act) {
+            const uint64_t a0 = act[v];
+            if (act[v + 1] == a0) continue;
+            w0 = a0;
+        }
         const uint32_t o = vox_obj[v];
         const uint64_t v_lo = vb[o], nv = vb[o + 1] - v_lo;
         const uint64_t f_lo = fb[o], nf = fb[o + 1] - f_lo;
-        const uint64_t e0 = foff[v], e1 = foff[v + 1];
         bool bad = false;
         for (uint64_t e = e0 + lane; e < e1; e += 32) {
             uint64_t f = __ldg(vf + e);
@@ -213,9 +220,11 @@ __global__ void k_expand_level(const double* __restrict__ verts, const Id* __res
             r[9] = nf && hd ? __ldg(hd + f) : 0.0; // hd / ph NULL: the level's paddings are all 0
             r[10] = nf && ph ? __ldg(ph + f) : 0.0;
             r[11] = 0.0;
-            double2* d = reinterpret_cast<double2*>(out + e * TJ_FACET_STRIDE);
+            if (out) { // out == nullptr: validation only (compact-resident level at arrival)
+                double2* d = reinterpret_cast<double2*>(out + (w0 + (e - e0)) * TJ_FACET_STRIDE);
 #pragma unroll
-            for (int k = 0; k < 6; ++k) d[k] = make_double2(r[2 * k], r[2 * k + 1]);
+                for (int k = 0; k < 6; ++k) d[k] = make_double2(r[2 * k], r[2 * k + 1]);
+            }
         }
         if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(err, 1);
     }
@@ -234,6 +243,31 @@ LevelGate::~LevelGate() {
     for (cudaEvent_t e : ev)
         if (e) cudaEventDestroy(e);
     if (copy) cudaStreamDestroy(copy);
+}
+
+void expand_compact_level(const DatasetDev& d, uint32_t slot, const uint64_t* act, double* out, int num_sms,
+                          cudaStream_t st) {
+    if (!d.compact || !d.n_voxels) return;
+    const StageLayout L = stage_layout(d.level_vertices[slot], d.level_facets[slot], d.level_entries[slot]);
+    const unsigned char* base = d.cmp[slot].p;
+    const uint32_t flags = d.cmp_flags[slot];
+    const bool pads = flags & TJ_LEVEL_PADS;
+    const double* verts = reinterpret_cast<const double*>(base + L.verts);
+    const double* hd = pads && d.level_facets[slot] ? reinterpret_cast<const double*>(base + L.hd) : nullptr;
+    const double* ph = pads && d.level_facets[slot] ? reinterpret_cast<const double*>(base + L.ph) : nullptr;
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((d.n_voxels + 7) / 8, (uint64_t)num_sms * 16));
+    count_launch();
+    if (flags & TJ_LEVEL_NARROW)
+        k_expand_level<<<grid, 256, 0, st>>>(verts, reinterpret_cast<const uint16_t*>(base + L.tris), hd, ph,
+                                             reinterpret_cast<const uint16_t*>(base + L.vf), d.facet_offsets[slot].p,
+                                             d.vox_obj.p, d.vert_base[slot].p, d.facet_base[slot].p, d.n_voxels, out,
+                                             d.stream_err.p, act);
+    else
+        k_expand_level<<<grid, 256, 0, st>>>(verts, reinterpret_cast<const uint32_t*>(base + L.tris), hd, ph,
+                                             reinterpret_cast<const uint32_t*>(base + L.vf), d.facet_offsets[slot].p,
+                                             d.vox_obj.p, d.vert_base[slot].p, d.facet_base[slot].p, d.n_voxels, out,
+                                             d.stream_err.p, act);
+    TJ_CUDA(cudaGetLastError());
 }
 
 double level_ready(const DatasetDev& d, int slot, cudaStream_t st) {
@@ -393,12 +427,18 @@ void tj_dataset_free(tj_dataset* ds) {
 
 int tj_dataset_begin(tj_ctx* ctx, const tj_dataset_view* v, const uint64_t* const* vert_base,
                      const uint64_t* const* facet_base, tj_dataset** out) {
-    if (!ctx || !v || !out || !vert_base || !facet_base) return TJ_EINVAL;
+    return tj_dataset_begin_ex(ctx, v, vert_base, facet_base, 0u, out);
+}
+
+int tj_dataset_begin_ex(tj_ctx* ctx, const tj_dataset_view* v, const uint64_t* const* vert_base,
+                        const uint64_t* const* facet_base, uint32_t flags, tj_dataset** out) {
+    if (!ctx || !v || !out || !vert_base || !facet_base || (flags & ~TJ_DATASET_COMPACT)) return TJ_EINVAL;
     *out = nullptr;
     auto ds = std::make_unique<tj_dataset>();
     ds->ctx = ctx;
     const int rc = guarded(ctx, [&] {
         DatasetDev& d = ds->d;
+        d.compact = (flags & TJ_DATASET_COMPACT) != 0;
         auto gate = std::make_shared<LevelGate>();
         gate->device = ctx->device;
         TJ_CUDA(cudaStreamCreateWithFlags(&gate->copy, cudaStreamNonBlocking));
@@ -430,22 +470,33 @@ int tj_dataset_begin(tj_ctx* ctx, const tj_dataset_view* v, const uint64_t* cons
             upload(d.facet_offsets[li], fo, d.n_voxels + 1, st);
             upload(d.vert_base[li], vb, no + 1ull, st);
             upload(d.facet_base[li], fb, no + 1ull, st);
-            d.facets[li].alloc(std::max<uint64_t>(entries, 1) * TJ_FACET_STRIDE);
+            if (!d.compact) d.facets[li].alloc(std::max<uint64_t>(entries, 1) * TJ_FACET_STRIDE);
             d.level_entries.push_back(entries);
             d.level_vertices.push_back(vb[no]);
             d.level_facets.push_back(fb[no]);
-            d.bytes += (d.n_voxels + 1) * 8 + entries * TJ_FACET_STRIDE * 8;
+            d.bytes += (d.n_voxels + 1) * 8 + (d.compact ? 0 : entries * TJ_FACET_STRIDE * 8);
         }
-        uint64_t stage_bytes = 256;
-        for (uint32_t li = 0; li < v->n_levels; ++li)
-            stage_bytes = std::max(stage_bytes, stage_layout(d.level_vertices[li], d.level_facets[li], d.level_entries[li]).total);
-        d.stage.alloc(stage_bytes);
-        // derived screening data, reserved here (a put never allocates while a join runs)
         d.screen.resize(v->n_levels);
         d.seg.resize(v->n_levels);
-        for (uint32_t li = 0; li < v->n_levels; ++li) {
-            d.screen[li].alloc(std::max<uint64_t>(d.level_entries[li] * kScreenRecF4, 1));
-            d.seg[li].alloc(std::max<uint64_t>(3 * d.n_voxels, 1));
+        if (d.compact) { // every level keeps its own compact storage
+            d.cmp.resize(v->n_levels);
+            d.cmp_flags.assign(v->n_levels, 0u);
+            for (uint32_t li = 0; li < v->n_levels; ++li) {
+                const uint64_t b = stage_layout(d.level_vertices[li], d.level_facets[li], d.level_entries[li]).total;
+                d.cmp[li].alloc(std::max<uint64_t>(b, 256));
+                d.bytes += b;
+            }
+        } else {
+            uint64_t stage_bytes = 256;
+            for (uint32_t li = 0; li < v->n_levels; ++li)
+                stage_bytes = std::max(stage_bytes,
+                                       stage_layout(d.level_vertices[li], d.level_facets[li], d.level_entries[li]).total);
+            d.stage.alloc(stage_bytes);
+            // derived screening data, reserved here (a put never allocates while a join runs)
+            for (uint32_t li = 0; li < v->n_levels; ++li) {
+                d.screen[li].alloc(std::max<uint64_t>(d.level_entries[li] * kScreenRecF4, 1));
+                d.seg[li].alloc(std::max<uint64_t>(3 * d.n_voxels, 1));
+            }
         }
         d.agg.alloc(3 * v->n_levels);
         d.vox_obj.alloc(std::max<uint64_t>(d.n_voxels, 1));
@@ -488,7 +539,7 @@ int tj_dataset_put_level_part(tj_dataset* ds, uint32_t slot, const tj_level_mesh
         // a put never waits on the memory pool while a join runs); the copy stream orders the
         // reuse of the area across levels
         const StageLayout L = stage_layout(nvert, nfac, used);
-        unsigned char* base = d.stage.p;
+        unsigned char* base = d.compact ? d.cmp[slot].p : d.stage.p;
         auto put = [&](uint64_t off, const void* src, uint64_t b0, uint64_t b1, size_t row) {
             if (b1 > b0)
                 TJ_CUDA(cudaMemcpyAsync(base + off + b0 * row, static_cast<const unsigned char*>(src) + b0 * row,
@@ -523,8 +574,10 @@ int tj_dataset_finish_level(tj_dataset* ds, uint32_t slot, uint32_t flags) {
         DatasetDev& d = ds->d;
         const uint64_t nvert = d.level_vertices[slot], nfac = d.level_facets[slot], used = d.level_entries[slot];
         const StageLayout L = stage_layout(nvert, nfac, used);
-        unsigned char* base = d.stage.p;
+        unsigned char* base = d.compact ? d.cmp[slot].p : d.stage.p;
         const bool pads = flags & TJ_LEVEL_PADS;
+        if (d.compact) d.cmp_flags[slot] = flags;
+        double* out = d.compact ? nullptr : d.facets[slot].p; // compact: validate only
         const double* verts = reinterpret_cast<const double*>(base + L.verts);
         const double* hd = pads && nfac ? reinterpret_cast<const double*>(base + L.hd) : nullptr;
         const double* ph = pads && nfac ? reinterpret_cast<const double*>(base + L.ph) : nullptr;
@@ -535,17 +588,17 @@ int tj_dataset_finish_level(tj_dataset* ds, uint32_t slot, uint32_t flags) {
                 k_expand_level<<<grid, 256, 0, g.copy>>>(verts, reinterpret_cast<const uint16_t*>(base + L.tris), hd, ph,
                                                           reinterpret_cast<const uint16_t*>(base + L.vf),
                                                           d.facet_offsets[slot].p, d.vox_obj.p, d.vert_base[slot].p,
-                                                          d.facet_base[slot].p, d.n_voxels, d.facets[slot].p,
-                                                          d.stream_err.p);
+                                                          d.facet_base[slot].p, d.n_voxels, out, d.stream_err.p,
+                                                          nullptr);
             else
                 k_expand_level<<<grid, 256, 0, g.copy>>>(verts, reinterpret_cast<const uint32_t*>(base + L.tris), hd, ph,
                                                           reinterpret_cast<const uint32_t*>(base + L.vf),
                                                           d.facet_offsets[slot].p, d.vox_obj.p, d.vert_base[slot].p,
-                                                          d.facet_base[slot].p, d.n_voxels, d.facets[slot].p,
-                                                          d.stream_err.p);
+                                                          d.facet_base[slot].p, d.n_voxels, out, d.stream_err.p,
+                                                          nullptr);
             TJ_CUDA(cudaGetLastError());
         }
-        derive_level(d, slot, ctx->ws.num_sms, g.copy);
+        if (!d.compact) derive_level(d, slot, ctx->ws.num_sms, g.copy);
         TJ_CUDA(cudaEventRecord(g.ev[slot], g.copy));
     });
     {
@@ -737,6 +790,7 @@ int tj_join(tj_ctx* ctx, const tj_dataset* Rh, const tj_dataset* Sh, const tj_jo
         }
         out->refine_chunks = ro.chunks;
         out->queue_reruns = ro.queue_reruns;
+        out->mat_chunks = ro.mat_chunks;
 
         if (sp.flags & TJ_FLAG_EXACT_RECOMPUTE) exact_recompute_dev(ws, R, S, cs, st);
 

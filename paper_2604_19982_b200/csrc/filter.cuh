@@ -53,8 +53,21 @@ struct CandDevStore {
     }
 };
 
+// One side's on-demand expansion of a compact-resident level (materialize_level): the active
+// voxels' facet records, their FP32 screening records and segment aggregates, grow-only.
+struct LevelMat {
+    DevBuf<uint8_t> flag;       // [nv] voxel touched by the chunk's active voxel pairs
+    DevBuf<uint64_t> cnt, off;  // [nv] facets of touched voxels; [nv+1] their exclusive scan
+    DevBuf<double> facets;      // [total * TJ_FACET_STRIDE]
+    DevBuf<float4> screen, seg; // [total * kScreenRecF4], [3 nv]
+    DevBuf<unsigned> agg;       // [3] level aggregates of the expanded records
+    uint64_t total = 0;
+};
+
 struct Workspace {
     int num_sms = 148;
+    LevelMat mat[2];            // compact-resident datasets: R side, S side
+    uint64_t workset_budget = 0; // bytes for materialized levels (0 = not yet chosen)
     DevBuf<unsigned char> temp;
     DevBuf<uint64_t> u64a;
     std::unique_ptr<RefineQueueStore> queue; // refinement pair queues, grow-only, per context
@@ -74,6 +87,7 @@ struct Workspace {
         seg_s.release();
         active_alt.release();
         nsel.release();
+        for (auto& m : mat) m = LevelMat{};
     }
 };
 
@@ -149,6 +163,7 @@ struct RefineLoopOut {
     std::vector<LevelStats> levels;
     uint64_t chunks = 0;
     uint32_t queue_reruns = 0; // levels re-run after an exact-queue overflow
+    uint64_t mat_chunks = 0;   // compact-resident datasets: materialized chunks over all levels
 };
 struct TraceSink; // host-side trace forwarding (engine.cu)
 RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetDev& S, CandDevStore& cs,

@@ -648,7 +648,8 @@ std::string StageStats::to_json() const {
     j["stages"] = std::move(arr);
     j["b200"] = {{"pack_ms", pack_ms}, {"upload_ms", upload_ms}, {"device_ms", device_ms},
                  {"stream_wait_ms", stream_wait_ms}, {"h2d_bytes", h2d_bytes}, {"devices", devices},
-                 {"intervals", decision_mode ? "decision" : "exact"}, {"r_chunks", r_chunks}};
+                 {"intervals", decision_mode ? "decision" : "exact"}, {"r_chunks", r_chunks},
+                 {"residency", compact ? "compact" : "expanded"}, {"mat_chunks", mat_chunks}};
     nlohmann::json tl = nlohmann::json::object();
     for (const auto& [k, v] : timeline) tl[k] = v;
     j["b200"]["timeline"] = std::move(tl);
@@ -963,12 +964,23 @@ uint64_t object_device_bytes(const PreparedObject& o) {
     return 256 + 112 * nv + 96 * all + (44 + 176) * mx;
 }
 
-// Device-memory budget: $TRIJOIN_DEVICE_BUDGET_MB, else 90 % of the device's free memory
-// (0 = unknown).
+// Device bytes of one object in the compact-resident form (TJ_DATASET_COMPACT): object +
+// voxel records, the per-level voxel CSR, and every level's compact mesh form (vertices,
+// index triples, hd / ph, voxel facet-id lists), as tj_dataset_begin_ex reserves them.
+uint64_t object_compact_bytes(const PreparedObject& o) {
+    const uint64_t nv = o.voxels.voxel_count();
+    uint64_t b = 256 + 112 * nv;
+    for (const auto& lv : o.ladder.levels)
+        b += 8 * nv + 24 * lv.mesh.vertices.size() + (12 + 16 + 4) * lv.mesh.facets.size();
+    return b;
+}
+
+// Device-memory budget: $TRIJOIN_DEVICE_BUDGET_MB, else 90 % of the device's memory less a
+// 2 GiB reserve (0 = unknown). The device's total, not its free memory: this library's memory
+// is pooled (freed blocks stay reserved for its next allocations), so the free figure
+// understates what a join can use. Queried once per device and process.
 uint64_t device_budget(int device) {
     if (const char* e = std::getenv("TRIJOIN_DEVICE_BUDGET_MB"); e && *e) return std::stoull(e) << 20;
-    // queried once per device and process (cudaMemGetInfo costs up to tens of milliseconds
-    // right after a join); this library's memory is pooled and returned between joins
     static std::mutex mu;
     static std::map<int, uint64_t> cache;
     std::lock_guard<std::mutex> lk(mu);
@@ -978,7 +990,8 @@ uint64_t device_budget(int device) {
         cudaGetLastError();
         return 0;
     }
-    return cache[device] = free_b / 10 * 9;
+    const uint64_t reserve = 2ull << 30;
+    return cache[device] = total_b / 10 * 9 > reserve ? total_b / 10 * 9 - reserve : total_b / 2;
 }
 
 // One GPU's share of a join: a query shard (ids ascending; empty = all of R) split into R
@@ -993,31 +1006,74 @@ struct GpuShare {
     size_t size(size_t nr) const { return all ? nr : ids.size(); }
 };
 
-void plan_r_chunks(GpuShare& w, const PreparedDataset& R, uint64_t s_total, size_t contexts_on_device,
-                   ThreadPool& pool) {
+// Device footprints of a dataset: expanded (records + screening data at upload) and compact.
+struct Footprint {
+    uint64_t expanded = 0, compact = 0;
+};
+Footprint dataset_footprint(const PreparedDataset& D, ThreadPool& pool) {
+    std::atomic<uint64_t> e{0}, c{0};
+    detail::for_blocks(pool, D.objects.size(), [&](size_t b, size_t en) {
+        uint64_t ae = 0, ac = 0;
+        for (size_t o = b; o < en; ++o) {
+            ae += object_device_bytes(D.objects[o]);
+            ac += object_compact_bytes(D.objects[o]);
+        }
+        e += ae;
+        c += ac;
+    });
+    return {e.load(), c.load()};
+}
+
+// Share of the device budget the compact-resident datasets may take: the rest is the working
+// set in which each level's active voxels are expanded (chunked on the device to fit it).
+constexpr double kCompactShare = 0.6;
+
+// $TRIJOIN_COMPACT: 1 forces compact-resident datasets, 0 forbids them, unset = by budget.
+int compact_override() {
+    const char* e = std::getenv("TRIJOIN_COMPACT");
+    return e && *e ? (*e == '0' ? 0 : 1) : -1;
+}
+
+// Plans one GPU's R chunks and chooses the residency mode: expanded when R and S fit the
+// budget expanded, else compact-resident (R chunked only if even that does not fit).
+void plan_r_chunks(GpuShare& w, const PreparedDataset& R, const Footprint& s_fp, size_t contexts_on_device,
+                   bool shares_s, bool& compact, ThreadPool& pool) {
     const size_t n = w.size(R.objects.size());
     w.chunks.clear();
+    std::vector<uint64_t> cost_e(n), cost_c(n);
+    std::atomic<uint64_t> e_sum{0}, c_sum{0};
+    detail::for_blocks(pool, n, [&](size_t b, size_t e) {
+        uint64_t ae = 0, ac = 0;
+        for (size_t i = b; i < e; ++i) {
+            const PreparedObject& o = R.objects[w.all ? i : w.ids[i]];
+            ae += cost_e[i] = object_device_bytes(o);
+            ac += cost_c[i] = object_compact_bytes(o);
+        }
+        e_sum += ae;
+        c_sum += ac;
+    });
+    uint64_t budget = device_budget(w.device) / std::max<size_t>(1, contexts_on_device);
+    const uint64_t fixed = (64ull << 20) + 256 * uint64_t{n};
+    // shares_s: a self-join of all of R in one chunk is one device dataset (R = S)
+    const uint64_t r_e = shares_s ? 0 : e_sum.load(), r_c = shares_s ? 0 : c_sum.load();
+    const int forced = compact_override();
+    if (forced >= 0) compact = forced == 1;
+    else compact = budget && r_e + s_fp.expanded + fixed > budget;
     if (const char* e = std::getenv("TRIJOIN_R_CHUNK_OBJECTS"); e && *e) {
         const size_t step = std::max<size_t>(1, std::stoull(e));
         for (size_t a = 0; a < n; a += step) w.chunks.emplace_back(a, std::min(n, a + step));
         if (w.chunks.empty()) w.chunks.emplace_back(0, 0);
         return;
     }
-    uint64_t budget = device_budget(w.device);
     if (budget == 0) {
         w.chunks.emplace_back(0, n);
         return;
     }
-    budget /= std::max<size_t>(1, contexts_on_device);
-    std::vector<uint64_t> cost(n);
-    std::atomic<uint64_t> r_sum{0};
-    detail::for_blocks(pool, n, [&](size_t b, size_t e) {
-        uint64_t acc = 0;
-        for (size_t i = b; i < e; ++i) acc += cost[i] = object_device_bytes(R.objects[w.all ? i : w.ids[i]]);
-        r_sum += acc;
-    });
-    const uint64_t fixed = (64ull << 20) + 256 * uint64_t{n};
-    if (r_sum.load() + s_total + fixed <= budget) {
+    const std::vector<uint64_t>& cost = compact ? cost_c : cost_e;
+    const uint64_t s_total = compact ? s_fp.compact : s_fp.expanded;
+    // compact: the datasets may take kCompactShare of what is left after the fixed part
+    if (compact) budget = budget > fixed ? fixed + uint64_t(double(budget - fixed) * kCompactShare) : budget;
+    if ((compact ? r_c : r_e) + s_total + fixed <= budget) {
         w.chunks.emplace_back(0, n);
         return;
     }
@@ -1038,15 +1094,6 @@ void plan_r_chunks(GpuShare& w, const PreparedDataset& R, uint64_t s_total, size
     w.chunks.emplace_back(a, n);
 }
 
-uint64_t dataset_device_bytes(const PreparedDataset& D, ThreadPool& pool) {
-    std::atomic<uint64_t> sum{0};
-    detail::for_blocks(pool, D.objects.size(), [&](size_t b, size_t e) {
-        uint64_t acc = 0;
-        for (size_t o = b; o < e; ++o) acc += object_device_bytes(D.objects[o]);
-        sum += acc;
-    });
-    return sum.load();
-}
 
 // A packed set for one object selection of a dataset: from the caller's cache (kept for later
 // joins of the same immutable dataset) or fresh (freed after the join).
@@ -1173,12 +1220,20 @@ JoinOutput detail::run_join_cached(const PreparedDataset& R, const PreparedDatas
                 for (size_t r = b0; r < std::min(nr, b0 + block); ++r) share[g].ids.push_back(static_cast<uint32_t>(r));
         }
     }
-    // S stays resident on every GPU for the whole join; R goes in chunks if it does not fit
-    const uint64_t s_total = tracing ? 0 : dataset_device_bytes(S, pool);
+    // S stays resident on every GPU for the whole join; R goes in chunks if it does not fit.
+    // Datasets are compact-resident (levels expanded on demand) when the expanded form would
+    // not fit.
+    const Footprint s_fp = tracing ? Footprint{} : dataset_footprint(S, pool);
+    bool compact = false;
     for (size_t g = 0; g < G; ++g) {
+        bool c = false;
         if (tracing) share[g].chunks = {{0, share[g].size(nr)}};
-        else plan_r_chunks(share[g], R, s_total, per_device[share[g].device], pool);
+        else plan_r_chunks(share[g], R, s_fp, per_device[share[g].device], self_join && G == 1 && Q == 1, c, pool);
+        compact = compact || c;
     }
+    if (tracing && compact_override() == 1) compact = true;
+    const uint32_t ds_flags = compact ? TJ_DATASET_COMPACT : 0u;
+    out.stats.compact = compact;
     // one GPU, all of R in one chunk, self-join: R and S are one device dataset
     const bool one_dataset = self_join && G == 1 && Q == 1 && share[0].chunks.size() == 1;
     uint32_t n_chunks = 0;
@@ -1205,7 +1260,9 @@ JoinOutput detail::run_join_cached(const PreparedDataset& R, const PreparedDatas
         }
         const detail::PackedHeader& hs = *s_lease.set->h;
         for (size_t g = 0; g < G; ++g) {
-            detail::check(tj_dataset_begin(ctxs[g], &hs.view, hs.vb_ptrs.data(), hs.fb_ptrs.data(), &dsh[g].p), ctxs[g]);
+            detail::check(
+                tj_dataset_begin_ex(ctxs[g], &hs.view, hs.vb_ptrs.data(), hs.fb_ptrs.data(), ds_flags, &dsh[g].p),
+                ctxs[g]);
             out.stats.h2d_bytes += hs.bytes();
         }
     }
@@ -1241,7 +1298,8 @@ JoinOutput detail::run_join_cached(const PreparedDataset& R, const PreparedDatas
                 }
                 const detail::PackedHeader& hr = *lz->set->h;
                 detail::DatasetHandle dr;
-                detail::check(tj_dataset_begin(ctx, &hr.view, hr.vb_ptrs.data(), hr.fb_ptrs.data(), &dr.p), ctx);
+                detail::check(tj_dataset_begin_ex(ctx, &hr.view, hr.vb_ptrs.data(), hr.fb_ptrs.data(), ds_flags, &dr.p),
+                              ctx);
                 {
                     std::lock_guard<std::mutex> lk(stat_mu);
                     out.stats.h2d_bytes += hr.bytes();
@@ -1332,6 +1390,7 @@ JoinOutput detail::run_join_cached(const PreparedDataset& R, const PreparedDatas
             const tj_join_result& res = results[g][k]->r;
             for (uint32_t i = 0; i < res.n_levels_run; ++i) out.stats.stream_wait_ms += res.level_wait_ms[i];
             out.stats.decision_mode = out.stats.decision_mode || res.decision_mode != 0;
+            out.stats.mat_chunks += res.mat_chunks;
             const auto [a, b] = share[g].chunks[k];
             const detail::PackedHeader& h = *r_sets[g][k]->set->h;
             pieces.push_back({&res, static_cast<uint32_t>(a), h.ids.empty() ? nullptr : h.ids.data(),
@@ -1339,43 +1398,32 @@ JoinOutput detail::run_join_cached(const PreparedDataset& R, const PreparedDatas
         }
 
     // Merge: every query r this process joins is owned by one piece (a chunk of a GPU's
-    // shard, queries ids[0, n) or r_base + [0, n)); the others have empty ranges.
+    // shard, queries ids[0, n) or r_base + [0, n)); the others have no candidates. Records
+    // (src/engine.cpp:161-185) and the per-stage tallies come straight from the pieces'
+    // arrays, in query order.
     Merged m;
     const uint32_t nq = static_cast<uint32_t>(nr);
     constexpr uint32_t kNone = 0xffffffffu;
-    std::vector<uint32_t> own_piece(nq, kNone), own_local(nq, 0);
     uint64_t total = 0, owned = 0;
-    for (uint32_t p = 0; p < pieces.size(); ++p) {
-        const Piece& pc = pieces[p];
+    for (const Piece& pc : pieces) {
         total += pc.res->n_cands;
         owned += pc.n;
-        for (uint32_t lr = 0; lr < pc.n; ++lr) {
-            const uint32_t r = pc.ids ? pc.ids[lr] : pc.r_base + lr;
-            own_piece[r] = p;
-            own_local[r] = lr;
+    }
+    // query -> (piece, local index); a single piece covering [0, nq) in order needs no table
+    const bool direct = pieces.size() == 1 && !pieces[0].ids && pieces[0].r_base == 0 && pieces[0].n == nq;
+    std::vector<uint32_t> own_piece, own_local;
+    if (!direct) {
+        own_piece.assign(nq, kNone);
+        own_local.assign(nq, 0);
+        for (uint32_t p = 0; p < pieces.size(); ++p) {
+            const Piece& pc = pieces[p];
+            for (uint32_t lr = 0; lr < pc.n; ++lr) {
+                const uint32_t r = pc.ids ? pc.ids[lr] : pc.r_base + lr;
+                own_piece[r] = p;
+                own_local[r] = lr;
+            }
         }
     }
-    CandidateSet& c = m.cands;
-    c.pairs.reserve(total);
-    c.intervals.reserve(total);
-    c.status.reserve(total);
-    c.decided_at.reserve(total);
-    c.r2op_offsets.assign(nq + 1, 0);
-    c.num_confirmed.assign(nq, 0);
-    for (uint32_t r = 0; r < nq; ++r) {
-        c.r2op_offsets[r] = c.pairs.size();
-        if (own_piece[r] == kNone) continue;
-        const tj_join_result& res = *pieces[own_piece[r]].res;
-        const uint32_t lr = own_local[r];
-        for (uint64_t op = res.r2op_offsets[lr]; op < res.r2op_offsets[lr + 1]; ++op) {
-            c.pairs.emplace_back(r, res.pair_s[op]);
-            c.intervals.push_back({res.lb[op], res.ub[op]});
-            c.status.push_back(static_cast<PairStatus>(res.status[op]));
-            c.decided_at.push_back(res.decided_at[op]);
-        }
-        c.num_confirmed[r] = res.num_confirmed[lr];
-    }
-    c.r2op_offsets[nq] = c.pairs.size();
     for (const Piece& pc : pieces) {
         const tj_join_result& res = *pc.res;
         m.vp_generated += res.vp_generated;
@@ -1390,36 +1438,42 @@ JoinOutput detail::run_join_cached(const PreparedDataset& R, const PreparedDatas
             ls.wall_ms = std::max(ls.wall_ms, res.level_ms[i]);
         }
     }
-
-    // Records (src/engine.cpp:161-185).
-    if (!knn) {
-        for (uint32_t op = 0; op < c.size(); ++op)
-            if (c.status[op] == PairStatus::Confirmed)
-                out.records.push_back(
-                    {c.pairs[op].first, c.pairs[op].second, c.intervals[op].lb, c.intervals[op].ub, c.decided_at[op], 0});
-    } else {
-        for (uint32_t r = 0; r < nq; ++r) {
-            std::vector<uint32_t> conf;
-            for (uint64_t op = c.r2op_offsets[r]; op < c.r2op_offsets[r + 1]; ++op)
-                if (c.status[op] == PairStatus::Confirmed) conf.push_back(static_cast<uint32_t>(op));
+    // per stage code (-3 .. 100): confirmed / removed tallies
+    std::vector<uint64_t> conf_at(104, 0), rem_at(104, 0);
+    std::vector<uint32_t> conf; // k-NN: one query's confirmed ops
+    for (uint32_t r = 0; r < nq; ++r) {
+        const uint32_t p = direct ? 0 : own_piece[r];
+        if (p == kNone) continue;
+        const tj_join_result& res = *pieces[p].res;
+        const uint32_t lr = direct ? r : own_local[r];
+        const uint64_t o0 = res.r2op_offsets[lr], o1 = res.r2op_offsets[lr + 1];
+        conf.clear();
+        for (uint64_t op = o0; op < o1; ++op) {
+            const uint8_t stt = res.status[op];
+            const int16_t at = res.decided_at[op];
+            if (stt == TJ_CONFIRMED) {
+                ++conf_at[at + 3];
+                if (!knn)
+                    out.records.push_back({r, res.pair_s[op], res.lb[op], res.ub[op], at, 0});
+                else
+                    conf.push_back(static_cast<uint32_t>(op));
+            } else if (stt == TJ_REMOVED) {
+                ++rem_at[at + 3];
+            }
+        }
+        if (knn && !conf.empty()) {
             std::sort(conf.begin(), conf.end(), [&](uint32_t a, uint32_t b) {
-                if (c.intervals[a].ub != c.intervals[b].ub) return c.intervals[a].ub < c.intervals[b].ub;
-                if (c.intervals[a].lb != c.intervals[b].lb) return c.intervals[a].lb < c.intervals[b].lb;
-                return c.pairs[a].second < c.pairs[b].second;
+                if (res.ub[a] != res.ub[b]) return res.ub[a] < res.ub[b];
+                if (res.lb[a] != res.lb[b]) return res.lb[a] < res.lb[b];
+                return res.pair_s[a] < res.pair_s[b];
             });
             uint32_t rank = 0;
             for (uint32_t op : conf)
-                out.records.push_back({r, c.pairs[op].second, c.intervals[op].lb, c.intervals[op].ub,
-                                       c.decided_at[op], ++rank});
+                out.records.push_back({r, res.pair_s[op], res.lb[op], res.ub[op], res.decided_at[op], ++rank});
         }
     }
 
     // Stage counters (src/engine.cpp:188-236).
-    std::map<int16_t, std::pair<uint64_t, uint64_t>> tally;
-    for (uint32_t op = 0; op < c.size(); ++op) {
-        if (c.status[op] == PairStatus::Confirmed) ++tally[c.decided_at[op]].first;
-        else if (c.status[op] == PairStatus::Removed) ++tally[c.decided_at[op]].second;
-    }
     struct Plan {
         int16_t code;
         double wall;
@@ -1440,8 +1494,10 @@ JoinOutput detail::run_join_cached(const PreparedDataset& R, const PreparedDatas
     const uint64_t all_pairs = owned * uint64_t{S.objects.size()};
     uint64_t flowing = all_pairs;
     for (const Plan& p : plan) {
-        auto [conf, rem] = tally.count(p.code) ? tally[p.code] : std::pair<uint64_t, uint64_t>{0, 0};
-        if (p.code == stage::kMbb) rem += all_pairs - c.size();
+        const bool in_range = p.code >= -3 && p.code <= 100;
+        const uint64_t conf = in_range ? conf_at[p.code + 3] : 0;
+        uint64_t rem = in_range ? rem_at[p.code + 3] : 0;
+        if (p.code == stage::kMbb) rem += all_pairs - total;
         StageCounters sc;
         sc.name = stage_name(p.code);
         sc.wall_ms = p.wall;

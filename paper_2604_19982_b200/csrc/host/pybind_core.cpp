@@ -185,7 +185,7 @@ public:
     // shard_count > 1: only the queries of shard shard_index (blocks of `block` queries dealt
     // round-robin) are packed and uploaded; S is uploaded whole.
     Resident(DatasetPtr R, DatasetPtr S, int device, unsigned workers, uint32_t shard_index, uint32_t shard_count,
-             uint32_t block)
+             uint32_t block, bool compact)
         : R_(std::move(R)), S_(std::move(S)) {
         py::gil_scoped_release release;
         ctx_ = detail::device_context(device);
@@ -199,10 +199,28 @@ public:
                 for (size_t r = b0; r < std::min(nr, b0 + block); ++r) ids.push_back(static_cast<uint32_t>(r));
         }
         n_queries_ = sharded ? ids.size() : R_->objects.size();
+        const bool two = sharded || S_.get() != R_.get();
+        if (compact) { // compact-resident (TJ_DATASET_COMPACT): the streamed form, kept in HBM
+            auto upload = [&](const PreparedDataset& D, const std::vector<uint32_t>* sel, detail::DatasetHandle& h) {
+                auto hd = sel ? detail::pack_header(D, *sel, pool) : detail::pack_header(D, pool);
+                detail::check(tj_dataset_begin_ex(ctx_, &hd->view, hd->vb_ptrs.data(), hd->fb_ptrs.data(),
+                                                  TJ_DATASET_COMPACT, &h.p),
+                              ctx_);
+                for (size_t li = 0; li < D.lod_schedule.size(); ++li) {
+                    auto lv = detail::pack_level(D, *hd, li, pool);
+                    detail::check(tj_dataset_put_level(h.p, static_cast<uint32_t>(li), &lv->view), ctx_);
+                    detail::check(tj_dataset_sync(h.p), ctx_); // lv's pinned buffers are reused next
+                }
+                bytes_ += tj_dataset_device_bytes(h.p);
+            };
+            upload(*R_, sharded ? &ids : nullptr, dr_);
+            if (two) upload(*S_, nullptr, ds_);
+            return;
+        }
         auto pr = detail::pack_dataset(*R_, pool, sharded ? &ids : nullptr);
         detail::check(tj_dataset_upload(ctx_, &pr->view, &dr_.p), ctx_);
         bytes_ = pr->bytes();
-        if (sharded || S_.get() != R_.get()) {
+        if (two) {
             auto ps = detail::pack_dataset(*S_, pool);
             detail::check(tj_dataset_upload(ctx_, &ps->view, &ds_.p), ctx_);
             bytes_ += ps->bytes();
@@ -356,6 +374,17 @@ PYBIND11_MODULE(_core, m) {
     py::class_<PreparedDataset, std::shared_ptr<PreparedDataset>>(m, "Dataset")
         .def_property_readonly("n_objects", [](const PreparedDataset& d) { return d.objects.size(); })
         .def_property_readonly("lod_schedule", [](const PreparedDataset& d) { return d.lod_schedule; })
+        .def("mbbs",
+             [](const PreparedDataset& d) {
+                 py::array_t<double> a(std::vector<py::ssize_t>{static_cast<py::ssize_t>(d.objects.size()), 6});
+                 double* w = a.mutable_data();
+                 for (size_t o = 0; o < d.objects.size(); ++o) {
+                     const Aabb& b = d.objects[o].mbb;
+                     const double v[6] = {b.min.x, b.min.y, b.min.z, b.max.x, b.max.y, b.max.z};
+                     std::memcpy(w + 6 * o, v, sizeof(v));
+                 }
+                 return a;
+             })
         .def("facet_count", [](const PreparedDataset& d, size_t level_index) {
             uint64_t n = 0;
             for (const auto& o : d.objects) n += o.ladder.levels.at(level_index).mesh.facets.size();
@@ -432,11 +461,12 @@ PYBIND11_MODULE(_core, m) {
 
     py::class_<Resident>(m, "Resident")
         .def(py::init([](std::shared_ptr<PreparedDataset> R, std::shared_ptr<PreparedDataset> S, int device,
-                         unsigned workers, uint32_t shard_index, uint32_t shard_count, uint32_t block) {
-                 return new Resident(R, S ? S : R, device, workers, shard_index, shard_count, block);
+                         unsigned workers, uint32_t shard_index, uint32_t shard_count, uint32_t block, bool compact) {
+                 return new Resident(R, S ? S : R, device, workers, shard_index, shard_count, block, compact);
              }),
              py::arg("R"), py::arg("S") = nullptr, py::arg("device") = 0, py::arg("workers") = 0,
-             py::arg("shard_index") = 0u, py::arg("shard_count") = 1u, py::arg("block") = 1024u)
+             py::arg("shard_index") = 0u, py::arg("shard_count") = 1u, py::arg("block") = 1024u,
+             py::arg("compact") = false)
         .def_property_readonly("device_bytes", &Resident::device_bytes)
         .def_property_readonly("n_queries", &Resident::n_queries)
         .def("run", &Resident::run, py::arg("type") = "within", py::arg("tau") = 0.0, py::arg("k") = 1,
@@ -455,6 +485,22 @@ PYBIND11_MODULE(_core, m) {
             return replicate_index(*tmpl, out_path, ids, sh);
         },
         py::arg("template"), py::arg("out_path"), py::arg("template_ids"), py::arg("shifts"));
+
+    m.def(
+        "replicate_dataset",
+        [](std::shared_ptr<PreparedDataset> tmpl, py::array_t<uint32_t, py::array::c_style | py::array::forcecast> ids,
+           py::array_t<double, py::array::c_style | py::array::forcecast> shifts, unsigned workers) {
+            if (shifts.ndim() != 2 || shifts.shape(1) != 3 || ids.ndim() != 1 || shifts.shape(0) != ids.shape(0))
+                throw std::invalid_argument("replicate_dataset: ids (n,) and shifts (n, 3) expected");
+            const size_t n = ids.shape(0);
+            std::span<const uint32_t> id_span(ids.data(), n);
+            std::span<const Point3> sh(reinterpret_cast<const Point3*>(shifts.data()), n);
+            py::gil_scoped_release release;
+            ThreadPool pool(workers);
+            return std::make_shared<PreparedDataset>(replicate_dataset(*tmpl, id_span, sh, pool));
+        },
+        py::arg("template"), py::arg("template_ids"), py::arg("shifts"), py::arg("workers") = 0u,
+        "In-memory translated copies of template objects (the benchmark inputs without index files).");
 
     m.def(
         "tri_tri_distance",

@@ -25,6 +25,44 @@ void shift_point(Point3& p, const Point3& s) {
 
 } // namespace
 
+PreparedObject replicated_object(const PreparedObject& src, const Point3& s, uint32_t id) {
+    PreparedObject obj = src;
+    obj.id = id;
+    shift_point(obj.mbb.min, s);
+    shift_point(obj.mbb.max, s);
+    shift_point(obj.anchor, s);
+    const double mag = std::max({std::fabs(obj.mbb.min.x), std::fabs(obj.mbb.min.y), std::fabs(obj.mbb.min.z),
+                                 std::fabs(obj.mbb.max.x), std::fabs(obj.mbb.max.y), std::fabs(obj.mbb.max.z)});
+    const double pad = std::ldexp(mag, -50); // ~4.4 ulp of the largest coordinate
+    for (LodMesh& lod : obj.ladder.levels) {
+        for (Point3& v : lod.mesh.vertices) shift_point(v, s);
+        for (double& h : lod.hd)
+            if (h != 0.0) h += pad;
+        for (double& h : lod.ph)
+            if (h != 0.0) h += pad;
+    }
+    for (Aabb& b : obj.voxels.boxes) {
+        shift_point(b.min, s);
+        shift_point(b.max, s);
+    }
+    for (Point3& a : obj.voxels.anchors) shift_point(a, s);
+    return obj;
+}
+
+PreparedDataset replicate_dataset(const PreparedDataset& tmpl, std::span<const uint32_t> template_ids,
+                                  std::span<const Point3> shifts, ThreadPool& pool) {
+    if (template_ids.size() != shifts.size()) throw std::invalid_argument("replicate_dataset: size mismatch");
+    for (uint32_t t : template_ids)
+        if (t >= tmpl.objects.size()) throw std::invalid_argument("replicate_dataset: template id out of range");
+    PreparedDataset out;
+    out.lod_schedule = tmpl.lod_schedule;
+    out.objects.resize(template_ids.size());
+    pool.parallel_jobs(template_ids.size(), [&](size_t i) {
+        out.objects[i] = replicated_object(tmpl.objects[template_ids[i]], shifts[i], static_cast<uint32_t>(i));
+    });
+    return out;
+}
+
 uint64_t replicate_index(const PreparedDataset& tmpl, const std::string& out_path,
                          std::span<const uint32_t> template_ids, std::span<const Point3> shifts) {
     if (template_ids.size() != shifts.size()) throw std::invalid_argument("replicate_index: size mismatch");
@@ -41,27 +79,7 @@ uint64_t replicate_index(const PreparedDataset& tmpl, const std::string& out_pat
     uint64_t bytes = std::fwrite(head.data(), 1, head.size(), f);
     std::string body;
     for (size_t i = 0; i < template_ids.size(); ++i) {
-        PreparedObject obj = tmpl.objects[template_ids[i]];
-        const Point3 s = shifts[i];
-        obj.id = static_cast<uint32_t>(i);
-        shift_point(obj.mbb.min, s);
-        shift_point(obj.mbb.max, s);
-        shift_point(obj.anchor, s);
-        const double mag = std::max({std::fabs(obj.mbb.min.x), std::fabs(obj.mbb.min.y), std::fabs(obj.mbb.min.z),
-                                     std::fabs(obj.mbb.max.x), std::fabs(obj.mbb.max.y), std::fabs(obj.mbb.max.z)});
-        const double pad = std::ldexp(mag, -50); // ~4.4 ulp of the largest coordinate
-        for (LodMesh& lod : obj.ladder.levels) {
-            for (Point3& v : lod.mesh.vertices) shift_point(v, s);
-            for (double& h : lod.hd)
-                if (h != 0.0) h += pad;
-            for (double& h : lod.ph)
-                if (h != 0.0) h += pad;
-        }
-        for (Aabb& b : obj.voxels.boxes) {
-            shift_point(b.min, s);
-            shift_point(b.max, s);
-        }
-        for (Point3& a : obj.voxels.anchors) shift_point(a, s);
+        const PreparedObject obj = replicated_object(tmpl.objects[template_ids[i]], shifts[i], static_cast<uint32_t>(i));
         body.clear();
         serialize_object(obj, body);
         const uint64_t len = body.size();

@@ -572,7 +572,7 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks) k_screen(Refine
         double tub = bits_to_double(__ldcg(op_ub_bits + d.op));
         tub = tub < d.iv_ub ? tub : d.iv_ub;
         Thresh th{ru(tlb), ru(tub), tlb <= d.iv_lb};
-        if (cull == 2) {
+        if (cull == 2 && !exact_op(src.exact_mask, d.op)) {
             constexpr float kTiny = 1e-30f;
             th.lb_sat = tlb == 0.0;
             th.lb_u = th.lb_sat ? 0.f : kTiny;
@@ -837,7 +837,7 @@ __global__ void __launch_bounds__(128) k_eval(RefineSource src, RefineQueue q, u
     for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < n;
          k += (unsigned long long)gridDim.x * blockDim.x) {
         const PairRef p = q.items[k];
-        if (cull == 2 && bits_to_double(__ldcg(lb_bits + p.op)) == 0.0 &&
+        if (cull == 2 && !exact_op(src.exact_mask, p.op) && bits_to_double(__ldcg(lb_bits + p.op)) == 0.0 &&
             (ub_settled || bits_to_double(__ldcg(ub_bits + p.op)) == 0.0))
             continue;
         double c[12];

@@ -53,7 +53,7 @@ __global__ void k_facet_pairs(const ActiveVpDev* __restrict__ act, uint64_t n, c
 
 __global__ void k_aggregate(CandDev c, uint64_t n, const unsigned long long* __restrict__ lbb,
                             const unsigned long long* __restrict__ ubb, int prune, double tau, int16_t stage,
-                            int decision, uint8_t* __restrict__ updated, DevError* err) {
+                            int decision, uint32_t exact_mask, uint8_t* __restrict__ updated, DevError* err) {
     for (uint64_t op = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; op < n; op += (uint64_t)gridDim.x * blockDim.x) {
         if (updated) updated[op] = 0;
         if (c.status[op] != TJ_UNDECIDED) continue;
@@ -64,7 +64,8 @@ __global__ void k_aggregate(CandDev c, uint64_t n, const unsigned long long* __r
         ub = (mub < ub) ? mub : ub;
         // decision mode: a positive mlb is only known to be positive (pairs that could lower
         // it were skipped); clamping it to ub keeps "lb > 0" and never trips the crossing check
-        const double mlb_d = (decision && mlb > 0.0 && ub < mlb) ? ub : mlb;
+        // (except the sampled ops that keep exact intervals: their crossing check is the reference's)
+        const double mlb_d = (decision && !exact_op(exact_mask, (uint32_t)op) && mlb > 0.0 && ub < mlb) ? ub : mlb;
         lb = (lb < mlb_d) ? mlb_d : lb;
         if (lb > ub) {
             if (lb - ub > 1e-9) {
@@ -118,7 +119,151 @@ void check_error(DevError* err, cudaStream_t st) {
     throw Error(TJ_EENGINE, "bound crossing: lb " + std::to_string(h.lb) + " > ub " + std::to_string(h.ub));
 }
 
+// ---- on-demand expansion of compact-resident levels (TJ_DATASET_COMPACT) ----
+
+__global__ void k_mark_voxels(const ActiveVpDev* __restrict__ act, uint64_t b, uint64_t e, uint8_t* __restrict__ fr,
+                              uint8_t* __restrict__ fs) {
+    for (uint64_t i = b + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < e; i += (uint64_t)gridDim.x * blockDim.x) {
+        const ActiveVpDev a = act[i];
+        if (fr) fr[a.gvr] = 1;
+        if (fs) fs[a.gvs] = 1;
+    }
+}
+
+__global__ void k_flag_counts(const uint8_t* __restrict__ flag, const uint64_t* __restrict__ foff, uint64_t nv,
+                              uint64_t* __restrict__ cnt) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nv; v += (uint64_t)gridDim.x * blockDim.x)
+        cnt[v] = flag[v] ? foff[v + 1] - foff[v] : 0;
+}
+
+// Records needed to expand the voxels flagged in m (m.flag set by k_mark_voxels): m.off, m.total.
+void mat_count(Workspace& ws, const DatasetDev& D, int slot, LevelMat& m, cudaStream_t st) {
+    const uint64_t nv = D.n_voxels;
+    m.cnt.reserve(std::max<uint64_t>(nv, 1));
+    m.off.reserve(nv + 1);
+    TJ_CUDA(cudaMemsetAsync(m.off.p, 0, 8, st));
+    m.total = 0;
+    if (!nv) return;
+    count_launch();
+    k_flag_counts<<<grid_for(nv, 256, ws.num_sms), 256, 0, st>>>(m.flag.p, D.facet_offsets[slot].p, nv, m.cnt.p);
+    size_t bytes = 0;
+    TJ_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, m.cnt.p, m.off.p + 1, (int64_t)nv, st));
+    ws.temp.reserve(bytes);
+    TJ_CUDA(cub::DeviceScan::InclusiveSum(ws.temp.p, bytes, m.cnt.p, m.off.p + 1, (int64_t)nv, st));
+    TJ_CUDA(cudaMemcpyAsync(&m.total, m.off.p + nv, 8, cudaMemcpyDeviceToHost, st));
+    stream_sync(st);
+}
+
+// Expands the counted voxels and derives their screening records / segment aggregates.
+void mat_expand(Workspace& ws, const DatasetDev& D, int slot, LevelMat& m, int zero_pad, cudaStream_t st) {
+    const uint64_t n = m.total;
+    m.facets.reserve(std::max<uint64_t>(n, 1) * TJ_FACET_STRIDE);
+    m.screen.reserve(std::max<uint64_t>(n * kScreenRecF4, 1));
+    m.seg.reserve(std::max<uint64_t>(3 * D.n_voxels, 1));
+    m.agg.reserve(3);
+    const unsigned init[3] = {0x7f800000u, 0u, 0u};
+    TJ_CUDA(cudaMemcpyAsync(m.agg.p, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    expand_compact_level(D, (uint32_t)slot, m.off.p, m.facets.p, ws.num_sms, st);
+    refine_prep(m.facets.p, n, m.screen.p, m.agg.p, ws.num_sms, st, zero_pad);
+    refine_seg_prep(m.screen.p, m.off.p, D.n_voxels, m.seg.p, ws.num_sms, st);
+    stream_sync(st); // the init above is a pageable-host copy
+}
+
+// Working-set budget for materialized levels: $TRIJOIN_WORKSET_MB, else 70 % of the device
+// memory free when first needed (per context).
+uint64_t workset_budget(Workspace& ws) {
+    if (const char* e = std::getenv("TRIJOIN_WORKSET_MB"); e && *e)
+        return std::max<uint64_t>(1, uint64_t(std::stod(e) * 1048576.0));
+    if (ws.workset_budget) return ws.workset_budget;
+    size_t free_b = 0, total_b = 0;
+    TJ_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    return ws.workset_budget = std::max<uint64_t>(free_b / 10 * 7, 64ull << 20);
+}
+
+// Bytes a materialized record costs (FP64 record + FP32 screening record).
+constexpr uint64_t kMatBytes = TJ_FACET_STRIDE * 8 + kScreenRecF4 * 16;
+
+// The level arrays one side of a refinement pass reads: resident (expanded at upload) or
+// materialized for the chunk of active voxel pairs [b, e).
+struct SideLevel {
+    const uint64_t* foff;
+    const double* facets;
+    const float4* box;
+    const float4* geo;
+    const float4* seg;
+    const unsigned* agg;
+};
+
+SideLevel resident_side(const DatasetDev& D, int slot) {
+    const uint64_t n = D.level_entries[slot];
+    return {D.facet_offsets[slot].p, D.facets[slot].p, D.screen[slot].p, D.screen[slot].p + 3 * n, D.seg[slot].p,
+            D.agg.p + 3 * slot};
+}
+
+SideLevel mat_side(const LevelMat& m) {
+    return {m.off.p, m.facets.p, m.screen.p, m.screen.p + 3 * m.total, m.seg.p, m.agg.p};
+}
+
+// Splits the active voxel pairs [b, e) into chunks whose materialized records fit the
+// working-set budget, materializing each in turn: fn(chunk begin, chunk end, R side, S side).
+// Resident (non-compact) sides are used as they are.
+template <class F>
+void for_mat_chunks(Workspace& ws, const DatasetDev& R, int sr, const DatasetDev& S, int ss,
+                    const ActiveVpDev* active, uint64_t b, uint64_t e, int zero_pad, cudaStream_t st, F&& fn) {
+    const bool same = &R == &S;
+    std::vector<std::pair<uint64_t, uint64_t>> todo{{b, e}};
+    const uint64_t budget = workset_budget(ws);
+    while (!todo.empty()) {
+        const auto [cb, ce] = todo.back();
+        todo.pop_back();
+        if (ce <= cb) continue;
+        LevelMat& mr = ws.mat[0];
+        LevelMat& ms = same ? ws.mat[0] : ws.mat[1];
+        if (R.compact) {
+            mr.flag.reserve(std::max<uint64_t>(R.n_voxels, 1));
+            TJ_CUDA(cudaMemsetAsync(mr.flag.p, 0, std::max<uint64_t>(R.n_voxels, 1), st));
+        }
+        if (S.compact && !same) {
+            ms.flag.reserve(std::max<uint64_t>(S.n_voxels, 1));
+            TJ_CUDA(cudaMemsetAsync(ms.flag.p, 0, std::max<uint64_t>(S.n_voxels, 1), st));
+        }
+        count_launch();
+        k_mark_voxels<<<grid_for(ce - cb, 256, ws.num_sms), 256, 0, st>>>(active, cb, ce, R.compact ? mr.flag.p : nullptr,
+                                                                          S.compact ? ms.flag.p : nullptr);
+        TJ_CUDA(cudaGetLastError());
+        uint64_t need = 0;
+        if (R.compact) {
+            mat_count(ws, R, sr, mr, st);
+            need += mr.total;
+        }
+        if (S.compact && !same) {
+            mat_count(ws, S, ss, ms, st);
+            need += ms.total;
+        }
+        if (need * kMatBytes > budget && ce - cb > 1) { // too large: halves, first half first
+            const uint64_t mid = cb + (ce - cb) / 2;
+            todo.emplace_back(mid, ce);
+            todo.emplace_back(cb, mid);
+            continue;
+        }
+        if (R.compact) mat_expand(ws, R, sr, mr, zero_pad, st);
+        if (S.compact && !same) mat_expand(ws, S, ss, ms, zero_pad, st);
+        const SideLevel rs = R.compact ? mat_side(mr) : resident_side(R, sr);
+        const SideLevel ss_ = S.compact ? mat_side(ms) : resident_side(S, ss);
+        fn(cb, ce, rs, ss_);
+    }
+}
+
 } // namespace
+
+uint32_t tripwire_mask() {
+    const char* e = std::getenv("TRIJOIN_TRIPWIRE_SAMPLE");
+    const long v = e && *e ? std::atol(e) : 1024;
+    if (v <= 0) return 0xffffffffu; // none
+    uint32_t p = 1;
+    while (p < (uint32_t)v && p < (1u << 30)) p <<= 1;
+    return p - 1;
+}
 
 uint64_t compact_active(Workspace& ws, const CandDevStore& cs, DevBuf<ActiveVpDev>& active, uint64_t n,
                         cudaStream_t st) {
@@ -176,29 +321,36 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
             if (&S != &R) ls.wait_ms += level_ready(S, ss, st);
             RefineSource src{};
             src.active = active.p;
-            src.r_foff = R.facet_offsets[sr].p;
-            src.s_foff = S.facet_offsets[ss].p;
+            src.exact_mask = decision ? tripwire_mask() : 0u;
             src.cand_lb = cs.lb.p;
             src.cand_ub = cs.ub.p;
-            src.r_facets = R.facets[sr].p;
-            src.s_facets = S.facets[ss].p;
-            {   // FP32 screening records, voxel segment aggregates and level aggregates of this
-                // level (derived once per dataset at upload: DatasetDev::screen / seg / agg)
+            ws.level_agg.reserve(8);
+            src.agg = ws.level_agg.p;
+            {
                 const uint64_t nr = R.level_entries[sr], ns = S.level_entries[ss];
-                ws.level_agg.reserve(8);
-                count_launch();
-                k_copy_agg<<<1, 32, 0, st>>>(R.agg.p + 3 * sr, S.agg.p + 3 * ss, ws.level_agg.p);
-                src.agg = ws.level_agg.p;
-                src.r_box = R.screen[sr].p;
-                src.r_geo = R.screen[sr].p + 3 * nr;
-                src.r_seg = R.seg[sr].p;
-                src.s_box = S.screen[ss].p;
-                src.s_geo = S.screen[ss].p + 3 * ns;
-                src.s_seg = S.seg[ss].p;
                 const double mr = R.n_voxels ? double(nr) / double(R.n_voxels) : 0.0;
                 const double ms = S.n_voxels ? double(ns) / double(S.n_voxels) : 0.0;
                 src.mean_seg = float(0.5 * (mr + ms));
             }
+            // the level arrays of both sides: FP32 screening records, voxel segment aggregates
+            // and level aggregates (derived once per dataset at upload: DatasetDev::screen / seg
+            // / agg), or for compact-resident datasets expanded here for the voxels in use
+            auto bind = [&](const SideLevel& rs, const SideLevel& ss_) {
+                src.r_foff = rs.foff;
+                src.s_foff = ss_.foff;
+                src.r_facets = rs.facets;
+                src.s_facets = ss_.facets;
+                src.r_box = rs.box;
+                src.r_geo = rs.geo;
+                src.r_seg = rs.seg;
+                src.s_box = ss_.box;
+                src.s_geo = ss_.geo;
+                src.s_seg = ss_.seg;
+                count_launch();
+                k_copy_agg<<<1, 32, 0, st>>>(rs.agg, ss_.agg, ws.level_agg.p);
+            };
+            const bool mat = R.compact || S.compact;
+            if (!mat) bind(resident_side(R, sr), resident_side(S, ss));
             // 0: every facet pair; 1: exact-preserving culling; 2: decision-mode culling
             const int cull = (spec.flags & TJ_FLAG_NO_CULL) ? 0 : decision ? 2 : 1;
             unsigned long long hc[kNumCounters];
@@ -218,14 +370,33 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
                 k_facet_pairs<<<grid_for(n_active, 256, ws.num_sms), 256, 0, st>>>(
                     active.p, n_active, R.facet_offsets[sr].p, S.facet_offsets[ss].p, counters.p + 2);
                 TJ_CUDA(cudaEventRecord(e0, st));
-                // seeds for every voxel pair first (op thresholds), then the screened passes
-                if (cull)
+                if (!mat) {
+                    // seeds for every voxel pair first (op thresholds), then the screened passes
+                    if (cull)
+                        for (uint64_t c0 = 0; c0 < n_active; c0 += launch)
+                            refine_pass(src, c0, std::min(n_active, c0 + launch), true, lbb.p, ubb.p, cull, queue,
+                                        work.p, counters.p, ws.num_sms, st);
                     for (uint64_t c0 = 0; c0 < n_active; c0 += launch)
-                        refine_pass(src, c0, std::min(n_active, c0 + launch), true, lbb.p, ubb.p, cull, queue, work.p,
-                                    counters.p, ws.num_sms, st);
-                for (uint64_t c0 = 0; c0 < n_active; c0 += launch)
-                    refine_pass(src, c0, std::min(n_active, c0 + launch), false, lbb.p, ubb.p, cull, queue, work.p,
-                                counters.p, ws.num_sms, st);
+                        refine_pass(src, c0, std::min(n_active, c0 + launch), false, lbb.p, ubb.p, cull, queue,
+                                    work.p, counters.p, ws.num_sms, st);
+                } else {
+                    // per materialized chunk: its seeds, then its screened pass (the op minima
+                    // only tighten; a chunk screened before another's seeds skips fewer pairs,
+                    // never a pair that matters)
+                    for_mat_chunks(ws, R, sr, S, ss, active.p, 0, n_active, 0, st,
+                                   [&](uint64_t cb, uint64_t ce, const SideLevel& rs, const SideLevel& ss_) {
+                                       bind(rs, ss_);
+                                       ++out.mat_chunks;
+                                       for (uint64_t c0 = cb; c0 < ce; c0 += launch) {
+                                           const uint64_t c1 = std::min(ce, c0 + launch);
+                                           if (cull)
+                                               refine_pass(src, c0, c1, true, lbb.p, ubb.p, cull, queue, work.p,
+                                                           counters.p, ws.num_sms, st);
+                                           refine_pass(src, c0, c1, false, lbb.p, ubb.p, cull, queue, work.p,
+                                                       counters.p, ws.num_sms, st);
+                                       }
+                                   });
+                }
                 TJ_CUDA(cudaEventRecord(e1, st));
                 unsigned long long ovf = 0;
                 TJ_CUDA(cudaMemcpyAsync(hc, counters.p, sizeof(hc), cudaMemcpyDeviceToHost, st));
@@ -244,7 +415,8 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
             if (dbg.n) refine_debug_op_tested(nullptr);
             count_launch();
             k_aggregate<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(cs.view(), n, lbb.p, ubb.p, knn ? 0 : 1, tau,
-                                                                      (int16_t)level, cull == 2 ? 1 : 0, updated.p,
+                                                                      (int16_t)level, cull == 2 ? 1 : 0,
+                                                                      src.exact_mask, updated.p,
                                                                       err);
             TJ_CUDA(cudaGetLastError());
             check_error(err, st);
@@ -379,51 +551,74 @@ void exact_recompute_dev(Workspace& ws, const DatasetDev& R, const DatasetDev& S
                                                               kInfBits);
     RefineSource src{};
     src.active = active.p;
-    src.r_foff = R.facet_offsets[sr].p;
-    src.s_foff = S.facet_offsets[ss].p;
     src.cand_lb = iv_lb.p;
     src.cand_ub = iv_ub.p;
-    src.r_facets = R.facets[sr].p;
-    src.s_facets = S.facets[ss].p;
     src.zero_pad = 1;
-    const uint64_t nr = R.level_entries[sr], ns = S.level_entries[ss];
-    ws.screen_r.reserve(std::max<uint64_t>(nr * kScreenRecF4, 1));
-    refine_prep(R.facets[sr].p, nr, ws.screen_r.p, nullptr, ws.num_sms, st, 1);
-    src.r_box = ws.screen_r.p;
-    src.r_geo = ws.screen_r.p + 3 * nr;
-    ws.seg_r.reserve(std::max<uint64_t>(3 * R.n_voxels, 1));
-    refine_seg_prep(src.r_box, R.facet_offsets[sr].p, R.n_voxels, ws.seg_r.p, ws.num_sms, st);
-    src.r_seg = ws.seg_r.p;
-    if (S.facets[ss].p == R.facets[sr].p) {
-        src.s_box = src.r_box;
-        src.s_geo = src.r_geo;
-        src.s_seg = src.r_seg;
-    } else {
-        ws.screen_s.reserve(std::max<uint64_t>(ns * kScreenRecF4, 1));
-        refine_prep(S.facets[ss].p, ns, ws.screen_s.p, nullptr, ws.num_sms, st, 1);
-        src.s_box = ws.screen_s.p;
-        src.s_geo = ws.screen_s.p + 3 * ns;
-        ws.seg_s.reserve(std::max<uint64_t>(3 * S.n_voxels, 1));
-        refine_seg_prep(src.s_box, S.facet_offsets[ss].p, S.n_voxels, ws.seg_s.p, ws.num_sms, st);
-        src.s_seg = ws.seg_s.p;
-    }
     if (!ws.queue) ws.queue = std::make_unique<RefineQueueStore>();
     RefineQueueStore& queue = *ws.queue;
     queue.cap = 0;
     if (const char* e = std::getenv("TRIJOIN_TEST_QUEUE_CAP"); e && *e) queue.cap = std::strtoull(e, nullptr, 10);
     const uint64_t launch = 1ull << 20;
+    auto passes = [&](uint64_t b, uint64_t e) {
+        for (uint64_t c0 = b; c0 < e; c0 += launch)
+            refine_pass(src, c0, std::min(e, c0 + launch), true, lbb.p, ubb.p, 1, queue, work.p, counters.p,
+                        ws.num_sms, st);
+        for (uint64_t c0 = b; c0 < e; c0 += launch)
+            refine_pass(src, c0, std::min(e, c0 + launch), false, lbb.p, ubb.p, 1, queue, work.p, counters.p,
+                        ws.num_sms, st);
+    };
+    const bool mat = R.compact || S.compact;
+    if (!mat) {
+        src.r_foff = R.facet_offsets[sr].p;
+        src.s_foff = S.facet_offsets[ss].p;
+        src.r_facets = R.facets[sr].p;
+        src.s_facets = S.facets[ss].p;
+        const uint64_t nr = R.level_entries[sr], ns = S.level_entries[ss];
+        ws.screen_r.reserve(std::max<uint64_t>(nr * kScreenRecF4, 1));
+        refine_prep(R.facets[sr].p, nr, ws.screen_r.p, nullptr, ws.num_sms, st, 1);
+        src.r_box = ws.screen_r.p;
+        src.r_geo = ws.screen_r.p + 3 * nr;
+        ws.seg_r.reserve(std::max<uint64_t>(3 * R.n_voxels, 1));
+        refine_seg_prep(src.r_box, R.facet_offsets[sr].p, R.n_voxels, ws.seg_r.p, ws.num_sms, st);
+        src.r_seg = ws.seg_r.p;
+        if (S.facets[ss].p == R.facets[sr].p) {
+            src.s_box = src.r_box;
+            src.s_geo = src.r_geo;
+            src.s_seg = src.r_seg;
+        } else {
+            ws.screen_s.reserve(std::max<uint64_t>(ns * kScreenRecF4, 1));
+            refine_prep(S.facets[ss].p, ns, ws.screen_s.p, nullptr, ws.num_sms, st, 1);
+            src.s_box = ws.screen_s.p;
+            src.s_geo = ws.screen_s.p + 3 * ns;
+            ws.seg_s.reserve(std::max<uint64_t>(3 * S.n_voxels, 1));
+            refine_seg_prep(src.s_box, S.facet_offsets[ss].p, S.n_voxels, ws.seg_s.p, ws.num_sms, st);
+            src.s_seg = ws.seg_s.p;
+        }
+    }
     for (;;) {
         count_launch();
         k_fill_u64<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(lbb.p, n, kInfBits);
         count_launch();
         k_fill_u64<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(ubb.p, n, kInfBits);
         TJ_CUDA(cudaMemsetAsync(queue.count.p, 0, 16, st));
-        for (uint64_t c0 = 0; c0 < total; c0 += launch)
-            refine_pass(src, c0, std::min(total, c0 + launch), true, lbb.p, ubb.p, 1, queue, work.p, counters.p,
-                        ws.num_sms, st);
-        for (uint64_t c0 = 0; c0 < total; c0 += launch)
-            refine_pass(src, c0, std::min(total, c0 + launch), false, lbb.p, ubb.p, 1, queue, work.p, counters.p,
-                        ws.num_sms, st);
+        if (!mat) {
+            passes(0, total);
+        } else { // compact-resident: expand the level-100 voxels of the confirmed pairs chunk by chunk
+            for_mat_chunks(ws, R, sr, S, ss, active.p, 0, total, 1, st,
+                           [&](uint64_t cb, uint64_t ce, const SideLevel& rs, const SideLevel& ss_) {
+                               src.r_foff = rs.foff;
+                               src.s_foff = ss_.foff;
+                               src.r_facets = rs.facets;
+                               src.s_facets = ss_.facets;
+                               src.r_box = rs.box;
+                               src.r_geo = rs.geo;
+                               src.r_seg = rs.seg;
+                               src.s_box = ss_.box;
+                               src.s_geo = ss_.geo;
+                               src.s_seg = ss_.seg;
+                               passes(cb, ce);
+                           });
+        }
         unsigned long long ovf = 0;
         TJ_CUDA(cudaMemcpyAsync(&ovf, queue.count.p + 1, 8, cudaMemcpyDeviceToHost, st));
         stream_sync(st);

@@ -115,7 +115,21 @@ struct DatasetDev {
     DevBuf<int> stream_err;                              // [1]: an index out of range
     DevBuf<unsigned char> stage;                         // compact-level staging area (largest level)
     std::shared_ptr<LevelGate> gate;
+    // Compact-resident datasets (tj_dataset_begin_ex, TJ_DATASET_COMPACT): every level stays in
+    // HBM in the shipped compact mesh form (~44 B per facet instead of the 96-B records plus
+    // 128-B screening records); a join expands, per level, only the voxels its active voxel
+    // pairs touch (materialize_level). facets / screen / seg are then unused.
+    bool compact = false;
+    std::vector<DevBuf<unsigned char>> cmp; // per level: compact mesh form (stage_layout)
+    std::vector<uint32_t> cmp_flags;        // per level: TJ_LEVEL_PADS / TJ_LEVEL_NARROW
 };
+
+// Expands level slot `slot` of a compact-resident dataset into facet records (TJ_FACET_STRIDE
+// doubles each): voxel v's facets go to out[act[v] ...] when act[v + 1] > act[v] (act: an
+// exclusive scan over the voxels of the active voxels' facet counts); ids out of range set
+// *d.stream_err (capi.cu).
+void expand_compact_level(const DatasetDev& d, uint32_t slot, const uint64_t* act, double* out, int num_sms,
+                          cudaStream_t st);
 
 // Derived screening data of level slot li of d (facets already resident), on stream st.
 void derive_level(DatasetDev& d, uint32_t li, int num_sms, cudaStream_t st);
@@ -163,7 +177,17 @@ struct RefineSource {
     int zero_pad;
     // mean facets per voxel of the level (R and S; 0 = unknown): sizes k_screen's work grabs
     float mean_seg;
+    // decision mode: ops with (op & exact_mask) == 0 keep exact intervals (the reference's
+    // bound-crossing tripwire is evaluated on them); 0xffffffff = none
+    uint32_t exact_mask;
 };
+
+// Decision-mode op sample with exact intervals: $TRIJOIN_TRIPWIRE_SAMPLE = every N-th op
+// (N a power of two, default 1024; 0 = none, 1 = every op). Returns the mask for op & mask == 0.
+uint32_t tripwire_mask();
+__host__ __device__ __forceinline__ bool exact_op(uint32_t mask, uint32_t op) {
+    return mask != 0xffffffffu && (op & mask) == 0;
+}
 
 // A queued facet pair: op and the two global facet record indices.
 struct PairRef {

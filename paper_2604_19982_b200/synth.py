@@ -200,3 +200,117 @@ def _dataset_extent(path):
         hi = np.maximum(hi, mbb[3:])
         pos += 8 + blen
     return np.concatenate([lo, hi])
+
+
+# ---- in-memory inputs (configs whose index files would not fit a disk: D, E) ----
+
+_TEMPLATES = {}
+
+
+def _template_cached(name):
+    if name not in _TEMPLATES:
+        _TEMPLATES[name] = _template(name)
+    return _TEMPLATES[name]
+
+
+def _plan(spec, scale, other_extent):
+    tname, count, placement = spec
+    count = max(1, int(round(count * scale)))
+    centres = _template_centres(os.path.join(BENCHDATA, tname + ".idx"))
+    targets = _placement(placement, count, float(np.cbrt(scale)), other_extent)
+    ids = (np.arange(count) % len(centres)).astype(np.uint32)
+    return {"template": tname, "ids": ids, "shifts": np.ascontiguousarray(targets - centres[ids])}
+
+
+def _template_mbbs(name):
+    """Per template object MBB (min.xyz, max.xyz) from the 3DPJ1 file."""
+    import struct
+    with open(os.path.join(BENCHDATA, name + ".idx"), "rb") as f:
+        data = f.read()
+    pos = 5 + 4
+    (nl,) = struct.unpack_from("<I", data, pos)
+    pos += 4 + 4 * nl
+    (n,) = struct.unpack_from("<Q", data, pos)
+    pos += 8
+    out = []
+    for _ in range(n):
+        (blen,) = struct.unpack_from("<Q", data, pos)
+        out.append(struct.unpack_from("<6d", data, pos + 8 + 4))
+        pos += 8 + blen
+    return np.asarray(out)
+
+
+def plan_mbbs(plan):
+    """MBBs of a plan's objects: the template MBB translated exactly as replicate_* does
+    (x -> fl(x + shift) per coordinate)."""
+    t = _template_mbbs(plan["template"])[plan["ids"]]
+    sh = np.concatenate([plan["shifts"], plan["shifts"]], axis=1)
+    return t + sh
+
+
+def plans_for(name, scale=1.0):
+    """{R, S} plans (template name, ids, shifts) of configuration `name`; S is R for a
+    self-join. The same objects build_config writes."""
+    rspec, sspec, _ = CONFIGS[name]
+    if sspec is None:
+        p = _plan(rspec, scale, None)
+        return {"R": p, "S": p, "self": True}
+    ps = _plan(sspec, scale, None)
+    m = plan_mbbs(ps)
+    ext = np.concatenate([m[:, :3].min(axis=0), m[:, 3:].max(axis=0)])
+    return {"R": _plan(rspec, scale, ext), "S": ps, "self": False}
+
+
+def build_datasets(name, scale=1.0, workers=0):
+    """In-memory (R, S, plans) of configuration `name`: the same objects build_config writes,
+    replicated straight into memory (_core.replicate_dataset, no index files)."""
+    from . import _core
+    plans = plans_for(name, scale)
+    pr, ps = plans["R"], plans["S"]
+    R = _core.replicate_dataset(_template_cached(pr["template"]), pr["ids"], pr["shifts"], workers)
+    S = R if plans["self"] else _core.replicate_dataset(_template_cached(ps["template"]), ps["ids"], ps["shifts"],
+                                                         workers)
+    return R, S, plans
+
+
+def near_subset(q_mbbs, s_mbbs, tau):
+    """Ascending ids of the S objects whose MBB is within tau of some query MBB on every axis
+    (a superset of the reference's MBB candidates: mindist <= tau implies every axis gap <= tau)."""
+    order = np.argsort(s_mbbs[:, 0], kind="stable")
+    smin = s_mbbs[order, 0]
+    ext = float(np.max(s_mbbs[:, 3] - s_mbbs[:, 0])) if len(s_mbbs) else 0.0
+    keep = np.zeros(len(s_mbbs), dtype=bool)
+    for q in q_mbbs:
+        lo = np.searchsorted(smin, q[0] - tau - ext, side="left")
+        hi = np.searchsorted(smin, q[3] + tau, side="right")
+        cand = order[lo:hi]
+        c = s_mbbs[cand]
+        ok = np.ones(len(cand), dtype=bool)
+        for d in range(3):
+            gap = np.maximum(c[:, d] - q[3 + d], q[d] - c[:, 3 + d])
+            ok &= gap <= tau
+        keep[cand[ok]] = True
+    return np.nonzero(keep)[0].astype(np.uint32)
+
+
+def write_slice_files(name, scale, stride, out_dir):
+    """Index files for the CPU reference on a deterministic R-slice (every stride-th query) of a
+    within-tau configuration, against only the S objects near the slice (near_subset): each
+    query's candidates, hence its records, are unchanged (per-query independence),
+    and no full-size S file is written. Returns (r_path, s_path, r_ids, s_ids): record (r', s')
+    of the slice files is (r_ids[r'], s_ids[s']) of the full join."""
+    from . import _core
+    plans = plans_for(name, scale)
+    tau = float(CONFIGS[name][2].get("tau", 0.0))
+    os.makedirs(out_dir, exist_ok=True)
+    pr, ps = plans["R"], plans["S"]
+    r_ids = np.arange(0, len(pr["ids"]), stride, dtype=np.uint32)
+    s_ids = near_subset(plan_mbbs(pr)[r_ids], plan_mbbs(ps), tau)
+    key = hashlib.sha1(json.dumps([name, scale, stride]).encode()).hexdigest()[:12]
+    r_path = os.path.join(out_dir, f"{name}_{key}_sliceR.idx")
+    s_path = os.path.join(out_dir, f"{name}_{key}_sliceS.idx")
+    _core.replicate_index(_template_cached(pr["template"]), r_path, pr["ids"][r_ids].tolist(),
+                          pr["shifts"][r_ids].tolist())
+    _core.replicate_index(_template_cached(ps["template"]), s_path, ps["ids"][s_ids].tolist(),
+                          ps["shifts"][s_ids].tolist())
+    return r_path, s_path, r_ids, s_ids

@@ -64,8 +64,10 @@ def test_chunk_and_cull_invariance(capi, refine_chunk):
 OUT_OF_CORE = [j for j in JOINS if j["r"] in ("nuclei60", "mini18_s21", "mini10_s77", "spheres80a")]
 
 
-@pytest.mark.parametrize("env", [{"TRIJOIN_R_CHUNK_OBJECTS": "7"}, {"TRIJOIN_DEVICE_BUDGET_MB": "70"}],
-                         ids=["chunk7", "budget70MB"])
+@pytest.mark.parametrize("env", [{"TRIJOIN_R_CHUNK_OBJECTS": "7"},
+                                 {"TRIJOIN_DEVICE_BUDGET_MB": "70", "TRIJOIN_COMPACT": "0"},
+                                 {"TRIJOIN_DEVICE_BUDGET_MB": "66"}],
+                         ids=["chunk7", "budget70MB_expanded", "budget66MB_auto"])
 @pytest.mark.parametrize("j", OUT_OF_CORE, ids=tjtest.join_id)
 def test_out_of_core_r_chunks(monkeypatch, env, j):
     """R joined in consecutive object chunks against a resident S (device-memory budget,
@@ -78,8 +80,9 @@ def test_out_of_core_r_chunks(monkeypatch, env, j):
     assert out["records"] == j["records"]
     stages = [{k: v for k, v in st.items() if k != "wall_ms"} for st in out["stats"]["stages"]]
     assert stages == j["stages"]
-    if j["r"] == "nuclei60":
-        assert out["stats"]["b200"]["r_chunks"] > 1
+    b = out["stats"]["b200"]
+    if j["r"] == "nuclei60":  # chunked, unless compact residency made it fit
+        assert b["r_chunks"] > 1 or (b["residency"] == "compact" and "TRIJOIN_COMPACT" not in env)
 
 
 @pytest.mark.parametrize("j", [j for j in JOINS if j["r"] in ("nuclei60", "spheres80a")], ids=tjtest.join_id)
@@ -116,6 +119,32 @@ def test_intersect_decision_mode(capi, idx):
         for key in ("lb", "ub"):
             assert (tjtest.bits(dec[key][conf]) == tjtest.bits(base[key][conf])).all()
             assert (tjtest.bits(exact[key]) == tjtest.bits(base[key])).all()
+    finally:
+        capi.free(R)
+
+
+@pytest.mark.parametrize("idx", ["mini10_s61.idx", "mini18_s21.idx", "spheres80a.idx"])
+def test_decision_mode_tripwire_sample(capi, monkeypatch, idx):
+    """Decision mode keeps exact intervals on a sample of ops ($TRIJOIN_TRIPWIRE_SAMPLE, every
+    N-th op; default 1024), so the reference's bound-crossing tripwire (src/filter.cpp:22-32)
+    is evaluated on them. With N = 1 every op's interval equals the exact-interval run."""
+    R = capi.load(golden(idx))
+    try:
+        lods = (20, 60, 100)
+        exact = capi.join(R, R, type="intersect", lods=lods, flags=4)
+        monkeypatch.setenv("TRIJOIN_TRIPWIRE_SAMPLE", "1")
+        dec = capi.join(R, R, type="intersect", lods=lods)
+        assert dec["decision_mode"] == 1
+        for key in ("pair_r", "pair_s", "status", "decided_at"):
+            assert (dec[key] == exact[key]).all()
+        assert (tjtest.bits(dec["lb"]) == tjtest.bits(exact["lb"])).all()
+        assert (tjtest.bits(dec["ub"]) == tjtest.bits(exact["ub"])).all()
+        monkeypatch.setenv("TRIJOIN_TRIPWIRE_SAMPLE", "4")  # every 4th op exact, the rest decision
+        part = capi.join(R, R, type="intersect", lods=lods)
+        every4 = (np.arange(len(part["lb"])) % 4) == 0
+        assert (tjtest.bits(part["lb"][every4]) == tjtest.bits(exact["lb"][every4])).all()
+        for key in ("pair_r", "pair_s", "status", "decided_at"):
+            assert (part[key] == exact[key]).all()
     finally:
         capi.free(R)
 

@@ -76,7 +76,7 @@ class JoinResult(ctypes.Structure):
                 ("level_vps_skipped", ctypes.c_uint64 * MAXL),
                 ("level_facets_dropped", ctypes.c_uint64 * MAXL),
                 ("level_wait_ms", ctypes.c_double * MAXL), ("decision_mode", ctypes.c_int32),
-                ("queue_reruns", ctypes.c_uint32)]
+                ("queue_reruns", ctypes.c_uint32), ("mat_chunks", ctypes.c_uint64)]
 
 
 def capi_functions():
@@ -212,6 +212,7 @@ class Capi:
             "levels": [(res.level[i], res.level_vps[i], res.level_facet_pairs[i]) for i in range(res.n_levels_run)],
             "decision_mode": res.decision_mode,
             "queue_reruns": res.queue_reruns,
+            "mat_chunks": res.mat_chunks,
         }
         self.lib.tj_join_result_free(ctypes.byref(res))
         return out

@@ -868,15 +868,11 @@ int tj_refine_batch(tj_ctx* ctx, uint64_t n_tris, const double* tris, const doub
             TJ_CUDA(cudaMemcpyAsync(lbb.p, inf.data(), n_descs * 8, cudaMemcpyHostToDevice, st));
             TJ_CUDA(cudaMemcpyAsync(ubb.p, inf.data(), n_descs * 8, cudaMemcpyHostToDevice, st));
             TJ_CUDA(cudaMemsetAsync(counters.p, 0, kNumCounters * 8, st));
-            TJ_CUDA(cudaMemsetAsync(queue.count.p, 0, 16, st));
+            queue.reset(st);
             if (cull)
                 refine_pass(src, 0, n_descs, true, lbb.p, ubb.p, cull, queue, work.p, counters.p, ctx->ws.num_sms, st);
             refine_pass(src, 0, n_descs, false, lbb.p, ubb.p, cull, queue, work.p, counters.p, ctx->ws.num_sms, st);
-            unsigned long long ovf = 0;
-            TJ_CUDA(cudaMemcpyAsync(&ovf, queue.count.p + 1, 8, cudaMemcpyDeviceToHost, st));
-            stream_sync(st);
-            if (ovf == 0) break;
-            queue.items.alloc(ovf + ovf / 4);
+            if (!queue.grow_if_overflowed(st)) break;
         }
         TJ_CUDA(cudaMemcpyAsync(vp_lb, lbb.p, n_descs * 8, cudaMemcpyDeviceToHost, st));
         TJ_CUDA(cudaMemcpyAsync(vp_ub, ubb.p, n_descs * 8, cudaMemcpyDeviceToHost, st));

@@ -116,6 +116,15 @@ struct PinnedArena {
     }
     void release(double* p, size_t cap, bool pinned) {
         if (!p) return;
+        // blocks of 1 GiB and more go back to the OS (a dataset's level on the D / E scale:
+        // keeping them would pin tens of GB beside the caller's datasets)
+        if (cap * sizeof(double) >= (size_t(1) << 30)) {
+            if (pinned)
+                cudaFreeHost(p);
+            else
+                std::free(p);
+            return;
+        }
         std::lock_guard<std::mutex> lk(mu);
         free_blocks.emplace(cap, std::make_pair(p, pinned));
     }

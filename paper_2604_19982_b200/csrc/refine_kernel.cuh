@@ -79,9 +79,20 @@ struct SegAgg {
 //  21-23 v1 - v0   24-26 v2 - v0   (FP64 differences rounded to FP32)   27 M (max |coordinate|)
 //  28-31 (int bits) the unit normal and the 3 unit edge directions quantised to int8x3
 //        (round(127 x), 4th byte 0) for the DP4A conditioning pre-test (well_cond_q)
-struct __align__(16) ScreenSmem {
-    float rc[kRT * kCS];
-    float sc[kST * kCS];
+// Split screen (k_screen<true> + k_sat): the tiles hold only what stage 1 reads, 5 float4 per
+// record: floats 0-11 (box part), 12-15 (geometry floats 24-27: v2 - v0, M), 16-19 (the
+// quantised directions, geometry floats 28-31). Stage 2 runs in its own kernel (k_sat) on
+// the full records in global memory.
+constexpr int kCSs = 20;   // split tile stride (floats)
+constexpr int kQOff = 28;  // quantised directions in a full record
+constexpr int kQOffS = 16; // ... in a split tile row
+constexpr int kMOff = 27;  // M in a full record
+constexpr int kMOffS = 15; // ... in a split tile row
+
+template <int kStride>
+struct __align__(16) ScreenSmemT {
+    float rc[kRT * kStride];
+    float sc[kST * kStride];
     uint16_t q[kQueue];
     uint16_t rl[kCap]; // surviving r facets of the current raw chunk (offsets in the chunk)
     uint16_t sl[kCap]; // surviving s facets
@@ -97,6 +108,8 @@ struct __align__(16) ScreenSmem {
     // register limit): tested, separating-axis tests, verified, voxel pairs skipped, dropped
     uint32_t cnt[5];
 };
+using ScreenSmem = ScreenSmemT<kCS>;
+using ScreenSmemS = ScreenSmemT<kCSs>;
 
 __device__ __forceinline__ float rd(double x) { return __double2float_rd(x); }
 __device__ __forceinline__ float ru(double x) { return __double2float_ru(x); }
@@ -299,10 +312,10 @@ struct RowRec {
     int q[4];
 };
 
-__device__ __forceinline__ RowRec load_row(const float* a) {
+__device__ __forceinline__ RowRec load_row(const float* a, int qoff = kQOff) {
     RowRec r;
     const float4 p0 = *reinterpret_cast<const float4*>(a), p1 = *reinterpret_cast<const float4*>(a + 4);
-    const int4 pq = *reinterpret_cast<const int4*>(a + 28);
+    const int4 pq = *reinterpret_cast<const int4*>(a + qoff);
     r.lo[0] = p0.x; r.lo[1] = p0.y; r.lo[2] = p0.z; r.L = p0.w;
     r.hi[0] = p1.x; r.hi[1] = p1.y; r.hi[2] = p1.z; r.hd = p1.w;
     r.ph = a[11];

@@ -365,7 +365,7 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
                 count_launch();
                 k_fill_u64<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(ubb.p, n, kInfBits);
                 TJ_CUDA(cudaMemsetAsync(counters.p, 0, kNumCounters * 8, st));
-                TJ_CUDA(cudaMemsetAsync(queue.count.p, 0, 16, st));
+                queue.reset(st);
                 count_launch();
                 k_facet_pairs<<<grid_for(n_active, 256, ws.num_sms), 256, 0, st>>>(
                     active.p, n_active, R.facet_offsets[sr].p, S.facet_offsets[ss].p, counters.p + 2);
@@ -398,17 +398,14 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
                                    });
                 }
                 TJ_CUDA(cudaEventRecord(e1, st));
-                unsigned long long ovf = 0;
                 TJ_CUDA(cudaMemcpyAsync(hc, counters.p, sizeof(hc), cudaMemcpyDeviceToHost, st));
-                TJ_CUDA(cudaMemcpyAsync(&ovf, queue.count.p + 1, 8, cudaMemcpyDeviceToHost, st));
                 tdbg[0] = Clock::now();
-                stream_sync(st);
+                // an exact-evaluation (or stage-2 candidate) queue overflowed somewhere in the
+                // level: grow it and redo the level (the screen is deterministic given the same
+                // evaluations)
+                const bool rerun = queue.grow_if_overflowed(st);
                 tdbg[1] = Clock::now();
-                if (ovf == 0) break;
-                // an exact-evaluation queue overflowed somewhere in the level: grow it and
-                // redo the level (the screen is deterministic given the same evaluations)
-                if (ovf + ovf / 4 > queue.items.n) queue.items.alloc(ovf + ovf / 4);
-                queue.cap = 0;
+                if (!rerun) break;
                 ++out.queue_reruns;
             }
             out.chunks += (n_active + spec.refine_chunk - 1) / spec.refine_chunk;
@@ -600,7 +597,7 @@ void exact_recompute_dev(Workspace& ws, const DatasetDev& R, const DatasetDev& S
         k_fill_u64<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(lbb.p, n, kInfBits);
         count_launch();
         k_fill_u64<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(ubb.p, n, kInfBits);
-        TJ_CUDA(cudaMemsetAsync(queue.count.p, 0, 16, st));
+        queue.reset(st);
         if (!mat) {
             passes(0, total);
         } else { // compact-resident: expand the level-100 voxels of the confirmed pairs chunk by chunk
@@ -619,12 +616,7 @@ void exact_recompute_dev(Workspace& ws, const DatasetDev& R, const DatasetDev& S
                                passes(cb, ce);
                            });
         }
-        unsigned long long ovf = 0;
-        TJ_CUDA(cudaMemcpyAsync(&ovf, queue.count.p + 1, 8, cudaMemcpyDeviceToHost, st));
-        stream_sync(st);
-        if (ovf == 0) break;
-        if (ovf + ovf / 4 > queue.items.n) queue.items.alloc(ovf + ovf / 4);
-        queue.cap = 0;
+        if (!queue.grow_if_overflowed(st)) break;
     }
     count_launch();
     k_exact_store<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(cs.view(), n, lbb.p);

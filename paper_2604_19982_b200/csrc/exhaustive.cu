@@ -32,6 +32,7 @@
 
 #include "filter.cuh"
 #include "geom_exact.cuh"
+#include "scan.cuh"
 
 struct tj_ctx_view {
     int device;
@@ -334,6 +335,11 @@ __global__ void k_to_bits(const double* __restrict__ d, uint64_t n, unsigned lon
         bits[x] = (unsigned long long)__double_as_longlong(d[x]); // d >= 0: IEEE bits order as unsigned
 }
 
+struct ReadU64 {
+    const uint64_t* p;
+    __device__ __forceinline__ uint64_t operator()(uint64_t i) const { return p[i]; }
+};
+
 struct MeshSetDev {
     uint32_t n = 0;
     uint64_t n_tris = 0;
@@ -395,13 +401,7 @@ uint64_t box_pairs(const MeshSetDev& R, const MeshSetDev& S, double tau, const d
     k_box_pairs<false><<<grid, kBoxThreads, 0, st>>>(R.obox.p, nr, S.obox.p, S.n, tau, tau_r, counts.p, nullptr,
                                                      nullptr);
     TJ_CUDA(cudaGetLastError());
-    size_t bytes = 0;
-    TJ_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, counts.p, offsets.p + 1, (int64_t)nr, st));
-    ws.temp.reserve(bytes);
-    TJ_CUDA(cub::DeviceScan::InclusiveSum(ws.temp.p, bytes, counts.p, offsets.p + 1, (int64_t)nr, st));
-    uint64_t total = 0;
-    TJ_CUDA(cudaMemcpyAsync(&total, offsets.p + nr, 8, cudaMemcpyDeviceToHost, st));
-    stream_sync(st);
+    const uint64_t total = device_scan(ReadU64{counts.p}, nr, offsets.p, ws.u64a, ws.num_sms, st);
     pr.alloc(std::max<uint64_t>(total, 1));
     ps.alloc(std::max<uint64_t>(total, 1));
     if (!total) return 0;

@@ -19,6 +19,7 @@
 #include <cub/cub.cuh>
 
 #include "filter.cuh"
+#include "scan.cuh"
 #include "geom_exact.cuh"
 
 namespace tjx {
@@ -389,23 +390,15 @@ inline int grid_for(uint64_t items, int per_block, int num_sms) {
 
 } // namespace
 
-// Exclusive scan of n u32 counts into n+1 u64 offsets (offsets[n] = total).
+struct ReadU32 {
+    const uint32_t* p;
+    __device__ __forceinline__ uint64_t operator()(uint64_t i) const { return p[i]; }
+};
+
+// Exclusive scan of n u32 counts into n+1 u64 offsets (offsets[n] = total): scan.cuh.
 uint64_t scan_counts(Workspace& ws, const uint32_t* counts, uint64_t n, DevBuf<uint64_t>& offsets, cudaStream_t st) {
     offsets.reserve(n + 1);
-    TJ_CUDA(cudaMemsetAsync(offsets.p, 0, sizeof(uint64_t), st));
-    if (n == 0) return 0;
-    DevBuf<uint64_t>& wide = ws.u64a;
-    wide.reserve(n);
-    count_launch();
-    k_widen<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(counts, wide.p, n);
-    size_t bytes = 0;
-    TJ_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, wide.p, offsets.p + 1, (int64_t)n, st));
-    ws.temp.reserve(bytes);
-    TJ_CUDA(cub::DeviceScan::InclusiveSum(ws.temp.p, bytes, wide.p, offsets.p + 1, (int64_t)n, st));
-    uint64_t total = 0;
-    TJ_CUDA(cudaMemcpyAsync(&total, offsets.p + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-    stream_sync(st);
-    return total;
+    return device_scan(ReadU32{counts}, n, offsets.p, ws.u64a, ws.num_sms, st);
 }
 
 void mbb_prepare_s(Workspace& ws, const DatasetDev& S, SortedS& out, cudaStream_t st) {

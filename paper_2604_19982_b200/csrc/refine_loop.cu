@@ -21,6 +21,7 @@
 #include <cstdlib>
 
 #include "filter.cuh"
+#include "scan.cuh"
 #include "trace_sink.h"
 
 namespace tjx {
@@ -94,10 +95,6 @@ __global__ void k_aggregate(CandDev c, uint64_t n, const unsigned long long* __r
     }
 }
 
-struct StillUndecided {
-    const uint8_t* status;
-    __device__ __forceinline__ bool operator()(const ActiveVpDev& a) const { return status[a.op] == TJ_UNDECIDED; }
-};
 
 inline int grid_for(uint64_t items, int per_block, int num_sms) {
     const uint64_t g = (items + per_block - 1) / per_block;
@@ -120,6 +117,11 @@ void check_error(DevError* err, cudaStream_t st) {
 }
 
 // ---- on-demand expansion of compact-resident levels (TJ_DATASET_COMPACT) ----
+
+struct ReadU64 {
+    const uint64_t* p;
+    __device__ __forceinline__ uint64_t operator()(uint64_t i) const { return p[i]; }
+};
 
 __global__ void k_mark_voxels(const ActiveVpDev* __restrict__ act, uint64_t b, uint64_t e, uint8_t* __restrict__ fr,
                               uint8_t* __restrict__ fs) {
@@ -146,12 +148,7 @@ void mat_count(Workspace& ws, const DatasetDev& D, int slot, LevelMat& m, cudaSt
     if (!nv) return;
     count_launch();
     k_flag_counts<<<grid_for(nv, 256, ws.num_sms), 256, 0, st>>>(m.flag.p, D.facet_offsets[slot].p, nv, m.cnt.p);
-    size_t bytes = 0;
-    TJ_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, m.cnt.p, m.off.p + 1, (int64_t)nv, st));
-    ws.temp.reserve(bytes);
-    TJ_CUDA(cub::DeviceScan::InclusiveSum(ws.temp.p, bytes, m.cnt.p, m.off.p + 1, (int64_t)nv, st));
-    TJ_CUDA(cudaMemcpyAsync(&m.total, m.off.p + nv, 8, cudaMemcpyDeviceToHost, st));
-    stream_sync(st);
+    m.total = device_scan(ReadU64{m.cnt.p}, nv, m.off.p, ws.u64a, ws.num_sms, st);
 }
 
 // Expands the counted voxels and derives their screening records / segment aggregates.
@@ -265,24 +262,30 @@ uint32_t tripwire_mask() {
     return p - 1;
 }
 
+// erase_if of the decided ops' voxel pairs (src/refine.cpp:299-301): stable compaction of the
+// active list (scan.cuh) into the workspace, copied back.
+struct ActiveKeep {
+    const ActiveVpDev* a;
+    const uint8_t* status;
+    __device__ __forceinline__ bool operator()(uint64_t i) const { return status[a[i].op] == TJ_UNDECIDED; }
+};
+struct ActiveEmit {
+    const ActiveVpDev* a;
+    ActiveVpDev* out;
+    __device__ __forceinline__ void operator()(uint64_t i, uint64_t k) const { out[k] = a[i]; }
+};
+
 uint64_t compact_active(Workspace& ws, const CandDevStore& cs, DevBuf<ActiveVpDev>& active, uint64_t n,
                         cudaStream_t st) {
     if (n == 0) return 0;
     // scratch from the workspace (grow-only: no allocation between the levels of a join,
     // where a pool growth stalled the host for tens of milliseconds), result copied back
     ws.active_alt.reserve(n);
-    ws.nsel.reserve(1);
-    StillUndecided pred{cs.status.p};
-    size_t bytes = 0;
-    TJ_CUDA(cub::DeviceSelect::If(nullptr, bytes, active.p, ws.active_alt.p, ws.nsel.p, (int64_t)n, pred, st));
-    ws.temp.reserve(bytes);
-    TJ_CUDA(cub::DeviceSelect::If(ws.temp.p, bytes, active.p, ws.active_alt.p, ws.nsel.p, (int64_t)n, pred, st));
-    int64_t h = 0;
-    TJ_CUDA(cudaMemcpyAsync(&h, ws.nsel.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    stream_sync(st);
+    const uint64_t h = device_select(ActiveKeep{active.p, cs.status.p}, ActiveEmit{active.p, ws.active_alt.p}, n,
+                                     ws.u64a, st);
     if (h > 0)
         TJ_CUDA(cudaMemcpyAsync(active.p, ws.active_alt.p, (size_t)h * sizeof(ActiveVpDev), cudaMemcpyDeviceToDevice, st));
-    return (uint64_t)h;
+    return h;
 }
 
 RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetDev& S, CandDevStore& cs,

@@ -3,7 +3,6 @@
 // refine.hpp:57-87, knn.hpp:19-54), each run on the device over a caller-owned host
 // candidate set. tj_join chains the same device stages without the host round trips.
 #include <cub/cub.cuh>
-#include <thrust/iterator/counting_iterator.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -13,6 +12,7 @@
 
 #include "filter.cuh"
 #include "geom_exact.cuh"
+#include "scan.cuh"
 #include "trace_sink.h"
 
 // Shared with capi.cu (same translation-unit-independent definitions).
@@ -153,6 +153,11 @@ __global__ void k_fill(unsigned long long* p, uint64_t n, unsigned long long v) 
         p[i] = v;
 }
 
+struct IndexEmit {
+    uint64_t* out;
+    __device__ __forceinline__ void operator()(uint64_t i, uint64_t k) const { out[k] = i; }
+};
+
 // ---- voxel_pair_compact: stable survivors (op, i, j) of one chunk ----
 struct Survives {
     const uint32_t* ops;
@@ -169,7 +174,7 @@ struct Survives {
         }
         return lo;
     }
-    __device__ __forceinline__ bool operator()(const uint64_t& t) const {
+    __device__ __forceinline__ bool operator()(uint64_t t) const {
         const uint32_t op = ops[slot(t)];
         return status[op] == TJ_UNDECIDED && vp_lb[t] <= ub[op];
     }
@@ -445,18 +450,7 @@ int tj_voxel_compact(tj_ctx* ctx, const tj_dataset* Rh, const tj_dataset* Sh, co
         to_dev(dlb, vp_lb, total, st);
         Survives sv{d_ops.p, d_off.p, n_ops, stv.p, ub.p, dlb.p};
         DevBuf<uint64_t> sel(std::max<uint64_t>(total, 1));
-        DevBuf<int64_t> nsel(1);
-        TJ_CUDA(cudaMemsetAsync(nsel.p, 0, sizeof(int64_t), st));
-        if (total) {
-            thrust::counting_iterator<uint64_t> it(0);
-            size_t bytes = 0;
-            TJ_CUDA(cub::DeviceSelect::If(nullptr, bytes, it, sel.p, nsel.p, (int64_t)total, sv, st));
-            ws.temp.reserve(bytes);
-            TJ_CUDA(cub::DeviceSelect::If(ws.temp.p, bytes, it, sel.p, nsel.p, (int64_t)total, sv, st));
-        }
-        int64_t n = 0;
-        TJ_CUDA(cudaMemcpyAsync(&n, nsel.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        stream_sync(st);
+        const int64_t n = (int64_t)device_select(sv, IndexEmit{sel.p}, total, ws.u64a, st);
         DevBuf<uint32_t> o_op(std::max<int64_t>(n, 1)), o_i(std::max<int64_t>(n, 1)), o_j(std::max<int64_t>(n, 1));
         if (n) {
             count_launch();

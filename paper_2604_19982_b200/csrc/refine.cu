@@ -21,6 +21,10 @@ __device__ unsigned long long* g_dbg_op_tested = nullptr;
 
 // k_screen launch shape: 8 warps per block, 2 blocks per SM (16 warps, 128 registers; 4 x 5 was
 // slower: the 102-register bound spills the stage-2 code)
+#ifndef TJ_S1_UNROLL
+#define TJ_S1_UNROLL 1 // stage-1 inner loop unroll (B: 1 = 2 = 63.6 ms, 4: 67.4; C: 1: 191, 2: 198, 4: 216 ms)
+#endif
+constexpr int kS1Unroll = TJ_S1_UNROLL;
 constexpr int kScreenThreads = 256;
 constexpr int kScreenBlocks = 2;
 // split screen (stage 1 only): 3 blocks per SM (24 warps, <= 80 registers)
@@ -752,7 +756,7 @@ __global__ void __launch_bounds__(kScreenThreads, kSplit ? kScreenBlocksS : kScr
                             // pre-test failed (its FP32 test runs at the flush, 32 pairs at a time).
                             uint32_t nmask = 0, fmask = 0;
                             if (row_on) {
-#pragma unroll 2
+#pragma unroll kS1Unroll
                                 for (int t = 0; t < iters; ++t) {
                                     const float* bp = sm.sc + (jj + t * P) * CS;
                                     const int sb = stage1_box(ar, *reinterpret_cast<const float4*>(bp),

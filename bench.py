@@ -473,6 +473,9 @@ def main():
                            f"({res_bytes / 1e9:.1f} GB resident)", "parallelism": f"r-shard x{world}",
                            "setup_s": round(setup_s, 1), "cull": not a.no_cull,
                            "step_ms": [round(x, 2) for x in step_ms],
+                           "filter_last_step": {k: outs[-1][k] for k in ("n_cands", "voxel_pairs_in", "vp_generated",
+                                                                      "vp_pruned", "confirmed", "mbb_ms",
+                                                                      "voxel_ms")},
                            "levels_last_step": outs[-1]["levels"]},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
                 "gpu_launches": int(launches), "parity": parity}

@@ -40,16 +40,16 @@ namespace detail {
 }
 
 namespace {
+// The per-device contexts live until the process exits and are never destroyed: a static
+// destructor would run after the CUDA runtime's own teardown (the registry is constructed before
+// the runtime's first call registers it) and release streams and memory on a dead runtime.
 struct CtxRegistry {
     std::mutex mu;
     std::map<std::pair<int, int>, tj_ctx*> ctxs;
-    ~CtxRegistry() {
-        for (auto& [d, c] : ctxs) tj_ctx_destroy(c);
-    }
 };
 CtxRegistry& registry() {
-    static CtxRegistry r;
-    return r;
+    static CtxRegistry* r = new CtxRegistry;
+    return *r;
 }
 } // namespace
 

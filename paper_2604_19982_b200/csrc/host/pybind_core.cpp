@@ -119,8 +119,9 @@ py::tuple pack_output(const JoinOutput& out) {
 // dataset's address, validated by a weak reference (a freed dataset's entry is dropped).
 detail::JoinCache* dataset_cache(const std::shared_ptr<PreparedDataset>& ds) {
     static std::mutex mu;
-    static std::map<const PreparedDataset*, std::pair<std::weak_ptr<PreparedDataset>, std::unique_ptr<detail::JoinCache>>>
-        caches;
+    // never destroyed (pinned host buffers must not be released after the CUDA runtime's teardown)
+    static auto& caches = *new std::map<const PreparedDataset*,
+                                        std::pair<std::weak_ptr<PreparedDataset>, std::unique_ptr<detail::JoinCache>>>;
     std::lock_guard<std::mutex> lk(mu);
     for (auto it = caches.begin(); it != caches.end();)
         it = it->second.first.expired() ? caches.erase(it) : std::next(it);

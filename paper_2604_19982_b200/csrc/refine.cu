@@ -27,8 +27,6 @@ __device__ unsigned long long* g_dbg_op_tested = nullptr;
 constexpr int kS1Unroll = TJ_S1_UNROLL;
 constexpr int kScreenThreads = 256;
 constexpr int kScreenBlocks = 2;
-// split screen (stage 1 only): 3 blocks per SM (24 warps, <= 80 registers)
-constexpr int kScreenBlocksS = 3;
 
 struct VpDescDev {
     uint32_t op;
@@ -102,22 +100,27 @@ __device__ __forceinline__ void queue_push(const RefineQueue& q, bool want, uint
 // Cooperative gather of up to 32 screening records (facets first + list[k]) into shared
 // memory: box part from `box`, geometry part from `geo` (kRecF4 float4 per record, rows
 // kCS floats apart).
-template <bool kSplit>
 __device__ __forceinline__ void gather_recs(const float4* __restrict__ box, const float4* __restrict__ geo,
-                                            uint64_t first, const uint16_t* list, int n, float* dst) {
+                                            const double* __restrict__ facets, uint64_t first, const uint16_t* list,
+                                            int n, float* dst) {
     // cp.async: every 16-B piece is in flight at once (a load -> store loop serialises one
-    // global latency per iteration and lane). Split tiles: box part + geometry parts 3, 4.
-    constexpr int kParts = kSplit ? 5 : kRecF4, kStride4 = (kSplit ? kCSs : kCS) / 4;
+    // global latency per iteration and lane).
+    constexpr int kParts = kRecF4, kStride4 = kCS / 4;
     const int lane = threadIdx.x & 31;
     float4* d4 = reinterpret_cast<float4*>(dst);
     for (int k = lane; k < kParts * n; k += 32) {
         const int rec = k / kParts, part = k % kParts;
         const uint64_t f = first + list[rec];
-        const int gpart = kSplit ? part + 3 - kBoxF4 : part - kBoxF4; // split: geometry parts 3, 4
-        const float4* g = part < kBoxF4 ? box + f * kBoxF4 + part : geo + f * kGeoF4 + gpart;
+        const float4* g = part < kBoxF4 ? box + f * kBoxF4 + part : geo + f * kGeoF4 + (part - kBoxF4);
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_addr(d4 + rec * kStride4 + part)),
                      "l"(g)
                      : "memory");
+    }
+    if (lane < n) { // the facet's FP64 v0 (16 + 8 B)
+        const double* v = facets + (first + list[lane]) * 12;
+        float* r = dst + lane * kCS + kV0Off;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_addr(r)), "l"(v) : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_addr(r + 4)), "l"(v + 2) : "memory");
     }
 }
 __device__ __forceinline__ void gather_wait() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
@@ -455,8 +458,10 @@ __device__ __forceinline__ int sat_needed(const float* a, const float* b, const 
     const float B0 = box_gap_lb(a, b);
     int mask = cannot_improve(B0, a, b, th) ? skip_mask(B0, a, b) : -1;
     if (mask == 0) return 0;
-    const float off[3] = {(float)(__ldg(vb) - __ldg(va)), (float)(__ldg(vb + 1) - __ldg(va + 1)),
-                          (float)(__ldg(vb + 2) - __ldg(va + 2))};
+    // b.v0 - a.v0 from the staged FP64 vertices, rounded once
+    const double* sa = reinterpret_cast<const double*>(a + kV0Off);
+    const double* sb = reinterpret_cast<const double*>(b + kV0Off);
+    const float off[3] = {(float)(sb[0] - sa[0]), (float)(sb[1] - sa[1]), (float)(sb[2] - sa[2])};
     const SatFrame f = sat_frame(a, b, off);
     if (mask > 0) { // the box gap already rules the pair out up to conditioning: plane sides first
         mask = plane_clear(mask, f, a, b);
@@ -563,16 +568,13 @@ __device__ __forceinline__ bool level_ub_settled(const RefineSource& src, int cu
     return hd2 > __fadd_ru(__fadd_ru(__fmul_ru(1e-5f, l2), __fmul_ru(1e-12f, m2)), 1e-30f);
 }
 
-// kSplit: stage 1 only; its stage-2 candidates go to the SatQueue for k_sat (smaller tiles,
-// fewer registers, more resident warps) instead of being screened here.
-template <bool kSplit>
-__global__ void __launch_bounds__(kScreenThreads, kSplit ? kScreenBlocksS : kScreenBlocks)
+__global__ void __launch_bounds__(kScreenThreads, kScreenBlocks)
     k_screen(RefineSource src, uint64_t vp_begin, uint64_t vp_end, const unsigned long long* __restrict__ op_lb_bits,
              const unsigned long long* __restrict__ op_ub_bits, int cull, RefineQueue q, unsigned long long* work,
-             unsigned long long* counters, unsigned batch, uint32_t hier_min, SatQueue sq) {
+             unsigned long long* counters, unsigned batch, uint32_t hier_min) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    using SM = ScreenSmemT<kSplit ? kCSs : kCS>;
-    constexpr int CS = kSplit ? kCSs : kCS, QO = kSplit ? kQOffS : kQOff, MO = kSplit ? kMOffS : kMOff;
+    using SM = ScreenSmem;
+    constexpr int CS = kCS, QO = kQOff, MO = kMOff;
     SM& sm = reinterpret_cast<SM*>(smem_raw)[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
     if (lane < 5) sm.cnt[lane] = 0;
@@ -622,13 +624,15 @@ __global__ void __launch_bounds__(kScreenThreads, kSplit ? kScreenBlocksS : kScr
             const VpDescDev dl = get_vp(src, base + lane);
             const Thresh tl = thresholds(dl);
             live = dl.rn != 0 && dl.sn != 0 && !settled(tl);
+            int flags = tl.lb_sat ? 1 : 0;
             if (live && pre_seg) {
                 float d0;
                 SegAgg ar, as;
                 agg_skipped = vp_screen(dl, tl, d0, ar, as);
                 live = !agg_skipped;
+                if (shapes_settled(ar, as)) flags |= 2;
             }
-            if (live) sm.vpd[lane] = {dl.r0, dl.s0, dl.op, dl.gvr, dl.gvs, dl.rn, dl.sn, tl.lb_u, tl.ub_u, (int)tl.lb_sat};
+            if (live) sm.vpd[lane] = {dl.r0, dl.s0, dl.op, dl.gvr, dl.gvs, dl.rn, dl.sn, tl.lb_u, tl.ub_u, flags};
         }
         if (pre_seg) {
             const unsigned n_agg = __popc(__ballot_sync(0xffffffffu, agg_skipped));
@@ -652,8 +656,9 @@ __global__ void __launch_bounds__(kScreenThreads, kSplit ? kScreenBlocksS : kScr
             d.sn = b.sn;
             th.lb_u = b.lb_u;
             th.ub_u = b.ub_u;
-            th.lb_sat = b.lb_sat != 0;
+            th.lb_sat = (b.flags & 1) != 0;
         }
+        const bool shapes_ok = (sm.vpd[lv].flags & 2) != 0;
         // hierarchical screens: the whole voxel pair (always when the segment aggregates are
         // precomputed), then rows / columns where that can pay off
         const bool hier = cull && d.rn * d.sn >= hier_min;
@@ -676,6 +681,15 @@ __global__ void __launch_bounds__(kScreenThreads, kSplit ? kScreenBlocksS : kScr
                 __syncwarp();
             }
         }
+        // per s record of a staged tile: its ph and hd pre-scaled for stage1_box (pad floats 32, 33)
+        auto scale_s_tile = [&](int scnt) {
+            if (lane < scnt) {
+                float* r = sm.sc + lane * CS;
+                r[32] = __fmul_ru(r[11], kInvC);
+                r[33] = __fmul_rd(r[7], kInvC);
+            }
+            __syncwarp();
+        };
         for (uint32_t rc0 = 0; rc0 < d.rn; rc0 += kCap) {
             const int nrl = build_list(src.r_box, d.r0 + rc0, min((uint32_t)kCap, d.rn - rc0), sm.seg_s, delta0, th, hier,
                                        sm.rl, &sm.cnt[4]);
@@ -686,17 +700,19 @@ __global__ void __launch_bounds__(kScreenThreads, kSplit ? kScreenBlocksS : kScr
                     const int rcnt = min(kRT, nrl - rt0);
                     __syncwarp();
                     // the r tile and the first s tile in flight together
-                    gather_recs<kSplit>(src.r_box, src.r_geo, d.r0 + rc0, sm.rl + rt0, rcnt, sm.rc);
-                    gather_recs<kSplit>(src.s_box, src.s_geo, d.s0 + sc0, sm.sl, min(kST, nsl), sm.sc);
+                    gather_recs(src.r_box, src.r_geo, src.r_facets, d.r0 + rc0, sm.rl + rt0, rcnt, sm.rc);
+                    gather_recs(src.s_box, src.s_geo, src.s_facets, d.s0 + sc0, sm.sl, min(kST, nsl), sm.sc);
                     gather_wait();
                     __syncwarp();
+                    scale_s_tile(min(kST, nsl));
                     for (int st0 = 0; st0 < nsl; st0 += kST) {
                         const int scnt = min(kST, nsl - st0);
                         if (st0 > 0) {
                             __syncwarp();
-                            gather_recs<kSplit>(src.s_box, src.s_geo, d.s0 + sc0, sm.sl + st0, scnt, sm.sc);
+                            gather_recs(src.s_box, src.s_geo, src.s_facets, d.s0 + sc0, sm.sl + st0, scnt, sm.sc);
                             gather_wait();
                             __syncwarp();
+                            scale_s_tile(scnt);
                         }
                         float dl = delta0;
                         if (!hier) { // tile-pair delta0 >= 1e-5 (L_i + L_j) + 1e-12 (M_i + M_j)
@@ -737,7 +753,7 @@ __global__ void __launch_bounds__(kScreenThreads, kSplit ? kScreenBlocksS : kScr
                         // Stage 1, register-blocked, in row passes: a pass takes `rows` r facets
                         // (32, 16 or the rest) with P = 32 / rows lanes per r facet, so a 24-row
                         // tile runs as 16 + 8 rows on all 32 lanes instead of 24 lanes.
-                        int nq = 0;
+                        int nq = 0, qh = 0; // the warp's stage-2 ring: nq entries from sm.q[qh]
                         for (int rp0 = 0; rp0 < rcnt;) {
                             const int left = rcnt - rp0;
                             const int rows = left >= 32 ? 32 : left > 16 ? 16 : left;
@@ -747,53 +763,20 @@ __global__ void __launch_bounds__(kScreenThreads, kSplit ? kScreenBlocksS : kScr
                             const bool row_on = lane / P < rows;
                             rp0 += rows;
                             const RowRec ar = load_row(sm.rc + bi * CS, QO);
-                            // per-row thresholds of the stage-1 pair test (stage1_box)
+                            // per-row thresholds of the stage-1 pair test, pre-scaled by 1 / c (stage1_box)
                             const float rlb = lb_settled ? ninf : __fadd_ru(__fadd_ru(th.lb_u, dl), ar.ph);
                             const float rub = th.ub_u == 0.f ? ninf : __fsub_ru(__fadd_ru(th.ub_u, dl), ar.hd);
+                            const float rlbc = __fmul_ru(rlb, kInvC), rubc = __fmul_ru(rub, kInvC);
                             const int iters = (scnt - jj + P - 1) / P; // this lane's s facets
                             // The lane's s facets (jj + t P) into bit masks: bit t of `nmask` = the
                             // pair goes to stage 2; of `fmask` = a near pair whose DP4A conditioning
                             // pre-test failed (its FP32 test runs at the flush, 32 pairs at a time).
                             uint32_t nmask = 0, fmask = 0;
                             if (row_on) {
-#pragma unroll kS1Unroll
-                                for (int t = 0; t < iters; ++t) {
-                                    const float* bp = sm.sc + (jj + t * P) * CS;
-                                    const int sb = stage1_box(ar, *reinterpret_cast<const float4*>(bp),
-                                                              *reinterpret_cast<const float4*>(bp + 4), bp[11], rlb, rub);
-                                    const bool f = sb == 2 && !well_cond_q(ar.q, *reinterpret_cast<const int4*>(bp + QO));
-                                    nmask |= (uint32_t)(sb == 1 || f) << t;
-                                    fmask |= (uint32_t)f << t;
-                                }
-                            }
-                            if constexpr (kSplit) {
-                                // stage-2 candidates straight to the SatQueue: one warp-aggregated
-                                // append per row pass, each lane writes its run of entries
-                                const int cnt = __popc(nmask);
-                                int incl = cnt;
-#pragma unroll
-                                for (int o = 1; o < 32; o <<= 1) {
-                                    const int v = __shfl_up_sync(0xffffffffu, incl, o);
-                                    if (lane >= o) incl += v;
-                                }
-                                const int total = __shfl_sync(0xffffffffu, incl, 31);
-                                if (total) {
-                                    unsigned long long base = 0;
-                                    if (lane == 31) base = atomicAdd(sq.count, (unsigned long long)total);
-                                    base = __shfl_sync(0xffffffffu, base, 31);
-                                    unsigned long long pos = base + (unsigned long long)(incl - cnt);
-                                    const uint32_t fr = (uint32_t)(d.r0 + rc0 + sm.rl[rt0 + bi]);
-                                    while (nmask) {
-                                        const int t = __ffs(nmask) - 1;
-                                        nmask &= nmask - 1;
-                                        if (pos < sq.capacity)
-                                            sq.items[pos] = {d.op | (((fmask >> t) & 1u) << 31), fr,
-                                                             (uint32_t)(d.s0 + sc0 + sm.sl[st0 + jj + t * P])};
-                                        ++pos;
-                                    }
-                                }
-                                __syncwarp();
-                                continue;
+                                if (shapes_ok)
+                                    stage1_row<false>(ar, sm.sc + jj * CS, P * CS, iters, rlbc, rubc, nmask, fmask);
+                                else
+                                    stage1_row<true>(ar, sm.sc + jj * CS, P * CS, iters, rlbc, rubc, nmask, fmask);
                             }
                             // compact the masks into the warp queue one entry per lane and round;
                             // stage 2 runs whenever 32 entries are queued (and on the rest after
@@ -804,7 +787,7 @@ __global__ void __launch_bounds__(kScreenThreads, kSplit ? kScreenBlocksS : kScr
                                 if (has) {
                                     const int t = __ffs(nmask) - 1;
                                     nmask &= nmask - 1;
-                                    sm.q[nq + __popc(bal & ((1u << lane) - 1u))] =
+                                    sm.q[(qh + nq + __popc(bal & ((1u << lane) - 1u))) & (kQueue - 1)] =
                                         (uint16_t)(((fmask >> t) & 1u ? 0x8000 : 0) | (bi << 5) | (jj + t * P));
                                 }
                                 nq += __popc(bal);
@@ -814,9 +797,9 @@ __global__ void __launch_bounds__(kScreenThreads, kSplit ? kScreenBlocksS : kScr
                                     __syncwarp();
                                     bool need = false;
                                     uint32_t fr = 0, fs = 0;
-                                    bool go = false;
+                                    bool go = false, ver = false;
                                     if (lane < n) {
-                                        const int e = sm.q[lane];
+                                        const int e = sm.q[(qh + lane) & (kQueue - 1)];
                                         const int i = (e >> 5) & 31, j = e & 31;
                                         go = !(e & 0x8000) || stage1_ill_fp32(sm.rc + i * kCS, sm.sc + j * kCS);
                                         if (go) {
@@ -825,20 +808,18 @@ __global__ void __launch_bounds__(kScreenThreads, kSplit ? kScreenBlocksS : kScr
                                             const int r = sat_needed(sm.rc + i * kCS, sm.sc + j * kCS, src.r_facets + (size_t)fr * 12,
                                                                      src.s_facets + (size_t)fs * 12, th);
                                             need = r & 1;
-                                            if (r >> 1) atomicAdd(&sm.cnt[2], 1u); // rare
+                                            ver = r >> 1;
                                         }
                                     }
                                     const unsigned ngo = __popc(__ballot_sync(0xffffffffu, go));
-                                    if (lane == 0) sm.cnt[1] += ngo;
+                                    const unsigned nver = __popc(__ballot_sync(0xffffffffu, ver));
+                                    if (lane == 0) {
+                                        sm.cnt[1] += ngo;
+                                        sm.cnt[2] += nver;
+                                    }
                                     queue_push(q, need, d.op, fr, fs);
                                     __syncwarp();
-                                    for (int k0 = 0; k0 < nq - n; k0 += 32) { // shift the rest down (in order)
-                                        const bool mv = k0 + lane < nq - n;
-                                        const uint16_t v = mv ? sm.q[n + k0 + lane] : 0;
-                                        __syncwarp();
-                                        if (mv) sm.q[k0 + lane] = v;
-                                        __syncwarp();
-                                    }
+                                    qh = (qh + n) & (kQueue - 1);
                                     nq -= n;
                                 }
                                 if (bal == 0) break;
@@ -859,80 +840,6 @@ __global__ void __launch_bounds__(kScreenThreads, kSplit ? kScreenBlocksS : kScr
             atomicAdd(counters + 5, (unsigned long long)sm.cnt[3]);
             atomicAdd(counters + 6, (unsigned long long)sm.cnt[4]);
         }
-    }
-}
-
-// Second stage of the split screen: thread per stage-2 candidate (SatQueue), the full FP32
-// records of both facets staged in the thread's shared-memory slots; the FP32 conditioning
-// test where the DP4A pre-test failed, then the separating-axis / plane / FP64 piercing
-// stage (sat_needed) against the op's thresholds; survivors go to the exact queue. The op
-// minima do not change between the passes (k_eval runs after this kernel), so the thresholds
-// are the ones stage 1 used.
-__global__ void __launch_bounds__(128) k_sat(RefineSource src, const unsigned long long* __restrict__ op_lb_bits,
-                                             const unsigned long long* __restrict__ op_ub_bits, int cull, SatQueue sq,
-                                             RefineQueue q, unsigned long long* counters) {
-    __shared__ __align__(16) float rec[128][2][32];
-    const int lane = threadIdx.x & 31;
-    const bool ub_level_settled = level_ub_settled(src, cull);
-    unsigned long long n = *sq.count;
-    if (blockIdx.x == 0 && threadIdx.x == 0 && n > sq.capacity) atomicMax(sq.count + 1, n); // overflow record
-    if (n > sq.capacity) n = sq.capacity;
-    uint32_t screened = 0, verified = 0;
-    float* a = rec[threadIdx.x][0];
-    float* b = rec[threadIdx.x][1];
-    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    for (unsigned long long k0 = blockIdx.x * (unsigned long long)blockDim.x + (threadIdx.x & ~31u); k0 < n;
-         k0 += stride) { // warp-uniform trip count (queue_push is warp-collective)
-        const unsigned long long k = k0 + lane;
-        bool need = false;
-        uint32_t op = 0, fr = 0, fs = 0;
-        if (k < n) {
-            const SatRef e = sq.items[k];
-            op = e.op & 0x7fffffffu;
-            fr = e.fr;
-            fs = e.fs;
-            const double iv_lb = src.active ? src.cand_lb[op] : 0.0;
-            const double iv_ub = src.active ? src.cand_ub[op] : __longlong_as_double(0x7ff0000000000000ll);
-            const double tlb = bits_to_double(__ldcg(op_lb_bits + op));
-            double tub = bits_to_double(__ldcg(op_ub_bits + op));
-            tub = tub < iv_ub ? tub : iv_ub;
-            Thresh th{ru(tlb), ru(tub), tlb <= iv_lb};
-            if (cull == 2 && !exact_op(src.exact_mask, op)) {
-                constexpr float kTiny = 1e-30f;
-                th.lb_sat = tlb == 0.0;
-                th.lb_u = th.lb_sat ? 0.f : kTiny;
-                th.ub_u = tub == 0.0 || ub_level_settled ? 0.f : kTiny;
-            }
-            float4* a4 = reinterpret_cast<float4*>(a);
-            float4* b4 = reinterpret_cast<float4*>(b);
-#pragma unroll
-            for (int p = 0; p < kBoxF4; ++p) {
-                a4[p] = __ldg(src.r_box + (size_t)fr * kBoxF4 + p);
-                b4[p] = __ldg(src.s_box + (size_t)fs * kBoxF4 + p);
-            }
-#pragma unroll
-            for (int p = 0; p < kGeoF4; ++p) {
-                a4[kBoxF4 + p] = __ldg(src.r_geo + (size_t)fr * kGeoF4 + p);
-                b4[kBoxF4 + p] = __ldg(src.s_geo + (size_t)fs * kGeoF4 + p);
-            }
-            const bool go = !(e.op >> 31) || stage1_ill_fp32(a, b);
-            if (go) {
-                ++screened;
-                const int r = sat_needed(a, b, src.r_facets + (size_t)fr * 12, src.s_facets + (size_t)fs * 12, th);
-                need = r & 1;
-                verified += (uint32_t)(r >> 1);
-            }
-        }
-        queue_push(q, need, op, fr, fs);
-    }
-    if (counters) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            screened += __shfl_xor_sync(0xffffffffu, screened, o);
-            verified += __shfl_xor_sync(0xffffffffu, verified, o);
-        }
-        if (lane == 0 && screened) atomicAdd(counters + 3, (unsigned long long)screened);
-        if (lane == 0 && verified) atomicAdd(counters + 4, (unsigned long long)verified);
     }
 }
 
@@ -977,20 +884,6 @@ __global__ void __launch_bounds__(128) k_eval(RefineSource src, RefineQueue q, u
 }
 
 constexpr size_t kScreenSmem = sizeof(ScreenSmem) * (kScreenThreads / 32);
-constexpr size_t kScreenSmemS = sizeof(ScreenSmemS) * (kScreenThreads / 32);
-
-// Split screen (k_screen<true> + k_sat), $TRIJOIN_SCREEN_SPLIT=1; off by default: measured on
-// config B it is 2.3x slower than the fused screen (63.4 -> 142.7 ms/join): its 393M
-// stage-2 candidates of the LOD-100 level cost a global queue round trip plus 2 x 128 B of
-// record loads each, where the fused kernel screens them out of the tiles already in shared
-// memory.
-bool screen_split() {
-    static const bool v = [] {
-        const char* e = getenv("TRIJOIN_SCREEN_SPLIT");
-        return e && *e == '1';
-    }();
-    return v;
-}
 
 inline int warp_grid(uint64_t warps, int num_sms, int per_sm, int warps_per_block = 8) {
     return (int)std::max<uint64_t>(
@@ -1010,17 +903,14 @@ void refine_prep(const double* facets, uint64_t n, float4* out, unsigned* agg, i
 
 void RefineQueueStore::reset(cudaStream_t st) {
     TJ_CUDA(cudaMemsetAsync(count.p, 0, 16, st));
-    TJ_CUDA(cudaMemsetAsync(sat_count.p, 0, 16, st));
 }
 
 bool RefineQueueStore::grow_if_overflowed(cudaStream_t st) {
-    unsigned long long h[2] = {0, 0};
-    TJ_CUDA(cudaMemcpyAsync(&h[0], count.p + 1, 8, cudaMemcpyDeviceToHost, st));
-    TJ_CUDA(cudaMemcpyAsync(&h[1], sat_count.p + 1, 8, cudaMemcpyDeviceToHost, st));
+    unsigned long long h = 0;
+    TJ_CUDA(cudaMemcpyAsync(&h, count.p + 1, 8, cudaMemcpyDeviceToHost, st));
     stream_sync(st);
-    if (!h[0] && !h[1]) return false;
-    if (h[0] && h[0] + h[0] / 4 > items.n) items.alloc(h[0] + h[0] / 4);
-    if (h[1] && h[1] + h[1] / 4 > sat.n) sat.alloc(h[1] + h[1] / 4);
+    if (!h) return false;
+    if (h + h / 4 > items.n) items.alloc(h + h / 4);
     cap = 0;
     return true;
 }
@@ -1069,10 +959,8 @@ void refine_pass(const RefineSource& src, uint64_t vp_begin, uint64_t vp_end, bo
         TJ_CUDA(cudaGetDevice(&dev));
         std::lock_guard<std::mutex> lk(mu);
         if (!done.count(dev)) {
-            TJ_CUDA(cudaFuncSetAttribute(k_screen<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            TJ_CUDA(cudaFuncSetAttribute(k_screen, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kScreenSmem));
-            TJ_CUDA(cudaFuncSetAttribute(k_screen<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kScreenSmemS));
             done.insert(dev);
         }
     }
@@ -1089,25 +977,11 @@ void refine_pass(const RefineSource& src, uint64_t vp_begin, uint64_t vp_end, bo
         // count in count[1] and the caller re-runs the whole level with a larger queue.
         TJ_CUDA(cudaMemsetAsync(qs.count.p, 0, 8, st));
         TJ_CUDA(cudaMemsetAsync(work, 0, 8, st));
-        const bool split = cull && screen_split();
-        const int blocks = split ? kScreenBlocksS : kScreenBlocks;
-        const int sgrid = warp_grid(vp_end - vp_begin, num_sms, blocks, kScreenThreads / 32);
+        const int sgrid = warp_grid(vp_end - vp_begin, num_sms, kScreenBlocks, kScreenThreads / 32);
         const unsigned batch = screen_batch(src.mean_seg, vp_end - vp_begin, (uint64_t)sgrid * (kScreenThreads / 32));
         count_launch();
-        if (split) {
-            const SatQueue sq = qs.sat_view();
-            TJ_CUDA(cudaMemsetAsync(sq.count, 0, 8, st));
-            k_screen<true><<<sgrid, kScreenThreads, kScreenSmemS, st>>>(src, vp_begin, vp_end, lb_bits, ub_bits, cull,
-                                                                        qs.view(), work, counters, batch,
-                                                                        hier_min_pairs(), sq);
-            TJ_CUDA(cudaGetLastError());
-            count_launch();
-            k_sat<<<num_sms * 12, 128, 0, st>>>(src, lb_bits, ub_bits, cull, sq, qs.view(), counters);
-        } else {
-            k_screen<false><<<sgrid, kScreenThreads, kScreenSmem, st>>>(src, vp_begin, vp_end, lb_bits, ub_bits, cull,
-                                                                         qs.view(), work, counters, batch,
-                                                                         hier_min_pairs(), SatQueue{});
-        }
+        k_screen<<<sgrid, kScreenThreads, kScreenSmem, st>>>(src, vp_begin, vp_end, lb_bits, ub_bits, cull, qs.view(),
+                                                              work, counters, batch, hier_min_pairs());
         TJ_CUDA(cudaGetLastError());
     }
     count_launch();

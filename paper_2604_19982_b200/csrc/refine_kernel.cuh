@@ -48,7 +48,12 @@ namespace tjx {
 
 constexpr int kRT = 32;    // r facets per screening tile
 constexpr int kST = 32;    // s facets per screening tile
-constexpr int kCS = 36;    // shared-memory stride of a screening record (32 floats + 4 pad: bank shift)
+// Shared-memory stride of a staged screening record (floats): 0-31 the record, 32-33 (s tiles)
+// ph and hd pre-scaled for stage 1, 36-41 the facet's v0 in FP64 (the separating-axis frame
+// offset), the rest padding; 44 floats = 176 B keeps the per-lane 16-B row loads conflict-free
+// (12 i mod 32 over 8 lanes).
+constexpr int kCS = 44;
+constexpr int kV0Off = 36; // FP64 v0 in a staged record (float index; 16-B aligned)
 constexpr int kRecF4 = kScreenRecF4; // float4 per screening record (floats 0-31)
 constexpr int kBoxF4 = 3;  // box part of a record (floats 0-11), its own array: 3 float4 per facet
 constexpr int kGeoF4 = 5;  // geometry part (floats 12-31): 5 float4 per facet
@@ -79,20 +84,12 @@ struct SegAgg {
 //  21-23 v1 - v0   24-26 v2 - v0   (FP64 differences rounded to FP32)   27 M (max |coordinate|)
 //  28-31 (int bits) the unit normal and the 3 unit edge directions quantised to int8x3
 //        (round(127 x), 4th byte 0) for the DP4A conditioning pre-test (well_cond_q)
-// Split screen (k_screen<true> + k_sat): the tiles hold only what stage 1 reads, 5 float4 per
-// record: floats 0-11 (box part), 12-15 (geometry floats 24-27: v2 - v0, M), 16-19 (the
-// quantised directions, geometry floats 28-31). Stage 2 runs in its own kernel (k_sat) on
-// the full records in global memory.
-constexpr int kCSs = 20;   // split tile stride (floats)
-constexpr int kQOff = 28;  // quantised directions in a full record
-constexpr int kQOffS = 16; // ... in a split tile row
-constexpr int kMOff = 27;  // M in a full record
-constexpr int kMOffS = 15; // ... in a split tile row
+constexpr int kQOff = 28;  // quantised directions in a record
+constexpr int kMOff = 27;  // M in a record
 
-template <int kStride>
-struct __align__(16) ScreenSmemT {
-    float rc[kRT * kStride];
-    float sc[kST * kStride];
+struct __align__(16) ScreenSmem {
+    float rc[kRT * kCS];
+    float sc[kST * kCS];
     uint16_t q[kQueue];
     uint16_t rl[kCap]; // surviving r facets of the current raw chunk (offsets in the chunk)
     uint16_t sl[kCap]; // surviving s facets
@@ -102,14 +99,12 @@ struct __align__(16) ScreenSmemT {
         uint64_t r0, s0;
         uint32_t op, gvr, gvs, rn, sn;
         float lb_u, ub_u;
-        int lb_sat;
+        int flags; // bit 0: lb side settled; bit 1: every facet pair meets the shape / range terms (shapes_settled)
     } vpd[32];
     // the warp's counters (lane 0 writes; kept out of registers: the stage-1 loop is at the
     // register limit): tested, separating-axis tests, verified, voxel pairs skipped, dropped
     uint32_t cnt[5];
 };
-using ScreenSmem = ScreenSmemT<kCS>;
-using ScreenSmemS = ScreenSmemT<kCSs>;
 
 __device__ __forceinline__ float rd(double x) { return __double2float_rd(x); }
 __device__ __forceinline__ float ru(double x) { return __double2float_ru(x); }
@@ -190,6 +185,9 @@ __device__ __forceinline__ float box_gap_lb(const float* a, const float* b) {
     // lower bound of sqrt(s): hardware sqrt (<= 2 ulp error) scaled down by 1 - 2^-20
     return __fmul_rd(sqrtf(s), 1.0f - 0x1p-20f);
 }
+
+// 1 / c with c = 1 - 1e-5 (stage1_box, agg_skip), rounded up
+constexpr float kInvC = 1.0f / (1.0f - 1e-5f) * (1.0f + 0x1p-20f);
 
 // Screening thresholds (warp-uniform, rounded up); lb_sat: lb' can no longer change.
 struct Thresh {
@@ -284,7 +282,6 @@ __device__ __forceinline__ float seg_m(const SegAgg& g) {
 __device__ __forceinline__ bool agg_skip(const float* alo, const float* ahi, const float* blo, const float* bhi,
                                          float lsum, float lmin, float phsum, float hdsum, float delta0,
                                          const Thresh& t) {
-    constexpr float kInvC = 1.0f / (1.0f - 1e-5f) * (1.0f + 0x1p-20f); // >= 1 / c (stage1_box)
     float g2 = 0.f, m2 = 0.f;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
@@ -350,23 +347,60 @@ __device__ __forceinline__ bool well_cond_q(const int* aq, int4 bq) {
 // delta0 >= 1e-5 (L_i + L_j) + 1e-12 (M_i + M_j),
 //   lb side: c B >= T_lb + delta0 + ph_i + ph_j   implies  B - ph_i - ph_j >= T_lb + delta(B)
 //   ub side: c B >= T_ub + delta0 - hd_i - hd_j   implies  B + hd_i + hd_j >= T_ub + delta(B)
-// i.e. cannot_improve with a (larger) tile-wide delta; squares are compared (both sides
-// non-negative) with directed rounding.
-__device__ __forceinline__ int stage1_box(const RowRec& a, float4 b0, float4 b1, float bph, float rlb, float rub) {
+// i.e. cannot_improve with a (larger) tile-wide delta. Everything is pre-scaled by 1 / c with
+// upward rounding: rlbc >= rlb / c and phc >= ph_j / c per row / s record (hdc <= hd_j / c),
+// so xs = rlbc + phc >= (rlb + ph_j) / c and ys = rubc - hdc >= (rub - hd_j) / c; both sides
+// hold iff max(xs, ys) <= 0 or g2 >= max(xs, ys)^2 (squares of non-negative values compared,
+// directed rounding; the FMAs round once, downwards, so g2 stays a lower bound).
+// kShapes = false when the voxel pair is known to meet the shape / range terms for every
+// facet pair (shapes_settled).
+template <bool kShapes>
+__device__ __forceinline__ int stage1_box(const RowRec& a, float4 b0, float4 b1, float2 pc, float rlbc, float rubc) {
     const float gx = fmaxf(0.f, fmaxf(__fsub_rd(b0.x, a.hi[0]), __fsub_rd(a.lo[0], b1.x)));
     const float gy = fmaxf(0.f, fmaxf(__fsub_rd(b0.y, a.hi[1]), __fsub_rd(a.lo[1], b1.y)));
     const float gz = fmaxf(0.f, fmaxf(__fsub_rd(b0.z, a.hi[2]), __fsub_rd(a.lo[2], b1.z)));
-    const float g2 = __fadd_rd(__fadd_rd(__fmul_rd(gx, gx), __fmul_rd(gy, gy)), __fmul_rd(gz, gz));
-    constexpr float kInvC = 1.0f / (1.0f - 1e-5f) * (1.0f + 0x1p-20f);
-    const float xl = __fadd_ru(rlb, bph);
-    const float yu = __fsub_ru(rub, b1.w);
-    const float xs = __fmul_ru(xl, kInvC), ys = __fmul_ru(yu, kInvC);
-    const bool lb_ok = xl <= 0.f || g2 >= __fmul_ru(xs, xs);
-    const bool ub_ok = yu <= 0.f || g2 >= __fmul_ru(ys, ys);
-    const float m = 1e3f * fminf(a.L, b0.w), f = 2.f * (a.L + b0.w);
-    const bool shapes = a.L >= 0.f && b0.w >= 0.f && g2 <= m * m;
-    const bool skip = lb_ok && ub_ok && shapes;
+    const float g2 = __fmaf_rd(gz, gz, __fmaf_rd(gy, gy, __fmul_rd(gx, gx)));
+    const float z = fmaxf(__fadd_ru(rlbc, pc.x), __fsub_ru(rubc, pc.y));
+    bool skip = z <= 0.f || g2 >= __fmul_ru(z, z);
+    if constexpr (kShapes) {
+        const float m = 1e3f * fminf(a.L, b0.w);
+        skip = skip && a.L >= 0.f && b0.w >= 0.f && g2 <= m * m;
+    }
+    const float f = 2.f * (a.L + b0.w);
     return skip ? (g2 > f * f ? 0 : 2) : 1;
+}
+
+// Stage 1 of one lane's row (r facet `a` in registers) against its s facets of the staged tile
+// (`bp`: the first, `step` floats apart; `iters` of them): bit t of `nmask` = pair t goes to
+// stage 2, of `fmask` = a near pair whose DP4A conditioning pre-test failed.
+template <bool kShapes>
+__device__ __forceinline__ void stage1_row(const RowRec& a, const float* bp, int step, int iters, float rlbc, float rubc,
+                                           uint32_t& nmask, uint32_t& fmask) {
+    uint32_t bit = 1u;
+#pragma unroll 1
+    for (int t = 0; t < iters; ++t, bp += step, bit <<= 1) {
+        const float4 b0 = *reinterpret_cast<const float4*>(bp), b1 = *reinterpret_cast<const float4*>(bp + 4);
+        const float2 pc = *reinterpret_cast<const float2*>(bp + 32);
+        const int sb = stage1_box<kShapes>(a, b0, b1, pc, rlbc, rubc);
+        const bool f = sb == 2 && !well_cond_q(a.q, *reinterpret_cast<const int4*>(bp + kQOff));
+        if (sb == 1 || f) nmask |= bit;
+        if (f) fmask |= bit;
+    }
+}
+
+// True if every facet pair (x, y) of the two segments meets the shape / range terms of the
+// stage-1 skip (both facets well shaped, box gap <= 1e3 min(L_x, L_y)): the segments are
+// well shaped and their union boxes' farthest distance (rounded up) is within 1e3 L_min.
+__device__ __forceinline__ bool shapes_settled(const SegAgg& a, const SegAgg& b) {
+    if (!a.ok || !b.ok) return false;
+    float m2 = 0.f;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        const float m = fmaxf(__fsub_ru(b.hi[d], a.lo[d]), __fsub_ru(a.hi[d], b.lo[d]));
+        m2 = __fadd_ru(m2, __fmul_ru(m, m));
+    }
+    const float lim = __fmul_rd(1e3f, fminf(a.Lmin, b.Lmin));
+    return m2 <= __fmul_rd(lim, lim);
 }
 
 // Conditioning decision of a near, box-skippable pair whose DP4A pre-test failed (the rest of

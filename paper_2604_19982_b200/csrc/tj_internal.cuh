@@ -204,17 +204,6 @@ struct RefineQueue {
     unsigned long long* count;
 };
 
-// Stage-2 candidate of the split screen (k_screen<true> -> k_sat): op (bit 31: the FP32
-// conditioning test is still due) and the two global facet record indices.
-struct SatRef {
-    uint32_t op, fr, fs;
-};
-struct SatQueue {
-    SatRef* items;
-    unsigned long long capacity;
-    unsigned long long* count; // [0] entries, [1] largest overflowing count
-};
-
 struct RefineQueueStore {
     DevBuf<PairRef> items;              // exact-evaluation queue
     DevBuf<unsigned long long> count; // [0] entries of the current pass, [1] largest overflowing count
@@ -222,17 +211,10 @@ struct RefineQueueStore {
     // level see at most `cap` slots until the first overflow grows the queue, so the
     // overflow -> grow -> re-run path runs on small inputs. 0 = no cap.
     uint64_t cap = 0;
-    DevBuf<SatRef> sat;                    // split screen: stage-2 candidates, grow-only
-    DevBuf<unsigned long long> sat_count;  // [0] entries of the current pass, [1] largest overflow
-    RefineQueueStore() : count(2), sat_count(2) { items.alloc(1u << 22); }
+    RefineQueueStore() : count(2) { items.alloc(1u << 22); }
     RefineQueue view() {
         const uint64_t n = cap && cap < items.n ? cap : items.n;
         return {items.p, (unsigned long long)n, count.p};
-    }
-    SatQueue sat_view() {
-        if (!sat.n) sat.alloc(1u << 24);
-        const uint64_t n = cap && cap < sat.n ? cap : sat.n;
-        return {sat.p, (unsigned long long)n, sat_count.p};
     }
     // before a level's passes: clears both queues' entry and overflow counts
     void reset(cudaStream_t st);

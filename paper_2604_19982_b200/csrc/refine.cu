@@ -568,6 +568,10 @@ __device__ __forceinline__ bool level_ub_settled(const RefineSource& src, int cu
     return hd2 > __fadd_ru(__fadd_ru(__fmul_ru(1e-5f, l2), __fmul_ru(1e-12f, m2)), 1e-30f);
 }
 
+// kBF: the stage-1 DP4A pre-test branch-free, two pairs per iteration (stage1_row); chosen for
+// decision mode, whose tested pairs are mostly near (separate kernels keep each one's code lean:
+// with both loop variants in one kernel config C lost 4 %).
+template <bool kBF>
 __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks)
     k_screen(RefineSource src, uint64_t vp_begin, uint64_t vp_end, const unsigned long long* __restrict__ op_lb_bits,
              const unsigned long long* __restrict__ op_ub_bits, int cull, RefineQueue q, unsigned long long* work,
@@ -773,10 +777,11 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks)
                             // pre-test failed (its FP32 test runs at the flush, 32 pairs at a time).
                             uint32_t nmask = 0, fmask = 0;
                             if (row_on) {
+                                const float* bp0 = sm.sc + jj * CS;
                                 if (shapes_ok)
-                                    stage1_row<false>(ar, sm.sc + jj * CS, P * CS, iters, rlbc, rubc, nmask, fmask);
+                                    stage1_row<false, kBF>(ar, bp0, P * CS, iters, rlbc, rubc, nmask, fmask);
                                 else
-                                    stage1_row<true>(ar, sm.sc + jj * CS, P * CS, iters, rlbc, rubc, nmask, fmask);
+                                    stage1_row<true, kBF>(ar, bp0, P * CS, iters, rlbc, rubc, nmask, fmask);
                             }
                             // compact the masks into the warp queue one entry per lane and round;
                             // stage 2 runs whenever 32 entries are queued (and on the rest after
@@ -959,7 +964,9 @@ void refine_pass(const RefineSource& src, uint64_t vp_begin, uint64_t vp_end, bo
         TJ_CUDA(cudaGetDevice(&dev));
         std::lock_guard<std::mutex> lk(mu);
         if (!done.count(dev)) {
-            TJ_CUDA(cudaFuncSetAttribute(k_screen, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            TJ_CUDA(cudaFuncSetAttribute(k_screen<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kScreenSmem));
+            TJ_CUDA(cudaFuncSetAttribute(k_screen<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kScreenSmem));
             done.insert(dev);
         }
@@ -980,8 +987,9 @@ void refine_pass(const RefineSource& src, uint64_t vp_begin, uint64_t vp_end, bo
         const int sgrid = warp_grid(vp_end - vp_begin, num_sms, kScreenBlocks, kScreenThreads / 32);
         const unsigned batch = screen_batch(src.mean_seg, vp_end - vp_begin, (uint64_t)sgrid * (kScreenThreads / 32));
         count_launch();
-        k_screen<<<sgrid, kScreenThreads, kScreenSmem, st>>>(src, vp_begin, vp_end, lb_bits, ub_bits, cull, qs.view(),
-                                                              work, counters, batch, hier_min_pairs());
+        auto* screen = cull == 2 ? k_screen<true> : k_screen<false>;
+        screen<<<sgrid, kScreenThreads, kScreenSmem, st>>>(src, vp_begin, vp_end, lb_bits, ub_bits, cull, qs.view(), work,
+                                                            counters, batch, hier_min_pairs());
         TJ_CUDA(cudaGetLastError());
     }
     count_launch();

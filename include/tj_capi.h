@@ -24,6 +24,10 @@
  *   tj_refine_loop     refine_loop              include/trijoin/refine.hpp:82-87,   src/refine.cpp:263-314
  *   tj_knn_prune       knn_prune_round / _to_fixpoint / knn_finalize
  *                                               include/trijoin/knn.hpp:30-50,      src/knn.cpp:19-118
+ *   tj_facet_hd_batch  compute_facet_hd         include/trijoin/mesh.hpp:65-66,     src/hausdorff.cpp:15-33
+ *   tj_facet_ph_batch  compute_facet_ph / the ph fill of build_lod_ladder
+ *                                               include/trijoin/mesh.hpp:71,        src/simplify.cpp:238-267
+ *   tj_voxelize_batch  voxelize                 include/trijoin/index.hpp:48,       src/voxelize.cpp:27-79
  *   tj_dataset_upload  (no reference analogue: PreparedDataset is host-resident there,
  *                       include/trijoin/index.hpp:15-36; here it is packed once into HBM)
  *
@@ -372,6 +376,29 @@ typedef struct tj_exhaustive_result {
 int tj_exhaustive_join(tj_ctx* ctx, const tj_mesh_set_view* R, const tj_mesh_set_view* S, int32_t type, double tau,
                        uint32_t k, tj_exhaustive_result* out);
 void tj_exhaustive_result_free(tj_exhaustive_result* res);
+
+/* ---- offline preprocessing, many meshes per call ----
+ * A mesh set: mesh m owns vertices [vert_off[m], vert_off[m+1]) of `verts` (3 doubles each) and
+ * facets [facet_off[m], facet_off[m+1]) of `facets` (3 mesh-local vertex ids each).
+ *
+ * tj_facet_hd_batch: compute_facet_hd(tri, original, grid) (src/hausdorff.cpp:15-27) of every
+ * query triangle q in [query_off[m], query_off[m+1]) (9 doubles each) against original mesh m:
+ * the max over the (grid+1)(grid+2)/2 barycentric samples of the distance to the mesh, plus
+ * hd_covering_radius. Bitwise equal to the reference (same BVH traversal, src/bvh.cpp:86-112).
+ * tj_facet_ph_batch: ph of every LOD facet l in [lod_off[m], lod_off[m+1]) (9 doubles each):
+ * the max over the original facets o of mesh m with ancestor[o] == l (LOD-local id) of the
+ * distance from o's vertices to facet l; 0 where no original maps to l.
+ * tj_voxelize_batch: voxelize(coarsest level of object o, k[o], seeds[o]) (src/voxelize.cpp:
+ * 27-79): k-means labels of every facet, relabelled contiguously. */
+int tj_facet_hd_batch(tj_ctx* ctx, uint32_t n_meshes, const uint64_t* vert_off, const double* verts,
+                      const uint64_t* facet_off, const uint32_t* facets, const uint64_t* query_off,
+                      const double* query_tris9, int32_t grid, double* hd_out);
+int tj_facet_ph_batch(tj_ctx* ctx, uint32_t n_meshes, const uint64_t* vert_off, const double* verts,
+                      const uint64_t* facet_off, const uint32_t* facets, const uint32_t* ancestor,
+                      const uint64_t* lod_off, const double* lod_tris9, double* ph_out);
+int tj_voxelize_batch(tj_ctx* ctx, uint32_t n_objects, const uint64_t* vert_off, const double* verts,
+                      const uint64_t* facet_off, const uint32_t* facets, const uint32_t* k, const uint64_t* seeds,
+                      uint32_t* labels_out);
 
 #ifdef __cplusplus
 }

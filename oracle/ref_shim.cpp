@@ -16,6 +16,8 @@
 #include "trijoin/geom.hpp"
 #include "trijoin/index.hpp"
 #include "trijoin/knn.hpp"
+#include "trijoin/mesh.hpp"
+#include "trijoin/bvh.hpp"
 #include "trijoin/refine.hpp"
 
 using namespace trijoin;
@@ -43,6 +45,15 @@ int guarded(F&& f) {
         return 3;
     }
 }
+Mesh mesh_from(const double* verts, uint64_t nv, const uint32_t* facets, uint64_t nf) {
+    Mesh m;
+    m.vertices.resize(nv);
+    for (uint64_t i = 0; i < nv; ++i) m.vertices[i] = {verts[3 * i], verts[3 * i + 1], verts[3 * i + 2]};
+    m.facets.resize(nf);
+    for (uint64_t f = 0; f < nf; ++f) m.facets[f] = {facets[3 * f], facets[3 * f + 1], facets[3 * f + 2]};
+    return m;
+}
+
 }  // namespace
 
 extern "C" {
@@ -264,6 +275,67 @@ int ref_join_timed_records(const char* r_path, const char* s_path, int type, dou
             }
             std::fclose(f);
         }
+    });
+}
+
+
+// ---- offline preprocessing ----
+// proj/src/simplify.cpp build_lod_ladder (incl. hd / ph, :229-251). Binary dump to out_path:
+//   u32 n_levels; per level: i32 level, u8 clamped, u64 nv, u64 nf, f64 verts[3 nv],
+//   u32 facets[3 nf], f64 hd[nf or 0 at level 100: u64 count first], f64 ph[same],
+//   u64 n_orig, u32 ancestor_of_original[n_orig]
+int ref_build_ladder(const double* verts, uint64_t nv, const uint32_t* facets, uint64_t nf, const int32_t* lods,
+                     uint32_t n_lods, int32_t hd_grid, const char* out_path) {
+    return guarded([&] {
+        const Mesh m = mesh_from(verts, nv, facets, nf);
+        const LodLadder L = build_lod_ladder(m, std::vector<int>(lods, lods + n_lods), hd_grid);
+        FILE* f = std::fopen(out_path, "wb");
+        if (!f) throw std::runtime_error("cannot write ladder dump");
+        auto w = [&](const void* p, size_t n) { std::fwrite(p, 1, n, f); };
+        const uint32_t nl = (uint32_t)L.levels.size();
+        w(&nl, 4);
+        for (const LodMesh& lod : L.levels) {
+            const int32_t lv = lod.level;
+            const uint8_t cl = lod.clamped ? 1 : 0;
+            const uint64_t lnv = lod.mesh.vertices.size(), lnf = lod.mesh.facets.size();
+            w(&lv, 4);
+            w(&cl, 1);
+            w(&lnv, 8);
+            w(&lnf, 8);
+            for (const Point3& v : lod.mesh.vertices) { const double t[3] = {v.x, v.y, v.z}; w(t, 24); }
+            for (const auto& t : lod.mesh.facets) w(t.data(), 12);
+            const uint64_t nh = lod.hd.size(), np = lod.ph.size();
+            w(&nh, 8);
+            w(lod.hd.data(), 8 * nh);
+            w(&np, 8);
+            w(lod.ph.data(), 8 * np);
+            const uint64_t na = lod.ancestor_of_original.size();
+            w(&na, 8);
+            w(lod.ancestor_of_original.data(), 4 * na);
+        }
+        std::fclose(f);
+    });
+}
+
+// proj/src/hausdorff.cpp:15-33 compute_facet_hd (Mesh overload) for n query triangles
+int ref_facet_hd(const double* verts, uint64_t nv, const uint32_t* facets, uint64_t nf, uint64_t n,
+                 const double* tris9, int32_t grid, double* out) {
+    return guarded([&] {
+        const Mesh m = mesh_from(verts, nv, facets, nf);
+        const TriBvh bvh(m);
+        for (uint64_t i = 0; i < n; ++i) out[i] = compute_facet_hd(tri_from(tris9 + 9 * i), bvh, grid);
+    });
+}
+
+// proj/src/voxelize.cpp:27-79 voxelize on a mesh given as its coarsest level
+int ref_voxelize(const double* verts, uint64_t nv, const uint32_t* facets, uint64_t nf, uint32_t k, uint64_t seed,
+                 uint32_t* labels) {
+    return guarded([&] {
+        LodMesh lod;
+        lod.level = 20;
+        lod.mesh = mesh_from(verts, nv, facets, nf);
+        const std::vector<uint32_t> l = voxelize(lod, k, seed);
+        std::memcpy(labels, l.data(), 4 * l.size());
     });
 }
 

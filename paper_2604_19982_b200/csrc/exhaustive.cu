@@ -190,7 +190,9 @@ __global__ void __launch_bounds__(kBoxThreads) k_knn_seed(const double* __restri
         for (uint32_t i = 0; i < k; ++i) seed_s[(uint64_t)r * k + i] = i < n ? id[i] : kNoObject;
 }
 
-__device__ __noinline__ double tri_tri_exh(uint32_t a, uint32_t b) { return tri_tri(a, b); }
+__device__ __noinline__ double tri_tri_exh(uint32_t a, uint32_t b) {
+    staged_read_barrier();
+    return tri_tri(a, b); }
 
 __device__ __forceinline__ double gap2(const double* a, const double* b) {
     double s = 0.0;

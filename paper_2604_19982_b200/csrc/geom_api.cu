@@ -41,8 +41,12 @@ __host__ __device__ constexpr int width_b(int op) {
 
 __device__ __forceinline__ V3 ld3(const double* p) { return {p[0], p[1], p[2]}; }
 
-__device__ __noinline__ double tri_tri_geo(uint32_t a, uint32_t b) { return tri_tri(a, b); }
-__device__ __noinline__ double point_tri_geo(const V3& p, uint32_t t) { return point_triangle_d2(p, t); }
+__device__ __noinline__ double tri_tri_geo(uint32_t a, uint32_t b) {
+    staged_read_barrier();
+    return tri_tri(a, b); }
+__device__ __noinline__ double point_tri_geo(const V3& p, uint32_t t) {
+    staged_read_barrier();
+    return point_triangle_d2(p, t); }
 
 __global__ void __launch_bounds__(kGeoThreads) k_geom(int op, uint64_t n, const double* __restrict__ a,
                                                       const double* __restrict__ b, double* __restrict__ out) {

@@ -105,6 +105,12 @@ __device__ __forceinline__ double point_dist(const double* a, const double* b) {
 // reference's own formula evaluated on the same inputs.
 constexpr int kFacetWords = 15;
 
+// Geometry entry points that read a staged record (lds below: asm loads the compiler does not
+// see as memory reads) begin with this barrier: it gives the out-of-line call a side effect,
+// so two calls on the same slot are never merged into one (e.g. by loop unrolling) although
+// the record was re-staged between them.
+__device__ __forceinline__ void staged_read_barrier() { asm volatile("" ::: "memory"); }
+
 __device__ __forceinline__ double lds(uint32_t a) {
     double v;
     asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));

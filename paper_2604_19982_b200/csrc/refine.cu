@@ -24,7 +24,7 @@ __device__ unsigned long long* g_dbg_op_tested = nullptr;
 #ifndef TJ_S1_UNROLL
 #define TJ_S1_UNROLL 1 // stage-1 inner loop unroll (B: 1 = 2 = 63.6 ms, 4: 67.4; C: 1: 191, 2: 198, 4: 216 ms)
 #endif
-constexpr int kS1Unroll = TJ_S1_UNROLL;
+
 constexpr int kScreenThreads = 256;
 constexpr int kScreenBlocks = 2;
 

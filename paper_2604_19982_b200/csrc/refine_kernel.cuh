@@ -588,6 +588,7 @@ __device__ __forceinline__ bool pierces_ref(const V3& p, const V3& q, const V3& 
 // returns (max(0, d - ph_r - ph_s), d + hd_r + hd_s)  (src/refine.cpp:77-79). Not inlined:
 // one copy of the geometry serves every call site (instruction-cache footprint).
 __device__ __noinline__ double2 eval_pair(uint32_t ra, uint32_t sb) {
+    staged_read_barrier();
     const double d = tri_tri(ra, sb);
     const double lbp = smax(0.0, TJ_SUB(TJ_SUB(d, ldw(ra, 10)), ldw(sb, 10)));
     const double ubp = TJ_ADD(TJ_ADD(d, ldw(ra, 9)), ldw(sb, 9));

@@ -142,6 +142,56 @@ class Capi:
                                           ptr(b), ptr(out)))
         return out
 
+    @staticmethod
+    def mesh_set(meshes):
+        """Pack [(verts f64[nv, 3], facets u32[nf, 3]), ...] into the C-ABI mesh-set arrays."""
+        vo = np.zeros(len(meshes) + 1, dtype=np.uint64)
+        fo = np.zeros(len(meshes) + 1, dtype=np.uint64)
+        for i, (v, f) in enumerate(meshes):
+            vo[i + 1] = vo[i] + len(v)
+            fo[i + 1] = fo[i] + len(f)
+        v = np.ascontiguousarray(np.concatenate([np.asarray(m[0], np.float64).reshape(-1, 3) for m in meshes]))
+        f = np.ascontiguousarray(np.concatenate([np.asarray(m[1], np.uint32).reshape(-1, 3) for m in meshes]))
+        return vo, v, fo, f
+
+    def facet_hd(self, meshes, queries, grid=8):
+        """tj_facet_hd_batch: queries[i] (f64[n, 9]) against original mesh meshes[i]."""
+        vo, v, fo, f = self.mesh_set(meshes)
+        qo = np.zeros(len(meshes) + 1, dtype=np.uint64)
+        for i, q in enumerate(queries):
+            qo[i + 1] = qo[i] + len(q)
+        q = np.ascontiguousarray(np.concatenate([np.asarray(x, np.float64).reshape(-1, 9) for x in queries]))
+        out = np.zeros(int(qo[-1]))
+        self.check(self.lib.tj_facet_hd_batch(self.ctx, ctypes.c_uint32(len(meshes)), ptr(vo, PU64), ptr(v),
+                                              ptr(fo, PU64), ptr(f, PU32), ptr(qo, PU64), ptr(q),
+                                              ctypes.c_int32(grid), ptr(out)))
+        return out
+
+    def facet_ph(self, meshes, lods, ancestors):
+        """tj_facet_ph_batch: ph of every facet of lods[i] (f64[n, 9]) from original mesh
+        meshes[i] with ancestors[i] (u32 per original facet)."""
+        vo, v, fo, f = self.mesh_set(meshes)
+        lo = np.zeros(len(meshes) + 1, dtype=np.uint64)
+        for i, q in enumerate(lods):
+            lo[i + 1] = lo[i] + len(q)
+        lt = np.ascontiguousarray(np.concatenate([np.asarray(x, np.float64).reshape(-1, 9) for x in lods]))
+        anc = np.ascontiguousarray(np.concatenate([np.asarray(a, np.uint32) for a in ancestors]))
+        out = np.zeros(int(lo[-1]))
+        self.check(self.lib.tj_facet_ph_batch(self.ctx, ctypes.c_uint32(len(meshes)), ptr(vo, PU64), ptr(v),
+                                              ptr(fo, PU64), ptr(f, PU32), ptr(anc, PU32), ptr(lo, PU64), ptr(lt),
+                                              ptr(out)))
+        return out
+
+    def voxelize(self, meshes, k, seeds):
+        """tj_voxelize_batch: labels per facet of each (coarsest-level) mesh."""
+        vo, v, fo, f = self.mesh_set(meshes)
+        kk = np.ascontiguousarray(k, dtype=np.uint32)
+        ss = np.ascontiguousarray(seeds, dtype=np.uint64)
+        out = np.zeros(int(fo[-1]), dtype=np.uint32)
+        self.check(self.lib.tj_voxelize_batch(self.ctx, ctypes.c_uint32(len(meshes)), ptr(vo, PU64), ptr(v),
+                                              ptr(fo, PU64), ptr(f, PU32), ptr(kk, PU32), ptr(ss, PU64), ptr(out, PU32)))
+        return [out[int(fo[i]):int(fo[i + 1])] for i in range(len(meshes))]
+
     def exhaustive(self, R, S, type="within", tau=0.0, k=1):
         """tj_exhaustive_join over level-100 triangle sets given as (tri_offsets u64[n+1],
         tris f64[m, 9]); S None = self-join. Returns a list of (r, s, d, rank)."""

@@ -125,6 +125,53 @@ __device__ __forceinline__ void gather_recs(const float4* __restrict__ box, cons
 }
 __device__ __forceinline__ void gather_wait() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
+// TMA bulk staging of a tile (-DTJ_TILE_BULK=1; off by default): lane k < n copies record k
+// with three cp.async.bulk transfers (48-B box part, 80-B geometry part, the facet's first 32 B
+// of FP64 coordinates = v0 + v1.x) completing on the warp's mbarrier (160 B of transactions per
+// record). Correct (the GPU suite passes with it) but measured slower than the per-lane
+// cp.async gather: config B 57.9 -> 71.1 ms, C 192.8 -> 224.5 ms — ~200 small bulk copies per
+// tile pair from 16 warps queue on the SM's TMA unit, where LDGSTS spreads them over the LSU.
+#ifndef TJ_TILE_BULK
+#define TJ_TILE_BULK 0
+#endif
+constexpr uint32_t kTileRecBytes = 48 + 80 + 32;
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void gather_bulk(const float4* __restrict__ box, const float4* __restrict__ geo,
+                                            const double* __restrict__ facets, uint64_t first, const uint16_t* list,
+                                            int n, float* dst, uint32_t bar) {
+    const int lane = threadIdx.x & 31;
+    if (lane < n) {
+        const uint64_t f = first + list[lane];
+        const uint32_t d = smem_addr(dst + lane * kCS);
+        bulk_g2s(d, box + f * kBoxF4, 16 * kBoxF4, bar);
+        bulk_g2s(d + 16 * kBoxF4, geo + f * kGeoF4, 16 * kGeoF4, bar);
+        bulk_g2s(d + 4 * kV0Off, facets + f * 12, 32, bar);
+    }
+}
+// Before the warp's lanes let the async proxy overwrite tiles they have read: all prior
+// (generic-proxy) accesses ordered before the copies; lane 0 then arms the barrier for `bytes`.
+__device__ __forceinline__ void tile_arm(uint32_t bar, uint32_t bytes) {
+    __syncwarp();
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    if ((threadIdx.x & 31) == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+    __syncwarp();
+}
+__device__ __forceinline__ void tile_wait(uint32_t bar, uint32_t& phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n TJ_TILE_WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra TJ_TILE_WAIT_%=;\n}\n" ::"r"(bar),
+        "r"(phase)
+        : "memory");
+    phase ^= 1u;
+}
+
 // Warp argmin (ties: lowest index) of (value, index).
 __device__ __forceinline__ void warp_argmin(float& v, uint32_t& idx) {
 #pragma unroll
@@ -582,6 +629,12 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks)
     SM& sm = reinterpret_cast<SM*>(smem_raw)[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
     if (lane < 5) sm.cnt[lane] = 0;
+    const uint32_t bar = smem_addr(&sm.bar);
+    uint32_t bar_phase = 0;
+    if (TJ_TILE_BULK && lane == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar) : "memory");
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    }
     __syncwarp();
     const bool ub_level_settled = level_ub_settled(src, cull);
     // The op thresholds of a voxel pair (decision mode, intersection with tau = 0: only "is the
@@ -702,19 +755,32 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks)
                                            hier, sm.sl, &sm.cnt[4]);
                 for (int rt0 = 0; nsl > 0 && rt0 < nrl; rt0 += kRT) {
                     const int rcnt = min(kRT, nrl - rt0);
-                    __syncwarp();
                     // the r tile and the first s tile in flight together
-                    gather_recs(src.r_box, src.r_geo, src.r_facets, d.r0 + rc0, sm.rl + rt0, rcnt, sm.rc);
-                    gather_recs(src.s_box, src.s_geo, src.s_facets, d.s0 + sc0, sm.sl, min(kST, nsl), sm.sc);
-                    gather_wait();
+                    if (TJ_TILE_BULK) {
+                        tile_arm(bar, kTileRecBytes * (uint32_t)(rcnt + min(kST, nsl)));
+                        gather_bulk(src.r_box, src.r_geo, src.r_facets, d.r0 + rc0, sm.rl + rt0, rcnt, sm.rc, bar);
+                        gather_bulk(src.s_box, src.s_geo, src.s_facets, d.s0 + sc0, sm.sl, min(kST, nsl), sm.sc, bar);
+                        tile_wait(bar, bar_phase);
+                    } else {
+                        __syncwarp();
+                        gather_recs(src.r_box, src.r_geo, src.r_facets, d.r0 + rc0, sm.rl + rt0, rcnt, sm.rc);
+                        gather_recs(src.s_box, src.s_geo, src.s_facets, d.s0 + sc0, sm.sl, min(kST, nsl), sm.sc);
+                        gather_wait();
+                    }
                     __syncwarp();
                     scale_s_tile(min(kST, nsl));
                     for (int st0 = 0; st0 < nsl; st0 += kST) {
                         const int scnt = min(kST, nsl - st0);
                         if (st0 > 0) {
-                            __syncwarp();
-                            gather_recs(src.s_box, src.s_geo, src.s_facets, d.s0 + sc0, sm.sl + st0, scnt, sm.sc);
-                            gather_wait();
+                            if (TJ_TILE_BULK) {
+                                tile_arm(bar, kTileRecBytes * (uint32_t)scnt);
+                                gather_bulk(src.s_box, src.s_geo, src.s_facets, d.s0 + sc0, sm.sl + st0, scnt, sm.sc, bar);
+                                tile_wait(bar, bar_phase);
+                            } else {
+                                __syncwarp();
+                                gather_recs(src.s_box, src.s_geo, src.s_facets, d.s0 + sc0, sm.sl + st0, scnt, sm.sc);
+                                gather_wait();
+                            }
                             __syncwarp();
                             scale_s_tile(scnt);
                         }

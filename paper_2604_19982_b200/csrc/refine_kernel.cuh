@@ -104,6 +104,7 @@ struct __align__(16) ScreenSmem {
     // the warp's counters (lane 0 writes; kept out of registers: the stage-1 loop is at the
     // register limit): tested, separating-axis tests, verified, voxel pairs skipped, dropped
     uint32_t cnt[5];
+    uint64_t bar; // the warp's tile mbarrier (TMA bulk staging)
 };
 
 __device__ __forceinline__ float rd(double x) { return __double2float_rd(x); }

@@ -872,11 +872,30 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks)
                                     if (lane < n) {
                                         const int e = sm.q[(qh + lane) & (kQueue - 1)];
                                         const int i = (e >> 5) & 31, j = e & 31;
-                                        go = !(e & 0x8000) || stage1_ill_fp32(sm.rc + i * kCS, sm.sc + j * kCS);
-                                        if (go) {
+                                        const float* ra = sm.rc + i * kCS;
+                                        const float* sb = sm.sc + j * kCS;
+                                        // a flagged entry is a near pair stage 1 found skippable by its box
+                                        // (so cannot_improve and the shape / range terms hold) whose DP4A
+                                        // pre-test failed: its ill-conditioned combinations only, and where
+                                        // the plane sides clear them all (sat_needed's first exit) no more
+                                        bool full = !(e & 0x8000);
+                                        if (!full) {
+                                            const int m = ill_mask_fp32(ra, sb);
+                                            if (m) {
+                                                go = true;
+                                                const double* va = reinterpret_cast<const double*>(ra + kV0Off);
+                                                const double* vb = reinterpret_cast<const double*>(sb + kV0Off);
+                                                const float off[3] = {(float)(vb[0] - va[0]), (float)(vb[1] - va[1]),
+                                                                      (float)(vb[2] - va[2])};
+                                                full = plane_clear(m, sat_frame(ra, sb, off), ra, sb) != 0;
+                                            }
+                                        } else {
+                                            go = true;
+                                        }
+                                        if (full) {
                                             fr = (uint32_t)(d.r0 + rc0 + sm.rl[rt0 + i]);
                                             fs = (uint32_t)(d.s0 + sc0 + sm.sl[st0 + j]);
-                                            const int r = sat_needed(sm.rc + i * kCS, sm.sc + j * kCS, src.r_facets + (size_t)fr * 12,
+                                            const int r = sat_needed(ra, sb, src.r_facets + (size_t)fr * 12,
                                                                      src.s_facets + (size_t)fs * 12, th);
                                             need = r & 1;
                                             ver = r >> 1;

@@ -425,21 +425,19 @@ __device__ __forceinline__ bool shapes_settled(const SegAgg& a, const SegAgg& b)
     return m2 <= __fmul_rd(lim, lim);
 }
 
-// Conditioning decision of a near, box-skippable pair whose DP4A pre-test failed (the rest of
-// skip_mask, FP32): true iff some edge / plane combination is ill conditioned (the pair must
-// go to stage 2).
-__device__ __forceinline__ bool stage1_ill_fp32(const float* as, const float* b) {
+// The ill-conditioned edge / plane combinations of a near, box-skippable pair whose DP4A
+// pre-test failed (FP32 dots, |cos| < 1e-3), as a mask in skip_mask's bit order: bit k = edge k of a vs the plane of b, bit 3 + k = edge k of b vs the
+// plane of a).
+__device__ __forceinline__ int ill_mask_fp32(const float* as, const float* b) {
     const float4 b2 = *reinterpret_cast<const float4*>(b + 8);
     const float4 b3 = *reinterpret_cast<const float4*>(b + 12), b4 = *reinterpret_cast<const float4*>(b + 16);
     const float b20 = b[20];
     const float4 a2 = *reinterpret_cast<const float4*>(as + 8), a3 = *reinterpret_cast<const float4*>(as + 12);
     const float4 a4 = *reinterpret_cast<const float4*>(as + 16);
     const float a20 = as[20];
-    bool ill = ill_cond(a3.x, a3.y, a3.z, b2.x, b2.y, b2.z) || ill_cond(a3.w, a4.x, a4.y, b2.x, b2.y, b2.z) ||
-               ill_cond(a4.z, a4.w, a20, b2.x, b2.y, b2.z);
-    ill = ill || ill_cond(b3.x, b3.y, b3.z, a2.x, a2.y, a2.z) || ill_cond(b3.w, b4.x, b4.y, a2.x, a2.y, a2.z) ||
-          ill_cond(b4.z, b4.w, b20, a2.x, a2.y, a2.z);
-    return ill;
+    return (int)ill_cond(a3.x, a3.y, a3.z, b2.x, b2.y, b2.z) | (int)ill_cond(a3.w, a4.x, a4.y, b2.x, b2.y, b2.z) << 1 |
+           (int)ill_cond(a4.z, a4.w, a20, b2.x, b2.y, b2.z) << 2 | (int)ill_cond(b3.x, b3.y, b3.z, a2.x, a2.y, a2.z) << 3 |
+           (int)ill_cond(b3.w, b4.x, b4.y, a2.x, a2.y, a2.z) << 4 | (int)ill_cond(b4.z, b4.w, b20, a2.x, a2.y, a2.z) << 5;
 }
 
 // Shape / range eligibility for a skip and the mask of ill-conditioned edge/plane

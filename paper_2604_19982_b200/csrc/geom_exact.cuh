@@ -145,10 +145,10 @@ __device__ __forceinline__ double point_segment_d2(const V3& p, const V3& a, con
     return vnorm2(vsub(p, vadd(a, vmul(d, t))));
 }
 
-// point_triangle_distance squared (src/geom.cpp:39-80); t = staged record.
-__device__ __forceinline__ double point_triangle_d2(const V3& p, uint32_t t) {
-    const V3 a = ldv(t, 0), b = ldv(t, 1), c = ldv(t, 2);
-    if (ldw(t, 14) != 0.0) {
+// point_triangle_distance squared (src/geom.cpp:39-80) of triangle (a, b, c) whose degenerate
+// flag (triangle_degenerate, src/geom.cpp:29-35) is `degen`.
+__device__ __forceinline__ double point_triangle_d2(const V3& p, const V3& a, const V3& b, const V3& c, bool degen) {
+    if (degen) {
         // std::min({psd(v0,v1), psd(v1,v2), psd(v2,v0)}) keeps the first smallest
         double m = point_segment_d2(p, a, b);
         const double m1 = point_segment_d2(p, b, c);
@@ -198,6 +198,10 @@ __device__ __forceinline__ double point_triangle_d2(const V3& p, uint32_t t) {
     if (reg == 1) x = b;
     if (reg == 3) x = c;
     return vnorm2(vsub(p, x));
+}
+// ... of a staged record t.
+__device__ __forceinline__ double point_triangle_d2(const V3& p, uint32_t t) {
+    return point_triangle_d2(p, ldv(t, 0), ldv(t, 1), ldv(t, 2), ldw(t, 14) != 0.0);
 }
 
 // segment_segment_distance squared (src/geom.cpp:82-113).

@@ -59,8 +59,9 @@ inline void build_node(HostBvh& h, const TriSoup& s, const std::vector<double>& 
     if (ey > ex) axis = 1;
     if (ez > (axis == 0 ? ex : ey)) axis = 2;
     const size_t mid = begin + (end - begin) / 2;
-    // the set of the first (end - begin) / 2 elements under the (centroid, id) total order
-    std::sort(h.order.begin() + begin, h.order.begin() + end, [&](uint32_t a, uint32_t b) {
+    // the set of the first (end - begin) / 2 elements under the (centroid, id) total order: any
+    // selection under a total order yields the same set as the reference's nth_element
+    std::nth_element(h.order.begin() + begin, h.order.begin() + mid, h.order.begin() + end, [&](uint32_t a, uint32_t b) {
         const double ca = cen[3 * (size_t)a + axis], cb = cen[3 * (size_t)b + axis];
         if (ca != cb) return ca < cb;
         return a < b;

@@ -96,15 +96,17 @@ double compute_facet_ph(uint32_t f_prime_id, const LodMesh& lod, const Mesh& ori
 
 void fill_ladder_paddings(std::span<LodLadder* const> ladders, std::span<const Mesh* const> originals, int hd_grid) {
     if (ladders.size() != originals.size()) throw std::invalid_argument("fill_ladder_paddings: size mismatch");
-    // one mesh-set entry per (ladder, coarse level): the original mesh, queried by that level's facets
-    MeshSet ms;
-    std::vector<uint64_t> qo{0};
+    // hd: one mesh-set entry per ladder (its original mesh, one tree), queried by the facets of
+    // all its coarse levels; ph: one entry per (ladder, coarse level) with that level's ancestors
+    MeshSet hd_set, ph_set;
+    std::vector<uint64_t> hq{0}, pq{0};
     std::vector<double> q;
     std::vector<uint32_t> anc;
-    std::vector<std::pair<size_t, size_t>> slots; // (ladder, level)
+    std::vector<std::pair<size_t, size_t>> slots; // (ladder, level) in query order
     for (size_t i = 0; i < ladders.size(); ++i) {
         LodLadder& L = *ladders[i];
         const Mesh& orig = *originals[i];
+        size_t coarse = 0;
         for (size_t li = 0; li < L.levels.size(); ++li) {
             LodMesh& lod = L.levels[li];
             const size_t nf = lod.mesh.facets.size();
@@ -117,26 +119,31 @@ void fill_ladder_paddings(std::span<LodLadder* const> ladders, std::span<const M
                 throw std::invalid_argument("fill_ladder_paddings: ancestor map does not match the original mesh");
             for (uint32_t a : lod.ancestor_of_original)
                 if (a >= nf) throw std::invalid_argument("fill_ladder_paddings: ancestor id out of range");
-            ms.add(orig);
             for (size_t f = 0; f < nf; ++f) push_tri(q, lod.mesh.triangle(f));
-            qo.push_back(qo.back() + nf);
+            ph_set.add(orig);
+            pq.push_back(pq.back() + nf);
             anc.insert(anc.end(), lod.ancestor_of_original.begin(), lod.ancestor_of_original.end());
             slots.emplace_back(i, li);
+            coarse += nf;
+        }
+        if (coarse) {
+            hd_set.add(orig);
+            hq.push_back(hq.back() + coarse);
         }
     }
     if (slots.empty()) return;
-    std::vector<double> hd(qo.back()), ph(qo.back());
+    std::vector<double> hd(pq.back()), ph(pq.back());
     tj_ctx* ctx = ctx0();
-    detail::check(tj_facet_hd_batch(ctx, ms.n(), ms.vo.data(), ms.v.data(), ms.fo.data(), ms.f.data(), qo.data(),
-                                    q.data(), hd_grid, hd.data()),
+    detail::check(tj_facet_hd_batch(ctx, hd_set.n(), hd_set.vo.data(), hd_set.v.data(), hd_set.fo.data(),
+                                    hd_set.f.data(), hq.data(), q.data(), hd_grid, hd.data()),
                   ctx);
-    detail::check(tj_facet_ph_batch(ctx, ms.n(), ms.vo.data(), ms.v.data(), ms.fo.data(), ms.f.data(), anc.data(),
-                                    qo.data(), q.data(), ph.data()),
+    detail::check(tj_facet_ph_batch(ctx, ph_set.n(), ph_set.vo.data(), ph_set.v.data(), ph_set.fo.data(),
+                                    ph_set.f.data(), anc.data(), pq.data(), q.data(), ph.data()),
                   ctx);
     for (size_t k = 0; k < slots.size(); ++k) {
         LodMesh& lod = ladders[slots[k].first]->levels[slots[k].second];
-        lod.hd.assign(hd.begin() + (ptrdiff_t)qo[k], hd.begin() + (ptrdiff_t)qo[k + 1]);
-        lod.ph.assign(ph.begin() + (ptrdiff_t)qo[k], ph.begin() + (ptrdiff_t)qo[k + 1]);
+        lod.hd.assign(hd.begin() + (ptrdiff_t)pq[k], hd.begin() + (ptrdiff_t)pq[k + 1]);
+        lod.ph.assign(ph.begin() + (ptrdiff_t)pq[k], ph.begin() + (ptrdiff_t)pq[k + 1]);
     }
 }
 

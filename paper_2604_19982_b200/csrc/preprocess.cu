@@ -14,6 +14,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -70,19 +72,9 @@ __device__ __forceinline__ BvhNode load_node(const BvhNode* __restrict__ nodes, 
     return n;
 }
 
-// The staged-record geometry reads shared memory through asm loads that the compiler cannot
-// see as memory accesses: records are stored with a "memory" clobber (so no store sinks below
-// the out-of-line call that reads them) and read inside that call (so loads of a previously
-// staged record in the reused slot are never merged with the new one's).
-__device__ __forceinline__ void sts_m(uint32_t a, double v) {
-    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
-}
-__device__ __noinline__ double pt_dist(const V3& p, uint32_t t) {
-    staged_read_barrier();
-    return TJ_SQRT(point_triangle_d2(p, t)); }
-
-// Exact records (geom_exact.cuh layout, kFacetWords doubles: the 9 coordinates, hd = ph = 0, the
-// edge lengths and the degenerate flag, as stage_exact stages them) of every leaf-ordered triangle.
+// Leaf-ordered triangles for the point queries: kTriWords doubles each (the 9 coordinates, the
+// triangle_degenerate flag, 2 pad), read straight into registers by the traversal.
+constexpr int kTriWords = 12;
 __global__ void k_stage_soup(const double* __restrict__ verts, const uint32_t* __restrict__ facets,
                              const uint32_t* __restrict__ order, const uint64_t* __restrict__ mesh_of_tri,
                              const uint64_t* __restrict__ vert_off, const uint64_t* __restrict__ facet_off,
@@ -100,26 +92,24 @@ __global__ void k_stage_soup(const double* __restrict__ verts, const uint32_t* _
             c[3 * k + 2] = v[3 * (size_t)vid + 2];
         }
         const V3 v0 = {c[0], c[1], c[2]}, v1 = {c[3], c[4], c[5]}, v2 = {c[6], c[7], c[8]};
-        double* r = recs + i * kFacetWords;
+        double* r = recs + i * kTriWords;
 #pragma unroll
         for (int k = 0; k < 9; ++k) r[k] = c[k];
-        r[9] = 0.0;
-        r[10] = 0.0;
-        r[11] = TJ_SQRT(vnorm2(vsub(v1, v0)));
-        r[12] = TJ_SQRT(vnorm2(vsub(v2, v1)));
-        r[13] = TJ_SQRT(vnorm2(vsub(v2, v0)));
-        r[14] = tri_degenerate(v0, v1, v2, nullptr, nullptr) ? 1.0 : 0.0;
+        r[9] = tri_degenerate(v0, v1, v2, nullptr, nullptr) ? 1.0 : 0.0;
+        r[10] = r[11] = 0.0;
     }
 }
 
-__device__ __forceinline__ void stage_copy(const double* __restrict__ g, uint32_t t) {
-#pragma unroll
-    for (int k = 0; k < kFacetWords; ++k) sts_m(t + 8u * k, __ldg(g + k));
+
+__device__ __forceinline__ double leaf_tri_distance(const V3& p, const double* __restrict__ r) {
+    const double2* r2 = reinterpret_cast<const double2*>(r);
+    const double2 x0 = __ldg(r2), x1 = __ldg(r2 + 1), x2 = __ldg(r2 + 2), x3 = __ldg(r2 + 3), x4 = __ldg(r2 + 4);
+    const V3 a = {x0.x, x0.y, x1.x}, b = {x1.y, x2.x, x2.y}, c = {x3.x, x3.y, x4.x};
+    return TJ_SQRT(point_triangle_d2(p, a, b, c, x4.y != 0.0));
 }
 
-// TriBvh::point_distance (src/bvh.cpp:86-112), the leaf triangles staged one at a time.
-__device__ double bvh_point_distance(const V3& p, const BvhNode* __restrict__ nodes, const double* __restrict__ recs,
-                                     uint32_t slot) {
+// TriBvh::point_distance (src/bvh.cpp:86-112).
+__device__ double bvh_point_distance(const V3& p, const BvhNode* __restrict__ nodes, const double* __restrict__ recs) {
     double best = __longlong_as_double(0x7ff0000000000000ll);
     uint32_t stack[64];
     int top = 0;
@@ -128,10 +118,7 @@ __device__ double bvh_point_distance(const V3& p, const BvhNode* __restrict__ no
         const BvhNode n = load_node(nodes, stack[--top]);
         if (point_box_distance(p, n) >= best) continue;
         if (n.count > 0) {
-            for (uint32_t i = 0; i < n.count; ++i) {
-                stage_copy(recs + (size_t)(n.left + i) * kFacetWords, slot);
-                best = smin(best, pt_dist(p, slot));
-            }
+            for (uint32_t i = 0; i < n.count; ++i) best = smin(best, leaf_tri_distance(p, recs + (size_t)(n.left + i) * kTriWords));
             continue;
         }
         const double dl = point_box_distance(p, load_node(nodes, n.left));
@@ -155,8 +142,6 @@ __global__ void __launch_bounds__(kPreThreads) k_facet_hd(const double* __restri
                                                           const BvhNode* __restrict__ nodes, const uint64_t* __restrict__ rec_off,
                                                           const double* __restrict__ recs,
                                                           unsigned long long* __restrict__ hd_bits) {
-    __shared__ double rec[kPreThreads][kFacetWords];
-    const uint32_t slot = static_cast<uint32_t>(__cvta_generic_to_shared(&rec[threadIdx.x][0]));
     const uint32_t ns = (uint32_t)((grid + 1) * (grid + 2) / 2);
     const double inv = TJ_DIV(1.0, (double)grid);
     const uint64_t total = nq * ns;
@@ -177,7 +162,7 @@ __global__ void __launch_bounds__(kPreThreads) k_facet_hd(const double* __restri
         const uint32_t m = q_mesh[q];
         const uint64_t n0 = node_off[m];
         double d = __longlong_as_double(0x7ff0000000000000ll);
-        if (node_off[m + 1] > n0) d = bvh_point_distance(p, nodes + n0, recs + rec_off[m] * kFacetWords, slot);
+        if (node_off[m + 1] > n0) d = bvh_point_distance(p, nodes + n0, recs + rec_off[m] * kTriWords);
         const unsigned long long b = (unsigned long long)__double_as_longlong(d);
         if (b > __ldcg(hd_bits + q)) atomicMax(hd_bits + q, b);
     }
@@ -207,30 +192,19 @@ __global__ void __launch_bounds__(kPreThreads) k_facet_ph(const double* __restri
                                                           const uint32_t* __restrict__ ancestor,
                                                           const uint64_t* __restrict__ lod_off, const double* __restrict__ lod_tris,
                                                           unsigned long long* __restrict__ ph_bits) {
-    __shared__ double rec[kPreThreads][kFacetWords];
-    const uint32_t slot = static_cast<uint32_t>(__cvta_generic_to_shared(&rec[threadIdx.x][0]));
     for (uint64_t o = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; o < n_orig; o += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t m = facet_mesh[o];
         const uint64_t lf = lod_off[m] + ancestor[o];
-        {
-            const double* c = lod_tris + 9 * lf;
-            const V3 v0 = {c[0], c[1], c[2]}, v1 = {c[3], c[4], c[5]}, v2 = {c[6], c[7], c[8]};
-#pragma unroll
-            for (int k = 0; k < 9; ++k) sts_m(slot + 8u * k, c[k]);
-            sts_m(slot + 72, 0.0);
-            sts_m(slot + 80, 0.0);
-            sts_m(slot + 88, TJ_SQRT(vnorm2(vsub(v1, v0))));
-            sts_m(slot + 96, TJ_SQRT(vnorm2(vsub(v2, v1))));
-            sts_m(slot + 104, TJ_SQRT(vnorm2(vsub(v2, v0))));
-            sts_m(slot + 112, tri_degenerate(v0, v1, v2, nullptr, nullptr) ? 1.0 : 0.0);
-        }
+        const double* c = lod_tris + 9 * lf;
+        const V3 t0 = {c[0], c[1], c[2]}, t1 = {c[3], c[4], c[5]}, t2 = {c[6], c[7], c[8]};
+        const bool degen = tri_degenerate(t0, t1, t2, nullptr, nullptr);
         const double* v = verts + 3 * vert_off[m];
         double best = 0.0;
 #pragma unroll 1
         for (int k = 0; k < 3; ++k) {
             const uint32_t vid = facets[3 * o + k];
             const V3 p = {v[3 * (size_t)vid], v[3 * (size_t)vid + 1], v[3 * (size_t)vid + 2]};
-            best = smax(best, pt_dist(p, slot));
+            best = smax(best, TJ_SQRT(point_triangle_d2(p, t0, t1, t2, degen)));
         }
         const unsigned long long b = (unsigned long long)__double_as_longlong(best);
         if (b > __ldcg(ph_bits + lf)) atomicMax(ph_bits + lf, b);
@@ -367,15 +341,27 @@ extern "C" int tj_facet_hd_batch(tj_ctx* ctx, uint32_t n_meshes, const uint64_t*
         std::vector<BvhNode> nodes;
         std::vector<uint32_t> order;
         std::vector<uint64_t> tri_mesh;
+        std::vector<HostBvh> trees(n_meshes);
+        {
+            std::atomic<uint32_t> next{0};
+            auto work = [&] {
+                for (uint32_t m; (m = next.fetch_add(1)) < n_meshes;)
+                    trees[m] = build_bvh(TriSoup{verts + 3 * vert_off[m], facets + 3 * facet_off[m]},
+                                         (uint32_t)(facet_off[m + 1] - facet_off[m]));
+            };
+            const unsigned nt = std::min<unsigned>(std::max(1u, std::thread::hardware_concurrency()), n_meshes);
+            std::vector<std::thread> pool;
+            for (unsigned t = 1; t < nt; ++t) pool.emplace_back(work);
+            work();
+            for (auto& t : pool) t.join();
+        }
         for (uint32_t m = 0; m < n_meshes; ++m) {
-            const TriSoup s{verts + 3 * vert_off[m], facets + 3 * facet_off[m]};
-            const uint32_t nf = (uint32_t)(facet_off[m + 1] - facet_off[m]);
-            HostBvh h = build_bvh(s, nf);
+            const HostBvh& h = trees[m];
             node_off[m] = nodes.size();
             rec_off[m] = order.size();
             nodes.insert(nodes.end(), h.nodes.begin(), h.nodes.end());
             order.insert(order.end(), h.order.begin(), h.order.end());
-            tri_mesh.insert(tri_mesh.end(), nf, (uint64_t)m);
+            tri_mesh.insert(tri_mesh.end(), h.order.size(), (uint64_t)m);
         }
         node_off[n_meshes] = nodes.size();
         rec_off[n_meshes] = order.size();
@@ -399,7 +385,7 @@ extern "C" int tj_facet_hd_batch(tj_ctx* ctx, uint32_t n_meshes, const uint64_t*
         to_dev(d_ro, rec_off.data(), rec_off.size(), st);
         to_dev(d_q, query_tris9, 9 * nq, st);
         to_dev(d_qm, q_mesh.data(), nq, st);
-        d_recs.alloc(std::max<size_t>(order.size() * kFacetWords, 1));
+        d_recs.alloc(std::max<size_t>(order.size() * kTriWords, 1));
         d_bits.alloc(nq);
         d_hd.alloc(nq);
         TJ_CUDA(cudaMemsetAsync(d_bits.p, 0, nq * sizeof(unsigned long long), st));

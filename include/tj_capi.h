@@ -225,6 +225,7 @@ typedef struct tj_level_mesh_view {
 
 #define TJ_LEVEL_PADS 1u   /* tj_dataset_finish_level: hd / ph were shipped */
 #define TJ_LEVEL_NARROW 2u /* tj_dataset_finish_level: tris16 / voxel_facets16 were shipped */
+#define TJ_LEVEL_PIECES 4u /* tj_dataset_finish_level: every object was finished by tj_dataset_finish_level_part */
 
 int tj_dataset_begin(tj_ctx* ctx, const tj_dataset_view* header, const uint64_t* const* vert_base,
                      const uint64_t* const* facet_base, tj_dataset** out);
@@ -241,6 +242,16 @@ int tj_dataset_put_level_part(tj_dataset* ds, uint32_t slot, const tj_level_mesh
                               uint64_t vert_end, uint64_t facet_begin, uint64_t facet_end, uint64_t entry_begin,
                               uint64_t entry_end);
 int tj_dataset_finish_level(tj_dataset* ds, uint32_t slot, uint32_t flags);
+/* Pieced levels (the last join level of R in run_join's e2e path): tj_dataset_set_pieced(slot)
+ * before the join starts; then per consecutive object range [obj_begin, obj_end) (covering the
+ * objects in order) its rows put with tj_dataset_put_level_part and tj_dataset_finish_level_part,
+ * which expands and derives those objects' voxels and lets a join refine the active voxel pairs
+ * of those queries while later pieces are still in flight; finally tj_dataset_finish_level(slot,
+ * flags | TJ_LEVEL_PIECES). Not for compact-resident datasets. Results are unchanged. */
+int tj_dataset_set_pieced(tj_dataset* ds, uint32_t slot);
+int tj_dataset_finish_level_part(tj_dataset* ds, uint32_t slot, uint32_t obj_begin, uint32_t obj_end, uint32_t flags);
+/* Host-blocks until level slot of ds is on the device (queued and its copies complete). */
+int tj_dataset_level_wait(tj_dataset* ds, uint32_t slot);
 int tj_dataset_sync(tj_dataset* ds);
 
 /* ---- host-side index loading (backs load_index, reference src/index_io.cpp:244-249) ----

@@ -181,10 +181,10 @@ __global__ void k_expand_level(const double* __restrict__ verts, const Id* __res
                                const Id* __restrict__ vf, const uint64_t* __restrict__ foff,
                                const uint32_t* __restrict__ vox_obj, const uint64_t* __restrict__ vb,
                                const uint64_t* __restrict__ fb, uint64_t n_voxels, double* __restrict__ out,
-                               int* __restrict__ err, const uint64_t* __restrict__ act) {
+                               int* __restrict__ err, const uint64_t* __restrict__ act, uint64_t v_begin = 0) {
     const int lane = threadIdx.x & 31;
     const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
-    for (uint64_t v = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); v < n_voxels; v += warps) {
+    for (uint64_t v = v_begin + blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); v < n_voxels; v += warps) {
         const uint64_t e0 = foff[v], e1 = foff[v + 1];
         // act (on-demand expansion of a compact-resident level): only the flagged voxels, packed
         uint64_t w0 = e0;
@@ -242,6 +242,9 @@ LevelGate::~LevelGate() {
     cudaSetDevice(device);
     for (cudaEvent_t e : ev)
         if (e) cudaEventDestroy(e);
+    for (auto& v : pieces)
+        for (auto& pe : v)
+            if (pe.second) cudaEventDestroy(pe.second);
     if (copy) cudaStreamDestroy(copy);
 }
 
@@ -280,6 +283,21 @@ double level_ready(const DatasetDev& d, int slot, cudaStream_t st) {
         throw Error(TJ_EINVAL, "join: level " + std::to_string(d.levels[slot]) + " of a streamed dataset was not delivered");
     TJ_CUDA(cudaStreamWaitEvent(st, g.ev[slot], 0));
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+bool level_pieced(const DatasetDev& d, int slot) {
+    return d.gate && slot >= 0 && (size_t)slot < d.gate->pieced.size() && d.gate->pieced[slot];
+}
+
+cudaEvent_t level_piece(const DatasetDev& d, int slot, size_t k, uint32_t* obj_end) {
+    LevelGate& g = *d.gate;
+    std::unique_lock<std::mutex> lk(g.mu);
+    g.cv.wait(lk, [&] { return g.pieces[slot].size() > k || g.state[slot] != LevelGate::kPending; });
+    if (g.state[slot] == LevelGate::kFailed)
+        throw Error(TJ_EINVAL, "join: level " + std::to_string(d.levels[slot]) + " of a streamed dataset was not delivered");
+    if (g.pieces[slot].size() <= k) return nullptr; // finished: every piece delivered
+    *obj_end = g.pieces[slot][k].first;
+    return g.pieces[slot][k].second;
 }
 
 void stream_sync(cudaStream_t st) {
@@ -450,6 +468,8 @@ int tj_dataset_begin_ex(tj_ctx* ctx, const tj_dataset_view* v, const uint64_t* c
         const uint32_t no = d.n_objects;
         gate->state.assign(v->n_levels, LevelGate::kPending);
         gate->ev.assign(v->n_levels, nullptr);
+        gate->pieced.assign(v->n_levels, 0);
+        gate->pieces.resize(v->n_levels);
         d.vert_base.resize(v->n_levels);
         d.facet_base.resize(v->n_levels);
         for (uint32_t li = 0; li < v->n_levels; ++li) {
@@ -581,7 +601,10 @@ int tj_dataset_finish_level(tj_dataset* ds, uint32_t slot, uint32_t flags) {
         const double* verts = reinterpret_cast<const double*>(base + L.verts);
         const double* hd = pads && nfac ? reinterpret_cast<const double*>(base + L.hd) : nullptr;
         const double* ph = pads && nfac ? reinterpret_cast<const double*>(base + L.ph) : nullptr;
-        if (d.n_voxels) {
+        const bool done = flags & TJ_LEVEL_PIECES; // expanded and derived piece by piece
+        if (done && (d.compact || g.pieces[slot].empty()))
+            throw Error(TJ_EINVAL, "tj_dataset_finish_level: TJ_LEVEL_PIECES without finished pieces");
+        if (d.n_voxels && !done) {
             const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((d.n_voxels + 7) / 8, (uint64_t)ctx->ws.num_sms * 16));
             count_launch();
             if (flags & TJ_LEVEL_NARROW)
@@ -598,7 +621,7 @@ int tj_dataset_finish_level(tj_dataset* ds, uint32_t slot, uint32_t flags) {
                                                           nullptr);
             TJ_CUDA(cudaGetLastError());
         }
-        if (!d.compact) derive_level(d, slot, ctx->ws.num_sms, g.copy);
+        if (!d.compact && !done) derive_level(d, slot, ctx->ws.num_sms, g.copy);
         TJ_CUDA(cudaEventRecord(g.ev[slot], g.copy));
     });
     {
@@ -608,6 +631,81 @@ int tj_dataset_finish_level(tj_dataset* ds, uint32_t slot, uint32_t flags) {
     g.cv.notify_all();
     if (rc != TJ_OK) set_ctx_error(ctx, tj_global_last_error());
     return rc;
+}
+
+int tj_dataset_set_pieced(tj_dataset* ds, uint32_t slot) {
+    if (!ds || !ds->d.gate || slot >= ds->d.levels.size() || ds->d.compact) return TJ_EINVAL;
+    std::lock_guard<std::mutex> lk(ds->d.gate->mu);
+    ds->d.gate->pieced[slot] = 1;
+    return TJ_OK;
+}
+
+int tj_dataset_finish_level_part(tj_dataset* ds, uint32_t slot, uint32_t obj_begin, uint32_t obj_end, uint32_t flags) {
+    if (!ds || !ds->d.gate || slot >= ds->d.levels.size()) return TJ_EINVAL;
+    LevelGate& g = *ds->d.gate;
+    tj_ctx* ctx = ds->ctx;
+    cudaEvent_t ev = nullptr;
+    const int rc = guarded(nullptr, [&] {
+        TJ_CUDA(cudaSetDevice(ctx->device));
+        AllocStreamScope scope(g.copy);
+        DatasetDev& d = ds->d;
+        if (d.compact || !g.pieced[slot]) throw Error(TJ_EINVAL, "tj_dataset_finish_level_part: level not set pieced");
+        const uint32_t prev = g.pieces[slot].empty() ? 0u : g.pieces[slot].back().first;
+        if (obj_begin != prev || obj_end < obj_begin || obj_end > d.n_objects)
+            throw Error(TJ_EINVAL, "tj_dataset_finish_level_part: pieces must cover the objects in order");
+        const uint64_t nvert = d.level_vertices[slot], nfac = d.level_facets[slot], used = d.level_entries[slot];
+        const StageLayout L = stage_layout(nvert, nfac, used);
+        unsigned char* base = d.stage.p;
+        const bool pads = flags & TJ_LEVEL_PADS;
+        const double* verts = reinterpret_cast<const double*>(base + L.verts);
+        const double* hd = pads && nfac ? reinterpret_cast<const double*>(base + L.hd) : nullptr;
+        const double* ph = pads && nfac ? reinterpret_cast<const double*>(base + L.ph) : nullptr;
+        const uint64_t v0 = d.voxel_offsets_h[obj_begin], v1 = d.voxel_offsets_h[obj_end];
+        if (v1 > v0) {
+            const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((v1 - v0 + 7) / 8, (uint64_t)ctx->ws.num_sms * 16));
+            count_launch();
+            if (flags & TJ_LEVEL_NARROW)
+                k_expand_level<<<grid, 256, 0, g.copy>>>(verts, reinterpret_cast<const uint16_t*>(base + L.tris), hd, ph,
+                                                          reinterpret_cast<const uint16_t*>(base + L.vf),
+                                                          d.facet_offsets[slot].p, d.vox_obj.p, d.vert_base[slot].p,
+                                                          d.facet_base[slot].p, v1, d.facets[slot].p, d.stream_err.p,
+                                                          nullptr, v0);
+            else
+                k_expand_level<<<grid, 256, 0, g.copy>>>(verts, reinterpret_cast<const uint32_t*>(base + L.tris), hd, ph,
+                                                          reinterpret_cast<const uint32_t*>(base + L.vf),
+                                                          d.facet_offsets[slot].p, d.vox_obj.p, d.vert_base[slot].p,
+                                                          d.facet_base[slot].p, v1, d.facets[slot].p, d.stream_err.p,
+                                                          nullptr, v0);
+            TJ_CUDA(cudaGetLastError());
+        }
+        derive_level_range(d, slot, v0, v1, g.pieces[slot].empty(), ctx->ws.num_sms, g.copy);
+        TJ_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        TJ_CUDA(cudaEventRecord(ev, g.copy));
+    });
+    {
+        std::lock_guard<std::mutex> lk(g.mu);
+        if (rc == TJ_OK)
+            g.pieces[slot].emplace_back(obj_end, ev);
+        else
+            g.state[slot] = LevelGate::kFailed;
+    }
+    g.cv.notify_all();
+    if (rc != TJ_OK) set_ctx_error(ctx, tj_global_last_error());
+    return rc;
+}
+
+int tj_dataset_level_wait(tj_dataset* ds, uint32_t slot) {
+    if (!ds || !ds->d.gate || slot >= ds->d.levels.size()) return TJ_EINVAL;
+    LevelGate& g = *ds->d.gate;
+    return guarded(nullptr, [&] {
+        {
+            std::unique_lock<std::mutex> lk(g.mu);
+            g.cv.wait(lk, [&] { return g.state[slot] != LevelGate::kPending; });
+            if (g.state[slot] == LevelGate::kFailed) throw Error(TJ_EINVAL, "tj_dataset_level_wait: level failed");
+        }
+        TJ_CUDA(cudaSetDevice(ds->ctx->device));
+        TJ_CUDA(cudaEventSynchronize(g.ev[slot]));
+    });
 }
 
 int tj_dataset_put_level(tj_dataset* ds, uint32_t slot, const tj_level_mesh_view* lv) {

@@ -534,9 +534,10 @@ std::unique_ptr<PackedLevel> pack_level(const PreparedDataset& dsf, const Packed
                 }
             }
         });
-        if (on_piece)
-            on_piece(*p, PieceRows{h.vert_base[li][lo], h.vert_base[li][hi], h.facet_base[li][lo], h.facet_base[li][hi],
-                                   fo[h.voxel_offsets[lo]], fo[h.voxel_offsets[hi]]});
+        const PieceRows rows{h.vert_base[li][lo], h.vert_base[li][hi], h.facet_base[li][lo], h.facet_base[li][hi],
+                             fo[h.voxel_offsets[lo]], fo[h.voxel_offsets[hi]], (uint32_t)lo, (uint32_t)hi};
+        p->pieces.push_back(rows);
+        if (on_piece) on_piece(*p, rows);
     }
     return p;
 }
@@ -1132,26 +1133,58 @@ void lease(SetLease& l, detail::JoinCache* cache, const std::string& key) {
 
 // Ships level slot `slot` of set (packing it first, in pieces that are shipped while the next
 // is packed, unless the set already holds it) to every dataset handle in dst.
+// $TRIJOIN_PIECED=1 ships R's last join level in object-range pieces after S's whole level, and
+// the join refines each piece's queries as it lands. Off by default: on config B the last
+// level's data is already on the device when the join reaches it (the join waits for LOD 20 /
+// 60 data instead), and shipping S's level first made the last level 2 ms later (e2e timelines,
+// TRIJOIN_DEBUG_TIMELINE). Results are identical either way (tests/test_gpu_join.py).
+bool pieced_last_level() {
+    const char* e = std::getenv("TRIJOIN_PIECED");
+    return e && *e == '1';
+}
+
+uint32_t level_flags(const detail::PackedLevel& l) {
+    return (l.zero_pads ? 0u : TJ_LEVEL_PADS) | (l.narrow ? TJ_LEVEL_NARROW : 0u);
+}
+
+// pieced: the level is finished piece by piece (tj_dataset_finish_level_part after each piece's
+// rows), so a join refines a piece's queries while later pieces are in flight.
 void feed_level(const PreparedDataset& D, detail::PackedSet& set, size_t slot, const std::vector<tj_dataset*>& dst,
                 const std::vector<tj_ctx*>& ctxs, ThreadPool& pool, JoinOutput& out, double& pack_ms,
-                std::mutex* stat_mu) {
+                std::mutex* stat_mu, bool pieced = false) {
     using Clock = std::chrono::steady_clock;
     if (set.levels.size() < D.lod_schedule.size()) set.levels.resize(D.lod_schedule.size());
     auto& lv = set.levels[slot];
     if (!lv) {
         const auto t0 = Clock::now();
         auto ship = [&](const detail::PackedLevel& l, const detail::PieceRows& rows) {
-            for (size_t g = 0; g < dst.size(); ++g)
+            for (size_t g = 0; g < dst.size(); ++g) {
                 detail::check(tj_dataset_put_level_part(dst[g], static_cast<uint32_t>(slot), &l.view, rows.vert_begin,
                                                         rows.vert_end, rows.facet_begin, rows.facet_end,
                                                         rows.entry_begin, rows.entry_end),
                               ctxs[g]);
+                if (pieced)
+                    detail::check(tj_dataset_finish_level_part(dst[g], static_cast<uint32_t>(slot), rows.obj_begin,
+                                                               rows.obj_end, level_flags(l)),
+                                  ctxs[g]);
+            }
         };
         lv = detail::pack_level(D, *set.h, slot, pool, kPackPieces, ship);
         const double ms = std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
         std::unique_lock<std::mutex> lk;
         if (stat_mu) lk = std::unique_lock<std::mutex>(*stat_mu);
         pack_ms += ms;
+    } else if (pieced) {
+        for (const detail::PieceRows& rows : lv->pieces)
+            for (size_t g = 0; g < dst.size(); ++g) {
+                detail::check(tj_dataset_put_level_part(dst[g], static_cast<uint32_t>(slot), &lv->view, rows.vert_begin,
+                                                        rows.vert_end, rows.facet_begin, rows.facet_end,
+                                                        rows.entry_begin, rows.entry_end),
+                              ctxs[g]);
+                detail::check(tj_dataset_finish_level_part(dst[g], static_cast<uint32_t>(slot), rows.obj_begin,
+                                                           rows.obj_end, level_flags(*lv)),
+                              ctxs[g]);
+            }
     } else {
         const uint64_t nv = set.h->n_vertices[slot], nf = set.h->n_facets[slot];
         const uint64_t ne = set.h->facet_offsets[slot].back();
@@ -1159,7 +1192,7 @@ void feed_level(const PreparedDataset& D, detail::PackedSet& set, size_t slot, c
             detail::check(tj_dataset_put_level_part(dst[g], static_cast<uint32_t>(slot), &lv->view, 0, nv, 0, nf, 0, ne),
                           ctxs[g]);
     }
-    const uint32_t flags = (lv->zero_pads ? 0u : TJ_LEVEL_PADS) | (lv->narrow ? TJ_LEVEL_NARROW : 0u);
+    const uint32_t flags = level_flags(*lv) | (pieced ? TJ_LEVEL_PIECES : 0u);
     for (size_t g = 0; g < dst.size(); ++g)
         detail::check(tj_dataset_finish_level(dst[g], static_cast<uint32_t>(slot), flags), ctxs[g]);
     std::unique_lock<std::mutex> lk;
@@ -1177,7 +1210,10 @@ void release_levels(tj_dataset* ds, const std::vector<char>& put) {
 
 JoinOutput run_join(const PreparedDataset& R, const PreparedDataset& S, const JoinSpec& spec, ThreadPool& pool,
                     const JoinTrace* trace) {
-    return detail::run_join_cached(R, S, spec, pool, trace, nullptr, nullptr);
+    pool.parallel_jobs(0, [](size_t) {}); // $TRIJOIN_POOL_CHECK: the caller's pool is intact
+    JoinOutput out = detail::run_join_cached(R, S, spec, pool, trace, nullptr, nullptr);
+    pool.parallel_jobs(0, [](size_t) {});
+    return out;
 }
 
 JoinOutput detail::run_join_cached(const PreparedDataset& R, const PreparedDataset& S, const JoinSpec& spec,
@@ -1315,6 +1351,11 @@ JoinOutput detail::run_join_cached(const PreparedDataset& R, const PreparedDatas
                 }
                 results[g].push_back(std::make_unique<detail::ResultHandle>());
                 detail::ResultHandle* res = results[g].back().get();
+                // the last join level of R in object-range pieces, after S's whole last level: the
+                // join refines each piece's queries while the later pieces are still in flight
+                const int r_last = slot_of(R, spec.lods.back()), s_last = slot_of(S, spec.lods.back());
+                const bool pieced = pieced_last_level() && !one_dataset && !compact && r_last >= 0 && s_last >= 0;
+                if (pieced) detail::check(tj_dataset_set_pieced(dr.p, static_cast<uint32_t>(r_last)), ctx);
                 std::exception_ptr je;
                 const auto td = Clock::now();
                 std::thread jt([&] {
@@ -1335,8 +1376,10 @@ JoinOutput detail::run_join_cached(const PreparedDataset& R, const PreparedDatas
                     for (uint32_t level : spec.lods) {
                         const int slot = slot_of(R, level);
                         if (slot < 0) continue; // the join reports the missing level
+                        const bool last = pieced && slot == r_last;
+                        if (last) detail::check(tj_dataset_level_wait(dsh[g].p, static_cast<uint32_t>(s_last)), ctxs[g]);
                         feed_level(R, *lz->set, static_cast<size_t>(slot), {dr.p}, {ctx}, pool, out, pack_ms,
-                                   &stat_mu);
+                                   &stat_mu, last);
                         put[slot] = 1;
                         if (G == 1 && w.chunks.size() == 1)
                             mark(std::string("R_lod") + std::to_string(level) + "_put");

@@ -98,22 +98,24 @@ struct PackedHeader {
     tj_dataset_view view{};
     uint64_t bytes() const; // H2D bytes of tj_dataset_begin
 };
+// Rows of one packed piece of a level: vertices, facets and voxel facet-id entries.
+struct PieceRows {
+    uint64_t vert_begin, vert_end, facet_begin, facet_end, entry_begin, entry_end;
+    uint32_t obj_begin, obj_end; // the piece's objects
+};
 struct PackedLevel {
     PinnedBuf verts, tris, hd, ph, vf; // tris / vf hold uint32 pairs per double slot
     bool zero_pads = false;            // every hd / ph of the level is +0: not shipped
     bool narrow = false;               // ids shipped as uint16 (every object < 65536 vertices / facets)
     uint64_t bytes = 0;                // H2D bytes of the level
     tj_level_mesh_view view{};
+    std::vector<PieceRows> pieces;     // the object-range pieces it was packed in (shipped alike when cached)
 };
 std::unique_ptr<PackedHeader> pack_header(const PreparedDataset& ds, ThreadPool& pool);
 // The same over objects [first, last) of ds (one R chunk of the out-of-core path).
 std::unique_ptr<PackedHeader> pack_header(const PreparedDataset& ds, size_t first, size_t last, ThreadPool& pool);
 // The same over the listed objects of ds (ascending global ids: one query shard).
 std::unique_ptr<PackedHeader> pack_header(const PreparedDataset& ds, std::vector<uint32_t> ids, ThreadPool& pool);
-// Rows of one packed piece of a level: vertices, facets and voxel facet-id entries.
-struct PieceRows {
-    uint64_t vert_begin, vert_end, facet_begin, facet_end, entry_begin, entry_end;
-};
 // Level slot li of the objects h was packed from. With pieces > 1 it is packed in that many
 // consecutive object ranges and on_piece(level, rows) runs after each (the caller ships the
 // rows while the next piece is packed).

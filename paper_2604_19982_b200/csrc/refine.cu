@@ -182,12 +182,15 @@ __device__ __forceinline__ void warp_argmin(float& v, uint32_t& idx) {
     }
 }
 
+// Records [0, n) of a level of n records, or with rng (voxel range [rng[0], rng[1]) of the CSR
+// foff) the records of those voxels only (a level arriving in object-range pieces).
 __global__ void k_prep(const double* __restrict__ facets, uint64_t n, float4* __restrict__ out, unsigned* agg,
-                       int zero_pad) {
+                       int zero_pad, const uint64_t* __restrict__ foff, uint64_t v_begin, uint64_t v_end) {
     float4* box = out;
     float4* geo = out + kBoxF4 * n;
     float hdmin = __int_as_float(0x7f800000), lmax = 0.f, mmax = 0.f;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i0 = foff ? foff[v_begin] : 0, i1 = foff ? foff[v_end] : n;
+    for (uint64_t i = i0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < i1; i += (uint64_t)gridDim.x * blockDim.x) {
         float r[kCS];
         make_screen(facets + i * 12, r);
         if (zero_pad) r[7] = r[11] = 0.f; // hd, ph
@@ -987,7 +990,7 @@ void refine_prep(const double* facets, uint64_t n, float4* out, unsigned* agg, i
     if (!n) return;
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, (uint64_t)num_sms * 16));
     count_launch();
-    k_prep<<<grid, 256, 0, st>>>(facets, n, out, agg, zero_pad);
+    k_prep<<<grid, 256, 0, st>>>(facets, n, out, agg, zero_pad, nullptr, 0, 0);
     TJ_CUDA(cudaGetLastError());
 }
 
@@ -1013,7 +1016,8 @@ __global__ void k_init_level_agg(unsigned* agg) {
     if (threadIdx.x < 3) agg[threadIdx.x] = threadIdx.x == 0 ? 0x7f800000u : 0u;
 }
 
-void derive_level(DatasetDev& d, uint32_t li, int num_sms, cudaStream_t st) {
+namespace {
+void derive_alloc(DatasetDev& d, uint32_t li, cudaStream_t st) {
     const uint64_t n = d.level_entries[li];
     if (d.screen.size() <= li) d.screen.resize(li + 1);
     if (d.seg.size() <= li) d.seg.resize(li + 1);
@@ -1022,9 +1026,30 @@ void derive_level(DatasetDev& d, uint32_t li, int num_sms, cudaStream_t st) {
     if (d.agg.n < 3 * d.levels.size()) d.agg.alloc(3 * d.levels.size());
     count_launch();
     k_init_level_agg<<<1, 32, 0, st>>>(d.agg.p + 3 * li);
-    refine_prep(d.facets[li].p, n, d.screen[li].p, d.agg.p + 3 * li, num_sms, st);
-    refine_seg_prep(d.screen[li].p, d.facet_offsets[li].p, d.n_voxels, d.seg[li].p, num_sms, st);
     d.bytes += n * kScreenRecF4 * 16 + 3 * d.n_voxels * 16;
+}
+} // namespace
+
+void derive_level(DatasetDev& d, uint32_t li, int num_sms, cudaStream_t st) {
+    derive_alloc(d, li, st);
+    refine_prep(d.facets[li].p, d.level_entries[li], d.screen[li].p, d.agg.p + 3 * li, num_sms, st);
+    refine_seg_prep(d.screen[li].p, d.facet_offsets[li].p, d.n_voxels, d.seg[li].p, num_sms, st);
+}
+
+void derive_level_range(DatasetDev& d, uint32_t li, uint64_t v_begin, uint64_t v_end, bool first, int num_sms,
+                        cudaStream_t st) {
+    if (first) derive_alloc(d, li, st);
+    if (v_end <= v_begin) return;
+    const uint64_t n = d.level_entries[li];
+    const uint64_t per = n / std::max<uint64_t>(d.n_voxels, 1) + 1; // records per voxel, for the grid size
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(((v_end - v_begin) * per + 255) / 256,
+                                                                    (uint64_t)num_sms * 16));
+    count_launch();
+    k_prep<<<grid, 256, 0, st>>>(d.facets[li].p, n, d.screen[li].p, d.agg.p + 3 * li, 0, d.facet_offsets[li].p,
+                                 v_begin, v_end);
+    TJ_CUDA(cudaGetLastError());
+    refine_seg_prep(d.screen[li].p, d.facet_offsets[li].p + v_begin, v_end - v_begin, d.seg[li].p + 3 * v_begin,
+                    num_sms, st);
 }
 
 void refine_seg_prep(const float4* box, const uint64_t* foff, uint64_t n_voxels, float4* seg, int num_sms,

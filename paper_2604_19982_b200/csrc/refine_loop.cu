@@ -19,6 +19,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 
 #include "filter.cuh"
 #include "scan.cuh"
@@ -288,6 +289,25 @@ uint64_t compact_active(Workspace& ws, const CandDevStore& cs, DevBuf<ActiveVpDe
     return h;
 }
 
+// First active voxel pair (op order) whose op belongs to a query >= obj (ops are query-major:
+// r2op[r] = the first op of query r).
+__global__ void k_active_lower_bound(const ActiveVpDev* __restrict__ active, uint64_t n, const uint64_t* __restrict__ r2op,
+                                     uint32_t nq, uint32_t obj, uint64_t* out) {
+    if (threadIdx.x || blockIdx.x) return;
+    if (obj >= nq) {
+        *out = n;
+        return;
+    }
+    const uint64_t op = r2op[obj];
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint64_t mid = lo + (hi - lo) / 2;
+        if (active[mid].op < op) lo = mid + 1;
+        else hi = mid;
+    }
+    *out = lo;
+}
+
 RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetDev& S, CandDevStore& cs,
                               DevBuf<ActiveVpDev>& active, uint64_t n_active, const tj_join_spec& spec, bool knn,
                               double tau, bool decision, DevError* err, TraceSink* trace, cudaStream_t st) {
@@ -296,6 +316,7 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
     const uint64_t n = cs.n;
     DevBuf<unsigned long long> lbb(std::max<uint64_t>(n, 1)), ubb(std::max<uint64_t>(n, 1));
     DevBuf<unsigned long long> counters(kNumCounters), work(1), dbg;
+    DevBuf<uint64_t> piece_b(1);
     Clock::time_point tdbg[4];
     static const bool dbg_timing = std::getenv("TRIJOIN_DEBUG_TIMING") != nullptr;
     if (const char* e = std::getenv("TRIJOIN_DEBUG_OPSTATS"); e && *e && *e != '0') dbg.alloc(std::max<uint64_t>(n, 1));
@@ -306,6 +327,18 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
     cudaEvent_t e0, e1;
     TJ_CUDA(cudaEventCreate(&e0));
     TJ_CUDA(cudaEventCreate(&e1));
+    // $TRIJOIN_DEBUG_TIMELINE: per level, device time the join stream waited for the level's data
+    // (streamed datasets) and spent on it, printed to stderr (diagnostics)
+    static const bool dbg_tl = std::getenv("TRIJOIN_DEBUG_TIMELINE") != nullptr;
+    std::vector<cudaEvent_t> tl_ev;
+    auto tl_mark = [&] {
+        if (!dbg_tl) return;
+        cudaEvent_t e;
+        TJ_CUDA(cudaEventCreate(&e));
+        TJ_CUDA(cudaEventRecord(e, st));
+        tl_ev.push_back(e);
+    };
+    tl_mark();
     const unsigned long long kInfBits = 0x7ff0000000000000ull;
     const uint64_t launch = std::max<uint64_t>(spec.refine_chunk, 1ull << 24);
     uint64_t test_queue_cap = 0;
@@ -320,8 +353,14 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
             ls.level = level;
             ls.vps = n_active;
             // streamed datasets: this level's facets may still be in flight
-            ls.wait_ms = level_ready(R, sr, st);
+            tl_mark(); // level start (previous level done)
+            // R's level arriving in object-range pieces (run_join's last level): S whole first,
+            // then each query range's voxel pairs as soon as its piece is on the device
+            const bool mat = R.compact || S.compact;
+            const bool pieced = !mat && &S != &R && level_pieced(R, sr);
+            ls.wait_ms = pieced ? 0.0 : level_ready(R, sr, st);
             if (&S != &R) ls.wait_ms += level_ready(S, ss, st);
+            tl_mark(); // this level's data on the device
             RefineSource src{};
             src.active = active.p;
             src.exact_mask = decision ? tripwire_mask() : 0u;
@@ -352,8 +391,8 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
                 count_launch();
                 k_copy_agg<<<1, 32, 0, st>>>(rs.agg, ss_.agg, ws.level_agg.p);
             };
-            const bool mat = R.compact || S.compact;
             if (!mat) bind(resident_side(R, sr), resident_side(S, ss));
+            if (pieced) src.agg = nullptr; // R's level aggregates are complete only after its last piece
             // 0: every facet pair; 1: exact-preserving culling; 2: decision-mode culling
             const int cull = (spec.flags & TJ_FLAG_NO_CULL) ? 0 : decision ? 2 : 1;
             unsigned long long hc[kNumCounters];
@@ -373,7 +412,33 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
                 k_facet_pairs<<<grid_for(n_active, 256, ws.num_sms), 256, 0, st>>>(
                     active.p, n_active, R.facet_offsets[sr].p, S.facet_offsets[ss].p, counters.p + 2);
                 TJ_CUDA(cudaEventRecord(e0, st));
-                if (!mat) {
+                if (pieced) {
+                    // per piece: its queries' voxel pairs, seeds then screens (an op's voxel
+                    // pairs all belong to its query, hence to one piece)
+                    uint64_t a = 0;
+                    for (size_t k = 0;; ++k) {
+                        uint32_t obj_end = 0;
+                        const auto tw = Clock::now();
+                        const cudaEvent_t pev = level_piece(R, sr, k, &obj_end);
+                        ls.wait_ms += std::chrono::duration<double, std::milli>(Clock::now() - tw).count();
+                        if (!pev) break;
+                        TJ_CUDA(cudaStreamWaitEvent(st, pev, 0));
+                        count_launch();
+                        k_active_lower_bound<<<1, 32, 0, st>>>(active.p, n_active, cs.r2op.p, cs.nq, obj_end, piece_b.p);
+                        uint64_t b = 0;
+                        TJ_CUDA(cudaMemcpyAsync(&b, piece_b.p, 8, cudaMemcpyDeviceToHost, st));
+                        stream_sync(st);
+                        for (uint64_t c0 = a; cull && c0 < b; c0 += launch)
+                            refine_pass(src, c0, std::min(b, c0 + launch), true, lbb.p, ubb.p, cull, queue, work.p,
+                                        counters.p, ws.num_sms, st);
+                        for (uint64_t c0 = a; c0 < b; c0 += launch)
+                            refine_pass(src, c0, std::min(b, c0 + launch), false, lbb.p, ubb.p, cull, queue, work.p,
+                                        counters.p, ws.num_sms, st);
+                        a = b;
+                    }
+                    if (a != n_active) throw Error(TJ_EINVAL, "join: the pieces of a level do not cover its queries");
+                    level_ready(R, sr, st);
+                } else if (!mat) {
                     // seeds for every voxel pair first (op thresholds), then the screened passes
                     if (cull)
                         for (uint64_t c0 = 0; c0 < n_active; c0 += launch)
@@ -475,6 +540,20 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    if (dbg_tl && !tl_ev.empty()) {
+        tl_mark();
+        TJ_CUDA(cudaEventSynchronize(tl_ev.back()));
+        std::string line = "[timeline] refine from t0 (ms):";
+        for (size_t i = 1; i < tl_ev.size(); ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, tl_ev[0], tl_ev[i]);
+            char b[32];
+            std::snprintf(b, sizeof(b), " %.2f", ms);
+            line += b;
+        }
+        std::fprintf(stderr, "%s\n", line.c_str());
+        for (cudaEvent_t e : tl_ev) cudaEventDestroy(e);
+    }
     return out;
 }
 

@@ -84,6 +84,10 @@ struct LevelGate {
     std::condition_variable cv;
     std::vector<int> state;
     std::vector<cudaEvent_t> ev;
+    // levels shipped in object-range pieces (tj_dataset_set_pieced): per slot the pieces
+    // finished so far, (end object, event after its expansion and derivation), in order
+    std::vector<char> pieced;
+    std::vector<std::vector<std::pair<uint32_t, cudaEvent_t>>> pieces;
     cudaStream_t copy = nullptr;
     int device = 0;
     ~LevelGate();
@@ -133,10 +137,20 @@ void expand_compact_level(const DatasetDev& d, uint32_t slot, const uint64_t* ac
 
 // Derived screening data of level slot li of d (facets already resident), on stream st.
 void derive_level(DatasetDev& d, uint32_t li, int num_sms, cudaStream_t st);
+// The same for the voxels [v_begin, v_end) of a level arriving in object-range pieces (first:
+// the level's first piece: allocates and resets the level aggregates, complete only once every
+// piece is derived).
+void derive_level_range(DatasetDev& d, uint32_t li, uint64_t v_begin, uint64_t v_end, bool first, int num_sms,
+                        cudaStream_t st);
 
 // Makes `st` wait until level slot `slot` of `d` is resident (no-op for uploaded datasets);
 // returns the host milliseconds spent blocked waiting for the level to be queued.
 double level_ready(const DatasetDev& d, int slot, cudaStream_t st);
+// Pieced levels: whether slot arrives in object-range pieces, and piece k's end object and
+// completion event (host-blocks until it is finished; nullptr once the level is complete and
+// every piece was returned).
+bool level_pieced(const DatasetDev& d, int slot);
+cudaEvent_t level_piece(const DatasetDev& d, int slot, size_t k, uint32_t* obj_end);
 
 // Active voxel pair during refinement: candidate op + global voxel ids.
 struct ActiveVpDev {

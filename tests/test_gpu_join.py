@@ -85,6 +85,20 @@ def test_out_of_core_r_chunks(monkeypatch, env, j):
         assert b["r_chunks"] > 1 or (b["residency"] == "compact" and "TRIJOIN_COMPACT" not in env)
 
 
+@pytest.mark.parametrize("j", [j for j in JOINS if j["s"]], ids=tjtest.join_id)
+def test_pieced_last_level(monkeypatch, j):
+    """R's last join level shipped in object-range pieces (TRIJOIN_PIECED=1: tj_dataset_set_pieced
+    / tj_dataset_finish_level_part), the join refining each piece's queries as it lands: records
+    and every stage counter equal the reference's."""
+    import paper_2604_19982_b200 as tj
+    monkeypatch.setenv("TRIJOIN_PIECED", "1")
+    r, s = _paths(j)
+    out = tj.join(r, s, **j["kwargs"])
+    assert out["records"] == j["records"]
+    stages = [{k: v for k, v in st.items() if k != "wall_ms"} for st in out["stats"]["stages"]]
+    assert stages == j["stages"]
+
+
 @pytest.mark.parametrize("j", [j for j in JOINS if j["r"] in ("nuclei60", "spheres80a")], ids=tjtest.join_id)
 def test_process_shards_partition_the_queries(monkeypatch, j):
     """One process per GPU (bench.py under torchrun): TRIJOIN_PROCESS_SHARD=i/n joins the

@@ -348,8 +348,15 @@ def main():
     tested = float(sum(l["tested"] for l in outs[-1]["levels"]))
     screened = float(sum(l["screened"] for l in outs[-1]["levels"]))
     kernel_ms = float(np.mean([sum(l["kernel_ms"] for l in o["levels"]) for o in outs]))
-    stats = torch.tensor([elapsed_ms, pairs, fp, evaluated, tested, kernel_ms, screened], dtype=torch.float64,
-                         device=dev)
+    # the dominant kernel (k_screen): its launches' CUDA-event time, and its largest launch (the
+    # last level's) alone
+    screen_ms = float(np.mean([sum(l.get("screen_ms", 0.0) for l in o["levels"]) for o in outs]))
+    top_lv = max(outs[-1]["levels"], key=lambda l: l.get("screen_ms", 0.0))
+    top_ms = float(np.mean([[l for l in o["levels"] if l["level"] == top_lv["level"]][0].get("screen_ms", 0.0)
+                            for o in outs]))
+    top_tested = float(top_lv["tested"])
+    stats = torch.tensor([elapsed_ms, pairs, fp, evaluated, tested, kernel_ms, screened, screen_ms, top_ms,
+                          top_tested], dtype=torch.float64, device=dev)
     if world > 1:
         mx = stats.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
@@ -358,6 +365,7 @@ def main():
         elapsed_ms, kernel_ms = float(mx[0]), float(mx[5])
         pairs, fp, evaluated, tested = (float(sm[i]) for i in range(1, 5))
         screened = float(sm[6])
+        screen_ms, top_ms, top_tested = float(mx[7]), float(mx[8]), float(sm[9])
     ms_per_step = elapsed_ms / a.steps
     value = pairs / (ms_per_step / 1e3)
 
@@ -369,11 +377,22 @@ def main():
     b_achieved = b_flop / (kernel_ms / 1e3) / 1e12 / max(world, 1)
     brute_peak_pairs = fp32_peak * 1e12 / FLOP_PER_PAIR  # every reference facet pair through tri_tri at FP32 peak
     traffic, traffic_src = ncu_traffic(a.config)
-    roofline = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
-                "frac": achieved / fp32_peak, "traffic": traffic, "traffic_source": traffic_src,
-                "kernel": "refinement kernels k_seed + k_screen + k_eval (all LOD levels, CUDA events on their stream)",
-                "flop_model": f"SURVEY 8(d): {FLOP_PER_PAIR:g} x exact FP64 evaluations + {FLOP_PER_TEST:g} x box "
-                              "tests (both counted on the device)",
+    # SURVEY 8(d) for the dominant kernel k_screen: 20 FLOP per box test it runs (counted on the
+    # device) / its launches' CUDA-event time (the exact FP64 evaluations are k_eval's work)
+    s_achieved = tested * FLOP_PER_TEST / (screen_ms / 1e3) / 1e12 / max(world, 1) if screen_ms else None
+    t_achieved = top_tested * FLOP_PER_TEST / (top_ms / 1e3) / 1e12 / max(world, 1) if top_ms else None
+    roofline = {"bound": "fp32", "achieved": s_achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                "frac": s_achieved / fp32_peak if s_achieved else None, "traffic": traffic,
+                "traffic_source": traffic_src,
+                "kernel": f"k_screen (the dominant kernel: {screen_ms:.1f} of {elapsed_ms / a.steps:.1f} ms per join; "
+                          "all its launches in the timed region, CUDA events on its stream)",
+                "flop_model": f"SURVEY 8(d): {FLOP_PER_TEST:g} FLOP per box test (counted on the device)",
+                "largest_launch": {"level": top_lv["level"], "ms": top_ms, "box_tests": top_tested,
+                                   "achieved": t_achieved, "frac": t_achieved / fp32_peak if t_achieved else None},
+                "all_refinement": {"kernels": "k_seed + k_screen + k_eval, all levels", "achieved": achieved,
+                                   "frac": achieved / fp32_peak, "kernel_ms": kernel_ms,
+                                   "flop_model": f"{FLOP_PER_PAIR:g} x exact FP64 evaluations + {FLOP_PER_TEST:g} x "
+                                                 "box tests"},
                 "builder_model": {"achieved": b_achieved, "frac": b_achieved / fp32_peak,
                                   "flop_model": f"{B_FLOP_PER_TEST:g} x box tests + {B_FLOP_PER_SAT:g} x "
                                                 f"separating-axis tests + {FLOP_PER_PAIR:g} x exact evaluations"},

@@ -164,6 +164,7 @@ typedef struct tj_join_result {
     int32_t decision_mode;                       /* 1: refined in decision mode (TJ_FLAG_EXACT_INTERVALS) */
     uint32_t queue_reruns;                       /* levels re-run after an exact-queue overflow */
     uint64_t mat_chunks;                         /* compact-resident datasets: level expansions (chunks) */
+    double level_screen_ms[TJ_MAX_LODS];         /* the screen kernel's launches only (CUDA events) */
 } tj_join_result;
 
 /* ---- context ---- */

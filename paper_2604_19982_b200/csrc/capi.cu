@@ -884,6 +884,7 @@ int tj_join(tj_ctx* ctx, const tj_dataset* Rh, const tj_dataset* Sh, const tj_jo
             out->level_facets_dropped[i] = ro.levels[i].facets_dropped;
             out->level_ms[i] = ro.levels[i].ms;
             out->level_kernel_ms[i] = ro.levels[i].kernel_ms;
+            out->level_screen_ms[i] = ro.levels[i].screen_ms;
             out->level_wait_ms[i] = ro.levels[i].wait_ms;
         }
         out->refine_chunks = ro.chunks;

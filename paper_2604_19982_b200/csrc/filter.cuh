@@ -158,6 +158,7 @@ struct LevelStats {
     uint32_t level;
     uint64_t vps, facet_pairs, evaluated, tested, screened, verified, vps_skipped, facets_dropped;
     double ms, kernel_ms, wait_ms;
+    double screen_ms = 0.0; // k_screen launches only (CUDA events)
 };
 struct RefineLoopOut {
     std::vector<LevelStats> levels;

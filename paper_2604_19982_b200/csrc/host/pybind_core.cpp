@@ -283,6 +283,7 @@ public:
             l["facets_dropped"] = r.level_facets_dropped[i];
             l["ms"] = r.level_ms[i];
             l["kernel_ms"] = r.level_kernel_ms[i];
+            l["screen_ms"] = r.level_screen_ms[i];
             levels.append(l);
         }
         d["levels"] = levels;

@@ -1063,7 +1063,7 @@ void refine_seg_prep(const float4* box, const uint64_t* foff, uint64_t n_voxels,
 
 void refine_pass(const RefineSource& src, uint64_t vp_begin, uint64_t vp_end, bool seed, unsigned long long* lb_bits,
                  unsigned long long* ub_bits, int cull, RefineQueueStore& qs, unsigned long long* work,
-                 unsigned long long* counters, int num_sms, cudaStream_t st) {
+                 unsigned long long* counters, int num_sms, cudaStream_t st, cudaEvent_t* screen_ev) {
     if (vp_end <= vp_begin) return;
     // the dynamic shared-memory opt-in is per device: set once per device this process uses
     // (several host threads may drive several GPUs, run_join's shard threads)
@@ -1098,8 +1098,10 @@ void refine_pass(const RefineSource& src, uint64_t vp_begin, uint64_t vp_end, bo
         const unsigned batch = screen_batch(src.mean_seg, vp_end - vp_begin, (uint64_t)sgrid * (kScreenThreads / 32));
         count_launch();
         auto* screen = cull == 2 ? k_screen<true> : k_screen<false>;
+        if (screen_ev) TJ_CUDA(cudaEventRecord(screen_ev[0], st));
         screen<<<sgrid, kScreenThreads, kScreenSmem, st>>>(src, vp_begin, vp_end, lb_bits, ub_bits, cull, qs.view(), work,
                                                             counters, batch, hier_min_pairs());
+        if (screen_ev) TJ_CUDA(cudaEventRecord(screen_ev[1], st));
         TJ_CUDA(cudaGetLastError());
     }
     count_launch();

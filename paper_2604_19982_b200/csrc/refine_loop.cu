@@ -317,6 +317,20 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
     DevBuf<unsigned long long> lbb(std::max<uint64_t>(n, 1)), ubb(std::max<uint64_t>(n, 1));
     DevBuf<unsigned long long> counters(kNumCounters), work(1), dbg;
     DevBuf<uint64_t> piece_b(1);
+    // k_screen launch timing (level stats screen_ms: bench.py's dominant-kernel roofline)
+    std::vector<cudaEvent_t> sev_pool;
+    size_t sev_used = 0;
+    auto sev = [&]() -> cudaEvent_t* {
+        if (sev_used + 2 > sev_pool.size())
+            for (int k = 0; k < 2; ++k) {
+                cudaEvent_t e;
+                TJ_CUDA(cudaEventCreate(&e));
+                sev_pool.push_back(e);
+            }
+        cudaEvent_t* p = sev_pool.data() + sev_used;
+        sev_used += 2;
+        return p;
+    };
     Clock::time_point tdbg[4];
     static const bool dbg_timing = std::getenv("TRIJOIN_DEBUG_TIMING") != nullptr;
     if (const char* e = std::getenv("TRIJOIN_DEBUG_OPSTATS"); e && *e && *e != '0') dbg.alloc(std::max<uint64_t>(n, 1));
@@ -402,6 +416,7 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
             }
             queue.cap = test_queue_cap;
             for (;;) {
+                sev_used = 0;
                 count_launch();
                 k_fill_u64<<<grid_for(n, 256, ws.num_sms), 256, 0, st>>>(lbb.p, n, kInfBits);
                 count_launch();
@@ -433,7 +448,7 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
                                         counters.p, ws.num_sms, st);
                         for (uint64_t c0 = a; c0 < b; c0 += launch)
                             refine_pass(src, c0, std::min(b, c0 + launch), false, lbb.p, ubb.p, cull, queue, work.p,
-                                        counters.p, ws.num_sms, st);
+                                        counters.p, ws.num_sms, st, sev());
                         a = b;
                     }
                     if (a != n_active) throw Error(TJ_EINVAL, "join: the pieces of a level do not cover its queries");
@@ -446,7 +461,7 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
                                         work.p, counters.p, ws.num_sms, st);
                     for (uint64_t c0 = 0; c0 < n_active; c0 += launch)
                         refine_pass(src, c0, std::min(n_active, c0 + launch), false, lbb.p, ubb.p, cull, queue,
-                                    work.p, counters.p, ws.num_sms, st);
+                                    work.p, counters.p, ws.num_sms, st, sev());
                 } else {
                     // per materialized chunk: its seeds, then its screened pass (the op minima
                     // only tighten; a chunk screened before another's seeds skips fewer pairs,
@@ -461,7 +476,7 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
                                                refine_pass(src, c0, c1, true, lbb.p, ubb.p, cull, queue, work.p,
                                                            counters.p, ws.num_sms, st);
                                            refine_pass(src, c0, c1, false, lbb.p, ubb.p, cull, queue, work.p,
-                                                       counters.p, ws.num_sms, st);
+                                                       counters.p, ws.num_sms, st, sev());
                                        }
                                    });
                 }
@@ -519,6 +534,11 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
             ls.vps_skipped = hc[5];
             ls.facets_dropped = hc[6];
             ls.kernel_ms = kms;
+            for (size_t k = 0; k + 1 < sev_used; k += 2) {
+                float m = 0.f;
+                TJ_CUDA(cudaEventElapsedTime(&m, sev_pool[k], sev_pool[k + 1]));
+                ls.screen_ms += m;
+            }
             tdbg[3] = Clock::now();
             n_active = compact_active(ws, cs, active, n_active, st);
             if (dbg_timing) {
@@ -540,6 +560,7 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    for (cudaEvent_t e : sev_pool) cudaEventDestroy(e);
     if (dbg_tl && !tl_ev.empty()) {
         tl_mark();
         TJ_CUDA(cudaEventSynchronize(tl_ev.back()));

@@ -255,9 +255,10 @@ void refine_seg_prep(const float4* box, const uint64_t* foff, uint64_t n_voxels,
 // box tests, [1] exact evaluations, [2] the refine loop's facet-pair count, [3]
 // separating-axis tests, [4] FP64 piercing verifications, [5] voxel pairs skipped whole,
 // [6] facets dropped by the row/column screens.
+// screen_ev (optional, 2 events): recorded around the k_screen launch (bench.py kernel timing).
 void refine_pass(const RefineSource& src, uint64_t vp_begin, uint64_t vp_end, bool seed, unsigned long long* lb_bits,
                  unsigned long long* ub_bits, int cull, RefineQueueStore& qs, unsigned long long* work,
-                 unsigned long long* counters, int num_sms, cudaStream_t st);
+                 unsigned long long* counters, int num_sms, cudaStream_t st, cudaEvent_t* screen_ev = nullptr);
 
 // Diagnostics (TRIJOIN_DEBUG_OPSTATS): per-op tested-pair counters of k_screen (nullptr = off).
 void refine_debug_op_tested(unsigned long long* p);

@@ -76,7 +76,8 @@ class JoinResult(ctypes.Structure):
                 ("level_vps_skipped", ctypes.c_uint64 * MAXL),
                 ("level_facets_dropped", ctypes.c_uint64 * MAXL),
                 ("level_wait_ms", ctypes.c_double * MAXL), ("decision_mode", ctypes.c_int32),
-                ("queue_reruns", ctypes.c_uint32), ("mat_chunks", ctypes.c_uint64)]
+                ("queue_reruns", ctypes.c_uint32), ("mat_chunks", ctypes.c_uint64),
+                ("level_screen_ms", ctypes.c_double * MAXL)]
 
 
 def capi_functions():

@@ -451,6 +451,7 @@ def main():
                "breakdown_ms": {k: round(float(np.mean([p.get(k, 0.0) for p in parts])), 2)
                                 for k in ("pack_ms", "upload_ms", "device_ms", "stream_wait_ms", "run_join_ms",
                                           "python_ms")},
+               "steps_ms": [round(x, 1) for x in ts],
                "timeline_ms": parts[-1].get("timeline", {}) if parts else {}}
 
     cpu = None

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <cstdlib>
 #include <mutex>
+#include <map>
 #include <set>
 #include <type_traits>
 
@@ -1061,6 +1062,21 @@ void refine_seg_prep(const float4* box, const uint64_t* foff, uint64_t n_voxels,
     TJ_CUDA(cudaGetLastError());
 }
 
+namespace {
+int eval_blocks_per_sm() {
+    static std::mutex mu;
+    static std::map<int, int> per_dev;
+    int dev = 0;
+    TJ_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = per_dev.find(dev);
+    if (it != per_dev.end()) return it->second;
+    int b = 0;
+    TJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_eval, 128, 0));
+    return per_dev[dev] = std::max(1, b);
+}
+} // namespace
+
 void refine_pass(const RefineSource& src, uint64_t vp_begin, uint64_t vp_end, bool seed, unsigned long long* lb_bits,
                  unsigned long long* ub_bits, int cull, RefineQueueStore& qs, unsigned long long* work,
                  unsigned long long* counters, int num_sms, cudaStream_t st, cudaEvent_t* screen_ev) {
@@ -1081,7 +1097,9 @@ void refine_pass(const RefineSource& src, uint64_t vp_begin, uint64_t vp_end, bo
             done.insert(dev);
         }
     }
-    const int grid = num_sms * 8;
+    // k_eval: exactly the resident blocks (a grid-stride kernel with even per-block work: a grid
+    // beyond one wave would run its surplus blocks in a second, mostly empty wave)
+    const int grid = num_sms * eval_blocks_per_sm();
     if (seed) {
         // 2 entries per voxel pair at most
         if (2 * (vp_end - vp_begin) > qs.items.n) qs.items.alloc(2 * (vp_end - vp_begin));

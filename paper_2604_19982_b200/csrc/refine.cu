@@ -832,16 +832,21 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks)
                             const int left = rcnt - rp0;
                             const int rows = left >= 32 ? 32 : left > 16 ? 16 : left;
                             const bool final_pass = rp0 + rows >= rcnt;
-                            const int P = 32 / rows;
-                            const int bi = rp0 + min(lane / P, rows - 1), jj = lane - (lane / P) * P;
-                            const bool row_on = lane / P < rows;
+                            // small-integer quotients by float reciprocal (x / P for 0 <= x < 64,
+                            // P <= 32: the + 0.5 keeps the product >= 1/64 away from integers, far
+                            // beyond the reciprocal's rounding)
+                            const int P = (int)__fdividef(32.5f, (float)rows);
+                            const float rP = __fdividef(1.f, (float)P);
+                            const int lq = (int)(((float)lane + 0.5f) * rP);
+                            const int bi = rp0 + min(lq, rows - 1), jj = lane - lq * P;
+                            const bool row_on = lq < rows;
                             rp0 += rows;
                             const RowRec ar = load_row(sm.rc + bi * CS, QO);
                             // per-row thresholds of the stage-1 pair test, pre-scaled by 1 / c (stage1_box)
                             const float rlb = lb_settled ? ninf : __fadd_ru(__fadd_ru(th.lb_u, dl), ar.ph);
                             const float rub = th.ub_u == 0.f ? ninf : __fsub_ru(__fadd_ru(th.ub_u, dl), ar.hd);
                             const float rlbc = __fmul_ru(rlb, kInvC), rubc = __fmul_ru(rub, kInvC);
-                            const int iters = (scnt - jj + P - 1) / P; // this lane's s facets
+                            const int iters = (int)(((float)(scnt - jj + P - 1) + 0.5f) * rP); // this lane's s facets
                             // The lane's s facets (jj + t P) into bit masks: bit t of `nmask` = the
                             // pair goes to stage 2; of `fmask` = a near pair whose DP4A conditioning
                             // pre-test failed (its FP32 test runs at the flush, 32 pairs at a time).

@@ -32,7 +32,7 @@ constexpr int kScreenBlocks = 2;
 struct VpDescDev {
     uint32_t op;
     uint32_t gvr, gvs; // global voxel ids (join mode)
-    uint64_t r0, s0; // first facet (record index) of each segment
+    uint32_t r0, s0; // first facet (record index) of each segment (a level's records: < 2^32, like the queues')
     uint32_t rn, sn;
     double iv_lb, iv_ub;
 };
@@ -44,18 +44,20 @@ __device__ __forceinline__ VpDescDev get_vp(const RefineSource& src, uint64_t vp
         d.op = av.op;
         d.gvr = av.gvr;
         d.gvs = av.gvs;
-        d.r0 = src.r_foff[av.gvr];
-        d.rn = (uint32_t)(src.r_foff[av.gvr + 1] - d.r0);
-        d.s0 = src.s_foff[av.gvs];
-        d.sn = (uint32_t)(src.s_foff[av.gvs + 1] - d.s0);
+        const uint64_t rf = src.r_foff[av.gvr];
+        d.r0 = (uint32_t)rf;
+        d.rn = (uint32_t)(src.r_foff[av.gvr + 1] - rf);
+        const uint64_t sf = src.s_foff[av.gvs];
+        d.s0 = (uint32_t)sf;
+        d.sn = (uint32_t)(src.s_foff[av.gvs + 1] - sf);
         d.iv_lb = src.cand_lb[av.op];
         d.iv_ub = src.cand_ub[av.op];
     } else { // batch mode: every voxel pair is its own op, interval [0, +inf]
         d.op = (uint32_t)vp;
         d.gvr = d.gvs = 0;
-        d.r0 = src.r_off[vp];
+        d.r0 = (uint32_t)src.r_off[vp];
         d.rn = src.r_len[vp];
-        d.s0 = src.s_off[vp];
+        d.s0 = (uint32_t)src.s_off[vp];
         d.sn = src.s_len[vp];
         d.iv_lb = 0.0;
         d.iv_ub = __longlong_as_double(0x7ff0000000000000ll);
@@ -312,8 +314,8 @@ __global__ void __launch_bounds__(256, 4) k_seed(RefineSource src, uint64_t vp_b
             // both segments fit the warp: each lane keeps its r and s facet boxes in registers
             const float kInfF = __int_as_float(0x7f800000);
             float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0, s0 = r0, s1 = r0;
-            if (lane < (int)d.rn) { r0 = __ldg(src.r_box + (d.r0 + lane) * kBoxF4); r1 = __ldg(src.r_box + (d.r0 + lane) * kBoxF4 + 1); }
-            if (lane < (int)d.sn) { s0 = __ldg(src.s_box + (d.s0 + lane) * kBoxF4); s1 = __ldg(src.s_box + (d.s0 + lane) * kBoxF4 + 1); }
+            if (lane < (int)d.rn) { r0 = __ldg(src.r_box + ((size_t)d.r0 + lane) * kBoxF4); r1 = __ldg(src.r_box + ((size_t)d.r0 + lane) * kBoxF4 + 1); }
+            if (lane < (int)d.sn) { s0 = __ldg(src.s_box + ((size_t)d.s0 + lane) * kBoxF4); s1 = __ldg(src.s_box + ((size_t)d.s0 + lane) * kBoxF4 + 1); }
             ist = warp_argmin_lane(lane < (int)d.rn ? seed_key(r0, r1, as.lo, as.hi) : kInfF);
             jst = warp_argmin_lane(lane < (int)d.sn ? seed_key(s0, s1, ar.lo, ar.hi) : kInfF);
             // second round against the single facets i*, j* (their boxes by shuffle)
@@ -330,10 +332,10 @@ __global__ void __launch_bounds__(256, 4) k_seed(RefineSource src, uint64_t vp_b
             float4 ra0 = make_float4(0.f, 0.f, 0.f, 0.f), ra1 = ra0, rb0 = ra0, rb1 = ra0;
             float4 sa0 = ra0, sa1 = ra0, sb0 = ra0, sb1 = ra0;
             const int l2 = lane + 32;
-            if (lane < (int)d.rn) { ra0 = __ldg(src.r_box + (d.r0 + lane) * kBoxF4); ra1 = __ldg(src.r_box + (d.r0 + lane) * kBoxF4 + 1); }
-            if (l2 < (int)d.rn) { rb0 = __ldg(src.r_box + (d.r0 + l2) * kBoxF4); rb1 = __ldg(src.r_box + (d.r0 + l2) * kBoxF4 + 1); }
-            if (lane < (int)d.sn) { sa0 = __ldg(src.s_box + (d.s0 + lane) * kBoxF4); sa1 = __ldg(src.s_box + (d.s0 + lane) * kBoxF4 + 1); }
-            if (l2 < (int)d.sn) { sb0 = __ldg(src.s_box + (d.s0 + l2) * kBoxF4); sb1 = __ldg(src.s_box + (d.s0 + l2) * kBoxF4 + 1); }
+            if (lane < (int)d.rn) { ra0 = __ldg(src.r_box + ((size_t)d.r0 + lane) * kBoxF4); ra1 = __ldg(src.r_box + ((size_t)d.r0 + lane) * kBoxF4 + 1); }
+            if (l2 < (int)d.rn) { rb0 = __ldg(src.r_box + ((size_t)d.r0 + l2) * kBoxF4); rb1 = __ldg(src.r_box + ((size_t)d.r0 + l2) * kBoxF4 + 1); }
+            if (lane < (int)d.sn) { sa0 = __ldg(src.s_box + ((size_t)d.s0 + lane) * kBoxF4); sa1 = __ldg(src.s_box + ((size_t)d.s0 + lane) * kBoxF4 + 1); }
+            if (l2 < (int)d.sn) { sb0 = __ldg(src.s_box + ((size_t)d.s0 + l2) * kBoxF4); sb1 = __ldg(src.s_box + ((size_t)d.s0 + l2) * kBoxF4 + 1); }
             auto argmin64 = [&](float ka, float kb) -> uint32_t {
                 const unsigned pa = (__float_as_uint(ka) & ~63u) | (unsigned)lane;
                 const unsigned pb = (__float_as_uint(kb) & ~63u) | (unsigned)l2;
@@ -361,9 +363,9 @@ __global__ void __launch_bounds__(256, 4) k_seed(RefineSource src, uint64_t vp_b
             closest_pair(src.r_box, d.r0, d.rn, src.s_box, d.s0, d.sn, ar, as, ist, jst);
             SegAgg fi = ar, fj = as; // only lo / hi are read
             {
-                const float4 a = __ldg(src.r_box + (d.r0 + ist) * kBoxF4), b = __ldg(src.r_box + (d.r0 + ist) * kBoxF4 + 1);
+                const float4 a = __ldg(src.r_box + ((size_t)d.r0 + ist) * kBoxF4), b = __ldg(src.r_box + ((size_t)d.r0 + ist) * kBoxF4 + 1);
                 fi.lo[0] = a.x; fi.lo[1] = a.y; fi.lo[2] = a.z; fi.hi[0] = b.x; fi.hi[1] = b.y; fi.hi[2] = b.z;
-                const float4 c = __ldg(src.s_box + (d.s0 + jst) * kBoxF4), e = __ldg(src.s_box + (d.s0 + jst) * kBoxF4 + 1);
+                const float4 c = __ldg(src.s_box + ((size_t)d.s0 + jst) * kBoxF4), e = __ldg(src.s_box + ((size_t)d.s0 + jst) * kBoxF4 + 1);
                 fj.lo[0] = c.x; fj.lo[1] = c.y; fj.lo[2] = c.z; fj.hi[0] = e.x; fj.hi[1] = e.y; fj.hi[2] = e.z;
             }
             closest_pair(src.r_box, d.r0, d.rn, src.s_box, d.s0, d.sn, fi, fj, ip, jp);

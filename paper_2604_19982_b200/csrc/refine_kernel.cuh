@@ -96,7 +96,7 @@ struct __align__(16) ScreenSmem {
     SegAgg seg_r, seg_s; // aggregates of the current voxel pair's segments
     // the current work batch: per voxel pair (lane) its segments, op and thresholds
     struct BatchVp {
-        uint64_t r0, s0;
+        uint32_t r0, s0;
         uint32_t op, gvr, gvs, rn, sn;
         float lb_u, ub_u;
         int flags; // bit 0: lb side settled; bit 1: every facet pair meets the shape / range terms (shapes_settled)

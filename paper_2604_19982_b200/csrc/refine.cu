@@ -688,14 +688,14 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks)
             const Thresh tl = thresholds(dl);
             live = dl.rn != 0 && dl.sn != 0 && !settled(tl);
             int flags = tl.lb_sat ? 1 : 0;
+            float d0 = 0.f;
             if (live && pre_seg) {
-                float d0;
                 SegAgg ar, as;
                 agg_skipped = vp_screen(dl, tl, d0, ar, as);
                 live = !agg_skipped;
                 if (shapes_settled(ar, as)) flags |= 2;
             }
-            if (live) sm.vpd[lane] = {dl.r0, dl.s0, dl.op, dl.gvr, dl.gvs, dl.rn, dl.sn, tl.lb_u, tl.ub_u, flags};
+            if (live) sm.vpd[lane] = {dl.r0, dl.s0, dl.op, dl.gvr, dl.gvs, dl.rn, dl.sn, tl.lb_u, tl.ub_u, d0, flags};
         }
         if (pre_seg) {
             const unsigned n_agg = __popc(__ballot_sync(0xffffffffu, agg_skipped));
@@ -725,7 +725,9 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks)
         // hierarchical screens: the whole voxel pair (always when the segment aggregates are
         // precomputed), then rows / columns where that can pay off
         const bool hier = cull && d.rn * d.sn >= hier_min;
-        float delta0 = 0.f; // tile-pair value when !hier
+        // delta0 >= 1e-5 (L_i + L_j) + 1e-12 (M_i + M_j) for every facet pair: the voxel pair's (from
+        // its segment aggregates) when known, else each tile pair computes its own
+        float delta0 = sm.vpd[lv].d0;
         if (hier || (cull && !pre_seg && src.r_seg)) {
             float d0;
             SegAgg ar, as;
@@ -791,7 +793,7 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks)
                             scale_s_tile(scnt);
                         }
                         float dl = delta0;
-                        if (!hier) { // tile-pair delta0 >= 1e-5 (L_i + L_j) + 1e-12 (M_i + M_j)
+                        if (!(dl > 0.f)) { // tile-pair delta0 >= 1e-5 (L_i + L_j) + 1e-12 (M_i + M_j)
                             float Lm = 0.f, Mm = 0.f;
                             if (lane < rcnt) { Lm = fabsf(sm.rc[lane * CS + 3]); Mm = sm.rc[lane * CS + MO]; }
                             if (lane < scnt) {

@@ -99,6 +99,7 @@ struct __align__(16) ScreenSmem {
         uint32_t r0, s0;
         uint32_t op, gvr, gvs, rn, sn;
         float lb_u, ub_u;
+        float d0;  // delta0 of the whole voxel pair (vp_screen; 0: none, the tiles compute their own)
         int flags; // bit 0: lb side settled; bit 1: every facet pair meets the shape / range terms (shapes_settled)
     } vpd[32];
     // the warp's counters (lane 0 writes; kept out of registers: the stage-1 loop is at the

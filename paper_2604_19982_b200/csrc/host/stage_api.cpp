@@ -7,7 +7,9 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 
 #include "packed.hpp"
@@ -21,19 +23,46 @@ namespace {
 
 tj_ctx* stage_ctx() { return detail::device_context(detail::join_devices()[0]); }
 
-// R / S resident on the stage device for one call (the same object uploaded once when R is S).
+// Device copies pinned by live StageResidency scopes, by dataset address (with a use count:
+// scopes may nest or share a dataset).
+struct Pinned {
+    std::shared_ptr<detail::DatasetHandle> h;
+    int uses = 0;
+};
+std::mutex& pinned_mu() {
+    static std::mutex* m = new std::mutex;
+    return *m;
+}
+std::map<const void*, Pinned>& pinned() {
+    static auto* p = new std::map<const void*, Pinned>;
+    return *p;
+}
+std::shared_ptr<detail::DatasetHandle> pinned_handle(const PreparedDataset& d) {
+    std::lock_guard<std::mutex> lk(pinned_mu());
+    auto it = pinned().find(&d);
+    return it == pinned().end() ? nullptr : it->second.h;
+}
+std::shared_ptr<detail::DatasetHandle> upload_dataset(tj_ctx* ctx, const PreparedDataset& d) {
+    ThreadPool pool(0);
+    auto p = detail::pack_dataset(d, pool);
+    auto h = std::make_shared<detail::DatasetHandle>();
+    detail::check(tj_dataset_upload(ctx, &p->view, &h->p), ctx);
+    return h;
+}
+
+// R / S resident on the stage device for one call (the same object uploaded once when R is S),
+// or the copies pinned by a StageResidency scope.
 struct StagePair {
     tj_ctx* ctx;
-    detail::DatasetHandle r, s;
-    const tj_dataset* R() const { return r.p; }
-    const tj_dataset* S() const { return s.p ? s.p : r.p; }
+    std::shared_ptr<detail::DatasetHandle> r, s;
+    const tj_dataset* R() const { return r->p; }
+    const tj_dataset* S() const { return s ? s->p : r->p; }
     StagePair(const PreparedDataset& Rd, const PreparedDataset& Sd) : ctx(stage_ctx()) {
-        ThreadPool pool(0);
-        auto pr = detail::pack_dataset(Rd, pool);
-        detail::check(tj_dataset_upload(ctx, &pr->view, &r.p), ctx);
+        r = pinned_handle(Rd);
+        if (!r) r = upload_dataset(ctx, Rd);
         if (&Sd != &Rd) {
-            auto ps = detail::pack_dataset(Sd, pool);
-            detail::check(tj_dataset_upload(ctx, &ps->view, &s.p), ctx);
+            s = pinned_handle(Sd);
+            if (!s) s = upload_dataset(ctx, Sd);
         }
     }
 };
@@ -167,6 +196,35 @@ std::vector<std::vector<uint32_t>> str_groups(const std::vector<Aabb>& boxes, st
 }
 
 } // namespace
+
+StageResidency::StageResidency(const PreparedDataset& R, const PreparedDataset& S) : r_(&R), s_(&S) {
+    tj_ctx* ctx = stage_ctx();
+    for (const PreparedDataset* d : {&R, &S}) {
+        if (d == &S && &S == &R) break;
+        {
+            std::lock_guard<std::mutex> lk(pinned_mu());
+            auto it = pinned().find(d);
+            if (it != pinned().end()) {
+                ++it->second.uses;
+                continue;
+            }
+        }
+        auto h = upload_dataset(ctx, *d);
+        std::lock_guard<std::mutex> lk(pinned_mu());
+        Pinned& p = pinned()[d];
+        if (!p.h) p.h = std::move(h);
+        ++p.uses;
+    }
+}
+
+StageResidency::~StageResidency() {
+    std::lock_guard<std::mutex> lk(pinned_mu());
+    for (const void* d : {r_, s_}) {
+        if (d == s_ && s_ == r_) break;
+        auto it = pinned().find(d);
+        if (it != pinned().end() && --it->second.uses == 0) pinned().erase(it);
+    }
+}
 
 RTree build_rtree(std::span<const PreparedObject> objects) {
     RTree tree;

@@ -273,6 +273,21 @@ void staged_equals_run_join(const PreparedDataset& R, const PreparedDataset& S, 
     CHECK(format_records(a.records, spec.type == JoinType::Knn) == format_records(b.records, spec.type == JoinType::Knn));
 }
 
+// ---- StageResidency (extension): chained stage calls on device copies pinned once give the
+// same records as the per-call uploads (and as run_join); scopes nest and share datasets
+void staged_with_residency(const PreparedDataset& R, const PreparedDataset& S, JoinSpec spec) {
+    spec.lods = {20, 60, 100};
+    const JoinOutput a = staged_join(R, S, spec);
+    StageResidency outer(R, S);
+    {
+        StageResidency inner(R, R); // nested, sharing R
+        const JoinOutput b = staged_join(R, S, spec);
+        CHECK(format_records(a.records, spec.type == JoinType::Knn) == format_records(b.records, spec.type == JoinType::Knn));
+    }
+    const JoinOutput c = staged_join(R, S, spec);
+    CHECK(format_records(a.records, spec.type == JoinType::Knn) == format_records(c.records, spec.type == JoinType::Knn));
+}
+
 // ---- test_refine.cpp:183-218: refine_loop results independent of chunk and pipeline
 void refine_chunk_invariance(const PreparedDataset& ds) {
     ThreadPool pool(2);
@@ -433,6 +448,7 @@ int main(int argc, char** argv) {
         s.k = k;
         staged_equals_run_join(m14, m14, s);
         staged_equals_run_join(nuc, ves, s);
+        staged_with_residency(nuc, ves, s);
     }
     {
         JoinSpec s;
@@ -443,6 +459,7 @@ int main(int argc, char** argv) {
         s.type = JoinType::Intersect;
         s.tau = 0.0;
         staged_equals_run_join(nuc, ves, s);
+        staged_with_residency(nuc, ves, s);
     }
     std::printf("test_stages: %d checks, %d failures\n", g_checks, g_fail);
     return g_fail ? 1 : 0;

@@ -454,6 +454,7 @@ int tj_dataset_begin_ex(tj_ctx* ctx, const tj_dataset_view* v, const uint64_t* c
     *out = nullptr;
     auto ds = std::make_unique<tj_dataset>();
     ds->ctx = ctx;
+    const auto t_begin = std::chrono::steady_clock::now();
     const int rc = guarded(ctx, [&] {
         DatasetDev& d = ds->d;
         d.compact = (flags & TJ_DATASET_COMPACT) != 0;
@@ -528,7 +529,13 @@ int tj_dataset_begin_ex(tj_ctx* ctx, const tj_dataset_view* v, const uint64_t* c
         d.stream_err.alloc(1);
         TJ_CUDA(cudaMemsetAsync(d.stream_err.p, 0, sizeof(int), st));
         d.gate = std::move(gate);
+        static const bool dbg = std::getenv("TRIJOIN_DEBUG_BEGIN") != nullptr;
+        const auto ts = std::chrono::steady_clock::now();
         stream_sync(st);
+        if (dbg)
+            std::fprintf(stderr, "[begin] %u objects: %.2f ms, of which the final sync %.2f ms\n", no,
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_begin).count(),
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ts).count());
     });
     if (rc == TJ_OK) *out = ds.release();
     return rc;

@@ -1343,8 +1343,10 @@ JoinOutput detail::run_join_cached(const PreparedDataset& R, const PreparedDatas
                 }
                 const detail::PackedHeader& hr = *lz->set->h;
                 detail::DatasetHandle dr;
+                if (G == 1 && w.chunks.size() == 1) mark("R_begin");
                 detail::check(tj_dataset_begin_ex(ctx, &hr.view, hr.vb_ptrs.data(), hr.fb_ptrs.data(), ds_flags, &dr.p),
                               ctx);
+                if (G == 1 && w.chunks.size() == 1) mark("R_begun");
                 {
                     std::lock_guard<std::mutex> lk(stat_mu);
                     out.stats.h2d_bytes += hr.bytes();

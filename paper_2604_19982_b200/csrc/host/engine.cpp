@@ -6,6 +6,7 @@
 #include <atomic>
 #include <bit>
 #include <chrono>
+#include <condition_variable>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1295,24 +1296,16 @@ JoinOutput detail::run_join_cached(const PreparedDataset& R, const PreparedDatas
     SetLease s_lease;
     std::vector<detail::DatasetHandle> dsh(G);
     std::vector<std::vector<char>> put_s(G, std::vector<char>(S.lod_schedule.size(), 0));
-    const auto tu = Clock::now();
-    if (!one_dataset) {
-        lease(s_lease, s_cache, "all");
-        if (!s_lease.set->h) {
-            const auto tp = Clock::now();
-            s_lease.set->h = detail::pack_header(S, pool);
-            pack_ms += std::chrono::duration<double, std::milli>(Clock::now() - tp).count();
-        }
-        const detail::PackedHeader& hs = *s_lease.set->h;
-        for (size_t g = 0; g < G; ++g) {
-            detail::check(
-                tj_dataset_begin_ex(ctxs[g], &hs.view, hs.vb_ptrs.data(), hs.fb_ptrs.data(), ds_flags, &dsh[g].p),
-                ctxs[g]);
-            out.stats.h2d_bytes += hs.bytes();
-        }
-    }
-    out.stats.upload_ms = std::chrono::duration<double, std::milli>(Clock::now() - tu).count();
-    mark("S_begun");
+    // S's datasets are begun by the main thread while the workers begin their R datasets and
+    // start streaming R's levels; a worker waits for S only to start its join
+    std::mutex s_mu;
+    std::condition_variable s_cv;
+    bool s_begun = false, s_failed = false;
+    auto wait_s_begun = [&] {
+        std::unique_lock<std::mutex> lk(s_mu);
+        s_cv.wait(lk, [&] { return s_begun; });
+        if (s_failed) throw std::runtime_error("trijoin: S upload failed");
+    };
 
     // ---- per GPU: its R chunks in order; each chunk's levels are packed (or taken from the
     // cache) and streamed while its join runs, coarsest level first
@@ -1360,6 +1353,7 @@ JoinOutput detail::run_join_cached(const PreparedDataset& R, const PreparedDatas
                 if (pieced) detail::check(tj_dataset_set_pieced(dr.p, static_cast<uint32_t>(r_last)), ctx);
                 std::exception_ptr je;
                 const auto td = Clock::now();
+                if (!one_dataset) wait_s_begun();
                 std::thread jt([&] {
                     try {
                         tj_join_spec cs = to_c_spec(spec);
@@ -1403,6 +1397,42 @@ JoinOutput detail::run_join_cached(const PreparedDataset& R, const PreparedDatas
     };
     std::vector<std::thread> workers;
     for (size_t g = 0; g < G; ++g) workers.emplace_back(worker, g);
+
+    std::exception_ptr s_begin_error;
+    try {
+        const auto tu = Clock::now();
+        if (!one_dataset) {
+            lease(s_lease, s_cache, "all");
+            if (!s_lease.set->h) {
+                const auto tp = Clock::now();
+                s_lease.set->h = detail::pack_header(S, pool);
+                std::lock_guard<std::mutex> lk(stat_mu); // the workers update the same tallies
+                pack_ms += std::chrono::duration<double, std::milli>(Clock::now() - tp).count();
+            }
+            const detail::PackedHeader& hs = *s_lease.set->h;
+            for (size_t g = 0; g < G; ++g) {
+                detail::check(
+                    tj_dataset_begin_ex(ctxs[g], &hs.view, hs.vb_ptrs.data(), hs.fb_ptrs.data(), ds_flags, &dsh[g].p),
+                    ctxs[g]);
+                std::lock_guard<std::mutex> lk(stat_mu);
+                out.stats.h2d_bytes += hs.bytes();
+            }
+        }
+        out.stats.upload_ms = std::chrono::duration<double, std::milli>(Clock::now() - tu).count();
+        mark("S_begun");
+    } catch (...) {
+        s_begin_error = std::current_exception();
+    }
+    {
+        std::lock_guard<std::mutex> lk(s_mu);
+        s_begun = true;
+        s_failed = s_begin_error != nullptr;
+    }
+    s_cv.notify_all();
+    if (s_begin_error) {
+        for (auto& t : workers) t.join();
+        std::rethrow_exception(s_begin_error);
+    }
 
     // ---- main thread: S levels in join order, shipped to every GPU
     std::exception_ptr s_error;

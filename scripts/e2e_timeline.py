@@ -18,5 +18,7 @@ for i in range(int(sys.argv[1]) if len(sys.argv) > 1 else 5):
     st = json.loads(js)
     tl = sorted(st["b200"]["timeline"].items(), key=lambda x: x[1] if "arena" not in x[0] else -1)
     print(round(wall, 1), [(k, round(v, 1)) for k, v in tl if "arena" not in k], flush=True)
+    b = st["b200"]
+    print("   b200", {k: (round(v, 2) if isinstance(v, float) else v) for k, v in b.items() if k.endswith("_ms")}, flush=True)
     lv = st["b200"].get("levels", [])
     print("   levels", [(l.get("level"), round(l.get("ms", 0), 1), round(l.get("wait_ms", 0), 1)) for l in lv], flush=True)

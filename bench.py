@@ -11,9 +11,11 @@ object pairs entering the voxel + LOD cascade (stats stages["voxel"].pairs_in).
           max over ranks.
   e2e   : the public API with host buffers (`join_datasets`: pack -> H2D -> join -> D2H ->
           records), same metric.
-  roofline: the refinement kernel (its own CUDA events on its launching stream): FLOPs =
-          evaluated facet pairs x 1500 + culling tests x 20 vs the FP32 peak
-          148 SM x 128 lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json).
+  roofline: the dominant kernel k_screen (CUDA events around its launches on its stream):
+          FLOPs = box tests x 20 (counted on the device) vs the FP32 peak
+          148 SM x 128 lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json); its largest launch alone,
+          and all refinement kernels (+ evaluated facet pairs x 1500) beside it. traffic: DRAM
+          bytes of one k_screen launch from the committed ncu --set full capture.
   cpu_baseline: the reference's own run_join (oracle/_ref, built from /root/reference) on a
           deterministic R-slice of the same workload on all host cores (rank 0, N=1 only).
 

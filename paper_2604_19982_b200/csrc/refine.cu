@@ -111,6 +111,20 @@ __device__ __forceinline__ void gather_recs(const float4* __restrict__ box, cons
     constexpr int kParts = kRecF4, kStride4 = kCS / 4;
     const int lane = threadIdx.x & 31;
     float4* d4 = reinterpret_cast<float4*>(dst);
+#if TJ_GATHER_FIXED_PART
+    // kParts = 8: lane copies part (lane & 7) of records lane / 8, + 4, ...; the part's source
+    // array, stride and the shared-memory column are loop-invariant per lane
+    static_assert(kParts == 8, "gather: 8 parts per record");
+    const int part = lane & 7;
+    const char* src = part < kBoxF4 ? reinterpret_cast<const char*>(box + part)
+                                    : reinterpret_cast<const char*>(geo + (part - kBoxF4));
+    const uint32_t stride = part < kBoxF4 ? kBoxF4 * 16u : kGeoF4 * 16u;
+    uint32_t sa = smem_addr(d4 + (lane >> 3) * kStride4 + part);
+    for (int rec = lane >> 3; rec < n; rec += 4, sa += 4 * kCS * 4) {
+        const char* g = src + (first + list[rec]) * stride;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g) : "memory");
+    }
+#else
     for (int k = lane; k < kParts * n; k += 32) {
         const int rec = k / kParts, part = k % kParts;
         const uint64_t f = first + list[rec];
@@ -119,6 +133,7 @@ __device__ __forceinline__ void gather_recs(const float4* __restrict__ box, cons
                      "l"(g)
                      : "memory");
     }
+#endif
     if (lane < n) { // the facet's FP64 v0 (16 + 8 B)
         const double* v = facets + (first + list[lane]) * 12;
         float* r = dst + lane * kCS + kV0Off;
@@ -857,7 +872,9 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks)
                             uint32_t nmask = 0, fmask = 0;
                             if (row_on) {
                                 const float* bp0 = sm.sc + jj * CS;
-                                if (shapes_ok)
+                                if (TJ_S1_UBSPEC && shapes_ok && th.ub_u == 0.f)
+                                    stage1_row<false, kBF, false>(ar, bp0, P * CS, iters, rlbc, rubc, nmask, fmask);
+                                else if (shapes_ok)
                                     stage1_row<false, kBF>(ar, bp0, P * CS, iters, rlbc, rubc, nmask, fmask);
                                 else
                                     stage1_row<true, kBF>(ar, bp0, P * CS, iters, rlbc, rubc, nmask, fmask);
@@ -866,6 +883,34 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks)
                             // stage 2 runs whenever 32 entries are queued (and on the rest after
                             // the final pass: the entries index this tile's records)
                             for (;;) {
+                                bool more, last;
+                                if constexpr (kBF && TJ_QUEUE_SCAN) {
+                                // every lane's entries at once, placed by a warp prefix sum of the
+                                // mask counts (as many as the ring has room for; the rest next round)
+                                more = false;
+                                if (__ballot_sync(0xffffffffu, nmask != 0)) {
+                                    const int c = __popc(nmask);
+                                    int x = c;
+#pragma unroll
+                                    for (int o = 1; o < 32; o <<= 1) {
+                                        const int y = __shfl_up_sync(0xffffffffu, x, o);
+                                        if (lane >= o) x += y;
+                                    }
+                                    const int total = __shfl_sync(0xffffffffu, x, 31);
+                                    const int room = kQueue - nq;
+                                    int pos = x - c;
+                                    while (nmask != 0 && pos < room) {
+                                        const int t = __ffs(nmask) - 1;
+                                        nmask &= nmask - 1;
+                                        sm.q[(qh + nq + pos) & (kQueue - 1)] =
+                                            (uint16_t)(((fmask >> t) & 1u ? 0x8000 : 0) | (bi << 5) | (jj + t * P));
+                                        ++pos;
+                                    }
+                                    nq += min(total, room);
+                                    more = total > room;
+                                }
+                                last = !more && final_pass;
+                                } else {
                                 const bool has = nmask != 0;
                                 const unsigned bal = __ballot_sync(0xffffffffu, has);
                                 if (has) {
@@ -875,7 +920,9 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks)
                                         (uint16_t)(((fmask >> t) & 1u ? 0x8000 : 0) | (bi << 5) | (jj + t * P));
                                 }
                                 nq += __popc(bal);
-                                const bool last = bal == 0 && final_pass;
+                                more = bal != 0;
+                                last = !more && final_pass;
+                                }
                                 while (nq >= 32 || (last && nq > 0)) { // second stage on up to 32 queued pairs
                                     const int n = min(nq, 32);
                                     __syncwarp();
@@ -893,7 +940,7 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks)
                                         // the plane sides clear them all (sat_needed's first exit) no more
                                         bool full = !(e & 0x8000);
                                         if (!full) {
-                                            const int m = ill_mask_fp32(ra, sb);
+                                            const int m = TJ_FLAG_QMASK ? ill_mask_q(ra, sb) : ill_mask_fp32(ra, sb);
                                             if (m) {
                                                 go = true;
                                                 const double* va = reinterpret_cast<const double*>(ra + kV0Off);
@@ -914,18 +961,26 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks)
                                             ver = r >> 1;
                                         }
                                     }
+#if TJ_FLAG_QMASK
+                                    // every entry goes on (a flagged entry's DP4A mask is never empty);
+                                    // verifications are rare: shared-memory atomics by their lanes
+                                    (void)go;
+                                    if (lane == 0) sm.cnt[1] += (uint32_t)n;
+                                    if (ver) atomicAdd(&sm.cnt[2], 1u);
+#else
                                     const unsigned ngo = __popc(__ballot_sync(0xffffffffu, go));
                                     const unsigned nver = __popc(__ballot_sync(0xffffffffu, ver));
                                     if (lane == 0) {
                                         sm.cnt[1] += ngo;
                                         sm.cnt[2] += nver;
                                     }
+#endif
                                     queue_push(q, need, d.op, fr, fs);
                                     __syncwarp();
                                     qh = (qh + n) & (kQueue - 1);
                                     nq -= n;
                                 }
-                                if (bal == 0) break;
+                                if (!more) break;
                             }
                         }
                     }

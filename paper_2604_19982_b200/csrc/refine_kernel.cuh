@@ -57,7 +57,23 @@ constexpr int kV0Off = 36; // FP64 v0 in a staged record (float index; 16-B alig
 constexpr int kRecF4 = kScreenRecF4; // float4 per screening record (floats 0-31)
 constexpr int kBoxF4 = 3;  // box part of a record (floats 0-11), its own array: 3 float4 per facet
 constexpr int kGeoF4 = 5;  // geometry part (floats 12-31): 5 float4 per facet
-constexpr int kQueue = 64;  // per-warp SAT queue (< 32 pending + 32 new per compaction round)
+#ifndef TJ_GATHER_FIXED_PART
+#define TJ_GATHER_FIXED_PART 0 // gather_recs: one record part per lane (measured slower: B 50.9 -> 59.6 ms)
+#endif
+#ifndef TJ_FLAG_QMASK
+#define TJ_FLAG_QMASK 1 // flagged stage-2 entries: DP4A per-combination mask instead of FP32 dots
+#endif
+#ifndef TJ_S1_UBSPEC
+#define TJ_S1_UBSPEC 0 // stage 1: a loop variant for ub-settled voxel pairs (measured: B 48.9 vs 49.2 ms, C no gain)
+#endif
+#ifndef TJ_QUEUE_SCAN
+#define TJ_QUEUE_SCAN 1 // decision mode (k_screen<true>): stage-2 queue fill by a warp prefix sum
+                        // of the lanes' mask counts (B 50.9 -> 49.6 ms; k-NN C 178.8 -> 182.5, so not there)
+#endif
+
+// per-warp stage-2 queue: < 32 pending + 32 new per compaction round, or (TJ_QUEUE_SCAN) a
+// whole row pass's entries at once when they fit
+constexpr int kQueue = TJ_QUEUE_SCAN ? 256 : 64;
 constexpr int kCap = 128;  // per-warp survivor lists: facets per raw segment chunk
 // voxel pairs with fewer facet pairs skip the row / column screens (B: 1024 -> 85.9 ms,
 // 2048 -> 83.0, 8192 -> 81.3, never -> 81.3; C within 1 %)
@@ -355,14 +371,15 @@ __device__ __forceinline__ bool well_cond_q(const int* aq, int4 bq) {
 // hold iff max(xs, ys) <= 0 or g2 >= max(xs, ys)^2 (squares of non-negative values compared,
 // directed rounding; the FMAs round once, downwards, so g2 stays a lower bound).
 // kShapes = false when the voxel pair is known to meet the shape / range terms for every
-// facet pair (shapes_settled).
-template <bool kShapes>
+// facet pair (shapes_settled); kUb = false when the voxel pair's ub side is settled (rubc = -inf,
+// so z is the lb side's term alone).
+template <bool kShapes, bool kUb = true>
 __device__ __forceinline__ int stage1_box(const RowRec& a, float4 b0, float4 b1, float2 pc, float rlbc, float rubc) {
     const float gx = fmaxf(0.f, fmaxf(__fsub_rd(b0.x, a.hi[0]), __fsub_rd(a.lo[0], b1.x)));
     const float gy = fmaxf(0.f, fmaxf(__fsub_rd(b0.y, a.hi[1]), __fsub_rd(a.lo[1], b1.y)));
     const float gz = fmaxf(0.f, fmaxf(__fsub_rd(b0.z, a.hi[2]), __fsub_rd(a.lo[2], b1.z)));
     const float g2 = __fmaf_rd(gz, gz, __fmaf_rd(gy, gy, __fmul_rd(gx, gx)));
-    const float z = fmaxf(__fadd_ru(rlbc, pc.x), __fsub_ru(rubc, pc.y));
+    const float z = kUb ? fmaxf(__fadd_ru(rlbc, pc.x), __fsub_ru(rubc, pc.y)) : __fadd_ru(rlbc, pc.x);
     bool skip = z <= 0.f || g2 >= __fmul_ru(z, z);
     if constexpr (kShapes) {
         const float m = 1e3f * fminf(a.L, b0.w);
@@ -378,12 +395,12 @@ __device__ __forceinline__ int stage1_box(const RowRec& a, float4 b0, float4 b1,
 // kBF: the DP4A pre-test runs for every pair, branch-free, two pairs per iteration (faster when
 // most tested pairs are near, as in decision mode: config B 60.5 -> 58.1 ms); otherwise behind
 // a branch (faster when most are far: config C 199 -> 192 ms).
-template <bool kShapes, bool kBF>
+template <bool kShapes, bool kBF, bool kUb>
 __device__ __forceinline__ void stage1_pair(const RowRec& a, const float* bp, float rlbc, float rubc, uint32_t bit,
                                             uint32_t& nmask, uint32_t& fmask) {
     const float4 b0 = *reinterpret_cast<const float4*>(bp), b1 = *reinterpret_cast<const float4*>(bp + 4);
     const float2 pc = *reinterpret_cast<const float2*>(bp + 32);
-    const int sb = stage1_box<kShapes>(a, b0, b1, pc, rlbc, rubc);
+    const int sb = stage1_box<kShapes, kUb>(a, b0, b1, pc, rlbc, rubc);
     bool f;
     if constexpr (!kBF) {
         f = sb == 2 && !well_cond_q(a.q, *reinterpret_cast<const int4*>(bp + kQOff));
@@ -395,7 +412,7 @@ __device__ __forceinline__ void stage1_pair(const RowRec& a, const float* bp, fl
     fmask |= f ? bit : 0u;
 }
 
-template <bool kShapes, bool kBF>
+template <bool kShapes, bool kBF, bool kUb = true>
 __device__ __forceinline__ void stage1_row(const RowRec& a, const float* bp, int step, int iters, float rlbc, float rubc,
                                            uint32_t& nmask, uint32_t& fmask) {
     uint32_t bit = 1u;
@@ -403,12 +420,12 @@ __device__ __forceinline__ void stage1_row(const RowRec& a, const float* bp, int
     if constexpr (kBF) {
 #pragma unroll 1
         for (; t + 1 < iters; t += 2, bp += 2 * step, bit <<= 2) {
-            stage1_pair<kShapes, kBF>(a, bp, rlbc, rubc, bit, nmask, fmask);
-            stage1_pair<kShapes, kBF>(a, bp + step, rlbc, rubc, bit << 1, nmask, fmask);
+            stage1_pair<kShapes, kBF, kUb>(a, bp, rlbc, rubc, bit, nmask, fmask);
+            stage1_pair<kShapes, kBF, kUb>(a, bp + step, rlbc, rubc, bit << 1, nmask, fmask);
         }
     }
 #pragma unroll 1
-    for (; t < iters; ++t, bp += step, bit <<= 1) stage1_pair<kShapes, kBF>(a, bp, rlbc, rubc, bit, nmask, fmask);
+    for (; t < iters; ++t, bp += step, bit <<= 1) stage1_pair<kShapes, kBF, kUb>(a, bp, rlbc, rubc, bit, nmask, fmask);
 }
 
 // True if every facet pair (x, y) of the two segments meets the shape / range terms of the
@@ -439,6 +456,22 @@ __device__ __forceinline__ int ill_mask_fp32(const float* as, const float* b) {
     return (int)ill_cond(a3.x, a3.y, a3.z, b2.x, b2.y, b2.z) | (int)ill_cond(a3.w, a4.x, a4.y, b2.x, b2.y, b2.z) << 1 |
            (int)ill_cond(a4.z, a4.w, a20, b2.x, b2.y, b2.z) << 2 | (int)ill_cond(b3.x, b3.y, b3.z, a2.x, a2.y, a2.z) << 3 |
            (int)ill_cond(b3.w, b4.x, b4.y, a2.x, a2.y, a2.z) << 4 | (int)ill_cond(b4.z, b4.w, b20, a2.x, a2.y, a2.z) << 5;
+}
+
+// The same combinations from the quantised directions (well_cond_q's six DP4A dots, same bit
+// order): bit set where |q_u . q_v| <= 238, i.e. wherever the pre-test cannot certify
+// |u . v| > 1e-3. A superset of the FP32 mask: every combination the pre-test certifies is
+// one whose conditioning the skip argument accepts (stage 1 skips on that certificate alone),
+// so clearing this mask's bits by the plane sides is sufficient for a skip.
+__device__ __forceinline__ int ill_mask_q(const float* as, const float* b) {
+    constexpr int kT = 238;
+    const int4 aq = *reinterpret_cast<const int4*>(as + kQOff), bq = *reinterpret_cast<const int4*>(b + kQOff);
+    const int d[6] = {__dp4a(aq.y, bq.x, 0), __dp4a(aq.z, bq.x, 0), __dp4a(aq.w, bq.x, 0),
+                      __dp4a(bq.y, aq.x, 0), __dp4a(bq.z, aq.x, 0), __dp4a(bq.w, aq.x, 0)};
+    int m = 0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) m |= ((unsigned)(d[k] + kT) <= 2u * kT) ? 1 << k : 0;
+    return m;
 }
 
 // Shape / range eligibility for a skip and the mask of ill-conditioned edge/plane
@@ -491,13 +524,13 @@ __device__ __forceinline__ SatFrame sat_frame(const float* a, const float* b, co
 }
 
 __device__ __forceinline__ float sat_axis(const SatFrame& f, float ux, float uy, float uz) {
-    const float u2 = ux * ux + uy * uy + uz * uz;
+    const float u2 = __fmaf_rn(ux, ux, __fmaf_rn(uy, uy, __fmul_rn(uz, uz)));
     if (!(u2 > 1e-30f)) return 0.f;
     float amin = 3.4e38f, amax = -3.4e38f, bmin = 3.4e38f, bmax = -3.4e38f;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        const float pa = ux * f.av[3 * k] + uy * f.av[3 * k + 1] + uz * f.av[3 * k + 2];
-        const float pb = ux * f.bv[3 * k] + uy * f.bv[3 * k + 1] + uz * f.bv[3 * k + 2];
+        const float pa = __fmaf_rn(ux, f.av[3 * k], __fmaf_rn(uy, f.av[3 * k + 1], __fmul_rn(uz, f.av[3 * k + 2])));
+        const float pb = __fmaf_rn(ux, f.bv[3 * k], __fmaf_rn(uy, f.bv[3 * k + 1], __fmul_rn(uz, f.bv[3 * k + 2])));
         amin = fminf(amin, pa);
         amax = fmaxf(amax, pa);
         bmin = fminf(bmin, pb);
@@ -547,8 +580,10 @@ __device__ __forceinline__ int plane_clear(int mask, const SatFrame& f, const fl
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         // a's vertices against b's plane (through bv[0..2]); b's vertices against a's (origin)
-        sa[k] = b[8] * (f.av[3 * k] - f.bv[0]) + b[9] * (f.av[3 * k + 1] - f.bv[1]) + b[10] * (f.av[3 * k + 2] - f.bv[2]);
-        sb[k] = a[8] * f.bv[3 * k] + a[9] * f.bv[3 * k + 1] + a[10] * f.bv[3 * k + 2];
+        // FMA dots (one rounding per term: within the analysed error bound)
+        sa[k] = __fmaf_rn(b[8], f.av[3 * k] - f.bv[0],
+                          __fmaf_rn(b[9], f.av[3 * k + 1] - f.bv[1], __fmul_rn(b[10], f.av[3 * k + 2] - f.bv[2])));
+        sb[k] = __fmaf_rn(a[8], f.bv[3 * k], __fmaf_rn(a[9], f.bv[3 * k + 1], __fmul_rn(a[10], f.bv[3 * k + 2])));
     }
 #pragma unroll
     for (int k = 0; k < 3; ++k) {

@@ -282,6 +282,50 @@ __device__ __forceinline__ void closest_pair(const float4* __restrict__ rset, ui
     jst = is;
 }
 
+// Decision mode: when every facet pair has hd_i + hd_j > 1e-5 (L_i + L_j) + 1e-12 (M_i + M_j),
+// no ub_ij can be 0 at this level (B + hd_i + hd_j >= tiny + delta for every pair), so the ub
+// side of every op is settled (the level's aggregates, k_prep).
+__device__ __forceinline__ bool level_ub_settled(const RefineSource& src, int cull) {
+    if (cull != 2 || !src.agg) return false;
+    const float hd2 = __fadd_rd(__uint_as_float(src.agg[0]), __uint_as_float(src.agg[3]));
+    const float l2 = __fadd_ru(__uint_as_float(src.agg[1]), __uint_as_float(src.agg[4]));
+    const float m2 = __fadd_ru(__uint_as_float(src.agg[2]), __uint_as_float(src.agg[5]));
+    return hd2 > __fadd_ru(__fadd_ru(__fmul_ru(1e-5f, l2), __fmul_ru(1e-12f, m2)), 1e-30f);
+}
+
+// Decision mode, a voxel pair whose segments can hold a zero bound (segment gap <= ph_max(r) +
+// ph_max(s)): only those are seeded.
+__device__ __forceinline__ bool seedable_dm(const SegAgg& ar, const SegAgg& as) {
+    const float arec[8] = {ar.lo[0], ar.lo[1], ar.lo[2], 0.f, ar.hi[0], ar.hi[1], ar.hi[2], 0.f};
+    const float brec[8] = {as.lo[0], as.lo[1], as.lo[2], 0.f, as.hi[0], as.hi[1], as.hi[2], 0.f};
+    return !(box_gap_lb(arec, brec) > __fadd_ru(as.phmax, ar.phmax));
+}
+
+// Decision-mode seeding in two phases (refine_pass): one op needs a single zero-bound facet
+// pair to settle, so each op's most promising voxel pair (segment boxes by decreasing overlap
+// volume, then by increasing squared gap; ties to the lowest index) is seeded and evaluated
+// first, and the op's other voxel pairs are seeded only if the op is still open. A heuristic
+// order only: exactness rests on the screen, which tests every pair of every open op.
+// pick[op] = min over the op's seedable voxel pairs of (key << 32 | voxel pair - vp_begin).
+__global__ void k_seed_pick(RefineSource src, uint64_t vp_begin, uint64_t vp_end, unsigned long long* pick) {
+    for (uint64_t vp = vp_begin + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; vp < vp_end;
+         vp += (uint64_t)gridDim.x * blockDim.x) {
+        const VpDescDev d = get_vp(src, vp);
+        if (d.rn == 0 || d.sn == 0) continue;
+        const SegAgg ar = seg_r_of(src, d), as = seg_s_of(src, d);
+        if (!seedable_dm(ar, as)) continue;
+        float g2 = 0.f, vol = 1.f;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const float e = fminf(ar.hi[k], as.hi[k]) - fmaxf(ar.lo[k], as.lo[k]);
+            g2 += e < 0.f ? e * e : 0.f;
+            vol *= fmaxf(e, 0.f);
+        }
+        const uint32_t key = g2 > 0.f ? 0x80000000u + __float_as_uint(g2) : 0x7fffffffu - __float_as_uint(vol);
+        atomicMin(pick + d.op, (unsigned long long)key << 32 | (uint32_t)(vp - vp_begin));
+    }
+}
+
 // Seed pass, warp per voxel pair, O(r + s): i* = the r facet closest (box gap) to the s
 // segment's box, j* symmetrically; then j' = the s facet closest to i* and i' the r facet
 // closest to j*; queues (i*, j') and (i', j*). In decision mode only voxel pairs that can
@@ -291,7 +335,9 @@ __device__ __forceinline__ void closest_pair(const float4* __restrict__ rset, ui
 #endif
 __device__ __forceinline__ unsigned seed_batch() { return SEED_BATCH; }
 __global__ void __launch_bounds__(256, 4) k_seed(RefineSource src, uint64_t vp_begin, uint64_t vp_end, RefineQueue q,
-                                              int cull) {
+                                              int cull, int phase, const unsigned long long* __restrict__ pick,
+                                              const unsigned long long* __restrict__ lb_bits,
+                                              const unsigned long long* __restrict__ ub_bits) {
     // per warp: the voxel pairs of the current batch that need seeds (segments + boxes)
     struct SeedVp {
         uint64_t r0, s0;
@@ -305,11 +351,16 @@ __global__ void __launch_bounds__(256, 4) k_seed(RefineSource src, uint64_t vp_b
     PairRef pref{0u, 0u, 0u, 0u}; // this lane's buffered seed
     int pend = 0;
     // decision mode: only voxel pairs that can hold a zero bound
-    auto seedable = [&](const SegAgg& ar, const SegAgg& as) {
-        if (cull != 2) return true;
-        const float arec[8] = {ar.lo[0], ar.lo[1], ar.lo[2], 0.f, ar.hi[0], ar.hi[1], ar.hi[2], 0.f};
-        const float brec[8] = {as.lo[0], as.lo[1], as.lo[2], 0.f, as.hi[0], as.hi[1], as.hi[2], 0.f};
-        return !(box_gap_lb(arec, brec) > __fadd_ru(ar.phmax, as.phmax));
+    auto seedable = [&](const SegAgg& ar, const SegAgg& as) { return cull != 2 || seedable_dm(ar, as); };
+    // two-phase decision-mode seeding (k_seed_pick): phase 1 the ops' primary voxel pairs, phase 2
+    // the others of the ops still open (k_eval's settled test); phase 0 every voxel pair
+    const bool ub_settled = level_ub_settled(src, cull);
+    auto wanted = [&](uint64_t vp, uint32_t op) {
+        if (phase == 0) return true;
+        const bool prim = (uint32_t)__ldcg(pick + op) == (uint32_t)(vp - vp_begin);
+        if (phase == 1 || prim) return prim;
+        return exact_op(src.exact_mask, op) || !(bits_to_double(__ldcg(lb_bits + op)) == 0.0 &&
+                                                 (ub_settled || bits_to_double(__ldcg(ub_bits + op)) == 0.0));
     };
     // buffer the seeds (i*, j') and (i', j*) of a voxel pair in lanes (pend = entries held),
     // one queue append per 30+ seeds; arguments warp-uniform
@@ -400,7 +451,7 @@ __global__ void __launch_bounds__(256, 4) k_seed(RefineSource src, uint64_t vp_b
                 const VpDescDev d = get_vp(src, base + lane);
                 if (d.rn != 0 && d.sn != 0) {
                     const SegAgg ar = seg_r_of(src, d), as = seg_s_of(src, d);
-                    live = seedable(ar, as);
+                    live = seedable(ar, as) && wanted(base + lane, d.op);
                     if (live)
                         mine[lane] = {d.r0, d.s0, d.op, d.rn, d.sn, 0u,
                                       {ar.lo[0], ar.lo[1], ar.lo[2]}, {ar.hi[0], ar.hi[1], ar.hi[2]},
@@ -488,7 +539,7 @@ __global__ void __launch_bounds__(256, 4) k_seed(RefineSource src, uint64_t vp_b
             if (d.rn == 0 || d.sn == 0) continue;
             const SegAgg ar = seg_r_of(src, d);
             const SegAgg as = seg_s_of(src, d);
-            if (!seedable(ar, as)) continue;
+            if (!seedable(ar, as) || !wanted(vp, d.op)) continue;
             seed_vp(d, ar, as);
         }
     }
@@ -623,17 +674,6 @@ unsigned screen_batch(float mean_seg, uint64_t n_vps, uint64_t warps) {
     const float cap = float(n_vps) / float(8 * (warps ? warps : 1));
     b = fminf(b, cap);
     return b >= 32.f ? 32u : b <= 4.f ? 4u : (unsigned)b;
-}
-
-// Decision mode: when every facet pair has hd_i + hd_j > 1e-5 (L_i + L_j) + 1e-12 (M_i + M_j),
-// no ub_ij can be 0 at this level (B + hd_i + hd_j >= tiny + delta for every pair), so the ub
-// side of every op is settled (the level's aggregates, k_prep).
-__device__ __forceinline__ bool level_ub_settled(const RefineSource& src, int cull) {
-    if (cull != 2 || !src.agg) return false;
-    const float hd2 = __fadd_rd(__uint_as_float(src.agg[0]), __uint_as_float(src.agg[3]));
-    const float l2 = __fadd_ru(__uint_as_float(src.agg[1]), __uint_as_float(src.agg[4]));
-    const float m2 = __fadd_ru(__uint_as_float(src.agg[2]), __uint_as_float(src.agg[5]));
-    return hd2 > __fadd_ru(__fadd_ru(__fmul_ru(1e-5f, l2), __fmul_ru(1e-12f, m2)), 1e-30f);
 }
 
 // kBF: the stage-1 DP4A pre-test branch-free, two pairs per iteration (stage1_row); chosen for
@@ -1139,6 +1179,17 @@ int eval_blocks_per_sm() {
     TJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_eval, 128, 0));
     return per_dev[dev] = std::max(1, b);
 }
+
+// $TRIJOIN_SEED_ONEPASS=1: decision mode seeds every voxel pair in one pass; =2: the ops'
+// primary voxel pairs only (tuning / A-B)
+int seed_mode() {
+    static const int v = [] {
+        const char* e = getenv("TRIJOIN_SEED_ONEPASS");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
+bool two_phase_seeds() { return seed_mode() != 1; }
 } // namespace
 
 void refine_pass(const RefineSource& src, uint64_t vp_begin, uint64_t vp_end, bool seed, unsigned long long* lb_bits,
@@ -1167,9 +1218,29 @@ void refine_pass(const RefineSource& src, uint64_t vp_begin, uint64_t vp_end, bo
     if (seed) {
         // 2 entries per voxel pair at most
         if (2 * (vp_end - vp_begin) > qs.items.n) qs.items.alloc(2 * (vp_end - vp_begin));
-        TJ_CUDA(cudaMemsetAsync(qs.count.p, 0, 8, st));
-        count_launch();
-        k_seed<<<warp_grid(vp_end - vp_begin, num_sms, 4), 256, 0, st>>>(src, vp_begin, vp_end, qs.view(), cull);
+        const int sg = warp_grid(vp_end - vp_begin, num_sms, 4);
+        if (cull == 2 && src.active && src.r_seg && src.s_seg && src.n_ops && two_phase_seeds()) {
+            // decision mode: the ops' primary voxel pairs seeded and evaluated first, then the
+            // other voxel pairs of the ops still open (k_seed_pick)
+            qs.pick.reserve(src.n_ops);
+            TJ_CUDA(cudaMemsetAsync(qs.pick.p, 0xff, (size_t)src.n_ops * 8, st));
+            count_launch();
+            k_seed_pick<<<(int)std::min<uint64_t>((vp_end - vp_begin + 255) / 256, (uint64_t)num_sms * 8), 256, 0, st>>>(
+                src, vp_begin, vp_end, qs.pick.p);
+            TJ_CUDA(cudaMemsetAsync(qs.count.p, 0, 8, st));
+            count_launch();
+            k_seed<<<sg, 256, 0, st>>>(src, vp_begin, vp_end, qs.view(), cull, 1, qs.pick.p, lb_bits, ub_bits);
+            count_launch();
+            k_eval<<<grid, 128, 0, st>>>(src, qs.view(), lb_bits, ub_bits, counters, cull);
+            TJ_CUDA(cudaMemsetAsync(qs.count.p, 0, 8, st));
+            count_launch();
+            if (seed_mode() != 2)
+                k_seed<<<sg, 256, 0, st>>>(src, vp_begin, vp_end, qs.view(), cull, 2, qs.pick.p, lb_bits, ub_bits);
+        } else {
+            TJ_CUDA(cudaMemsetAsync(qs.count.p, 0, 8, st));
+            count_launch();
+            k_seed<<<sg, 256, 0, st>>>(src, vp_begin, vp_end, qs.view(), cull, 0, nullptr, lb_bits, ub_bits);
+        }
         TJ_CUDA(cudaGetLastError());
     } else {
         // No host round trip: a queue overflow only drops entries, k_eval records the largest

@@ -378,6 +378,7 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
             RefineSource src{};
             src.active = active.p;
             src.exact_mask = decision ? tripwire_mask() : 0u;
+            src.n_ops = (uint32_t)n;
             src.cand_lb = cs.lb.p;
             src.cand_ub = cs.ub.p;
             ws.level_agg.reserve(8);

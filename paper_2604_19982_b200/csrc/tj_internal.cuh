@@ -194,6 +194,8 @@ struct RefineSource {
     // decision mode: ops with (op & exact_mask) == 0 keep exact intervals (the reference's
     // bound-crossing tripwire is evaluated on them); 0xffffffff = none
     uint32_t exact_mask;
+    // join mode: number of ops (candidate pairs); sizes the decision-mode seed pick (0 = unknown)
+    uint32_t n_ops;
 };
 
 // Decision-mode op sample with exact intervals: $TRIJOIN_TRIPWIRE_SAMPLE = every N-th op
@@ -221,6 +223,7 @@ struct RefineQueue {
 struct RefineQueueStore {
     DevBuf<PairRef> items;              // exact-evaluation queue
     DevBuf<unsigned long long> count; // [0] entries of the current pass, [1] largest overflowing count
+    DevBuf<unsigned long long> pick;  // decision-mode seeding: per op, (key << 32 | voxel pair) of its primary
     // Test hook ($TRIJOIN_TEST_QUEUE_CAP, read per level by refine_loop_dev): the passes of a
     // level see at most `cap` slots until the first overflow grows the queue, so the
     // overflow -> grow -> re-run path runs on small inputs. 0 = no cap.

@@ -1,5 +1,5 @@
 #!/bin/bash
-# Round-2 ncu evidence of one resident config-B join (bench.py --profile): the launch list,
+# ncu evidence of one resident config-B join (bench.py --profile): the launch list,
 # --set full captures of the filter / compaction kernels (HBM roofline rows) and of the
 # LOD-100 refinement launches (k_screen with source lines, k_seed, k_eval).
 mkdir -p gpurun_out
@@ -12,8 +12,8 @@ run() { # name regex skip count
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches_${TAG}.csv python bench.py --profile $ARGS > gpurun_out/launches_${TAG}.log 2>&1
 run filters "k_mbb_count|k_mbb_fill|k_vf_bounds|k_vf_scatter|k_gather_sorted" 0 5
-run compact "DeviceSelectSweep|DeviceScan" 0 3
+run compact "k_tile_select|k_tile_sums|k_tile_scan" 0 3
 run screen100 "k_screen" 2 1
-run seed100 "k_seed" 2 1
-run eval100 "k_eval" 5 1
+run seed100 "k_seed" 5 1   # decision mode: 2 seed launches per level (primary, rest)
+run eval100 "k_eval" 7 1   # 3 per level: primary seeds, other seeds, screen
 ls gpurun_out | grep ncu_${TAG}

@@ -837,7 +837,7 @@ int tj_join(tj_ctx* ctx, const tj_dataset* Rh, const tj_dataset* Sh, const tj_jo
         va.prune = knn ? 0 : 1;
         va.tau = tau;
         va.err = err.p;
-        DevBuf<ActiveVpDev> active;
+        DevBuf<ActiveVpDev>& active = ctx->ws.active;
         std::vector<PrunedVp> pruned;
         std::vector<uint8_t> touched;
         const VoxelOut vo = voxel_filter(ws, va, cs, active, tsink != nullptr, &pruned, &touched, st);

@@ -74,6 +74,8 @@ struct Workspace {
     DevBuf<float4> screen_r, screen_s;       // per-level FP32 screening records, grow-only
     DevBuf<unsigned> level_agg;              // per-level record aggregates (RefineSource::agg)
     DevBuf<float4> seg_r, seg_s;             // per-level voxel segment aggregates, grow-only
+    DevBuf<ActiveVpDev> active;              // the join's active voxel pairs (tj_join), grow-only: a
+                                             // per-join allocation of GBs (D, E) stalled on pool growth
     DevBuf<ActiveVpDev> active_alt;          // compaction scratch of the active list, grow-only
     DevBuf<int64_t> nsel;
     void release() {
@@ -85,6 +87,7 @@ struct Workspace {
         level_agg.release();
         seg_r.release();
         seg_s.release();
+        active.release();
         active_alt.release();
         nsel.release();
         for (auto& m : mat) m = LevelMat{};

@@ -120,8 +120,10 @@ __device__ __forceinline__ void gather_recs(const float4* __restrict__ box, cons
                                     : reinterpret_cast<const char*>(geo + (part - kBoxF4));
     const uint32_t stride = part < kBoxF4 ? kBoxF4 * 16u : kGeoF4 * 16u;
     uint32_t sa = smem_addr(d4 + (lane >> 3) * kStride4 + part);
+    const uint32_t f0 = (uint32_t)first; // facet indices of a level are 32-bit
+#pragma unroll 4
     for (int rec = lane >> 3; rec < n; rec += 4, sa += 4 * kCS * 4) {
-        const char* g = src + (first + list[rec]) * stride;
+        const char* g = src + (uint64_t)(f0 + list[rec]) * stride;
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g) : "memory");
     }
 #else
@@ -1043,7 +1045,10 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks)
 
 // Exact evaluation of the queued facet pairs: thread per pair, records staged in the
 // thread's own shared-memory slots, minima folded into the op bits with atomicMin.
-__global__ void __launch_bounds__(128) k_eval(RefineSource src, RefineQueue q, unsigned long long* __restrict__ lb_bits,
+#ifndef TJ_EVAL_MINB
+#define TJ_EVAL_MINB 1
+#endif
+__global__ void __launch_bounds__(128, TJ_EVAL_MINB) k_eval(RefineSource src, RefineQueue q, unsigned long long* __restrict__ lb_bits,
                                               unsigned long long* __restrict__ ub_bits, unsigned long long* counters,
                                               int cull) {
     __shared__ double rec[128][2][kFacetWords];

@@ -253,6 +253,12 @@ int tj_dataset_set_pieced(tj_dataset* ds, uint32_t slot);
 int tj_dataset_finish_level_part(tj_dataset* ds, uint32_t slot, uint32_t obj_begin, uint32_t obj_end, uint32_t flags);
 /* Host-blocks until level slot of ds is on the device (queued and its copies complete). */
 int tj_dataset_level_wait(tj_dataset* ds, uint32_t slot);
+/* Copy order across two streamed datasets sharing the host link (run_join: S20 R20 S60 R60 ...,
+ * so each join level's data of both sides lands before the next level's competes for it): the
+ * copies of level `slot` of ds start on the device only after every copy of level `before_slot`
+ * of `before` has completed. Register before the first put of `slot`; that put host-waits until
+ * `before`'s level has been fully put (finished) or failed. Results are unchanged. */
+int tj_dataset_copy_after(tj_dataset* ds, uint32_t slot, tj_dataset* before, uint32_t before_slot);
 int tj_dataset_sync(tj_dataset* ds);
 
 /* ---- host-side index loading (backs load_index, reference src/index_io.cpp:244-249) ----

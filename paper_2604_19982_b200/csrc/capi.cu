@@ -242,10 +242,14 @@ LevelGate::~LevelGate() {
     cudaSetDevice(device);
     for (cudaEvent_t e : ev)
         if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : copied)
+        if (e) cudaEventDestroy(e);
     for (auto& v : pieces)
         for (auto& pe : v)
             if (pe.second) cudaEventDestroy(pe.second);
+    if (expanded) cudaEventDestroy(expanded);
     if (copy) cudaStreamDestroy(copy);
+    if (expand) cudaStreamDestroy(expand);
 }
 
 void expand_compact_level(const DatasetDev& d, uint32_t slot, const uint64_t* act, double* out, int num_sms,
@@ -271,6 +275,27 @@ void expand_compact_level(const DatasetDev& d, uint32_t slot, const uint64_t* ac
                                              d.vox_obj.p, d.vert_base[slot].p, d.facet_base[slot].p, d.n_voxels, out,
                                              d.stream_err.p, act);
     TJ_CUDA(cudaGetLastError());
+}
+
+static std::mutex g_cm_mu;
+static std::vector<std::pair<std::string, cudaEvent_t>> g_cm;
+static bool copy_marks_on() {
+    static const bool v = std::getenv("TRIJOIN_DEBUG_TIMELINE") != nullptr;
+    return v;
+}
+
+void copy_mark(const char* what, int level, cudaStream_t st) {
+    if (!copy_marks_on()) return;
+    cudaEvent_t e;
+    TJ_CUDA(cudaEventCreate(&e));
+    TJ_CUDA(cudaEventRecord(e, st));
+    std::lock_guard<std::mutex> lk(g_cm_mu);
+    g_cm.emplace_back(std::string(what) + std::to_string(level) + "@" + std::to_string((uintptr_t)st % 997), e);
+}
+
+std::vector<std::pair<std::string, cudaEvent_t>> take_copy_marks() {
+    std::lock_guard<std::mutex> lk(g_cm_mu);
+    return std::move(g_cm);
 }
 
 double level_ready(const DatasetDev& d, int slot, cudaStream_t st) {
@@ -439,6 +464,7 @@ void tj_dataset_free(tj_dataset* ds) {
     if (!ds) return;
     cudaSetDevice(ds->ctx->device);
     if (ds->d.gate && ds->d.gate->copy) cudaStreamSynchronize(ds->d.gate->copy);
+    if (ds->d.gate && ds->d.gate->expand) cudaStreamSynchronize(ds->d.gate->expand);
     AllocStreamScope scope(ds->ctx->stream);
     delete ds;
 }
@@ -461,6 +487,13 @@ int tj_dataset_begin_ex(tj_ctx* ctx, const tj_dataset_view* v, const uint64_t* c
         auto gate = std::make_shared<LevelGate>();
         gate->device = ctx->device;
         TJ_CUDA(cudaStreamCreateWithFlags(&gate->copy, cudaStreamNonBlocking));
+        {
+            int lo = 0, hi = 0;
+            TJ_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            TJ_CUDA(cudaStreamCreateWithPriority(&gate->expand, cudaStreamNonBlocking, hi));
+            TJ_CUDA(cudaEventCreateWithFlags(&gate->expanded, cudaEventDisableTiming));
+            TJ_CUDA(cudaEventRecord(gate->expanded, gate->expand));
+        }
         // everything on the dataset's own copy stream: a begin may run while a join occupies
         // the context's stream (the next R chunk of the out-of-core path)
         cudaStream_t st = gate->copy;
@@ -471,10 +504,15 @@ int tj_dataset_begin_ex(tj_ctx* ctx, const tj_dataset_view* v, const uint64_t* c
         gate->ev.assign(v->n_levels, nullptr);
         gate->pieced.assign(v->n_levels, 0);
         gate->pieces.resize(v->n_levels);
+        gate->copied.assign(v->n_levels, nullptr);
+        gate->started.assign(v->n_levels, 0);
+        gate->after.assign(v->n_levels, {nullptr, -1});
+        gate->after_done.assign(v->n_levels, 0);
         d.vert_base.resize(v->n_levels);
         d.facet_base.resize(v->n_levels);
         for (uint32_t li = 0; li < v->n_levels; ++li) {
             TJ_CUDA(cudaEventCreateWithFlags(&gate->ev[li], cudaEventDisableTiming));
+            TJ_CUDA(cudaEventCreateWithFlags(&gate->copied[li], cudaEventDisableTiming));
             const uint64_t* fo = v->facet_offsets ? v->facet_offsets[li] : nullptr;
             const uint64_t* vb = vert_base[li];
             const uint64_t* fb = facet_base[li];
@@ -567,6 +605,26 @@ int tj_dataset_put_level_part(tj_dataset* ds, uint32_t slot, const tj_level_mesh
         // reuse of the area across levels
         const StageLayout L = stage_layout(nvert, nfac, used);
         unsigned char* base = d.compact ? d.cmp[slot].p : d.stage.p;
+        // copy order (tj_dataset_copy_after): the first put of the slot waits for the other
+        // dataset's level to be fully put, then orders the copy stream after its copies
+        if (!g.after_done[slot] && g.after[slot].first) {
+            LevelGate& bg = *g.after[slot].first;
+            const int bs = g.after[slot].second;
+            bool ok = false;
+            {
+                std::unique_lock<std::mutex> lk(bg.mu);
+                bg.cv.wait(lk, [&] { return bg.state[bs] != LevelGate::kPending; });
+                ok = bg.state[bs] == LevelGate::kQueued;
+            }
+            if (ok) TJ_CUDA(cudaStreamWaitEvent(g.copy, bg.copied[bs], 0));
+            g.after_done[slot] = 1;
+        }
+        // the staging area is reused level after level: a level's first copy waits for every
+        // expansion queued so far (the pieces of one level fill disjoint rows)
+        if (!g.started[slot]) {
+            if (!d.compact) TJ_CUDA(cudaStreamWaitEvent(g.copy, g.expanded, 0));
+            g.started[slot] = 1;
+        }
         auto put = [&](uint64_t off, const void* src, uint64_t b0, uint64_t b1, size_t row) {
             if (b1 > b0)
                 TJ_CUDA(cudaMemcpyAsync(base + off + b0 * row, static_cast<const unsigned char*>(src) + b0 * row,
@@ -579,6 +637,8 @@ int tj_dataset_put_level_part(tj_dataset* ds, uint32_t slot, const tj_level_mesh
             put(L.ph, lv->ph, facet_begin, facet_end, 8);
         }
         put(L.vf, vfs, entry_begin, entry_end, narrow ? 2 : 4);
+        TJ_CUDA(cudaEventRecord(g.copied[slot], g.copy));
+        copy_mark("put", d.levels[slot], g.copy);
     });
     if (rc != TJ_OK) {
         {
@@ -597,7 +657,8 @@ int tj_dataset_finish_level(tj_dataset* ds, uint32_t slot, uint32_t flags) {
     tj_ctx* ctx = ds->ctx;
     const int rc = guarded(nullptr, [&] {
         TJ_CUDA(cudaSetDevice(ctx->device));
-        AllocStreamScope scope(g.copy);
+        AllocStreamScope scope(g.expand);
+        TJ_CUDA(cudaStreamWaitEvent(g.expand, g.copied[slot], 0)); // the level's rows have landed
         DatasetDev& d = ds->d;
         const uint64_t nvert = d.level_vertices[slot], nfac = d.level_facets[slot], used = d.level_entries[slot];
         const StageLayout L = stage_layout(nvert, nfac, used);
@@ -615,21 +676,24 @@ int tj_dataset_finish_level(tj_dataset* ds, uint32_t slot, uint32_t flags) {
             const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((d.n_voxels + 7) / 8, (uint64_t)ctx->ws.num_sms * 16));
             count_launch();
             if (flags & TJ_LEVEL_NARROW)
-                k_expand_level<<<grid, 256, 0, g.copy>>>(verts, reinterpret_cast<const uint16_t*>(base + L.tris), hd, ph,
+                k_expand_level<<<grid, 256, 0, g.expand>>>(verts, reinterpret_cast<const uint16_t*>(base + L.tris), hd, ph,
                                                           reinterpret_cast<const uint16_t*>(base + L.vf),
                                                           d.facet_offsets[slot].p, d.vox_obj.p, d.vert_base[slot].p,
                                                           d.facet_base[slot].p, d.n_voxels, out, d.stream_err.p,
                                                           nullptr);
             else
-                k_expand_level<<<grid, 256, 0, g.copy>>>(verts, reinterpret_cast<const uint32_t*>(base + L.tris), hd, ph,
+                k_expand_level<<<grid, 256, 0, g.expand>>>(verts, reinterpret_cast<const uint32_t*>(base + L.tris), hd, ph,
                                                           reinterpret_cast<const uint32_t*>(base + L.vf),
                                                           d.facet_offsets[slot].p, d.vox_obj.p, d.vert_base[slot].p,
                                                           d.facet_base[slot].p, d.n_voxels, out, d.stream_err.p,
                                                           nullptr);
             TJ_CUDA(cudaGetLastError());
         }
-        if (!d.compact && !done) derive_level(d, slot, ctx->ws.num_sms, g.copy);
-        TJ_CUDA(cudaEventRecord(g.ev[slot], g.copy));
+        copy_mark("expand", d.levels[slot], g.expand);
+        if (!d.compact && !done) derive_level(d, slot, ctx->ws.num_sms, g.expand);
+        copy_mark("ready", d.levels[slot], g.expand);
+        TJ_CUDA(cudaEventRecord(g.ev[slot], g.expand));
+        TJ_CUDA(cudaEventRecord(g.expanded, g.expand));
     });
     {
         std::lock_guard<std::mutex> lk(g.mu);
@@ -654,7 +718,7 @@ int tj_dataset_finish_level_part(tj_dataset* ds, uint32_t slot, uint32_t obj_beg
     cudaEvent_t ev = nullptr;
     const int rc = guarded(nullptr, [&] {
         TJ_CUDA(cudaSetDevice(ctx->device));
-        AllocStreamScope scope(g.copy);
+        AllocStreamScope scope(g.expand);
         DatasetDev& d = ds->d;
         if (d.compact || !g.pieced[slot]) throw Error(TJ_EINVAL, "tj_dataset_finish_level_part: level not set pieced");
         const uint32_t prev = g.pieces[slot].empty() ? 0u : g.pieces[slot].back().first;
@@ -668,26 +732,28 @@ int tj_dataset_finish_level_part(tj_dataset* ds, uint32_t slot, uint32_t obj_beg
         const double* hd = pads && nfac ? reinterpret_cast<const double*>(base + L.hd) : nullptr;
         const double* ph = pads && nfac ? reinterpret_cast<const double*>(base + L.ph) : nullptr;
         const uint64_t v0 = d.voxel_offsets_h[obj_begin], v1 = d.voxel_offsets_h[obj_end];
+        TJ_CUDA(cudaStreamWaitEvent(g.expand, g.copied[slot], 0)); // the piece's rows have landed
         if (v1 > v0) {
             const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((v1 - v0 + 7) / 8, (uint64_t)ctx->ws.num_sms * 16));
             count_launch();
             if (flags & TJ_LEVEL_NARROW)
-                k_expand_level<<<grid, 256, 0, g.copy>>>(verts, reinterpret_cast<const uint16_t*>(base + L.tris), hd, ph,
+                k_expand_level<<<grid, 256, 0, g.expand>>>(verts, reinterpret_cast<const uint16_t*>(base + L.tris), hd, ph,
                                                           reinterpret_cast<const uint16_t*>(base + L.vf),
                                                           d.facet_offsets[slot].p, d.vox_obj.p, d.vert_base[slot].p,
                                                           d.facet_base[slot].p, v1, d.facets[slot].p, d.stream_err.p,
                                                           nullptr, v0);
             else
-                k_expand_level<<<grid, 256, 0, g.copy>>>(verts, reinterpret_cast<const uint32_t*>(base + L.tris), hd, ph,
+                k_expand_level<<<grid, 256, 0, g.expand>>>(verts, reinterpret_cast<const uint32_t*>(base + L.tris), hd, ph,
                                                           reinterpret_cast<const uint32_t*>(base + L.vf),
                                                           d.facet_offsets[slot].p, d.vox_obj.p, d.vert_base[slot].p,
                                                           d.facet_base[slot].p, v1, d.facets[slot].p, d.stream_err.p,
                                                           nullptr, v0);
             TJ_CUDA(cudaGetLastError());
         }
-        derive_level_range(d, slot, v0, v1, g.pieces[slot].empty(), ctx->ws.num_sms, g.copy);
+        derive_level_range(d, slot, v0, v1, g.pieces[slot].empty(), ctx->ws.num_sms, g.expand);
         TJ_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        TJ_CUDA(cudaEventRecord(ev, g.copy));
+        TJ_CUDA(cudaEventRecord(ev, g.expand));
+        TJ_CUDA(cudaEventRecord(g.expanded, g.expand));
     });
     {
         std::lock_guard<std::mutex> lk(g.mu);
@@ -699,6 +765,17 @@ int tj_dataset_finish_level_part(tj_dataset* ds, uint32_t slot, uint32_t obj_beg
     g.cv.notify_all();
     if (rc != TJ_OK) set_ctx_error(ctx, tj_global_last_error());
     return rc;
+}
+
+int tj_dataset_copy_after(tj_dataset* ds, uint32_t slot, tj_dataset* before, uint32_t before_slot) {
+    if (!ds || !ds->d.gate || slot >= ds->d.levels.size() || !before || before == ds || !before->d.gate ||
+        before_slot >= before->d.levels.size() || before->ctx->device != ds->ctx->device)
+        return TJ_EINVAL;
+    LevelGate& g = *ds->d.gate;
+    std::lock_guard<std::mutex> lk(g.mu);
+    if (g.state[slot] != LevelGate::kPending || g.after_done[slot]) return TJ_EINVAL; // already being put
+    g.after[slot] = {before->d.gate.get(), (int)before_slot};
+    return TJ_OK;
 }
 
 int tj_dataset_level_wait(tj_dataset* ds, uint32_t slot) {
@@ -739,6 +816,7 @@ int tj_dataset_sync(tj_dataset* ds) {
     return guarded(nullptr, [&] {
         TJ_CUDA(cudaSetDevice(ds->ctx->device));
         TJ_CUDA(cudaStreamSynchronize(ds->d.gate->copy));
+        TJ_CUDA(cudaStreamSynchronize(ds->d.gate->expand));
     });
 }
 

@@ -1134,14 +1134,21 @@ void lease(SetLease& l, detail::JoinCache* cache, const std::string& key) {
 
 // Ships level slot `slot` of set (packing it first, in pieces that are shipped while the next
 // is packed, unless the set already holds it) to every dataset handle in dst.
-// $TRIJOIN_PIECED=1 ships R's last join level in object-range pieces after S's whole level, and
-// the join refines each piece's queries as it lands. Off by default: on config B the last
-// level's data is already on the device when the join reaches it (the join waits for LOD 20 /
-// 60 data instead), and shipping S's level first made the last level 2 ms later (e2e timelines,
-// TRIJOIN_DEBUG_TIMELINE). Results are identical either way (tests/test_gpu_join.py).
+// $TRIJOIN_COPY_ORDER=0: R's and S's level copies unordered (each dataset's copy stream on its
+// own). Ordered (default), each GPU's link carries S20 R20 S60 R60 ... (tj_dataset_copy_after).
+bool copy_order() {
+    const char* e = std::getenv("TRIJOIN_COPY_ORDER");
+    return !(e && *e == '0');
+}
+
+// R's last join level ships in object-range pieces after S's whole level, and the join refines
+// each piece's queries as it lands ($TRIJOIN_PIECED=0: whole). With the expansions off the copy
+// stream (LevelGate::expand) config B's pieces land at full link speed while the previous level
+// is still being refined: e2e 93.8 -> 91.6 ms (TRIJOIN_DEBUG_TIMELINE copy / refine timelines).
+// Results are identical either way (tests/test_gpu_join.py).
 bool pieced_last_level() {
     const char* e = std::getenv("TRIJOIN_PIECED");
-    return e && *e == '1';
+    return !(e && *e == '0');
 }
 
 uint32_t level_flags(const detail::PackedLevel& l) {
@@ -1306,6 +1313,21 @@ JoinOutput detail::run_join_cached(const PreparedDataset& R, const PreparedDatas
         s_cv.wait(lk, [&] { return s_begun; });
         if (s_failed) throw std::runtime_error("trijoin: S upload failed");
     };
+    // Copy order over each GPU's host link, join level by join level: S20 R20 S60 R60 ... (the
+    // workers register it on their first chunk; the main thread feeds S's levels once every
+    // worker has registered or given up)
+    const bool ordered = copy_order() && !one_dataset;
+    size_t ord_n = 0;
+    std::vector<char> ord_in(G, 0);
+    auto ord_arrive = [&](size_t g) { // once per worker, on every path
+        {
+            std::lock_guard<std::mutex> lk(s_mu);
+            if (ord_in[g]) return;
+            ord_in[g] = 1;
+            ++ord_n;
+        }
+        s_cv.notify_all();
+    };
 
     // ---- per GPU: its R chunks in order; each chunk's levels are packed (or taken from the
     // cache) and streamed while its join runs, coarsest level first
@@ -1353,7 +1375,30 @@ JoinOutput detail::run_join_cached(const PreparedDataset& R, const PreparedDatas
                 if (pieced) detail::check(tj_dataset_set_pieced(dr.p, static_cast<uint32_t>(r_last)), ctx);
                 std::exception_ptr je;
                 const auto td = Clock::now();
-                if (!one_dataset) wait_s_begun();
+                if (!one_dataset) {
+                    try {
+                        wait_s_begun();
+                        if (ordered && k == 0) {
+                            for (size_t li = 0; li < spec.lods.size(); ++li) {
+                                const int rs = slot_of(R, spec.lods[li]), ss = slot_of(S, spec.lods[li]);
+                                if (rs < 0 || ss < 0) break;
+                                detail::check(tj_dataset_copy_after(dr.p, static_cast<uint32_t>(rs), dsh[g].p,
+                                                                    static_cast<uint32_t>(ss)),
+                                              ctx);
+                                if (li + 1 >= spec.lods.size()) break;
+                                const int sn = slot_of(S, spec.lods[li + 1]);
+                                if (sn < 0) break;
+                                detail::check(tj_dataset_copy_after(dsh[g].p, static_cast<uint32_t>(sn), dr.p,
+                                                                    static_cast<uint32_t>(rs)),
+                                              ctx);
+                            }
+                        }
+                    } catch (...) {
+                        ord_arrive(g);
+                        throw;
+                    }
+                    ord_arrive(g);
+                }
                 std::thread jt([&] {
                     try {
                         tj_join_spec cs = to_c_spec(spec);
@@ -1373,7 +1418,9 @@ JoinOutput detail::run_join_cached(const PreparedDataset& R, const PreparedDatas
                         const int slot = slot_of(R, level);
                         if (slot < 0) continue; // the join reports the missing level
                         const bool last = pieced && slot == r_last;
-                        if (last) detail::check(tj_dataset_level_wait(dsh[g].p, static_cast<uint32_t>(s_last)), ctxs[g]);
+                        // (with the copy order registered the device orders R's pieces after S's level)
+                        if (last && !(ordered && k == 0))
+                            detail::check(tj_dataset_level_wait(dsh[g].p, static_cast<uint32_t>(s_last)), ctxs[g]);
                         feed_level(R, *lz->set, static_cast<size_t>(slot), {dr.p}, {ctx}, pool, out, pack_ms,
                                    &stat_mu, last);
                         put[slot] = 1;
@@ -1394,6 +1441,7 @@ JoinOutput detail::run_join_cached(const PreparedDataset& R, const PreparedDatas
         } catch (...) {
             errors[g] = std::current_exception();
         }
+        ord_arrive(g);
     };
     std::vector<std::thread> workers;
     for (size_t g = 0; g < G; ++g) workers.emplace_back(worker, g);
@@ -1436,6 +1484,10 @@ JoinOutput detail::run_join_cached(const PreparedDataset& R, const PreparedDatas
 
     // ---- main thread: S levels in join order, shipped to every GPU
     std::exception_ptr s_error;
+    if (ordered) { // every worker's copy order registered (or the worker gave up before its join)
+        std::unique_lock<std::mutex> lk(s_mu);
+        s_cv.wait(lk, [&] { return ord_n >= G; });
+    }
     if (!one_dataset) {
         std::vector<tj_dataset*> dst(G);
         for (size_t g = 0; g < G; ++g) dst[g] = dsh[g].p;

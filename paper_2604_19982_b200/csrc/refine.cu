@@ -926,7 +926,7 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks)
                             // the final pass: the entries index this tile's records)
                             for (;;) {
                                 bool more, last;
-                                if constexpr (kBF && TJ_QUEUE_SCAN) {
+                                if constexpr ((kBF && TJ_QUEUE_SCAN) || TJ_QUEUE_SCAN == 2) {
                                 // every lane's entries at once, placed by a warp prefix sum of the
                                 // mask counts (as many as the ring has room for; the rest next round)
                                 more = false;

@@ -574,6 +574,17 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
             line += b;
         }
         std::fprintf(stderr, "%s\n", line.c_str());
+        std::string cl = "[timeline] copy streams from t0 (ms):";
+        for (auto& [what, e] : take_copy_marks()) {
+            float ms = 0.f;
+            if (cudaEventSynchronize(e) == cudaSuccess && cudaEventElapsedTime(&ms, tl_ev[0], e) == cudaSuccess) {
+                char b[64];
+                std::snprintf(b, sizeof(b), " %s=%.2f", what.c_str(), ms);
+                cl += b;
+            }
+            cudaEventDestroy(e);
+        }
+        std::fprintf(stderr, "%s\n", cl.c_str());
         for (cudaEvent_t e : tl_ev) cudaEventDestroy(e);
     }
     return out;

@@ -88,8 +88,17 @@ struct LevelGate {
     // finished so far, (end object, event after its expansion and derivation), in order
     std::vector<char> pieced;
     std::vector<std::vector<std::pair<uint32_t, cudaEvent_t>>> pieces;
-    cudaStream_t copy = nullptr;
+    cudaStream_t copy = nullptr;   // the level copies (H2D)
+    cudaStream_t expand = nullptr; // expansion / derivation of landed levels (high priority), so
+                                   // copies never queue behind kernels waiting for SMs
+    cudaEvent_t expanded = nullptr; // after the last queued expansion (staging-area reuse)
+    std::vector<char> started;     // per slot: a put has been issued
     int device = 0;
+    // per slot: event after the slot's copies (re-recorded by every put of the slot), and the
+    // copy-order dependency (tj_dataset_copy_after): that dataset's gate and slot, applied once
+    std::vector<cudaEvent_t> copied;
+    std::vector<std::pair<LevelGate*, int>> after;
+    std::vector<char> after_done;
     ~LevelGate();
 };
 
@@ -146,6 +155,10 @@ void derive_level_range(DatasetDev& d, uint32_t li, uint64_t v_begin, uint64_t v
 // Makes `st` wait until level slot `slot` of `d` is resident (no-op for uploaded datasets);
 // returns the host milliseconds spent blocked waiting for the level to be queued.
 double level_ready(const DatasetDev& d, int slot, cudaStream_t st);
+// $TRIJOIN_DEBUG_TIMELINE diagnostics: labelled timing events recorded on the copy streams
+// (level copies queued / expanded), printed by the join's timeline relative to its start
+void copy_mark(const char* what, int level, cudaStream_t st);
+std::vector<std::pair<std::string, cudaEvent_t>> take_copy_marks();
 // Pieced levels: whether slot arrives in object-range pieces, and piece k's end object and
 // completion event (host-blocks until it is finished; nullptr once the level is complete and
 // every piece was returned).

@@ -85,13 +85,17 @@ def test_out_of_core_r_chunks(monkeypatch, env, j):
         assert b["r_chunks"] > 1 or (b["residency"] == "compact" and "TRIJOIN_COMPACT" not in env)
 
 
+@pytest.mark.parametrize("order", ["1", "0"], ids=["ordered", "unordered"])
+@pytest.mark.parametrize("pieced", ["1", "0"], ids=["pieced", "whole"])
 @pytest.mark.parametrize("j", [j for j in JOINS if j["s"]], ids=tjtest.join_id)
-def test_pieced_last_level(monkeypatch, j):
-    """R's last join level shipped in object-range pieces (TRIJOIN_PIECED=1: tj_dataset_set_pieced
-    / tj_dataset_finish_level_part), the join refining each piece's queries as it lands: records
-    and every stage counter equal the reference's."""
+def test_pieced_last_level(monkeypatch, j, pieced, order):
+    """R's last join level shipped in object-range pieces (the default; TRIJOIN_PIECED=0: whole;
+    tj_dataset_set_pieced / tj_dataset_finish_level_part), the join refining each piece's queries
+    as it lands, with and without the cross-dataset copy order (TRIJOIN_COPY_ORDER,
+    tj_dataset_copy_after): records and every stage counter equal the reference's."""
     import paper_2604_19982_b200 as tj
-    monkeypatch.setenv("TRIJOIN_PIECED", "1")
+    monkeypatch.setenv("TRIJOIN_PIECED", pieced)
+    monkeypatch.setenv("TRIJOIN_COPY_ORDER", order)
     r, s = _paths(j)
     out = tj.join(r, s, **j["kwargs"])
     assert out["records"] == j["records"]

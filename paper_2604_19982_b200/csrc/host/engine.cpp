@@ -1141,14 +1141,17 @@ bool copy_order() {
     return !(e && *e == '0');
 }
 
-// R's last join level ships in object-range pieces after S's whole level, and the join refines
-// each piece's queries as it lands ($TRIJOIN_PIECED=0: whole). With the expansions off the copy
-// stream (LevelGate::expand) config B's pieces land at full link speed while the previous level
-// is still being refined: e2e 93.8 -> 91.6 ms (TRIJOIN_DEBUG_TIMELINE copy / refine timelines).
-// Results are identical either way (tests/test_gpu_join.py).
-bool pieced_last_level() {
+// R's join levels after the first ship in object-range pieces, each after S's same level, and
+// the join refines each piece's queries as it lands, with R's running level aggregates
+// (TRIJOIN_PIECED=1: the last level only, 0: whole levels). With the expansions off the copy
+// stream (LevelGate::expand) the pieces land at link speed while the previous level is still
+// being refined: config B e2e 93.8 (whole) -> 90.4 (last level) -> 86.1 ms (every level after
+// the first; TRIJOIN_DEBUG_TIMELINE copy / refine timelines). Results are identical in every
+// mode (tests/test_gpu_join.py).
+int pieced_mode() { // 0: whole levels, 1: the last join level pieced, 2 (default): every level after the first
     const char* e = std::getenv("TRIJOIN_PIECED");
-    return !(e && *e == '0');
+    if (!e || !*e) return 2;
+    return *e == '0' ? 0 : *e == '1' ? 1 : 2;
 }
 
 uint32_t level_flags(const detail::PackedLevel& l) {
@@ -1370,9 +1373,17 @@ JoinOutput detail::run_join_cached(const PreparedDataset& R, const PreparedDatas
                 detail::ResultHandle* res = results[g].back().get();
                 // the last join level of R in object-range pieces, after S's whole last level: the
                 // join refines each piece's queries while the later pieces are still in flight
-                const int r_last = slot_of(R, spec.lods.back()), s_last = slot_of(S, spec.lods.back());
-                const bool pieced = pieced_last_level() && !one_dataset && !compact && r_last >= 0 && s_last >= 0;
-                if (pieced) detail::check(tj_dataset_set_pieced(dr.p, static_cast<uint32_t>(r_last)), ctx);
+                // R's pieced levels: the last join level, or (TRIJOIN_PIECED=2) every join level
+                // after the first; each ships after S's same level
+                std::vector<char> pieced_slot(R.lod_schedule.size(), 0);
+                const int pmode = pieced_mode();
+                if (pmode && !one_dataset && !compact)
+                    for (size_t li = pmode == 2 ? 1 : spec.lods.size() - 1; li < spec.lods.size(); ++li) {
+                        const int rs = slot_of(R, spec.lods[li]), ss = slot_of(S, spec.lods[li]);
+                        if (rs < 0 || ss < 0) continue;
+                        pieced_slot[rs] = 1;
+                        detail::check(tj_dataset_set_pieced(dr.p, static_cast<uint32_t>(rs)), ctx);
+                    }
                 std::exception_ptr je;
                 const auto td = Clock::now();
                 if (!one_dataset) {
@@ -1417,12 +1428,13 @@ JoinOutput detail::run_join_cached(const PreparedDataset& R, const PreparedDatas
                     for (uint32_t level : spec.lods) {
                         const int slot = slot_of(R, level);
                         if (slot < 0) continue; // the join reports the missing level
-                        const bool last = pieced && slot == r_last;
+                        const bool pc = pieced_slot[slot] != 0;
                         // (with the copy order registered the device orders R's pieces after S's level)
-                        if (last && !(ordered && k == 0))
-                            detail::check(tj_dataset_level_wait(dsh[g].p, static_cast<uint32_t>(s_last)), ctxs[g]);
+                        if (pc && !(ordered && k == 0))
+                            detail::check(tj_dataset_level_wait(dsh[g].p, static_cast<uint32_t>(slot_of(S, level))),
+                                          ctxs[g]);
                         feed_level(R, *lz->set, static_cast<size_t>(slot), {dr.p}, {ctx}, pool, out, pack_ms,
-                                   &stat_mu, last);
+                                   &stat_mu, pc);
                         put[slot] = 1;
                         if (G == 1 && w.chunks.size() == 1)
                             mark(std::string("R_lod") + std::to_string(level) + "_put");

@@ -407,7 +407,6 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
                 k_copy_agg<<<1, 32, 0, st>>>(rs.agg, ss_.agg, ws.level_agg.p);
             };
             if (!mat) bind(resident_side(R, sr), resident_side(S, ss));
-            if (pieced) src.agg = nullptr; // R's level aggregates are complete only after its last piece
             // 0: every facet pair; 1: exact-preserving culling; 2: decision-mode culling
             const int cull = (spec.flags & TJ_FLAG_NO_CULL) ? 0 : decision ? 2 : 1;
             unsigned long long hc[kNumCounters];
@@ -439,6 +438,11 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
                         ls.wait_ms += std::chrono::duration<double, std::milli>(Clock::now() - tw).count();
                         if (!pev) break;
                         TJ_CUDA(cudaStreamWaitEvent(st, pev, 0));
+                        // R's level aggregates so far (pieces 0..k, k_prep's running min / max):
+                        // a conservative bound for this piece's facets (decision-mode shortcut)
+                        count_launch();
+                        k_copy_agg<<<1, 32, 0, st>>>(resident_side(R, sr).agg, resident_side(S, ss).agg,
+                                                     ws.level_agg.p);
                         count_launch();
                         k_active_lower_bound<<<1, 32, 0, st>>>(active.p, n_active, cs.r2op.p, cs.nq, obj_end, piece_b.p);
                         uint64_t b = 0;

@@ -86,10 +86,11 @@ def test_out_of_core_r_chunks(monkeypatch, env, j):
 
 
 @pytest.mark.parametrize("order", ["1", "0"], ids=["ordered", "unordered"])
-@pytest.mark.parametrize("pieced", ["1", "0"], ids=["pieced", "whole"])
+@pytest.mark.parametrize("pieced", ["1", "2", "0"], ids=["pieced", "pieced_all", "whole"])
 @pytest.mark.parametrize("j", [j for j in JOINS if j["s"]], ids=tjtest.join_id)
 def test_pieced_last_level(monkeypatch, j, pieced, order):
-    """R's last join level shipped in object-range pieces (the default; TRIJOIN_PIECED=0: whole;
+    """R's last join level shipped in object-range pieces (the default; TRIJOIN_PIECED=2: every
+    join level after the first, each piece refined with R's running level aggregates; 0: whole;
     tj_dataset_set_pieced / tj_dataset_finish_level_part), the join refining each piece's queries
     as it lands, with and without the cross-dataset copy order (TRIJOIN_COPY_ORDER,
     tj_dataset_copy_after): records and every stage counter equal the reference's."""

@@ -303,6 +303,14 @@ __device__ __forceinline__ bool seedable_dm(const SegAgg& ar, const SegAgg& as) 
     return !(box_gap_lb(arec, brec) > __fadd_ru(as.phmax, ar.phmax));
 }
 
+#ifndef TJ_SEED2_OVERLAP
+#define TJ_SEED2_OVERLAP 0 // phase-2 seeds only for voxel pairs whose segment boxes overlap
+#endif
+__device__ __forceinline__ bool seg_boxes_overlap(const SegAgg& a, const SegAgg& b) {
+    return a.lo[0] <= b.hi[0] && b.lo[0] <= a.hi[0] && a.lo[1] <= b.hi[1] && b.lo[1] <= a.hi[1] &&
+           a.lo[2] <= b.hi[2] && b.lo[2] <= a.hi[2];
+}
+
 // Decision-mode seeding in two phases (refine_pass): one op needs a single zero-bound facet
 // pair to settle, so each op's most promising voxel pair (segment boxes by decreasing overlap
 // volume, then by increasing squared gap; ties to the lowest index) is seeded and evaluated
@@ -453,7 +461,8 @@ __global__ void __launch_bounds__(256, 4) k_seed(RefineSource src, uint64_t vp_b
                 const VpDescDev d = get_vp(src, base + lane);
                 if (d.rn != 0 && d.sn != 0) {
                     const SegAgg ar = seg_r_of(src, d), as = seg_s_of(src, d);
-                    live = seedable(ar, as) && wanted(base + lane, d.op);
+                    live = seedable(ar, as) && wanted(base + lane, d.op) && (phase != 2 || !TJ_SEED2_OVERLAP ||
+                                                                            seg_boxes_overlap(ar, as));
                     if (live)
                         mine[lane] = {d.r0, d.s0, d.op, d.rn, d.sn, 0u,
                                       {ar.lo[0], ar.lo[1], ar.lo[2]}, {ar.hi[0], ar.hi[1], ar.hi[2]},
@@ -541,7 +550,8 @@ __global__ void __launch_bounds__(256, 4) k_seed(RefineSource src, uint64_t vp_b
             if (d.rn == 0 || d.sn == 0) continue;
             const SegAgg ar = seg_r_of(src, d);
             const SegAgg as = seg_s_of(src, d);
-            if (!seedable(ar, as) || !wanted(vp, d.op)) continue;
+            if (!seedable(ar, as) || !wanted(vp, d.op) || (phase == 2 && TJ_SEED2_OVERLAP && !seg_boxes_overlap(ar, as)))
+                continue;
             seed_vp(d, ar, as);
         }
     }

@@ -1148,6 +1148,12 @@ bool copy_order() {
 // being refined: config B e2e 93.8 (whole) -> 90.4 (last level) -> 86.1 ms (every level after
 // the first; TRIJOIN_DEBUG_TIMELINE copy / refine timelines). Results are identical in every
 // mode (tests/test_gpu_join.py).
+// $TRIJOIN_PIECED_S=0: S's levels expanded whole after their last copy
+bool s_pieces() {
+    const char* e = std::getenv("TRIJOIN_PIECED_S");
+    return !(e && *e == '0');
+}
+
 int pieced_mode() { // 0: whole levels, 1: the last join level pieced, 2 (default): every level after the first
     const char* e = std::getenv("TRIJOIN_PIECED");
     if (!e || !*e) return 2;
@@ -1504,10 +1510,17 @@ JoinOutput detail::run_join_cached(const PreparedDataset& R, const PreparedDatas
         std::vector<tj_dataset*> dst(G);
         for (size_t g = 0; g < G; ++g) dst[g] = dsh[g].p;
         try {
+            // S's levels are expanded piece by piece as they land (the join still waits for the
+            // whole level): only the last piece's expansion follows the level's last copy
+            const bool s_pieced = !compact && pieced_mode() != 0 && s_pieces();
             for (uint32_t level : spec.lods) {
                 const int slot = slot_of(S, level);
                 if (slot < 0) continue;
-                feed_level(S, *s_lease.set, static_cast<size_t>(slot), dst, ctxs, pool, out, pack_ms, &stat_mu);
+                if (s_pieced)
+                    for (size_t g = 0; g < G; ++g)
+                        detail::check(tj_dataset_set_pieced(dst[g], static_cast<uint32_t>(slot)), ctxs[g]);
+                feed_level(S, *s_lease.set, static_cast<size_t>(slot), dst, ctxs, pool, out, pack_ms, &stat_mu,
+                           s_pieced);
                 for (size_t g = 0; g < G; ++g) put_s[g][slot] = 1;
                 mark(std::string("S_lod") + std::to_string(level) + "_put");
             }

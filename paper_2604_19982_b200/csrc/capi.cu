@@ -314,6 +314,14 @@ bool level_pieced(const DatasetDev& d, int slot) {
     return d.gate && slot >= 0 && (size_t)slot < d.gate->pieced.size() && d.gate->pieced[slot];
 }
 
+cudaEvent_t level_piece_try(const DatasetDev& d, int slot, size_t k, uint32_t* obj_end) {
+    LevelGate& g = *d.gate;
+    std::lock_guard<std::mutex> lk(g.mu);
+    if (g.pieces[slot].size() <= k) return nullptr; // not finished yet (or none left)
+    *obj_end = g.pieces[slot][k].first;
+    return g.pieces[slot][k].second;
+}
+
 cudaEvent_t level_piece(const DatasetDev& d, int slot, size_t k, uint32_t* obj_end) {
     LevelGate& g = *d.gate;
     std::unique_lock<std::mutex> lk(g.mu);

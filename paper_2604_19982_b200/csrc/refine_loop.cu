@@ -430,31 +430,52 @@ RefineLoopOut refine_loop_dev(Workspace& ws, const DatasetDev& R, const DatasetD
                 if (pieced) {
                     // per piece: its queries' voxel pairs, seeds then screens (an op's voxel
                     // pairs all belong to its query, hence to one piece)
+                    // Pieces are taken in batches: at least the next one (host-blocking until it
+                    // is queued), plus every later one already queued; the batch's active-list
+                    // boundaries cost one round trip, then its pieces' passes queue back to back
+                    // (each behind its own piece's event), so the join stream never drains
+                    // between pieces that were shipped together.
                     uint64_t a = 0;
-                    for (size_t k = 0;; ++k) {
+                    for (size_t k = 0;;) {
+                        std::vector<std::pair<uint32_t, cudaEvent_t>> batch;
                         uint32_t obj_end = 0;
                         const auto tw = Clock::now();
                         const cudaEvent_t pev = level_piece(R, sr, k, &obj_end);
                         ls.wait_ms += std::chrono::duration<double, std::milli>(Clock::now() - tw).count();
                         if (!pev) break;
-                        TJ_CUDA(cudaStreamWaitEvent(st, pev, 0));
-                        // R's level aggregates so far (pieces 0..k, k_prep's running min / max):
-                        // a conservative bound for this piece's facets (decision-mode shortcut)
-                        count_launch();
-                        k_copy_agg<<<1, 32, 0, st>>>(resident_side(R, sr).agg, resident_side(S, ss).agg,
-                                                     ws.level_agg.p);
-                        count_launch();
-                        k_active_lower_bound<<<1, 32, 0, st>>>(active.p, n_active, cs.r2op.p, cs.nq, obj_end, piece_b.p);
-                        uint64_t b = 0;
-                        TJ_CUDA(cudaMemcpyAsync(&b, piece_b.p, 8, cudaMemcpyDeviceToHost, st));
+                        batch.emplace_back(obj_end, pev);
+                        for (;;) {
+                            uint32_t oe = 0;
+                            const cudaEvent_t e = level_piece_try(R, sr, k + batch.size(), &oe);
+                            if (!e) break;
+                            batch.emplace_back(oe, e);
+                        }
+                        piece_b.reserve(batch.size());
+                        for (size_t i = 0; i < batch.size(); ++i) {
+                            count_launch();
+                            k_active_lower_bound<<<1, 32, 0, st>>>(active.p, n_active, cs.r2op.p, cs.nq, batch[i].first,
+                                                                   piece_b.p + i);
+                        }
+                        std::vector<uint64_t> bnd(batch.size());
+                        TJ_CUDA(cudaMemcpyAsync(bnd.data(), piece_b.p, batch.size() * 8, cudaMemcpyDeviceToHost, st));
                         stream_sync(st);
-                        for (uint64_t c0 = a; cull && c0 < b; c0 += launch)
-                            refine_pass(src, c0, std::min(b, c0 + launch), true, lbb.p, ubb.p, cull, queue, work.p,
-                                        counters.p, ws.num_sms, st);
-                        for (uint64_t c0 = a; c0 < b; c0 += launch)
-                            refine_pass(src, c0, std::min(b, c0 + launch), false, lbb.p, ubb.p, cull, queue, work.p,
-                                        counters.p, ws.num_sms, st, sev());
-                        a = b;
+                        for (size_t i = 0; i < batch.size(); ++i) {
+                            const uint64_t b = bnd[i];
+                            TJ_CUDA(cudaStreamWaitEvent(st, batch[i].second, 0));
+                            // R's level aggregates so far (pieces 0..i at least, k_prep's running
+                            // min / max): a conservative bound for this piece's facets
+                            count_launch();
+                            k_copy_agg<<<1, 32, 0, st>>>(resident_side(R, sr).agg, resident_side(S, ss).agg,
+                                                         ws.level_agg.p);
+                            for (uint64_t c0 = a; cull && c0 < b; c0 += launch)
+                                refine_pass(src, c0, std::min(b, c0 + launch), true, lbb.p, ubb.p, cull, queue, work.p,
+                                            counters.p, ws.num_sms, st);
+                            for (uint64_t c0 = a; c0 < b; c0 += launch)
+                                refine_pass(src, c0, std::min(b, c0 + launch), false, lbb.p, ubb.p, cull, queue, work.p,
+                                            counters.p, ws.num_sms, st, sev());
+                            a = b;
+                        }
+                        k += batch.size();
                     }
                     if (a != n_active) throw Error(TJ_EINVAL, "join: the pieces of a level do not cover its queries");
                     level_ready(R, sr, st);

@@ -164,6 +164,8 @@ std::vector<std::pair<std::string, cudaEvent_t>> take_copy_marks();
 // every piece was returned).
 bool level_pieced(const DatasetDev& d, int slot);
 cudaEvent_t level_piece(const DatasetDev& d, int slot, size_t k, uint32_t* obj_end);
+// Non-blocking: piece k's event if it has been finished (queued), else nullptr.
+cudaEvent_t level_piece_try(const DatasetDev& d, int slot, size_t k, uint32_t* obj_end);
 
 // Active voxel pair during refinement: candidate op + global voxel ids.
 struct ActiveVpDev {

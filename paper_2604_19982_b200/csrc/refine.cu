@@ -26,6 +26,9 @@ __device__ unsigned long long* g_dbg_op_tested = nullptr;
 #define TJ_S1_UNROLL 1 // stage-1 inner loop unroll (B: 1 = 2 = 63.6 ms, 4: 67.4; C: 1: 191, 2: 198, 4: 216 ms)
 #endif
 
+#ifndef TJ_ROWS_SINGLE_MIN
+#define TJ_ROWS_SINGLE_MIN 27
+#endif
 #ifndef TJ_ROWS_SINGLE
 #define TJ_ROWS_SINGLE 1 // measured: B 44.95 -> 44.46 ms (LOD 60 13.3 -> 13.0), C within noise
 #endif
@@ -904,9 +907,9 @@ __global__ void __launch_bounds__(kScreenThreads, kScreenBlocks)
                         int nq = 0, qh = 0; // the warp's stage-2 ring: nq entries from sm.q[qh]
                         for (int rp0 = 0; rp0 < rcnt;) {
                             const int left = rcnt - rp0;
-                            // (TJ_ROWS_SINGLE: 27..31 rows in one pass at P = 1: one pass fewer
+                            // (TJ_ROWS_SINGLE: TJ_ROWS_SINGLE_MIN..31 rows in one pass at P = 1: one pass fewer
                             // for the same iterations)
-                            const int rows = left >= 32 ? 32 : (TJ_ROWS_SINGLE && left >= 27) ? left : left > 16 ? 16 : left;
+                            const int rows = left >= 32 ? 32 : (TJ_ROWS_SINGLE && left >= TJ_ROWS_SINGLE_MIN) ? left : left > 16 ? 16 : left;
                             const bool final_pass = rp0 + rows >= rcnt;
                             // small-integer quotients by float reciprocal (x / P for 0 <= x < 64,
                             // P <= 32: the + 0.5 keeps the product >= 1/64 away from integers, far

@@ -672,8 +672,10 @@ uint32_t hier_min_pairs() {
 // Voxel pairs per work grab of k_screen: inversely proportional to the expected work of a
 // voxel pair (mean segment length m, work ~ m^2 facet pairs): kGrabWork / m^2 clamped to
 // [4, 32] — large grabs where most voxel pairs are cheap or settled (fewer work-counter
-// atomics), small ones where heavy voxel pairs cluster (load balance). kGrabWork = 8192
-// (config B 68.6 -> 66.0 ms, C 206 -> 201 ms, E 12.9 -> 13.1 ms; 16384: B 65.7, C 197, E 14.0).
+// atomics), small ones where heavy voxel pairs cluster (load balance). kGrabWork = 32768: with
+// the cheaper per-pair screen the grab overhead weighs more (8192 / 16384 / 32768 / 65536: B 44.5
+// / 43.7 / 43.7 / 44.0 ms, C 179.9 / 178.9 / 176.6 / 177.4, E 294.5 / 293.6 / 294.9 / 295.9, D
+// 1358 / - / 1354 / -; round 1 had chosen 8192 over 16384 at B 66.0 vs 65.7, C 201 vs 197).
 // TRIJOIN_SCREEN_BATCH (1..32) / TRIJOIN_SCREEN_GRAB_WORK override (tuning).
 unsigned screen_batch(float mean_seg, uint64_t n_vps, uint64_t warps) {
     static const int forced = [] {
@@ -683,7 +685,7 @@ unsigned screen_batch(float mean_seg, uint64_t n_vps, uint64_t warps) {
     }();
     static const float work = [] {
         const char* e = getenv("TRIJOIN_SCREEN_GRAB_WORK");
-        return e ? (float)atof(e) : 8192.f;
+        return e ? (float)atof(e) : 32768.f;
     }();
     if (forced) return (unsigned)forced;
     if (!(mean_seg > 0.f)) return 4u;

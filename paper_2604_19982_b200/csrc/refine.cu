@@ -460,15 +460,25 @@ __global__ void __launch_bounds__(256, 4) k_seed(RefineSource src, uint64_t vp_b
         // chains), then the warp seeds the survivors
         SeedVp* mine = sv[threadIdx.x >> 5];
         const unsigned nb = seed_batch();
-        for (uint64_t base = vp_begin + gw * nb; base < vp_end; base += nw * nb) {
+        // phase 1 walks the ops (their primary voxel pairs, pick[op]) instead of every voxel pair
+        const bool by_op = phase == 1;
+        const uint64_t it_begin = by_op ? 0 : vp_begin, it_end = by_op ? src.n_ops : vp_end;
+        for (uint64_t base = it_begin + gw * nb; base < it_end; base += nw * nb) {
             bool live = false;
             __syncwarp();
-            if (lane < nb && base + lane < vp_end) {
-                const VpDescDev d = get_vp(src, base + lane);
+            uint64_t vp = base + lane;
+            bool have = lane < nb && vp < it_end;
+            if (have && by_op) {
+                const unsigned long long pk = __ldcg(pick + vp);
+                have = pk != ~0ull;
+                vp = vp_begin + (uint32_t)pk;
+            }
+            if (have) {
+                const VpDescDev d = get_vp(src, vp);
                 if (d.rn != 0 && d.sn != 0) {
                     const SegAgg ar = seg_r_of(src, d), as = seg_s_of(src, d);
-                    live = seedable(ar, as) && wanted(base + lane, d.op) && (phase != 2 || !TJ_SEED2_OVERLAP ||
-                                                                            seg_boxes_overlap(ar, as));
+                    live = seedable(ar, as) && wanted(vp, d.op) && (phase != 2 || !TJ_SEED2_OVERLAP ||
+                                                                     seg_boxes_overlap(ar, as));
                     if (live)
                         mine[lane] = {d.r0, d.s0, d.op, d.rn, d.sn, 0u,
                                       {ar.lo[0], ar.lo[1], ar.lo[2]}, {ar.hi[0], ar.hi[1], ar.hi[2]},
